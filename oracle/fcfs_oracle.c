@@ -1,0 +1,650 @@
+/*
+ * oracle/fcfs_oracle.c -- CPU oracle for FCFS, "Fully Convolutional Fractional
+ * Scaling" (arXiv 2203.10670).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (paper_2203_10670_b200/) never links, imports or calls it,
+ * and this file includes no header of the product: the two share no code.
+ *
+ * What it is: a plain, slow, obviously correct double-precision
+ * implementation of the paper's layer, written step by step in the paper's
+ * order.  Build with -ffp-contract=off so that no FMA contraction changes the
+ * rounding of the written expressions.
+ *
+ * Citations are PAPER.md line numbers (the LaTeX source of the paper) with the
+ * section they sit in; "Z<n>" refers to the reading table in DESIGN.md §3
+ * (inherited from SURVEY.md §8c) wherever the paper is silent or garbled.
+ *
+ *   1D FCFS (§3.1):
+ *       x = pad(x, padding=2K)
+ *       x = conv(x, out_channels=r, stride=s, kernel_shape=2K+1, kernel_weights=W)
+ *       return pixelshuffle(x, factors=r)
+ *   ND FCFS (§4.2): the same with conv2d, out_channels=prod r_i,
+ *       stride [s_i], and the ND pixelshuffle of §4.1.
+ *
+ * Notation: the paper's factor r/s is written p/q here (p = r phases,
+ * q = s stride), reduced by gcd.
+ *
+ * Two independent evaluators live here:
+ *   fcfs_oracle_staged_*  -- the layer literally: materialised padding, a
+ *                            p^d-output-channel strided convolution with the
+ *                            full (zero-extended) kernel window, pixelshuffle,
+ *                            crop.
+ *   fcfs_oracle_direct_*  -- per-output direct evaluation of the interpolation
+ *                            formula at u = m*q/p with virtual padding; no
+ *                            convolution, no pixelshuffle.
+ * They share only the scalar weight formulas of §5.2 (pinned separately to the
+ * paper's printed values by tests/test_oracle_pins.py).
+ *
+ * Parity status: the nearest / bilinear / bicubic (Keys a=-1/2) weights, the
+ * index map, padding, pixelshuffle and the pipeline are pinned (see DESIGN.md
+ * §3).  The paper's printed 3x3 bicubic matrices are NOT
+ * reproduced by any reading -- "parity unpinned" for those two matrices (Z8).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* ---- enumerations (values mirror the public ABI numbers, by convention only) */
+enum { ORC_NEAREST = 0, ORC_BILINEAR = 1, ORC_BICUBIC = 2 };
+enum { ORC_PAD_ZERO = 0, ORC_PAD_REPLICATE = 1, ORC_PAD_REFLECT = 2 };
+enum { ORC_IN_F64 = 0, ORC_IN_F32 = 1 };
+
+#define ORC_OK 0
+#define ORC_E_ARG (-1)
+#define ORC_E_PAD (-2)
+#define ORC_E_SHAPE (-3)
+#define ORC_E_NOMEM (-4)
+#define ORC_E_WINDOW (-5)
+
+#define ORC_PMAX 64
+
+int fcfs_oracle_version(void) { return 1; }
+
+static int64_t orc_gcd(int64_t a, int64_t b) {
+    while (b) { int64_t t = a % b; a = b; b = t; }
+    return a;
+}
+
+static int64_t floordiv(int64_t a, int64_t b) { /* b > 0 */
+    int64_t d = a / b;
+    if ((a % b) != 0 && (a < 0)) d -= 1;
+    return d;
+}
+
+/* ---------------------------------------------------------------------------
+ * §5.2.3: bicubic weight W(Delta).
+ *   |D| <= 1      : 1.5|D|^3 - 2.5|D|^2 + 1            (printed)
+ *   1 < |D| < 2   : -0.5|D|^3 + 2.5|D|^2 - 4|D| - 4a   (printed; reading Z7:
+ *                   Keys' kernel with a = -1/2, so -4a = +2)
+ *   otherwise     : 0
+ * -------------------------------------------------------------------------*/
+double fcfs_oracle_cubic_weight(double delta) {
+    const double a = -0.5;
+    double d = fabs(delta);
+    if (d <= 1.0) return 1.5 * d * d * d - 2.5 * d * d + 1.0;
+    if (d < 2.0) return -0.5 * d * d * d + 2.5 * d * d - 4.0 * d - 4.0 * a;
+    return 0.0;
+}
+
+/* ---------------------------------------------------------------------------
+ * §3.1.1: "Each of the r convolution kernels produces an
+ * interpolation for offset i + (j-1)/r".  Reading Z1: output m = p*i + j
+ * (0-based phase j) samples the input coordinate u = m*q/p, so relative to the
+ * hidden position's window origin q*i the sample sits at j*q/p:
+ *     base_j = floor(j*q/p),  frac_j = (j*q mod p)/p.
+ * §5.2 weights at fraction f (reading Z2 for nearest: floor):
+ *     nearest  : tap {base}                      weight {1}          (§5.2.1)
+ *     bilinear : taps {base, base+1}             weights {1-f, f}    (§5.2.2)
+ *     bicubic  : taps {base-1 .. base+2}         weights W(f+1), W(f), W(1-f), W(2-f)
+ *                                                                    (§5.2.3)
+ * Returns the number of taps; *first_off = offset of the first tap relative
+ * to q*i; w[] receives the weights.
+ * -------------------------------------------------------------------------*/
+int fcfs_oracle_phase_taps(int mode, int p, int q, int j, int *first_off, double *w) {
+    if (p < 1 || q < 1 || j < 0 || j >= p || !first_off || !w) return ORC_E_ARG;
+    int base = (int)(((int64_t)j * q) / p);
+    double f = (double)(((int64_t)j * q) % p) / (double)p;
+    switch (mode) {
+    case ORC_NEAREST:
+        *first_off = base;
+        w[0] = 1.0;
+        return 1;
+    case ORC_BILINEAR:
+        *first_off = base;
+        w[0] = 1.0 - f;
+        w[1] = f;
+        return 2;
+    case ORC_BICUBIC:
+        *first_off = base - 1;
+        w[0] = fcfs_oracle_cubic_weight(f + 1.0);
+        w[1] = fcfs_oracle_cubic_weight(f);
+        w[2] = fcfs_oracle_cubic_weight(1.0 - f);
+        w[3] = fcfs_oracle_cubic_weight(2.0 - f);
+        return 4;
+    default:
+        return ORC_E_ARG;
+    }
+}
+
+/* The shared conv window of all p phases of one dimension: taps of every
+ * phase fall in [lo, hi] relative to q*i; T = hi - lo + 1 (the paper's
+ * kernel_shape 2K+1, taken tight -- reading Z4). */
+static int phase_window(int mode, int p, int q, int *lo, int *hi) {
+    double w[4];
+    int first, n;
+    *lo = 1 << 30;
+    *hi = -(1 << 30);
+    for (int j = 0; j < p; ++j) {
+        n = fcfs_oracle_phase_taps(mode, p, q, j, &first, w);
+        if (n < 0) return n;
+        if (first < *lo) *lo = first;
+        if (first + n - 1 > *hi) *hi = first + n - 1;
+    }
+    return ORC_OK;
+}
+
+/* 1D kernel of phase j placed in the shared T-wide window (zeros elsewhere).
+ * This is the paper's "kernel_weights=W" for one output channel (§3.1). */
+static int phase_kernel_1d(int mode, int p, int q, int j, int lo, int T, double *k) {
+    double w[4];
+    int first;
+    int n = fcfs_oracle_phase_taps(mode, p, q, j, &first, w);
+    if (n < 0) return n;
+    for (int t = 0; t < T; ++t) k[t] = 0.0;
+    for (int t = 0; t < n; ++t) k[first - lo + t] = w[t];
+    return ORC_OK;
+}
+
+/* §4.2: the 2D kernel of output channel (jy, jx) is the
+ * outer product of the 1D phase kernels (§5.2.2 prints W_{1,1} = [[.44,.22],
+ * [.22,.11]] at 3/2, an outer product).  K is T x T row-major. */
+int fcfs_oracle_kernel2d(int mode, int p, int q, int jy, int jx, int *T_out, int *lo_out,
+                         double *K) {
+    int lo, hi;
+    if (p < 1 || q < 1 || p > ORC_PMAX || q > ORC_PMAX) return ORC_E_ARG;
+    int g = (int)orc_gcd(p, q);
+    p /= g;
+    q /= g;
+    if (jy < 0 || jy >= p || jx < 0 || jx >= p) return ORC_E_ARG;
+    int rc = phase_window(mode, p, q, &lo, &hi);
+    if (rc) return rc;
+    int T = hi - lo + 1;
+    double ky[4 * ORC_PMAX], kx[4 * ORC_PMAX];
+    phase_kernel_1d(mode, p, q, jy, lo, T, ky);
+    phase_kernel_1d(mode, p, q, jx, lo, T, kx);
+    for (int a = 0; a < T; ++a)
+        for (int b = 0; b < T; ++b) K[a * T + b] = ky[a] * kx[b];
+    *T_out = T;
+    *lo_out = lo;
+    return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * §3 Padding: "Padding by 2p is the concatenation c^p|x|c^p.
+ * There are other padding methods including reflection, zeros, and repetition
+ * of edge pixels."  Reading Z5: zero = constant 0; replicate = repeat the edge
+ * element; reflect = mirror without repeating the edge element (single
+ * bounce), e.g. [1,2,3,4,5] by 1 -> [2,1,2,3,4,5,4].
+ * pad_index maps a virtual index t of an n-long array to a source index; it
+ * returns 0 when the value is the zero constant, -1 when reflect cannot reach.
+ * -------------------------------------------------------------------------*/
+static int pad_index(int64_t t, int64_t n, int pad, int64_t *src) {
+    if (t >= 0 && t < n) { *src = t; return 1; }
+    switch (pad) {
+    case ORC_PAD_ZERO:
+        return 0;
+    case ORC_PAD_REPLICATE:
+        *src = t < 0 ? 0 : n - 1;
+        return 1;
+    case ORC_PAD_REFLECT: {
+        int64_t r = t < 0 ? -t : 2 * (n - 1) - t;
+        if (r < 0 || r >= n) return -1;
+        *src = r;
+        return 1;
+    }
+    default:
+        return -1;
+    }
+}
+
+/* pad(x, left, right) of a 1D array (SPEC.md:48-56 examples are pinned). */
+int fcfs_oracle_pad1d(const double *x, int64_t n, int64_t left, int64_t right, int pad,
+                      double *out) {
+    if (n < 1 || left < 0 || right < 0) return ORC_E_ARG;
+    for (int64_t i = 0; i < n + left + right; ++i) {
+        int64_t src;
+        int k = pad_index(i - left, n, pad, &src);
+        if (k < 0) return ORC_E_PAD;
+        out[i] = k ? x[src] : 0.0;
+    }
+    return ORC_OK;
+}
+
+/* §3 Stride: (x *_s h)[i] = (x*h)[s*i], with C output
+ * channels each with its own T-tap kernel, taken as cross-correlation
+ * (reading Z6): out[c][i] = sum_t x[s*i + t] * k[c][t], for the
+ * floor((n - T)/s) + 1 positions where the window fits. */
+int fcfs_oracle_strided_conv1d(const double *x, int64_t n, const double *kern, int C, int T,
+                               int s, double *out, int64_t *npos) {
+    if (n < T || T < 1 || s < 1 || C < 1) return ORC_E_SHAPE;
+    int64_t m = (n - T) / s + 1;
+    for (int c = 0; c < C; ++c)
+        for (int64_t i = 0; i < m; ++i) {
+            double acc = 0.0;
+            for (int t = 0; t < T; ++t) acc += x[s * i + t] * kern[c * T + t];
+            out[c * m + i] = acc;
+        }
+    *npos = m;
+    return ORC_OK;
+}
+
+/* §3 Pixel Shuffling: r x N -> rN, out[r*i + j] = x[j][i]. */
+int fcfs_oracle_pixelshuffle1d(const double *h, int r, int64_t n, double *out) {
+    for (int j = 0; j < r; ++j)
+        for (int64_t i = 0; i < n; ++i) out[(int64_t)r * i + j] = h[(int64_t)j * n + i];
+    return ORC_OK;
+}
+
+/* §4.1 ND Pixelshuffle, n = 2: a (r1*r2) x N1 x N2 tensor
+ * becomes r1N1 x r2N2 with Out[i1][i2] = x[c][floor(i1/r1)][floor(i2/r2)].
+ * Reading Z10: channel c = (i1 mod r1)*r2 + (i2 mod r2) (last dim fastest, the
+ * order torch's pixel_shuffle uses); the output is independent of this choice
+ * because the kernels are generated in the same order. */
+int fcfs_oracle_pixelshuffle2d(const double *h, int r1, int r2, int64_t n1, int64_t n2,
+                               double *out) {
+    int64_t W = (int64_t)r2 * n2;
+    for (int64_t i1 = 0; i1 < (int64_t)r1 * n1; ++i1)
+        for (int64_t i2 = 0; i2 < W; ++i2) {
+            int64_t c = (i1 % r1) * r2 + (i2 % r2);
+            out[i1 * W + i2] = h[(c * n1 + i1 / r1) * n2 + i2 / r2];
+        }
+    return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * Output extent (reading Z3).  Paper: p*ceil(N/q) (§5.1 "9x9 = 3/2*(5+1)",
+ * PAPER.md:180-182).  Floor: floor(N*p/q) (the size BASELINE.json
+ * states for config 3: 128 at 5/3 -> 213).
+ * -------------------------------------------------------------------------*/
+int fcfs_oracle_output_extent(int64_t n, int p, int q, int floor_extent, int64_t *out) {
+    if (n < 1 || p < 1 || q < 1) return ORC_E_ARG;
+    int64_t g = orc_gcd(p, q);
+    int64_t pp = p / g, qq = q / g;
+    *out = floor_extent ? (n * pp) / qq : pp * ((n + qq - 1) / qq);
+    return ORC_OK;
+}
+
+/* Input row window: the oracle may be handed only global rows
+ * [row0, row0 + nrows) of an H-row plane (strip tests).  Values are read as
+ * double from either a double or a float32 array. */
+typedef struct {
+    const void *x;
+    int in_kind;
+    int64_t H, W, row0, nrows, plane_stride;
+} orc_src;
+
+static double src_at(const orc_src *s, int64_t plane, int64_t r, int64_t c) {
+    int64_t idx = plane * s->plane_stride + (r - s->row0) * s->W + c;
+    if (s->in_kind == ORC_IN_F32) return (double)((const float *)s->x)[idx];
+    return ((const double *)s->x)[idx];
+}
+
+typedef struct {
+    int p, q, mode, pad, is1d;
+    int64_t H, W, Ho, Wo;
+} orc_job;
+
+static int make_job(int64_t H, int64_t W, int p, int q, int mode, int pad, int floor_ext,
+                    int is1d, orc_job *j) {
+    if (p < 1 || q < 1 || p > ORC_PMAX || q > ORC_PMAX || H < 1 || W < 1) return ORC_E_ARG;
+    if (mode < 0 || mode > 2 || pad < 0 || pad > 2) return ORC_E_ARG;
+    int64_t g = orc_gcd(p, q);
+    j->p = (int)(p / g);
+    j->q = (int)(q / g);
+    j->mode = mode;
+    j->pad = pad;
+    j->is1d = is1d;
+    j->H = H;
+    j->W = W;
+    fcfs_oracle_output_extent(W, j->p, j->q, floor_ext, &j->Wo);
+    if (is1d) j->Ho = H;
+    else fcfs_oracle_output_extent(H, j->p, j->q, floor_ext, &j->Ho);
+    if (j->Ho < 1 || j->Wo < 1) return ORC_E_SHAPE;
+    return ORC_OK;
+}
+
+/* Value of the padded plane at virtual (r, c); rows are padded only in 2D.
+ * Returns ORC_E_PAD / ORC_E_WINDOW through *err. */
+static double padded_at(const orc_src *s, const orc_job *jb, int64_t plane, int64_t r,
+                        int64_t c, int *err) {
+    int64_t sr, sc;
+    int kr = pad_index(r, s->H, jb->pad, &sr);
+    int kc = pad_index(c, s->W, jb->pad, &sc);
+    if (kr < 0 || kc < 0) { *err = ORC_E_PAD; return 0.0; }
+    if (kr == 0 || kc == 0) return 0.0;
+    if (sr < s->row0 || sr >= s->row0 + s->nrows) { *err = ORC_E_WINDOW; return 0.0; }
+    return src_at(s, plane, sr, sc);
+}
+
+/* Reflect feasibility over the taps the kept outputs reach, zero-weight taps
+ * of an output's own tap list included (bilinear at f = 0 still lists
+ * {b, b+1}): reflect needs every reached virtual index to fold back inside the
+ * array with one bounce.  The furthest taps are those of
+ * output 0 (first tap) and of the last kept output (last tap). */
+static int check_reach(const orc_job *jb) {
+    if (jb->pad != ORC_PAD_REFLECT) return ORC_OK;
+    double w[4];
+    int first0, first_last;
+    int64_t dims[2] = {jb->W, jb->H}, outs[2] = {jb->Wo, jb->Ho};
+    for (int d = 0; d < (jb->is1d ? 1 : 2); ++d) {
+        int64_t n = dims[d];
+        int64_t mlast = outs[d] - 1;
+        fcfs_oracle_phase_taps(jb->mode, jb->p, jb->q, 0, &first0, w);
+        int nt = fcfs_oracle_phase_taps(jb->mode, jb->p, jb->q, (int)(mlast % jb->p), &first_last, w);
+        int64_t vmin = first0; /* output 0: hidden position 0, phase 0 */
+        int64_t vmax = (int64_t)jb->q * (mlast / jb->p) + first_last + nt - 1;
+        int64_t s;
+        if (vmin < 0 && pad_index(vmin, n, ORC_PAD_REFLECT, &s) < 0) return ORC_E_PAD;
+        if (vmax > n - 1 && pad_index(vmax, n, ORC_PAD_REFLECT, &s) < 0) return ORC_E_PAD;
+    }
+    return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * STAGED evaluator, 2D (§4.2), one plane, output rows
+ * [r0, r1) (all Wo columns).  Steps in the paper's order:
+ *   1. pad     : materialise the padded window the conv reads (§3 Padding);
+ *   2. conv2d  : p*p output channels, stride [q, q], kernel T x T (§4.2, §3 Stride);
+ *   3. pixelshuffle([p, p])  (§4.1);
+ *   4. crop to the output extent (reading Z3).
+ * The hidden layer has ceil(Wo/p) columns and the rows needed by [r0, r1):
+ * its shape p^2 x N/q is "the space and time complexity" (§3.1.1).
+ * -------------------------------------------------------------------------*/
+static int staged_plane_2d(const orc_src *s, const orc_job *jb, int64_t plane, int64_t r0,
+                           int64_t r1, double *out) {
+    int p = jb->p, q = jb->q, lo, hi, err = 0;
+    phase_window(jb->mode, p, q, &lo, &hi);
+    int T = hi - lo + 1;
+    int64_t iy0 = r0 / p, iy1 = (r1 - 1) / p + 1; /* hidden rows [iy0, iy1)       */
+    int64_t nix = (jb->Wo + p - 1) / p;            /* hidden cols [0, nix)         */
+    int64_t nhy = iy1 - iy0;
+    /* 1. pad: padded rows cover virtual rows [q*iy0 + lo, q*(iy1-1) + hi],
+     *    padded cols cover virtual cols [lo, q*(nix-1) + hi]. */
+    int64_t PR = (nhy - 1) * q + T, PC = (nix - 1) * q + T;
+    int64_t vr0 = (int64_t)q * iy0 + lo, vc0 = lo;
+    double *xp = (double *)malloc(sizeof(double) * PR * PC);
+    double *hid = (double *)malloc(sizeof(double) * (size_t)p * p * nhy * nix);
+    double *sh = (double *)malloc(sizeof(double) * (size_t)p * nhy * p * nix);
+    double *K = (double *)malloc(sizeof(double) * (size_t)p * p * T * T);
+    if (!xp || !hid || !sh || !K) { free(xp); free(hid); free(sh); free(K); return ORC_E_NOMEM; }
+    for (int64_t a = 0; a < PR; ++a)
+        for (int64_t b = 0; b < PC; ++b) {
+            int e = 0;
+            double v = padded_at(s, jb, plane, vr0 + a, vc0 + b, &e);
+            if (e == ORC_E_WINDOW) { err = e; goto done; }
+            /* positions reflect cannot reach only feed cropped outputs (check_reach
+             * validated the kept ones); they are filled with the clamped edge. */
+            if (e == ORC_E_PAD) {
+                int64_t rr = vr0 + a < 0 ? 0 : (vr0 + a >= s->H ? s->H - 1 : vr0 + a);
+                int64_t cc = vc0 + b < 0 ? 0 : (vc0 + b >= s->W ? s->W - 1 : vc0 + b);
+                int e2 = 0;
+                v = padded_at(s, jb, plane, rr, cc, &e2);
+                if (e2) { err = e2; goto done; }
+            }
+            xp[a * PC + b] = v;
+        }
+    /* 2. conv2d, out_channels = p*p, stride [q, q], kernel T x T. */
+    for (int jy = 0; jy < p; ++jy)
+        for (int jx = 0; jx < p; ++jx) {
+            int TT, llo;
+            fcfs_oracle_kernel2d(jb->mode, p, q, jy, jx, &TT, &llo, K + (size_t)(jy * p + jx) * T * T);
+        }
+    for (int c = 0; c < p * p; ++c)
+        for (int64_t iy = 0; iy < nhy; ++iy)
+            for (int64_t ix = 0; ix < nix; ++ix) {
+                double acc = 0.0;
+                const double *k = K + (size_t)c * T * T;
+                for (int a = 0; a < T; ++a)
+                    for (int b = 0; b < T; ++b)
+                        acc += xp[(q * iy + a) * PC + q * ix + b] * k[a * T + b];
+                hid[((size_t)c * nhy + iy) * nix + ix] = acc;
+            }
+    /* 3. pixelshuffle([p, p]) */
+    fcfs_oracle_pixelshuffle2d(hid, p, p, nhy, nix, sh);
+    /* 4. crop */
+    for (int64_t r = r0; r < r1; ++r)
+        for (int64_t m = 0; m < jb->Wo; ++m)
+            out[(r - r0) * jb->Wo + m] = sh[(r - iy0 * p) * (p * nix) + m];
+done:
+    free(xp);
+    free(hid);
+    free(sh);
+    free(K);
+    return err;
+}
+
+/* STAGED evaluator, 1D (§3.1) along W for every row of the
+ * plane (flag "1D": the H rows are independent signals). */
+static int staged_row_1d(const orc_src *s, const orc_job *jb, int64_t plane, int64_t r,
+                         double *out) {
+    int p = jb->p, q = jb->q, lo, hi, err = 0;
+    phase_window(jb->mode, p, q, &lo, &hi);
+    int T = hi - lo + 1;
+    int64_t ni = (jb->Wo + p - 1) / p;
+    int64_t L = (ni - 1) * q + T;
+    double *xp = (double *)malloc(sizeof(double) * L);
+    double *K = (double *)malloc(sizeof(double) * (size_t)p * T);
+    double *hid = (double *)malloc(sizeof(double) * (size_t)p * ni);
+    double *sh = (double *)malloc(sizeof(double) * (size_t)p * ni);
+    if (!xp || !K || !hid || !sh) { free(xp); free(K); free(hid); free(sh); return ORC_E_NOMEM; }
+    /* 1. pad */
+    for (int64_t b = 0; b < L; ++b) {
+        int64_t sc;
+        int k = pad_index(lo + b, s->W, jb->pad, &sc);
+        if (k < 0) { /* unreachable by kept outputs (check_reach) */
+            sc = lo + b < 0 ? 0 : s->W - 1;
+            k = 1;
+        }
+        if (r < s->row0 || r >= s->row0 + s->nrows) { err = ORC_E_WINDOW; goto done; }
+        xp[b] = k ? src_at(s, plane, r, sc) : 0.0;
+    }
+    /* 2. conv, out_channels = p, stride q, kernel T */
+    for (int j = 0; j < p; ++j) phase_kernel_1d(jb->mode, p, q, j, lo, T, K + (size_t)j * T);
+    int64_t npos;
+    fcfs_oracle_strided_conv1d(xp, L, K, p, T, q, hid, &npos);
+    /* 3. pixelshuffle(p) */
+    fcfs_oracle_pixelshuffle1d(hid, p, npos, sh);
+    /* 4. crop */
+    for (int64_t m = 0; m < jb->Wo; ++m) out[m] = sh[m];
+done:
+    free(xp);
+    free(K);
+    free(hid);
+    free(sh);
+    return err;
+}
+
+/* Public staged entry point.
+ *   x          : planes x nrows x W input (global rows [row0, row0+nrows) of
+ *                an H-row image), double or float32 (in_kind)
+ *   out        : planes x (r1 - r0) x Wo, double
+ *   r0, r1     : output rows to produce (r1 <= 0 means all Ho rows)
+ *   nthreads   : OpenMP threads (0 = runtime default); every output is computed
+ *                by one thread in a fixed order, so results do not depend on it.
+ */
+int fcfs_oracle_staged(const void *x, int in_kind, int64_t planes, int64_t H, int64_t W,
+                       int64_t row0, int64_t nrows, int p, int q, int mode, int pad,
+                       int floor_ext, int is1d, int64_t r0, int64_t r1, double *out,
+                       int nthreads) {
+    orc_job jb;
+    int rc = make_job(H, W, p, q, mode, pad, floor_ext, is1d, &jb);
+    if (rc) return rc;
+    if (r1 <= 0) { r0 = 0; r1 = jb.Ho; }
+    if (r0 < 0 || r1 > jb.Ho || r0 >= r1) return ORC_E_ARG;
+    rc = check_reach(&jb);
+    if (rc) return rc;
+    orc_src s = {x, in_kind, H, W, row0, nrows, nrows * W};
+    int64_t nr = r1 - r0;
+    /* work items: (plane, block of output rows) */
+    const int64_t RB = is1d ? 64 : (int64_t)jb.p * 16;
+    int64_t nb = (nr + RB - 1) / RB;
+    int64_t nitems = planes * nb;
+    int bad = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+    for (int64_t it = 0; it < nitems; ++it) {
+        int64_t pl = it / nb, b = it % nb;
+        int64_t a0 = r0 + b * RB, a1 = a0 + RB < r1 ? a0 + RB : r1;
+        double *o = out + (pl * nr + (a0 - r0)) * jb.Wo;
+        int e = 0;
+        if (is1d) {
+            for (int64_t r = a0; r < a1 && !e; ++r) e = staged_row_1d(&s, &jb, pl, r, o + (r - a0) * jb.Wo);
+        } else {
+            e = staged_plane_2d(&s, &jb, pl, a0, a1, o);
+        }
+        if (e) {
+#ifdef _OPENMP
+#pragma omp atomic write
+#endif
+            bad = e;
+        }
+    }
+    return bad;
+}
+
+/* ---------------------------------------------------------------------------
+ * DIRECT evaluator (independent of the staged one): for output (m_y, m_x),
+ * u = m*q/p per dimension (reading Z1), base b = (m*q) div p, fraction
+ * f = ((m*q) mod p)/p; the §5.2 weights at f; virtual padding.
+ *   nearest : y = x~[b_y][b_x]
+ *   bilinear: y = sum_{a,c in {0,1}} w_a(f_y) w_c(f_x) x~[b_y+a][b_x+c]
+ *   bicubic : y = sum_{a,c in {-1..2}} W(f_y - a) W(f_x - c) x~[b_y+a][b_x+c]
+ * -------------------------------------------------------------------------*/
+static int direct_weights(int mode, double f, int *first, double *w) {
+    switch (mode) {
+    case ORC_NEAREST:
+        *first = 0;
+        w[0] = 1.0;
+        return 1;
+    case ORC_BILINEAR:
+        *first = 0;
+        w[0] = 1.0 - f;
+        w[1] = f;
+        return 2;
+    default:
+        *first = -1;
+        for (int t = -1; t <= 2; ++t) w[t + 1] = fcfs_oracle_cubic_weight(f - (double)t);
+        return 4;
+    }
+}
+
+static double direct_one(const orc_src *s, const orc_job *jb, int64_t plane, int64_t my,
+                         int64_t mx, int *err) {
+    double wy[4], wx[4];
+    int fy0, fx0, ny, nx;
+    int64_t by, bx;
+    if (jb->is1d) {
+        by = my;
+        fy0 = 0;
+        ny = 1;
+        wy[0] = 1.0;
+    } else {
+        by = floordiv(my * jb->q, jb->p);
+        ny = direct_weights(jb->mode, (double)((my * jb->q) % jb->p) / jb->p, &fy0, wy);
+    }
+    bx = floordiv(mx * jb->q, jb->p);
+    nx = direct_weights(jb->mode, (double)((mx * jb->q) % jb->p) / jb->p, &fx0, wx);
+    double acc = 0.0;
+    for (int a = 0; a < ny; ++a) {
+        for (int c = 0; c < nx; ++c) {
+            int e = 0;
+            int64_t r = by + fy0 + a, col = bx + fx0 + c;
+            double v;
+            if (jb->is1d) {
+                int64_t sc;
+                int k = pad_index(col, s->W, jb->pad, &sc);
+                if (k < 0) { *err = ORC_E_PAD; return 0.0; }
+                if (r < s->row0 || r >= s->row0 + s->nrows) { *err = ORC_E_WINDOW; return 0.0; }
+                v = k ? src_at(s, plane, r, sc) : 0.0;
+            } else {
+                v = padded_at(s, jb, plane, r, col, &e);
+                if (e) { *err = e; return 0.0; }
+            }
+            acc += wy[a] * wx[c] * v;
+        }
+    }
+    return acc;
+}
+
+/* Direct evaluation of output rows [r0, r1) (all columns) of every plane. */
+int fcfs_oracle_direct_rows(const void *x, int in_kind, int64_t planes, int64_t H, int64_t W,
+                            int64_t row0, int64_t nrows, int p, int q, int mode, int pad,
+                            int floor_ext, int is1d, int64_t r0, int64_t r1, double *out,
+                            int nthreads) {
+    orc_job jb;
+    int rc = make_job(H, W, p, q, mode, pad, floor_ext, is1d, &jb);
+    if (rc) return rc;
+    if (r1 <= 0) { r0 = 0; r1 = jb.Ho; }
+    if (r0 < 0 || r1 > jb.Ho || r0 >= r1) return ORC_E_ARG;
+    rc = check_reach(&jb);
+    if (rc) return rc;
+    orc_src s = {x, in_kind, H, W, row0, nrows, nrows * W};
+    int64_t nr = r1 - r0;
+    int bad = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(static)
+#endif
+    for (int64_t it = 0; it < planes * nr; ++it) {
+        int64_t pl = it / nr, r = r0 + it % nr;
+        int e = 0;
+        for (int64_t m = 0; m < jb.Wo && !e; ++m)
+            out[it * jb.Wo + m] = direct_one(&s, &jb, pl, r, m, &e);
+        if (e) {
+#ifdef _OPENMP
+#pragma omp atomic write
+#endif
+            bad = e;
+        }
+    }
+    return bad;
+}
+
+/* Direct evaluation at n sampled outputs pts[3*i .. 3*i+2] = (plane, my, mx). */
+int fcfs_oracle_direct_points(const void *x, int in_kind, int64_t planes, int64_t H,
+                              int64_t W, int64_t row0, int64_t nrows, int p, int q, int mode,
+                              int pad, int floor_ext, int is1d, const int64_t *pts, int64_t n,
+                              double *out, int nthreads) {
+    orc_job jb;
+    int rc = make_job(H, W, p, q, mode, pad, floor_ext, is1d, &jb);
+    if (rc) return rc;
+    rc = check_reach(&jb);
+    if (rc) return rc;
+    orc_src s = {x, in_kind, H, W, row0, nrows, nrows * W};
+    int bad = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(static)
+#endif
+    for (int64_t i = 0; i < n; ++i) {
+        int e = 0;
+        int64_t pl = pts[3 * i], my = pts[3 * i + 1], mx = pts[3 * i + 2];
+        if (pl < 0 || pl >= planes || my < 0 || my >= jb.Ho || mx < 0 || mx >= jb.Wo) e = ORC_E_ARG;
+        else out[i] = direct_one(&s, &jb, pl, my, mx, &e);
+        if (e) {
+#ifdef _OPENMP
+#pragma omp atomic write
+#endif
+            bad = e;
+        }
+    }
+    return bad;
+}
