@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""FCFS hot-path benchmark (BASELINE.json metric: output Mpix/s and achieved
+HBM GB/s vs 8 TB/s, 1/2/4/8 B200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2] [--impl fcfs|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU, NCCL)
+
+A step is one pass of the whole hot path over one batch: every launch of the
+workload (C2 = nearest 2/3 and 3/4 on 16x3x512^2 fp32, BASELINE.json
+configs[1]).  Batched workloads scale weakly: every rank scales its own batch,
+no data-path collective.  C5 (one 32768^2 image) shards by row strips with an
+NCCL halo exchange when N > 1 (paper_2203_10670_b200.dist).
+
+Prints ONE JSON line on rank 0.  Inputs are resident in HBM before the timed
+region; between steps the input/output buffers rotate over a set larger than
+4x L2, so no step reads its input from L2.  Times are CUDA events on the
+launching stream, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "FCFS resize output Mpix/s per GPU and achieved HBM GB/s vs 8 TB/s, 1/2/4/8 B200"
+DTYPE_TAG = {"float32": "f32", "float16": "f16", "bfloat16": "bf16"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="C2", choices=sorted(synth.WORKLOADS))
+    ap.add_argument("--impl", default="fcfs", choices=["fcfs", "reference"])
+    ap.add_argument("--soak-s", type=float, default=1.0, help="untimed steady-state run before warm-up (clocks)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the run."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.marks = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.idx)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, name):
+        self.marks.append((name, time.time()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        rows = []
+        for ts, line in self.lines:
+            if t0 - 0.15 <= ts <= t1 + 0.15:
+                f = [x.strip() for x in line.split(",")]
+                if len(f) >= 9:
+                    rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+
+
+def physical_gpu_index(local_rank: int) -> int:
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        try:
+            return int(vis.split(",")[local_rank])
+        except Exception:
+            return local_rank
+    return local_rank
+
+
+# --------------------------------------------------------------------------- CPU oracle leg
+def oracle_sample_run(cfgs, planes_per_cfg: int):
+    """Run the oracle (staged, as it stands) on `planes_per_cfg` planes of every
+    launch of the workload; returns (outputs, seconds, description)."""
+    import oracle
+    outs, secs, parts = 0, 0.0, []
+    for cfg in cfgs:
+        n_img = max(1, min(cfg.N, -(-planes_per_cfg // cfg.C)))
+        if cfg.values == "field":
+            rows = (0, min(cfg.H, 600))
+            x = synth.make_values(cfg, 0, 1, rows=rows)
+            Ho_rows = (0, (rows[1] * cfg.p) // cfg.q - 2)
+            t0 = time.perf_counter()
+            y = oracle.staged(x[0], cfg.p, cfg.q, cfg.mode, cfg.pad, floor_extent=True, rows=Ho_rows, H=cfg.H)
+            secs += time.perf_counter() - t0
+            outs += y.size
+            parts.append(f"{cfg.name}: output rows {Ho_rows[0]}..{Ho_rows[1]} of 1 plane")
+            continue
+        x = synth.make_values(cfg, 0, n_img)
+        t0 = time.perf_counter()
+        y = oracle.staged(x, cfg.p, cfg.q, cfg.mode, cfg.pad, floor_extent=cfg.floor_extent, is1d=cfg.is1d)
+        secs += time.perf_counter() - t0
+        outs += y.size
+        parts.append(f"{cfg.name}: {n_img * cfg.C} of {cfg.planes} planes")
+    return outs, secs, "; ".join(parts)
+
+
+def cpu_baseline(cfgs, budget_s=15.0):
+    cores = os.cpu_count() or 1
+    planes = max(1, cores)
+    outs, secs, desc = oracle_sample_run(cfgs, planes)
+    # grow the sample toward the time budget (bounded)
+    while secs < budget_s / 4 and planes < 4096:
+        planes *= 4
+        outs, secs, desc = oracle_sample_run(cfgs, planes)
+        if all(planes >= c.planes for c in cfgs):
+            break
+    return {"value": outs / secs / 1e6, "unit": "Mpix/s", "cores": cores, "kind": "oracle",
+            "sample": f"staged C oracle (double, OpenMP {cores} threads) on {desc}; {secs:.2f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfgs = [synth.CONFIGS[n] for n in synth.WORKLOADS[args.workload]]
+    cores = os.cpu_count() or 1
+    planes = max(1, cores)
+    for _ in range(args.warmup):
+        oracle_sample_run(cfgs, planes)
+    tot_o, tot_s, desc = 0, 0.0, ""
+    for _ in range(args.steps):
+        o, s, desc = oracle_sample_run(cfgs, planes)
+        tot_o += o
+        tot_s += s
+    value = tot_o / tot_s / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": DTYPE_TAG[cfgs[0].dtype], "data": "synthetic",
+            "config": {"workload": args.workload, "launches": [c.name for c in cfgs]},
+            "cpu_baseline": {"value": value, "unit": "Mpix/s", "cores": cores, "kind": "oracle",
+                             "sample": f"each step: {desc}"},
+            "e2e": {"value": value, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU leg
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2203_10670_b200 as fc
+
+    cfgs = [synth.CONFIGS[n] for n in synth.WORKLOADS[args.workload]]
+    if args.workload == "C5" and world > 1:
+        from paper_2203_10670_b200 import dist as fdist
+        return fdist.bench_strips(args, cfgs[0], rank, world, dev, METRIC)
+
+    stream = torch.cuda.current_stream(dev)
+    props = torch.cuda.get_device_properties(dev)
+    l2 = getattr(props, "L2_cache_size", 126 * 2 ** 20) or 126 * 2 ** 20
+    launches = []
+    for cfg in cfgs:
+        pl = fc.Plan(cfg.p, cfg.q, cfg.mode, cfg.pad, cfg.C, cfg.H, cfg.W, cfg.dtype,
+                     "floor" if cfg.floor_extent else "paper", cfg.is1d)
+        x = synth.make_input(cfg, batch_offset=rank * cfg.N)
+        launches.append({"cfg": cfg, "plan": pl, "x_host": x, "bytes": pl.compulsory_bytes(cfg.N),
+                         "outputs": cfg.N * cfg.C * pl.Ho * pl.Wo})
+    # input/output buffers per rotation set; several launches may share one input
+    set_bytes = 0
+    host_inputs = {}
+    for L in launches:
+        key = (L["cfg"].seed, L["cfg"].N, L["cfg"].H, L["cfg"].W, L["cfg"].dtype)
+        if key not in host_inputs:
+            host_inputs[key] = L["x_host"]
+            set_bytes += L["x_host"].numel() * L["x_host"].element_size()
+        L["key"] = key
+        set_bytes += L["outputs"] * L["x_host"].element_size()
+    R = max(2, min(64, -(-4 * l2 // set_bytes)))
+    free = torch.cuda.mem_get_info(dev)[0]
+    R = max(1, min(R, int(0.8 * free // set_bytes)))
+    dev_inputs = {k: [v.to(dev) for _ in range(R)] for k, v in host_inputs.items()}
+    for L in launches:
+        L["outs"] = [torch.empty((L["cfg"].N, L["cfg"].C, L["plan"].Ho, L["plan"].Wo), dtype=L["x_host"].dtype,
+                                 device=dev) for _ in range(R)]
+    torch.cuda.synchronize(dev)
+
+    def step(r, evs=None):
+        for i, L in enumerate(launches):
+            if evs is not None:
+                evs[i][0].record(stream)
+            L["plan"].run(dev_inputs[L["key"]][r], out=L["outs"][r], stream=stream)
+            if evs is not None:
+                evs[i][1].record(stream)
+
+    sampler = ClockSampler(physical_gpu_index(local))
+    sampler.start()
+    t_soak0 = time.time()
+    k = 0
+    while time.time() - t_soak0 < args.soak_s:
+        for _ in range(50):
+            step(k % R)
+            k += 1
+        torch.cuda.synchronize(dev)
+    for w in range(args.warmup):
+        step(w % R)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in launches]
+           for _ in range(args.steps)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_wall0 = time.time()
+    e0.record(stream)
+    for s in range(args.steps):
+        step(s % R, evs[s])
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    t_wall1 = time.time()
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = e0.elapsed_time(e1)
+    per_launch_ms = [sum(evs[s][i][0].elapsed_time(evs[s][i][1]) for s in range(args.steps)) / args.steps
+                     for i in range(len(launches))]
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    clocks = sampler.summary(t_soak0, t_wall1)
+    sampler.stop()
+
+    outputs_per_step = sum(L["outputs"] for L in launches)
+    bytes_per_step = sum(L["bytes"] for L in launches)
+    ms_per_step = elapsed_ms / args.steps
+    value = world * outputs_per_step * args.steps / (elapsed_ms * 1e-3) / 1e6
+    peak, peak_kind = peaks()
+    dom = max(range(len(launches)), key=lambda i: per_launch_ms[i])
+    dom_ms = per_launch_ms[dom]
+    achieved = launches[dom]["bytes"] / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        traffic = tj.get(launches[dom]["cfg"].name)
+    except Exception:
+        pass
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(launches, args, dev, stream, world, dist)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": DTYPE_TAG[cfgs[0].dtype], "data": "synthetic",
+        "config": {"workload": args.workload, "launches": [
+            {"name": L["cfg"].name, "shape": [L["cfg"].N, L["cfg"].C, L["cfg"].H, L["cfg"].W],
+             "factor": f"{L['cfg'].p}/{L['cfg'].q}", "mode": L["cfg"].mode, "pad": L["cfg"].pad,
+             "dtype": L["cfg"].dtype, "out": [L["plan"].Ho, L["plan"].Wo], "kernel": L["plan"].kernel,
+             "compulsory_bytes": L["bytes"], "avg_launch_us": per_launch_ms[i] * 1e3}
+            for i, L in enumerate(launches)],
+            "per_rank_batch": "own batch per rank (weak scaling)",
+            "l2": f"rotating {R} buffer sets of {set_bytes / 2**20:.0f} MiB (> 4x {l2 / 2**20:.0f} MiB L2); no flush",
+            "soak_s": args.soak_s, "parallelism": f"dp{world}"},
+        "per_gpu_mpix_s": value / world,
+        "achieved_GBps_step": bytes_per_step / (ms_per_step * 1e-3) / 1e9,
+        "frac_of_8TBps_step": bytes_per_step / (ms_per_step * 1e-3) / 8e12,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": launches[dom]["plan"].kernel, "launch": launches[dom]["cfg"].name,
+                     "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs" if peak_kind == "measured" else
+                     "fallback 6.65 TB/s (B200_PROFILING.md)",
+                     "algorithmic_bytes_per_launch": launches[dom]["bytes"], "avg_launch_us": dom_ms * 1e3},
+        "gpu_launches": args.steps * len(launches),
+        "clocks": clocks,
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfgs)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(launches, args, dev, stream, world, dist):
+    """Same metric through the public host-buffer call (fcfs_run_host): every step
+    copies its inputs H2D from pinned memory, runs, and reads the outputs D2H."""
+    import torch
+    pin_in = {}
+    for L in launches:
+        if L["key"] not in pin_in:
+            pin_in[L["key"]] = L["x_host"].pin_memory()
+        L["pin_out"] = torch.empty(L["outs"][0].shape, dtype=L["x_host"].dtype).pin_memory()
+    din = {k: torch.empty(v.shape, dtype=v.dtype, device=dev) for k, v in pin_in.items()}
+    h2d = sum(v.numel() * v.element_size() for v in pin_in.values()) * 0
+    # every launch copies its own input (the C-ABI call is per launch)
+    h2d = sum(pin_in[L["key"]].numel() * pin_in[L["key"]].element_size() for L in launches)
+    d2h = sum(L["pin_out"].numel() * L["pin_out"].element_size() for L in launches)
+
+    def step():
+        for L in launches:
+            L["plan"].run_host(pin_in[L["key"]], L["pin_out"], din[L["key"]], L["outs"][0], stream=stream)
+
+    for _ in range(max(2, args.warmup)):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    steps = max(1, min(args.steps, 50))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    outputs = sum(L["outputs"] for L in launches)
+    return {"value": world * outputs * steps / (ms * 1e-3) / 1e6, "unit": "Mpix/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": steps, "ms_per_step": ms / steps,
+            "path": "fcfs_run_host (pinned host -> HBM -> kernel -> pinned host)"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

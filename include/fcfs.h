@@ -1,0 +1,183 @@
+/*
+ * include/fcfs.h -- C ABI of the B200-native FCFS hot path (libfcfs.so).
+ *
+ * FCFS, "Fully Convolutional Fractional Scaling" (arXiv 2203.10670), resizes
+ * a signal by a rational factor p/q (the paper's r/s) as ONE
+ * layer (§3.1; ND form §4.2):
+ *
+ *     x = pad(x, padding = 2K)                                  (§3 Padding)
+ *     x = conv(x, out_channels = p (1D) or p*p (2D), stride = q,
+ *              kernel_shape = 2K+1, kernel_weights = W)         (§3 Stride)
+ *     return pixelshuffle(x, factors = p)                       (§3; §4.1, :129-139)
+ *
+ * with W the nearest / bilinear / bicubic phase kernels of §5.2
+ * (PAPER.md:191-229).  Output m (per dimension, 0-based) samples input
+ * coordinate m*q/p: base floor(m*q/p), fraction ((m*q) mod p)/p (DESIGN.md
+ * reading Z1; nearest takes the base pixel, reading Z2; bicubic is Keys'
+ * kernel with a = -1/2, reading Z7).  The library evaluates pad + strided
+ * polyphase convolution + pixelshuffle in one fused sm_100a pass; the p^d-
+ * channel hidden layer (§3.1.1) never exists in memory.
+ *
+ * Conventions for every entry point:
+ *   - Every function returns fcfs_status (FCFS_OK = 0) and never throws or
+ *     aborts; fcfs_destroy returns nothing.
+ *   - Tensors are dense, contiguous NCHW with W fastest; the element type is
+ *     the plan's dtype for both input and output.  Input N x C x H x W,
+ *     output N x C x Ho x Wo (fcfs_output_shape).  With FCFS_FLAG_1D only W
+ *     is scaled (Ho = H; each row is an independent 1D signal).
+ *   - Device pointers are CUDA device addresses on the plan's device; the
+ *     caller owns them.  Input and output must not overlap (FCFS_E_ARG).
+ *   - Runs are asynchronous on the caller's stream (a cudaStream_t passed as
+ *     void*; NULL = legacy default stream) and never allocate device memory.
+ *   - A plan is immutable after fcfs_plan*; concurrent runs of one plan on
+ *     different streams are allowed.  The caller must let every run finish
+ *     before fcfs_destroy.
+ *   - Arithmetic: fp32 accumulation with fp32 phase weights for every dtype;
+ *     fp16/bf16 outputs are rounded to nearest even.  Nearest-neighbour is a
+ *     pure copy (bit-exact).  For a given plan the value of every output does
+ *     not depend on N, on the stream, on row windows (strips) or on which
+ *     kernel variant ran.
+ */
+#ifndef FCFS_H_
+#define FCFS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FCFS_VERSION 1
+#define FCFS_MAX_FACTOR 64 /* p and q (after gcd reduction) must be <= 64 */
+
+typedef struct fcfs_plan_s *fcfs_plan_t;
+
+/* Interpolation method, §5.2.1-§5.2.3. */
+typedef enum { FCFS_NEAREST = 0, FCFS_BILINEAR = 1, FCFS_BICUBIC = 2 } fcfs_mode;
+
+/* Padding mode, §3: zeros, repetition of edge pixels,
+ * reflection (mirror without repeating the edge pixel: [1,2,3] -> [2|1,2,3|2]). */
+typedef enum { FCFS_PAD_ZERO = 0, FCFS_PAD_REPLICATE = 1, FCFS_PAD_REFLECT = 2 } fcfs_pad;
+
+/* Element type of input and output (compute is fp32). */
+typedef enum { FCFS_F32 = 0, FCFS_F16 = 1, FCFS_BF16 = 2 } fcfs_dtype;
+
+enum {
+    FCFS_FLAG_1D = 1u << 0,           /* scale W only; the H rows are independent 1D signals (§3.1) */
+    FCFS_FLAG_EXTENT_FLOOR = 1u << 1, /* Ho,Wo = floor(N*p/q) instead of the paper's p*ceil(N/q) (§5.1) */
+    FCFS_FLAG_FORCE_REFERENCE = 1u << 8 /* diagnostic: always run the one-thread-per-output reference
+                                           kernel (same arithmetic, bitwise-identical results) */
+};
+
+typedef enum {
+    FCFS_OK = 0,
+    FCFS_E_ARG = 1,         /* bad argument: p,q out of [1,64]; C,H,W < 1; N < 0; unknown enum; NULL
+                               pointer; overlapping in/out; bad row window arguments */
+    FCFS_E_SHAPE = 2,       /* empty output extent (e.g. 5 at 2/11 with FCFS_FLAG_EXTENT_FLOOR), or a row
+                               window that does not hold the rows the requested outputs need */
+    FCFS_E_PAD = 3,         /* reflect padding cannot reach a needed tap (dimension too small) */
+    FCFS_E_UNSUPPORTED = 4, /* configuration the library does not implement */
+    FCFS_E_DEVICE = 5,      /* no CUDA device, or the current device is not the plan's device */
+    FCFS_E_CUDA = 6,        /* a CUDA call or kernel launch failed (cudaGetLastError) */
+    FCFS_E_NOMEM = 7        /* host allocation failed */
+} fcfs_status;
+
+/* fcfs_plan_ex -- validate a scaling job and precompute everything a run
+ * needs (host only; no device memory is allocated).
+ *   p, q   : scale factor p/q (paper r/s), each in [1, 64] after reduction by
+ *            gcd ("stored reduced").
+ *   mode   : fcfs_mode;  pad: fcfs_pad;  dtype: fcfs_dtype.
+ *   C, H, W: channels and spatial size of one image (N is given per run).
+ *   flags  : FCFS_FLAG_*.
+ *   out    : receives the plan; unchanged on error.
+ * Errors: FCFS_E_ARG, FCFS_E_SHAPE (empty extent), FCFS_E_PAD (reflect needs a
+ * tap beyond one mirror bounce), FCFS_E_NOMEM.  Records the current CUDA
+ * device if there is one (runs on another device fail with FCFS_E_DEVICE). */
+fcfs_status fcfs_plan_ex(int p, int q, int mode, int pad, int64_t C, int64_t H, int64_t W, int dtype,
+                         unsigned flags, fcfs_plan_t *out);
+
+/* fcfs_plan -- fcfs_plan_ex with flags = 0 (paper extent, 2D). */
+fcfs_status fcfs_plan(int p, int q, int mode, int pad, int64_t C, int64_t H, int64_t W, int dtype,
+                      fcfs_plan_t *out);
+
+/* Output spatial size (Ho, Wo): paper extent p*ceil(N/q) (§5.1,
+ * 5x5 at 3/2 -> 9x9) or floor(N*p/q) with
+ * FCFS_FLAG_EXTENT_FLOOR; Ho = H with FCFS_FLAG_1D. */
+fcfs_status fcfs_output_shape(fcfs_plan_t plan, int64_t *Ho, int64_t *Wo);
+
+/* fcfs_run -- scale a batch.  in: device N x C x H x W; out: device
+ * N x C x Ho x Wo; N >= 0 (N = 0 is a no-op); stream: cudaStream_t or NULL.
+ * Errors: FCFS_E_ARG (NULL/overlap), FCFS_E_DEVICE, FCFS_E_CUDA. */
+fcfs_status fcfs_run(fcfs_plan_t plan, const void *in, void *out, int64_t N, void *stream);
+
+/* fcfs_run_rows -- scale only output rows [out_row0, out_row0 + out_nrows)
+ * of every plane, reading only input rows [in_row0, in_row0 + in_nrows).
+ * H in the plan is the GLOBAL height: padding is applied at global rows 0 and
+ * H-1 only (a row strip of a larger image, reading Z16).
+ *   in_rows : device N x C x in_nrows x W (rows in_row0.. of the image)
+ *   out_rows: device N x C x out_nrows x Wo (rows out_row0.. of the output)
+ * Errors: FCFS_E_ARG (window outside [0,H) / [0,Ho), NULL), FCFS_E_SHAPE (the
+ * input window lacks a row the outputs need: use fcfs_strip_rows),
+ * FCFS_E_DEVICE, FCFS_E_CUDA.  Not available with FCFS_FLAG_1D windows other
+ * than row ranges (1D rows map one to one). */
+fcfs_status fcfs_run_rows(fcfs_plan_t plan, const void *in_rows, int64_t in_row0, int64_t in_nrows,
+                          void *out_rows, int64_t out_row0, int64_t out_nrows, int64_t N, void *stream);
+
+/* fcfs_strip_rows -- row-strip ownership for multi-GPU sharding.  A rank that
+ * owns input rows [own_in_row0, own_in_row1) owns the output rows whose base
+ * row floor(m*q/p) lies in them (the last strip, own_in_row1 == H, also owns
+ * the paper-extent rows whose base is >= H):
+ *   *out_row0, *out_row1  : the owned output rows [out_row0, out_row1)
+ *   *need_row0, *need_row1: the input rows those outputs read, halo included,
+ *                           after global padding [need_row0, need_row1)
+ * An empty ownership gives out_row0 == out_row1.  Errors: FCFS_E_ARG. */
+fcfs_status fcfs_strip_rows(fcfs_plan_t plan, int64_t own_in_row0, int64_t own_in_row1, int64_t *out_row0,
+                            int64_t *out_row1, int64_t *need_row0, int64_t *need_row1);
+
+/* fcfs_run_host -- the end-to-end call with HOST buffers: copies host_in
+ * (N x C x H x W, ideally pinned) to dev_in, runs, copies dev_out to
+ * host_out (N x C x Ho x Wo), all asynchronously on stream.  dev_in/dev_out
+ * are caller-owned device scratch of at least the input/output sizes.
+ * Errors: as fcfs_run. */
+fcfs_status fcfs_run_host(fcfs_plan_t plan, const void *host_in, void *host_out, int64_t N, void *dev_in,
+                          void *dev_out, void *stream);
+
+/* Read-only plan description (introspection and bench accounting). */
+typedef struct {
+    int p, q;               /* reduced factor */
+    int mode, pad, dtype;
+    unsigned flags;
+    int64_t C, H, W, Ho, Wo;
+    int ntaps;              /* taps per dimension: 1, 2 or 4 */
+    int lo;                 /* first tap offset relative to floor(m*q/p): 0 or -1 */
+    int kernel;             /* variant fcfs_run uses: 0 reference, 1 nearest gather, 2 fused separable */
+    int device;             /* CUDA device recorded at plan time, -1 if none */
+    int64_t in_rows_referenced; /* input rows (of H) some kept output's tap reads */
+} fcfs_plan_info_t;
+
+fcfs_status fcfs_plan_info(fcfs_plan_t plan, fcfs_plan_info_t *info);
+
+/* The fp32 phase table the kernels use: for phase j in [0, p), weights
+ * w[4*j + t] (t < ntaps; unused entries 0) and base offsets base[j] =
+ * floor(j*q/p).  w must hold 4*p floats, base p ints.  Errors: FCFS_E_ARG. */
+fcfs_status fcfs_phase_table(fcfs_plan_t plan, float *w, int *base);
+
+/* Algorithmic (compulsory) HBM bytes of one fcfs_run over N images: every
+ * output byte written once plus every input row some kept output's tap reads
+ * (whole rows: a 32-byte sector holds 8-16 elements, so column skipping is
+ * not realisable). */
+fcfs_status fcfs_compulsory_bytes(fcfs_plan_t plan, int64_t N, int64_t *bytes);
+
+/* Release a plan (NULL is ignored). */
+void fcfs_destroy(fcfs_plan_t plan);
+
+/* Static string for a status code. */
+const char *fcfs_status_str(fcfs_status s);
+
+/* FCFS_VERSION of the library. */
+int fcfs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FCFS_H_ */

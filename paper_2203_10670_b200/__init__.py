@@ -1,0 +1,12 @@
+"""B200-native FCFS (arXiv 2203.10670): fractional p/q scaling as one fused
+pad -> strided polyphase conv -> pixelshuffle pass (libfcfs.so, sm_100a).
+
+Public API:
+    scale(x, p, q, mode, pad, extent, is1d)  -- resize a CUDA tensor
+    Plan(...)                                 -- an explicit plan (run / run_rows / run_host)
+    dist                                      -- multi-GPU drivers (batch shards, row strips + NCCL halo)
+"""
+from ._lib import FcfsError, LIB_PATH  # noqa: F401  (raises ImportError if libfcfs.so is missing)
+from .fcfs import Plan, get_plan, scale  # noqa: F401
+
+__all__ = ["Plan", "get_plan", "scale", "FcfsError", "LIB_PATH"]

@@ -1,0 +1,101 @@
+// Device helpers shared by the FCFS kernels: padding index map, dtype
+// conversion, fast division, mbarrier / bulk-copy PTX wrappers (sm_100a).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "fcfs_internal.h"
+
+namespace fcfs {
+
+// §3 Padding, reading Z5.  Maps virtual index t of an
+// n-long axis to a source index; -1 means "the zero constant".  Indices that
+// reflect cannot reach with one bounce are clamped: plan validation
+// guarantees no kept output reads them (they only feed masked lanes).
+__device__ __forceinline__ int64_t pad_src(int64_t t, int64_t n, int pad) {
+    if ((uint64_t)t < (uint64_t)n) return t;
+    if (pad == FCFS_PAD_ZERO) return -1;
+    if (pad == FCFS_PAD_REPLICATE) return t < 0 ? 0 : n - 1;
+    int64_t r = t < 0 ? -t : 2 * (n - 1) - t;
+    return r < 0 ? 0 : (r >= n ? n - 1 : r);
+}
+__device__ __forceinline__ int pad_src32(int t, int n, int pad) {
+    if ((unsigned)t < (unsigned)n) return t;
+    if (pad == FCFS_PAD_ZERO) return -1;
+    if (pad == FCFS_PAD_REPLICATE) return t < 0 ? 0 : n - 1;
+    int r = t < 0 ? -t : 2 * (n - 1) - t;
+    return r < 0 ? 0 : (r >= n ? n - 1 : r);
+}
+
+template <typename T> struct DT;
+template <> struct DT<float> {
+    static __device__ __forceinline__ float to_f(float v) { return v; }
+    static __device__ __forceinline__ float from_f(float v) { return v; }
+};
+template <> struct DT<__half> {
+    static __device__ __forceinline__ float to_f(__half v) { return __half2float(v); }
+    static __device__ __forceinline__ __half from_f(float v) { return __float2half_rn(v); }
+};
+template <> struct DT<__nv_bfloat16> {
+    static __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+    static __device__ __forceinline__ __nv_bfloat16 from_f(float v) { return __float2bfloat16_rn(v); }
+};
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f) {
+    uint32_t t = __umulhi(n, f.m);
+    return (t + n) >> f.s;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---- mbarrier (shared::cta) ------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// ---- bulk async copy global -> shared (TMA engine, 1D) -----------------------
+// dst/src 16-B aligned, bytes a multiple of 16; completes tx on `bar`.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+        "%4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// named barrier among `count` threads (id != 0)
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+}  // namespace fcfs

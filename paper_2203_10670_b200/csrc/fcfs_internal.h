@@ -1,0 +1,108 @@
+// Internal declarations shared by the plan builder (plan.cpp) and the
+// kernels (*.cu).  Not part of the ABI.
+#pragma once
+#include <cstdint>
+
+#include "fcfs.h"
+
+namespace fcfs {
+
+constexpr int kPMax = FCFS_MAX_FACTOR;
+
+// Run geometry common to every kernel.  Row indices are GLOBAL (0..H-1 input,
+// 0..Ho-1 output); the buffers hold the windows [in_row0, in_row0+in_nrows)
+// and [out_row0, out_row0+out_nrows) of each plane.
+struct RunGeom {
+    const void *in;
+    void *out;
+    int64_t planes;             // N * C
+    int64_t H, W, Ho, Wo;       // global sizes
+    int64_t in_row0, in_nrows;  // input row window held by `in`
+    int64_t out_row0, out_nrows;  // output rows produced into `out`
+    int64_t in_plane_stride;    // elements between planes of `in`  (= in_nrows * W)
+    int64_t out_plane_stride;   // elements between planes of `out` (= out_nrows * Wo)
+};
+
+// Per-dimension phase table (identical for both dimensions: one factor p/q).
+struct PhaseTable {
+    float w[kPMax][4];   // fp32 weights of phase j, tap t
+    int base[kPMax];     // floor(j*q/p)
+    int p, q;
+    int ntaps;           // 1, 2, 4
+    int lo;              // first tap offset relative to the base: 0 or -1
+};
+
+struct RefArgs {         // reference kernel: one thread per output
+    RunGeom g;
+    PhaseTable t;
+    int pad;
+    int is1d;
+};
+
+// 32-bit division by a run-time invariant divisor (n < 2^31).
+struct FastDiv {
+    uint32_t d, m, s;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f;
+    f.d = d;
+    uint32_t s = 0;
+    while (s < 32 && (1ull << s) < d) ++s;
+    f.s = s;
+    uint64_t one = 1;
+    f.m = (uint32_t)(((one << 32) * ((one << s) - d)) / d + 1);
+    return f;
+}
+
+struct NearestArgs {     // nearest gather: one thread per 32-byte output chunk
+    RunGeom g;
+    FastDiv div_wo, div_rows, div_p;
+    int p, q, pad, is1d;
+    int vec_ok;          // output base 16-B aligned
+};
+
+// Fused separable kernel (bilinear / bicubic), see fused.cuh for the layout.
+struct FusedArgs {
+    const void *in;
+    void *out;
+    int64_t in_plane_stride, out_plane_stride;
+    int32_t H, W, Ho, Wo;
+    int32_t in_row0, in_nrows, out_row0, out_nrows;
+    int32_t planes, pad;
+    int32_t NP;          // planes per CTA task (full-width mode)
+    int32_t CPT;         // column chunks per tile (a chunk = K x-periods = K*P outputs)
+    int32_t nch;         // chunks per output row
+    int32_t ntile;       // column tiles per row
+    int32_t ngroups;     // plane groups
+    int32_t PB;          // y-periods per band
+    int32_t nbands;
+    int32_t iy_first, iy_last;
+    int32_t ntasks;
+    int32_t S;           // pipeline stages
+    int32_t SR;          // rows per stage
+    int32_t seg_pitch;   // bytes per (plane, row) in a stage
+    int32_t stage_bytes;
+    int32_t out_pitch;   // bytes per plane (full width) or per (plane, row) segment (tiled)
+    int32_t obuf_bytes;
+    int32_t full_width;
+    float w[16][4];      // phase weights (fused variants have p <= 16)
+};
+
+// Launchers (host functions defined in the .cu files).  Return cudaError_t as int.
+int launch_reference(int dtype, const RefArgs &a, void *stream);
+int launch_nearest(int dtype, const NearestArgs &a, void *stream);
+
+// Fused: the variant table.  fused_lookup returns an opaque kernel handle or
+// nullptr when (dtype, p, q, ntaps) has no compiled instantiation; K (periods
+// per thread chunk) is reported.
+struct FusedVariant {
+    const void *fn;
+    int P, Q, TAPS, LO, K;
+};
+const FusedVariant *fused_lookup(int dtype, int p, int q, int ntaps);
+int launch_fused(const FusedVariant *v, const FusedArgs &a, int grid, int block, int smem, void *stream);
+
+constexpr int kFusedConsumerWarps = 8;
+constexpr int kFusedThreads = 32 * (1 + kFusedConsumerWarps);
+
+}  // namespace fcfs

@@ -1,0 +1,537 @@
+// FCFS plan builder and C-ABI entry points (include/fcfs.h).
+//
+// Host-only: validation, the per-dimension phase table (§3.1.1 + §5.2), the
+// output extent (§5.1), strip ownership, compulsory-byte accounting, kernel
+// selection and launch geometry.  No device memory is ever allocated here.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "fcfs.h"
+#include "fcfs_internal.h"
+
+using namespace fcfs;
+
+struct fcfs_plan_s {
+    int p, q, mode, pad, dtype;
+    unsigned flags;
+    int64_t C, H, W, Ho, Wo;
+    int is1d;
+    PhaseTable tab;
+    int kernel;  // 0 reference, 1 nearest, 2 fused
+    const FusedVariant *fused;
+    int device;
+    int64_t rows_ref;
+    int sm_count;
+};
+
+namespace {
+
+int64_t gcd64(int64_t a, int64_t b) {
+    while (b) {
+        int64_t t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+int esize(int dtype) { return dtype == FCFS_F32 ? 4 : 2; }
+
+// floor(a / b) for b > 0
+int64_t fdiv64(int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+// Output extent (reading Z3): paper p*ceil(N/q) or floor(N*p/q).
+int64_t extent(int64_t n, int p, int q, bool floor_ext) {
+    return floor_ext ? (n * p) / q : (int64_t)p * ((n + q - 1) / q);
+}
+
+// §5.2 phase weights at fraction f = k/p (reading Z1).  Bicubic: Keys'
+// convolution kernel with a = -1/2 (reading Z7) written as its four closed-form
+// tap polynomials over the common denominator 2p^3 (exact integers).
+void phase_table(PhaseTable &t, int p, int q, int mode) {
+    std::memset(&t, 0, sizeof(t));
+    t.p = p;
+    t.q = q;
+    t.ntaps = mode == FCFS_NEAREST ? 1 : (mode == FCFS_BILINEAR ? 2 : 4);
+    t.lo = mode == FCFS_BICUBIC ? -1 : 0;
+    for (int j = 0; j < p; ++j) {
+        const int64_t jq = (int64_t)j * q;
+        t.base[j] = (int)(jq / p);
+        const int64_t k = jq % p;
+        if (mode == FCFS_NEAREST) {
+            t.w[j][0] = 1.0f;
+        } else if (mode == FCFS_BILINEAR) {
+            t.w[j][0] = (float)((double)(p - k) / (double)p);
+            t.w[j][1] = (float)((double)k / (double)p);
+        } else {
+            const int64_t P = p, K = k, d = 2 * P * P * P;
+            const int64_t n[4] = {-K * K * K + 2 * K * K * P - K * P * P, 3 * K * K * K - 5 * K * K * P + 2 * P * P * P,
+                                  -3 * K * K * K + 4 * K * K * P + K * P * P, K * K * K - K * K * P};
+            for (int i = 0; i < 4; ++i) t.w[j][i] = (float)((double)n[i] / (double)d);
+        }
+    }
+}
+
+// Virtual index range one dimension's kept outputs [m0, m1) read (their own
+// taps, zero-weight taps of the tap list included).
+void tap_range(const fcfs_plan_s *pl, int64_t m0, int64_t m1, int64_t *vmin, int64_t *vmax) {
+    *vmin = fdiv64(m0 * pl->q, pl->p) + pl->tab.lo;
+    *vmax = fdiv64((m1 - 1) * pl->q, pl->p) + pl->tab.lo + pl->tab.ntaps - 1;
+}
+
+bool reflect_ok(int64_t vmin, int64_t vmax, int64_t n) {
+    if (vmin < 0 && -vmin > n - 1) return false;
+    if (vmax > n - 1 && 2 * (n - 1) - vmax < 0) return false;
+    return true;
+}
+
+int64_t pad_src_host(int64_t t, int64_t n, int pad) {
+    if (t >= 0 && t < n) return t;
+    if (pad == FCFS_PAD_ZERO) return -1;
+    if (pad == FCFS_PAD_REPLICATE) return t < 0 ? 0 : n - 1;
+    return t < 0 ? -t : 2 * (n - 1) - t;
+}
+
+// Input rows output rows [m0, m1) need, as a range [need0, need1) of real rows.
+void needed_rows(const fcfs_plan_s *pl, int64_t m0, int64_t m1, int64_t *need0, int64_t *need1) {
+    int64_t vmin, vmax;
+    if (pl->is1d) {
+        vmin = m0;
+        vmax = m1 - 1;
+    } else {
+        tap_range(pl, m0, m1, &vmin, &vmax);
+    }
+    int64_t n0 = std::max<int64_t>(vmin, 0), n1 = std::min<int64_t>(vmax + 1, pl->H);
+    if (pl->pad != FCFS_PAD_ZERO) {
+        if (vmin < 0) n1 = std::max(n1, pad_src_host(vmin, pl->H, pl->pad) + 1);
+        if (vmax >= pl->H) n0 = std::min(n0, pad_src_host(vmax, pl->H, pl->pad));
+    }
+    if (n1 <= n0) {  // all taps in zero padding
+        n0 = n1 = std::min<int64_t>(std::max<int64_t>(vmin, 0), pl->H);
+    }
+    *need0 = n0;
+    *need1 = n1;
+}
+
+// Rows of the image some kept output reads with a NONZERO weight.
+int64_t rows_referenced(const fcfs_plan_s *pl) {
+    if (pl->is1d) return pl->H;
+    std::vector<char> used(pl->H, 0);
+    for (int64_t my = 0; my < pl->Ho; ++my) {
+        int j = (int)(my % pl->p);
+        int64_t by = (my / pl->p) * pl->q + pl->tab.base[j];
+        for (int t = 0; t < pl->tab.ntaps; ++t) {
+            bool nz = pl->tab.ntaps == 1 || (j == 0 ? (t == -pl->tab.lo) : pl->tab.w[j][t] != 0.0f);
+            if (!nz) continue;
+            int64_t s = pad_src_host(by + pl->tab.lo + t, pl->H, pl->pad);
+            if (s >= 0 && s < pl->H) used[s] = 1;
+        }
+    }
+    int64_t n = 0;
+    for (char u : used) n += u;
+    return n;
+}
+
+bool ranges_overlap(const void *a, int64_t na, const void *b, int64_t nb) {
+    auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+    return x < y + (uint64_t)nb && y < x + (uint64_t)na;
+}
+
+// ---------------------------------------------------------------- fused launch geometry
+struct FusedLaunch {
+    FusedArgs a;
+    int grid, smem;
+};
+
+bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
+    const FusedVariant *v = pl->fused;
+    const int P = v->P, Q = v->Q, K = v->K, TAPS = v->TAPS, LO = v->LO;
+    const int ESZ = esize(pl->dtype), A = 16 / ESZ;
+    const int HI = ((P - 1) * Q) / P + LO + TAPS - 1;
+    const int Lw = HI - LO + 1;
+    const int Cc = Lw > Q ? Lw - Q : 0;
+    const int Ff = Lw - Cc;
+    const int NT = 32 * kFusedConsumerWarps;
+    const int KP = K * P;
+    FusedArgs &a = L.a;
+    std::memset(&a, 0, sizeof(a));
+    a.in = g.in;
+    a.out = g.out;
+    a.in_plane_stride = g.in_plane_stride;
+    a.out_plane_stride = g.out_plane_stride;
+    a.H = (int32_t)g.H;
+    a.W = (int32_t)g.W;
+    a.Ho = (int32_t)g.Ho;
+    a.Wo = (int32_t)g.Wo;
+    a.in_row0 = (int32_t)g.in_row0;
+    a.in_nrows = (int32_t)g.in_nrows;
+    a.out_row0 = (int32_t)g.out_row0;
+    a.out_nrows = (int32_t)g.out_nrows;
+    a.planes = (int32_t)g.planes;
+    a.pad = pl->pad;
+    for (int j = 0; j < P; ++j)
+        for (int t = 0; t < 4; ++t) a.w[j][t] = pl->tab.w[j][t];
+    a.nch = (int32_t)((g.Wo + KP - 1) / KP);
+    a.SR = std::max(Ff, Cc);
+    const int budget = 110 * 1024;  // two CTAs per SM
+    auto seg_pitch_for = [&](int cpt) {
+        int64_t elems = std::min<int64_t>(g.W, (int64_t)cpt * K * Q - Q + Lw + 2 * A);
+        elems = (elems + A - 1) / A * A;
+        return (int)(elems * ESZ);
+    };
+    int S = 0;
+    for (int tries = 0; tries < 64; ++tries) {
+        if (a.nch <= NT && tries == 0) {
+            a.full_width = 1;
+            a.CPT = a.nch;
+            a.ntile = 1;
+            a.NP = (int)std::min<int64_t>(NT / a.CPT, g.planes);
+        } else if (a.full_width && a.NP > 1) {
+            a.NP = std::max(1, a.NP / 2);
+        } else {
+            if (a.full_width || a.CPT == 0) {
+                a.full_width = 0;
+                a.ntile = std::max(1, (a.nch + NT - 1) / NT);
+            } else {
+                a.ntile += 1;
+            }
+            a.CPT = (a.nch + a.ntile - 1) / a.ntile;
+            a.ntile = (a.nch + a.CPT - 1) / a.CPT;
+            a.NP = 1;
+        }
+        a.seg_pitch = seg_pitch_for(a.CPT);
+        a.stage_bytes = a.NP * a.SR * a.seg_pitch;
+        if (a.full_width) {
+            a.out_pitch = (int)(((int64_t)P * g.Wo * ESZ + 16 + 15) / 16 * 16);
+            a.obuf_bytes = a.NP * a.out_pitch;
+        } else {
+            a.out_pitch = ((a.CPT * KP * ESZ + 16) + 15) / 16 * 16;
+            a.obuf_bytes = a.NP * P * a.out_pitch;
+        }
+        const int fixed = 128 + 128 + 2 * a.obuf_bytes;
+        S = std::min(8, (budget - fixed) / std::max(1, a.stage_bytes));
+        if (S >= 3 || (S >= 2 && a.CPT <= 16)) break;
+    }
+    if (S < 2) return false;
+    a.S = S;
+    a.ngroups = (int32_t)((g.planes + a.NP - 1) / a.NP);
+    a.iy_first = (int32_t)(g.out_row0 / P);
+    a.iy_last = (int32_t)((g.out_row0 + g.out_nrows - 1) / P);
+    const int nper = a.iy_last - a.iy_first + 1;
+    const int resident = pl->sm_count * 2;
+    const int64_t base_tasks = (int64_t)a.ngroups * a.ntile;
+    int nbands = 1;
+    if (base_tasks < 4 * resident) {
+        const int want = (int)((4 * resident + base_tasks - 1) / base_tasks);
+        const int min_pb = std::max(2, (4 * Cc + Q - 1) / std::max(1, Q));  // warm-up <= ~25%
+        nbands = std::max(1, std::min(want, nper / min_pb));
+    }
+    a.PB = (nper + nbands - 1) / nbands;
+    a.nbands = (nper + a.PB - 1) / a.PB;
+    const int64_t ntasks = base_tasks * a.nbands;
+    if (ntasks > INT32_MAX) return false;
+    a.ntasks = (int32_t)ntasks;
+    L.grid = (int)std::min<int64_t>(ntasks, resident);
+    L.smem = 128 + a.S * a.stage_bytes + 128 + 2 * a.obuf_bytes;
+    return true;
+}
+
+fcfs_status check_device(const fcfs_plan_s *pl) {
+    int dev = -1;
+    if (pl->device < 0 || cudaGetDevice(&dev) != cudaSuccess || dev != pl->device) {
+        cudaGetLastError();
+        return FCFS_E_DEVICE;
+    }
+    return FCFS_OK;
+}
+
+fcfs_status run_window(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t in_nrows, void *out,
+                       int64_t out_row0, int64_t out_nrows, int64_t N, void *stream) {
+    if (!pl || N < 0) return FCFS_E_ARG;
+    if (in_row0 < 0 || in_nrows < 1 || in_row0 + in_nrows > pl->H) return FCFS_E_ARG;
+    if (out_row0 < 0 || out_nrows < 0 || out_row0 + out_nrows > pl->Ho) return FCFS_E_ARG;
+    if (N == 0 || out_nrows == 0) return FCFS_OK;
+    if (!in || !out) return FCFS_E_ARG;
+    const int ESZ = esize(pl->dtype);
+    const int64_t planes = N * pl->C;
+    const int64_t in_bytes = planes * in_nrows * pl->W * ESZ, out_bytes = planes * out_nrows * pl->Wo * ESZ;
+    if (ranges_overlap(in, in_bytes, out, out_bytes)) return FCFS_E_ARG;
+    int64_t n0, n1;
+    needed_rows(pl, out_row0, out_row0 + out_nrows, &n0, &n1);
+    if (n0 < in_row0 || n1 > in_row0 + in_nrows) return FCFS_E_SHAPE;
+    fcfs_status st = check_device(pl);
+    if (st != FCFS_OK) return st;
+
+    RunGeom g;
+    g.in = in;
+    g.out = out;
+    g.planes = planes;
+    g.H = pl->H;
+    g.W = pl->W;
+    g.Ho = pl->Ho;
+    g.Wo = pl->Wo;
+    g.in_row0 = in_row0;
+    g.in_nrows = in_nrows;
+    g.out_row0 = out_row0;
+    g.out_nrows = out_nrows;
+    g.in_plane_stride = in_nrows * pl->W;
+    g.out_plane_stride = out_nrows * pl->Wo;
+
+    int kernel = pl->kernel;
+    const int64_t total = planes * out_nrows * pl->Wo;
+    if (kernel == 1) {  // 32-bit index ranges of the gather kernel
+        if (total > INT32_MAX - 64 || pl->Wo * pl->q > INT32_MAX || pl->Ho * pl->q > INT32_MAX) kernel = 0;
+    }
+    if (kernel == 2) {
+        if ((reinterpret_cast<uintptr_t>(in) & 15) || planes * std::max(in_nrows * pl->W, out_nrows * pl->Wo) > INT32_MAX * 16LL)
+            kernel = 0;
+    }
+    int rc = 0;
+    if (kernel == 1) {
+        NearestArgs a;
+        a.g = g;
+        a.div_wo = make_fastdiv((uint32_t)pl->Wo);
+        a.div_rows = make_fastdiv((uint32_t)out_nrows);
+        a.div_p = make_fastdiv((uint32_t)pl->p);
+        a.p = pl->p;
+        a.q = pl->q;
+        a.pad = pl->pad;
+        a.is1d = pl->is1d;
+        a.vec_ok = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+        rc = launch_nearest(pl->dtype, a, stream);
+    } else if (kernel == 2) {
+        FusedLaunch L;
+        if (plan_fused(pl, g, L)) {
+            rc = launch_fused(pl->fused, L.a, L.grid, kFusedThreads, L.smem, stream);
+        } else {
+            kernel = 0;
+        }
+    }
+    if (kernel == 0) {
+        RefArgs a;
+        a.g = g;
+        a.t = pl->tab;
+        a.pad = pl->pad;
+        a.is1d = pl->is1d;
+        rc = launch_reference(pl->dtype, a, stream);
+    }
+    return rc == 0 ? FCFS_OK : FCFS_E_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fcfs_version(void) { return FCFS_VERSION; }
+
+const char *fcfs_status_str(fcfs_status s) {
+    switch (s) {
+    case FCFS_OK: return "ok";
+    case FCFS_E_ARG: return "invalid argument";
+    case FCFS_E_SHAPE: return "invalid shape or row window";
+    case FCFS_E_PAD: return "reflect padding cannot reach a needed tap";
+    case FCFS_E_UNSUPPORTED: return "unsupported configuration";
+    case FCFS_E_DEVICE: return "no CUDA device or wrong device";
+    case FCFS_E_CUDA: return "CUDA error";
+    case FCFS_E_NOMEM: return "out of host memory";
+    }
+    return "unknown status";
+}
+
+fcfs_status fcfs_plan_ex(int p, int q, int mode, int pad, int64_t C, int64_t H, int64_t W, int dtype,
+                         unsigned flags, fcfs_plan_t *out) {
+    if (!out) return FCFS_E_ARG;
+    if (p < 1 || q < 1) return FCFS_E_ARG;
+    {
+        const int64_t g0 = gcd64(p, q);
+        if (p / g0 > FCFS_MAX_FACTOR || q / g0 > FCFS_MAX_FACTOR) return FCFS_E_ARG;
+    }
+    if (mode < FCFS_NEAREST || mode > FCFS_BICUBIC || pad < FCFS_PAD_ZERO || pad > FCFS_PAD_REFLECT) return FCFS_E_ARG;
+    if (dtype < FCFS_F32 || dtype > FCFS_BF16) return FCFS_E_ARG;
+    if (C < 1 || H < 1 || W < 1 || H > INT32_MAX || W > INT32_MAX) return FCFS_E_ARG;
+    const unsigned known = FCFS_FLAG_1D | FCFS_FLAG_EXTENT_FLOOR | FCFS_FLAG_FORCE_REFERENCE;
+    if (flags & ~known) return FCFS_E_ARG;
+    fcfs_plan_s *pl = new (std::nothrow) fcfs_plan_s;
+    if (!pl) return FCFS_E_NOMEM;
+    std::memset(pl, 0, sizeof(*pl));
+    const int64_t g = gcd64(p, q);
+    pl->p = (int)(p / g);
+    pl->q = (int)(q / g);
+    pl->mode = mode;
+    pl->pad = pad;
+    pl->dtype = dtype;
+    pl->flags = flags;
+    pl->C = C;
+    pl->H = H;
+    pl->W = W;
+    pl->is1d = (flags & FCFS_FLAG_1D) ? 1 : 0;
+    const bool fl = (flags & FCFS_FLAG_EXTENT_FLOOR) != 0;
+    pl->Wo = extent(W, pl->p, pl->q, fl);
+    pl->Ho = pl->is1d ? H : extent(H, pl->p, pl->q, fl);
+    if (pl->Ho < 1 || pl->Wo < 1 || pl->Ho > INT32_MAX || pl->Wo > INT32_MAX) {
+        delete pl;
+        return FCFS_E_SHAPE;
+    }
+    phase_table(pl->tab, pl->p, pl->q, mode);
+    if (pad == FCFS_PAD_REFLECT) {
+        int64_t vmin, vmax;
+        tap_range(pl, 0, pl->Wo, &vmin, &vmax);
+        bool ok = reflect_ok(vmin, vmax, W);
+        if (!pl->is1d) {
+            tap_range(pl, 0, pl->Ho, &vmin, &vmax);
+            ok = ok && reflect_ok(vmin, vmax, H);
+        }
+        if (!ok) {
+            delete pl;
+            return FCFS_E_PAD;
+        }
+    }
+    pl->kernel = 0;
+    pl->fused = nullptr;
+    if (!(flags & FCFS_FLAG_FORCE_REFERENCE)) {
+        if (mode == FCFS_NEAREST) {
+            pl->kernel = 1;
+        } else if (!pl->is1d && (W * esize(dtype)) % 16 == 0) {
+            pl->fused = fused_lookup(dtype, pl->p, pl->q, pl->tab.ntaps);
+            if (pl->fused) pl->kernel = 2;
+        }
+    }
+    pl->rows_ref = rows_referenced(pl);
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        dev = -1;
+    }
+    int ndev = 0;
+    if (dev >= 0 && (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)) {
+        cudaGetLastError();
+        dev = -1;
+    }
+    pl->device = dev;
+    pl->sm_count = 148;
+    if (dev >= 0) {
+        int sms = 0;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
+            pl->sm_count = sms;
+        cudaGetLastError();
+    }
+    *out = pl;
+    return FCFS_OK;
+}
+
+fcfs_status fcfs_plan(int p, int q, int mode, int pad, int64_t C, int64_t H, int64_t W, int dtype, fcfs_plan_t *out) {
+    return fcfs_plan_ex(p, q, mode, pad, C, H, W, dtype, 0u, out);
+}
+
+fcfs_status fcfs_output_shape(fcfs_plan_t pl, int64_t *Ho, int64_t *Wo) {
+    if (!pl || !Ho || !Wo) return FCFS_E_ARG;
+    *Ho = pl->Ho;
+    *Wo = pl->Wo;
+    return FCFS_OK;
+}
+
+fcfs_status fcfs_run(fcfs_plan_t pl, const void *in, void *out, int64_t N, void *stream) {
+    if (!pl) return FCFS_E_ARG;
+    return run_window(pl, in, 0, pl->H, out, 0, pl->Ho, N, stream);
+}
+
+fcfs_status fcfs_run_rows(fcfs_plan_t pl, const void *in_rows, int64_t in_row0, int64_t in_nrows, void *out_rows,
+                          int64_t out_row0, int64_t out_nrows, int64_t N, void *stream) {
+    return run_window(pl, in_rows, in_row0, in_nrows, out_rows, out_row0, out_nrows, N, stream);
+}
+
+fcfs_status fcfs_strip_rows(fcfs_plan_t pl, int64_t own0, int64_t own1, int64_t *out0, int64_t *out1, int64_t *need0,
+                            int64_t *need1) {
+    if (!pl || !out0 || !out1 || !need0 || !need1) return FCFS_E_ARG;
+    if (own0 < 0 || own1 > pl->H || own0 > own1) return FCFS_E_ARG;
+    int64_t m0, m1;
+    if (pl->is1d) {
+        m0 = own0;
+        m1 = own1;
+    } else {
+        // smallest m with floor(m*q/p) >= own  <=>  m >= own*p/q
+        m0 = own0 == 0 ? 0 : (own0 * pl->p + pl->q - 1) / pl->q;
+        m1 = own1 == pl->H ? pl->Ho : (own1 * pl->p + pl->q - 1) / pl->q;
+        m0 = std::min(m0, pl->Ho);
+        m1 = std::max(m0, std::min(m1, pl->Ho));
+    }
+    *out0 = m0;
+    *out1 = m1;
+    if (m1 == m0) {
+        *need0 = *need1 = own0;
+        return FCFS_OK;
+    }
+    needed_rows(pl, m0, m1, need0, need1);
+    return FCFS_OK;
+}
+
+fcfs_status fcfs_run_host(fcfs_plan_t pl, const void *host_in, void *host_out, int64_t N, void *dev_in, void *dev_out,
+                          void *stream) {
+    if (!pl || N < 0) return FCFS_E_ARG;
+    if (N == 0) return FCFS_OK;
+    if (!host_in || !host_out || !dev_in || !dev_out) return FCFS_E_ARG;
+    fcfs_status st = check_device(pl);
+    if (st != FCFS_OK) return st;
+    const int ESZ = esize(pl->dtype);
+    const size_t in_bytes = (size_t)(N * pl->C * pl->H * pl->W * ESZ);
+    const size_t out_bytes = (size_t)(N * pl->C * pl->Ho * pl->Wo * ESZ);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (cudaMemcpyAsync(dev_in, host_in, in_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+        cudaGetLastError();
+        return FCFS_E_CUDA;
+    }
+    st = fcfs_run(pl, dev_in, dev_out, N, stream);
+    if (st != FCFS_OK) return st;
+    if (cudaMemcpyAsync(host_out, dev_out, out_bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) {
+        cudaGetLastError();
+        return FCFS_E_CUDA;
+    }
+    return FCFS_OK;
+}
+
+fcfs_status fcfs_plan_info(fcfs_plan_t pl, fcfs_plan_info_t *info) {
+    if (!pl || !info) return FCFS_E_ARG;
+    info->p = pl->p;
+    info->q = pl->q;
+    info->mode = pl->mode;
+    info->pad = pl->pad;
+    info->dtype = pl->dtype;
+    info->flags = pl->flags;
+    info->C = pl->C;
+    info->H = pl->H;
+    info->W = pl->W;
+    info->Ho = pl->Ho;
+    info->Wo = pl->Wo;
+    info->ntaps = pl->tab.ntaps;
+    info->lo = pl->tab.lo;
+    info->kernel = pl->kernel;
+    info->device = pl->device;
+    info->in_rows_referenced = pl->rows_ref;
+    return FCFS_OK;
+}
+
+fcfs_status fcfs_phase_table(fcfs_plan_t pl, float *w, int *base) {
+    if (!pl || !w || !base) return FCFS_E_ARG;
+    for (int j = 0; j < pl->p; ++j) {
+        base[j] = pl->tab.base[j];
+        for (int t = 0; t < 4; ++t) w[4 * j + t] = pl->tab.w[j][t];
+    }
+    return FCFS_OK;
+}
+
+fcfs_status fcfs_compulsory_bytes(fcfs_plan_t pl, int64_t N, int64_t *bytes) {
+    if (!pl || !bytes || N < 0) return FCFS_E_ARG;
+    const int ESZ = esize(pl->dtype);
+    *bytes = N * pl->C * (pl->rows_ref * pl->W + pl->Ho * pl->Wo) * ESZ;
+    return FCFS_OK;
+}
+
+void fcfs_destroy(fcfs_plan_t pl) { delete pl; }
+
+}  // extern "C"

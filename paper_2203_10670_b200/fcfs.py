@@ -1,0 +1,167 @@
+"""Python face of the FCFS hot path: plans and scale() over torch CUDA tensors.
+
+torch is used only for device memory and streams; every step of the path
+(pad, strided polyphase conv, pixelshuffle) runs in libfcfs.so.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+
+from . import _lib
+from ._lib import FLAG_1D, FLAG_EXTENT_FLOOR, FLAG_FORCE_REFERENCE, check
+
+_TORCH_DTYPES = None
+
+
+def _dtype_name(dt) -> str:
+    import torch
+    names = {torch.float32: "float32", torch.float16: "float16", torch.bfloat16: "bfloat16"}
+    if dt not in names:
+        raise TypeError(f"FCFS supports float32, float16 and bfloat16 tensors, got {dt}")
+    return names[dt]
+
+
+class Plan:
+    """An immutable FCFS plan (fcfs_plan_ex).
+
+    p/q: scale factor (paper r/s); mode: nearest|bilinear|bicubic;
+    pad: zero|replicate|reflect; C, H, W: one image; dtype: float32|float16|
+    bfloat16; extent: "paper" (p*ceil(N/q)) or "floor" (floor(N*p/q));
+    is1d: scale W only.
+    """
+
+    def __init__(self, p: int, q: int, mode: str = "bilinear", pad: str = "replicate", C: int = 1, H: int = 1,
+                 W: int = 1, dtype: str = "float32", extent: str = "paper", is1d: bool = False,
+                 force_reference: bool = False):
+        flags = (FLAG_EXTENT_FLOOR if extent == "floor" else 0) | (FLAG_1D if is1d else 0) | \
+            (FLAG_FORCE_REFERENCE if force_reference else 0)
+        if extent not in ("paper", "floor"):
+            raise ValueError(extent)
+        h = ctypes.c_void_p()
+        check(_lib.lib.fcfs_plan_ex(p, q, _lib.MODES[mode], _lib.PADS[pad], C, H, W, _lib.DTYPES[dtype], flags,
+                                    ctypes.byref(h)), "fcfs_plan_ex")
+        self._h = h
+        self.mode, self.pad, self.dtype, self.extent, self.is1d = mode, pad, dtype, extent, is1d
+        info = _lib.PlanInfo()
+        check(_lib.lib.fcfs_plan_info(h, ctypes.byref(info)), "fcfs_plan_info")
+        self.info = info
+        self.p, self.q = info.p, info.q
+        self.C, self.H, self.W, self.Ho, self.Wo = info.C, info.H, info.W, info.Ho, info.Wo
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.lib.fcfs_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def kernel(self) -> str:
+        return _lib.KERNELS[self.info.kernel]
+
+    def output_shape(self):
+        return self.Ho, self.Wo
+
+    def phase_table(self):
+        w = (ctypes.c_float * (4 * self.p))()
+        b = (ctypes.c_int * self.p)()
+        check(_lib.lib.fcfs_phase_table(self._h, w, b), "fcfs_phase_table")
+        return [list(w[4 * j: 4 * j + 4]) for j in range(self.p)], list(b)
+
+    def compulsory_bytes(self, N: int) -> int:
+        out = ctypes.c_int64()
+        check(_lib.lib.fcfs_compulsory_bytes(self._h, N, ctypes.byref(out)), "fcfs_compulsory_bytes")
+        return out.value
+
+    def strip_rows(self, own0: int, own1: int):
+        """(out_row0, out_row1, need_row0, need_row1) for a strip owning input rows [own0, own1)."""
+        v = [ctypes.c_int64() for _ in range(4)]
+        check(_lib.lib.fcfs_strip_rows(self._h, own0, own1, *[ctypes.byref(x) for x in v]), "fcfs_strip_rows")
+        return tuple(x.value for x in v)
+
+    # ---------------------------------------------------------------- runs
+    def _stream(self, stream):
+        import torch
+        s = torch.cuda.current_stream() if stream is None else stream
+        return ctypes.c_void_p(s.cuda_stream)
+
+    def _check_tensor(self, t, shape, what):
+        import torch
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise TypeError(f"{what} must be a CUDA tensor")
+        if _dtype_name(t.dtype) != self.dtype:
+            raise TypeError(f"{what} dtype {t.dtype} does not match the plan's {self.dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{what} must be contiguous")
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{what} shape {tuple(t.shape)} != {tuple(shape)}")
+
+    def run(self, x, out=None, stream=None):
+        """out[N, C, Ho, Wo] = FCFS(x[N, C, H, W]) on the current (or given) stream."""
+        import torch
+        N = x.shape[0]
+        self._check_tensor(x, (N, self.C, self.H, self.W), "input")
+        if out is None:
+            out = torch.empty((N, self.C, self.Ho, self.Wo), dtype=x.dtype, device=x.device)
+        self._check_tensor(out, (N, self.C, self.Ho, self.Wo), "output")
+        check(_lib.lib.fcfs_run(self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), N,
+                                self._stream(stream)), "fcfs_run")
+        return out
+
+    def run_rows(self, x_rows, in_row0: int, out_row0: int, out_nrows: int, out=None, stream=None):
+        """Output rows [out_row0, out_row0+out_nrows) from input rows [in_row0, in_row0+x_rows.shape[2])."""
+        import torch
+        N, in_nrows = x_rows.shape[0], x_rows.shape[2]
+        self._check_tensor(x_rows, (N, self.C, in_nrows, self.W), "input rows")
+        if out is None:
+            out = torch.empty((N, self.C, out_nrows, self.Wo), dtype=x_rows.dtype, device=x_rows.device)
+        self._check_tensor(out, (N, self.C, out_nrows, self.Wo), "output rows")
+        check(_lib.lib.fcfs_run_rows(self._h, ctypes.c_void_p(x_rows.data_ptr()), in_row0, in_nrows,
+                                     ctypes.c_void_p(out.data_ptr()), out_row0, out_nrows, N,
+                                     self._stream(stream)), "fcfs_run_rows")
+        return out
+
+    def run_host(self, x_host, out_host, dev_in, dev_out, stream=None):
+        """End-to-end call with host buffers (H2D copy, run, D2H copy on the stream)."""
+        N = x_host.shape[0]
+        check(_lib.lib.fcfs_run_host(self._h, ctypes.c_void_p(x_host.data_ptr()), ctypes.c_void_p(out_host.data_ptr()),
+                                     N, ctypes.c_void_p(dev_in.data_ptr()), ctypes.c_void_p(dev_out.data_ptr()),
+                                     self._stream(stream)), "fcfs_run_host")
+        return out_host
+
+
+_cache: dict = {}
+_cache_lock = threading.Lock()
+
+
+def get_plan(p, q, mode, pad, C, H, W, dtype, extent="paper", is1d=False, device=None) -> Plan:
+    key = (p, q, mode, pad, C, H, W, dtype, extent, is1d, device)
+    with _cache_lock:
+        pl = _cache.get(key)
+        if pl is None:
+            pl = Plan(p, q, mode, pad, C, H, W, dtype, extent, is1d)
+            _cache[key] = pl
+    return pl
+
+
+def scale(x, p: int, q: int, mode: str = "bilinear", pad: str = "replicate", extent: str = "paper",
+          is1d: bool = False, out=None, stream=None):
+    """FCFS-resize a CUDA tensor x of shape (N, C, H, W) (or (C, H, W), (H, W))
+    by p/q.  Returns a new tensor (N, C, Ho, Wo) of x's dtype."""
+    import torch
+    squeeze = 0
+    while x.dim() < 4:
+        x = x.unsqueeze(0)
+        squeeze += 1
+    x = x.contiguous()
+    with torch.cuda.device(x.device):
+        pl = get_plan(p, q, mode, pad, x.shape[1], x.shape[2], x.shape[3], _dtype_name(x.dtype), extent, is1d,
+                      x.device.index)
+        y = pl.run(x, out=out, stream=stream)
+    for _ in range(squeeze):
+        y = y.squeeze(0)
+    return y

@@ -1,0 +1,189 @@
+"""Host-side checks of libfcfs.so (no GPU needed): it loads, exports every
+symbol include/fcfs.h declares, and its host logic (validation, extents, phase
+table, strip ownership, byte accounting, status codes) is right."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "fcfs.h")
+
+
+@pytest.fixture(scope="module")
+def fc():
+    import paper_2203_10670_b200 as fc
+    return fc
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(fcfs_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(fc):
+    names = declared_functions()
+    assert "fcfs_plan" in names and "fcfs_run" in names and "fcfs_destroy" in names and len(names) >= 13
+    lib = ctypes.CDLL(fc.LIB_PATH)
+    for n in names:
+        assert hasattr(lib, n), n
+    nm = subprocess.run(["nm", "-D", "--defined-only", fc.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (fcfs_\w+)", nm))
+    assert set(names) <= exported
+    # the binding declares exactly the header's functions
+    from paper_2203_10670_b200 import _lib
+    assert set(_lib.SIGNATURES) == set(names)
+
+
+def test_library_is_sm100a(fc):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", fc.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_oracle_or_torch_in_product_path():
+    pkg = os.path.join(ROOT, "paper_2203_10670_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f
+                assert "fcfs_oracle" not in src, f
+    # the oracle includes nothing from the product
+    osrc = open(os.path.join(ROOT, "oracle", "fcfs_oracle.c")).read()
+    assert "fcfs.h" not in osrc and "fcfs_internal" not in osrc
+
+
+@pytest.mark.parametrize("p,q,H,W,floor,out", [(3, 2, 5, 5, False, (9, 9)), (3, 2, 48, 64, True, (72, 96)),
+                                                (5, 3, 128, 128, True, (213, 213)), (5, 3, 128, 128, False, (215, 215)),
+                                                (2, 11, 1024, 1024, False, (188, 188)), (6, 4, 5, 5, False, (9, 9)),
+                                                (7, 5, 2160, 3840, True, (3024, 5376)),
+                                                (4, 7, 2160, 3840, True, (1234, 2194)),
+                                                (3, 5, 32768, 32768, True, (19660, 19660))])
+def test_output_shapes(fc, p, q, H, W, floor, out):
+    pl = fc.Plan(p, q, "bilinear", "replicate", 1, H, W, "float32", "floor" if floor else "paper")
+    assert pl.output_shape() == out
+    assert pl.output_shape() == oracle.output_shape(H, W, p, q, floor)
+
+
+def test_errors(fc):
+    from paper_2203_10670_b200._lib import FcfsError
+    cases = [((0, 1, "bilinear", "zero", 1, 4, 4), "FCFS_E_ARG"), ((65, 1, "bilinear", "zero", 1, 4, 4), "FCFS_E_ARG"),
+             ((1, 1, "bilinear", "zero", 0, 4, 4), "FCFS_E_ARG"), ((1, 1, "bilinear", "zero", 1, 0, 4), "FCFS_E_ARG"),
+             ((5, 3, "bicubic", "reflect", 1, 1, 8), "FCFS_E_PAD"), ((3, 2, "bilinear", "reflect", 1, 8, 1), "FCFS_E_PAD")]
+    for args, name in cases:
+        with pytest.raises(FcfsError) as e:
+            fc.Plan(*args)
+        assert e.value.name == name, args
+    with pytest.raises(FcfsError) as e:
+        fc.Plan(2, 11, "bilinear", "replicate", 1, 5, 5, "float32", "floor")
+    assert e.value.name == "FCFS_E_SHAPE"
+    # reducible factors beyond 64 are fine once reduced
+    assert fc.Plan(128, 64, "nearest", "zero", 1, 4, 4).p == 2
+    with pytest.raises(FcfsError):
+        fc.Plan(65, 64, "nearest", "zero", 1, 4, 4)
+
+
+def test_unknown_enum_and_flags():
+    from paper_2203_10670_b200 import _lib
+    h = ctypes.c_void_p()
+    assert _lib.lib.fcfs_plan_ex(3, 2, 7, 0, 1, 4, 4, 0, 0, ctypes.byref(h)) == 1
+    assert _lib.lib.fcfs_plan_ex(3, 2, 0, 9, 1, 4, 4, 0, 0, ctypes.byref(h)) == 1
+    assert _lib.lib.fcfs_plan_ex(3, 2, 0, 0, 1, 4, 4, 5, 0, ctypes.byref(h)) == 1
+    assert _lib.lib.fcfs_plan_ex(3, 2, 0, 0, 1, 4, 4, 0, 1 << 20, ctypes.byref(h)) == 1
+    assert _lib.lib.fcfs_plan_ex(3, 2, 0, 0, 1, 4, 4, 0, 0, None) == 1
+    assert _lib.lib.fcfs_status_str(6).decode() == "CUDA error"
+    assert _lib.lib.fcfs_version() == 1
+
+
+def test_run_without_device_is_refused(fc):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("host without GPU only")
+    from paper_2203_10670_b200 import _lib
+    pl = fc.Plan(3, 2, "bilinear", "replicate", 1, 8, 8)
+    assert pl.info.device == -1
+    st = _lib.lib.fcfs_run(pl.handle, ctypes.c_void_p(0x1000), ctypes.c_void_p(0x100000), 1, None)
+    assert _lib.STATUS[st] == "FCFS_E_DEVICE"
+
+
+@pytest.mark.parametrize("mode", ["nearest", "bilinear", "bicubic"])
+@pytest.mark.parametrize("p,q", [(3, 2), (5, 3), (7, 5), (4, 7), (3, 5), (27, 11), (1, 1)])
+def test_phase_table_matches_oracle_weights(fc, mode, p, q):
+    pl = fc.Plan(p, q, mode, "replicate", 1, 64, 64)
+    w, base = pl.phase_table()
+    for j in range(p):
+        first, ow = oracle.phase_taps(mode, p, q, j)
+        assert base[j] == (j * q) // p
+        assert first - base[j] == pl.info.lo
+        # fp32 rounding of the exact weight (the oracle keeps double)
+        np.testing.assert_array_equal(np.float32(ow), np.float32(w[j][: len(ow)]))
+        assert all(v == 0 for v in w[j][len(ow):])
+
+
+def test_kernel_selection(fc):
+    assert fc.Plan(5, 3, "bicubic", "reflect", 1, 128, 128, "bfloat16").kernel == "fused_separable"
+    assert fc.Plan(2, 3, "nearest", "zero", 1, 512, 512).kernel == "nearest_gather"
+    assert fc.Plan(27, 11, "bicubic", "replicate", 1, 64, 64).kernel == "reference"  # no fused variant
+    assert fc.Plan(3, 2, "bilinear", "replicate", 1, 64, 101).kernel == "reference"  # row pitch not 16-B
+    assert fc.Plan(3, 2, "bilinear", "replicate", 1, 64, 64, is1d=True).kernel == "reference"
+    assert fc.Plan(3, 2, "bilinear", "replicate", 1, 64, 64, force_reference=True).kernel == "reference"
+
+
+def _own(p, q, H, Ho, own0, own1):
+    """Brute force: outputs whose base row floor(m*q/p) lies in [own0, own1)."""
+    ms = [m for m in range(Ho) if own0 <= (m * q) // p < own1 or (own1 == H and (m * q) // p >= H)]
+    return (ms[0], ms[-1] + 1) if ms else None
+
+
+@pytest.mark.parametrize("p,q,mode,pad,ext", [(3, 5, "bicubic", "replicate", "floor"), (5, 3, "bicubic", "reflect", "paper"),
+                                              (7, 5, "bilinear", "zero", "floor"), (2, 3, "nearest", "zero", "paper"),
+                                              (4, 7, "bilinear", "replicate", "paper")])
+def test_strip_rows_partition_and_halo(fc, p, q, mode, pad, ext):
+    H, W = 203, 16
+    pl = fc.Plan(p, q, mode, pad, 1, H, W, "float32", ext)
+    Ho = pl.Ho
+    for G in (1, 2, 3, 7, 8):
+        prev = 0
+        for g in range(G):
+            own0, own1 = g * H // G, (g + 1) * H // G
+            o0, o1, n0, n1 = pl.strip_rows(own0, own1)
+            assert o0 == prev
+            prev = o1
+            bf = _own(p, q, H, Ho, own0, own1)
+            assert (bf is None and o0 == o1) or bf == (o0, o1)
+            if o1 > o0:
+                # every row a kept output's tap reads (after global padding) is inside [n0, n1)
+                taps = {"nearest": [0], "bilinear": [0, 1], "bicubic": [-1, 0, 1, 2]}[mode]
+                rows = set()
+                for m in range(o0, o1):
+                    for t in taps:
+                        v = (m * q) // p + t
+                        if 0 <= v < H:
+                            rows.add(v)
+                        elif pad == "replicate":
+                            rows.add(0 if v < 0 else H - 1)
+                        elif pad == "reflect":
+                            rows.add(-v if v < 0 else 2 * (H - 1) - v)
+                assert min(rows) == n0 and max(rows) == n1 - 1
+        assert prev == Ho
+
+
+def test_compulsory_bytes(fc):
+    # SURVEY.md Appendix A / BASELINE.md §3 figures
+    pl = fc.Plan(2, 3, "nearest", "zero", 3, 512, 512, "float32", "floor")
+    assert pl.compulsory_bytes(16) == 55847616
+    pl = fc.Plan(3, 4, "nearest", "zero", 3, 512, 512, "float32", "floor")
+    assert pl.compulsory_bytes(16) == 66060288
+    pl = fc.Plan(5, 3, "bicubic", "reflect", 64, 128, 128, "bfloat16", "floor")
+    assert pl.compulsory_bytes(64) == 505880576
+    pl = fc.Plan(7, 5, "bilinear", "replicate", 3, 2160, 3840, "float16", "floor")
+    assert pl.compulsory_bytes(8) == 1178468352
+    pl = fc.Plan(4, 7, "bilinear", "replicate", 3, 2160, 3840, "float16", "floor")
+    assert pl.compulsory_bytes(8) == 527901888

@@ -1,0 +1,286 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): nearest bit-exact; fp32 max abs error <=
+1e-5 x input range; fp16/bf16 within 1 ulp of the oracle's fp32 result rounded
+to the dtype.  Full-size configs are checked on sampled outputs (plus whole
+border rows/columns) computed one by one by the oracle's direct evaluator, on
+every output of whole planes by the staged oracle, and on every output against
+the reference kernel (bitwise: both kernels share one arithmetic contract).
+"""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from helpers import compare, oracle_input, sample_points
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_2203_10670_b200 as fc
+    from paper_2203_10670_b200 import Plan
+    from paper_2203_10670_b200._lib import FcfsError
+
+DEV = "cuda:0"
+
+
+def run_cfg(cfg: synth.Config, x_dev, force_reference=False):
+    pl = Plan(cfg.p, cfg.q, cfg.mode, cfg.pad, cfg.C, cfg.H, cfg.W, cfg.dtype,
+              "floor" if cfg.floor_extent else "paper", cfg.is1d, force_reference=force_reference)
+    y = pl.run(x_dev)
+    torch.cuda.synchronize()
+    return pl, y
+
+
+def check_full_config(cfg: synth.Config, n_points=60000, whole_planes=(0,)):
+    x = synth.make_input(cfg)
+    xd = x.to(DEV)
+    pl, y = run_cfg(cfg, xd)
+    xr = oracle_input(x)
+    rng = float(xr.max() - xr.min())
+    planes = cfg.planes
+    Ho, Wo = pl.output_shape()
+    assert tuple(y.shape) == (cfg.N, cfg.C, Ho, Wo)
+    ext = dict(floor_extent=cfg.floor_extent, is1d=cfg.is1d)
+    # (1) sampled outputs, direct evaluator, one by one
+    rs = np.random.RandomState(cfg.seed % 1000)
+    pts = sample_points(rs, planes, Ho, Wo, n_points)
+    ref = oracle.direct_points(xr.reshape(planes, cfg.H, cfg.W), pts, cfg.p, cfg.q, cfg.mode, cfg.pad, **ext)
+    got = y.reshape(planes, Ho, Wo)[torch.from_numpy(pts[:, 0]), torch.from_numpy(pts[:, 1]),
+                                    torch.from_numpy(pts[:, 2])]
+    compare(got, ref, cfg.dtype, cfg.mode, rng, f"{cfg.name} sampled")
+    # (2) whole planes, staged oracle
+    for pli in whole_planes:
+        ref = oracle.staged(xr.reshape(planes, cfg.H, cfg.W)[pli], cfg.p, cfg.q, cfg.mode, cfg.pad, **ext)
+        compare(y.reshape(planes, Ho, Wo)[pli], ref, cfg.dtype, cfg.mode, rng, f"{cfg.name} plane {pli}")
+    # (3) every output: fused/gather kernel == reference kernel, bitwise
+    _, yr = run_cfg(cfg, xd, force_reference=True)
+    assert torch.equal(y.view(torch.int16 if cfg.dtype != "float32" else torch.int32),
+                       yr.view(torch.int16 if cfg.dtype != "float32" else torch.int32)), f"{cfg.name}: kernels differ"
+    return pl
+
+
+@pytest.mark.parametrize("name", ["C1a", "C1b"])
+def test_config1_every_output(name):
+    cfg = synth.CONFIGS[name]
+    x = synth.make_input(cfg)
+    pl, y = run_cfg(cfg, x.to(DEV))
+    ref = oracle.staged(oracle_input(x), cfg.p, cfg.q, cfg.mode, cfg.pad, floor_extent=cfg.floor_extent,
+                        is1d=cfg.is1d)
+    compare(y, ref, cfg.dtype, cfg.mode, float(x.max() - x.min()), name)
+    assert tuple(y.shape[-2:]) == {"C1a": (72, 96), "C1b": (1, 67)}[name]
+
+
+@pytest.mark.parametrize("name", ["C2a", "C2b"])
+def test_config2_nearest_bit_exact_every_output(name):
+    cfg = synth.CONFIGS[name]
+    x = synth.make_input(cfg)
+    pl, y = run_cfg(cfg, x.to(DEV))
+    assert pl.kernel == "nearest_gather"
+    ref = oracle.staged(oracle_input(x), cfg.p, cfg.q, cfg.mode, cfg.pad, floor_extent=True)
+    compare(y, ref, cfg.dtype, cfg.mode, 1.0, name)
+
+
+def test_config3_bicubic_bf16():
+    pl = check_full_config(synth.CONFIGS["C3"], whole_planes=(0, 4095))
+    assert pl.kernel == "fused_separable" and pl.output_shape() == (213, 213)
+
+
+@pytest.mark.parametrize("name", ["C4a", "C4b"])
+def test_config4_bilinear_fp16(name):
+    pl = check_full_config(synth.CONFIGS[name], whole_planes=(5,))
+    assert pl.kernel == "fused_separable"
+
+
+def test_config5_giant_image_sampled():
+    cfg = synth.CONFIGS["C5"]
+    x = synth.make_input(cfg)
+    xd = x.to(DEV)
+    pl, y = run_cfg(cfg, xd)
+    assert pl.kernel == "fused_separable" and pl.output_shape() == (19660, 19660)
+    xr = x.numpy()
+    rng = float(xr.max() - xr.min())
+    rs = np.random.RandomState(5)
+    pts = sample_points(rs, 1, 19660, 19660, 100000)
+    ref = oracle.direct_points(xr.reshape(1, cfg.H, cfg.W), pts, cfg.p, cfg.q, cfg.mode, cfg.pad, floor_extent=True)
+    got = y.reshape(19660, 19660)[torch.from_numpy(pts[:, 1]), torch.from_numpy(pts[:, 2])]
+    compare(got, ref, "float32", "bicubic", rng, "C5 sampled")
+    # every output row within +-4 of each 8-way strip boundary
+    rows = []
+    for g in range(1, 8):
+        o0, o1, n0, n1 = pl.strip_rows(g * 4096, (g + 1) * 4096)
+        rows += list(range(max(0, o0 - 4), min(19660, o0 + 5)))
+    r = np.array(sorted(set(rows)))
+    for r0 in r:
+        lo = max(0, (r0 * 5) // 3 - 2)
+        hi = min(cfg.H, (r0 * 5) // 3 + 4)
+        ref = oracle.direct(xr[0, 0, lo:hi], 3, 5, "bicubic", "replicate", floor_extent=True, rows=(r0, r0 + 1),
+                            H=cfg.H, row0=lo)
+        compare(y[0, 0, r0:r0 + 1], ref, "float32", "bicubic", rng, f"C5 row {r0}")
+    # every output: fused == reference, bitwise
+    _, yr = run_cfg(cfg, xd, force_reference=True)
+    assert torch.equal(y.view(torch.int32), yr.view(torch.int32))
+
+
+FACTORS = [(1, 1), (3, 2), (2, 3), (5, 3), (3, 5), (7, 5), (4, 7), (2, 1), (1, 2), (4, 3), (5, 4), (2, 11),
+           (27, 11), (6, 5), (3, 4)]
+DTYPES = ["float32", "float16", "bfloat16"]
+
+
+def _rand_input(seed, shape, dtype):
+    v = synth.normal_f32(seed, int(np.prod(shape))).reshape(shape)
+    return torch.from_numpy(v).to(getattr(torch, dtype))
+
+
+@pytest.mark.parametrize("mode", ["nearest", "bilinear", "bicubic"])
+@pytest.mark.parametrize("pad", ["zero", "replicate", "reflect"])
+def test_sweep_every_output(mode, pad):
+    """Small ragged shapes spanning several tiles, every factor/dtype/extent: all outputs."""
+    rs = np.random.RandomState(hash((mode, pad)) % 2 ** 31)
+    n = 0
+    for (p, q), dtype in itertools.product(FACTORS, DTYPES):
+        H = int(rs.randint(3, 90))
+        W = int(rs.choice([8, 16, 24, 40, 64, 72, 96, 104, 120, 200, 264, 328, 37, 101]))
+        N, C = int(rs.randint(1, 3)), int(rs.randint(1, 4))
+        ext = ["paper", "floor"][n % 2]
+        n += 1
+        x = _rand_input(1000 + n, (N, C, H, W), dtype)
+        try:
+            pl = Plan(p, q, mode, pad, C, H, W, dtype, ext)
+        except FcfsError as e:
+            with pytest.raises(oracle.OracleError):
+                oracle.staged(oracle_input(x), p, q, mode, pad, floor_extent=(ext == "floor"))
+            assert e.name in ("FCFS_E_PAD", "FCFS_E_SHAPE")
+            continue
+        y = pl.run(x.to(DEV))
+        torch.cuda.synchronize()
+        xr = oracle_input(x)
+        ref = oracle.staged(xr, p, q, mode, pad, floor_extent=(ext == "floor"))
+        compare(y, ref, dtype, mode, float(xr.max() - xr.min()), f"{p}/{q} {mode} {pad} {dtype} {ext} {H}x{W}")
+        yr = Plan(p, q, mode, pad, C, H, W, dtype, ext, force_reference=True).run(x.to(DEV))
+        assert torch.equal(y.cpu().view(torch.uint8), yr.cpu().view(torch.uint8)), f"{p}/{q} {mode} {pad} kernels"
+
+
+@pytest.mark.parametrize("mode", ["nearest", "bilinear", "bicubic"])
+def test_1d_rows(mode):
+    for (p, q), dtype in itertools.product([(2, 3), (3, 2), (5, 3), (27, 11)], DTYPES):
+        x = _rand_input(7, (2, 3, 5, 101), dtype)
+        pl = Plan(p, q, mode, "replicate", 3, 5, 101, dtype, "floor", is1d=True)
+        y = pl.run(x.to(DEV))
+        ref = oracle.staged(oracle_input(x), p, q, mode, "replicate", floor_extent=True, is1d=True)
+        compare(y, ref, dtype, mode, float(x.float().max() - x.float().min()), f"1d {p}/{q} {dtype}")
+
+
+def test_identity_bit_exact():
+    for mode, pad, dtype in itertools.product(["nearest", "bilinear", "bicubic"], ["zero", "replicate", "reflect"],
+                                              DTYPES):
+        x = _rand_input(3, (2, 3, 33, 64), dtype).to(DEV)
+        y = fc.scale(x, 3, 3, mode, pad)
+        assert torch.equal(y.view(torch.int16 if dtype != "float32" else torch.int32),
+                           x.view(torch.int16 if dtype != "float32" else torch.int32))
+
+
+def test_pixel_repetition():
+    x = _rand_input(4, (1, 2, 21, 40), "float32").to(DEV)
+    for p in (2, 3, 4):
+        y = fc.scale(x, p, 1, "nearest", "zero")
+        ref = x.repeat_interleave(p, dim=2).repeat_interleave(p, dim=3)
+        assert torch.equal(y, ref)
+
+
+def test_strips_equal_whole_image():
+    """Row strips run one after another on one GPU (halo rows sliced from the
+    whole input) reproduce the single-launch output bit for bit."""
+    for (p, q, mode, pad, dtype) in [(3, 5, "bicubic", "replicate", "float32"), (5, 3, "bicubic", "reflect", "bfloat16"),
+                                     (7, 5, "bilinear", "zero", "float16"), (2, 3, "nearest", "zero", "float32"),
+                                     (4, 7, "bilinear", "replicate", "float16")]:
+        H, W = 997, 640
+        x = _rand_input(9, (1, 2, H, W), dtype).to(DEV)
+        pl = Plan(p, q, mode, pad, 2, H, W, dtype, "floor")
+        whole = pl.run(x)
+        for G in (2, 3, 8):
+            parts = []
+            for g in range(G):
+                own0, own1 = g * H // G, (g + 1) * H // G
+                o0, o1, n0, n1 = pl.strip_rows(own0, own1)
+                local = x[:, :, n0:n1].contiguous()
+                parts.append(pl.run_rows(local, n0, o0, o1 - o0))
+                if o1 > o0 and n1 - n0 > 1:  # a window without its first halo row is refused
+                    with pytest.raises(FcfsError) as e:
+                        pl.run_rows(x[:, :, n0 + 1:n1].contiguous(), n0 + 1, o0, o1 - o0)
+                    assert e.value.name == "FCFS_E_SHAPE"
+            got = torch.cat(parts, dim=2)
+            assert torch.equal(got.view(torch.uint8), whole.view(torch.uint8)), f"{p}/{q} {mode} G={G}"
+
+
+def test_misaligned_and_odd_pitch_buffers():
+    # an input view offset by one element defeats 16-B bulk copies: the plan must
+    # still be correct (reference kernel), and odd W too.
+    for dtype in DTYPES:
+        base = _rand_input(5, (1 * 2 * 50 * 64 + 1,), dtype).to(DEV)
+        x = base[1:].view(1, 2, 50, 64)
+        pl = Plan(5, 3, "bicubic", "reflect", 2, 50, 64, dtype, "floor")
+        y = pl.run(x)
+        ref = oracle.staged(oracle_input(x.cpu()), 5, 3, "bicubic", "reflect", floor_extent=True)
+        compare(y, ref, dtype, "bicubic", float(x.float().max() - x.float().min()), f"misaligned {dtype}")
+        out_base = torch.empty(y.numel() + 1, dtype=y.dtype, device=DEV)
+        y2 = out_base[1:].view(y.shape)
+        pl.run(x, out=y2)
+        assert torch.equal(y2.view(torch.uint8), y.view(torch.uint8))
+
+
+def test_edge_shapes():
+    for (N, C, H, W) in [(1, 1, 1, 1), (1, 1, 1, 8), (1, 1, 2, 2), (3, 1, 7, 5), (1, 1, 300, 8), (1, 1, 2, 2048)]:
+        for mode, pad in itertools.product(["nearest", "bilinear", "bicubic"], ["zero", "replicate", "reflect"]):
+            x = _rand_input(6, (N, C, H, W), "float32")
+            try:
+                pl = Plan(5, 3, mode, pad, C, H, W, "float32", "paper")
+            except FcfsError as e:
+                assert e.name == "FCFS_E_PAD" and pad == "reflect"
+                continue
+            y = pl.run(x.to(DEV))
+            ref = oracle.staged(x.numpy(), 5, 3, mode, pad)
+            compare(y, ref, "float32", mode, float(x.max() - x.min()) or 1.0, f"{N}x{C}x{H}x{W} {mode} {pad}")
+
+
+def test_empty_batch_and_errors():
+    pl = Plan(3, 2, "bilinear", "replicate", 2, 16, 16, "float32")
+    x = torch.empty((0, 2, 16, 16), device=DEV)
+    assert pl.run(x).shape == (0, 2, 24, 24)
+    from paper_2203_10670_b200 import _lib
+    import ctypes
+    buf = torch.zeros(2 * 16 * 16 * 4, device=DEV)
+    st = _lib.lib.fcfs_run(pl.handle, ctypes.c_void_p(buf.data_ptr()), ctypes.c_void_p(buf.data_ptr() + 64), 1, None)
+    assert _lib.STATUS[st] == "FCFS_E_ARG"  # overlapping in/out
+    st = _lib.lib.fcfs_run(pl.handle, None, ctypes.c_void_p(buf.data_ptr()), 1, None)
+    assert _lib.STATUS[st] == "FCFS_E_ARG"
+
+
+def test_run_host_end_to_end():
+    cfg = synth.CONFIGS["C3"]
+    x = synth.make_input(cfg, 0, 2).pin_memory()
+    pl = Plan(cfg.p, cfg.q, cfg.mode, cfg.pad, cfg.C, cfg.H, cfg.W, cfg.dtype, "floor")
+    out = torch.empty((2, cfg.C, 213, 213), dtype=x.dtype).pin_memory()
+    din = torch.empty_like(x, device=DEV)
+    dout = torch.empty(out.shape, dtype=x.dtype, device=DEV)
+    pl.run_host(x, out, din, dout)
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int16), pl.run(x.to(DEV)).cpu().view(torch.int16))
+
+
+def test_streams_and_concurrency():
+    cfg = synth.CONFIGS["C4b"]
+    x = synth.make_input(cfg, 0, 2).to(DEV)
+    pl = Plan(cfg.p, cfg.q, cfg.mode, cfg.pad, cfg.C, cfg.H, cfg.W, cfg.dtype, "floor")
+    ref = pl.run(x)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        a = pl.run(x)
+    with torch.cuda.stream(s2):
+        b = pl.run(x)
+    torch.cuda.synchronize()
+    assert torch.equal(a, ref) and torch.equal(b, ref)
