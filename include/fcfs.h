@@ -134,6 +134,14 @@ fcfs_status fcfs_run_rows(fcfs_plan_t plan, const void *in_rows, int64_t in_row0
 fcfs_status fcfs_strip_rows(fcfs_plan_t plan, int64_t own_in_row0, int64_t own_in_row1, int64_t *out_row0,
                             int64_t *out_row1, int64_t *need_row0, int64_t *need_row1);
 
+/* fcfs_needed_rows -- the input rows [*need_row0, *need_row1) that output
+ * rows [out_row0, out_row1) read (their own taps, after global padding; an
+ * empty range when every tap is zero padding).  Used to split a strip into
+ * interior rows (computable before the halo arrives) and boundary rows.
+ * Errors: FCFS_E_ARG (range outside [0, Ho] or empty). */
+fcfs_status fcfs_needed_rows(fcfs_plan_t plan, int64_t out_row0, int64_t out_row1, int64_t *need_row0,
+                             int64_t *need_row1);
+
 /* fcfs_run_host -- the end-to-end call with HOST buffers: copies host_in
  * (N x C x H x W, ideally pinned) to dev_in, runs, copies dev_out to
  * host_out (N x C x Ho x Wo), all asynchronously on stream.  dev_in/dev_out

@@ -35,6 +35,7 @@ SIGNATURES = {
     "fcfs_run": (i32, [vp, vp, vp, i64, vp]),
     "fcfs_run_rows": (i32, [vp, vp, i64, i64, vp, i64, i64, i64, vp]),
     "fcfs_strip_rows": (i32, [vp, i64, i64, P64, P64, P64, P64]),
+    "fcfs_needed_rows": (i32, [vp, i64, i64, P64, P64]),
     "fcfs_run_host": (i32, [vp, vp, vp, i64, vp, vp, vp]),
     "fcfs_plan_info": (i32, [vp, ctypes.POINTER(PlanInfo)]),
     "fcfs_phase_table": (i32, [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int)]),

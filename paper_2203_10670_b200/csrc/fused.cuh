@@ -3,24 +3,28 @@
 // p^2-channel hidden layer of §3.1.1 lives only in registers.
 //
 // Structure:
-//   * warp 0 is the producer: one lane streams input rows into a ring of
-//     S shared-memory stages with 1D bulk async copies (TMA engine,
-//     cp.async.bulk + mbarrier complete_tx, L2 evict_first);
+//   * warp 0 is the producer: one lane streams the input rows of each task into
+//     a ring of S shared-memory stages with 1D bulk async copies (TMA engine,
+//     cp.async.bulk + mbarrier complete_tx, L2 evict_first).  A stage holds the
+//     fresh rows of one y-period (Q new input rows) for every plane of the task.
 //   * warps 1..8 are consumers: thread (pl, c) owns column chunk c (K
-//     x-periods = K*P outputs) of plane pl of the task and walks down the
-//     rows.  Per y-period (P output rows from Q new input rows) it
+//     x-periods = K*P outputs) of plane pl and walks down the rows.  Per
+//     y-period (P output rows) it
 //       - horizontally filters the F fresh input rows of the period window
 //         into registers h[L][K*P] (rows shared with the previous period are
-//         carried, not recomputed),
+//         carried in registers, not recomputed),
 //       - vertically filters h into P output rows,
-//       - rounds to the dtype and stores them into a shared staging buffer
-//         laid out exactly like the contiguous global span, co-aligned mod 16;
-//     then the 256 consumers copy the span out with 16-B vector stores
-//     (coalesced whatever the row pitch) -- double-buffered, one named
-//     barrier per period.
+//       - rounds to the dtype and stores them into a shared staging buffer laid
+//         out exactly like the contiguous global span, co-aligned mod 16;
+//     after one named barrier the 16-B-aligned body of every span leaves with a
+//     bulk async store (TMA engine) and a few threads write the unaligned
+//     head/tail elements -- coalesced whatever the row pitch, double-buffered.
+//   * Chunks whose window reaches the image's left/right padding are mapped
+//     to the first consumer threads, so only warp 1 ever takes the padding
+//     path; every other warp reads its window with plain word loads.
 //   * Period/phase structure is compile time (P, Q, TAPS, LO template
 //     parameters), so every weight index is static and the weights are
-//     constant-bank operands of the FFMAs.
+//     constant-bank operands of the FMAs.
 //
 // Arithmetic is exactly the reference kernel's (k_reference.cu): identical
 // fp32 operation sequence per output, so both kernels agree bit for bit.
@@ -68,23 +72,18 @@ __device__ __forceinline__ void load_fast(const T *s, int e0, float (&win)[WIN])
     }
 }
 
+// Window whose columns reach the image border: per-column padding (§3, reading Z5).
 template <typename T, int WIN>
-__device__ __forceinline__ void load_window(const unsigned char *srow, int a0, int a1, int ws, int W, int pad,
-                                            float (&win)[WIN]) {
-    const T *s = reinterpret_cast<const T *>(srow);
-    if (ws >= a0 && ws + WIN <= a1) {
-        load_fast<T, WIN>(s, ws - a0, win);
-    } else {  // columns outside the loaded span: padding (§3, reading Z5)
+__device__ __forceinline__ void load_padded(const T *s, int a0, int a1, int ws, int W, int pad, float (&win)[WIN]) {
 #pragma unroll
-        for (int i = 0; i < WIN; ++i) {
-            int c = pad_src32(ws + i, W, pad);
-            float v = 0.0f;
-            if (c >= 0) {
-                c = min(max(c, a0), a1 - 1);
-                v = DT<T>::to_f(s[c - a0]);
-            }
-            win[i] = v;
+    for (int i = 0; i < WIN; ++i) {
+        int c = pad_src32(ws + i, W, pad);
+        float v = 0.0f;
+        if (c >= 0) {
+            c = min(max(c, a0), a1 - 1);
+            v = DT<T>::to_f(s[c - a0]);
         }
+        win[i] = v;
     }
 }
 
@@ -117,28 +116,6 @@ __device__ __forceinline__ FusedTask fused_decode(const FusedArgs &a, int task) 
     return t;
 }
 
-template <typename T>
-__device__ __forceinline__ void copy_span(unsigned char *g, const unsigned char *s, int bytes, int tid, int nthr) {
-    constexpr int ESZ = sizeof(T);
-    int head = (16 - (int)(reinterpret_cast<uintptr_t>(g) & 15)) & 15;
-    head = min(head, bytes);
-    int nvec = (bytes - head) >> 4;
-    int nh = head / ESZ;
-    int nt = (bytes - head - nvec * 16) / ESZ;
-    for (int u = tid; u < nh + nvec + nt; u += nthr) {
-        if (u < nh) {
-            reinterpret_cast<T *>(g)[u] = reinterpret_cast<const T *>(s)[u];
-        } else if (u < nh + nvec) {
-            int v = u - nh;
-            uint4 val = *reinterpret_cast<const uint4 *>(s + head + v * 16);
-            __stcs(reinterpret_cast<uint4 *>(g + head + v * 16), val);
-        } else {
-            int e = u - nh - nvec;
-            reinterpret_cast<T *>(g + head + nvec * 16)[e] = reinterpret_cast<const T *>(s + head + nvec * 16)[e];
-        }
-    }
-}
-
 template <typename T, int P, int Q, int TAPS, int LO, int K>
 __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __grid_constant__ FusedArgs a) {
     using G = Geo<P, Q, TAPS, LO>;
@@ -169,16 +146,15 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         // ------------------------------------------------------------ producer
         if (lane != 0) return;
         const uint64_t pol = policy_evict_first();
-        uint32_t seq = 0;
+        int slot = 0;
+        uint32_t phase = 0, nfill = 0;
         for (int task = blockIdx.x; task < a.ntasks; task += gridDim.x) {
             const FusedTask t = fused_decode<P, Q, TAPS, LO, K, ESZ>(a, task);
             const int nst = (C > 0 ? 1 : 0) + (t.iy1 - t.iy0);
             const uint32_t seg_bytes = (uint32_t)(t.a1 - t.a0) * ESZ;
             const bool whole_rows = (t.a0 == 0) && (t.a1 == a.W) && ((int)seg_bytes == a.seg_pitch);
-            for (int k = 0; k < nst; ++k, ++seq) {
-                const int slot = seq % a.S;
-                const uint32_t use = seq / a.S;
-                if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);
+            for (int k = 0; k < nst; ++k) {
+                if (nfill >= (uint32_t)a.S) mbar_wait(&empty[slot], phase ^ 1);
                 int vf, nr;
                 if (C > 0 && k == 0) {
                     vf = Q * t.iy0 + LO;
@@ -216,6 +192,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                     }
                 }
                 mbar_arrive(&full[slot]);
+                ++nfill;
+                if (++slot == a.S) { slot = 0; phase ^= 1; }
             }
         }
         return;
@@ -223,18 +201,40 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
 
     // ---------------------------------------------------------------- consumers
     const int ctid = threadIdx.x - 32;
+    const int span_id = ctid >> 4, span_e = ctid & 15;  // copy-out roles
+    const int rowb = a.Wo * ESZ;
     float h[L][KP];
-    uint32_t seq = 0;
+    int slot = 0;
+    uint32_t phase = 0;
     int ob = 0;
     for (int task = blockIdx.x; task < a.ntasks; task += gridDim.x) {
         const FusedTask t = fused_decode<P, Q, TAPS, LO, K, ESZ>(a, task);
-        const int pl = ctid / a.CPT;
-        const int chunk = t.ch0 + (ctid - pl * a.CPT);
+        // thread -> (plane, chunk), chunks that touch the border first
+        const int ilo = max(t.ch0, a.c_lo_int);
+        const int ihi = max(ilo, min(t.ch1, a.c_first_bad));
+        const int nL = max(0, min(ilo, t.ch1) - t.ch0);
+        const int rstart = max(ihi, t.ch0);
+        const int nR = max(0, t.ch1 - rstart);
+        const int E = nL + nR;
+        const int I = (t.ch1 - t.ch0) - E;
+        int pl, chunk;
+        if (ctid < a.NP * E) {
+            pl = ctid / E;
+            const int e = ctid - pl * E;
+            chunk = e < nL ? t.ch0 + e : rstart + (e - nL);
+        } else {
+            const int j = ctid - a.NP * E;
+            pl = I > 0 ? j / I : a.NP;
+            chunk = ilo + (j - pl * I);
+        }
         const int plane = t.group * a.NP + pl;
-        const bool active = (pl < a.NP) && (plane < a.planes) && (chunk < t.ch1);
+        const bool active = (pl < a.NP) && (plane < a.planes);
         const int ws = chunk * K * Q + LO;
+        const bool fast = ws >= t.a0 && ws + WIN <= t.a1;
+        const int col = chunk * KP;
+        const bool full_chunk = col + KP <= t.c1;
         const int in_off = pl * a.SR * a.seg_pitch;
-        T *const pout = static_cast<T *>(a.out) + (int64_t)plane * a.out_plane_stride;
+        const int64_t plane_out = (int64_t)plane * a.out_plane_stride;
 
         auto row_h = [&](float(&hr)[KP], int v, const unsigned char *srow) {
             if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) {
@@ -243,7 +243,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 return;
             }
             float win[WIN];
-            load_window<T, WIN>(srow, t.a0, t.a1, ws, a.W, a.pad, win);
+            const T *s = reinterpret_cast<const T *>(srow);
+            if (fast) load_fast<T, WIN>(s, ws - t.a0, win);
+            else load_padded<T, WIN>(s, t.a0, t.a1, ws, a.W, a.pad, win);
 #pragma unroll
             for (int k = 0; k < K; ++k) {
 #pragma unroll
@@ -263,16 +265,15 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         };
 
         if constexpr (C > 0) {  // warm-up: the first C window rows of the first period
-            const int slot = seq % a.S;
-            mbar_wait(&full[slot], (seq / a.S) & 1);
+            mbar_wait(&full[slot], phase);
             if (active) {
                 const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
 #pragma unroll
                 for (int i = 0; i < C; ++i) row_h(h[i], Q * t.iy0 + LO + i, sb + i * a.seg_pitch);
             }
             __syncwarp();
-            if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot]);
-            ++seq;
+            if (lane == 0) mbar_arrive(&empty[slot]);
+            if (++slot == a.S) { slot = 0; phase ^= 1; }
         }
 
         for (int iy = t.iy0; iy < t.iy1; ++iy) {
@@ -284,22 +285,31 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                         for (int c = 0; c < KP; ++c) h[i][c] = h[Q + i][c];
                 }
             }
-            {
-                const int slot = seq % a.S;
-                mbar_wait(&full[slot], (seq / a.S) & 1);
-                if (active) {
-                    const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
+            mbar_wait(&full[slot], phase);
+            if (active) {
+                const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
 #pragma unroll
-                    for (int i = 0; i < F; ++i) row_h(h[C + i], Q * iy + LO + C + i, sb + i * a.seg_pitch);
-                }
-                __syncwarp();
-                if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot]);
-                ++seq;
+                for (int i = 0; i < F; ++i) row_h(h[C + i], Q * iy + LO + C + i, sb + i * a.seg_pitch);
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+            if (++slot == a.S) { slot = 0; phase ^= 1; }
 
             const int mfirst = max(iy * P, t.my_lo), mlast = min(iy * P + P, t.my_hi);
             unsigned char *ob_base = obuf + ob * a.obuf_bytes;
             if (active) {
+                // staging address of (row iy*P, column `col`) for this thread
+                unsigned char *sp;
+                int jy_step;
+                if (a.full_width) {
+                    const uintptr_t g = reinterpret_cast<uintptr_t>(static_cast<T *>(a.out) + plane_out +
+                                                                    (int64_t)(mfirst - a.out_row0) * a.Wo);
+                    sp = ob_base + pl * a.out_pitch + (g & 15) + (iy * P - mfirst) * rowb + col * ESZ;
+                    jy_step = rowb;
+                } else {
+                    sp = ob_base + (col - t.c0) * ESZ;
+                    jy_step = a.out_pitch;
+                }
 #pragma unroll
                 for (int jy = 0; jy < P; ++jy) {
                     const int my = iy * P + jy;
@@ -318,53 +328,72 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                             o[c] = v2;
                         }
                     }
-                    unsigned char *srow;
-                    int col0;
+                    T *sr;
                     if (a.full_width) {
-                        const uintptr_t g = reinterpret_cast<uintptr_t>(pout + (int64_t)(mfirst - a.out_row0) * a.Wo);
-                        srow = ob_base + pl * a.out_pitch + (g & 15) + (my - mfirst) * a.Wo * ESZ;
-                        col0 = 0;
+                        sr = reinterpret_cast<T *>(sp + jy * jy_step);
                     } else {
-                        const uintptr_t g = reinterpret_cast<uintptr_t>(pout + (int64_t)(my - a.out_row0) * a.Wo + t.c0);
-                        srow = ob_base + (pl * P + jy) * a.out_pitch + (g & 15);
-                        col0 = t.c0;
+                        const uintptr_t g = reinterpret_cast<uintptr_t>(static_cast<T *>(a.out) + plane_out +
+                                                                        (int64_t)(my - a.out_row0) * a.Wo + t.c0);
+                        sr = reinterpret_cast<T *>(sp + jy * jy_step + (g & 15));
                     }
-                    T *sr = reinterpret_cast<T *>(srow);
+                    if (full_chunk) {
 #pragma unroll
-                    for (int c = 0; c < KP; ++c) {
-                        const int mx = chunk * KP + c;
-                        if (mx < t.c1) sr[mx - col0] = DT<T>::from_f(o[c]);
+                        for (int c = 0; c < KP; ++c) sr[c] = DT<T>::from_f(o[c]);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < KP; ++c)
+                            if (col + c < t.c1) sr[c] = DT<T>::from_f(o[c]);
                     }
                 }
+                fence_proxy_async_smem();
             }
+            if (span_e == 0) bulk_wait_read0();  // my previous bulk store has read its buffer
             named_bar_sync(1, NCT);
+            // copy-out: span (tid >> 4), element slot (tid & 15): slot 0 issues the
+            // bulk body; slots 0..7 copy head elements, 8..15 tail elements.
             if (mlast > mfirst) {
                 const int nrow = mlast - mfirst;
-                const int nsp = a.full_width ? a.NP : a.NP * nrow;
-                for (int sp = 0; sp < nsp; ++sp) {
-                    const int spl = a.full_width ? sp : sp / nrow;
+                const int nsp = a.full_width ? a.NP : nrow;
+                if (span_id < nsp) {
+                    const int spl = a.full_width ? span_id : 0;
                     const int plane2 = t.group * a.NP + spl;
-                    if (plane2 >= a.planes) break;
-                    T *po = static_cast<T *>(a.out) + (int64_t)plane2 * a.out_plane_stride;
-                    unsigned char *g;
-                    const unsigned char *s;
-                    int bytes;
-                    if (a.full_width) {
-                        g = reinterpret_cast<unsigned char *>(po + (int64_t)(mfirst - a.out_row0) * a.Wo);
-                        bytes = nrow * a.Wo * ESZ;
-                        s = ob_base + spl * a.out_pitch + (reinterpret_cast<uintptr_t>(g) & 15);
-                    } else {
-                        const int my = mfirst + sp % nrow;
-                        g = reinterpret_cast<unsigned char *>(po + (int64_t)(my - a.out_row0) * a.Wo + t.c0);
-                        bytes = (t.c1 - t.c0) * ESZ;
-                        s = ob_base + (spl * P + (my - iy * P)) * a.out_pitch + (reinterpret_cast<uintptr_t>(g) & 15);
+                    if (plane2 < a.planes) {
+                        T *po = static_cast<T *>(a.out) + (int64_t)plane2 * a.out_plane_stride;
+                        unsigned char *g;
+                        const unsigned char *s;
+                        int bytes;
+                        if (a.full_width) {
+                            g = reinterpret_cast<unsigned char *>(po + (int64_t)(mfirst - a.out_row0) * a.Wo);
+                            bytes = nrow * rowb;
+                            s = ob_base + spl * a.out_pitch + (reinterpret_cast<uintptr_t>(g) & 15);
+                        } else {
+                            const int my = mfirst + span_id;
+                            g = reinterpret_cast<unsigned char *>(po + (int64_t)(my - a.out_row0) * a.Wo + t.c0);
+                            bytes = (t.c1 - t.c0) * ESZ;
+                            s = ob_base + (my - iy * P) * a.out_pitch + (reinterpret_cast<uintptr_t>(g) & 15);
+                        }
+                        const int head = min(bytes, (16 - (int)(reinterpret_cast<uintptr_t>(g) & 15)) & 15);
+                        const int body = (bytes - head) & ~15;
+                        const int tail = bytes - head - body;
+                        if (span_e == 0 && body > 0) {
+                            bulk_s2g(g + head, s + head, (uint32_t)body);
+                            bulk_commit();
+                        }
+                        if (span_e < 8) {
+                            if (span_e * ESZ < head)
+                                reinterpret_cast<T *>(g)[span_e] = reinterpret_cast<const T *>(s)[span_e];
+                        } else {
+                            const int e = span_e - 8;
+                            if (e * ESZ < tail)
+                                reinterpret_cast<T *>(g + head + body)[e] = reinterpret_cast<const T *>(s + head + body)[e];
+                        }
                     }
-                    copy_span<T>(g, s, bytes, ctid, NCT);
                 }
             }
             ob ^= 1;
         }
     }
+    if (span_e == 0) bulk_wait0();
 }
 
 }  // namespace fcfs

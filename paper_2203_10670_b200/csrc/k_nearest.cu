@@ -3,75 +3,87 @@
 //     out[m_y][m_x] = x~[floor(m_y*q/p)][floor(m_x*q/p)]
 // with no arithmetic on the value (bit-exact; -0, NaN and Inf pass through).
 //
-// Layout: the output of all planes is one flat array; each thread produces
-// V = 32 B of consecutive outputs and writes them with two 16-B stores
-// (coalesced regardless of odd row pitches such as 341*4 B), reading its
-// sources with cached scalar loads (consecutive outputs read nearly
-// consecutive inputs; unreferenced input rows are never touched).  Index math
-// is 32-bit with multiply-shift division (plan checks the ranges).
+// Layout: one warp per output row (grid-stride over planes x rows); the lanes
+// sweep the row's columns, 32 consecutive outputs per instruction, so every
+// load instruction reads a short contiguous run of the source row and every
+// store instruction writes 32 consecutive outputs (coalesced whatever the row
+// pitch).  Row index math happens once per warp; the column index is advanced
+// incrementally (no division in the inner loop).  Source rows that no output
+// references are never read.
 #include "device_common.cuh"
 
 namespace fcfs {
 
-template <typename T>
+template <typename T, int U>
 __global__ void __launch_bounds__(256) fcfs_nearest_kernel(const __grid_constant__ NearestArgs a) {
-    constexpr int V = 32 / sizeof(T);
     const RunGeom &g = a.g;
-    const uint32_t total = (uint32_t)(g.planes * g.out_nrows * g.Wo);
-    const uint32_t Wo = (uint32_t)g.Wo, nrows = (uint32_t)g.out_nrows;
-    const int32_t H = (int32_t)g.H, W = (int32_t)g.W, row0 = (int32_t)g.in_row0;
+    const int lane = threadIdx.x & 31;
+    const int64_t nrows_total = g.planes * g.out_nrows;
+    const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int32_t W = (int32_t)g.W, Wo = (int32_t)g.Wo, H = (int32_t)g.H;
+    const int p = a.p, q = a.q;
+    // per-lane column stepping: mx advances by 32*U per iteration
+    const int step = 32 * U;
+    const int dq = (int)(((int64_t)step * q) / p), dr = (int)(((int64_t)step * q) % p);
     const T *__restrict__ in = static_cast<const T *>(g.in);
     T *__restrict__ out = static_cast<T *>(g.out);
-    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; (uint64_t)c * V < total; c += gridDim.x * blockDim.x) {
-        const uint32_t f0 = c * V;
-        uint32_t rowflat = fdiv(f0, a.div_wo);
-        uint32_t mx = f0 - rowflat * Wo;
-        uint32_t plane = fdiv(rowflat, a.div_rows);
-        uint32_t lr = rowflat - plane * nrows;
-        T vals[V];
+    for (int64_t rw = warp0; rw < nrows_total; rw += nwarps) {
+        const int64_t plane = rw / g.out_nrows;
+        const int64_t lr = rw - plane * g.out_nrows;
+        const int64_t my = g.out_row0 + lr;
+        const int64_t by = a.is1d ? my : (my * q) / p;
+        const int64_t rs = pad_src(by, H, a.pad);
+        T *orow = out + plane * g.out_plane_stride + lr * Wo;
+        if (rs < 0) {  // a zero-padding row
+            for (int mx = lane; mx < Wo; mx += 32) orow[mx] = DT<T>::from_f(0.0f);
+            continue;
+        }
+        const T *irow = in + plane * g.in_plane_stride + (rs - g.in_row0) * W;
+        // source column and remainder of the first output of each of the U sub-slots
+        int bx[U], rem[U];
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            T val = DT<T>::from_f(0.0f);
-            if (f0 + v < total) {
-                int32_t my = (int32_t)(lr + g.out_row0);
-                int32_t by = a.is1d ? my : (int32_t)fdiv((uint32_t)my * a.q, a.div_p);
-                int32_t bx = (int32_t)fdiv(mx * a.q, a.div_p);
-                int32_t rs = pad_src32(by, H, a.pad);
-                int32_t cs = pad_src32(bx, W, a.pad);
-                if (rs >= 0 && cs >= 0)
-                    val = in[(int64_t)plane * g.in_plane_stride + (int64_t)(rs - row0) * W + cs];
-                if (++mx == Wo) {
-                    mx = 0;
-                    if (++lr == nrows) { lr = 0; ++plane; }
+        for (int u = 0; u < U; ++u) {
+            const int mx = lane + 32 * u;
+            bx[u] = (int)(((int64_t)mx * q) / p);
+            rem[u] = (int)(((int64_t)mx * q) % p);
+        }
+        for (int mx0 = 0; mx0 < Wo; mx0 += step) {
+            T v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int mx = mx0 + lane + 32 * u;
+                v[u] = DT<T>::from_f(0.0f);
+                if (mx < Wo) {
+                    const int cs = bx[u] < W ? bx[u] : pad_src32(bx[u], W, a.pad);
+                    if (cs >= 0) v[u] = irow[cs];
                 }
             }
-            vals[v] = val;
-        }
-        if (a.vec_ok && f0 + V <= total) {
-            const uint4 *s = reinterpret_cast<const uint4 *>(vals);
-            uint4 *d = reinterpret_cast<uint4 *>(out + f0);
-            d[0] = s[0];
-            d[1] = s[1];
-        } else {
 #pragma unroll
-            for (int v = 0; v < V; ++v)
-                if (f0 + v < total) out[f0 + v] = vals[v];
+            for (int u = 0; u < U; ++u) {
+                const int mx = mx0 + lane + 32 * u;
+                if (mx < Wo) orow[mx] = v[u];
+                bx[u] += dq;
+                rem[u] += dr;
+                if (rem[u] >= p) {
+                    rem[u] -= p;
+                    bx[u] += 1;
+                }
+            }
         }
     }
 }
 
 int launch_nearest(int dtype, const NearestArgs &a, void *stream) {
-    const int64_t total = a.g.planes * a.g.out_nrows * a.g.Wo;
-    if (total == 0) return 0;
-    const int V = dtype == FCFS_F32 ? 8 : 16;
-    int64_t threads = (total + V - 1) / V;
-    int64_t blocks = (threads + 255) / 256;
-    if (blocks > 148 * 64) blocks = 148 * 64;
+    const int64_t rows = a.g.planes * a.g.out_nrows;
+    if (rows == 0 || a.g.Wo == 0) return 0;
+    int64_t blocks = (rows + 7) / 8;  // 8 warps per block, one row per warp
+    if (blocks > 148 * 8 * 4) blocks = 148 * 8 * 4;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     switch (dtype) {
-    case FCFS_F32: fcfs_nearest_kernel<float><<<(int)blocks, 256, 0, s>>>(a); break;
-    case FCFS_F16: fcfs_nearest_kernel<__half><<<(int)blocks, 256, 0, s>>>(a); break;
-    default: fcfs_nearest_kernel<__nv_bfloat16><<<(int)blocks, 256, 0, s>>>(a); break;
+    case FCFS_F32: fcfs_nearest_kernel<float, 4><<<(int)blocks, 256, 0, s>>>(a); break;
+    case FCFS_F16: fcfs_nearest_kernel<__half, 4><<<(int)blocks, 256, 0, s>>>(a); break;
+    default: fcfs_nearest_kernel<__nv_bfloat16, 4><<<(int)blocks, 256, 0, s>>>(a); break;
     }
     return (int)cudaGetLastError();
 }

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -179,6 +180,13 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
         for (int t = 0; t < 4; ++t) a.w[j][t] = pl->tab.w[j][t];
     a.nch = (int32_t)((g.Wo + KP - 1) / KP);
     a.SR = std::max(Ff, Cc);
+    {  // chunks whose column window reaches the left / right padding
+        const int WIN = (K - 1) * Q + Lw;
+        a.c_lo_int = LO < 0 ? 1 : 0;
+        const int64_t room = g.W - WIN - LO;
+        int64_t cfb = room < 0 ? 0 : room / (K * Q) + 1;
+        a.c_first_bad = (int32_t)std::min<int64_t>(std::max<int64_t>(cfb, a.c_lo_int), a.nch);
+    }
     const int budget = 110 * 1024;  // two CTAs per SM
     auto seg_pitch_for = [&](int cpt) {
         int64_t elems = std::min<int64_t>(g.W, (int64_t)cpt * K * Q - Q + Lw + 2 * A);
@@ -191,7 +199,7 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
             a.full_width = 1;
             a.CPT = a.nch;
             a.ntile = 1;
-            a.NP = (int)std::min<int64_t>(NT / a.CPT, g.planes);
+            a.NP = (int)std::min<int64_t>(std::min(16, NT / a.CPT), g.planes);  // <= 16 copy-out spans
         } else if (a.full_width && a.NP > 1) {
             a.NP = std::max(1, a.NP / 2);
         } else {
@@ -232,12 +240,22 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
         const int min_pb = std::max(2, (4 * Cc + Q - 1) / std::max(1, Q));  // warm-up <= ~25%
         nbands = std::max(1, std::min(want, nper / min_pb));
     }
+    if (const char *e = std::getenv("FCFS_DEBUG_NBANDS")) nbands = std::max(1, std::min(nper, std::atoi(e)));
     a.PB = (nper + nbands - 1) / nbands;
     a.nbands = (nper + a.PB - 1) / a.PB;
     const int64_t ntasks = base_tasks * a.nbands;
     if (ntasks > INT32_MAX) return false;
     a.ntasks = (int32_t)ntasks;
     L.grid = (int)std::min<int64_t>(ntasks, resident);
+    if (const char *e = std::getenv("FCFS_DEBUG_GRID")) L.grid = std::max(1, std::min(L.grid, std::atoi(e)));
+    if (const char *e = std::getenv("FCFS_DEBUG_S")) a.S = std::max(2, std::min(a.S, std::atoi(e)));
+    if (std::getenv("FCFS_DEBUG_PRINT"))
+        std::fprintf(stderr,
+                     "fused P%d Q%d T%d K%d: full_width=%d NP=%d CPT=%d nch=%d ntile=%d ngroups=%d S=%d SR=%d "
+                     "seg_pitch=%d stage=%d out_pitch=%d obuf=%d nper=%d PB=%d nbands=%d ntasks=%d grid=%d smem=%d\n",
+                     P, Q, TAPS, K, a.full_width, a.NP, a.CPT, a.nch, a.ntile, a.ngroups, a.S, a.SR, a.seg_pitch,
+                     a.stage_bytes, a.out_pitch, a.obuf_bytes, nper, a.PB, a.nbands, a.ntasks, L.grid,
+                     128 + a.S * a.stage_bytes + 128 + 2 * a.obuf_bytes);
     L.smem = 128 + a.S * a.stage_bytes + 128 + 2 * a.obuf_bytes;
     return true;
 }
@@ -285,9 +303,7 @@ fcfs_status run_window(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t 
 
     int kernel = pl->kernel;
     const int64_t total = planes * out_nrows * pl->Wo;
-    if (kernel == 1) {  // 32-bit index ranges of the gather kernel
-        if (total > INT32_MAX - 64 || pl->Wo * pl->q > INT32_MAX || pl->Ho * pl->q > INT32_MAX) kernel = 0;
-    }
+    (void)total;
     if (kernel == 2) {
         if ((reinterpret_cast<uintptr_t>(in) & 15) || planes * std::max(in_nrows * pl->W, out_nrows * pl->Wo) > INT32_MAX * 16LL)
             kernel = 0;
@@ -467,6 +483,12 @@ fcfs_status fcfs_strip_rows(fcfs_plan_t pl, int64_t own0, int64_t own1, int64_t 
         *need0 = *need1 = own0;
         return FCFS_OK;
     }
+    needed_rows(pl, m0, m1, need0, need1);
+    return FCFS_OK;
+}
+
+fcfs_status fcfs_needed_rows(fcfs_plan_t pl, int64_t m0, int64_t m1, int64_t *need0, int64_t *need1) {
+    if (!pl || !need0 || !need1 || m0 < 0 || m1 > pl->Ho || m0 >= m1) return FCFS_E_ARG;
     needed_rows(pl, m0, m1, need0, need1);
     return FCFS_OK;
 }

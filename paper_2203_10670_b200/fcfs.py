@@ -83,6 +83,12 @@ class Plan:
         check(_lib.lib.fcfs_strip_rows(self._h, own0, own1, *[ctypes.byref(x) for x in v]), "fcfs_strip_rows")
         return tuple(x.value for x in v)
 
+    def needed_rows(self, out0: int, out1: int):
+        """Input rows [need0, need1) that output rows [out0, out1) read."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        check(_lib.lib.fcfs_needed_rows(self._h, out0, out1, ctypes.byref(a), ctypes.byref(b)), "fcfs_needed_rows")
+        return a.value, b.value
+
     # ---------------------------------------------------------------- runs
     def _stream(self, stream):
         import torch

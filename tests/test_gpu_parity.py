@@ -8,6 +8,7 @@ every output of whole planes by the staged oracle, and on every output against
 the reference kernel (bitwise: both kernels share one arithmetic contract).
 """
 import itertools
+import zlib
 
 import numpy as np
 import pytest
@@ -139,7 +140,7 @@ def _rand_input(seed, shape, dtype):
 @pytest.mark.parametrize("pad", ["zero", "replicate", "reflect"])
 def test_sweep_every_output(mode, pad):
     """Small ragged shapes spanning several tiles, every factor/dtype/extent: all outputs."""
-    rs = np.random.RandomState(hash((mode, pad)) % 2 ** 31)
+    rs = np.random.RandomState(zlib.crc32(f"{mode}-{pad}".encode()))
     n = 0
     for (p, q), dtype in itertools.product(FACTORS, DTYPES):
         H = int(rs.randint(3, 90))
