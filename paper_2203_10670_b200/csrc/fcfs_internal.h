@@ -85,8 +85,7 @@ struct FusedArgs {
     int32_t out_pitch;   // bytes per plane (full width) or per (plane, row) segment (tiled)
     int32_t obuf_bytes;
     int32_t full_width;
-    int32_t c_lo_int;    // first chunk whose window never reaches left padding (0 or 1)
-    int32_t c_first_bad; // first chunk whose window reaches right padding
+    int32_t rpad;        // right padding columns materialised after the last image column
     float w[16][4];      // phase weights (fused variants have p <= 16)
 };
 

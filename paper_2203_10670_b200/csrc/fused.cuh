@@ -3,10 +3,13 @@
 // p^2-channel hidden layer of §3.1.1 lives only in registers.
 //
 // Structure:
-//   * warp 0 is the producer: one lane streams the input rows of each task into
+//   * warp 0 is the producer.  Lane 0 streams the input rows of each task into
 //     a ring of S shared-memory stages with 1D bulk async copies (TMA engine,
-//     cp.async.bulk + mbarrier complete_tx, L2 evict_first).  A stage holds the
-//     fresh rows of one y-period (Q new input rows) for every plane of the task.
+//     cp.async.bulk + mbarrier complete_tx, L2 evict_first), running up to S
+//     stages ahead.  When a stage has landed the whole warp materialises the
+//     padding columns (§3 Padding) in the row margins, then
+//     releases the stage to the consumers.  A stage holds the fresh rows of one
+//     y-period (Q new input rows) of every plane of the task.
 //   * warps 1..8 are consumers: thread (pl, c) owns column chunk c (K
 //     x-periods = K*P outputs) of plane pl and walks down the rows.  Per
 //     y-period (P output rows) it
@@ -19,12 +22,15 @@
 //     after one named barrier the 16-B-aligned body of every span leaves with a
 //     bulk async store (TMA engine) and a few threads write the unaligned
 //     head/tail elements -- coalesced whatever the row pitch, double-buffered.
-//   * Chunks whose window reaches the image's left/right padding are mapped
-//     to the first consumer threads, so only warp 1 ever takes the padding
-//     path; every other warp reads its window with plain word loads.
+//     Every consumer runs the same branch-free path (padding is already in
+//     shared memory).
 //   * Period/phase structure is compile time (P, Q, TAPS, LO template
 //     parameters), so every weight index is static and the weights are
 //     constant-bank operands of the FMAs.
+//
+// Shared row layout: [A margin elements][loaded columns a0..a1)][rpad margin],
+// A = 16 B / element size.  Virtual column c of the row lives at element
+// A + c - a0.
 //
 // Arithmetic is exactly the reference kernel's (k_reference.cu): identical
 // fp32 operation sequence per output, so both kernels agree bit for bit.
@@ -52,7 +58,7 @@ template <> struct HalfBits<__nv_bfloat16> {
 
 // Load WIN consecutive elements starting at element e0 of a shared row.
 template <typename T, int WIN>
-__device__ __forceinline__ void load_fast(const T *s, int e0, float (&win)[WIN]) {
+__device__ __forceinline__ void load_win(const T *s, int e0, float (&win)[WIN]) {
     if constexpr (sizeof(T) == 4) {
 #pragma unroll
         for (int i = 0; i < WIN; ++i) win[i] = s[e0 + i];
@@ -69,21 +75,6 @@ __device__ __forceinline__ void load_fast(const T *s, int e0, float (&win)[WIN])
             uint32_t b1 = ((i + 1) & 1) ? (wd[(i + 1) >> 1] >> 16) : (wd[(i + 1) >> 1] & 0xffffu);
             win[i] = HalfBits<T>::f(odd ? b1 : b0);
         }
-    }
-}
-
-// Window whose columns reach the image border: per-column padding (§3, reading Z5).
-template <typename T, int WIN>
-__device__ __forceinline__ void load_padded(const T *s, int a0, int a1, int ws, int W, int pad, float (&win)[WIN]) {
-#pragma unroll
-    for (int i = 0; i < WIN; ++i) {
-        int c = pad_src32(ws + i, W, pad);
-        float v = 0.0f;
-        if (c >= 0) {
-            c = min(max(c, a0), a1 - 1);
-            v = DT<T>::to_f(s[c - a0]);
-        }
-        win[i] = v;
     }
 }
 
@@ -116,6 +107,49 @@ __device__ __forceinline__ FusedTask fused_decode(const FusedArgs &a, int task) 
     return t;
 }
 
+// Producer-side stage cursor: (task, stage k) of a CTA's sequence of stages.
+template <int P, int Q, int TAPS, int LO, int K, int ESZ>
+struct StageCursor {
+    int task, k, nst, slot;
+    uint32_t phase, seq;
+    FusedTask t;
+    __device__ __forceinline__ void start(const FusedArgs &a) {
+        task = blockIdx.x;
+        k = 0;
+        slot = 0;
+        phase = 0;
+        seq = 0;
+        load(a);
+    }
+    __device__ __forceinline__ void load(const FusedArgs &a) {
+        if (task < a.ntasks) {
+            t = fused_decode<P, Q, TAPS, LO, K, ESZ>(a, task);
+            nst = (Geo<P, Q, TAPS, LO>::C > 0 ? 1 : 0) + (t.iy1 - t.iy0);
+        }
+    }
+    __device__ __forceinline__ void next(const FusedArgs &a) {
+        ++seq;
+        if (++slot == a.S) { slot = 0; phase ^= 1; }
+        if (++k == nst) {
+            k = 0;
+            task += gridDim.x;
+            load(a);
+        }
+    }
+    // virtual rows [vf, vf + nr) of the stage
+    __device__ __forceinline__ void rows(int &vf, int &nr) const {
+        using G = Geo<P, Q, TAPS, LO>;
+        if (G::C > 0 && k == 0) {
+            vf = Q * t.iy0 + LO;
+            nr = G::C;
+        } else {
+            const int iy = t.iy0 + k - (G::C > 0 ? 1 : 0);
+            vf = Q * iy + LO + G::C;
+            nr = G::F;
+        }
+    }
+};
+
 template <typename T, int P, int Q, int TAPS, int LO, int K>
 __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __grid_constant__ FusedArgs a) {
     using G = Geo<P, Q, TAPS, LO>;
@@ -123,19 +157,23 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     constexpr int KP = K * P;
     constexpr int WIN = (K - 1) * Q + L;
     constexpr int ESZ = sizeof(T);
+    constexpr int A = 16 / ESZ;  // left margin (elements)
     constexpr int NCT = 32 * kFusedConsumerWarps;
     static_assert(P <= 16, "fused variants have p <= 16");
+    static_assert(-LO <= A, "left margin too small");
 
     extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem);
-    uint64_t *empty = full + 8;
-    unsigned char *stages = smem + 128;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);   // TMA landed       (count 1 + tx)
+    uint64_t *ready = full + 8;                             // padding written  (count 32)
+    uint64_t *empty = full + 16;                            // consumers done   (count 8 warps)
+    unsigned char *stages = smem + 256;
     unsigned char *obuf = stages + a.S * a.stage_bytes + 128;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < a.S; ++s) {
             mbar_init(&full[s], 1);
+            mbar_init(&ready[s], 32);
             mbar_init(&empty[s], kFusedConsumerWarps);
         }
         mbar_fence_init();
@@ -144,57 +182,74 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
-        if (lane != 0) return;
         const uint64_t pol = policy_evict_first();
-        int slot = 0;
-        uint32_t phase = 0, nfill = 0;
-        for (int task = blockIdx.x; task < a.ntasks; task += gridDim.x) {
-            const FusedTask t = fused_decode<P, Q, TAPS, LO, K, ESZ>(a, task);
-            const int nst = (C > 0 ? 1 : 0) + (t.iy1 - t.iy0);
-            const uint32_t seg_bytes = (uint32_t)(t.a1 - t.a0) * ESZ;
-            const bool whole_rows = (t.a0 == 0) && (t.a1 == a.W) && ((int)seg_bytes == a.seg_pitch);
-            for (int k = 0; k < nst; ++k) {
-                if (nfill >= (uint32_t)a.S) mbar_wait(&empty[slot], phase ^ 1);
-                int vf, nr;
-                if (C > 0 && k == 0) {
-                    vf = Q * t.iy0 + LO;
-                    nr = C;
-                } else {
-                    const int iy = t.iy0 + k - (C > 0 ? 1 : 0);
-                    vf = Q * iy + LO + C;
-                    nr = F;
-                }
-                unsigned char *sbase = stages + slot * a.stage_bytes;
-                for (int pl = 0; pl < a.NP; ++pl) {
-                    const int plane = t.group * a.NP + pl;
-                    if (plane >= a.planes) break;
-                    const T *pin = static_cast<const T *>(a.in) + (int64_t)plane * a.in_plane_stride;
-                    int r = 0;
-                    while (r < nr) {
-                        const int v = vf + r;
-                        if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) { ++r; continue; }
-                        // rows outside the window only feed masked outputs: clamp
-                        const int src = min(max(pad_src32(v, a.H, a.pad) - a.in_row0, 0), a.in_nrows - 1);
-                        int run = 1;
-                        if (whole_rows) {
-                            while (r + run < nr) {
-                                const int v2 = v + run;
-                                if (v2 < 0 || v2 >= a.H) break;
-                                if (min(max(v2 - a.in_row0, 0), a.in_nrows - 1) != src + run) break;
-                                ++run;
-                            }
-                        }
-                        const uint32_t bytes = seg_bytes * run;
-                        mbar_expect_tx(&full[slot], bytes);
-                        bulk_g2s(sbase + (pl * a.SR + r) * a.seg_pitch, pin + (int64_t)src * a.W + t.a0, bytes,
-                                 &full[slot], pol);
-                        r += run;
+        StageCursor<P, Q, TAPS, LO, K, ESZ> ci, cf;  // issue cursor runs ahead of the fix-up cursor
+        ci.start(a);
+        cf.start(a);
+        while (cf.task < a.ntasks) {
+            // issue bulk loads up to S stages ahead of the oldest unfinished stage
+            while (ci.task < a.ntasks && ci.seq < cf.seq + (uint32_t)a.S) {
+                if (ci.seq >= (uint32_t)a.S) {
+                    if (ci.seq == cf.seq) {
+                        mbar_wait(&empty[ci.slot], ci.phase ^ 1);
+                    } else {
+                        bool free_slot = lane == 0 ? mbar_test(&empty[ci.slot], ci.phase ^ 1) : false;
+                        if (!__shfl_sync(0xffffffffu, free_slot, 0)) break;
                     }
                 }
-                mbar_arrive(&full[slot]);
-                ++nfill;
-                if (++slot == a.S) { slot = 0; phase ^= 1; }
+                if (lane == 0) {
+                    const FusedTask &t = ci.t;
+                    int vf, nr;
+                    ci.rows(vf, nr);
+                    const uint32_t seg_bytes = (uint32_t)(t.a1 - t.a0) * ESZ;
+                    unsigned char *sbase = stages + ci.slot * a.stage_bytes + A * ESZ;
+                    for (int pl = 0; pl < a.NP; ++pl) {
+                        const int plane = t.group * a.NP + pl;
+                        if (plane >= a.planes) break;
+                        const T *pin = static_cast<const T *>(a.in) + (int64_t)plane * a.in_plane_stride + t.a0;
+                        for (int r = 0; r < nr; ++r) {
+                            const int v = vf + r;
+                            if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;
+                            // rows outside the window only feed masked outputs: clamp
+                            const int src = min(max(pad_src32(v, a.H, a.pad) - a.in_row0, 0), a.in_nrows - 1);
+                            mbar_expect_tx(&full[ci.slot], seg_bytes);
+                            bulk_g2s(sbase + (pl * a.SR + r) * a.seg_pitch, pin + (int64_t)src * a.W, seg_bytes,
+                                     &full[ci.slot], pol);
+                        }
+                    }
+                    mbar_arrive(&full[ci.slot]);
+                }
+                __syncwarp();
+                ci.next(a);
             }
+            // the oldest stage: wait for its bytes, write the padding columns, release it
+            mbar_wait(&full[cf.slot], cf.phase);
+            {
+                const FusedTask &t = cf.t;
+                const int lpad = t.a0 == 0 ? -LO : 0;             // left padding columns
+                const int rpad = t.a1 == a.W ? a.rpad : 0;         // right padding columns
+                const int cells = lpad + rpad;
+                if (cells > 0) {
+                    int vf, nr;
+                    cf.rows(vf, nr);
+                    const int npl = min(a.NP, a.planes - t.group * a.NP);
+                    unsigned char *sbase = stages + cf.slot * a.stage_bytes;
+                    const int total = npl * nr * cells;
+                    for (int u = lane; u < total; u += 32) {
+                        const int cell = u % cells;
+                        const int rr = u / cells;
+                        const int r = rr % nr, pl = rr / nr;
+                        const int v = vf + r;
+                        if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;
+                        T *row = reinterpret_cast<T *>(sbase + (pl * a.SR + r) * a.seg_pitch);
+                        const int c = cell < lpad ? -1 - cell : a.W + (cell - lpad);  // virtual column
+                        const int s = pad_src32(c, a.W, a.pad);
+                        row[A + c - t.a0] = s < 0 ? DT<T>::from_f(0.0f) : row[A + min(max(s, t.a0), t.a1 - 1) - t.a0];
+                    }
+                }
+            }
+            mbar_arrive(&ready[cf.slot]);
+            cf.next(a);
         }
         return;
     }
@@ -209,28 +264,11 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     int ob = 0;
     for (int task = blockIdx.x; task < a.ntasks; task += gridDim.x) {
         const FusedTask t = fused_decode<P, Q, TAPS, LO, K, ESZ>(a, task);
-        // thread -> (plane, chunk), chunks that touch the border first
-        const int ilo = max(t.ch0, a.c_lo_int);
-        const int ihi = max(ilo, min(t.ch1, a.c_first_bad));
-        const int nL = max(0, min(ilo, t.ch1) - t.ch0);
-        const int rstart = max(ihi, t.ch0);
-        const int nR = max(0, t.ch1 - rstart);
-        const int E = nL + nR;
-        const int I = (t.ch1 - t.ch0) - E;
-        int pl, chunk;
-        if (ctid < a.NP * E) {
-            pl = ctid / E;
-            const int e = ctid - pl * E;
-            chunk = e < nL ? t.ch0 + e : rstart + (e - nL);
-        } else {
-            const int j = ctid - a.NP * E;
-            pl = I > 0 ? j / I : a.NP;
-            chunk = ilo + (j - pl * I);
-        }
+        const int pl = ctid / a.CPT;
+        const int chunk = t.ch0 + (ctid - pl * a.CPT);
         const int plane = t.group * a.NP + pl;
-        const bool active = (pl < a.NP) && (plane < a.planes);
-        const int ws = chunk * K * Q + LO;
-        const bool fast = ws >= t.a0 && ws + WIN <= t.a1;
+        const bool active = (pl < a.NP) && (plane < a.planes) && (chunk < t.ch1);
+        const int e0 = A + chunk * K * Q + LO - t.a0;  // window start (element) in a shared row
         const int col = chunk * KP;
         const bool full_chunk = col + KP <= t.c1;
         const int in_off = pl * a.SR * a.seg_pitch;
@@ -243,9 +281,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 return;
             }
             float win[WIN];
-            const T *s = reinterpret_cast<const T *>(srow);
-            if (fast) load_fast<T, WIN>(s, ws - t.a0, win);
-            else load_padded<T, WIN>(s, t.a0, t.a1, ws, a.W, a.pad, win);
+            load_win<T, WIN>(reinterpret_cast<const T *>(srow), e0, win);
 #pragma unroll
             for (int k = 0; k < K; ++k) {
 #pragma unroll
@@ -265,7 +301,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         };
 
         if constexpr (C > 0) {  // warm-up: the first C window rows of the first period
-            mbar_wait(&full[slot], phase);
+            mbar_wait(&ready[slot], phase);
             if (active) {
                 const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
 #pragma unroll
@@ -285,7 +321,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                         for (int c = 0; c < KP; ++c) h[i][c] = h[Q + i][c];
                 }
             }
-            mbar_wait(&full[slot], phase);
+            mbar_wait(&ready[slot], phase);
             if (active) {
                 const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
 #pragma unroll

@@ -28,25 +28,32 @@ __global__ void __launch_bounds__(256) fcfs_nearest_kernel(const __grid_constant
     const int dq = (int)(((int64_t)step * q) / p), dr = (int)(((int64_t)step * q) % p);
     const T *__restrict__ in = static_cast<const T *>(g.in);
     T *__restrict__ out = static_cast<T *>(g.out);
+    // source column and remainder of each lane's first output of the U sub-slots
+    // (row independent: computed once)
+    int bx0[U], rem0[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint32_t mq = (uint32_t)(lane + 32 * u) * (uint32_t)q;
+        bx0[u] = (int)fdiv(mq, a.div_p);
+        rem0[u] = (int)(mq - (uint32_t)bx0[u] * (uint32_t)p);
+    }
     for (int64_t rw = warp0; rw < nrows_total; rw += nwarps) {
-        const int64_t plane = rw / g.out_nrows;
-        const int64_t lr = rw - plane * g.out_nrows;
-        const int64_t my = g.out_row0 + lr;
-        const int64_t by = a.is1d ? my : (my * q) / p;
-        const int64_t rs = pad_src(by, H, a.pad);
-        T *orow = out + plane * g.out_plane_stride + lr * Wo;
+        const uint32_t plane = fdiv((uint32_t)rw, a.div_rows);
+        const uint32_t lr = (uint32_t)rw - plane * (uint32_t)g.out_nrows;
+        const uint32_t my = (uint32_t)g.out_row0 + lr;
+        const int32_t by = a.is1d ? (int32_t)my : (int32_t)fdiv(my * (uint32_t)q, a.div_p);
+        const int32_t rs = pad_src32(by, H, a.pad);
+        T *orow = out + (int64_t)plane * g.out_plane_stride + (int64_t)lr * Wo;
         if (rs < 0) {  // a zero-padding row
             for (int mx = lane; mx < Wo; mx += 32) orow[mx] = DT<T>::from_f(0.0f);
             continue;
         }
-        const T *irow = in + plane * g.in_plane_stride + (rs - g.in_row0) * W;
-        // source column and remainder of the first output of each of the U sub-slots
+        const T *irow = in + (int64_t)plane * g.in_plane_stride + (int64_t)(rs - g.in_row0) * W;
         int bx[U], rem[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int mx = lane + 32 * u;
-            bx[u] = (int)(((int64_t)mx * q) / p);
-            rem[u] = (int)(((int64_t)mx * q) % p);
+            bx[u] = bx0[u];
+            rem[u] = rem0[u];
         }
         for (int mx0 = 0; mx0 < Wo; mx0 += step) {
             T v[U];
@@ -81,9 +88,9 @@ int launch_nearest(int dtype, const NearestArgs &a, void *stream) {
     if (blocks > 148 * 8 * 4) blocks = 148 * 8 * 4;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     switch (dtype) {
-    case FCFS_F32: fcfs_nearest_kernel<float, 4><<<(int)blocks, 256, 0, s>>>(a); break;
-    case FCFS_F16: fcfs_nearest_kernel<__half, 4><<<(int)blocks, 256, 0, s>>>(a); break;
-    default: fcfs_nearest_kernel<__nv_bfloat16, 4><<<(int)blocks, 256, 0, s>>>(a); break;
+    case FCFS_F32: fcfs_nearest_kernel<float, 8><<<(int)blocks, 256, 0, s>>>(a); break;
+    case FCFS_F16: fcfs_nearest_kernel<__half, 8><<<(int)blocks, 256, 0, s>>>(a); break;
+    default: fcfs_nearest_kernel<__nv_bfloat16, 8><<<(int)blocks, 256, 0, s>>>(a); break;
     }
     return (int)cudaGetLastError();
 }

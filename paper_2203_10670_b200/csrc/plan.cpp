@@ -182,15 +182,14 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     a.SR = std::max(Ff, Cc);
     {  // chunks whose column window reaches the left / right padding
         const int WIN = (K - 1) * Q + Lw;
-        a.c_lo_int = LO < 0 ? 1 : 0;
-        const int64_t room = g.W - WIN - LO;
-        int64_t cfb = room < 0 ? 0 : room / (K * Q) + 1;
-        a.c_first_bad = (int32_t)std::min<int64_t>(std::max<int64_t>(cfb, a.c_lo_int), a.nch);
+        const int64_t reach = (int64_t)(a.nch - 1) * K * Q + LO + WIN;  // one past the last window column
+        a.rpad = (int32_t)std::max<int64_t>(0, reach - g.W);
     }
     const int budget = 110 * 1024;  // two CTAs per SM
+    // shared row: [A-element margin][loaded columns][right padding], 16-B multiple
     auto seg_pitch_for = [&](int cpt) {
         int64_t elems = std::min<int64_t>(g.W, (int64_t)cpt * K * Q - Q + Lw + 2 * A);
-        elems = (elems + A - 1) / A * A;
+        elems = (elems + A - 1) / A * A + A + (a.rpad + A - 1) / A * A;
         return (int)(elems * ESZ);
     };
     int S = 0;
@@ -222,7 +221,7 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
             a.out_pitch = ((a.CPT * KP * ESZ + 16) + 15) / 16 * 16;
             a.obuf_bytes = a.NP * P * a.out_pitch;
         }
-        const int fixed = 128 + 128 + 2 * a.obuf_bytes;
+        const int fixed = 256 + 128 + 2 * a.obuf_bytes;
         S = std::min(8, (budget - fixed) / std::max(1, a.stage_bytes));
         if (S >= 3 || (S >= 2 && a.CPT <= 16)) break;
     }
@@ -255,8 +254,8 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
                      "seg_pitch=%d stage=%d out_pitch=%d obuf=%d nper=%d PB=%d nbands=%d ntasks=%d grid=%d smem=%d\n",
                      P, Q, TAPS, K, a.full_width, a.NP, a.CPT, a.nch, a.ntile, a.ngroups, a.S, a.SR, a.seg_pitch,
                      a.stage_bytes, a.out_pitch, a.obuf_bytes, nper, a.PB, a.nbands, a.ntasks, L.grid,
-                     128 + a.S * a.stage_bytes + 128 + 2 * a.obuf_bytes);
-    L.smem = 128 + a.S * a.stage_bytes + 128 + 2 * a.obuf_bytes;
+                     256 + a.S * a.stage_bytes + 128 + 2 * a.obuf_bytes);
+    L.smem = 256 + a.S * a.stage_bytes + 128 + 2 * a.obuf_bytes;
     return true;
 }
 
@@ -304,6 +303,7 @@ fcfs_status run_window(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t 
     int kernel = pl->kernel;
     const int64_t total = planes * out_nrows * pl->Wo;
     (void)total;
+    if (kernel == 1 && (planes * out_nrows >= INT32_MAX || pl->Ho * pl->q >= INT32_MAX)) kernel = 0;  // 32-bit index math
     if (kernel == 2) {
         if ((reinterpret_cast<uintptr_t>(in) & 15) || planes * std::max(in_nrows * pl->W, out_nrows * pl->Wo) > INT32_MAX * 16LL)
             kernel = 0;

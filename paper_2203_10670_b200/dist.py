@@ -41,6 +41,8 @@ class StripLayout:
     sends: list
     recvs: list
     interior: tuple  # output rows computable from own rows only [i0, i1)
+    loc0: int = 0    # the local buffer holds input rows [loc0, loc1) = own rows + halo
+    loc1: int = 0
 
 
 def own_rows(H: int, rank: int, world: int):
@@ -76,7 +78,9 @@ def strip_layout(plan, rank: int, world: int) -> StripLayout:
             i0 += 1
         while i1 > i0 and not _inside(plan, i1 - 1, i1, own0, own1):
             i1 -= 1
-    return StripLayout(rank, world, own0, own1, out0, out1, need0, need1, sends, recvs, (i0, i1))
+    loc0 = min(own0, need0) if out1 > out0 else own0
+    loc1 = max(own1, need1) if out1 > out0 else own1
+    return StripLayout(rank, world, own0, own1, out0, out1, need0, need1, sends, recvs, (i0, i1), loc0, loc1)
 
 
 def _inside(plan, m0, m1, own0, own1) -> bool:
@@ -90,14 +94,14 @@ def exchange(local, lay: StripLayout, group=None):
     import torch.distributed as dist
     ops, keep = [], []
     for t in lay.sends:
-        buf = local[:, :, t.row0 - lay.need0:t.row1 - lay.need0]
+        buf = local[:, :, t.row0 - lay.loc0:t.row1 - lay.loc0]
         if not buf.is_contiguous():
             buf = buf.contiguous()
             keep.append(buf)
         ops.append(dist.P2POp(dist.isend, buf, t.peer, group))
     staged = []
     for t in lay.recvs:
-        view = local[:, :, t.row0 - lay.need0:t.row1 - lay.need0]
+        view = local[:, :, t.row0 - lay.loc0:t.row1 - lay.loc0]
         buf = view if view.is_contiguous() else view.new_empty(view.shape)
         if buf is not view:
             staged.append((view, buf))
@@ -123,11 +127,11 @@ class StripRunner:
     def alloc_local(self, N: int, dtype, device):
         import torch
         lay = self.lay
-        return torch.empty((N, self.plan.C, max(1, lay.need1 - lay.need0), self.plan.W), dtype=dtype, device=device)
+        return torch.empty((N, self.plan.C, max(1, lay.loc1 - lay.loc0), self.plan.W), dtype=dtype, device=device)
 
     def own_view(self, local):
         lay = self.lay
-        return local[:, :, lay.own0 - lay.need0:lay.own1 - lay.need0]
+        return local[:, :, lay.own0 - lay.loc0:lay.own1 - lay.loc0]
 
     def alloc_out(self, N: int, dtype, device):
         import torch
@@ -160,9 +164,9 @@ class StripRunner:
         lay, pl = self.lay, self.plan
         dst = out[:, :, m0 - lay.out0:m1 - lay.out0]
         if dst.is_contiguous():
-            pl.run_rows(local, lay.need0, m0, m1 - m0, out=dst)
+            pl.run_rows(local, lay.loc0, m0, m1 - m0, out=dst)
         else:
-            tmp = pl.run_rows(local, lay.need0, m0, m1 - m0)
+            tmp = pl.run_rows(local, lay.loc0, m0, m1 - m0)
             dst.copy_(tmp)
 
 
@@ -223,7 +227,7 @@ def bench_strips(args, cfg, rank, world, dev, metric):
     ms_step = ms / args.steps
     peak, kind = peaks()
     # per-rank algorithmic bytes: own output rows + own + halo input rows
-    rank_bytes = ((lay.out1 - lay.out0) * pl.Wo + (lay.need1 - lay.need0) * pl.W) * 4
+    rank_bytes = ((lay.out1 - lay.out0) * pl.Wo + (lay.loc1 - lay.loc0) * pl.W) * 4
     achieved = rank_bytes / (ms_step * 1e-3) / 1e9
     line = {"metric": metric, "value": outputs * args.steps / (ms * 1e-3) / 1e6, "unit": "Mpix/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,

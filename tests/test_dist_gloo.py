@@ -1,0 +1,98 @@
+"""Multi-process (gloo, CPU) tests of the row-strip driver's host logic: strip
+ownership, which halo rows travel where, the exchange itself
+(batch_isend_irecv), and that each rank's strip -- evaluated by the oracle
+from its local rows only -- equals the whole-image result."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+CASES = [  # (p, q, mode, pad, H, W, N, C)
+    (3, 5, "bicubic", "replicate", 97, 40, 1, 1),
+    (5, 3, "bicubic", "reflect", 61, 24, 1, 2),
+    (7, 5, "bilinear", "zero", 50, 32, 2, 1),
+    (4, 7, "bilinear", "replicate", 83, 16, 1, 1),
+]
+
+
+def _worker(rank, world, port, case, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import synth
+        import paper_2203_10670_b200 as fc
+        from paper_2203_10670_b200.dist import exchange, finish_exchange, strip_layout
+        p, q, mode, pad, H, W, N, C = case
+        pl = fc.Plan(p, q, mode, pad, C, H, W, "float32", "floor")
+        lay = strip_layout(pl, rank, world)
+        cfg = synth.Config("strip", N, C, H, W, "float32", "uniform", p, q, mode, pad, seed=4242)
+        full = synth.make_values(cfg)
+        own = synth.make_values(cfg, rows=(lay.own0, lay.own1))
+        local = torch.full((N, C, max(1, lay.loc1 - lay.loc0), W), float("nan"))
+        local[:, :, lay.own0 - lay.loc0:lay.own1 - lay.loc0] = torch.from_numpy(own)
+        works, staged = exchange(local, lay)
+        finish_exchange(works, staged)
+        res = {"rank": rank, "ok": True, "msg": ""}
+        if lay.loc1 > lay.loc0:
+            if not np.array_equal(local.numpy(), full[:, :, lay.loc0:lay.loc1]):
+                res.update(ok=False, msg="halo rows differ")
+        if lay.out1 > lay.out0 and res["ok"]:
+            mine = oracle.direct(local.numpy(), p, q, mode, pad, floor_extent=True, rows=(lay.out0, lay.out1),
+                                 H=H, row0=lay.loc0)
+            whole = oracle.direct(full, p, q, mode, pad, floor_extent=True)[:, :, lay.out0:lay.out1]
+            if not np.array_equal(mine, whole):
+                res.update(ok=False, msg="strip output differs")
+            i0, i1 = lay.interior
+            if i1 > i0:  # the interior needs only own rows
+                own_only = oracle.direct(own, p, q, mode, pad, floor_extent=True, rows=(i0, i1), H=H,
+                                         row0=lay.own0)
+                if not np.array_equal(own_only, whole[:, :, i0 - lay.out0:i1 - lay.out0]):
+                    res.update(ok=False, msg="interior differs")
+        res["out"] = (lay.out0, lay.out1)
+        res["sent"] = [(t.peer, t.row0, t.row1) for t in lay.sends]
+        out_q.put(res)
+    except Exception as e:  # report, do not hang the peers
+        out_q.put({"rank": rank, "ok": False, "msg": repr(e)})
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", CASES)
+def test_strip_exchange_gloo(world, case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    results = [q.get(timeout=180) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+    for r in results:
+        assert r["ok"], r
+    # the strips partition the output rows
+    spans = sorted(r["out"] for r in results)
+    H, p, q_ = case[4], case[0], case[1]
+    assert spans[0][0] == 0
+    for a, b in zip(spans, spans[1:]):
+        assert a[1] == b[0]
+    # every halo message is at most 2 rows (bicubic reach) and goes to a neighbour
+    for r in results:
+        for peer, r0, r1 in r["sent"]:
+            assert abs(peer - r["rank"]) == 1 and 0 < r1 - r0 <= 2
