@@ -3,34 +3,31 @@
 // p^2-channel hidden layer of §3.1.1 lives only in registers.
 //
 // Structure:
-//   * warp 0 is the producer.  Lane 0 streams the input rows of each task into
-//     a ring of S shared-memory stages with 1D bulk async copies (TMA engine,
-//     cp.async.bulk + mbarrier complete_tx, L2 evict_first), running up to S
-//     stages ahead.  When a stage has landed the whole warp materialises the
-//     padding columns (§3 Padding) in the row margins, then
-//     releases the stage to the consumers.  A stage holds the fresh rows of one
-//     y-period (Q new input rows) of every plane of the task.
+//   * warp 0 is the producer.  Its lanes (one per plane of the task) stream
+//     the input rows into a ring of S shared-memory stages with 1D bulk async
+//     copies (TMA engine, cp.async.bulk + mbarrier complete_tx, L2
+//     evict_first), running up to S stages ahead.  When a stage has landed the
+//     warp writes the padding columns (§3 Padding) into the row
+//     margins and releases the stage.  A stage holds the fresh input rows of
+//     one y-period (the rows that P output rows add) of every plane.
 //   * warps 1..8 are consumers: thread (pl, c) owns column chunk c (K
-//     x-periods = K*P outputs) of plane pl and walks down the rows.  Per
-//     y-period (P output rows) it
-//       - horizontally filters the F fresh input rows of the period window
-//         into registers h[L][K*P] (rows shared with the previous period are
-//         carried in registers, not recomputed),
-//       - vertically filters h into P output rows,
-//       - rounds to the dtype and stores them into a shared staging buffer laid
-//         out exactly like the contiguous global span, co-aligned mod 16;
-//     after one named barrier the 16-B-aligned body of every span leaves with a
-//     bulk async store (TMA engine) and a few threads write the unaligned
-//     head/tail elements -- coalesced whatever the row pitch, double-buffered.
-//     Every consumer runs the same branch-free path (padding is already in
-//     shared memory).
-//   * Period/phase structure is compile time (P, Q, TAPS, LO template
-//     parameters), so every weight index is static and the weights are
-//     constant-bank operands of the FMAs.
+//     x-periods = K*P outputs) of plane pl and walks down the rows.  It filters
+//     each fresh window row horizontally into a register ring of TAPS rows and,
+//     as soon as the last tap row of an output row is in the ring, filters that
+//     output row vertically, rounds it and stores it into a shared staging
+//     buffer laid out exactly like the contiguous global span (co-aligned mod
+//     16).  After one named barrier per y-period the 16-B-aligned body of every
+//     span leaves with a bulk async store (TMA engine) and a few threads write
+//     the unaligned head/tail elements -- coalesced whatever the row pitch,
+//     double-buffered.  All consumers run the same branch-free code.
+//   * Period/phase/tap structure is compile time (P, Q, TAPS, LO, K template
+//     parameters): weights are constant-bank operands of the FMAs and every
+//     register index is static.  K = 2 for 16-bit data with odd q makes the
+//     per-thread column stride an odd number of words (conflict-free shared
+//     loads) and the element parity of every window a compile-time constant.
 //
 // Shared row layout: [A margin elements][loaded columns a0..a1)][rpad margin],
-// A = 16 B / element size.  Virtual column c of the row lives at element
-// A + c - a0.
+// A = 16 B / element size.  Virtual column c lives at element A + c - a0.
 //
 // Arithmetic is exactly the reference kernel's (k_reference.cu): identical
 // fp32 operation sequence per output, so both kernels agree bit for bit.
@@ -46,6 +43,8 @@ struct Geo {
     static constexpr int L = HI - LO + 1;                          // window rows/cols of one period
     static constexpr int C = L > Q ? L - Q : 0;                    // rows carried to the next period
     static constexpr int F = L - C;                                // fresh rows per period
+    // window row after which output row j of the period is complete
+    static __host__ __device__ constexpr int last_row(int j) { return j == 0 ? -LO : base(j) + TAPS - 1; }
 };
 
 template <typename T> struct HalfBits;
@@ -57,7 +56,8 @@ template <> struct HalfBits<__nv_bfloat16> {
 };
 
 // Load WIN consecutive elements starting at element e0 of a shared row.
-template <typename T, int WIN>
+// PAR: parity of e0 when known at compile time (16-bit types), else -1.
+template <typename T, int WIN, int PAR>
 __device__ __forceinline__ void load_win(const T *s, int e0, float (&win)[WIN]) {
     if constexpr (sizeof(T) == 4) {
 #pragma unroll
@@ -65,10 +65,10 @@ __device__ __forceinline__ void load_win(const T *s, int e0, float (&win)[WIN]) 
     } else {
         constexpr int NWD = (WIN + 2) / 2;
         const uint32_t *wp = reinterpret_cast<const uint32_t *>(s) + (e0 >> 1);
-        const bool odd = e0 & 1;
         uint32_t wd[NWD];
 #pragma unroll
         for (int k = 0; k < NWD; ++k) wd[k] = wp[k];
+        const bool odd = PAR < 0 ? (e0 & 1) : PAR == 1;
 #pragma unroll
         for (int i = 0; i < WIN; ++i) {
             uint32_t b0 = (i & 1) ? (wd[i >> 1] >> 16) : (wd[i >> 1] & 0xffffu);
@@ -153,12 +153,14 @@ struct StageCursor {
 template <typename T, int P, int Q, int TAPS, int LO, int K>
 __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __grid_constant__ FusedArgs a) {
     using G = Geo<P, Q, TAPS, LO>;
-    constexpr int L = G::L, C = G::C, F = G::F;
+    constexpr int L = G::L, C = G::C;
     constexpr int KP = K * P;
     constexpr int WIN = (K - 1) * Q + L;
     constexpr int ESZ = sizeof(T);
     constexpr int A = 16 / ESZ;  // left margin (elements)
     constexpr int NCT = 32 * kFusedConsumerWarps;
+    // element parity of every window start (16-bit types), when it is static
+    constexpr int PAR = (ESZ == 2 && (K * Q) % 2 == 0) ? ((LO % 2 + 2) % 2) : -1;
     static_assert(P <= 16, "fused variants have p <= 16");
     static_assert(-LO <= A, "left margin too small");
 
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         ci.start(a);
         cf.start(a);
         while (cf.task < a.ntasks) {
-            // issue bulk loads up to S stages ahead of the oldest unfinished stage
+            // issue bulk loads up to S stages ahead of the oldest unreleased stage
             while (ci.task < a.ntasks && ci.seq < cf.seq + (uint32_t)a.S) {
                 if (ci.seq >= (uint32_t)a.S) {
                     if (ci.seq == cf.seq) {
@@ -197,27 +199,26 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                         if (!__shfl_sync(0xffffffffu, free_slot, 0)) break;
                     }
                 }
-                if (lane == 0) {
-                    const FusedTask &t = ci.t;
-                    int vf, nr;
-                    ci.rows(vf, nr);
-                    const uint32_t seg_bytes = (uint32_t)(t.a1 - t.a0) * ESZ;
-                    unsigned char *sbase = stages + ci.slot * a.stage_bytes + A * ESZ;
-                    for (int pl = 0; pl < a.NP; ++pl) {
-                        const int plane = t.group * a.NP + pl;
-                        if (plane >= a.planes) break;
-                        const T *pin = static_cast<const T *>(a.in) + (int64_t)plane * a.in_plane_stride + t.a0;
-                        for (int r = 0; r < nr; ++r) {
-                            const int v = vf + r;
-                            if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;
-                            // rows outside the window only feed masked outputs: clamp
-                            const int src = min(max(pad_src32(v, a.H, a.pad) - a.in_row0, 0), a.in_nrows - 1);
-                            mbar_expect_tx(&full[ci.slot], seg_bytes);
-                            bulk_g2s(sbase + (pl * a.SR + r) * a.seg_pitch, pin + (int64_t)src * a.W, seg_bytes,
-                                     &full[ci.slot], pol);
-                        }
+                const FusedTask &t = ci.t;
+                int vf, nr;
+                ci.rows(vf, nr);
+                const uint32_t seg_bytes = (uint32_t)(t.a1 - t.a0) * ESZ;
+                const int npl = min(a.NP, a.planes - t.group * a.NP);
+                int nreal = 0;  // rows that are not zero padding
+                for (int r = 0; r < nr; ++r) nreal += !(a.pad == FCFS_PAD_ZERO && (vf + r < 0 || vf + r >= a.H));
+                if (lane == 0) mbar_arrive_expect_tx(&full[ci.slot], seg_bytes * (uint32_t)(nreal * npl));
+                __syncwarp();
+                for (int pl = lane; pl < npl; pl += 32) {  // one lane per plane issues its rows
+                    const T *pin = static_cast<const T *>(a.in) +
+                                   (int64_t)(t.group * a.NP + pl) * a.in_plane_stride + t.a0;
+                    unsigned char *sbase = stages + ci.slot * a.stage_bytes + A * ESZ + pl * a.SR * a.seg_pitch;
+                    for (int r = 0; r < nr; ++r) {
+                        const int v = vf + r;
+                        if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;
+                        // rows outside the window only feed masked outputs: clamp
+                        const int src = min(max(pad_src32(v, a.H, a.pad) - a.in_row0, 0), a.in_nrows - 1);
+                        bulk_g2s(sbase + r * a.seg_pitch, pin + (int64_t)src * a.W, seg_bytes, &full[ci.slot], pol);
                     }
-                    mbar_arrive(&full[ci.slot]);
                 }
                 __syncwarp();
                 ci.next(a);
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     const int ctid = threadIdx.x - 32;
     const int span_id = ctid >> 4, span_e = ctid & 15;  // copy-out roles
     const int rowb = a.Wo * ESZ;
-    float h[L][KP];
+    float hr[TAPS][KP];  // ring: window row r lives in hr[r % TAPS]
     int slot = 0;
     uint32_t phase = 0;
     int ob = 0;
@@ -274,14 +275,15 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         const int in_off = pl * a.SR * a.seg_pitch;
         const int64_t plane_out = (int64_t)plane * a.out_plane_stride;
 
-        auto row_h = [&](float(&hr)[KP], int v, const unsigned char *srow) {
+        // horizontal taps of one window row into a ring slot
+        auto row_h = [&](float(&h)[KP], int v, const unsigned char *srow) {
             if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) {
 #pragma unroll
-                for (int c = 0; c < KP; ++c) hr[c] = 0.0f;
+                for (int c = 0; c < KP; ++c) h[c] = 0.0f;
                 return;
             }
             float win[WIN];
-            load_win<T, WIN>(reinterpret_cast<const T *>(srow), e0, win);
+            load_win<T, WIN, PAR>(reinterpret_cast<const T *>(srow), e0, win);
 #pragma unroll
             for (int k = 0; k < K; ++k) {
 #pragma unroll
@@ -295,17 +297,17 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
 #pragma unroll
                         for (int tp = 1; tp < TAPS; ++tp) v2 = __fmaf_rn(a.w[jx][tp], win[b + tp], v2);
                     }
-                    hr[k * P + jx] = v2;
+                    h[k * P + jx] = v2;
                 }
             }
         };
 
-        if constexpr (C > 0) {  // warm-up: the first C window rows of the first period
+        if constexpr (C > 0) {  // warm-up: window rows 0..C-1 of the first period
             mbar_wait(&ready[slot], phase);
             if (active) {
                 const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
 #pragma unroll
-                for (int i = 0; i < C; ++i) row_h(h[i], Q * t.iy0 + LO + i, sb + i * a.seg_pitch);
+                for (int i = 0; i < C; ++i) row_h(hr[i % TAPS], Q * t.iy0 + LO + i, sb + i * a.seg_pitch);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
@@ -313,76 +315,90 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         }
 
         for (int iy = t.iy0; iy < t.iy1; ++iy) {
-            if constexpr (C > 0) {
-                if (iy > t.iy0) {
+            const int mfirst = max(iy * P, t.my_lo), mlast = min(iy * P + P, t.my_hi);
+            unsigned char *ob_base = obuf + ob * a.obuf_bytes;
+            // staging address of (output row iy*P, column `col`) for this thread
+            unsigned char *sp;
+            int jy_step;
+            if (a.full_width) {
+                const uintptr_t g = reinterpret_cast<uintptr_t>(static_cast<T *>(a.out) + plane_out +
+                                                                (int64_t)(mfirst - a.out_row0) * a.Wo);
+                sp = ob_base + pl * a.out_pitch + (g & 15) + (iy * P - mfirst) * rowb + col * ESZ;
+                jy_step = rowb;
+            } else {
+                sp = ob_base + (col - t.c0) * ESZ;
+                jy_step = a.out_pitch;
+            }
+            // vertical taps of output row jy (its tap rows are in the ring) -> staging
+            auto emit = [&](int jy) {
+                const int my = iy * P + jy;
+                if (my < mfirst || my >= mlast) return;
+                float o[KP];
+                if (jy == 0) {
 #pragma unroll
-                    for (int i = 0; i < C; ++i)
+                    for (int c = 0; c < KP; ++c) o[c] = hr[(-LO) % TAPS][c];
+                } else {
+                    const int b = G::base(jy);
 #pragma unroll
-                        for (int c = 0; c < KP; ++c) h[i][c] = h[Q + i][c];
+                    for (int c = 0; c < KP; ++c) {
+                        float v2 = __fmul_rn(a.w[jy][0], hr[b % TAPS][c]);
+#pragma unroll
+                        for (int tp = 1; tp < TAPS; ++tp) v2 = __fmaf_rn(a.w[jy][tp], hr[(b + tp) % TAPS][c], v2);
+                        o[c] = v2;
+                    }
                 }
+                T *sr;
+                if (a.full_width) {
+                    sr = reinterpret_cast<T *>(sp + jy * jy_step);
+                } else {
+                    const uintptr_t g = reinterpret_cast<uintptr_t>(static_cast<T *>(a.out) + plane_out +
+                                                                    (int64_t)(my - a.out_row0) * a.Wo + t.c0);
+                    sr = reinterpret_cast<T *>(sp + jy * jy_step + (g & 15));
+                }
+                if (full_chunk) {
+#pragma unroll
+                    for (int c = 0; c < KP; ++c) sr[c] = DT<T>::from_f(o[c]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < KP; ++c)
+                        if (col + c < t.c1) sr[c] = DT<T>::from_f(o[c]);
+                }
+            };
+
+            if (active) {
+                // output rows complete with the carried rows alone
+#pragma unroll
+                for (int jy = 0; jy < P; ++jy)
+                    if (G::last_row(jy) < C) emit(jy);
             }
             mbar_wait(&ready[slot], phase);
             if (active) {
                 const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
 #pragma unroll
-                for (int i = 0; i < F; ++i) row_h(h[C + i], Q * iy + LO + C + i, sb + i * a.seg_pitch);
+                for (int r = C; r < L; ++r) {
+                    row_h(hr[r % TAPS], Q * iy + LO + r, sb + (r - C) * a.seg_pitch);
+#pragma unroll
+                    for (int jy = 0; jy < P; ++jy)
+                        if (G::last_row(jy) == r) emit(jy);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
             if (++slot == a.S) { slot = 0; phase ^= 1; }
-
-            const int mfirst = max(iy * P, t.my_lo), mlast = min(iy * P + P, t.my_hi);
-            unsigned char *ob_base = obuf + ob * a.obuf_bytes;
-            if (active) {
-                // staging address of (row iy*P, column `col`) for this thread
-                unsigned char *sp;
-                int jy_step;
-                if (a.full_width) {
-                    const uintptr_t g = reinterpret_cast<uintptr_t>(static_cast<T *>(a.out) + plane_out +
-                                                                    (int64_t)(mfirst - a.out_row0) * a.Wo);
-                    sp = ob_base + pl * a.out_pitch + (g & 15) + (iy * P - mfirst) * rowb + col * ESZ;
-                    jy_step = rowb;
-                } else {
-                    sp = ob_base + (col - t.c0) * ESZ;
-                    jy_step = a.out_pitch;
+            if constexpr (C > 0) {  // carry window rows Q..L-1 -> rows 0..C-1 of the next period
+                if ((Q % TAPS) != 0) {
+                    float tmp[C][KP];
+#pragma unroll
+                    for (int i = 0; i < C; ++i)
+#pragma unroll
+                        for (int c = 0; c < KP; ++c) tmp[i][c] = hr[(Q + i) % TAPS][c];
+#pragma unroll
+                    for (int i = 0; i < C; ++i)
+#pragma unroll
+                        for (int c = 0; c < KP; ++c) hr[i % TAPS][c] = tmp[i][c];
                 }
-#pragma unroll
-                for (int jy = 0; jy < P; ++jy) {
-                    const int my = iy * P + jy;
-                    if (my < mfirst || my >= mlast) continue;
-                    float o[KP];
-                    if (jy == 0) {
-#pragma unroll
-                        for (int c = 0; c < KP; ++c) o[c] = h[-LO][c];
-                    } else {
-                        const int b = G::base(jy);
-#pragma unroll
-                        for (int c = 0; c < KP; ++c) {
-                            float v2 = __fmul_rn(a.w[jy][0], h[b][c]);
-#pragma unroll
-                            for (int tp = 1; tp < TAPS; ++tp) v2 = __fmaf_rn(a.w[jy][tp], h[b + tp][c], v2);
-                            o[c] = v2;
-                        }
-                    }
-                    T *sr;
-                    if (a.full_width) {
-                        sr = reinterpret_cast<T *>(sp + jy * jy_step);
-                    } else {
-                        const uintptr_t g = reinterpret_cast<uintptr_t>(static_cast<T *>(a.out) + plane_out +
-                                                                        (int64_t)(my - a.out_row0) * a.Wo + t.c0);
-                        sr = reinterpret_cast<T *>(sp + jy * jy_step + (g & 15));
-                    }
-                    if (full_chunk) {
-#pragma unroll
-                        for (int c = 0; c < KP; ++c) sr[c] = DT<T>::from_f(o[c]);
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < KP; ++c)
-                            if (col + c < t.c1) sr[c] = DT<T>::from_f(o[c]);
-                    }
-                }
-                fence_proxy_async_smem();
             }
+            if (active) fence_proxy_async_smem();
             if (span_e == 0) bulk_wait_read0();  // my previous bulk store has read its buffer
             named_bar_sync(1, NCT);
             // copy-out: span (tid >> 4), element slot (tid & 15): slot 0 issues the
@@ -430,6 +446,12 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         }
     }
     if (span_e == 0) bulk_wait0();
+}
+
+// periods per thread chunk: 2 for 16-bit data with odd q (odd word stride), else 1
+template <typename T, int Q>
+constexpr int fused_k() {
+    return (sizeof(T) == 2 && (Q % 2) == 1) ? 2 : 1;
 }
 
 }  // namespace fcfs

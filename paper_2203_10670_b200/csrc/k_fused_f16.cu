@@ -5,8 +5,8 @@
 namespace fcfs {
 
 #define FCFS_V(P, Q) \
-    {reinterpret_cast<const void *>(&fcfs_fused_kernel<__half, P, Q, 2, 0, 1>), P, Q, 2, 0, 1}, \
-    {reinterpret_cast<const void *>(&fcfs_fused_kernel<__half, P, Q, 4, -1, 1>), P, Q, 4, -1, 1},
+    {reinterpret_cast<const void *>(&fcfs_fused_kernel<__half, P, Q, 2, 0, fused_k<__half, Q>()>), P, Q, 2, 0, fused_k<__half, Q>()}, \
+    {reinterpret_cast<const void *>(&fcfs_fused_kernel<__half, P, Q, 4, -1, fused_k<__half, Q>()>), P, Q, 4, -1, fused_k<__half, Q>()},
 extern const FusedVariant kFusedVariants_f16[] = {FCFS_FUSED_PAIRS(FCFS_V){nullptr, 0, 0, 0, 0, 0}};
 #undef FCFS_V
 
