@@ -165,6 +165,15 @@ typedef struct {
 
 fcfs_status fcfs_plan_info(fcfs_plan_t plan, fcfs_plan_info_t *info);
 
+/* fcfs_launch_info -- host-only description (a JSON object written to buf,
+ * NUL-terminated, truncated to buflen) of the kernel and launch geometry a run
+ * of N images over output rows [out_row0, out_row0 + out_nrows) would use,
+ * assuming 16-B-aligned buffers: kernel name, grid, block, dynamic shared
+ * memory and, for the fused kernel, the task decomposition.  Errors:
+ * FCFS_E_ARG. */
+fcfs_status fcfs_launch_info(fcfs_plan_t plan, int64_t N, int64_t out_row0, int64_t out_nrows, char *buf,
+                             int64_t buflen);
+
 /* The fp32 phase table the kernels use: for phase j in [0, p), weights
  * w[4*j + t] (t < ntaps; unused entries 0) and base offsets base[j] =
  * floor(j*q/p).  w must hold 4*p floats, base p ints.  Errors: FCFS_E_ARG. */

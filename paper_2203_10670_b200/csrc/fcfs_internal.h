@@ -62,6 +62,7 @@ struct NearestArgs {     // nearest gather: one thread per 32-byte output chunk
 };
 
 // Fused separable kernel (bilinear / bicubic), see fused.cuh for the layout.
+// A task = NS segments x one band of y-periods; a segment = (plane, column tile).
 struct FusedArgs {
     const void *in;
     void *out;
@@ -69,23 +70,22 @@ struct FusedArgs {
     int32_t H, W, Ho, Wo;
     int32_t in_row0, in_nrows, out_row0, out_nrows;
     int32_t planes, pad;
-    int32_t NP;          // planes per CTA task (full-width mode)
+    int32_t NS;          // segments per task
     int32_t CPT;         // column chunks per tile (a chunk = K x-periods = K*P outputs)
     int32_t nch;         // chunks per output row
-    int32_t ntile;       // column tiles per row
-    int32_t ngroups;     // plane groups
+    int32_t ntile;       // column tiles per row (1 = full-width segments)
+    int32_t nseg;        // planes * ntile
     int32_t PB;          // y-periods per band
     int32_t nbands;
     int32_t iy_first, iy_last;
     int32_t ntasks;
-    int32_t S;           // pipeline stages
+    int32_t S;           // input pipeline stages
     int32_t SR;          // rows per stage
-    int32_t seg_pitch;   // bytes per (plane, row) in a stage
+    int32_t seg_pitch;   // bytes per (segment, row) in a stage
     int32_t stage_bytes;
-    int32_t out_pitch;   // bytes per plane (full width) or per (plane, row) segment (tiled)
-    int32_t obuf_bytes;
-    int32_t full_width;
-    int32_t rpad;        // right padding columns materialised after the last image column
+    int32_t out_pitch;   // staging bytes per segment (full width) or per (segment, row) (tiled)
+    int32_t slot_bytes;  // one output staging slot (a group of output rows of all segments)
+    int32_t rfix;        // right padding columns kept outputs read (written by the producer)
     float w[16][4];      // phase weights (fused variants have p <= 16)
 };
 

@@ -2,31 +2,33 @@
 // §5.2.3): pad + stride-q polyphase conv + pixelshuffle in ONE pass; the
 // p^2-channel hidden layer of §3.1.1 lives only in registers.
 //
-// Structure:
-//   * warp 0 is the producer.  Its lanes (one per plane of the task) stream
-//     the input rows into a ring of S shared-memory stages with 1D bulk async
-//     copies (TMA engine, cp.async.bulk + mbarrier complete_tx, L2
-//     evict_first), running up to S stages ahead.  When a stage has landed the
-//     warp writes the padding columns (§3 Padding) into the row
-//     margins and releases the stage.  A stage holds the fresh input rows of
-//     one y-period (the rows that P output rows add) of every plane.
-//   * warps 1..8 are consumers: thread (pl, c) owns column chunk c (K
-//     x-periods = K*P outputs) of plane pl and walks down the rows.  It filters
-//     each fresh window row horizontally into a register ring of TAPS rows and,
-//     as soon as the last tap row of an output row is in the ring, filters that
-//     output row vertically, rounds it and stores it into a shared staging
-//     buffer laid out exactly like the contiguous global span (co-aligned mod
-//     16).  After one named barrier per y-period the 16-B-aligned body of every
-//     span leaves with a bulk async store (TMA engine) and a few threads write
-//     the unaligned head/tail elements -- coalesced whatever the row pitch,
-//     double-buffered.  All consumers run the same branch-free code.
+// Work: a task is NS segments (a segment = one plane x one column tile) times
+// a band of y-periods (P output rows from Q new input rows each).
+//
+//   * warp 0 is the producer.  Lane s streams the fresh input rows of segment s
+//     into a ring of S shared-memory stages with 1D bulk async copies (TMA
+//     engine, cp.async.bulk + mbarrier complete_tx, L2 evict_first), running up
+//     to S stages ahead.  When a stage has landed the warp writes the padding
+//     columns the kept outputs read (§3 Padding) into the row
+//     margins and releases the stage.
+//   * warps 1..8 are consumers: thread (s, c) owns column chunk c (K x-periods
+//     = K*P outputs) of segment s.  It filters each fresh window row
+//     horizontally into a register ring of TAPS rows and, as soon as the last
+//     tap row of an output row is in the ring, filters that output row
+//     vertically, rounds it and stores it into shared staging laid out exactly
+//     like the contiguous global span (co-aligned mod 16).  Output rows are
+//     flushed in two groups per period (two staging slots used alternately):
+//     one named barrier, then the 16-B-aligned body of every span leaves with a
+//     bulk async store (TMA engine) and 16 threads per span write the unaligned
+//     head/tail -- coalesced whatever the row pitch.  All consumers run the
+//     same branch-free code.
 //   * Period/phase/tap structure is compile time (P, Q, TAPS, LO, K template
 //     parameters): weights are constant-bank operands of the FMAs and every
 //     register index is static.  K = 2 for 16-bit data with odd q makes the
 //     per-thread column stride an odd number of words (conflict-free shared
 //     loads) and the element parity of every window a compile-time constant.
 //
-// Shared row layout: [A margin elements][loaded columns a0..a1)][rpad margin],
+// Shared row layout: [A margin elements][loaded columns a0..a1)][right margin],
 // A = 16 B / element size.  Virtual column c lives at element A + c - a0.
 //
 // Arithmetic is exactly the reference kernel's (k_reference.cu): identical
@@ -45,6 +47,10 @@ struct Geo {
     static constexpr int F = L - C;                                // fresh rows per period
     // window row after which output row j of the period is complete
     static __host__ __device__ constexpr int last_row(int j) { return j == 0 ? -LO : base(j) + TAPS - 1; }
+    // output rows are flushed in G groups: [0, JM) and [JM, P)
+    static constexpr int G = P >= 2 ? 2 : 1;
+    static constexpr int JM = G == 2 ? (P + 1) / 2 : P;
+    static constexpr int JMAX = JM;  // rows in the larger group
 };
 
 template <typename T> struct HalfBits;
@@ -78,41 +84,53 @@ __device__ __forceinline__ void load_win(const T *s, int e0, float (&win)[WIN]) 
     }
 }
 
-struct FusedTask {
-    int group, tile, iy0, iy1, ch0, ch1, c0, c1, a0, a1, my_lo, my_hi;
+// Geometry of one segment (plane x column tile).
+struct SegGeo {
+    int plane, ch0, ch1, c0, c1, a0, a1;
 };
 
 template <int P, int Q, int TAPS, int LO, int K, int ESZ>
-__device__ __forceinline__ FusedTask fused_decode(const FusedArgs &a, int task) {
+__device__ __forceinline__ SegGeo seg_geo(const FusedArgs &a, int gs) {
     using G = Geo<P, Q, TAPS, LO>;
     constexpr int A = 16 / ESZ;
-    FusedTask t;
-    int band = task % a.nbands;
-    int r = task / a.nbands;
-    t.tile = r % a.ntile;
-    t.group = r / a.ntile;
-    t.iy0 = a.iy_first + band * a.PB;
-    t.iy1 = min(a.iy_last + 1, t.iy0 + a.PB);
-    t.ch0 = t.tile * a.CPT;
-    t.ch1 = min(a.nch, t.ch0 + a.CPT);
-    t.c0 = t.ch0 * K * P;
-    t.c1 = min(a.Wo, t.ch1 * K * P);
-    int v0 = t.ch0 * K * Q + LO;
-    int v1 = (t.ch1 - 1) * K * Q + (K - 1) * Q + G::HI;
-    int lo_c = max(v0, 0), hi_c = min(v1 + 1, a.W);
-    t.a0 = (lo_c / A) * A;
-    t.a1 = min(a.W, ((hi_c + A - 1) / A) * A);
-    t.my_lo = max(t.iy0 * P, a.out_row0);
-    t.my_hi = min(t.iy1 * P, a.out_row0 + a.out_nrows);
-    return t;
+    SegGeo s;
+    s.plane = gs / a.ntile;
+    const int tile = gs - s.plane * a.ntile;
+    s.ch0 = tile * a.CPT;
+    s.ch1 = min(a.nch, s.ch0 + a.CPT);
+    s.c0 = s.ch0 * K * P;
+    s.c1 = min(a.Wo, s.ch1 * K * P);
+    const int v0 = s.ch0 * K * Q + LO;
+    const int v1 = (s.ch1 - 1) * K * Q + (K - 1) * Q + G::HI;
+    const int lo_c = max(v0, 0), hi_c = min(v1 + 1, a.W);
+    s.a0 = (lo_c / A) * A;
+    s.a1 = min(a.W, ((hi_c + A - 1) / A) * A);
+    return s;
+}
+
+struct BandInfo {
+    int group, iy0, iy1, my_lo, my_hi, nsg;
+};
+
+template <int P>
+__device__ __forceinline__ BandInfo band_info(const FusedArgs &a, int task) {
+    BandInfo b;
+    const int band = task % a.nbands;
+    b.group = task / a.nbands;
+    b.iy0 = a.iy_first + band * a.PB;
+    b.iy1 = min(a.iy_last + 1, b.iy0 + a.PB);
+    b.my_lo = max(b.iy0 * P, a.out_row0);
+    b.my_hi = min(b.iy1 * P, a.out_row0 + a.out_nrows);
+    b.nsg = min(a.NS, a.nseg - b.group * a.NS);
+    return b;
 }
 
 // Producer-side stage cursor: (task, stage k) of a CTA's sequence of stages.
-template <int P, int Q, int TAPS, int LO, int K, int ESZ>
+template <int P, int Q, int TAPS, int LO>
 struct StageCursor {
     int task, k, nst, slot;
     uint32_t phase, seq;
-    FusedTask t;
+    BandInfo b;
     __device__ __forceinline__ void start(const FusedArgs &a) {
         task = blockIdx.x;
         k = 0;
@@ -123,8 +141,8 @@ struct StageCursor {
     }
     __device__ __forceinline__ void load(const FusedArgs &a) {
         if (task < a.ntasks) {
-            t = fused_decode<P, Q, TAPS, LO, K, ESZ>(a, task);
-            nst = (Geo<P, Q, TAPS, LO>::C > 0 ? 1 : 0) + (t.iy1 - t.iy0);
+            b = band_info<P>(a, task);
+            nst = (Geo<P, Q, TAPS, LO>::C > 0 ? 1 : 0) + (b.iy1 - b.iy0);
         }
     }
     __device__ __forceinline__ void next(const FusedArgs &a) {
@@ -140,10 +158,10 @@ struct StageCursor {
     __device__ __forceinline__ void rows(int &vf, int &nr) const {
         using G = Geo<P, Q, TAPS, LO>;
         if (G::C > 0 && k == 0) {
-            vf = Q * t.iy0 + LO;
+            vf = Q * b.iy0 + LO;
             nr = G::C;
         } else {
-            const int iy = t.iy0 + k - (G::C > 0 ? 1 : 0);
+            const int iy = b.iy0 + k - (G::C > 0 ? 1 : 0);
             vf = Q * iy + LO + G::C;
             nr = G::F;
         }
@@ -185,7 +203,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     if (warp == 0) {
         // ------------------------------------------------------------ producer
         const uint64_t pol = policy_evict_first();
-        StageCursor<P, Q, TAPS, LO, K, ESZ> ci, cf;  // issue cursor runs ahead of the fix-up cursor
+        StageCursor<P, Q, TAPS, LO> ci, cf;  // issue cursor runs ahead of the fix-up cursor
         ci.start(a);
         cf.start(a);
         while (cf.task < a.ntasks) {
@@ -199,19 +217,24 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                         if (!__shfl_sync(0xffffffffu, free_slot, 0)) break;
                     }
                 }
-                const FusedTask &t = ci.t;
                 int vf, nr;
                 ci.rows(vf, nr);
-                const uint32_t seg_bytes = (uint32_t)(t.a1 - t.a0) * ESZ;
-                const int npl = min(a.NP, a.planes - t.group * a.NP);
                 int nreal = 0;  // rows that are not zero padding
                 for (int r = 0; r < nr; ++r) nreal += !(a.pad == FCFS_PAD_ZERO && (vf + r < 0 || vf + r >= a.H));
-                if (lane == 0) mbar_arrive_expect_tx(&full[ci.slot], seg_bytes * (uint32_t)(nreal * npl));
+                SegGeo sg;
+                uint32_t seg_bytes = 0;
+                if (lane < ci.b.nsg) {
+                    sg = seg_geo<P, Q, TAPS, LO, K, ESZ>(a, ci.b.group * a.NS + lane);
+                    seg_bytes = (uint32_t)(sg.a1 - sg.a0) * ESZ;
+                }
+                uint32_t tot = seg_bytes * (uint32_t)nreal;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+                if (lane == 0) mbar_arrive_expect_tx(&full[ci.slot], tot);
                 __syncwarp();
-                for (int pl = lane; pl < npl; pl += 32) {  // one lane per plane issues its rows
-                    const T *pin = static_cast<const T *>(a.in) +
-                                   (int64_t)(t.group * a.NP + pl) * a.in_plane_stride + t.a0;
-                    unsigned char *sbase = stages + ci.slot * a.stage_bytes + A * ESZ + pl * a.SR * a.seg_pitch;
+                if (lane < ci.b.nsg) {  // lane s issues the rows of segment s
+                    const T *pin = static_cast<const T *>(a.in) + (int64_t)sg.plane * a.in_plane_stride + sg.a0;
+                    unsigned char *sbase = stages + ci.slot * a.stage_bytes + A * ESZ + lane * a.SR * a.seg_pitch;
                     for (int r = 0; r < nr; ++r) {
                         const int v = vf + r;
                         if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;
@@ -226,26 +249,28 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             // the oldest stage: wait for its bytes, write the padding columns, release it
             mbar_wait(&full[cf.slot], cf.phase);
             {
-                const FusedTask &t = cf.t;
-                const int lpad = t.a0 == 0 ? -LO : 0;             // left padding columns
-                const int rpad = t.a1 == a.W ? a.rpad : 0;         // right padding columns
-                const int cells = lpad + rpad;
-                if (cells > 0) {
-                    int vf, nr;
-                    cf.rows(vf, nr);
-                    const int npl = min(a.NP, a.planes - t.group * a.NP);
-                    unsigned char *sbase = stages + cf.slot * a.stage_bytes;
-                    const int total = npl * nr * cells;
-                    for (int u = lane; u < total; u += 32) {
-                        const int cell = u % cells;
-                        const int rr = u / cells;
-                        const int r = rr % nr, pl = rr / nr;
-                        const int v = vf + r;
-                        if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;
-                        T *row = reinterpret_cast<T *>(sbase + (pl * a.SR + r) * a.seg_pitch);
-                        const int c = cell < lpad ? -1 - cell : a.W + (cell - lpad);  // virtual column
-                        const int s = pad_src32(c, a.W, a.pad);
-                        row[A + c - t.a0] = s < 0 ? DT<T>::from_f(0.0f) : row[A + min(max(s, t.a0), t.a1 - 1) - t.a0];
+                int vf, nr;
+                cf.rows(vf, nr);
+                unsigned char *sbase = stages + cf.slot * a.stage_bytes;
+                const int pairs = cf.b.nsg * nr;
+                for (int u = lane; u < pairs; u += 32) {
+                    const int s = u / nr, r = u - s * nr;
+                    const int v = vf + r;
+                    if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;
+                    const SegGeo sg = seg_geo<P, Q, TAPS, LO, K, ESZ>(a, cf.b.group * a.NS + s);
+                    T *row = reinterpret_cast<T *>(sbase + (s * a.SR + r) * a.seg_pitch) + A - sg.a0;  // row[c]
+                    if (sg.a0 == 0) {
+#pragma unroll
+                        for (int c = LO; c < 0; ++c) {
+                            const int sc = pad_src32(c, a.W, a.pad);
+                            row[c] = sc < 0 ? DT<T>::from_f(0.0f) : row[min(sc, sg.a1 - 1)];
+                        }
+                    }
+                    if (sg.a1 == a.W) {
+                        for (int c = a.W; c < a.W + a.rfix; ++c) {
+                            const int sc = pad_src32(c, a.W, a.pad);
+                            row[c] = sc < 0 ? DT<T>::from_f(0.0f) : row[max(sc, sg.a0)];
+                        }
                     }
                 }
             }
@@ -259,21 +284,25 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     const int ctid = threadIdx.x - 32;
     const int span_id = ctid >> 4, span_e = ctid & 15;  // copy-out roles
     const int rowb = a.Wo * ESZ;
+    const bool full_width = a.ntile == 1;
     float hr[TAPS][KP];  // ring: window row r lives in hr[r % TAPS]
     int slot = 0;
     uint32_t phase = 0;
-    int ob = 0;
+    uint32_t fk = 0;     // flush counter: staging slot = fk & 1
     for (int task = blockIdx.x; task < a.ntasks; task += gridDim.x) {
-        const FusedTask t = fused_decode<P, Q, TAPS, LO, K, ESZ>(a, task);
-        const int pl = ctid / a.CPT;
-        const int chunk = t.ch0 + (ctid - pl * a.CPT);
-        const int plane = t.group * a.NP + pl;
-        const bool active = (pl < a.NP) && (plane < a.planes) && (chunk < t.ch1);
-        const int e0 = A + chunk * K * Q + LO - t.a0;  // window start (element) in a shared row
+        const BandInfo b = band_info<P>(a, task);
+        const int sgi = ctid / a.CPT;
+        const int chl = ctid - sgi * a.CPT;
+        const bool seg_ok = sgi < b.nsg;
+        SegGeo sg = {0, 0, 0, 0, 0, 0, 1};
+        if (seg_ok) sg = seg_geo<P, Q, TAPS, LO, K, ESZ>(a, b.group * a.NS + sgi);
+        const int chunk = sg.ch0 + chl;
+        const bool active = seg_ok && chunk < sg.ch1;
+        const int e0 = A + chunk * K * Q + LO - sg.a0;  // window start (element) in a shared row
         const int col = chunk * KP;
-        const bool full_chunk = col + KP <= t.c1;
-        const int in_off = pl * a.SR * a.seg_pitch;
-        const int64_t plane_out = (int64_t)plane * a.out_plane_stride;
+        const bool full_chunk = col + KP <= sg.c1;
+        const int in_off = sgi * a.SR * a.seg_pitch;
+        const int64_t plane_out = (int64_t)sg.plane * a.out_plane_stride;
 
         // horizontal taps of one window row into a ring slot
         auto row_h = [&](float(&h)[KP], int v, const unsigned char *srow) {
@@ -292,10 +321,10 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                     if (jx == 0) {
                         v2 = win[k * Q - LO];  // fraction 0: the tap at offset 0, exactly
                     } else {
-                        const int b = k * Q + G::base(jx);
-                        v2 = __fmul_rn(a.w[jx][0], win[b]);
+                        const int bb = k * Q + G::base(jx);
+                        v2 = __fmul_rn(a.w[jx][0], win[bb]);
 #pragma unroll
-                        for (int tp = 1; tp < TAPS; ++tp) v2 = __fmaf_rn(a.w[jx][tp], win[b + tp], v2);
+                        for (int tp = 1; tp < TAPS; ++tp) v2 = __fmaf_rn(a.w[jx][tp], win[bb + tp], v2);
                     }
                     h[k * P + jx] = v2;
                 }
@@ -307,79 +336,129 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             if (active) {
                 const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
 #pragma unroll
-                for (int i = 0; i < C; ++i) row_h(hr[i % TAPS], Q * t.iy0 + LO + i, sb + i * a.seg_pitch);
+                for (int i = 0; i < C; ++i) row_h(hr[i % TAPS], Q * b.iy0 + LO + i, sb + i * a.seg_pitch);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
             if (++slot == a.S) { slot = 0; phase ^= 1; }
         }
 
-        for (int iy = t.iy0; iy < t.iy1; ++iy) {
-            const int mfirst = max(iy * P, t.my_lo), mlast = min(iy * P + P, t.my_hi);
-            unsigned char *ob_base = obuf + ob * a.obuf_bytes;
-            // staging address of (output row iy*P, column `col`) for this thread
-            unsigned char *sp;
-            int jy_step;
-            if (a.full_width) {
-                const uintptr_t g = reinterpret_cast<uintptr_t>(static_cast<T *>(a.out) + plane_out +
-                                                                (int64_t)(mfirst - a.out_row0) * a.Wo);
-                sp = ob_base + pl * a.out_pitch + (g & 15) + (iy * P - mfirst) * rowb + col * ESZ;
-                jy_step = rowb;
-            } else {
-                sp = ob_base + (col - t.c0) * ESZ;
-                jy_step = a.out_pitch;
-            }
+        for (int iy = b.iy0; iy < b.iy1; ++iy) {
+            // first kept output row of flush group g of this period
+            auto gfirst = [&](int g) { return max(iy * P + (g ? G::JM : 0), b.my_lo); };
+            auto glast = [&](int g) { return min(iy * P + (g ? P : G::JM), b.my_hi); };
+            // staging address of output row jy, column `col`, for this thread
+            auto srow = [&](int jy) -> T * {
+                const int g = jy >= G::JM ? 1 : 0;
+                unsigned char *base = obuf + ((fk + g) & 1) * a.slot_bytes;
+                const int my = iy * P + jy;
+                if (full_width) {
+                    const int m0 = gfirst(g);
+                    const uintptr_t ga = reinterpret_cast<uintptr_t>(static_cast<T *>(a.out) + plane_out +
+                                                                     (int64_t)(m0 - a.out_row0) * a.Wo);
+                    return reinterpret_cast<T *>(base + sgi * a.out_pitch + (ga & 15) + (my - m0) * rowb + col * ESZ);
+                }
+                const int ri = jy - (g ? G::JM : 0);
+                const uintptr_t ga = reinterpret_cast<uintptr_t>(static_cast<T *>(a.out) + plane_out +
+                                                                 (int64_t)(my - a.out_row0) * a.Wo + sg.c0);
+                return reinterpret_cast<T *>(base + (sgi * G::JMAX + ri) * a.out_pitch + (ga & 15) +
+                                             (col - sg.c0) * ESZ);
+            };
             // vertical taps of output row jy (its tap rows are in the ring) -> staging
             auto emit = [&](int jy) {
                 const int my = iy * P + jy;
-                if (my < mfirst || my >= mlast) return;
+                if (my < b.my_lo || my >= b.my_hi) return;
                 float o[KP];
                 if (jy == 0) {
 #pragma unroll
                     for (int c = 0; c < KP; ++c) o[c] = hr[(-LO) % TAPS][c];
                 } else {
-                    const int b = G::base(jy);
+                    const int bb = G::base(jy);
 #pragma unroll
                     for (int c = 0; c < KP; ++c) {
-                        float v2 = __fmul_rn(a.w[jy][0], hr[b % TAPS][c]);
+                        float v2 = __fmul_rn(a.w[jy][0], hr[bb % TAPS][c]);
 #pragma unroll
-                        for (int tp = 1; tp < TAPS; ++tp) v2 = __fmaf_rn(a.w[jy][tp], hr[(b + tp) % TAPS][c], v2);
+                        for (int tp = 1; tp < TAPS; ++tp) v2 = __fmaf_rn(a.w[jy][tp], hr[(bb + tp) % TAPS][c], v2);
                         o[c] = v2;
                     }
                 }
-                T *sr;
-                if (a.full_width) {
-                    sr = reinterpret_cast<T *>(sp + jy * jy_step);
-                } else {
-                    const uintptr_t g = reinterpret_cast<uintptr_t>(static_cast<T *>(a.out) + plane_out +
-                                                                    (int64_t)(my - a.out_row0) * a.Wo + t.c0);
-                    sr = reinterpret_cast<T *>(sp + jy * jy_step + (g & 15));
-                }
+                T *sr = srow(jy);
                 if (full_chunk) {
 #pragma unroll
                     for (int c = 0; c < KP; ++c) sr[c] = DT<T>::from_f(o[c]);
                 } else {
 #pragma unroll
                     for (int c = 0; c < KP; ++c)
-                        if (col + c < t.c1) sr[c] = DT<T>::from_f(o[c]);
+                        if (col + c < sg.c1) sr[c] = DT<T>::from_f(o[c]);
+                }
+            };
+            // one named barrier, then bulk stores of flush group g
+            auto flush = [&](int g) {
+                if (active) fence_proxy_async_smem();
+                if (span_e == 0) bulk_wait_read0();  // my previous bulk store has read its slot
+                named_bar_sync(1, NCT);
+                const int m0 = gfirst(g), m1 = glast(g);
+                if (m1 > m0) {
+                    const int nrow = m1 - m0;
+                    const int nsp = full_width ? b.nsg : b.nsg * nrow;
+                    if (span_id < nsp) {
+                        const int s = full_width ? span_id : span_id / nrow;
+                        const SegGeo q = seg_geo<P, Q, TAPS, LO, K, ESZ>(a, b.group * a.NS + s);
+                        T *po = static_cast<T *>(a.out) + (int64_t)q.plane * a.out_plane_stride;
+                        unsigned char *base = obuf + ((fk + g) & 1) * a.slot_bytes;
+                        unsigned char *gp;
+                        const unsigned char *sp;
+                        int bytes;
+                        if (full_width) {
+                            gp = reinterpret_cast<unsigned char *>(po + (int64_t)(m0 - a.out_row0) * a.Wo);
+                            bytes = nrow * rowb;
+                            sp = base + s * a.out_pitch + (reinterpret_cast<uintptr_t>(gp) & 15);
+                        } else {
+                            const int my = m0 + (span_id - s * nrow);
+                            gp = reinterpret_cast<unsigned char *>(po + (int64_t)(my - a.out_row0) * a.Wo + q.c0);
+                            bytes = (q.c1 - q.c0) * ESZ;
+                            const int ri = my - iy * P - (g ? G::JM : 0);
+                            sp = base + (s * G::JMAX + ri) * a.out_pitch + (reinterpret_cast<uintptr_t>(gp) & 15);
+                        }
+                        const int head = min(bytes, (16 - (int)(reinterpret_cast<uintptr_t>(gp) & 15)) & 15);
+                        const int body = (bytes - head) & ~15;
+                        const int tail = bytes - head - body;
+                        if (span_e == 0 && body > 0) {
+                            bulk_s2g(gp + head, sp + head, (uint32_t)body);
+                            bulk_commit();
+                        }
+                        if (span_e < 8) {
+                            if (span_e * ESZ < head)
+                                reinterpret_cast<T *>(gp)[span_e] = reinterpret_cast<const T *>(sp)[span_e];
+                        } else {
+                            const int e = span_e - 8;
+                            if (e * ESZ < tail)
+                                reinterpret_cast<T *>(gp + head + body)[e] =
+                                    reinterpret_cast<const T *>(sp + head + body)[e];
+                        }
+                    }
                 }
             };
 
-            if (active) {
-                // output rows complete with the carried rows alone
+            // output rows complete with the carried rows alone
 #pragma unroll
-                for (int jy = 0; jy < P; ++jy)
-                    if (G::last_row(jy) < C) emit(jy);
+            for (int jy = 0; jy < P; ++jy) {
+                if (G::last_row(jy) < C) {
+                    if (active) emit(jy);
+                    if (G::G == 2 && jy == G::JM - 1) flush(0);
+                }
             }
             mbar_wait(&ready[slot], phase);
-            if (active) {
-                const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
+            const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
 #pragma unroll
-                for (int r = C; r < L; ++r) {
-                    row_h(hr[r % TAPS], Q * iy + LO + r, sb + (r - C) * a.seg_pitch);
+            for (int r = C; r < L; ++r) {
+                if (active) row_h(hr[r % TAPS], Q * iy + LO + r, sb + (r - C) * a.seg_pitch);
 #pragma unroll
-                    for (int jy = 0; jy < P; ++jy)
-                        if (G::last_row(jy) == r) emit(jy);
+                for (int jy = 0; jy < P; ++jy) {
+                    if (G::last_row(jy) == r) {
+                        if (active) emit(jy);
+                        if (G::G == 2 && jy == G::JM - 1) flush(0);
+                    }
                 }
             }
             __syncwarp();
@@ -398,51 +477,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                         for (int c = 0; c < KP; ++c) hr[i % TAPS][c] = tmp[i][c];
                 }
             }
-            if (active) fence_proxy_async_smem();
-            if (span_e == 0) bulk_wait_read0();  // my previous bulk store has read its buffer
-            named_bar_sync(1, NCT);
-            // copy-out: span (tid >> 4), element slot (tid & 15): slot 0 issues the
-            // bulk body; slots 0..7 copy head elements, 8..15 tail elements.
-            if (mlast > mfirst) {
-                const int nrow = mlast - mfirst;
-                const int nsp = a.full_width ? a.NP : nrow;
-                if (span_id < nsp) {
-                    const int spl = a.full_width ? span_id : 0;
-                    const int plane2 = t.group * a.NP + spl;
-                    if (plane2 < a.planes) {
-                        T *po = static_cast<T *>(a.out) + (int64_t)plane2 * a.out_plane_stride;
-                        unsigned char *g;
-                        const unsigned char *s;
-                        int bytes;
-                        if (a.full_width) {
-                            g = reinterpret_cast<unsigned char *>(po + (int64_t)(mfirst - a.out_row0) * a.Wo);
-                            bytes = nrow * rowb;
-                            s = ob_base + spl * a.out_pitch + (reinterpret_cast<uintptr_t>(g) & 15);
-                        } else {
-                            const int my = mfirst + span_id;
-                            g = reinterpret_cast<unsigned char *>(po + (int64_t)(my - a.out_row0) * a.Wo + t.c0);
-                            bytes = (t.c1 - t.c0) * ESZ;
-                            s = ob_base + (my - iy * P) * a.out_pitch + (reinterpret_cast<uintptr_t>(g) & 15);
-                        }
-                        const int head = min(bytes, (16 - (int)(reinterpret_cast<uintptr_t>(g) & 15)) & 15);
-                        const int body = (bytes - head) & ~15;
-                        const int tail = bytes - head - body;
-                        if (span_e == 0 && body > 0) {
-                            bulk_s2g(g + head, s + head, (uint32_t)body);
-                            bulk_commit();
-                        }
-                        if (span_e < 8) {
-                            if (span_e * ESZ < head)
-                                reinterpret_cast<T *>(g)[span_e] = reinterpret_cast<const T *>(s)[span_e];
-                        } else {
-                            const int e = span_e - 8;
-                            if (e * ESZ < tail)
-                                reinterpret_cast<T *>(g + head + body)[e] = reinterpret_cast<const T *>(s + head + body)[e];
-                        }
-                    }
-                }
-            }
-            ob ^= 1;
+            flush(G::G - 1);
+            fk += G::G;
         }
     }
     if (span_e == 0) bulk_wait0();

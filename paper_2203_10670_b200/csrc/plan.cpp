@@ -148,6 +148,7 @@ bool ranges_overlap(const void *a, int64_t na, const void *b, int64_t nb) {
 struct FusedLaunch {
     FusedArgs a;
     int grid, smem;
+    char desc[768];
 };
 
 bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
@@ -180,59 +181,65 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
         for (int t = 0; t < 4; ++t) a.w[j][t] = pl->tab.w[j][t];
     a.nch = (int32_t)((g.Wo + KP - 1) / KP);
     a.SR = std::max(Ff, Cc);
-    {  // chunks whose column window reaches the left / right padding
-        const int WIN = (K - 1) * Q + Lw;
-        const int64_t reach = (int64_t)(a.nch - 1) * K * Q + LO + WIN;  // one past the last window column
-        a.rpad = (int32_t)std::max<int64_t>(0, reach - g.W);
-    }
-    const int budget = 110 * 1024;  // two CTAs per SM
-    // shared row: [A-element margin][loaded columns][right padding], 16-B multiple
+    const int WIN = (K - 1) * Q + Lw;
+    // right margin: every window read stays inside the row slot (allocation);
+    // only the columns kept outputs' own taps reach are written (rfix)
+    const int64_t reach_all = (int64_t)(a.nch - 1) * K * Q + LO + WIN;  // one past the last window column
+    const int64_t ralloc = std::max<int64_t>(0, reach_all - g.W);
+    const int64_t reach_kept = ((g.Wo - 1) * Q) / P + LO + TAPS;       // one past the last kept tap
+    a.rfix = (int32_t)std::max<int64_t>(0, std::min<int64_t>(reach_kept - g.W, ralloc));
+    const int JMAX = P >= 2 ? (P + 1) / 2 : P;  // output rows per staging slot (fused.cuh Geo::JMAX)
+    const int budget = 110 * 1024;              // two CTAs per SM
+    // shared row: [A-element margin][loaded columns][right margin], 16-B multiple
     auto seg_pitch_for = [&](int cpt) {
         int64_t elems = std::min<int64_t>(g.W, (int64_t)cpt * K * Q - Q + Lw + 2 * A);
-        elems = (elems + A - 1) / A * A + A + (a.rpad + A - 1) / A * A;
+        elems = (elems + A - 1) / A * A + A + (ralloc + A - 1) / A * A;
         return (int)(elems * ESZ);
     };
-    int S = 0;
-    for (int tries = 0; tries < 64; ++tries) {
-        if (a.nch <= NT && tries == 0) {
-            a.full_width = 1;
-            a.CPT = a.nch;
-            a.ntile = 1;
-            a.NP = (int)std::min<int64_t>(std::min(16, NT / a.CPT), g.planes);  // <= 16 copy-out spans
-        } else if (a.full_width && a.NP > 1) {
-            a.NP = std::max(1, a.NP / 2);
+    // geometry search: segments of CPT chunks (one plane x one column tile), NS
+    // segments per task; maximise busy consumer threads, then prefer fewer tiles
+    const int64_t min_tiles = (a.nch + NT - 1) / NT;
+    double best_score = -1.0;
+    FusedArgs best = a;
+    for (int64_t nt = min_tiles; nt <= std::min<int64_t>(a.nch, min_tiles + 64); ++nt) {
+        FusedArgs c = a;
+        c.CPT = (int32_t)((a.nch + nt - 1) / nt);
+        c.ntile = (int32_t)((a.nch + c.CPT - 1) / c.CPT);
+        if (nt > min_tiles && c.ntile != nt) continue;
+        const int64_t nseg = g.planes * c.ntile;
+        if (nseg > INT32_MAX) continue;
+        c.nseg = (int32_t)nseg;
+        const int span_cap = c.ntile == 1 ? 16 : 16 / JMAX;  // copy-out spans per flush <= 16
+        c.NS = (int32_t)std::min<int64_t>(std::min(NT / c.CPT, span_cap), nseg);
+        if (c.NS < 1) continue;
+        c.seg_pitch = seg_pitch_for(c.CPT);
+        c.stage_bytes = c.NS * c.SR * c.seg_pitch;
+        if (c.ntile == 1) {
+            c.out_pitch = (int)(((int64_t)JMAX * g.Wo * ESZ + 16 + 15) / 16 * 16);
+            c.slot_bytes = c.NS * c.out_pitch;
         } else {
-            if (a.full_width || a.CPT == 0) {
-                a.full_width = 0;
-                a.ntile = std::max(1, (a.nch + NT - 1) / NT);
-            } else {
-                a.ntile += 1;
-            }
-            a.CPT = (a.nch + a.ntile - 1) / a.ntile;
-            a.ntile = (a.nch + a.CPT - 1) / a.CPT;
-            a.NP = 1;
+            c.out_pitch = ((c.CPT * KP * ESZ + 16) + 15) / 16 * 16;
+            c.slot_bytes = c.NS * JMAX * c.out_pitch;
         }
-        a.seg_pitch = seg_pitch_for(a.CPT);
-        a.stage_bytes = a.NP * a.SR * a.seg_pitch;
-        if (a.full_width) {
-            a.out_pitch = (int)(((int64_t)P * g.Wo * ESZ + 16 + 15) / 16 * 16);
-            a.obuf_bytes = a.NP * a.out_pitch;
-        } else {
-            a.out_pitch = ((a.CPT * KP * ESZ + 16) + 15) / 16 * 16;
-            a.obuf_bytes = a.NP * P * a.out_pitch;
+        const int fixed = 256 + 128 + 2 * c.slot_bytes;
+        const int S = std::min(8, (budget - fixed) / std::max(1, c.stage_bytes));
+        if (S < 2) continue;
+        c.S = S;
+        const double util = (double)c.NS * c.CPT / NT;
+        const double score = util * (S >= 3 ? 1.0 : 0.9) - 0.001 * (double)c.ntile;
+        if (score > best_score) {
+            best_score = score;
+            best = c;
         }
-        const int fixed = 256 + 128 + 2 * a.obuf_bytes;
-        S = std::min(8, (budget - fixed) / std::max(1, a.stage_bytes));
-        if (S >= 3 || (S >= 2 && a.CPT <= 16)) break;
+        if (util > 0.97 && S >= 3) break;
     }
-    if (S < 2) return false;
-    a.S = S;
-    a.ngroups = (int32_t)((g.planes + a.NP - 1) / a.NP);
+    if (best_score < 0) return false;
+    a = best;
     a.iy_first = (int32_t)(g.out_row0 / P);
     a.iy_last = (int32_t)((g.out_row0 + g.out_nrows - 1) / P);
     const int nper = a.iy_last - a.iy_first + 1;
     const int resident = pl->sm_count * 2;
-    const int64_t base_tasks = (int64_t)a.ngroups * a.ntile;
+    const int64_t base_tasks = ((int64_t)a.nseg + a.NS - 1) / a.NS;
     int nbands = 1;
     if (base_tasks < 4 * resident) {
         const int want = (int)((4 * resident + base_tasks - 1) / base_tasks);
@@ -248,14 +255,17 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     L.grid = (int)std::min<int64_t>(ntasks, resident);
     if (const char *e = std::getenv("FCFS_DEBUG_GRID")) L.grid = std::max(1, std::min(L.grid, std::atoi(e)));
     if (const char *e = std::getenv("FCFS_DEBUG_S")) a.S = std::max(2, std::min(a.S, std::atoi(e)));
-    if (std::getenv("FCFS_DEBUG_PRINT"))
-        std::fprintf(stderr,
-                     "fused P%d Q%d T%d K%d: full_width=%d NP=%d CPT=%d nch=%d ntile=%d ngroups=%d S=%d SR=%d "
-                     "seg_pitch=%d stage=%d out_pitch=%d obuf=%d nper=%d PB=%d nbands=%d ntasks=%d grid=%d smem=%d\n",
-                     P, Q, TAPS, K, a.full_width, a.NP, a.CPT, a.nch, a.ntile, a.ngroups, a.S, a.SR, a.seg_pitch,
-                     a.stage_bytes, a.out_pitch, a.obuf_bytes, nper, a.PB, a.nbands, a.ntasks, L.grid,
-                     256 + a.S * a.stage_bytes + 128 + 2 * a.obuf_bytes);
-    L.smem = 256 + a.S * a.stage_bytes + 128 + 2 * a.obuf_bytes;
+    L.smem = 256 + a.S * a.stage_bytes + 128 + 2 * a.slot_bytes;
+    std::snprintf(L.desc, sizeof(L.desc),
+                  "{\"kernel\": \"fused_separable\", \"P\": %d, \"Q\": %d, \"taps\": %d, \"K\": %d, \"NS\": %d, "
+                  "\"CPT\": %d, \"nch\": %d, \"ntile\": %d, \"nseg\": %d, \"S\": %d, \"SR\": %d, \"seg_pitch\": %d, "
+                  "\"stage_bytes\": %d, \"out_pitch\": %d, \"slot_bytes\": %d, \"rfix\": %d, \"periods\": %d, "
+                  "\"PB\": %d, \"nbands\": %d, \"ntasks\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, "
+                  "\"busy_threads\": %d}",
+                  P, Q, TAPS, K, a.NS, a.CPT, a.nch, a.ntile, a.nseg, a.S, a.SR, a.seg_pitch, a.stage_bytes,
+                  a.out_pitch, a.slot_bytes, a.rfix, nper, a.PB, a.nbands, a.ntasks, L.grid, kFusedThreads, L.smem,
+                  a.NS * a.CPT);
+    if (std::getenv("FCFS_DEBUG_PRINT")) std::fprintf(stderr, "%s\n", L.desc);
     return true;
 }
 
@@ -266,6 +276,31 @@ fcfs_status check_device(const fcfs_plan_s *pl) {
         return FCFS_E_DEVICE;
     }
     return FCFS_OK;
+}
+
+// The kernel a run uses (0 reference, 1 nearest gather, 2 fused) after the
+// run-time checks: 32-bit index ranges (gather), 16-B-aligned input and a
+// feasible shared-memory geometry (fused).  Fills L for the fused kernel.
+int select_kernel(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
+    int kernel = pl->kernel;
+    if (kernel == 1 && (g.planes * g.out_nrows >= INT32_MAX || pl->Ho * pl->q >= INT32_MAX)) kernel = 0;
+    if (kernel == 2) {
+        if ((reinterpret_cast<uintptr_t>(g.in) & 15) ||
+            g.planes * std::max(g.in_nrows * pl->W, g.out_nrows * pl->Wo) > INT32_MAX * 16LL || !plan_fused(pl, g, L))
+            kernel = 0;
+    }
+    if (kernel == 1) {
+        const int64_t rows = g.planes * g.out_nrows;
+        std::snprintf(L.desc, sizeof(L.desc),
+                      "{\"kernel\": \"nearest_gather\", \"rows\": %lld, \"grid\": %lld, \"block\": 256, "
+                      "\"outputs_per_lane_iter\": 8}",
+                      (long long)rows, (long long)std::min<int64_t>((rows + 7) / 8, 148 * 8 * 4));
+    } else if (kernel == 0) {
+        const int64_t total = g.planes * g.out_nrows * pl->Wo;
+        std::snprintf(L.desc, sizeof(L.desc), "{\"kernel\": \"reference\", \"grid\": %lld, \"block\": 256}",
+                      (long long)std::min<int64_t>((total + 255) / 256, 148 * 32));
+    }
+    return kernel;
 }
 
 fcfs_status run_window(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t in_nrows, void *out,
@@ -300,14 +335,8 @@ fcfs_status run_window(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t 
     g.in_plane_stride = in_nrows * pl->W;
     g.out_plane_stride = out_nrows * pl->Wo;
 
-    int kernel = pl->kernel;
-    const int64_t total = planes * out_nrows * pl->Wo;
-    (void)total;
-    if (kernel == 1 && (planes * out_nrows >= INT32_MAX || pl->Ho * pl->q >= INT32_MAX)) kernel = 0;  // 32-bit index math
-    if (kernel == 2) {
-        if ((reinterpret_cast<uintptr_t>(in) & 15) || planes * std::max(in_nrows * pl->W, out_nrows * pl->Wo) > INT32_MAX * 16LL)
-            kernel = 0;
-    }
+    FusedLaunch L;
+    const int kernel = select_kernel(pl, g, L);
     int rc = 0;
     if (kernel == 1) {
         NearestArgs a;
@@ -322,14 +351,8 @@ fcfs_status run_window(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t 
         a.vec_ok = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
         rc = launch_nearest(pl->dtype, a, stream);
     } else if (kernel == 2) {
-        FusedLaunch L;
-        if (plan_fused(pl, g, L)) {
-            rc = launch_fused(pl->fused, L.a, L.grid, kFusedThreads, L.smem, stream);
-        } else {
-            kernel = 0;
-        }
-    }
-    if (kernel == 0) {
+        rc = launch_fused(pl->fused, L.a, L.grid, kFusedThreads, L.smem, stream);
+    } else {
         RefArgs a;
         a.g = g;
         a.t = pl->tab;
@@ -535,6 +558,32 @@ fcfs_status fcfs_plan_info(fcfs_plan_t pl, fcfs_plan_info_t *info) {
     info->kernel = pl->kernel;
     info->device = pl->device;
     info->in_rows_referenced = pl->rows_ref;
+    return FCFS_OK;
+}
+
+fcfs_status fcfs_launch_info(fcfs_plan_t pl, int64_t N, int64_t out_row0, int64_t out_nrows, char *buf,
+                             int64_t buflen) {
+    if (!pl || !buf || buflen < 2 || N < 1) return FCFS_E_ARG;
+    if (out_row0 < 0 || out_nrows < 1 || out_row0 + out_nrows > pl->Ho) return FCFS_E_ARG;
+    int64_t n0, n1;
+    needed_rows(pl, out_row0, out_row0 + out_nrows, &n0, &n1);
+    RunGeom g;
+    g.in = nullptr;  // assumed 16-B aligned
+    g.out = nullptr;
+    g.planes = N * pl->C;
+    g.H = pl->H;
+    g.W = pl->W;
+    g.Ho = pl->Ho;
+    g.Wo = pl->Wo;
+    g.in_row0 = n0;
+    g.in_nrows = std::max<int64_t>(1, n1 - n0);
+    g.out_row0 = out_row0;
+    g.out_nrows = out_nrows;
+    g.in_plane_stride = g.in_nrows * pl->W;
+    g.out_plane_stride = out_nrows * pl->Wo;
+    FusedLaunch L;
+    select_kernel(pl, g, L);
+    std::snprintf(buf, (size_t)buflen, "%s", L.desc);
     return FCFS_OK;
 }
 

@@ -83,6 +83,14 @@ class Plan:
         check(_lib.lib.fcfs_strip_rows(self._h, own0, own1, *[ctypes.byref(x) for x in v]), "fcfs_strip_rows")
         return tuple(x.value for x in v)
 
+    def launch_info(self, N: int, out_row0: int = 0, out_nrows: int | None = None) -> dict:
+        """The kernel and launch geometry a run would use (host only)."""
+        import json
+        buf = ctypes.create_string_buffer(1024)
+        n = self.Ho - out_row0 if out_nrows is None else out_nrows
+        check(_lib.lib.fcfs_launch_info(self._h, N, out_row0, n, buf, 1024), "fcfs_launch_info")
+        return json.loads(buf.value.decode())
+
     def needed_rows(self, out0: int, out1: int):
         """Input rows [need0, need1) that output rows [out0, out1) read."""
         a, b = ctypes.c_int64(), ctypes.c_int64()

@@ -136,6 +136,28 @@ def test_kernel_selection(fc):
     assert fc.Plan(3, 2, "bilinear", "replicate", 1, 64, 64, force_reference=True).kernel == "reference"
 
 
+@pytest.mark.parametrize("name", ["C1a", "C1b", "C2a", "C2b", "C3", "C4a", "C4b", "C5"])
+def test_launch_geometry(fc, name):
+    """The planner's launch geometry for every config: fits the shared-memory
+    budget (2 CTAs/SM), keeps at least ~85% of the consumer threads busy on the
+    big configs, and tiles the output exactly."""
+    import synth
+    c = synth.CONFIGS[name]
+    pl = fc.Plan(c.p, c.q, c.mode, c.pad, c.C, c.H, c.W, c.dtype, "floor", c.is1d)
+    info = pl.launch_info(c.N)
+    assert info["kernel"] == pl.kernel
+    if info["kernel"] != "fused_separable":
+        return
+    assert info["smem"] <= 113 * 1024 and info["S"] >= 2 and info["grid"] <= 296
+    assert info["CPT"] * info["ntile"] >= info["nch"] and info["NS"] * info["CPT"] <= 256
+    assert info["nch"] * info["K"] * info["P"] >= pl.Wo
+    assert info["PB"] * info["nbands"] >= info["periods"]
+    assert info["ntasks"] == -(-info["nseg"] // info["NS"]) * info["nbands"]
+    if name in ("C3", "C4a", "C4b", "C5"):
+        assert info["busy_threads"] >= 0.85 * 256
+        assert info["ntasks"] >= 296  # every SM slot has work
+
+
 def _own(p, q, H, Ho, own0, own1):
     """Brute force: outputs whose base row floor(m*q/p) lies in [own0, own1)."""
     ms = [m for m in range(Ho) if own0 <= (m * q) // p < own1 or (own1 == H and (m * q) // p >= H)]
