@@ -85,6 +85,8 @@ struct FusedArgs {
     int32_t stage_bytes;
     int32_t out_pitch;   // staging bytes per segment (full width) or per (segment, row) (tiled)
     int32_t slot_bytes;  // one output staging slot (a group of output rows of all segments)
+    int32_t G;           // output flush groups per y-period (1: rows [0,P); 2: [0,JM) and [JM,P))
+    int32_t JM;          // first output row of group 1 (= P when G == 1)
     int32_t rfix;        // right padding columns kept outputs read (written by the producer)
     float w[16][4];      // phase weights (fused variants have p <= 16)
 };

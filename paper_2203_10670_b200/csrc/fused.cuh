@@ -47,10 +47,6 @@ struct Geo {
     static constexpr int F = L - C;                                // fresh rows per period
     // window row after which output row j of the period is complete
     static __host__ __device__ constexpr int last_row(int j) { return j == 0 ? -LO : base(j) + TAPS - 1; }
-    // output rows are flushed in G groups: [0, JM) and [JM, P)
-    static constexpr int G = P >= 2 ? 2 : 1;
-    static constexpr int JM = G == 2 ? (P + 1) / 2 : P;
-    static constexpr int JMAX = JM;  // rows in the larger group
 };
 
 template <typename T> struct HalfBits;
@@ -300,9 +296,19 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         const bool active = seg_ok && chunk < sg.ch1;
         const int e0 = A + chunk * K * Q + LO - sg.a0;  // window start (element) in a shared row
         const int col = chunk * KP;
-        const bool full_chunk = col + KP <= sg.c1;
+        const int nvalid = sg.c1 - col;  // outputs of this chunk inside the tile (>= KP: all)
         const int in_off = sgi * a.SR * a.seg_pitch;
         const int64_t plane_out = (int64_t)sg.plane * a.out_plane_stride;
+        const uintptr_t out_base = reinterpret_cast<uintptr_t>(a.out);
+        // this thread's offset inside a staging slot
+        const int st_off = full_width ? sgi * a.out_pitch + col * ESZ : sgi * a.JM * a.out_pitch + (col - sg.c0) * ESZ;
+        // copy-out role: span (span_seg, span_row) of every flush of this task
+        const int span_seg = full_width ? span_id : (b.nsg > 0 ? span_id % b.nsg : 0);
+        const int span_row = full_width ? 0 : span_id / max(b.nsg, 1);
+        const bool span_ok = full_width ? span_id < b.nsg : span_row < a.JM;
+        SegGeo sq = {0, 0, 0, 0, 0, 0, 1};
+        if (span_ok) sq = seg_geo<P, Q, TAPS, LO, K, ESZ>(a, b.group * a.NS + span_seg);
+        T *const span_out = static_cast<T *>(a.out) + (int64_t)sq.plane * a.out_plane_stride;
 
         // horizontal taps of one window row into a ring slot
         auto row_h = [&](float(&h)[KP], int v, const unsigned char *srow) {
@@ -344,25 +350,26 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         }
 
         for (int iy = b.iy0; iy < b.iy1; ++iy) {
-            // first kept output row of flush group g of this period
-            auto gfirst = [&](int g) { return max(iy * P + (g ? G::JM : 0), b.my_lo); };
-            auto glast = [&](int g) { return min(iy * P + (g ? P : G::JM), b.my_hi); };
+            // first / one-past-last kept output row of flush group g of this period
+            auto gfirst = [&](int g) { return max(iy * P + (g ? a.JM : 0), b.my_lo); };
+            auto glast = [&](int g) { return min(iy * P + (g ? P : a.JM), b.my_hi); };
+            // full width: staging address of this thread's (group-first row, col) per group
+            unsigned char *gbase[2];
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+                const int m0 = gfirst(g);
+                const uint32_t mis = (uint32_t)(out_base + (plane_out + (int64_t)(m0 - a.out_row0) * a.Wo) * ESZ) & 15;
+                gbase[g] = obuf + ((fk + g) & 1) * a.slot_bytes + st_off + mis + (iy * P + (g ? a.JM : 0) - m0) * rowb;
+            }
             // staging address of output row jy, column `col`, for this thread
             auto srow = [&](int jy) -> T * {
-                const int g = jy >= G::JM ? 1 : 0;
-                unsigned char *base = obuf + ((fk + g) & 1) * a.slot_bytes;
+                const int g = (a.G == 2 && jy >= a.JM) ? 1 : 0;
+                const int ri = jy - (g ? a.JM : 0);
+                if (full_width) return reinterpret_cast<T *>(gbase[g] + ri * rowb);
                 const int my = iy * P + jy;
-                if (full_width) {
-                    const int m0 = gfirst(g);
-                    const uintptr_t ga = reinterpret_cast<uintptr_t>(static_cast<T *>(a.out) + plane_out +
-                                                                     (int64_t)(m0 - a.out_row0) * a.Wo);
-                    return reinterpret_cast<T *>(base + sgi * a.out_pitch + (ga & 15) + (my - m0) * rowb + col * ESZ);
-                }
-                const int ri = jy - (g ? G::JM : 0);
-                const uintptr_t ga = reinterpret_cast<uintptr_t>(static_cast<T *>(a.out) + plane_out +
-                                                                 (int64_t)(my - a.out_row0) * a.Wo + sg.c0);
-                return reinterpret_cast<T *>(base + (sgi * G::JMAX + ri) * a.out_pitch + (ga & 15) +
-                                             (col - sg.c0) * ESZ);
+                const uint32_t mis =
+                    (uint32_t)(out_base + (plane_out + (int64_t)(my - a.out_row0) * a.Wo + sg.c0) * ESZ) & 15;
+                return reinterpret_cast<T *>(obuf + ((fk + g) & 1) * a.slot_bytes + st_off + ri * a.out_pitch + mis);
             };
             // vertical taps of output row jy (its tap rows are in the ring) -> staging
             auto emit = [&](int jy) {
@@ -383,14 +390,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                     }
                 }
                 T *sr = srow(jy);
-                if (full_chunk) {
 #pragma unroll
-                    for (int c = 0; c < KP; ++c) sr[c] = DT<T>::from_f(o[c]);
-                } else {
-#pragma unroll
-                    for (int c = 0; c < KP; ++c)
-                        if (col + c < sg.c1) sr[c] = DT<T>::from_f(o[c]);
-                }
+                for (int c = 0; c < KP; ++c)
+                    if (c < nvalid) sr[c] = DT<T>::from_f(o[c]);
             };
             // one named barrier, then bulk stores of flush group g
             auto flush = [&](int g) {
@@ -398,28 +400,24 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 if (span_e == 0) bulk_wait_read0();  // my previous bulk store has read its slot
                 named_bar_sync(1, NCT);
                 const int m0 = gfirst(g), m1 = glast(g);
-                if (m1 > m0) {
-                    const int nrow = m1 - m0;
-                    const int nsp = full_width ? b.nsg : b.nsg * nrow;
-                    if (span_id < nsp) {
-                        const int s = full_width ? span_id : span_id / nrow;
-                        const SegGeo q = seg_geo<P, Q, TAPS, LO, K, ESZ>(a, b.group * a.NS + s);
-                        T *po = static_cast<T *>(a.out) + (int64_t)q.plane * a.out_plane_stride;
-                        unsigned char *base = obuf + ((fk + g) & 1) * a.slot_bytes;
-                        unsigned char *gp;
-                        const unsigned char *sp;
-                        int bytes;
-                        if (full_width) {
-                            gp = reinterpret_cast<unsigned char *>(po + (int64_t)(m0 - a.out_row0) * a.Wo);
-                            bytes = nrow * rowb;
-                            sp = base + s * a.out_pitch + (reinterpret_cast<uintptr_t>(gp) & 15);
-                        } else {
-                            const int my = m0 + (span_id - s * nrow);
-                            gp = reinterpret_cast<unsigned char *>(po + (int64_t)(my - a.out_row0) * a.Wo + q.c0);
-                            bytes = (q.c1 - q.c0) * ESZ;
-                            const int ri = my - iy * P - (g ? G::JM : 0);
-                            sp = base + (s * G::JMAX + ri) * a.out_pitch + (reinterpret_cast<uintptr_t>(gp) & 15);
-                        }
+                const int nrow = m1 - m0;
+                if (span_ok && nrow > 0 && (full_width || span_row < nrow)) {
+                    unsigned char *base = obuf + ((fk + g) & 1) * a.slot_bytes;
+                    unsigned char *gp;
+                    const unsigned char *sp;
+                    int bytes;
+                    if (full_width) {
+                        gp = reinterpret_cast<unsigned char *>(span_out + (int64_t)(m0 - a.out_row0) * a.Wo);
+                        bytes = nrow * rowb;
+                        sp = base + span_seg * a.out_pitch + (reinterpret_cast<uintptr_t>(gp) & 15);
+                    } else {
+                        const int my = m0 + span_row;
+                        gp = reinterpret_cast<unsigned char *>(span_out + (int64_t)(my - a.out_row0) * a.Wo + sq.c0);
+                        bytes = (sq.c1 - sq.c0) * ESZ;
+                        const int ri = my - iy * P - (g ? a.JM : 0);
+                        sp = base + (span_seg * a.JM + ri) * a.out_pitch + (reinterpret_cast<uintptr_t>(gp) & 15);
+                    }
+                    {
                         const int head = min(bytes, (16 - (int)(reinterpret_cast<uintptr_t>(gp) & 15)) & 15);
                         const int body = (bytes - head) & ~15;
                         const int tail = bytes - head - body;
@@ -445,7 +443,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             for (int jy = 0; jy < P; ++jy) {
                 if (G::last_row(jy) < C) {
                     if (active) emit(jy);
-                    if (G::G == 2 && jy == G::JM - 1) flush(0);
+                    if (a.G == 2 && jy == a.JM - 1) flush(0);
                 }
             }
             mbar_wait(&ready[slot], phase);
@@ -457,7 +455,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 for (int jy = 0; jy < P; ++jy) {
                     if (G::last_row(jy) == r) {
                         if (active) emit(jy);
-                        if (G::G == 2 && jy == G::JM - 1) flush(0);
+                        if (a.G == 2 && jy == a.JM - 1) flush(0);
                     }
                 }
             }
@@ -477,8 +475,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                         for (int c = 0; c < KP; ++c) hr[i % TAPS][c] = tmp[i][c];
                 }
             }
-            flush(G::G - 1);
-            fk += G::G;
+            flush(a.G - 1);
+            fk += a.G;
         }
     }
     if (span_e == 0) bulk_wait0();

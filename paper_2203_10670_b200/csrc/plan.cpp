@@ -188,7 +188,6 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     const int64_t ralloc = std::max<int64_t>(0, reach_all - g.W);
     const int64_t reach_kept = ((g.Wo - 1) * Q) / P + LO + TAPS;       // one past the last kept tap
     a.rfix = (int32_t)std::max<int64_t>(0, std::min<int64_t>(reach_kept - g.W, ralloc));
-    const int JMAX = P >= 2 ? (P + 1) / 2 : P;  // output rows per staging slot (fused.cuh Geo::JMAX)
     const int budget = 110 * 1024;              // two CTAs per SM
     // shared row: [A-element margin][loaded columns][right margin], 16-B multiple
     auto seg_pitch_for = [&](int cpt) {
@@ -202,36 +201,43 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     double best_score = -1.0;
     FusedArgs best = a;
     for (int64_t nt = min_tiles; nt <= std::min<int64_t>(a.nch, min_tiles + 64); ++nt) {
-        FusedArgs c = a;
-        c.CPT = (int32_t)((a.nch + nt - 1) / nt);
-        c.ntile = (int32_t)((a.nch + c.CPT - 1) / c.CPT);
-        if (nt > min_tiles && c.ntile != nt) continue;
-        const int64_t nseg = g.planes * c.ntile;
-        if (nseg > INT32_MAX) continue;
-        c.nseg = (int32_t)nseg;
-        const int span_cap = c.ntile == 1 ? 16 : 16 / JMAX;  // copy-out spans per flush <= 16
-        c.NS = (int32_t)std::min<int64_t>(std::min(NT / c.CPT, span_cap), nseg);
-        if (c.NS < 1) continue;
-        c.seg_pitch = seg_pitch_for(c.CPT);
-        c.stage_bytes = c.NS * c.SR * c.seg_pitch;
-        if (c.ntile == 1) {
-            c.out_pitch = (int)(((int64_t)JMAX * g.Wo * ESZ + 16 + 15) / 16 * 16);
-            c.slot_bytes = c.NS * c.out_pitch;
-        } else {
-            c.out_pitch = ((c.CPT * KP * ESZ + 16) + 15) / 16 * 16;
-            c.slot_bytes = c.NS * JMAX * c.out_pitch;
+        // G = 1: one flush per y-period, two full-period staging slots;
+        // G = 2: two flushes per period, slots of ceil(P/2) rows (half the smem)
+        for (int Gf = 1; Gf <= (P >= 2 ? 2 : 1); ++Gf) {
+            FusedArgs c = a;
+            c.G = Gf;
+            c.JM = Gf == 2 ? (P + 1) / 2 : P;
+            c.CPT = (int32_t)((a.nch + nt - 1) / nt);
+            c.ntile = (int32_t)((a.nch + c.CPT - 1) / c.CPT);
+            if (nt > min_tiles && c.ntile != nt) continue;
+            const int64_t nseg = g.planes * c.ntile;
+            if (nseg > INT32_MAX) continue;
+            c.nseg = (int32_t)nseg;
+            const int span_cap = c.ntile == 1 ? 16 : 16 / c.JM;  // copy-out spans per flush <= 16
+            c.NS = (int32_t)std::min<int64_t>(std::min(NT / c.CPT, span_cap), nseg);
+            if (c.NS < 1) continue;
+            c.seg_pitch = seg_pitch_for(c.CPT);
+            c.stage_bytes = c.NS * c.SR * c.seg_pitch;
+            if (c.ntile == 1) {
+                c.out_pitch = (int)(((int64_t)c.JM * g.Wo * ESZ + 16 + 15) / 16 * 16);
+                c.slot_bytes = c.NS * c.out_pitch;
+            } else {
+                c.out_pitch = ((c.CPT * KP * ESZ + 16) + 15) / 16 * 16;
+                c.slot_bytes = c.NS * c.JM * c.out_pitch;
+            }
+            const int fixed = 256 + 128 + 2 * c.slot_bytes;
+            const int S = std::min(8, (budget - fixed) / std::max(1, c.stage_bytes));
+            if (S < 2) continue;
+            c.S = S;
+            const double util = (double)c.NS * c.CPT / NT;
+            // one flush per period is cheaper; deep enough input ring first
+            const double score = util * (S >= 3 ? 1.0 : 0.9) * (Gf == 1 ? 1.0 : 0.97) - 0.001 * (double)c.ntile;
+            if (score > best_score) {
+                best_score = score;
+                best = c;
+            }
         }
-        const int fixed = 256 + 128 + 2 * c.slot_bytes;
-        const int S = std::min(8, (budget - fixed) / std::max(1, c.stage_bytes));
-        if (S < 2) continue;
-        c.S = S;
-        const double util = (double)c.NS * c.CPT / NT;
-        const double score = util * (S >= 3 ? 1.0 : 0.9) - 0.001 * (double)c.ntile;
-        if (score > best_score) {
-            best_score = score;
-            best = c;
-        }
-        if (util > 0.97 && S >= 3) break;
+        if (best_score > 0.96) break;
     }
     if (best_score < 0) return false;
     a = best;
@@ -261,10 +267,10 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
                   "\"CPT\": %d, \"nch\": %d, \"ntile\": %d, \"nseg\": %d, \"S\": %d, \"SR\": %d, \"seg_pitch\": %d, "
                   "\"stage_bytes\": %d, \"out_pitch\": %d, \"slot_bytes\": %d, \"rfix\": %d, \"periods\": %d, "
                   "\"PB\": %d, \"nbands\": %d, \"ntasks\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, "
-                  "\"busy_threads\": %d}",
+                  "\"busy_threads\": %d, \"flush_groups\": %d}",
                   P, Q, TAPS, K, a.NS, a.CPT, a.nch, a.ntile, a.nseg, a.S, a.SR, a.seg_pitch, a.stage_bytes,
                   a.out_pitch, a.slot_bytes, a.rfix, nper, a.PB, a.nbands, a.ntasks, L.grid, kFusedThreads, L.smem,
-                  a.NS * a.CPT);
+                  a.NS * a.CPT, a.G);
     if (std::getenv("FCFS_DEBUG_PRINT")) std::fprintf(stderr, "%s\n", L.desc);
     return true;
 }
