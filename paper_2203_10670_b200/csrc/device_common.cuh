@@ -49,6 +49,28 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f) {
     return (t + n) >> f.s;
 }
 
+// Packed fp32x2 arithmetic (sm_100a FFMA2 / FMUL2, scalar operand broadcast):
+// each lane is an independent round-to-nearest-even fp32 operation, so the
+// results are bitwise those of the scalar __fmul_rn / __fmaf_rn sequence.
+__device__ __forceinline__ float2 fmul2_rn(float w, float2 x) {
+    float2 r;
+    asm("{.reg .b64 wv, xv, rv;\n\t"
+        "mov.b64 wv, {%2, %2};\n\tmov.b64 xv, {%3, %4};\n\t"
+        "mul.rn.f32x2 rv, wv, xv;\n\tmov.b64 {%0, %1}, rv;}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(w), "f"(x.x), "f"(x.y));
+    return r;
+}
+__device__ __forceinline__ float2 ffma2_rn(float w, float2 x, float2 c) {
+    float2 r;
+    asm("{.reg .b64 wv, xv, cv, rv;\n\t"
+        "mov.b64 wv, {%2, %2};\n\tmov.b64 xv, {%3, %4};\n\tmov.b64 cv, {%5, %6};\n\t"
+        "fma.rn.f32x2 rv, wv, xv, cv;\n\tmov.b64 {%0, %1}, rv;}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(w), "f"(x.x), "f"(x.y), "f"(c.x), "f"(c.y));
+    return r;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

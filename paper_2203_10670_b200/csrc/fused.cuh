@@ -299,7 +299,10 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         const int nvalid = sg.c1 - col;  // outputs of this chunk inside the tile (>= KP: all)
         const int in_off = sgi * a.SR * a.seg_pitch;
         const int64_t plane_out = (int64_t)sg.plane * a.out_plane_stride;
-        const uintptr_t out_base = reinterpret_cast<uintptr_t>(a.out);
+        // global byte address of output row out_row0, column c0 of this thread's segment, mod 16
+        const uint32_t mis_row0 =
+            (uint32_t)(reinterpret_cast<uintptr_t>(a.out) + (plane_out + (full_width ? 0 : sg.c0)) * ESZ) & 15;
+        const uint32_t rowb16 = (uint32_t)rowb & 15;
         // this thread's offset inside a staging slot
         const int st_off = full_width ? sgi * a.out_pitch + col * ESZ : sgi * a.JM * a.out_pitch + (col - sg.c0) * ESZ;
         // copy-out role: span (span_seg, span_row) of every flush of this task
@@ -319,20 +322,39 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             }
             float win[WIN];
             load_win<T, WIN, PAR>(reinterpret_cast<const T *>(srow), e0, win);
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
+            if constexpr (K == 2) {
+                // phase jx of both x-periods shares its weights: packed pairs
 #pragma unroll
                 for (int jx = 0; jx < P; ++jx) {
-                    float v2;
-                    if (jx == 0) {
-                        v2 = win[k * Q - LO];  // fraction 0: the tap at offset 0, exactly
+                    if (jx == 0) {  // fraction 0: the tap at offset 0, exactly
+                        h[0] = win[-LO];
+                        h[P] = win[Q - LO];
                     } else {
-                        const int bb = k * Q + G::base(jx);
-                        v2 = __fmul_rn(a.w[jx][0], win[bb]);
+                        const int bb = G::base(jx);
+                        float2 v2 = fmul2_rn(a.w[jx][0], make_float2(win[bb], win[Q + bb]));
 #pragma unroll
-                        for (int tp = 1; tp < TAPS; ++tp) v2 = __fmaf_rn(a.w[jx][tp], win[bb + tp], v2);
+                        for (int tp = 1; tp < TAPS; ++tp)
+                            v2 = ffma2_rn(a.w[jx][tp], make_float2(win[bb + tp], win[Q + bb + tp]), v2);
+                        h[jx] = v2.x;
+                        h[P + jx] = v2.y;
                     }
-                    h[k * P + jx] = v2;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+#pragma unroll
+                    for (int jx = 0; jx < P; ++jx) {
+                        float v2;
+                        if (jx == 0) {
+                            v2 = win[k * Q - LO];  // fraction 0: the tap at offset 0, exactly
+                        } else {
+                            const int bb = k * Q + G::base(jx);
+                            v2 = __fmul_rn(a.w[jx][0], win[bb]);
+#pragma unroll
+                            for (int tp = 1; tp < TAPS; ++tp) v2 = __fmaf_rn(a.w[jx][tp], win[bb + tp], v2);
+                        }
+                        h[k * P + jx] = v2;
+                    }
                 }
             }
         };
@@ -353,23 +375,19 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             // first / one-past-last kept output row of flush group g of this period
             auto gfirst = [&](int g) { return max(iy * P + (g ? a.JM : 0), b.my_lo); };
             auto glast = [&](int g) { return min(iy * P + (g ? P : a.JM), b.my_hi); };
-            // full width: staging address of this thread's (group-first row, col) per group
-            unsigned char *gbase[2];
-#pragma unroll
-            for (int g = 0; g < 2; ++g) {
-                const int m0 = gfirst(g);
-                const uint32_t mis = (uint32_t)(out_base + (plane_out + (int64_t)(m0 - a.out_row0) * a.Wo) * ESZ) & 15;
-                gbase[g] = obuf + ((fk + g) & 1) * a.slot_bytes + st_off + mis + (iy * P + (g ? a.JM : 0) - m0) * rowb;
-            }
-            // staging address of output row jy, column `col`, for this thread
+            // staging address of output row jy, column `col`, for this thread; the
+            // span start is co-aligned mod 16 with its global address (32-bit mod-16 math)
             auto srow = [&](int jy) -> T * {
                 const int g = (a.G == 2 && jy >= a.JM) ? 1 : 0;
                 const int ri = jy - (g ? a.JM : 0);
-                if (full_width) return reinterpret_cast<T *>(gbase[g] + ri * rowb);
-                const int my = iy * P + jy;
-                const uint32_t mis =
-                    (uint32_t)(out_base + (plane_out + (int64_t)(my - a.out_row0) * a.Wo + sg.c0) * ESZ) & 15;
-                return reinterpret_cast<T *>(obuf + ((fk + g) & 1) * a.slot_bytes + st_off + ri * a.out_pitch + mis);
+                unsigned char *slotp = obuf + ((fk + g) & 1) * a.slot_bytes + st_off;
+                if (full_width) {
+                    const int m0 = gfirst(g);
+                    const uint32_t mis = (mis_row0 + (uint32_t)(m0 - a.out_row0) * rowb16) & 15;
+                    return reinterpret_cast<T *>(slotp + mis + (iy * P + (g ? a.JM : 0) + ri - m0) * rowb);
+                }
+                const uint32_t mis = (mis_row0 + (uint32_t)(iy * P + jy - a.out_row0) * rowb16) & 15;
+                return reinterpret_cast<T *>(slotp + ri * a.out_pitch + mis);
             };
             // vertical taps of output row jy (its tap rows are in the ring) -> staging
             auto emit = [&](int jy) {
@@ -381,12 +399,22 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                     for (int c = 0; c < KP; ++c) o[c] = hr[(-LO) % TAPS][c];
                 } else {
                     const int bb = G::base(jy);
+                    constexpr int H2 = KP / 2;  // columns c and c + H2 share the row weights
 #pragma unroll
-                    for (int c = 0; c < KP; ++c) {
-                        float v2 = __fmul_rn(a.w[jy][0], hr[bb % TAPS][c]);
+                    for (int c = 0; c < H2; ++c) {
+                        float2 v2 = fmul2_rn(a.w[jy][0], make_float2(hr[bb % TAPS][c], hr[bb % TAPS][c + H2]));
 #pragma unroll
-                        for (int tp = 1; tp < TAPS; ++tp) v2 = __fmaf_rn(a.w[jy][tp], hr[(bb + tp) % TAPS][c], v2);
-                        o[c] = v2;
+                        for (int tp = 1; tp < TAPS; ++tp)
+                            v2 = ffma2_rn(a.w[jy][tp], make_float2(hr[(bb + tp) % TAPS][c], hr[(bb + tp) % TAPS][c + H2]),
+                                          v2);
+                        o[c] = v2.x;
+                        o[c + H2] = v2.y;
+                    }
+                    if constexpr (KP % 2 == 1) {
+                        float v1 = __fmul_rn(a.w[jy][0], hr[bb % TAPS][KP - 1]);
+#pragma unroll
+                        for (int tp = 1; tp < TAPS; ++tp) v1 = __fmaf_rn(a.w[jy][tp], hr[(bb + tp) % TAPS][KP - 1], v1);
+                        o[KP - 1] = v1;
                     }
                 }
                 T *sr = srow(jy);
