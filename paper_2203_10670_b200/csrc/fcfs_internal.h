@@ -106,6 +106,6 @@ const FusedVariant *fused_lookup(int dtype, int p, int q, int ntaps);
 int launch_fused(const FusedVariant *v, const FusedArgs &a, int grid, int block, int smem, void *stream);
 
 constexpr int kFusedConsumerWarps = 8;
-constexpr int kFusedThreads = 32 * (1 + kFusedConsumerWarps);
+constexpr int kFusedThreads = 32 * (2 + kFusedConsumerWarps);  // issuer warp, padding warp, consumers
 
 }  // namespace fcfs

@@ -197,22 +197,14 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     __syncthreads();
 
     if (warp == 0) {
-        // ------------------------------------------------------------ producer
+        // ------------------------------------------------------- producer: issue
+        // a stage's bulk loads as soon as the consumers have freed its slot
         const uint64_t pol = policy_evict_first();
-        StageCursor<P, Q, TAPS, LO> ci, cf;  // issue cursor runs ahead of the fix-up cursor
+        StageCursor<P, Q, TAPS, LO> ci;
         ci.start(a);
-        cf.start(a);
-        while (cf.task < a.ntasks) {
-            // issue bulk loads up to S stages ahead of the oldest unreleased stage
-            while (ci.task < a.ntasks && ci.seq < cf.seq + (uint32_t)a.S) {
-                if (ci.seq >= (uint32_t)a.S) {
-                    if (ci.seq == cf.seq) {
-                        mbar_wait(&empty[ci.slot], ci.phase ^ 1);
-                    } else {
-                        bool free_slot = lane == 0 ? mbar_test(&empty[ci.slot], ci.phase ^ 1) : false;
-                        if (!__shfl_sync(0xffffffffu, free_slot, 0)) break;
-                    }
-                }
+        while (ci.task < a.ntasks) {
+            {
+                if (ci.seq >= (uint32_t)a.S) mbar_wait(&empty[ci.slot], ci.phase ^ 1);
                 int vf, nr;
                 ci.rows(vf, nr);
                 int nreal = 0;  // rows that are not zero padding
@@ -242,7 +234,16 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 __syncwarp();
                 ci.next(a);
             }
-            // the oldest stage: wait for its bytes, write the padding columns, release it
+        }
+        return;
+    }
+    if (warp == 1) {
+        // ------------------------------------------- producer: padding + release
+        // once a stage's bytes have landed, write the padding columns the kept
+        // outputs read into the row margins and hand the stage to the consumers
+        StageCursor<P, Q, TAPS, LO> cf;
+        cf.start(a);
+        while (cf.task < a.ntasks) {
             mbar_wait(&full[cf.slot], cf.phase);
             {
                 int vf, nr;
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     }
 
     // ---------------------------------------------------------------- consumers
-    const int ctid = threadIdx.x - 32;
+    const int ctid = threadIdx.x - 64;
     const int span_id = ctid >> 4, span_e = ctid & 15;  // copy-out roles
     const int rowb = a.Wo * ESZ;
     const bool full_width = a.ntile == 1;

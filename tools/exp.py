@@ -1,0 +1,57 @@
+"""Quick kernel-time experiments on the GPU (developer tool).
+
+    python tools/exp.py C3 C4a C5 [--env FCFS_DEBUG_S=3,FCFS_DEBUG_S=4] [--reps 20]
+
+For each launch config and each env setting: median CUDA-event time of one
+fcfs_run over rotating buffers (> L2), achieved GB/s on algorithmic bytes.
+"""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+import paper_2203_10670_b200 as fc  # noqa: E402
+
+
+def time_cfg(name, reps, env):
+    for k in [k for k in os.environ if k.startswith("FCFS_DEBUG_")]:
+        del os.environ[k]
+    os.environ.update(env)
+    c = synth.CONFIGS[name]
+    pl = fc.Plan(c.p, c.q, c.mode, c.pad, c.C, c.H, c.W, c.dtype, "floor", c.is1d)
+    x = synth.make_input(c).cuda()
+    R = max(2, min(8, int(4 * 126e6 // (x.numel() * x.element_size() * 2)) + 1))
+    xs = [x.clone() for _ in range(R)]
+    ys = [torch.empty((c.N, c.C, pl.Ho, pl.Wo), dtype=x.dtype, device="cuda") for _ in range(R)]
+    for i in range(3):
+        pl.run(xs[i % R], out=ys[i % R])
+    torch.cuda.synchronize()
+    ts = []
+    for i in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        pl.run(xs[i % R], out=ys[i % R])
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    ts.sort()
+    med = ts[len(ts) // 2]
+    by = pl.compulsory_bytes(c.N)
+    return med, by / (med * 1e-6) / 1e9, pl.launch_info(c.N)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="+")
+    ap.add_argument("--env", default="")
+    ap.add_argument("--reps", type=int, default=20)
+    a = ap.parse_args()
+    envs = [{}] + [dict(kv.split("=") for kv in e.split("+")) for e in a.env.split(",") if e]
+    for name in a.configs:
+        for env in envs:
+            med, gbs, info = time_cfg(name, a.reps, env)
+            keys = {k: info[k] for k in ("NS", "CPT", "ntile", "S", "flush_groups", "grid") if k in info}
+            print(f"{name:4s} {str(env):34s} {med:9.1f} us {gbs:8.0f} GB/s {keys}", flush=True)
