@@ -80,6 +80,29 @@ __device__ __forceinline__ void load_win(const T *s, int e0, float (&win)[WIN]) 
     }
 }
 
+// Store KP (even) consecutive 16-bit outputs at sr (2-B aligned) with packed
+// conversions and 32-bit shared stores: when sr is not 4-B aligned the pairs
+// are realigned with a byte permute and the two end elements go out as 16-bit
+// stores (branch-free in the pair words).
+template <typename T, int KP>
+__device__ __forceinline__ void store_packed16(T *sr, const float (&o)[KP]) {
+    constexpr int NW = KP / 2;
+    uint32_t pk[NW];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) pk[i] = Pack2<T>::f(o[2 * i], o[2 * i + 1]);
+    const bool mis = (reinterpret_cast<uintptr_t>(sr) & 2) != 0;
+    uint32_t *w = reinterpret_cast<uint32_t *>(reinterpret_cast<uintptr_t>(sr) & ~uintptr_t(3)) + (mis ? 1 : 0);
+    const uint32_t sel = mis ? 0x5432u : 0x3210u;
+#pragma unroll
+    for (int j = 0; j < NW - 1; ++j) w[j] = __byte_perm(pk[j], pk[j + 1], sel);
+    if (mis) {
+        reinterpret_cast<unsigned short *>(sr)[0] = (unsigned short)pk[0];
+        reinterpret_cast<unsigned short *>(sr)[KP - 1] = (unsigned short)(pk[NW - 1] >> 16);
+    } else {
+        w[NW - 1] = pk[NW - 1];
+    }
+}
+
 // Geometry of one segment (plane x column tile).
 struct SegGeo {
     int plane, ch0, ch1, c0, c1, a0, a1;
@@ -204,7 +227,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         ci.start(a);
         while (ci.task < a.ntasks) {
             {
-                if (ci.seq >= (uint32_t)a.S) mbar_wait(&empty[ci.slot], ci.phase ^ 1);
+                if (ci.seq >= (uint32_t)a.S) mbar_wait_backoff(&empty[ci.slot], ci.phase ^ 1, 128);
                 int vf, nr;
                 ci.rows(vf, nr);
                 int nreal = 0;  // rows that are not zero padding
@@ -244,7 +267,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         StageCursor<P, Q, TAPS, LO> cf;
         cf.start(a);
         while (cf.task < a.ntasks) {
-            mbar_wait(&full[cf.slot], cf.phase);
+            mbar_wait_backoff(&full[cf.slot], cf.phase, 32);
             {
                 int vf, nr;
                 cf.rows(vf, nr);
@@ -288,13 +311,24 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     uint32_t fk = 0;     // flush counter: staging slot = fk & 1
     for (int task = blockIdx.x; task < a.ntasks; task += gridDim.x) {
         const BandInfo b = band_info<P>(a, task);
-        const int sgi = ctid / a.CPT;
-        const int chl = ctid - sgi * a.CPT;
+        // thread -> (segment, chunk): the last (possibly partial) chunk of every
+        // segment goes to the first consumer threads, so that only one warp ever
+        // takes the masked-store path
+        const bool last = ctid < b.nsg || a.CPT == 1;
+        int sgi, chl;
+        if (last) {
+            sgi = ctid;
+            chl = -1;
+        } else {
+            const int j = ctid - b.nsg;
+            sgi = j / (a.CPT - 1);
+            chl = j - sgi * (a.CPT - 1);
+        }
         const bool seg_ok = sgi < b.nsg;
         SegGeo sg = {0, 0, 0, 0, 0, 0, 1};
         if (seg_ok) sg = seg_geo<P, Q, TAPS, LO, K, ESZ>(a, b.group * a.NS + sgi);
-        const int chunk = sg.ch0 + chl;
-        const bool active = seg_ok && chunk < sg.ch1;
+        const int chunk = last ? sg.ch1 - 1 : sg.ch0 + chl;
+        const bool active = seg_ok && (last || chunk < sg.ch1 - 1);
         const int e0 = A + chunk * K * Q + LO - sg.a0;  // window start (element) in a shared row
         const int col = chunk * KP;
         const int nvalid = sg.c1 - col;  // outputs of this chunk inside the tile (>= KP: all)
@@ -419,6 +453,12 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                     }
                 }
                 T *sr = srow(jy);
+                if constexpr (ESZ == 2 && KP % 2 == 0) {
+                    if (nvalid >= KP) {  // every chunk but a segment's last (those sit in warp 2)
+                        store_packed16<T, KP>(sr, o);
+                        return;
+                    }
+                }
 #pragma unroll
                 for (int c = 0; c < KP; ++c)
                     if (c < nvalid) sr[c] = DT<T>::from_f(o[c]);
