@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         ci.start(a);
         while (ci.task < a.ntasks) {
             {
-                if (ci.seq >= (uint32_t)a.S) mbar_wait_backoff(&empty[ci.slot], ci.phase ^ 1, 128);
+                if (ci.seq >= (uint32_t)a.S) mbar_wait(&empty[ci.slot], ci.phase ^ 1);
                 int vf, nr;
                 ci.rows(vf, nr);
                 int nreal = 0;  // rows that are not zero padding
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         StageCursor<P, Q, TAPS, LO> cf;
         cf.start(a);
         while (cf.task < a.ntasks) {
-            mbar_wait_backoff(&full[cf.slot], cf.phase, 32);
+            mbar_wait(&full[cf.slot], cf.phase);
             {
                 int vf, nr;
                 cf.rows(vf, nr);

@@ -12,12 +12,14 @@
 // gather); registers are bounded so that 32+ warps stay resident per SM.
 // Source columns use a 32-bit multiply-shift division; source rows that no
 // output references are never read.
+#include <cstdlib>
+
 #include "device_common.cuh"
 
 namespace fcfs {
 
-template <typename T, int U, int RPW>
-__global__ void __launch_bounds__(256, 4) fcfs_nearest_kernel(const __grid_constant__ NearestArgs a) {
+template <typename T, int U, int RPW, int MINB>
+__global__ void __launch_bounds__(256, MINB) fcfs_nearest_kernel(const __grid_constant__ NearestArgs a) {
     const RunGeom &g = a.g;
     const int lane = threadIdx.x & 31;
     const uint32_t rows_total = (uint32_t)(g.planes * g.out_nrows);
@@ -69,17 +71,37 @@ __global__ void __launch_bounds__(256, 4) fcfs_nearest_kernel(const __grid_const
     }
 }
 
+template <typename T, int U, int RPW, int MINB>
+static void launch_nearest_v(const NearestArgs &a, cudaStream_t s) {
+    const int64_t rows = a.g.planes * a.g.out_nrows;
+    int64_t blocks = (rows + 8 * RPW - 1) / (8 * RPW);  // 8 warps per block
+    if (blocks > 148 * MINB) blocks = 148 * MINB;         // one resident wave, warps loop
+    fcfs_nearest_kernel<T, U, RPW, MINB><<<(int)blocks, 256, 0, s>>>(a);
+}
+
+// Variants (U columns per lane per pass, RPW rows per pass, CTAs per SM);
+// FCFS_DEBUG_NEAREST selects one for tuning sweeps.
+template <typename T>
+static void launch_nearest_t(const NearestArgs &a, cudaStream_t s) {
+    const char *e = std::getenv("FCFS_DEBUG_NEAREST");
+    switch (e ? std::atoi(e) : 0) {
+    case 1: launch_nearest_v<T, 8, 2, 4>(a, s); break;
+    case 2: launch_nearest_v<T, 8, 4, 4>(a, s); break;
+    case 3: launch_nearest_v<T, 16, 1, 4>(a, s); break;
+    case 4: launch_nearest_v<T, 12, 2, 3>(a, s); break;
+    case 5: launch_nearest_v<T, 12, 4, 2>(a, s); break;
+    default: launch_nearest_v<T, 12, 2, 4>(a, s); break;
+    }
+}
+
 int launch_nearest(int dtype, const NearestArgs &a, void *stream) {
     const int64_t rows = a.g.planes * a.g.out_nrows;
     if (rows == 0 || a.g.Wo == 0) return 0;
-    constexpr int RPW = 2, U = 12;
-    int64_t blocks = (rows + 8 * RPW - 1) / (8 * RPW);  // 8 warps per block
-    if (blocks > 148 * 4) blocks = 148 * 4;               // one resident wave (4 blocks/SM), warps loop
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     switch (dtype) {
-    case FCFS_F32: fcfs_nearest_kernel<float, U, RPW><<<(int)blocks, 256, 0, s>>>(a); break;
-    case FCFS_F16: fcfs_nearest_kernel<__half, U, RPW><<<(int)blocks, 256, 0, s>>>(a); break;
-    default: fcfs_nearest_kernel<__nv_bfloat16, U, RPW><<<(int)blocks, 256, 0, s>>>(a); break;
+    case FCFS_F32: launch_nearest_t<float>(a, s); break;
+    case FCFS_F16: launch_nearest_t<__half>(a, s); break;
+    default: launch_nearest_t<__nv_bfloat16>(a, s); break;
     }
     return (int)cudaGetLastError();
 }

@@ -19,6 +19,7 @@ all arithmetic runs in libfcfs.so.
 from __future__ import annotations
 
 import dataclasses
+import os
 
 
 @dataclasses.dataclass
@@ -246,6 +247,3 @@ def bench_strips(args, cfg, rank, world, dev, metric):
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
     return 0
-
-
-import os  # noqa: E402  (used by bench_strips)
