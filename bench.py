@@ -242,13 +242,25 @@ def main():
                                  device=dev) for _ in range(R)]
     torch.cuda.synchronize(dev)
 
+    # kernel launches of a step: nearest-gather launches of one dtype share one
+    # launch (fcfs_run_batch); every other launch is its own group
+    if len(launches) > 1 and all(L["plan"].kernel == "nearest_gather" for L in launches):
+        groups = [list(range(len(launches)))]
+    else:
+        groups = [[i] for i in range(len(launches))]
+
     def step(r, evs=None):
-        for i, L in enumerate(launches):
+        for gi, grp in enumerate(groups):
             if evs is not None:
-                evs[i][0].record(stream)
-            L["plan"].run(dev_inputs[L["key"]][r], out=L["outs"][r], stream=stream)
+                evs[gi][0].record(stream)
+            if len(grp) == 1:
+                L = launches[grp[0]]
+                L["plan"].run(dev_inputs[L["key"]][r], out=L["outs"][r], stream=stream)
+            else:
+                fc.run_batch([(launches[i]["plan"], dev_inputs[launches[i]["key"]][r], launches[i]["outs"][r])
+                              for i in grp], stream=stream)
             if evs is not None:
-                evs[i][1].record(stream)
+                evs[gi][1].record(stream)
 
     sampler = ClockSampler(physical_gpu_index(local))
     sampler.start()
@@ -265,7 +277,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in launches]
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in groups]
            for _ in range(args.steps)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_wall0 = time.time()
@@ -278,8 +290,8 @@ def main():
     if world > 1:
         dist.barrier()
     elapsed_ms = e0.elapsed_time(e1)
-    per_launch_ms = [sum(evs[s][i][0].elapsed_time(evs[s][i][1]) for s in range(args.steps)) / args.steps
-                     for i in range(len(launches))]
+    per_group_ms = [sum(evs[s][gi][0].elapsed_time(evs[s][gi][1]) for s in range(args.steps)) / args.steps
+                    for gi in range(len(groups))]
     if world > 1:
         t = torch.tensor([elapsed_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -292,13 +304,15 @@ def main():
     ms_per_step = elapsed_ms / args.steps
     value = world * outputs_per_step * args.steps / (elapsed_ms * 1e-3) / 1e6
     peak, peak_kind = peaks()
-    dom = max(range(len(launches)), key=lambda i: per_launch_ms[i])
-    dom_ms = per_launch_ms[dom]
-    achieved = launches[dom]["bytes"] / (dom_ms * 1e-3) / 1e9
+    dom = max(range(len(groups)), key=lambda gi: per_group_ms[gi])  # dominant kernel launch
+    dom_ms = per_group_ms[dom]
+    dom_name = "+".join(launches[i]["cfg"].name for i in groups[dom])
+    dom_bytes = sum(launches[i]["bytes"] for i in groups[dom])
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     traffic = None
     try:
         tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        traffic = tj.get(launches[dom]["cfg"].name)
+        traffic = tj.get(dom_name)
     except Exception:
         pass
 
@@ -314,8 +328,11 @@ def main():
             {"name": L["cfg"].name, "shape": [L["cfg"].N, L["cfg"].C, L["cfg"].H, L["cfg"].W],
              "factor": f"{L['cfg'].p}/{L['cfg'].q}", "mode": L["cfg"].mode, "pad": L["cfg"].pad,
              "dtype": L["cfg"].dtype, "out": [L["plan"].Ho, L["plan"].Wo], "kernel": L["plan"].kernel,
-             "compulsory_bytes": L["bytes"], "avg_launch_us": per_launch_ms[i] * 1e3}
+             "compulsory_bytes": L["bytes"],
+             "avg_launch_us": per_group_ms[next(gi for gi, g in enumerate(groups) if i in g)] * 1e3,
+             "shares_launch_with": [launches[j]["cfg"].name for g in groups if i in g for j in g if j != i]}
             for i, L in enumerate(launches)],
+            "launch_info": [launches[g[0]]["plan"].launch_info(launches[g[0]]["cfg"].N) for g in groups],
             "per_rank_batch": "own batch per rank (weak scaling)",
             "l2": f"rotating {R} buffer sets of {set_bytes / 2**20:.0f} MiB (> 4x {l2 / 2**20:.0f} MiB L2); no flush",
             "soak_s": args.soak_s, "parallelism": f"dp{world}"},
@@ -323,11 +340,12 @@ def main():
         "achieved_GBps_step": bytes_per_step / (ms_per_step * 1e-3) / 1e9,
         "frac_of_8TBps_step": bytes_per_step / (ms_per_step * 1e-3) / 8e12,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": launches[dom]["plan"].kernel, "launch": launches[dom]["cfg"].name,
+                     "traffic": traffic, "kernel": launches[groups[dom][0]]["plan"].kernel, "launch": dom_name,
                      "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs" if peak_kind == "measured" else
                      "fallback 6.65 TB/s (B200_PROFILING.md)",
-                     "algorithmic_bytes_per_launch": launches[dom]["bytes"], "avg_launch_us": dom_ms * 1e3},
-        "gpu_launches": args.steps * len(launches),
+                     "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_us": dom_ms * 1e3,
+                     "timing": "CUDA events around each launch on the launching stream, timed region average"},
+        "gpu_launches": args.steps * len(groups),
         "clocks": clocks,
     }
     if e2e is not None:

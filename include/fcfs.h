@@ -110,6 +110,23 @@ fcfs_status fcfs_output_shape(fcfs_plan_t plan, int64_t *Ho, int64_t *Wo);
  * Errors: FCFS_E_ARG (NULL/overlap), FCFS_E_DEVICE, FCFS_E_CUDA. */
 fcfs_status fcfs_run(fcfs_plan_t plan, const void *in, void *out, int64_t N, void *stream);
 
+/* One job of fcfs_run_batch: fcfs_run(plan, in, out, N, stream). */
+typedef struct {
+    fcfs_plan_t plan;
+    const void *in;
+    void *out;
+    int64_t N;
+} fcfs_job;
+
+/* fcfs_run_batch -- run njobs independent jobs on one stream, as if by
+ * fcfs_run in order, in as few kernel launches as possible (consecutive
+ * nearest-neighbour jobs of one dtype share one launch: e.g. several levels of
+ * a multi-scale pyramid of the same batch).  Jobs must be independent: no
+ * job's output may overlap any job's input or output (FCFS_E_ARG).  Every job
+ * is validated before anything is launched.  Errors: as fcfs_run,
+ * FCFS_E_NOMEM. */
+fcfs_status fcfs_run_batch(const fcfs_job *jobs, int njobs, void *stream);
+
 /* fcfs_run_rows -- scale only output rows [out_row0, out_row0 + out_nrows)
  * of every plane, reading only input rows [in_row0, in_row0 + in_nrows).
  * H in the plan is the GLOBAL height: padding is applied at global rows 0 and

@@ -7,6 +7,6 @@ Public API:
     dist                                      -- multi-GPU drivers (batch shards, row strips + NCCL halo)
 """
 from ._lib import FcfsError, LIB_PATH  # noqa: F401  (raises ImportError if libfcfs.so is missing)
-from .fcfs import Plan, get_plan, scale  # noqa: F401
+from .fcfs import Plan, get_plan, run_batch, scale  # noqa: F401
 
-__all__ = ["Plan", "get_plan", "scale", "FcfsError", "LIB_PATH"]
+__all__ = ["Plan", "get_plan", "run_batch", "scale", "FcfsError", "LIB_PATH"]

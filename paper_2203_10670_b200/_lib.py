@@ -21,6 +21,10 @@ i64, i32, u32, vp = ctypes.c_int64, ctypes.c_int, ctypes.c_uint, ctypes.c_void_p
 P64 = ctypes.POINTER(ctypes.c_int64)
 
 
+class Job(ctypes.Structure):
+    _fields_ = [("plan", vp), ("in_", vp), ("out", vp), ("N", i64)]
+
+
 class PlanInfo(ctypes.Structure):
     _fields_ = [("p", i32), ("q", i32), ("mode", i32), ("pad", i32), ("dtype", i32), ("flags", u32),
                 ("C", i64), ("H", i64), ("W", i64), ("Ho", i64), ("Wo", i64), ("ntaps", i32), ("lo", i32),
@@ -34,6 +38,7 @@ SIGNATURES = {
     "fcfs_output_shape": (i32, [vp, P64, P64]),
     "fcfs_run": (i32, [vp, vp, vp, i64, vp]),
     "fcfs_run_rows": (i32, [vp, vp, i64, i64, vp, i64, i64, i64, vp]),
+    "fcfs_run_batch": (i32, [vp, i32, vp]),
     "fcfs_strip_rows": (i32, [vp, i64, i64, P64, P64, P64, P64]),
     "fcfs_needed_rows": (i32, [vp, i64, i64, P64, P64]),
     "fcfs_run_host": (i32, [vp, vp, vp, i64, vp, vp, vp]),

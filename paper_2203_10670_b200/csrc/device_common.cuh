@@ -105,10 +105,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
-// Wait with a sleeping back-off between probes: for the producer warps, which
-// run ahead of the consumers and must not steal their issue slots by polling.
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t parity, uint32_t ns);
-
 // Non-blocking probe of phase `parity`.
 __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
     uint32_t ok;
@@ -121,25 +117,6 @@ __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
-
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t parity, uint32_t ns) {
-    while (!mbar_test(bar, parity)) __nanosleep(ns);
-}
-
-// ---- 16-bit output packing ---------------------------------------------------
-template <typename T> struct Pack2;
-template <> struct Pack2<__nv_bfloat16> {  // cvt.rn.bf16x2.f32: lo = a, hi = b
-    static __device__ __forceinline__ uint32_t f(float a, float b) {
-        __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
-        return *reinterpret_cast<uint32_t *>(&v);
-    }
-};
-template <> struct Pack2<__half> {  // cvt.rn.f16x2.f32
-    static __device__ __forceinline__ uint32_t f(float a, float b) {
-        __half2 v = __floats2half2_rn(a, b);
-        return *reinterpret_cast<uint32_t *>(&v);
-    }
-};
 
 // ---- bulk async copy shared -> global (TMA engine, 1D), bulk-group completion ----
 __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {

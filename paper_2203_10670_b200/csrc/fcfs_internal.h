@@ -91,9 +91,18 @@ struct FusedArgs {
     float w[16][4];      // phase weights (fused variants have p <= 16)
 };
 
+// Several nearest jobs (same dtype) in one launch (fcfs_run_batch).
+constexpr int kMaxBatchJobs = 8;
+struct NearestBatch {
+    int njobs;
+    uint32_t pass_prefix[kMaxBatchJobs + 1];  // filled by the launcher
+    NearestArgs job[kMaxBatchJobs];
+};
+
 // Launchers (host functions defined in the .cu files).  Return cudaError_t as int.
 int launch_reference(int dtype, const RefArgs &a, void *stream);
 int launch_nearest(int dtype, const NearestArgs &a, void *stream);
+int launch_nearest_batch(int dtype, const NearestBatch &nb, void *stream);
 
 // Fused: the variant table.  fused_lookup returns an opaque kernel handle or
 // nullptr when (dtype, p, q, ntaps) has no compiled instantiation; K (periods

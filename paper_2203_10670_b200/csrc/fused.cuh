@@ -49,6 +49,35 @@ struct Geo {
     static __host__ __device__ constexpr int last_row(int j) { return j == 0 ? -LO : base(j) + TAPS - 1; }
 };
 
+// Phase weights as compile-time constants (folded into the FMAs as
+// immediates).  Same closed forms and the same double -> fp32 rounding as the
+// plan's table (plan.cpp phase_table); the plan checks the two are identical
+// (FusedVariant::wtab) before it selects a fused variant.
+//   bilinear (§5.2.2): (1 - f, f), f = k/P;
+//   bicubic  (§5.2.3, Keys a = -1/2): numerators over 2P^3 (exact integers).
+template <int P, int Q, int TAPS>
+struct PhaseW {
+    static constexpr float w(int j, int t) {
+        const long long K = ((long long)j * Q) % P, PP = P, d = 2 * PP * PP * PP;
+        if (TAPS == 2) return t == 0 ? (float)((double)(PP - K) / (double)PP) : (float)((double)K / (double)PP);
+        const long long n = t == 0   ? -K * K * K + 2 * K * K * PP - K * PP * PP
+                            : t == 1 ? 3 * K * K * K - 5 * K * K * PP + 2 * PP * PP * PP
+                            : t == 2 ? -3 * K * K * K + 4 * K * K * PP + K * PP * PP
+                                     : K * K * K - K * K * PP;
+        return (float)((double)n / (double)d);
+    }
+    struct Table {
+        float v[16 * 4];
+    };
+    static constexpr Table table() {
+        Table tb{};
+        for (int j = 0; j < P; ++j)
+            for (int t = 0; t < TAPS; ++t) tb.v[4 * j + t] = w(j, t);
+        return tb;
+    }
+    static constexpr Table tab = table();
+};
+
 template <typename T> struct HalfBits;
 template <> struct HalfBits<__half> {
     static __device__ __forceinline__ float f(uint32_t b) { return __half2float(__ushort_as_half((unsigned short)b)); }
@@ -77,29 +106,6 @@ __device__ __forceinline__ void load_win(const T *s, int e0, float (&win)[WIN]) 
             uint32_t b1 = ((i + 1) & 1) ? (wd[(i + 1) >> 1] >> 16) : (wd[(i + 1) >> 1] & 0xffffu);
             win[i] = HalfBits<T>::f(odd ? b1 : b0);
         }
-    }
-}
-
-// Store KP (even) consecutive 16-bit outputs at sr (2-B aligned) with packed
-// conversions and 32-bit shared stores: when sr is not 4-B aligned the pairs
-// are realigned with a byte permute and the two end elements go out as 16-bit
-// stores (branch-free in the pair words).
-template <typename T, int KP>
-__device__ __forceinline__ void store_packed16(T *sr, const float (&o)[KP]) {
-    constexpr int NW = KP / 2;
-    uint32_t pk[NW];
-#pragma unroll
-    for (int i = 0; i < NW; ++i) pk[i] = Pack2<T>::f(o[2 * i], o[2 * i + 1]);
-    const bool mis = (reinterpret_cast<uintptr_t>(sr) & 2) != 0;
-    uint32_t *w = reinterpret_cast<uint32_t *>(reinterpret_cast<uintptr_t>(sr) & ~uintptr_t(3)) + (mis ? 1 : 0);
-    const uint32_t sel = mis ? 0x5432u : 0x3210u;
-#pragma unroll
-    for (int j = 0; j < NW - 1; ++j) w[j] = __byte_perm(pk[j], pk[j + 1], sel);
-    if (mis) {
-        reinterpret_cast<unsigned short *>(sr)[0] = (unsigned short)pk[0];
-        reinterpret_cast<unsigned short *>(sr)[KP - 1] = (unsigned short)(pk[NW - 1] >> 16);
-    } else {
-        w[NW - 1] = pk[NW - 1];
     }
 }
 
@@ -453,15 +459,14 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                     }
                 }
                 T *sr = srow(jy);
-                if constexpr (ESZ == 2 && KP % 2 == 0) {
-                    if (nvalid >= KP) {  // every chunk but a segment's last (those sit in warp 2)
-                        store_packed16<T, KP>(sr, o);
-                        return;
-                    }
-                }
+                if (nvalid >= KP) {  // every chunk but a segment's last (those sit in warp 2)
 #pragma unroll
-                for (int c = 0; c < KP; ++c)
-                    if (c < nvalid) sr[c] = DT<T>::from_f(o[c]);
+                    for (int c = 0; c < KP; ++c) sr[c] = DT<T>::from_f(o[c]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < KP; ++c)
+                        if (c < nvalid) sr[c] = DT<T>::from_f(o[c]);
+                }
             };
             // one named barrier, then bulk stores of flush group g
             auto flush = [&](int g) {

@@ -3,15 +3,16 @@
 //     out[m_y][m_x] = x~[floor(m_y*q/p)][floor(m_x*q/p)]
 // with no arithmetic on the value (bit-exact; -0, NaN and Inf pass through).
 //
-// Layout: a warp handles RPW output rows per pass (grid-stride over
-// planes x rows); the lanes sweep the columns, 32 consecutive outputs per
-// instruction, so every load instruction reads a short contiguous run of the
-// source row and every store instruction writes 32 consecutive outputs
-// (coalesced whatever the row pitch).  All RPW x U loads of a pass are issued
-// before the first store (memory-level parallelism for a latency-bound
-// gather); registers are bounded so that 32+ warps stay resident per SM.
-// Source columns use a 32-bit multiply-shift division; source rows that no
-// output references are never read.
+// Layout: a warp handles RPW output rows per pass (grid-stride over the
+// passes of every job of the launch); the lanes sweep the columns, 32
+// consecutive outputs per instruction, so every load instruction reads a short
+// contiguous run of the source row and every store instruction writes 32
+// consecutive outputs (coalesced whatever the row pitch).  All RPW x U loads of
+// a pass are issued before the first store (memory-level parallelism for a
+// latency-bound gather); registers are bounded so that 32+ warps stay resident
+// per SM.  Source columns use a 32-bit multiply-shift division; source rows
+// that no output references are never read.  One launch can carry several
+// jobs (fcfs_run_batch: e.g. the levels of a multi-scale pyramid of one batch).
 #include <cstdlib>
 
 #include "device_common.cuh"
@@ -19,17 +20,21 @@
 namespace fcfs {
 
 template <typename T, int U, int RPW, int MINB>
-__global__ void __launch_bounds__(256, MINB) fcfs_nearest_kernel(const __grid_constant__ NearestArgs a) {
-    const RunGeom &g = a.g;
+__global__ void __launch_bounds__(256, MINB) fcfs_nearest_kernel(const __grid_constant__ NearestBatch nb) {
     const int lane = threadIdx.x & 31;
-    const uint32_t rows_total = (uint32_t)(g.planes * g.out_nrows);
     const uint32_t warp0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    const int32_t W = (int32_t)g.W, Wo = (int32_t)g.Wo, H = (int32_t)g.H;
-    const uint32_t q = (uint32_t)a.q;
-    const T *__restrict__ in = static_cast<const T *>(g.in);
-    T *__restrict__ out = static_cast<T *>(g.out);
-    for (uint32_t rw0 = warp0 * RPW; rw0 < rows_total; rw0 += nwarps * RPW) {
+    for (uint32_t gp = warp0; gp < nb.pass_prefix[nb.njobs]; gp += nwarps) {
+        int j = 0;
+        while (j + 1 < nb.njobs && gp >= nb.pass_prefix[j + 1]) ++j;
+        const NearestArgs &a = nb.job[j];
+        const RunGeom &g = a.g;
+        const uint32_t rows_total = (uint32_t)(g.planes * g.out_nrows);
+        const int32_t W = (int32_t)g.W, Wo = (int32_t)g.Wo, H = (int32_t)g.H;
+        const uint32_t q = (uint32_t)a.q;
+        const T *__restrict__ in = static_cast<const T *>(g.in);
+        T *__restrict__ out = static_cast<T *>(g.out);
+        const uint32_t rw0 = (gp - nb.pass_prefix[j]) * RPW;
         const T *irow[RPW];
         T *orow[RPW];
         bool rd[RPW], wr[RPW];  // row reads its source / row exists
@@ -72,38 +77,49 @@ __global__ void __launch_bounds__(256, MINB) fcfs_nearest_kernel(const __grid_co
 }
 
 template <typename T, int U, int RPW, int MINB>
-static void launch_nearest_v(const NearestArgs &a, cudaStream_t s) {
-    const int64_t rows = a.g.planes * a.g.out_nrows;
-    int64_t blocks = (rows + 8 * RPW - 1) / (8 * RPW);  // 8 warps per block
-    if (blocks > 148 * MINB) blocks = 148 * MINB;         // one resident wave, warps loop
-    fcfs_nearest_kernel<T, U, RPW, MINB><<<(int)blocks, 256, 0, s>>>(a);
+static void launch_nearest_v(NearestBatch nb, cudaStream_t s) {
+    nb.pass_prefix[0] = 0;
+    for (int j = 0; j < nb.njobs; ++j) {
+        const int64_t rows = nb.job[j].g.planes * nb.job[j].g.out_nrows;
+        nb.pass_prefix[j + 1] = nb.pass_prefix[j] + (uint32_t)((rows + RPW - 1) / RPW);
+    }
+    int64_t blocks = ((int64_t)nb.pass_prefix[nb.njobs] + 7) / 8;  // 8 warps per block
+    if (blocks > 148 * MINB) blocks = 148 * MINB;                    // one resident wave, warps loop
+    if (blocks > 0) fcfs_nearest_kernel<T, U, RPW, MINB><<<(int)blocks, 256, 0, s>>>(nb);
 }
 
 // Variants (U columns per lane per pass, RPW rows per pass, CTAs per SM);
 // FCFS_DEBUG_NEAREST selects one for tuning sweeps.
 template <typename T>
-static void launch_nearest_t(const NearestArgs &a, cudaStream_t s) {
+static void launch_nearest_t(const NearestBatch &nb, cudaStream_t s) {
     const char *e = std::getenv("FCFS_DEBUG_NEAREST");
     switch (e ? std::atoi(e) : 0) {
-    case 1: launch_nearest_v<T, 8, 2, 4>(a, s); break;
-    case 2: launch_nearest_v<T, 8, 4, 4>(a, s); break;
-    case 3: launch_nearest_v<T, 16, 1, 4>(a, s); break;
-    case 4: launch_nearest_v<T, 12, 2, 3>(a, s); break;
-    case 5: launch_nearest_v<T, 12, 4, 2>(a, s); break;
-    default: launch_nearest_v<T, 12, 2, 4>(a, s); break;
+    case 1: launch_nearest_v<T, 8, 2, 4>(nb, s); break;
+    case 2: launch_nearest_v<T, 8, 4, 4>(nb, s); break;
+    case 3: launch_nearest_v<T, 16, 1, 4>(nb, s); break;
+    case 4: launch_nearest_v<T, 12, 2, 3>(nb, s); break;
+    case 5: launch_nearest_v<T, 12, 4, 2>(nb, s); break;
+    default: launch_nearest_v<T, 12, 2, 4>(nb, s); break;
     }
 }
 
-int launch_nearest(int dtype, const NearestArgs &a, void *stream) {
-    const int64_t rows = a.g.planes * a.g.out_nrows;
-    if (rows == 0 || a.g.Wo == 0) return 0;
+int launch_nearest_batch(int dtype, const NearestBatch &nb, void *stream) {
+    if (nb.njobs <= 0) return 0;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     switch (dtype) {
-    case FCFS_F32: launch_nearest_t<float>(a, s); break;
-    case FCFS_F16: launch_nearest_t<__half>(a, s); break;
-    default: launch_nearest_t<__nv_bfloat16>(a, s); break;
+    case FCFS_F32: launch_nearest_t<float>(nb, s); break;
+    case FCFS_F16: launch_nearest_t<__half>(nb, s); break;
+    default: launch_nearest_t<__nv_bfloat16>(nb, s); break;
     }
     return (int)cudaGetLastError();
+}
+
+int launch_nearest(int dtype, const NearestArgs &a, void *stream) {
+    if (a.g.planes * a.g.out_nrows == 0 || a.g.Wo == 0) return 0;
+    NearestBatch nb;
+    nb.njobs = 1;
+    nb.job[0] = a;
+    return launch_nearest_batch(dtype, nb, stream);
 }
 
 }  // namespace fcfs

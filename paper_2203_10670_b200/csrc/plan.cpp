@@ -309,8 +309,22 @@ int select_kernel(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     return kernel;
 }
 
-fcfs_status run_window(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t in_nrows, void *out,
-                       int64_t out_row0, int64_t out_nrows, int64_t N, void *stream) {
+// A validated launch: which kernel, with what arguments.
+struct Prepared {
+    fcfs_plan_t pl;
+    int kernel;  // -1: nothing to do
+    NearestArgs na;
+    RefArgs ra;
+    FusedLaunch L;
+    const void *in;
+    void *out;
+    int64_t in_bytes, out_bytes;
+};
+
+fcfs_status prepare(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t in_nrows, void *out, int64_t out_row0,
+                    int64_t out_nrows, int64_t N, Prepared &pr) {
+    pr.kernel = -1;
+    pr.pl = pl;
     if (!pl || N < 0) return FCFS_E_ARG;
     if (in_row0 < 0 || in_nrows < 1 || in_row0 + in_nrows > pl->H) return FCFS_E_ARG;
     if (out_row0 < 0 || out_nrows < 0 || out_row0 + out_nrows > pl->Ho) return FCFS_E_ARG;
@@ -341,11 +355,13 @@ fcfs_status run_window(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t 
     g.in_plane_stride = in_nrows * pl->W;
     g.out_plane_stride = out_nrows * pl->Wo;
 
-    FusedLaunch L;
-    const int kernel = select_kernel(pl, g, L);
-    int rc = 0;
-    if (kernel == 1) {
-        NearestArgs a;
+    pr.in = in;
+    pr.out = out;
+    pr.in_bytes = in_bytes;
+    pr.out_bytes = out_bytes;
+    pr.kernel = select_kernel(pl, g, pr.L);
+    if (pr.kernel == 1) {
+        NearestArgs &a = pr.na;
         a.g = g;
         a.div_wo = make_fastdiv((uint32_t)pl->Wo);
         a.div_rows = make_fastdiv((uint32_t)out_nrows);
@@ -355,18 +371,30 @@ fcfs_status run_window(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t 
         a.pad = pl->pad;
         a.is1d = pl->is1d;
         a.vec_ok = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-        rc = launch_nearest(pl->dtype, a, stream);
-    } else if (kernel == 2) {
-        rc = launch_fused(pl->fused, L.a, L.grid, kFusedThreads, L.smem, stream);
-    } else {
-        RefArgs a;
+    } else if (pr.kernel == 0) {
+        RefArgs &a = pr.ra;
         a.g = g;
         a.t = pl->tab;
         a.pad = pl->pad;
         a.is1d = pl->is1d;
-        rc = launch_reference(pl->dtype, a, stream);
     }
+    return FCFS_OK;
+}
+
+fcfs_status launch(const Prepared &pr, void *stream) {
+    int rc = 0;
+    if (pr.kernel == 1) rc = launch_nearest(pr.pl->dtype, pr.na, stream);
+    else if (pr.kernel == 2) rc = launch_fused(pr.pl->fused, pr.L.a, pr.L.grid, kFusedThreads, pr.L.smem, stream);
+    else if (pr.kernel == 0) rc = launch_reference(pr.pl->dtype, pr.ra, stream);
     return rc == 0 ? FCFS_OK : FCFS_E_CUDA;
+}
+
+fcfs_status run_window(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t in_nrows, void *out,
+                       int64_t out_row0, int64_t out_nrows, int64_t N, void *stream) {
+    Prepared pr;
+    fcfs_status st = prepare(pl, in, in_row0, in_nrows, out, out_row0, out_nrows, N, pr);
+    if (st != FCFS_OK || pr.kernel < 0) return st;
+    return launch(pr, stream);
 }
 
 }  // namespace
@@ -513,6 +541,55 @@ fcfs_status fcfs_strip_rows(fcfs_plan_t pl, int64_t own0, int64_t own1, int64_t 
         return FCFS_OK;
     }
     needed_rows(pl, m0, m1, need0, need1);
+    return FCFS_OK;
+}
+
+fcfs_status fcfs_run_batch(const fcfs_job *jobs, int njobs, void *stream) {
+    if (njobs < 0 || (njobs > 0 && !jobs)) return FCFS_E_ARG;
+    std::vector<Prepared> pr;
+    try {
+        pr.resize((size_t)njobs);
+    } catch (...) {
+        return FCFS_E_NOMEM;
+    }
+    for (int i = 0; i < njobs; ++i) {
+        const fcfs_plan_t pl = jobs[i].plan;
+        if (!pl) return FCFS_E_ARG;
+        fcfs_status st = prepare(pl, jobs[i].in, 0, pl->H, jobs[i].out, 0, pl->Ho, jobs[i].N, pr[i]);
+        if (st != FCFS_OK) return st;
+    }
+    // jobs must be independent: no output overlaps another job's input or output
+    for (int i = 0; i < njobs; ++i) {
+        if (pr[i].kernel < 0) continue;
+        for (int j = 0; j < njobs; ++j) {
+            if (j == i || pr[j].kernel < 0) continue;
+            if (ranges_overlap(pr[i].out, pr[i].out_bytes, pr[j].in, pr[j].in_bytes) ||
+                ranges_overlap(pr[i].out, pr[i].out_bytes, pr[j].out, pr[j].out_bytes))
+                return FCFS_E_ARG;
+        }
+    }
+    // consecutive nearest-gather jobs of one dtype share a launch
+    for (int i = 0; i < njobs;) {
+        if (pr[i].kernel == 1) {
+            NearestBatch nb;
+            nb.njobs = 0;
+            const int dt = pr[i].pl->dtype;
+            int j = i;
+            while (j < njobs && nb.njobs < kMaxBatchJobs && (pr[j].kernel == 1 || pr[j].kernel < 0) &&
+                   (pr[j].kernel < 0 || pr[j].pl->dtype == dt)) {
+                if (pr[j].kernel == 1) nb.job[nb.njobs++] = pr[j].na;
+                ++j;
+            }
+            if (launch_nearest_batch(dt, nb, stream) != 0) return FCFS_E_CUDA;
+            i = j;
+        } else {
+            if (pr[i].kernel >= 0) {
+                fcfs_status st = launch(pr[i], stream);
+                if (st != FCFS_OK) return st;
+            }
+            ++i;
+        }
+    }
     return FCFS_OK;
 }
 

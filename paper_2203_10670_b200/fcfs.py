@@ -148,6 +148,22 @@ class Plan:
         return out_host
 
 
+def run_batch(jobs, stream=None):
+    """Run [(plan, x, out), ...] (independent jobs) with fcfs_run_batch: compatible
+    jobs share kernel launches.  Outputs must be preallocated."""
+    import torch
+    arr = (_lib.Job * len(jobs))()
+    for i, (pl, x, out) in enumerate(jobs):
+        N = x.shape[0]
+        pl._check_tensor(x, (N, pl.C, pl.H, pl.W), "input")
+        pl._check_tensor(out, (N, pl.C, pl.Ho, pl.Wo), "output")
+        arr[i] = _lib.Job(pl.handle.value, x.data_ptr(), out.data_ptr(), N)
+    s = torch.cuda.current_stream() if stream is None else stream
+    check(_lib.lib.fcfs_run_batch(ctypes.cast(arr, ctypes.c_void_p), len(jobs), ctypes.c_void_p(s.cuda_stream)),
+          "fcfs_run_batch")
+    return [out for _, _, out in jobs]
+
+
 _cache: dict = {}
 _cache_lock = threading.Lock()
 

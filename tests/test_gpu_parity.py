@@ -272,6 +272,24 @@ def test_run_host_end_to_end():
     assert torch.equal(out.view(torch.int16), pl.run(x.to(DEV)).cpu().view(torch.int16))
 
 
+def test_run_batch_matches_single_runs():
+    """A multi-scale pyramid of one batch in one fcfs_run_batch call (nearest
+    levels share a launch) equals the individual runs bit for bit."""
+    x = _rand_input(21, (2, 3, 96, 160), "float32").to(DEV)
+    specs = [(2, 3, "nearest"), (3, 4, "nearest"), (1, 2, "nearest"), (5, 3, "bicubic"), (3, 5, "nearest"),
+             (7, 5, "bilinear")]
+    plans = [Plan(p, q, m, "replicate", 3, 96, 160, "float32", "floor") for p, q, m in specs]
+    outs = [torch.empty((2, 3, pl.Ho, pl.Wo), device=DEV) for pl in plans]
+    fc.run_batch([(pl, x, o) for pl, o in zip(plans, outs)])
+    torch.cuda.synchronize()
+    for pl, o in zip(plans, outs):
+        assert torch.equal(o, pl.run(x))
+    # overlapping jobs are refused before anything runs
+    with pytest.raises(FcfsError) as e:
+        fc.run_batch([(plans[0], x, outs[0]), (plans[0], x, outs[0])])
+    assert e.value.name == "FCFS_E_ARG"
+
+
 def test_streams_and_concurrency():
     cfg = synth.CONFIGS["C4b"]
     x = synth.make_input(cfg, 0, 2).to(DEV)
