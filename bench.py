@@ -134,7 +134,8 @@ def oracle_sample_run(cfgs, planes_per_cfg: int):
         if cfg.values == "field":
             rows = (0, min(cfg.H, 600))
             x = synth.make_values(cfg, 0, 1, rows=rows)
-            Ho_rows = (0, (rows[1] * cfg.p) // cfg.q - 2)
+            # output rows whose whole hidden-row window lies inside the sampled input rows
+            Ho_rows = (0, ((rows[1] - 2 * cfg.q - 4) // cfg.q) * cfg.p)
             t0 = time.perf_counter()
             y = oracle.staged(x[0], cfg.p, cfg.q, cfg.mode, cfg.pad, floor_extent=True, rows=Ho_rows, H=cfg.H)
             secs += time.perf_counter() - t0
@@ -150,18 +151,23 @@ def oracle_sample_run(cfgs, planes_per_cfg: int):
     return outs, secs, "; ".join(parts)
 
 
-def cpu_baseline(cfgs, budget_s=15.0):
+def cpu_baseline(cfgs, budget_s=10.0):
+    """The oracle as it stands on this host's cores: a sample of the workload
+    grown (then repeated) until it has run about budget_s seconds."""
     cores = os.cpu_count() or 1
     planes = max(1, cores)
     outs, secs, desc = oracle_sample_run(cfgs, planes)
-    # grow the sample toward the time budget (bounded)
-    while secs < budget_s / 4 and planes < 4096:
+    while secs < budget_s / 8 and not all(planes >= c.planes for c in cfgs):
         planes *= 4
         outs, secs, desc = oracle_sample_run(cfgs, planes)
-        if all(planes >= c.planes for c in cfgs):
-            break
-    return {"value": outs / secs / 1e6, "unit": "Mpix/s", "cores": cores, "kind": "oracle",
-            "sample": f"staged C oracle (double, OpenMP {cores} threads) on {desc}; {secs:.2f} s"}
+    tot_o, tot_s, reps = outs, secs, 1
+    while tot_s < budget_s and reps < 1000:
+        o, s, _ = oracle_sample_run(cfgs, planes)
+        tot_o += o
+        tot_s += s
+        reps += 1
+    return {"value": tot_o / tot_s / 1e6, "unit": "Mpix/s", "cores": cores, "kind": "oracle",
+            "sample": f"staged C oracle (double, OpenMP {cores} threads) on {desc}, {reps} passes; {tot_s:.1f} s"}
 
 
 def run_reference(args):
@@ -332,7 +338,8 @@ def main():
              "avg_launch_us": per_group_ms[next(gi for gi, g in enumerate(groups) if i in g)] * 1e3,
              "shares_launch_with": [launches[j]["cfg"].name for g in groups if i in g for j in g if j != i]}
             for i, L in enumerate(launches)],
-            "launch_info": [launches[g[0]]["plan"].launch_info(launches[g[0]]["cfg"].N) for g in groups],
+            "launch_info": [dict(launches[g[0]]["plan"].launch_info(launches[g[0]]["cfg"].N),
+                                 jobs=[launches[i]["cfg"].name for i in g]) for g in groups],
             "per_rank_batch": "own batch per rank (weak scaling)",
             "l2": f"rotating {R} buffer sets of {set_bytes / 2**20:.0f} MiB (> 4x {l2 / 2**20:.0f} MiB L2); no flush",
             "soak_s": args.soak_s, "parallelism": f"dp{world}"},

@@ -88,7 +88,6 @@ struct FusedArgs {
     int32_t G;           // output flush groups per y-period (1: rows [0,P); 2: [0,JM) and [JM,P))
     int32_t JM;          // first output row of group 1 (= P when G == 1)
     int32_t rfix;        // right padding columns kept outputs read (written by the producer)
-    float w[16][4];      // phase weights (fused variants have p <= 16)
 };
 
 // Several nearest jobs (same dtype) in one launch (fcfs_run_batch).
@@ -110,6 +109,7 @@ int launch_nearest_batch(int dtype, const NearestBatch &nb, void *stream);
 struct FusedVariant {
     const void *fn;
     int P, Q, TAPS, LO, K;
+    const float *wtab;  // the variant's compile-time phase weights, [4*j + t]
 };
 const FusedVariant *fused_lookup(int dtype, int p, int q, int ntaps);
 int launch_fused(const FusedVariant *v, const FusedArgs &a, int grid, int block, int smem, void *stream);

@@ -57,7 +57,7 @@ struct Geo {
 //   bicubic  (§5.2.3, Keys a = -1/2): numerators over 2P^3 (exact integers).
 template <int P, int Q, int TAPS>
 struct PhaseW {
-    static constexpr float w(int j, int t) {
+    static __host__ __device__ constexpr float w(int j, int t) {
         const long long K = ((long long)j * Q) % P, PP = P, d = 2 * PP * PP * PP;
         if (TAPS == 2) return t == 0 ? (float)((double)(PP - K) / (double)PP) : (float)((double)K / (double)PP);
         const long long n = t == 0   ? -K * K * K + 2 * K * K * PP - K * PP * PP
@@ -196,6 +196,7 @@ struct StageCursor {
 template <typename T, int P, int Q, int TAPS, int LO, int K>
 __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __grid_constant__ FusedArgs a) {
     using G = Geo<P, Q, TAPS, LO>;
+    using WT = PhaseW<P, Q, TAPS>;
     constexpr int L = G::L, C = G::C;
     constexpr int KP = K * P;
     constexpr int WIN = (K - 1) * Q + L;
@@ -372,10 +373,10 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                         h[P] = win[Q - LO];
                     } else {
                         const int bb = G::base(jx);
-                        float2 v2 = fmul2_rn(a.w[jx][0], make_float2(win[bb], win[Q + bb]));
+                        float2 v2 = fmul2_rn(WT::w(jx, 0), make_float2(win[bb], win[Q + bb]));
 #pragma unroll
                         for (int tp = 1; tp < TAPS; ++tp)
-                            v2 = ffma2_rn(a.w[jx][tp], make_float2(win[bb + tp], win[Q + bb + tp]), v2);
+                            v2 = ffma2_rn(WT::w(jx, tp), make_float2(win[bb + tp], win[Q + bb + tp]), v2);
                         h[jx] = v2.x;
                         h[P + jx] = v2.y;
                     }
@@ -390,9 +391,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                             v2 = win[k * Q - LO];  // fraction 0: the tap at offset 0, exactly
                         } else {
                             const int bb = k * Q + G::base(jx);
-                            v2 = __fmul_rn(a.w[jx][0], win[bb]);
+                            v2 = __fmul_rn(WT::w(jx, 0), win[bb]);
 #pragma unroll
-                            for (int tp = 1; tp < TAPS; ++tp) v2 = __fmaf_rn(a.w[jx][tp], win[bb + tp], v2);
+                            for (int tp = 1; tp < TAPS; ++tp) v2 = __fmaf_rn(WT::w(jx, tp), win[bb + tp], v2);
                         }
                         h[k * P + jx] = v2;
                     }
@@ -443,18 +444,18 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                     constexpr int H2 = KP / 2;  // columns c and c + H2 share the row weights
 #pragma unroll
                     for (int c = 0; c < H2; ++c) {
-                        float2 v2 = fmul2_rn(a.w[jy][0], make_float2(hr[bb % TAPS][c], hr[bb % TAPS][c + H2]));
+                        float2 v2 = fmul2_rn(WT::w(jy, 0), make_float2(hr[bb % TAPS][c], hr[bb % TAPS][c + H2]));
 #pragma unroll
                         for (int tp = 1; tp < TAPS; ++tp)
-                            v2 = ffma2_rn(a.w[jy][tp], make_float2(hr[(bb + tp) % TAPS][c], hr[(bb + tp) % TAPS][c + H2]),
+                            v2 = ffma2_rn(WT::w(jy, tp), make_float2(hr[(bb + tp) % TAPS][c], hr[(bb + tp) % TAPS][c + H2]),
                                           v2);
                         o[c] = v2.x;
                         o[c + H2] = v2.y;
                     }
                     if constexpr (KP % 2 == 1) {
-                        float v1 = __fmul_rn(a.w[jy][0], hr[bb % TAPS][KP - 1]);
+                        float v1 = __fmul_rn(WT::w(jy, 0), hr[bb % TAPS][KP - 1]);
 #pragma unroll
-                        for (int tp = 1; tp < TAPS; ++tp) v1 = __fmaf_rn(a.w[jy][tp], hr[(bb + tp) % TAPS][KP - 1], v1);
+                        for (int tp = 1; tp < TAPS; ++tp) v1 = __fmaf_rn(WT::w(jy, tp), hr[(bb + tp) % TAPS][KP - 1], v1);
                         o[KP - 1] = v1;
                     }
                 }

@@ -5,9 +5,11 @@
 namespace fcfs {
 
 #define FCFS_V(P, Q) \
-    {reinterpret_cast<const void *>(&fcfs_fused_kernel<__nv_bfloat16, P, Q, 2, 0, fused_k<__nv_bfloat16, Q>()>), P, Q, 2, 0, fused_k<__nv_bfloat16, Q>()}, \
-    {reinterpret_cast<const void *>(&fcfs_fused_kernel<__nv_bfloat16, P, Q, 4, -1, fused_k<__nv_bfloat16, Q>()>), P, Q, 4, -1, fused_k<__nv_bfloat16, Q>()},
-extern const FusedVariant kFusedVariants_bf16[] = {FCFS_FUSED_PAIRS(FCFS_V){nullptr, 0, 0, 0, 0, 0}};
+    {reinterpret_cast<const void *>(&fcfs_fused_kernel<__nv_bfloat16, P, Q, 2, 0, fused_k<__nv_bfloat16, Q>()>), P, Q, 2, 0, \
+     fused_k<__nv_bfloat16, Q>(), PhaseW<P, Q, 2>::tab.v}, \
+    {reinterpret_cast<const void *>(&fcfs_fused_kernel<__nv_bfloat16, P, Q, 4, -1, fused_k<__nv_bfloat16, Q>()>), P, Q, 4, -1, \
+     fused_k<__nv_bfloat16, Q>(), PhaseW<P, Q, 4>::tab.v},
+extern const FusedVariant kFusedVariants_bf16[] = {FCFS_FUSED_PAIRS(FCFS_V){nullptr, 0, 0, 0, 0, 0, nullptr}};
 #undef FCFS_V
 
 }  // namespace fcfs

@@ -177,8 +177,6 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     a.out_nrows = (int32_t)g.out_nrows;
     a.planes = (int32_t)g.planes;
     a.pad = pl->pad;
-    for (int j = 0; j < P; ++j)
-        for (int t = 0; t < 4; ++t) a.w[j][t] = pl->tab.w[j][t];
     a.nch = (int32_t)((g.Wo + KP - 1) / KP);
     a.SR = std::max(Ff, Cc);
     const int WIN = (K - 1) * Q + Lw;
@@ -472,6 +470,11 @@ fcfs_status fcfs_plan_ex(int p, int q, int mode, int pad, int64_t C, int64_t H, 
             pl->kernel = 1;
         } else if (!pl->is1d && (W * esize(dtype)) % 16 == 0) {
             pl->fused = fused_lookup(dtype, pl->p, pl->q, pl->tab.ntaps);
+            // the variant's compile-time weights must be this plan's table, bit for bit
+            for (int j = 0; pl->fused && j < pl->p; ++j)
+                for (int t = 0; t < pl->tab.ntaps; ++t)
+                    if (std::memcmp(&pl->fused->wtab[4 * j + t], &pl->tab.w[j][t], sizeof(float)) != 0)
+                        pl->fused = nullptr;
             if (pl->fused) pl->kernel = 2;
         }
     }
