@@ -88,6 +88,9 @@ struct FusedArgs {
     int32_t G;           // output flush groups per y-period (1: rows [0,P); 2: [0,JM) and [JM,P))
     int32_t JM;          // first output row of group 1 (= P when G == 1)
     int32_t rfix;        // right padding columns kept outputs read (written by the producer)
+    int32_t plane_even;  // > 0: segment order visits the even planes (this many) before the odd
+                         // ones, so that 16-bit outputs whose plane size is odd keep one 4-B
+                         // phase per task (packed staging stores without warp divergence)
 };
 
 // Several nearest jobs (same dtype) in one launch (fcfs_run_batch).

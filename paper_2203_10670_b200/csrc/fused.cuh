@@ -109,6 +109,37 @@ __device__ __forceinline__ void load_win(const T *s, int e0, float (&win)[WIN]) 
     }
 }
 
+// Round one output row chunk o[0..KP) to T and store it at staging address sr
+// (only the first nvalid elements when nvalid < KP).  16-bit types with an
+// even chunk are stored as packed pairs (cvt.rn.bf16x2.f32 / cvt.rn.f16x2.f32:
+// each half rounded exactly like the scalar conversion) in 32-bit words; a
+// start that is only 2-B aligned stores its first and last element alone.
+template <typename T, int KP>
+__device__ __forceinline__ void store_row(T *sr, const float (&o)[KP], int nvalid) {
+    if (nvalid >= KP) {
+        if constexpr (sizeof(T) == 2 && KP % 2 == 0) {
+            if ((reinterpret_cast<uintptr_t>(sr) & 2) == 0) {
+                uint32_t *w = reinterpret_cast<uint32_t *>(sr);
+#pragma unroll
+                for (int i = 0; i < KP / 2; ++i) w[i] = DT<T>::pack2(o[2 * i], o[2 * i + 1]);
+            } else {
+                sr[0] = DT<T>::from_f(o[0]);
+                uint32_t *w = reinterpret_cast<uint32_t *>(sr + 1);
+#pragma unroll
+                for (int i = 0; i < KP / 2 - 1; ++i) w[i] = DT<T>::pack2(o[2 * i + 1], o[2 * i + 2]);
+                sr[KP - 1] = DT<T>::from_f(o[KP - 1]);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < KP; ++c) sr[c] = DT<T>::from_f(o[c]);
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < KP; ++c)
+            if (c < nvalid) sr[c] = DT<T>::from_f(o[c]);
+    }
+}
+
 // Geometry of one segment (plane x column tile).
 struct SegGeo {
     int plane, ch0, ch1, c0, c1, a0, a1;
@@ -119,8 +150,11 @@ __device__ __forceinline__ SegGeo seg_geo(const FusedArgs &a, int gs) {
     using G = Geo<P, Q, TAPS, LO>;
     constexpr int A = 16 / ESZ;
     SegGeo s;
-    s.plane = gs / a.ntile;
-    const int tile = gs - s.plane * a.ntile;
+    const int k = gs / a.ntile;
+    const int tile = gs - k * a.ntile;
+    // plane_even > 0: even planes first, then odd ones (a task's planes share
+    // the 4-B phase of their output plane start; see FusedArgs::plane_even)
+    s.plane = a.plane_even ? (k < a.plane_even ? 2 * k : 2 * (k - a.plane_even) + 1) : k;
     s.ch0 = tile * a.CPT;
     s.ch1 = min(a.nch, s.ch0 + a.CPT);
     s.c0 = s.ch0 * K * P;
@@ -311,7 +345,11 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     const int ctid = threadIdx.x - 64;
     const int span_id = ctid >> 4, span_e = ctid & 15;  // copy-out roles
     const int rowb = a.Wo * ESZ;
+    const uint32_t rowb16 = (uint32_t)rowb & 15;
     const bool full_width = a.ntile == 1;
+    const int RS = full_width ? rowb : a.out_pitch;          // staging row stride
+    const uint32_t R16 = full_width ? 0u : rowb16;          // per-row shift increment (tiled)
+    constexpr int kJM = (P + 1) / 2;                        // first row of flush group 1 (plan: JM)
     float hr[TAPS][KP];  // ring: window row r lives in hr[r % TAPS]
     int slot = 0;
     uint32_t phase = 0;
@@ -344,7 +382,6 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         // global byte address of output row out_row0, column c0 of this thread's segment, mod 16
         const uint32_t mis_row0 =
             (uint32_t)(reinterpret_cast<uintptr_t>(a.out) + (plane_out + (full_width ? 0 : sg.c0)) * ESZ) & 15;
-        const uint32_t rowb16 = (uint32_t)rowb & 15;
         // this thread's offset inside a staging slot
         const int st_off = full_width ? sgi * a.out_pitch + col * ESZ : sgi * a.JM * a.out_pitch + (col - sg.c0) * ESZ;
         // copy-out role: span (span_seg, span_row) of every flush of this task
@@ -417,24 +454,37 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             // first / one-past-last kept output row of flush group g of this period
             auto gfirst = [&](int g) { return max(iy * P + (g ? a.JM : 0), b.my_lo); };
             auto glast = [&](int g) { return min(iy * P + (g ? P : a.JM), b.my_hi); };
-            // staging address of output row jy, column `col`, for this thread; the
-            // span start is co-aligned mod 16 with its global address (32-bit mod-16 math)
-            auto srow = [&](int jy) -> T * {
-                const int g = (a.G == 2 && jy >= a.JM) ? 1 : 0;
-                const int ri = jy - (g ? a.JM : 0);
-                unsigned char *slotp = obuf + ((fk + g) & 1) * a.slot_bytes + st_off;
+            const int p0 = iy * P;
+            // every output row of the period is kept (warp-uniform): no per-row range checks
+            const bool pfull = p0 >= b.my_lo && p0 + P <= b.my_hi;
+            // staging address of output row jy (column `col` of this thread) is
+            //   sbase[g(jy)] + jy * RS + ((M + jy * R16) & 15)
+            // with the span start co-aligned mod 16 with its global address
+            // (full width: one span per group, the shift is folded into sbase;
+            // tiled: one span per row, its own shift)
+            unsigned char *sbase[2];
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+                const int gg = (a.G == 2) ? g : 0;
+                unsigned char *slotp = obuf + ((fk + gg) & 1) * a.slot_bytes + st_off;
                 if (full_width) {
-                    const int m0 = gfirst(g);
+                    const int m0 = gfirst(gg);
                     const uint32_t mis = (mis_row0 + (uint32_t)(m0 - a.out_row0) * rowb16) & 15;
-                    return reinterpret_cast<T *>(slotp + mis + (iy * P + (g ? a.JM : 0) + ri - m0) * rowb);
+                    sbase[g] = slotp + mis - (m0 - p0) * rowb;
+                } else {
+                    sbase[g] = slotp - (gg ? a.JM : 0) * a.out_pitch;
                 }
-                const uint32_t mis = (mis_row0 + (uint32_t)(iy * P + jy - a.out_row0) * rowb16) & 15;
-                return reinterpret_cast<T *>(slotp + ri * a.out_pitch + mis);
+            }
+            const uint32_t M = full_width ? 0u : mis_row0 + (uint32_t)(p0 - a.out_row0) * rowb16;
+            auto srow = [&](int jy) -> T * {
+                return reinterpret_cast<T *>(sbase[jy < kJM ? 0 : 1] + jy * RS + ((M + (uint32_t)jy * R16) & 15));
             };
             // vertical taps of output row jy (its tap rows are in the ring) -> staging
             auto emit = [&](int jy) {
-                const int my = iy * P + jy;
-                if (my < b.my_lo || my >= b.my_hi) return;
+                if (!pfull) {
+                    const int my = p0 + jy;
+                    if (my < b.my_lo || my >= b.my_hi) return;
+                }
                 float o[KP];
                 if (jy == 0) {
 #pragma unroll
@@ -459,15 +509,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                         o[KP - 1] = v1;
                     }
                 }
-                T *sr = srow(jy);
-                if (nvalid >= KP) {  // every chunk but a segment's last (those sit in warp 2)
-#pragma unroll
-                    for (int c = 0; c < KP; ++c) sr[c] = DT<T>::from_f(o[c]);
-                } else {
-#pragma unroll
-                    for (int c = 0; c < KP; ++c)
-                        if (c < nvalid) sr[c] = DT<T>::from_f(o[c]);
-                }
+                store_row<T, KP>(srow(jy), o, nvalid);
             };
             // one named barrier, then bulk stores of flush group g
             auto flush = [&](int g) {
@@ -518,7 +560,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             for (int jy = 0; jy < P; ++jy) {
                 if (G::last_row(jy) < C) {
                     if (active) emit(jy);
-                    if (a.G == 2 && jy == a.JM - 1) flush(0);
+                    if (jy == kJM - 1 && a.G == 2) flush(0);
                 }
             }
             mbar_wait(&ready[slot], phase);
@@ -530,7 +572,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 for (int jy = 0; jy < P; ++jy) {
                     if (G::last_row(jy) == r) {
                         if (active) emit(jy);
-                        if (a.G == 2 && jy == a.JM - 1) flush(0);
+                        if (jy == kJM - 1 && a.G == 2) flush(0);
                     }
                 }
             }

@@ -239,6 +239,7 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     }
     if (best_score < 0) return false;
     a = best;
+    if (ESZ == 2 && a.ntile == 1 && (g.out_plane_stride & 1) && g.planes > 1) a.plane_even = (int32_t)((g.planes + 1) / 2);
     a.iy_first = (int32_t)(g.out_row0 / P);
     a.iy_last = (int32_t)((g.out_row0 + g.out_nrows - 1) / P);
     const int nper = a.iy_last - a.iy_first + 1;
