@@ -23,6 +23,8 @@ LIB = os.path.join(PKG, "libfcfs.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-I", INCLUDE, "-I", CSRC]
+# developer experiments only (e.g. FCFS_NVCC_EXTRA=-DFCFS_EXP_...); never set for a product build
+COMMON += os.environ.get("FCFS_NVCC_EXTRA", "").split()
 
 
 def _headers():
