@@ -34,9 +34,13 @@
 // Arithmetic is exactly the reference kernel's (k_reference.cu): identical
 // fp32 operation sequence per output, so both kernels agree bit for bit.
 #pragma once
+#include <type_traits>
+
 #include "device_common.cuh"
 
 namespace fcfs {
+
+__host__ __device__ constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 
 template <int P, int Q, int TAPS, int LO>
 struct Geo {
@@ -116,6 +120,9 @@ __device__ __forceinline__ void load_win(const T *s, int e0, float (&win)[WIN]) 
 // start that is only 2-B aligned stores its first and last element alone.
 template <typename T, int KP>
 __device__ __forceinline__ void store_row(T *sr, const float (&o)[KP], int nvalid) {
+#ifdef FCFS_EXP_NOMASK
+    nvalid = KP;
+#endif
     if (nvalid >= KP) {
         if constexpr (sizeof(T) == 2 && KP % 2 == 0) {
             if ((reinterpret_cast<uintptr_t>(sr) & 2) == 0) {
@@ -314,6 +321,17 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 cf.rows(vf, nr);
                 unsigned char *sbase = stages + cf.slot * a.stage_bytes;
                 const int pairs = cf.b.nsg * nr;
+                if (a.pad == FCFS_PAD_ZERO && (vf < 0 || vf + nr > a.H)) {
+                    // zero-padding rows (§3 Padding, zeros): written as zeros so
+                    // that consumers filter every row the same way
+                    const int n16 = a.seg_pitch / 16;
+                    for (int u = lane; u < pairs * n16; u += 32) {
+                        const int sr = u / n16, c16 = u - sr * n16;
+                        const int s = sr / nr, r = sr - s * nr;
+                        if (vf + r >= 0 && vf + r < a.H) continue;
+                        reinterpret_cast<uint4 *>(sbase + (s * a.SR + r) * a.seg_pitch)[c16] = make_uint4(0, 0, 0, 0);
+                    }
+                }
                 for (int u = lane; u < pairs; u += 32) {
                     const int s = u / nr, r = u - s * nr;
                     const int v = vf + r;
@@ -350,7 +368,10 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     const int RS = full_width ? rowb : a.out_pitch;          // staging row stride
     const uint32_t R16 = full_width ? 0u : rowb16;          // per-row shift increment (tiled)
     constexpr int kJM = (P + 1) / 2;                        // first row of flush group 1 (plan: JM)
-    float hr[TAPS][KP];  // ring: window row r lives in hr[r % TAPS]
+    float hr[TAPS][KP];  // ring of horizontally filtered window rows (see `period`)
+    // Unrolling the period loop over the ring offsets removes the carry copies
+    // but multiplies the loop body; worth it only for small register rings.
+    constexpr bool kRingUnroll = KP * TAPS <= 24;
     int slot = 0;
     uint32_t phase = 0;
     uint32_t fk = 0;     // flush counter: staging slot = fk & 1
@@ -393,12 +414,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         T *const span_out = static_cast<T *>(a.out) + (int64_t)sq.plane * a.out_plane_stride;
 
         // horizontal taps of one window row into a ring slot
-        auto row_h = [&](float(&h)[KP], int v, const unsigned char *srow) {
-            if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) {
-#pragma unroll
-                for (int c = 0; c < KP; ++c) h[c] = 0.0f;
-                return;
-            }
+        // (zero-padding rows arrive as zeros: +0 for every tap, as in the reference kernel)
+        auto row_h = [&](float(&h)[KP], const unsigned char *srow) {
             float win[WIN];
             load_win<T, WIN, PAR>(reinterpret_cast<const T *>(srow), e0, win);
             if constexpr (K == 2) {
@@ -443,14 +460,19 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             if (active) {
                 const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
 #pragma unroll
-                for (int i = 0; i < C; ++i) row_h(hr[i % TAPS], Q * b.iy0 + LO + i, sb + i * a.seg_pitch);
+                for (int i = 0; i < C; ++i) row_h(hr[i % TAPS], sb + i * a.seg_pitch);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
             if (++slot == a.S) { slot = 0; phase ^= 1; }
         }
 
-        for (int iy = b.iy0; iy < b.iy1; ++iy) {
+        // One y-period with window row r in ring slot (RO + r) % TAPS.  The next
+        // period's rows 0..C-1 are this period's rows Q..L-1, so its offset is
+        // RO + Q: the loop below is unrolled over the TAPS / gcd(Q, TAPS) ring
+        // offsets and no row is ever copied between ring slots.
+        auto period = [&](auto ro_c, const int iy) {
+            constexpr int RO = decltype(ro_c)::value;
             // first / one-past-last kept output row of flush group g of this period
             auto gfirst = [&](int g) { return max(iy * P + (g ? a.JM : 0), b.my_lo); };
             auto glast = [&](int g) { return min(iy * P + (g ? P : a.JM), b.my_hi); };
@@ -488,24 +510,25 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 float o[KP];
                 if (jy == 0) {
 #pragma unroll
-                    for (int c = 0; c < KP; ++c) o[c] = hr[(-LO) % TAPS][c];
+                    for (int c = 0; c < KP; ++c) o[c] = hr[(RO - LO) % TAPS][c];
                 } else {
                     const int bb = G::base(jy);
                     constexpr int H2 = KP / 2;  // columns c and c + H2 share the row weights
 #pragma unroll
                     for (int c = 0; c < H2; ++c) {
-                        float2 v2 = fmul2_rn(WT::w(jy, 0), make_float2(hr[bb % TAPS][c], hr[bb % TAPS][c + H2]));
+                        float2 v2 = fmul2_rn(WT::w(jy, 0), make_float2(hr[(RO + bb) % TAPS][c], hr[(RO + bb) % TAPS][c + H2]));
 #pragma unroll
                         for (int tp = 1; tp < TAPS; ++tp)
-                            v2 = ffma2_rn(WT::w(jy, tp), make_float2(hr[(bb + tp) % TAPS][c], hr[(bb + tp) % TAPS][c + H2]),
-                                          v2);
+                            v2 = ffma2_rn(WT::w(jy, tp),
+                                          make_float2(hr[(RO + bb + tp) % TAPS][c], hr[(RO + bb + tp) % TAPS][c + H2]), v2);
                         o[c] = v2.x;
                         o[c + H2] = v2.y;
                     }
                     if constexpr (KP % 2 == 1) {
-                        float v1 = __fmul_rn(WT::w(jy, 0), hr[bb % TAPS][KP - 1]);
+                        float v1 = __fmul_rn(WT::w(jy, 0), hr[(RO + bb) % TAPS][KP - 1]);
 #pragma unroll
-                        for (int tp = 1; tp < TAPS; ++tp) v1 = __fmaf_rn(WT::w(jy, tp), hr[(bb + tp) % TAPS][KP - 1], v1);
+                        for (int tp = 1; tp < TAPS; ++tp)
+                            v1 = __fmaf_rn(WT::w(jy, tp), hr[(RO + bb + tp) % TAPS][KP - 1], v1);
                         o[KP - 1] = v1;
                     }
                 }
@@ -567,7 +590,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
 #pragma unroll
             for (int r = C; r < L; ++r) {
-                if (active) row_h(hr[r % TAPS], Q * iy + LO + r, sb + (r - C) * a.seg_pitch);
+                if (active) row_h(hr[(RO + r) % TAPS], sb + (r - C) * a.seg_pitch);
 #pragma unroll
                 for (int jy = 0; jy < P; ++jy) {
                     if (G::last_row(jy) == r) {
@@ -579,21 +602,36 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
             if (++slot == a.S) { slot = 0; phase ^= 1; }
-            if constexpr (C > 0) {  // carry window rows Q..L-1 -> rows 0..C-1 of the next period
-                if ((Q % TAPS) != 0) {
-                    float tmp[C][KP];
+            if constexpr (!kRingUnroll && C > 0 && (Q % TAPS) != 0) {
+                // carry window rows Q..L-1 -> rows 0..C-1 of the next period
+                float tmp[C][KP];
 #pragma unroll
-                    for (int i = 0; i < C; ++i)
+                for (int i = 0; i < C; ++i)
 #pragma unroll
-                        for (int c = 0; c < KP; ++c) tmp[i][c] = hr[(Q + i) % TAPS][c];
+                    for (int c = 0; c < KP; ++c) tmp[i][c] = hr[(Q + i) % TAPS][c];
 #pragma unroll
-                    for (int i = 0; i < C; ++i)
+                for (int i = 0; i < C; ++i)
 #pragma unroll
-                        for (int c = 0; c < KP; ++c) hr[i % TAPS][c] = tmp[i][c];
-                }
+                    for (int c = 0; c < KP; ++c) hr[i % TAPS][c] = tmp[i][c];
             }
             flush(a.G - 1);
             fk += a.G;
+        };
+        // ring offsets before the cycle repeats (1: the carried rows are copied)
+        constexpr int U = kRingUnroll ? TAPS / cgcd(Q, TAPS) : 1;
+        for (int iy = b.iy0; iy < b.iy1;) {
+            period(std::integral_constant<int, 0>{}, iy);
+            if (++iy >= b.iy1) break;
+            if constexpr (U > 1) {
+                period(std::integral_constant<int, (Q % TAPS)>{}, iy);
+                if (++iy >= b.iy1) break;
+            }
+            if constexpr (U > 2) {
+                period(std::integral_constant<int, ((2 * Q) % TAPS)>{}, iy);
+                if (++iy >= b.iy1) break;
+                period(std::integral_constant<int, ((3 * Q) % TAPS)>{}, iy);
+                ++iy;
+            }
         }
     }
     if (span_e == 0) bulk_wait0();
