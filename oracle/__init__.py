@@ -72,6 +72,12 @@ def _load():
             lib.fcfs_oracle_direct_rows.argtypes = run_args
             lib.fcfs_oracle_direct_points.argtypes = [vp, i32, i64, i64, i64, i64, i64, i32, i32, i32,
                                                       i32, i32, i32, ctypes.POINTER(i64), i64, dp, i32]
+            nd_args = [vp, i32, i64, i32, ctypes.POINTER(i64), ctypes.POINTER(i32), ctypes.POINTER(i32), i32, i32,
+                       i32, dp, i32]
+            lib.fcfs_oracle_staged_nd.argtypes = nd_args
+            lib.fcfs_oracle_direct_nd.argtypes = nd_args
+            lib.fcfs_oracle_output_dims_nd.argtypes = [i32, ctypes.POINTER(i64), ctypes.POINTER(i32),
+                                                       ctypes.POINTER(i32), i32, ctypes.POINTER(i64)]
             _lib = lib
     return _lib
 
@@ -206,6 +212,53 @@ def direct_points(x, pts, p, q, mode="bilinear", pad="replicate", floor_extent=F
         int(is1d), pts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), pts.shape[0], _dptr(out), nthreads)
     _chk(rc, "direct_points")
     return out
+
+
+# ---------------------------------------------------------------- ND, per-dimension factors (§4.2)
+def _nd_params(p, q, R):
+    p = [int(v) for v in (p if hasattr(p, "__len__") else [p] * R)]
+    q = [int(v) for v in (q if hasattr(q, "__len__") else [q] * R)]
+    if len(p) != R or len(q) != R:
+        raise ValueError("one factor per spatial dimension")
+    return (ctypes.c_int * R)(*p), (ctypes.c_int * R)(*q)
+
+
+def output_dims_nd(dims, p, q, floor_extent=False):
+    R = len(dims)
+    pp, qq = _nd_params(p, q, R)
+    d = (ctypes.c_int64 * R)(*dims)
+    out = (ctypes.c_int64 * R)()
+    _chk(_load().fcfs_oracle_output_dims_nd(R, d, pp, qq, int(floor_extent), out), "output_dims_nd")
+    return tuple(out)
+
+
+def _run_nd(fn, x, p, q, R, mode, pad, floor_extent, nthreads):
+    xa, kind = _as_input(x)
+    if xa.ndim < R:
+        raise ValueError("input has fewer dimensions than the rank")
+    dims = xa.shape[xa.ndim - R:]
+    planes = int(np.prod(xa.shape[: xa.ndim - R])) if xa.ndim > R else 1
+    pp, qq = _nd_params(p, q, R)
+    odims = output_dims_nd(dims, p, q, floor_extent)
+    out = np.empty((planes,) + odims)
+    rc = fn(xa.ctypes.data, kind, planes, R, (ctypes.c_int64 * R)(*dims), pp, qq, MODES[mode], PADS[pad],
+            int(floor_extent), _dptr(out), nthreads)
+    _chk(rc, fn.__name__)
+    return out.reshape(tuple(xa.shape[: xa.ndim - R]) + odims)
+
+
+def staged_nd(x, p, q, mode="bilinear", pad="replicate", floor_extent=False, rank=None, nthreads=0):
+    """ND FCFS with per-dimension factors p[d]/q[d] (§4.2): pad -> conv with
+    prod p_d channels and stride q_d -> ND pixelshuffle (§4.1) -> crop, over the
+    last `rank` (= len(p)) axes of x, in double."""
+    R = rank if rank is not None else (len(p) if hasattr(p, "__len__") else 2)
+    return _run_nd(_load().fcfs_oracle_staged_nd, x, p, q, R, mode, pad, floor_extent, nthreads)
+
+
+def direct_nd(x, p, q, mode="bilinear", pad="replicate", floor_extent=False, rank=None, nthreads=0):
+    """Per-output direct evaluation of the ND interpolation formula (independent code)."""
+    R = rank if rank is not None else (len(p) if hasattr(p, "__len__") else 2)
+    return _run_nd(_load().fcfs_oracle_direct_nd, x, p, q, R, mode, pad, floor_extent, nthreads)
 
 
 # ---------------------------------------------------------------- rounding

@@ -648,3 +648,236 @@ int fcfs_oracle_direct_points(const void *x, int in_kind, int64_t planes, int64_
     }
     return bad;
 }
+
+/* ===========================================================================
+ * ND FCFS with per-dimension factors (§4.2): "To scale an
+ * ND input signal by scaling factors r_1/s_1, ..., r_n/s_n for the different
+ * dimensions":
+ *     x = pad(x, padding = 2K_1, ..., 2K_n)
+ *     x = conv(x, out_channels = prod_i r_i, stride = [s_1..s_n],
+ *              kernel_shape = [2K_1+1 .. 2K_n+1], kernel_weights = W)
+ *     return pixelshuffle(x, factors = [r_1..r_n])          (§4.1)
+ * Rank R in 1..3 spatial dimensions, ordered outermost first (D, H, W), each
+ * with its own reduced factor p_d/q_d; one interpolation mode and padding
+ * mode for all dimensions.  The kernel of output channel (j_1..j_R) is the
+ * outer product of the per-dimension 1D phase kernels (§4.2; the printed 2D
+ * bilinear kernels at 3/2 are outer products).
+ * ===========================================================================*/
+#define ORC_RMAX 3
+
+typedef struct {
+    int R, mode, pad;
+    int p[ORC_RMAX], q[ORC_RMAX];
+    int64_t n[ORC_RMAX], no[ORC_RMAX]; /* input / output extents per dimension */
+} orc_ndjob;
+
+static int make_ndjob(int R, const int64_t *dims, const int *p, const int *q, int mode, int pad,
+                      int floor_ext, orc_ndjob *j) {
+    if (R < 1 || R > ORC_RMAX || !dims || !p || !q) return ORC_E_ARG;
+    if (mode < 0 || mode > 2 || pad < 0 || pad > 2) return ORC_E_ARG;
+    j->R = R;
+    j->mode = mode;
+    j->pad = pad;
+    for (int d = 0; d < R; ++d) {
+        if (p[d] < 1 || q[d] < 1 || p[d] > ORC_PMAX || q[d] > ORC_PMAX || dims[d] < 1) return ORC_E_ARG;
+        int64_t g = orc_gcd(p[d], q[d]);
+        j->p[d] = (int)(p[d] / g);
+        j->q[d] = (int)(q[d] / g);
+        j->n[d] = dims[d];
+        fcfs_oracle_output_extent(dims[d], j->p[d], j->q[d], floor_ext, &j->no[d]);
+        if (j->no[d] < 1) return ORC_E_SHAPE;
+    }
+    /* reflect reach, per dimension (as check_reach) */
+    if (pad == ORC_PAD_REFLECT) {
+        for (int d = 0; d < R; ++d) {
+            double w[4];
+            int first0, first_last;
+            int64_t mlast = j->no[d] - 1, s;
+            fcfs_oracle_phase_taps(mode, j->p[d], j->q[d], 0, &first0, w);
+            int nt = fcfs_oracle_phase_taps(mode, j->p[d], j->q[d], (int)(mlast % j->p[d]), &first_last, w);
+            int64_t vmax = (int64_t)j->q[d] * (mlast / j->p[d]) + first_last + nt - 1;
+            if (first0 < 0 && pad_index(first0, j->n[d], ORC_PAD_REFLECT, &s) < 0) return ORC_E_PAD;
+            if (vmax > j->n[d] - 1 && pad_index(vmax, j->n[d], ORC_PAD_REFLECT, &s) < 0) return ORC_E_PAD;
+        }
+    }
+    return ORC_OK;
+}
+
+/* Output extents of an ND job (reading Z3 per dimension). */
+int fcfs_oracle_output_dims_nd(int R, const int64_t *dims, const int *p, const int *q, int floor_ext,
+                               int64_t *out) {
+    orc_ndjob jb;
+    int rc = make_ndjob(R, dims, p, q, ORC_BILINEAR, ORC_PAD_ZERO, floor_ext, &jb);
+    if (rc) return rc;
+    for (int d = 0; d < R; ++d) out[d] = jb.no[d];
+    return ORC_OK;
+}
+
+static double nd_in(const void *x, int in_kind, int64_t idx) {
+    return in_kind == ORC_IN_F32 ? (double)((const float *)x)[idx] : ((const double *)x)[idx];
+}
+
+/* Value of the padded input at virtual index v[0..R) (virtual padding; a
+ * reflect index no bounce reaches is clamped -- it only feeds cropped outputs,
+ * make_ndjob validated the kept ones). */
+static double nd_padded(const void *x, int in_kind, const orc_ndjob *jb, int64_t plane, const int64_t *v) {
+    int64_t idx = plane, s;
+    for (int d = 0; d < jb->R; ++d) {
+        int k = pad_index(v[d], jb->n[d], jb->pad, &s);
+        if (k == 0) return 0.0;
+        if (k < 0) s = v[d] < 0 ? 0 : jb->n[d] - 1;
+        idx = idx * jb->n[d] + s;
+    }
+    return nd_in(x, in_kind, idx);
+}
+
+/* STAGED evaluator, one plane: pad -> conv (prod p_d channels, stride q_d) ->
+ * ND pixelshuffle -> crop, in the paper's order. */
+static int staged_plane_nd(const void *x, int in_kind, const orc_ndjob *jb, int64_t plane, double *out) {
+    const int R = jb->R;
+    int lo[ORC_RMAX] = {0, 0, 0}, T[ORC_RMAX] = {1, 1, 1}, P[ORC_RMAX] = {1, 1, 1}, Q[ORC_RMAX] = {1, 1, 1};
+    int64_t nh[ORC_RMAX] = {1, 1, 1}, PD[ORC_RMAX] = {1, 1, 1}, NO[ORC_RMAX] = {1, 1, 1};
+    /* left-align the R real dimensions into slots 3-R .. 2 (unused outer slots are size 1) */
+    const int o = ORC_RMAX - R;
+    for (int d = 0; d < R; ++d) {
+        int hi;
+        phase_window(jb->mode, jb->p[d], jb->q[d], &lo[o + d], &hi);
+        T[o + d] = hi - lo[o + d] + 1;
+        P[o + d] = jb->p[d];
+        Q[o + d] = jb->q[d];
+        NO[o + d] = jb->no[d];
+        nh[o + d] = (jb->no[d] + jb->p[d] - 1) / jb->p[d];   /* hidden positions (§3.1.1) */
+        PD[o + d] = (nh[o + d] - 1) * jb->q[d] + T[o + d];   /* padded extent the conv reads */
+    }
+    const int64_t nxp = PD[0] * PD[1] * PD[2];
+    const int nch = P[0] * P[1] * P[2];
+    const int64_t nhid = nh[0] * nh[1] * nh[2];
+    const int64_t nsh = (int64_t)nch * nhid;
+    double *xp = (double *)malloc(sizeof(double) * nxp);
+    double *hid = (double *)malloc(sizeof(double) * nsh);
+    double *sh = (double *)malloc(sizeof(double) * nsh);
+    double *k1[ORC_RMAX];
+    for (int s = 0; s < ORC_RMAX; ++s) k1[s] = (double *)malloc(sizeof(double) * (size_t)P[s] * T[s]);
+    int err = ORC_OK;
+    if (!xp || !hid || !sh || !k1[0] || !k1[1] || !k1[2]) { err = ORC_E_NOMEM; goto done; }
+    /* 1. pad: materialise x~ over the window [lo_d, lo_d + PD_d) of every dimension */
+    for (int64_t a = 0; a < PD[0]; ++a)
+        for (int64_t b = 0; b < PD[1]; ++b)
+            for (int64_t c = 0; c < PD[2]; ++c) {
+                int64_t v3[ORC_RMAX] = {lo[0] + a, lo[1] + b, lo[2] + c};
+                xp[(a * PD[1] + b) * PD[2] + c] = nd_padded(x, in_kind, jb, plane, v3 + o);
+            }
+    /* 2. conv: channel (j0, j1, j2), last dimension fastest (reading Z10); its
+     *    kernel is the outer product k0[j0] x k1[j1] x k2[j2] of the 1D phase
+     *    kernels placed in each dimension's shared window. */
+    for (int s = 0; s < ORC_RMAX; ++s)
+        for (int j = 0; j < P[s]; ++j) {
+            if (s < o) { k1[s][0] = 1.0; continue; }     /* unused dimension: the identity */
+            phase_kernel_1d(jb->mode, P[s], Q[s], j, lo[s], T[s], k1[s] + (size_t)j * T[s]);
+        }
+    for (int j0 = 0; j0 < P[0]; ++j0)
+        for (int j1 = 0; j1 < P[1]; ++j1)
+            for (int j2 = 0; j2 < P[2]; ++j2) {
+                const int ch = (j0 * P[1] + j1) * P[2] + j2;
+                const double *ka = k1[0] + (size_t)j0 * T[0], *kb = k1[1] + (size_t)j1 * T[1],
+                             *kc = k1[2] + (size_t)j2 * T[2];
+                for (int64_t i0 = 0; i0 < nh[0]; ++i0)
+                    for (int64_t i1 = 0; i1 < nh[1]; ++i1)
+                        for (int64_t i2 = 0; i2 < nh[2]; ++i2) {
+                            double acc = 0.0;
+                            for (int t0 = 0; t0 < T[0]; ++t0)
+                                for (int t1 = 0; t1 < T[1]; ++t1)
+                                    for (int t2 = 0; t2 < T[2]; ++t2)
+                                        acc += xp[((Q[0] * i0 + t0) * PD[1] + Q[1] * i1 + t1) * PD[2] + Q[2] * i2 + t2] *
+                                               (ka[t0] * kb[t1] * kc[t2]);
+                            hid[(((int64_t)ch * nh[0] + i0) * nh[1] + i1) * nh[2] + i2] = acc;
+                        }
+            }
+    /* 3. ND pixelshuffle (§4.1): Out[i_0, i_1, i_2] = hid[c, i_0/r_0, i_1/r_1, i_2/r_2] */
+    {
+        const int64_t S0 = (int64_t)P[0] * nh[0], S1 = (int64_t)P[1] * nh[1], S2 = (int64_t)P[2] * nh[2];
+        for (int64_t i0 = 0; i0 < S0; ++i0)
+            for (int64_t i1 = 0; i1 < S1; ++i1)
+                for (int64_t i2 = 0; i2 < S2; ++i2) {
+                    const int64_t c = ((i0 % P[0]) * P[1] + i1 % P[1]) * P[2] + i2 % P[2];
+                    sh[(i0 * S1 + i1) * S2 + i2] = hid[((c * nh[0] + i0 / P[0]) * nh[1] + i1 / P[1]) * nh[2] + i2 / P[2]];
+                }
+        /* 4. crop to the output extents */
+        for (int64_t i0 = 0; i0 < NO[0]; ++i0)
+            for (int64_t i1 = 0; i1 < NO[1]; ++i1)
+                for (int64_t i2 = 0; i2 < NO[2]; ++i2)
+                    out[(i0 * NO[1] + i1) * NO[2] + i2] = sh[(i0 * S1 + i1) * S2 + i2];
+    }
+done:
+    free(xp);
+    free(hid);
+    free(sh);
+    for (int s = 0; s < ORC_RMAX; ++s) free(k1[s]);
+    return err;
+}
+
+/* Staged ND entry point.  x: planes x n_0 x .. x n_{R-1} (double or float32);
+ * out: planes x no_0 x .. x no_{R-1} (fcfs_oracle_output_dims_nd). */
+int fcfs_oracle_staged_nd(const void *x, int in_kind, int64_t planes, int R, const int64_t *dims, const int *p,
+                          const int *q, int mode, int pad, int floor_ext, double *out, int nthreads) {
+    orc_ndjob jb;
+    int rc = make_ndjob(R, dims, p, q, mode, pad, floor_ext, &jb);
+    if (rc) return rc;
+    int64_t nout = 1;
+    for (int d = 0; d < R; ++d) nout *= jb.no[d];
+    int bad = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+    for (int64_t pl = 0; pl < planes; ++pl) {
+        int e = staged_plane_nd(x, in_kind, &jb, pl, out + pl * nout);
+        if (e) {
+#ifdef _OPENMP
+#pragma omp atomic write
+#endif
+            bad = e;
+        }
+    }
+    return bad;
+}
+
+/* DIRECT ND evaluator (independent of the staged one): output m_d samples
+ * u_d = m_d*q_d/p_d per dimension (reading Z1); the value is the tensor
+ * product of the per-dimension §5.2 weights at the fractions f_d over the taps
+ * around b_d = floor(m_d*q_d/p_d), with virtual padding. */
+int fcfs_oracle_direct_nd(const void *x, int in_kind, int64_t planes, int R, const int64_t *dims, const int *p,
+                          const int *q, int mode, int pad, int floor_ext, double *out, int nthreads) {
+    orc_ndjob jb;
+    int rc = make_ndjob(R, dims, p, q, mode, pad, floor_ext, &jb);
+    if (rc) return rc;
+    int64_t nout = 1;
+    for (int d = 0; d < R; ++d) nout *= jb.no[d];
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(static)
+#endif
+    for (int64_t it = 0; it < planes * nout; ++it) {
+        int64_t pl = it / nout, rem = it % nout, m[ORC_RMAX], b[ORC_RMAX];
+        double w[ORC_RMAX][4];
+        int first[ORC_RMAX], nt[ORC_RMAX];
+        for (int d = R - 1; d >= 0; --d) {
+            m[d] = rem % jb.no[d];
+            rem /= jb.no[d];
+        }
+        for (int d = 0; d < R; ++d) {
+            b[d] = floordiv(m[d] * jb.q[d], jb.p[d]);
+            nt[d] = direct_weights(mode, (double)((m[d] * jb.q[d]) % jb.p[d]) / jb.p[d], &first[d], w[d]);
+        }
+        for (int d = R; d < ORC_RMAX; ++d) { nt[d] = 1; w[d][0] = 1.0; first[d] = 0; b[d] = 0; }
+        double acc = 0.0;
+        for (int t0 = 0; t0 < nt[0]; ++t0)
+            for (int t1 = 0; t1 < nt[1]; ++t1)
+                for (int t2 = 0; t2 < nt[2]; ++t2) {
+                    int64_t v[ORC_RMAX] = {b[0] + first[0] + t0, b[1] + first[1] + t1, b[2] + first[2] + t2};
+                    acc += w[0][t0] * w[1][t1] * w[2][t2] * nd_padded(x, in_kind, &jb, pl, v);
+                }
+        out[it] = acc;
+    }
+    return ORC_OK;
+}
