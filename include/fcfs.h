@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define FCFS_VERSION 1
+#define FCFS_VERSION 2
 #define FCFS_MAX_FACTOR 64 /* p and q (after gcd reduction) must be <= 64 */
 
 typedef struct fcfs_plan_s *fcfs_plan_t;
@@ -96,6 +96,29 @@ typedef enum {
 fcfs_status fcfs_plan_ex(int p, int q, int mode, int pad, int64_t C, int64_t H, int64_t W, int dtype,
                          unsigned flags, fcfs_plan_t *out);
 
+/* fcfs_plan_nd -- the ND form with per-dimension factors (§4.2, PAPER.md:150-167:
+ * "scaling factors r_1/s_1, ..., r_n/s_n for the different dimensions"; the
+ * conv has prod r_i output channels and stride [s_1..s_n], followed by the ND
+ * pixelshuffle of §4.1).
+ *   rank   : number of spatial dimensions, 1 (W), 2 (H, W) or 3 (D, H, W).
+ *   p, q   : rank factors each, outermost dimension first; each p[d]/q[d] in
+ *            [1, 64] after reduction by gcd.  One mode and one padding mode
+ *            for all dimensions.
+ *   dims   : rank extents (D, H, W order), each >= 1.
+ *   flags  : FCFS_FLAG_EXTENT_FLOOR, FCFS_FLAG_FORCE_REFERENCE (FCFS_FLAG_1D
+ *            is FCFS_E_ARG here: rank 1 is the 1D form).
+ * Tensors are N x C x dims[0] x .. x dims[rank-1] (W fastest), outputs
+ * N x C x odims (fcfs_output_dims).  A rank-2 plan with equal factors is the
+ * plan fcfs_plan_ex builds; rank 1 scales rows of W elements (the same as
+ * FCFS_FLAG_1D with H = 1).  fcfs_run, fcfs_run_batch and fcfs_run_host take
+ * every rank; the row-window calls (fcfs_run_rows, fcfs_strip_rows,
+ * fcfs_needed_rows) window the H rows of every D slice.  3D plans run the
+ * fused kernel when the D factor is 1/1 (slices are independent 2D planes),
+ * else the reference (bilinear / bicubic) or gather (nearest) kernel.
+ * Errors: as fcfs_plan_ex, plus FCFS_E_ARG for rank outside 1..3 or NULL arrays. */
+fcfs_status fcfs_plan_nd(int rank, const int *p, const int *q, int mode, int pad, int64_t C, const int64_t *dims,
+                         int dtype, unsigned flags, fcfs_plan_t *out);
+
 /* fcfs_plan -- fcfs_plan_ex with flags = 0 (paper extent, 2D). */
 fcfs_status fcfs_plan(int p, int q, int mode, int pad, int64_t C, int64_t H, int64_t W, int dtype,
                       fcfs_plan_t *out);
@@ -105,8 +128,12 @@ fcfs_status fcfs_plan(int p, int q, int mode, int pad, int64_t C, int64_t H, int
  * FCFS_FLAG_EXTENT_FLOOR; Ho = H with FCFS_FLAG_1D. */
 fcfs_status fcfs_output_shape(fcfs_plan_t plan, int64_t *Ho, int64_t *Wo);
 
-/* fcfs_run -- scale a batch.  in: device N x C x H x W; out: device
- * N x C x Ho x Wo; N >= 0 (N = 0 is a no-op); stream: cudaStream_t or NULL.
+/* Output extents of every spatial dimension (rank values, outermost first):
+ * p_d*ceil(n_d/q_d) or floor(n_d*p_d/q_d) with FCFS_FLAG_EXTENT_FLOOR. */
+fcfs_status fcfs_output_dims(fcfs_plan_t plan, int64_t *odims);
+
+/* fcfs_run -- scale a batch.  in: device N x C x H x W (x D outermost for
+ * rank 3); out: device N x C x Ho x Wo (x Do); N >= 0 (N = 0 is a no-op); stream: cudaStream_t or NULL.
  * Errors: FCFS_E_ARG (NULL/overlap), FCFS_E_DEVICE, FCFS_E_CUDA. */
 fcfs_status fcfs_run(fcfs_plan_t plan, const void *in, void *out, int64_t N, void *stream);
 
@@ -177,7 +204,10 @@ typedef struct {
     int lo;                 /* first tap offset relative to floor(m*q/p): 0 or -1 */
     int kernel;             /* variant fcfs_run uses: 0 reference, 1 nearest gather, 2 fused separable */
     int device;             /* CUDA device recorded at plan time, -1 if none */
-    int64_t in_rows_referenced; /* input rows (of H) some kept output's tap reads */
+    int64_t in_rows_referenced; /* input rows (of D x H) some kept output's tap reads with a nonzero weight */
+    int rank;               /* spatial rank (1 for FCFS_FLAG_1D plans) */
+    int pd[3], qd[3];       /* per-dimension reduced factors, outermost first (rank entries; rest 1) */
+    int64_t dims[3], odims[3]; /* per-dimension input / output extents (rank entries; rest 1) */
 } fcfs_plan_info_t;
 
 fcfs_status fcfs_plan_info(fcfs_plan_t plan, fcfs_plan_info_t *info);
@@ -191,10 +221,14 @@ fcfs_status fcfs_plan_info(fcfs_plan_t plan, fcfs_plan_info_t *info);
 fcfs_status fcfs_launch_info(fcfs_plan_t plan, int64_t N, int64_t out_row0, int64_t out_nrows, char *buf,
                              int64_t buflen);
 
-/* The fp32 phase table the kernels use: for phase j in [0, p), weights
+/* The fp32 phase table of the W dimension: for phase j in [0, p), weights
  * w[4*j + t] (t < ntaps; unused entries 0) and base offsets base[j] =
  * floor(j*q/p).  w must hold 4*p floats, base p ints.  Errors: FCFS_E_ARG. */
 fcfs_status fcfs_phase_table(fcfs_plan_t plan, float *w, int *base);
+
+/* The phase table of spatial dimension dim (0 = outermost, < rank), laid out
+ * as fcfs_phase_table's with that dimension's p.  Errors: FCFS_E_ARG. */
+fcfs_status fcfs_phase_table_dim(fcfs_plan_t plan, int dim, float *w, int *base);
 
 /* Algorithmic (compulsory) HBM bytes of one fcfs_run over N images: every
  * output byte written once plus every input row some kept output's tap reads

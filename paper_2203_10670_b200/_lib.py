@@ -28,13 +28,18 @@ class Job(ctypes.Structure):
 class PlanInfo(ctypes.Structure):
     _fields_ = [("p", i32), ("q", i32), ("mode", i32), ("pad", i32), ("dtype", i32), ("flags", u32),
                 ("C", i64), ("H", i64), ("W", i64), ("Ho", i64), ("Wo", i64), ("ntaps", i32), ("lo", i32),
-                ("kernel", i32), ("device", i32), ("in_rows_referenced", i64)]
+                ("kernel", i32), ("device", i32), ("in_rows_referenced", i64), ("rank", i32),
+                ("pd", i32 * 3), ("qd", i32 * 3), ("dims", i64 * 3), ("odims", i64 * 3)]
 
 
 # name -> (restype, argtypes); the ABI surface declared in include/fcfs.h
 SIGNATURES = {
     "fcfs_plan_ex": (i32, [i32, i32, i32, i32, i64, i64, i64, i32, u32, ctypes.POINTER(vp)]),
     "fcfs_plan": (i32, [i32, i32, i32, i32, i64, i64, i64, i32, ctypes.POINTER(vp)]),
+    "fcfs_plan_nd": (i32, [i32, ctypes.POINTER(i32), ctypes.POINTER(i32), i32, i32, i64, P64, i32, u32,
+                           ctypes.POINTER(vp)]),
+    "fcfs_output_dims": (i32, [vp, P64]),
+    "fcfs_phase_table_dim": (i32, [vp, i32, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int)]),
     "fcfs_output_shape": (i32, [vp, P64, P64]),
     "fcfs_run": (i32, [vp, vp, vp, i64, vp]),
     "fcfs_run_rows": (i32, [vp, vp, i64, i64, vp, i64, i64, i64, vp]),

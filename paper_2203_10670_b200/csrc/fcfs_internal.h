@@ -12,18 +12,21 @@ constexpr int kPMax = FCFS_MAX_FACTOR;
 // Run geometry common to every kernel.  Row indices are GLOBAL (0..H-1 input,
 // 0..Ho-1 output); the buffers hold the windows [in_row0, in_row0+in_nrows)
 // and [out_row0, out_row0+out_nrows) of each plane.
+// A plane is one (n, c) channel; a 3D plane holds D (output: Do) slices of
+// H x W (Ho x Wo); 2D plans have D = Do = 1.  Row windows apply to every slice.
 struct RunGeom {
     const void *in;
     void *out;
     int64_t planes;             // N * C
+    int64_t D, Do;              // slices per plane (input / output), 1 in 2D
     int64_t H, W, Ho, Wo;       // global sizes
     int64_t in_row0, in_nrows;  // input row window held by `in`
     int64_t out_row0, out_nrows;  // output rows produced into `out`
-    int64_t in_plane_stride;    // elements between planes of `in`  (= in_nrows * W)
-    int64_t out_plane_stride;   // elements between planes of `out` (= out_nrows * Wo)
+    int64_t in_plane_stride;    // elements between planes of `in`  (= D * in_nrows * W)
+    int64_t out_plane_stride;   // elements between planes of `out` (= Do * out_nrows * Wo)
 };
 
-// Per-dimension phase table (identical for both dimensions: one factor p/q).
+// Phase table of one dimension (its own factor p/q, §4.2 per-dimension factors).
 struct PhaseTable {
     float w[kPMax][4];   // fp32 weights of phase j, tap t
     int base[kPMax];     // floor(j*q/p)
@@ -34,7 +37,7 @@ struct PhaseTable {
 
 struct RefArgs {         // reference kernel: one thread per output
     RunGeom g;
-    PhaseTable t;
+    PhaseTable tx, ty, tz;  // W, H, D dimensions (ty unused with is1d, tz the identity in 2D)
     int pad;
     int is1d;
 };
@@ -54,10 +57,10 @@ inline FastDiv make_fastdiv(uint32_t d) {
     return f;
 }
 
-struct NearestArgs {     // nearest gather: one thread per 32-byte output chunk
+struct NearestArgs {     // nearest gather (one output row per warp pass slot)
     RunGeom g;
-    FastDiv div_wo, div_rows, div_p;
-    int p, q, pad, is1d;
+    FastDiv div_rows, div_do, div_px, div_py, div_pz;
+    int px, qx, py, qy, pz, qz, pad, is1d;
     int vec_ok;          // output base 16-B aligned
 };
 
@@ -107,14 +110,14 @@ int launch_nearest(int dtype, const NearestArgs &a, void *stream);
 int launch_nearest_batch(int dtype, const NearestBatch &nb, void *stream);
 
 // Fused: the variant table.  fused_lookup returns an opaque kernel handle or
-// nullptr when (dtype, p, q, ntaps) has no compiled instantiation; K (periods
-// per thread chunk) is reported.
+// nullptr when (dtype, py/qy, px/qx, ntaps) has no compiled instantiation; K
+// (x-periods per thread chunk) is reported.
 struct FusedVariant {
     const void *fn;
-    int P, Q, TAPS, LO, K;
-    const float *wtab;  // the variant's compile-time phase weights, [4*j + t]
+    int PY, QY, PX, QX, TAPS, LO, K;
+    const float *wtab_y, *wtab_x;  // the variant's compile-time phase weights, [4*j + t]
 };
-const FusedVariant *fused_lookup(int dtype, int p, int q, int ntaps);
+const FusedVariant *fused_lookup(int dtype, int py, int qy, int px, int qx, int ntaps);
 int launch_fused(const FusedVariant *v, const FusedArgs &a, int grid, int block, int smem, void *stream);
 
 constexpr int kFusedConsumerWarps = 8;

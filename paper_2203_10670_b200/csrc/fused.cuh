@@ -234,19 +234,21 @@ struct StageCursor {
     }
 };
 
-template <typename T, int P, int Q, int TAPS, int LO, int K>
+template <typename T, int PY, int QY, int PX, int QX, int TAPS, int LO, int K>
 __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __grid_constant__ FusedArgs a) {
-    using G = Geo<P, Q, TAPS, LO>;
-    using WT = PhaseW<P, Q, TAPS>;
-    constexpr int L = G::L, C = G::C;
-    constexpr int KP = K * P;
-    constexpr int WIN = (K - 1) * Q + L;
+    using GY = Geo<PY, QY, TAPS, LO>;  // rows: y-periods of PY output rows from QY input rows
+    using GX = Geo<PX, QX, TAPS, LO>;  // columns: x-periods of PX outputs from QX inputs
+    using WY = PhaseW<PY, QY, TAPS>;
+    using WX = PhaseW<PX, QX, TAPS>;
+    constexpr int L = GY::L, C = GY::C;  // window rows per period, rows carried to the next
+    constexpr int KP = K * PX;
+    constexpr int WIN = (K - 1) * QX + GX::L;
     constexpr int ESZ = sizeof(T);
     constexpr int A = 16 / ESZ;  // left margin (elements)
     constexpr int NCT = 32 * kFusedConsumerWarps;
     // element parity of every window start (16-bit types), when it is static
-    constexpr int PAR = (ESZ == 2 && (K * Q) % 2 == 0) ? ((LO % 2 + 2) % 2) : -1;
-    static_assert(P <= 16, "fused variants have p <= 16");
+    constexpr int PAR = (ESZ == 2 && (K * QX) % 2 == 0) ? ((LO % 2 + 2) % 2) : -1;
+    static_assert(PX <= 16 && PY <= 16, "fused variants have p <= 16");
     static_assert(-LO <= A, "left margin too small");
 
     extern __shared__ __align__(128) unsigned char smem[];
@@ -271,7 +273,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         // ------------------------------------------------------- producer: issue
         // a stage's bulk loads as soon as the consumers have freed its slot
         const uint64_t pol = policy_evict_first();
-        StageCursor<P, Q, TAPS, LO> ci;
+        StageCursor<PY, QY, TAPS, LO> ci;
         ci.start(a);
         while (ci.task < a.ntasks) {
             {
@@ -283,7 +285,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 SegGeo sg;
                 uint32_t seg_bytes = 0;
                 if (lane < ci.b.nsg) {
-                    sg = seg_geo<P, Q, TAPS, LO, K, ESZ>(a, ci.b.group * a.NS + lane);
+                    sg = seg_geo<PX, QX, TAPS, LO, K, ESZ>(a, ci.b.group * a.NS + lane);
                     seg_bytes = (uint32_t)(sg.a1 - sg.a0) * ESZ;
                 }
                 uint32_t tot = seg_bytes * (uint32_t)nreal;
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         // ------------------------------------------- producer: padding + release
         // once a stage's bytes have landed, write the padding columns the kept
         // outputs read into the row margins and hand the stage to the consumers
-        StageCursor<P, Q, TAPS, LO> cf;
+        StageCursor<PY, QY, TAPS, LO> cf;
         cf.start(a);
         while (cf.task < a.ntasks) {
             mbar_wait(&full[cf.slot], cf.phase);
@@ -336,7 +338,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                     const int s = u / nr, r = u - s * nr;
                     const int v = vf + r;
                     if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;
-                    const SegGeo sg = seg_geo<P, Q, TAPS, LO, K, ESZ>(a, cf.b.group * a.NS + s);
+                    const SegGeo sg = seg_geo<PX, QX, TAPS, LO, K, ESZ>(a, cf.b.group * a.NS + s);
                     T *row = reinterpret_cast<T *>(sbase + (s * a.SR + r) * a.seg_pitch) + A - sg.a0;  // row[c]
                     if (sg.a0 == 0) {
 #pragma unroll
@@ -367,7 +369,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     const bool full_width = a.ntile == 1;
     const int RS = full_width ? rowb : a.out_pitch;          // staging row stride
     const uint32_t R16 = full_width ? 0u : rowb16;          // per-row shift increment (tiled)
-    constexpr int kJM = (P + 1) / 2;                        // first row of flush group 1 (plan: JM)
+    constexpr int kJM = (PY + 1) / 2;                        // first row of flush group 1 (plan: JM)
     float hr[TAPS][KP];  // ring of horizontally filtered window rows (see `period`)
     // Unrolling the period loop over the ring offsets removes the carry copies
     // but multiplies the loop body; worth it only for small register rings.
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     uint32_t phase = 0;
     uint32_t fk = 0;     // flush counter: staging slot = fk & 1
     for (int task = blockIdx.x; task < a.ntasks; task += gridDim.x) {
-        const BandInfo b = band_info<P>(a, task);
+        const BandInfo b = band_info<PY>(a, task);
         // thread -> (segment, chunk): the last (possibly partial) chunk of every
         // segment goes to the first consumer threads, so that only one warp ever
         // takes the masked-store path
@@ -392,10 +394,10 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         }
         const bool seg_ok = sgi < b.nsg;
         SegGeo sg = {0, 0, 0, 0, 0, 0, 1};
-        if (seg_ok) sg = seg_geo<P, Q, TAPS, LO, K, ESZ>(a, b.group * a.NS + sgi);
+        if (seg_ok) sg = seg_geo<PX, QX, TAPS, LO, K, ESZ>(a, b.group * a.NS + sgi);
         const int chunk = last ? sg.ch1 - 1 : sg.ch0 + chl;
         const bool active = seg_ok && (last || chunk < sg.ch1 - 1);
-        const int e0 = A + chunk * K * Q + LO - sg.a0;  // window start (element) in a shared row
+        const int e0 = A + chunk * K * QX + LO - sg.a0;  // window start (element) in a shared row
         const int col = chunk * KP;
         const int nvalid = sg.c1 - col;  // outputs of this chunk inside the tile (>= KP: all)
         const int in_off = sgi * a.SR * a.seg_pitch;
@@ -410,7 +412,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         const int span_row = full_width ? 0 : span_id / max(b.nsg, 1);
         const bool span_ok = full_width ? span_id < b.nsg : span_row < a.JM;
         SegGeo sq = {0, 0, 0, 0, 0, 0, 1};
-        if (span_ok) sq = seg_geo<P, Q, TAPS, LO, K, ESZ>(a, b.group * a.NS + span_seg);
+        if (span_ok) sq = seg_geo<PX, QX, TAPS, LO, K, ESZ>(a, b.group * a.NS + span_seg);
         T *const span_out = static_cast<T *>(a.out) + (int64_t)sq.plane * a.out_plane_stride;
 
         // horizontal taps of one window row into a ring slot
@@ -421,35 +423,35 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             if constexpr (K == 2) {
                 // phase jx of both x-periods shares its weights: packed pairs
 #pragma unroll
-                for (int jx = 0; jx < P; ++jx) {
+                for (int jx = 0; jx < PX; ++jx) {
                     if (jx == 0) {  // fraction 0: the tap at offset 0, exactly
                         h[0] = win[-LO];
-                        h[P] = win[Q - LO];
+                        h[PX] = win[QX - LO];
                     } else {
-                        const int bb = G::base(jx);
-                        float2 v2 = fmul2_rn(WT::w(jx, 0), make_float2(win[bb], win[Q + bb]));
+                        const int bb = GX::base(jx);
+                        float2 v2 = fmul2_rn(WX::w(jx, 0), make_float2(win[bb], win[QX + bb]));
 #pragma unroll
                         for (int tp = 1; tp < TAPS; ++tp)
-                            v2 = ffma2_rn(WT::w(jx, tp), make_float2(win[bb + tp], win[Q + bb + tp]), v2);
+                            v2 = ffma2_rn(WX::w(jx, tp), make_float2(win[bb + tp], win[QX + bb + tp]), v2);
                         h[jx] = v2.x;
-                        h[P + jx] = v2.y;
+                        h[PX + jx] = v2.y;
                     }
                 }
             } else {
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
 #pragma unroll
-                    for (int jx = 0; jx < P; ++jx) {
+                    for (int jx = 0; jx < PX; ++jx) {
                         float v2;
                         if (jx == 0) {
-                            v2 = win[k * Q - LO];  // fraction 0: the tap at offset 0, exactly
+                            v2 = win[k * QX - LO];  // fraction 0: the tap at offset 0, exactly
                         } else {
-                            const int bb = k * Q + G::base(jx);
-                            v2 = __fmul_rn(WT::w(jx, 0), win[bb]);
+                            const int bb = k * QX + GX::base(jx);
+                            v2 = __fmul_rn(WX::w(jx, 0), win[bb]);
 #pragma unroll
-                            for (int tp = 1; tp < TAPS; ++tp) v2 = __fmaf_rn(WT::w(jx, tp), win[bb + tp], v2);
+                            for (int tp = 1; tp < TAPS; ++tp) v2 = __fmaf_rn(WX::w(jx, tp), win[bb + tp], v2);
                         }
-                        h[k * P + jx] = v2;
+                        h[k * PX + jx] = v2;
                     }
                 }
             }
@@ -468,17 +470,17 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         }
 
         // One y-period with window row r in ring slot (RO + r) % TAPS.  The next
-        // period's rows 0..C-1 are this period's rows Q..L-1, so its offset is
-        // RO + Q: the loop below is unrolled over the TAPS / gcd(Q, TAPS) ring
+        // period's rows 0..C-1 are this period's rows QY..L-1, so its offset is
+        // RO + QY: the loop below is unrolled over the TAPS / gcd(QY, TAPS) ring
         // offsets and no row is ever copied between ring slots.
         auto period = [&](auto ro_c, const int iy) {
             constexpr int RO = decltype(ro_c)::value;
             // first / one-past-last kept output row of flush group g of this period
-            auto gfirst = [&](int g) { return max(iy * P + (g ? a.JM : 0), b.my_lo); };
-            auto glast = [&](int g) { return min(iy * P + (g ? P : a.JM), b.my_hi); };
-            const int p0 = iy * P;
+            auto gfirst = [&](int g) { return max(iy * PY + (g ? a.JM : 0), b.my_lo); };
+            auto glast = [&](int g) { return min(iy * PY + (g ? PY : a.JM), b.my_hi); };
+            const int p0 = iy * PY;
             // every output row of the period is kept (warp-uniform): no per-row range checks
-            const bool pfull = p0 >= b.my_lo && p0 + P <= b.my_hi;
+            const bool pfull = p0 >= b.my_lo && p0 + PY <= b.my_hi;
             // staging address of output row jy (column `col` of this thread) is
             //   sbase[g(jy)] + jy * RS + ((M + jy * R16) & 15)
             // with the span start co-aligned mod 16 with its global address
@@ -512,23 +514,23 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
 #pragma unroll
                     for (int c = 0; c < KP; ++c) o[c] = hr[(RO - LO) % TAPS][c];
                 } else {
-                    const int bb = G::base(jy);
+                    const int bb = GY::base(jy);
                     constexpr int H2 = KP / 2;  // columns c and c + H2 share the row weights
 #pragma unroll
                     for (int c = 0; c < H2; ++c) {
-                        float2 v2 = fmul2_rn(WT::w(jy, 0), make_float2(hr[(RO + bb) % TAPS][c], hr[(RO + bb) % TAPS][c + H2]));
+                        float2 v2 = fmul2_rn(WY::w(jy, 0), make_float2(hr[(RO + bb) % TAPS][c], hr[(RO + bb) % TAPS][c + H2]));
 #pragma unroll
                         for (int tp = 1; tp < TAPS; ++tp)
-                            v2 = ffma2_rn(WT::w(jy, tp),
+                            v2 = ffma2_rn(WY::w(jy, tp),
                                           make_float2(hr[(RO + bb + tp) % TAPS][c], hr[(RO + bb + tp) % TAPS][c + H2]), v2);
                         o[c] = v2.x;
                         o[c + H2] = v2.y;
                     }
                     if constexpr (KP % 2 == 1) {
-                        float v1 = __fmul_rn(WT::w(jy, 0), hr[(RO + bb) % TAPS][KP - 1]);
+                        float v1 = __fmul_rn(WY::w(jy, 0), hr[(RO + bb) % TAPS][KP - 1]);
 #pragma unroll
                         for (int tp = 1; tp < TAPS; ++tp)
-                            v1 = __fmaf_rn(WT::w(jy, tp), hr[(RO + bb + tp) % TAPS][KP - 1], v1);
+                            v1 = __fmaf_rn(WY::w(jy, tp), hr[(RO + bb + tp) % TAPS][KP - 1], v1);
                         o[KP - 1] = v1;
                     }
                 }
@@ -554,7 +556,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                         const int my = m0 + span_row;
                         gp = reinterpret_cast<unsigned char *>(span_out + (int64_t)(my - a.out_row0) * a.Wo + sq.c0);
                         bytes = (sq.c1 - sq.c0) * ESZ;
-                        const int ri = my - iy * P - (g ? a.JM : 0);
+                        const int ri = my - iy * PY - (g ? a.JM : 0);
                         sp = base + (span_seg * a.JM + ri) * a.out_pitch + (reinterpret_cast<uintptr_t>(gp) & 15);
                     }
                     {
@@ -580,8 +582,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
 
             // output rows complete with the carried rows alone
 #pragma unroll
-            for (int jy = 0; jy < P; ++jy) {
-                if (G::last_row(jy) < C) {
+            for (int jy = 0; jy < PY; ++jy) {
+                if (GY::last_row(jy) < C) {
                     if (active) emit(jy);
                     if (jy == kJM - 1 && a.G == 2) flush(0);
                 }
@@ -592,8 +594,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             for (int r = C; r < L; ++r) {
                 if (active) row_h(hr[(RO + r) % TAPS], sb + (r - C) * a.seg_pitch);
 #pragma unroll
-                for (int jy = 0; jy < P; ++jy) {
-                    if (G::last_row(jy) == r) {
+                for (int jy = 0; jy < PY; ++jy) {
+                    if (GY::last_row(jy) == r) {
                         if (active) emit(jy);
                         if (jy == kJM - 1 && a.G == 2) flush(0);
                     }
@@ -602,13 +604,13 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
             if (++slot == a.S) { slot = 0; phase ^= 1; }
-            if constexpr (!kRingUnroll && C > 0 && (Q % TAPS) != 0) {
-                // carry window rows Q..L-1 -> rows 0..C-1 of the next period
+            if constexpr (!kRingUnroll && C > 0 && (QY % TAPS) != 0) {
+                // carry window rows QY..L-1 -> rows 0..C-1 of the next period
                 float tmp[C][KP];
 #pragma unroll
                 for (int i = 0; i < C; ++i)
 #pragma unroll
-                    for (int c = 0; c < KP; ++c) tmp[i][c] = hr[(Q + i) % TAPS][c];
+                    for (int c = 0; c < KP; ++c) tmp[i][c] = hr[(QY + i) % TAPS][c];
 #pragma unroll
                 for (int i = 0; i < C; ++i)
 #pragma unroll
@@ -618,18 +620,18 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             fk += a.G;
         };
         // ring offsets before the cycle repeats (1: the carried rows are copied)
-        constexpr int U = kRingUnroll ? TAPS / cgcd(Q, TAPS) : 1;
+        constexpr int U = kRingUnroll ? TAPS / cgcd(QY, TAPS) : 1;
         for (int iy = b.iy0; iy < b.iy1;) {
             period(std::integral_constant<int, 0>{}, iy);
             if (++iy >= b.iy1) break;
             if constexpr (U > 1) {
-                period(std::integral_constant<int, (Q % TAPS)>{}, iy);
+                period(std::integral_constant<int, (QY % TAPS)>{}, iy);
                 if (++iy >= b.iy1) break;
             }
             if constexpr (U > 2) {
-                period(std::integral_constant<int, ((2 * Q) % TAPS)>{}, iy);
+                period(std::integral_constant<int, ((2 * QY) % TAPS)>{}, iy);
                 if (++iy >= b.iy1) break;
-                period(std::integral_constant<int, ((3 * Q) % TAPS)>{}, iy);
+                period(std::integral_constant<int, ((3 * QY) % TAPS)>{}, iy);
                 ++iy;
             }
         }

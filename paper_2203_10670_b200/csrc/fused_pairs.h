@@ -1,7 +1,19 @@
-// (P, Q) pairs with a compiled fused variant, for each separable mode and
-// dtype.  Other factors run on the reference kernel.  X(P, Q)
+// Factor combinations with a compiled fused variant, for each separable mode
+// and dtype: X(PY, QY, PX, QX) = rows scaled by PY/QY, columns by PX/QX
+// (per-dimension factors, §4.2).  Other combinations run on the reference
+// kernel.
 #pragma once
-#define FCFS_FUSED_PAIRS(X) \
-    X(1, 1) X(2, 1) X(3, 1) X(4, 1) X(1, 2) X(1, 3) X(1, 4) \
-    X(3, 2) X(2, 3) X(4, 3) X(3, 4) X(5, 3) X(3, 5) X(5, 4) X(4, 5) \
-    X(7, 5) X(5, 7) X(4, 7) X(7, 4) X(5, 2) X(2, 5)
+#define FCFS_ISO_PAIRS(Y) \
+    Y(1, 1) Y(2, 1) Y(3, 1) Y(4, 1) Y(1, 2) Y(1, 3) Y(1, 4) \
+    Y(3, 2) Y(2, 3) Y(4, 3) Y(3, 4) Y(5, 3) Y(3, 5) Y(5, 4) Y(4, 5) \
+    Y(7, 5) Y(5, 7) Y(4, 7) Y(7, 4) Y(5, 2) Y(2, 5)
+#define FCFS_NONUNIT_PAIRS(Y) \
+    Y(2, 1) Y(3, 1) Y(4, 1) Y(1, 2) Y(1, 3) Y(1, 4) \
+    Y(3, 2) Y(2, 3) Y(4, 3) Y(3, 4) Y(5, 3) Y(3, 5) Y(5, 4) Y(4, 5) \
+    Y(7, 5) Y(5, 7) Y(4, 7) Y(7, 4) Y(5, 2) Y(2, 5)
+// isotropic p/q in both dimensions
+#define FCFS_ISO_X(X) FCFS_ISO_PAIRS(X##_ISO)
+// columns only (rows 1/1: 1D rows and width-only resizes)
+#define FCFS_W_X(X) FCFS_NONUNIT_PAIRS(X##_W)
+// rows only (columns 1/1)
+#define FCFS_H_X(X) FCFS_NONUNIT_PAIRS(X##_H)

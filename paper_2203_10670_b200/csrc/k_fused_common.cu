@@ -8,15 +8,18 @@
 
 namespace fcfs {
 
-extern const FusedVariant kFusedVariants_f32[];
-extern const FusedVariant kFusedVariants_f16[];
-extern const FusedVariant kFusedVariants_bf16[];
+extern const FusedVariant kFusedVariants_f32_iso[], kFusedVariants_f32_w[], kFusedVariants_f32_h[];
+extern const FusedVariant kFusedVariants_f16_iso[], kFusedVariants_f16_w[], kFusedVariants_f16_h[];
+extern const FusedVariant kFusedVariants_bf16_iso[], kFusedVariants_bf16_w[], kFusedVariants_bf16_h[];
 
-const FusedVariant *fused_lookup(int dtype, int p, int q, int ntaps) {
-    const FusedVariant *tab =
-        dtype == FCFS_F32 ? kFusedVariants_f32 : (dtype == FCFS_F16 ? kFusedVariants_f16 : kFusedVariants_bf16);
-    for (const FusedVariant *v = tab; v->fn; ++v)
-        if (v->P == p && v->Q == q && v->TAPS == ntaps) return v;
+const FusedVariant *fused_lookup(int dtype, int py, int qy, int px, int qx, int ntaps) {
+    const FusedVariant *sets[3][3] = {{kFusedVariants_f32_iso, kFusedVariants_f32_w, kFusedVariants_f32_h},
+                                      {kFusedVariants_f16_iso, kFusedVariants_f16_w, kFusedVariants_f16_h},
+                                      {kFusedVariants_bf16_iso, kFusedVariants_bf16_w, kFusedVariants_bf16_h}};
+    if (dtype < 0 || dtype > 2) return nullptr;
+    for (const FusedVariant *tab : sets[dtype])
+        for (const FusedVariant *v = tab; v->fn; ++v)
+            if (v->PY == py && v->QY == qy && v->PX == px && v->QX == qx && v->TAPS == ntaps) return v;
     return nullptr;
 }
 

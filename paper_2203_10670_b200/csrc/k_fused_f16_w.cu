@@ -1,0 +1,9 @@
+// Fused separable FCFS kernels: element type __half, factor set "w" (fused_pairs.h).
+#include "fused_inst.cuh"
+
+#define V_ISO(P, Q) FCFS_BOTH_MODES(__half, P, Q, P, Q)
+#define V_W(P, Q) FCFS_BOTH_MODES(__half, 1, 1, P, Q)
+#define V_H(P, Q) FCFS_BOTH_MODES(__half, P, Q, 1, 1)
+namespace fcfs {
+extern const FusedVariant kFusedVariants_f16_w[] = {FCFS_W_X(V){nullptr, 0, 0, 0, 0, 0, 0, 0, nullptr, nullptr}};
+}  // namespace fcfs

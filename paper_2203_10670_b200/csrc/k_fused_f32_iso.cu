@@ -1,0 +1,9 @@
+// Fused separable FCFS kernels: element type float, factor set "iso" (fused_pairs.h).
+#include "fused_inst.cuh"
+
+#define V_ISO(P, Q) FCFS_BOTH_MODES(float, P, Q, P, Q)
+#define V_W(P, Q) FCFS_BOTH_MODES(float, 1, 1, P, Q)
+#define V_H(P, Q) FCFS_BOTH_MODES(float, P, Q, 1, 1)
+namespace fcfs {
+extern const FusedVariant kFusedVariants_f32_iso[] = {FCFS_ISO_X(V){nullptr, 0, 0, 0, 0, 0, 0, 0, nullptr, nullptr}};
+}  // namespace fcfs

@@ -1,6 +1,7 @@
 // Nearest-neighbour FCFS (§5.2.1; floor rule, reading Z2):
-// every phase kernel is one-hot, so the layer is a gather
-//     out[m_y][m_x] = x~[floor(m_y*q/p)][floor(m_x*q/p)]
+// every phase kernel is one-hot, so the layer is a gather, per dimension with
+// its own factor (§4.2):
+//     out[m_z][m_y][m_x] = x~[floor(m_z*q_z/p_z)][floor(m_y*q_y/p_y)][floor(m_x*q_x/p_x)]
 // with no arithmetic on the value (bit-exact; -0, NaN and Inf pass through).
 //
 // Layout: a warp handles RPW output rows per pass (grid-stride over the
@@ -29,9 +30,9 @@ __global__ void __launch_bounds__(256, MINB) fcfs_nearest_kernel(const __grid_co
         while (j + 1 < nb.njobs && gp >= nb.pass_prefix[j + 1]) ++j;
         const NearestArgs &a = nb.job[j];
         const RunGeom &g = a.g;
-        const uint32_t rows_total = (uint32_t)(g.planes * g.out_nrows);
-        const int32_t W = (int32_t)g.W, Wo = (int32_t)g.Wo, H = (int32_t)g.H;
-        const uint32_t q = (uint32_t)a.q;
+        const uint32_t rows_total = (uint32_t)(g.planes * g.Do * g.out_nrows);
+        const int32_t W = (int32_t)g.W, Wo = (int32_t)g.Wo, H = (int32_t)g.H, D = (int32_t)g.D;
+        const uint32_t qx = (uint32_t)a.qx;
         const T *__restrict__ in = static_cast<const T *>(g.in);
         T *__restrict__ out = static_cast<T *>(g.out);
         const uint32_t rw0 = (gp - nb.pass_prefix[j]) * RPW;
@@ -42,21 +43,25 @@ __global__ void __launch_bounds__(256, MINB) fcfs_nearest_kernel(const __grid_co
         for (int k = 0; k < RPW; ++k) {
             const uint32_t rw = rw0 + k;
             wr[k] = rw < rows_total;
-            const uint32_t plane = fdiv(rw, a.div_rows);
-            const uint32_t lr = rw - plane * (uint32_t)g.out_nrows;
+            const uint32_t t = fdiv(rw, a.div_rows);             // (plane, output slice)
+            const uint32_t lr = rw - t * (uint32_t)g.out_nrows;
+            const uint32_t plane = fdiv(t, a.div_do);
+            const uint32_t mz = t - plane * (uint32_t)g.Do;
             const uint32_t my = (uint32_t)g.out_row0 + lr;
-            const int32_t by = a.is1d ? (int32_t)my : (int32_t)fdiv(my * q, a.div_p);
-            const int32_t rs = pad_src32(by, H, a.pad);
-            rd[k] = wr[k] && rs >= 0;
-            orow[k] = out + (int64_t)plane * g.out_plane_stride + (int64_t)lr * Wo;
-            irow[k] = in + (int64_t)plane * g.in_plane_stride + (int64_t)(max(rs, (int32_t)g.in_row0) - g.in_row0) * W;
+            const int32_t by = a.is1d ? (int32_t)my : (int32_t)fdiv(my * (uint32_t)a.qy, a.div_py);
+            const int32_t bz = (int32_t)fdiv(mz * (uint32_t)a.qz, a.div_pz);
+            const int32_t rs = pad_src32(by, H, a.pad), zs = pad_src32(bz, D, a.pad);
+            rd[k] = wr[k] && rs >= 0 && zs >= 0;
+            orow[k] = out + (int64_t)plane * g.out_plane_stride + ((int64_t)mz * g.out_nrows + lr) * Wo;
+            irow[k] = in + (int64_t)plane * g.in_plane_stride +
+                      ((int64_t)max(zs, 0) * g.in_nrows + (max(rs, (int32_t)g.in_row0) - g.in_row0)) * W;
         }
         for (int mx0 = lane; mx0 < Wo; mx0 += 32 * U) {
             T v[RPW][U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int mx = mx0 + 32 * u;
-                int cs = (int)fdiv((uint32_t)mx * q, a.div_p);
+                int cs = (int)fdiv((uint32_t)mx * qx, a.div_px);
                 if (cs >= W) cs = pad_src32(cs, W, a.pad);
                 const bool ok = mx < Wo && cs >= 0;
 #pragma unroll
@@ -80,7 +85,7 @@ template <typename T, int U, int RPW, int MINB>
 static void launch_nearest_v(NearestBatch nb, cudaStream_t s) {
     nb.pass_prefix[0] = 0;
     for (int j = 0; j < nb.njobs; ++j) {
-        const int64_t rows = nb.job[j].g.planes * nb.job[j].g.out_nrows;
+        const int64_t rows = nb.job[j].g.planes * nb.job[j].g.Do * nb.job[j].g.out_nrows;
         nb.pass_prefix[j + 1] = nb.pass_prefix[j] + (uint32_t)((rows + RPW - 1) / RPW);
     }
     int64_t blocks = ((int64_t)nb.pass_prefix[nb.njobs] + 7) / 8;  // 8 warps per block
@@ -115,7 +120,7 @@ int launch_nearest_batch(int dtype, const NearestBatch &nb, void *stream) {
 }
 
 int launch_nearest(int dtype, const NearestArgs &a, void *stream) {
-    if (a.g.planes * a.g.out_nrows == 0 || a.g.Wo == 0) return 0;
+    if (a.g.planes * a.g.Do * a.g.out_nrows == 0 || a.g.Wo == 0) return 0;
     NearestBatch nb;
     nb.njobs = 1;
     nb.job[0] = a;

@@ -1,16 +1,22 @@
 // Reference kernel: one thread per output element, direct per-output
-// evaluation through global memory.  It handles every plan (any p, q <= 64,
-// 1D, row windows, unaligned buffers) and defines the GPU arithmetic contract
-// that the fused kernel reproduces bit for bit:
+// evaluation through global memory.  It handles every plan (any per-dimension
+// p, q <= 64, rank 1-3, row windows, unaligned buffers) and defines the GPU
+// arithmetic contract that the fused kernel reproduces bit for bit.  Per
+// dimension d with factor p_d/q_d, output m_d = p_d*i + j_d has base
+// b_d = q_d*i + base_d[j_d] (§3.1.1, reading Z1), and
 //
-//   h(r)  = x~[r][b_x]                                      if j_x == 0 (fraction 0)
-//         = w[j_x][0]*x~[r][b_x+lo] (+fma) ... w[j_x][T-1]*x~[r][b_x+lo+T-1]   otherwise
-//         = 0                                               if row r is zero padding
-//   out   = h(b_y)                                          if j_y == 0
-//         = w[j_y][0]*h(b_y+lo) (+fma) ... w[j_y][T-1]*h(b_y+lo+T-1)          otherwise
+//   hx(s, r) = x~[s][r][b_x]                                   if j_x == 0 (fraction 0)
+//            = w_x[j_x][0]*x~[s][r][b_x+lo] (+fma) ... (+fma) w_x[j_x][T-1]*x~[s][r][b_x+lo+T-1]
+//            = 0                                               if slice s or row r is zero padding
+//   hz(r)    = hx(b_z, r)                                      if j_z == 0 (always in 2D)
+//            = w_z[j_z][0]*hx(b_z+lo, r) (+fma) ... w_z[j_z][T-1]*hx(b_z+lo+T-1, r)
+//   out      = hz(b_y)                                         if j_y == 0
+//            = w_y[j_y][0]*hz(b_y+lo) (+fma) ... w_y[j_y][T-1]*hz(b_y+lo+T-1)
 //
-// (fp32, __fmul_rn then __fmaf_rn in tap order), m = p*i + j, b = q*i + base[j]
-// (§3.1.1 with reading Z1).  Nearest (one tap) is a pure copy.
+// (fp32, __fmul_rn then __fmaf_rn in tap order: x first, then the slice
+// dimension, then rows; §4.2's kernels are outer products, so any order is the
+// same real number -- this one is the contract).  Nearest (one tap) is a pure
+// copy.  1D plans (FCFS_FLAG_1D) take out = hx(0, m_y).
 #include "device_common.cuh"
 
 namespace fcfs {
@@ -21,52 +27,69 @@ __device__ __forceinline__ float xval(const T *__restrict__ row, int64_t c, int6
     return s < 0 ? 0.0f : DT<T>::to_f(row[s]);
 }
 
+// horizontal pass of input row r of slice sl (virtual indices; padding applied)
 template <typename T>
-__device__ __forceinline__ float hval(const T *__restrict__ plane, const RefArgs &a, int64_t r, int jx, int64_t bx) {
+__device__ __forceinline__ float hxval(const T *__restrict__ plane, const RefArgs &a, int64_t sl, int64_t r, int jx,
+                                       int64_t bx) {
     const RunGeom &g = a.g;
-    if (a.pad == FCFS_PAD_ZERO && (r < 0 || r >= g.H)) return 0.0f;
-    int64_t rs = pad_src(r, g.H, a.pad) - g.in_row0;
-    const T *row = plane + rs * g.W;
-    if (jx == 0 || a.t.ntaps == 1) return xval(row, bx, g.W, a.pad);
-    float v = __fmul_rn(a.t.w[jx][0], xval(row, bx + a.t.lo, g.W, a.pad));
-    for (int t = 1; t < a.t.ntaps; ++t) v = __fmaf_rn(a.t.w[jx][t], xval(row, bx + a.t.lo + t, g.W, a.pad), v);
+    if (a.pad == FCFS_PAD_ZERO && (r < 0 || r >= g.H || sl < 0 || sl >= g.D)) return 0.0f;
+    const int64_t ss = pad_src(sl, g.D, a.pad);
+    const int64_t rs = pad_src(r, g.H, a.pad) - g.in_row0;
+    const T *row = plane + (ss * g.in_nrows + rs) * g.W;
+    if (jx == 0 || a.tx.ntaps == 1) return xval(row, bx, g.W, a.pad);
+    float v = __fmul_rn(a.tx.w[jx][0], xval(row, bx + a.tx.lo, g.W, a.pad));
+    for (int t = 1; t < a.tx.ntaps; ++t) v = __fmaf_rn(a.tx.w[jx][t], xval(row, bx + a.tx.lo + t, g.W, a.pad), v);
+    return v;
+}
+
+// slice-dimension pass at row r (identity in 2D: j_z = 0, b_z = 0)
+template <typename T>
+__device__ __forceinline__ float hzval(const T *__restrict__ plane, const RefArgs &a, int jz, int64_t bz, int64_t r,
+                                       int jx, int64_t bx) {
+    if (jz == 0 || a.tz.ntaps == 1) return hxval(plane, a, bz, r, jx, bx);
+    float v = __fmul_rn(a.tz.w[jz][0], hxval(plane, a, bz + a.tz.lo, r, jx, bx));
+    for (int t = 1; t < a.tz.ntaps; ++t) v = __fmaf_rn(a.tz.w[jz][t], hxval(plane, a, bz + a.tz.lo + t, r, jx, bx), v);
     return v;
 }
 
 template <typename T>
 __global__ void __launch_bounds__(256) fcfs_reference_kernel(const __grid_constant__ RefArgs a) {
     const RunGeom &g = a.g;
-    const int64_t total = g.planes * g.out_nrows * g.Wo;
-    const int p = a.t.p, q = a.t.q;
+    const int64_t total = g.planes * g.Do * g.out_nrows * g.Wo;
     for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total;
          f += (int64_t)gridDim.x * blockDim.x) {
-        int64_t mx = f % g.Wo;
+        const int64_t mx = f % g.Wo;
         int64_t t = f / g.Wo;
-        int64_t my = g.out_row0 + t % g.out_nrows;
-        int64_t plane = t / g.out_nrows;
+        const int64_t lr = t % g.out_nrows;  // output row within the window
+        t /= g.out_nrows;
+        const int64_t mz = t % g.Do;
+        const int64_t plane = t / g.Do;
+        const int64_t my = g.out_row0 + lr;
         const T *src = static_cast<const T *>(g.in) + plane * g.in_plane_stride;
-        int jx = (int)(mx % p);
-        int64_t bx = (mx / p) * q + a.t.base[jx];
+        const int jx = (int)(mx % a.tx.p);
+        const int64_t bx = (mx / a.tx.p) * a.tx.q + a.tx.base[jx];
+        const int jz = (int)(mz % a.tz.p);
+        const int64_t bz = (mz / a.tz.p) * a.tz.q + a.tz.base[jz];
         float out;
         if (a.is1d) {
-            out = hval(src, a, my, jx, bx);
+            out = hxval(src, a, 0, my, jx, bx);
         } else {
-            int jy = (int)(my % p);
-            int64_t by = (my / p) * q + a.t.base[jy];
-            if (jy == 0 || a.t.ntaps == 1) {
-                out = hval(src, a, by, jx, bx);
+            const int jy = (int)(my % a.ty.p);
+            const int64_t by = (my / a.ty.p) * a.ty.q + a.ty.base[jy];
+            if (jy == 0 || a.ty.ntaps == 1) {
+                out = hzval(src, a, jz, bz, by, jx, bx);
             } else {
-                out = __fmul_rn(a.t.w[jy][0], hval(src, a, by + a.t.lo, jx, bx));
-                for (int k = 1; k < a.t.ntaps; ++k)
-                    out = __fmaf_rn(a.t.w[jy][k], hval(src, a, by + a.t.lo + k, jx, bx), out);
+                out = __fmul_rn(a.ty.w[jy][0], hzval(src, a, jz, bz, by + a.ty.lo, jx, bx));
+                for (int k = 1; k < a.ty.ntaps; ++k)
+                    out = __fmaf_rn(a.ty.w[jy][k], hzval(src, a, jz, bz, by + a.ty.lo + k, jx, bx), out);
             }
         }
-        static_cast<T *>(g.out)[plane * g.out_plane_stride + t % g.out_nrows * g.Wo + mx] = DT<T>::from_f(out);
+        static_cast<T *>(g.out)[plane * g.out_plane_stride + (mz * g.out_nrows + lr) * g.Wo + mx] = DT<T>::from_f(out);
     }
 }
 
 int launch_reference(int dtype, const RefArgs &a, void *stream) {
-    const int64_t total = a.g.planes * a.g.out_nrows * a.g.Wo;
+    const int64_t total = a.g.planes * a.g.Do * a.g.out_nrows * a.g.Wo;
     if (total == 0) return 0;
     int64_t blocks = (total + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;

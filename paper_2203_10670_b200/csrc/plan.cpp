@@ -19,11 +19,14 @@
 using namespace fcfs;
 
 struct fcfs_plan_s {
-    int p, q, mode, pad, dtype;
+    int rank;                 // spatial rank as created: 1, 2 or 3 (fcfs_plan_ex: 2, or 1 with FCFS_FLAG_1D)
+    int p, q;                 // W (column) factor, reduced
+    int py, qy, pz, qz;       // H (row) and D (slice) factors, reduced (1/1 where absent)
+    int mode, pad, dtype;
     unsigned flags;
-    int64_t C, H, W, Ho, Wo;
-    int is1d;
-    PhaseTable tab;
+    int64_t C, D, H, W, Do, Ho, Wo;
+    int is1d;                 // rows are independent 1D signals (FCFS_FLAG_1D, rank 1)
+    PhaseTable tab, taby, tabz;  // per-dimension phase tables: W, H, D
     int kernel;  // 0 reference, 1 nearest, 2 fused
     const FusedVariant *fused;
     int device;
@@ -81,9 +84,9 @@ void phase_table(PhaseTable &t, int p, int q, int mode) {
 
 // Virtual index range one dimension's kept outputs [m0, m1) read (their own
 // taps, zero-weight taps of the tap list included).
-void tap_range(const fcfs_plan_s *pl, int64_t m0, int64_t m1, int64_t *vmin, int64_t *vmax) {
-    *vmin = fdiv64(m0 * pl->q, pl->p) + pl->tab.lo;
-    *vmax = fdiv64((m1 - 1) * pl->q, pl->p) + pl->tab.lo + pl->tab.ntaps - 1;
+void tap_range(const PhaseTable &t, int64_t m0, int64_t m1, int64_t *vmin, int64_t *vmax) {
+    *vmin = fdiv64(m0 * t.q, t.p) + t.lo;
+    *vmax = fdiv64((m1 - 1) * t.q, t.p) + t.lo + t.ntaps - 1;
 }
 
 bool reflect_ok(int64_t vmin, int64_t vmax, int64_t n) {
@@ -106,7 +109,7 @@ void needed_rows(const fcfs_plan_s *pl, int64_t m0, int64_t m1, int64_t *need0, 
         vmin = m0;
         vmax = m1 - 1;
     } else {
-        tap_range(pl, m0, m1, &vmin, &vmax);
+        tap_range(pl->taby, m0, m1, &vmin, &vmax);
     }
     int64_t n0 = std::max<int64_t>(vmin, 0), n1 = std::min<int64_t>(vmax + 1, pl->H);
     if (pl->pad != FCFS_PAD_ZERO) {
@@ -120,23 +123,30 @@ void needed_rows(const fcfs_plan_s *pl, int64_t m0, int64_t m1, int64_t *need0, 
     *need1 = n1;
 }
 
-// Rows of the image some kept output reads with a NONZERO weight.
-int64_t rows_referenced(const fcfs_plan_s *pl) {
-    if (pl->is1d) return pl->H;
-    std::vector<char> used(pl->H, 0);
-    for (int64_t my = 0; my < pl->Ho; ++my) {
-        int j = (int)(my % pl->p);
-        int64_t by = (my / pl->p) * pl->q + pl->tab.base[j];
-        for (int t = 0; t < pl->tab.ntaps; ++t) {
-            bool nz = pl->tab.ntaps == 1 || (j == 0 ? (t == -pl->tab.lo) : pl->tab.w[j][t] != 0.0f);
+// Indices (of n) along one dimension that some kept output (of no) reads with
+// a NONZERO weight.
+int64_t referenced(const PhaseTable &t, int64_t n, int64_t no, int pad) {
+    std::vector<char> used(n, 0);
+    for (int64_t m = 0; m < no; ++m) {
+        int j = (int)(m % t.p);
+        int64_t b = (m / t.p) * t.q + t.base[j];
+        for (int k = 0; k < t.ntaps; ++k) {
+            bool nz = t.ntaps == 1 || (j == 0 ? (k == -t.lo) : t.w[j][k] != 0.0f);
             if (!nz) continue;
-            int64_t s = pad_src_host(by + pl->tab.lo + t, pl->H, pl->pad);
-            if (s >= 0 && s < pl->H) used[s] = 1;
+            int64_t s = pad_src_host(b + t.lo + k, n, pad);
+            if (s >= 0 && s < n) used[s] = 1;
         }
     }
-    int64_t n = 0;
-    for (char u : used) n += u;
-    return n;
+    int64_t c = 0;
+    for (char u : used) c += u;
+    return c;
+}
+
+// Input rows (of every slice) some kept output reads with a NONZERO weight,
+// times the referenced slices (3D).
+int64_t rows_referenced(const fcfs_plan_s *pl) {
+    const int64_t rows = pl->is1d ? pl->H : referenced(pl->taby, pl->H, pl->Ho, pl->pad);
+    return rows * referenced(pl->tabz, pl->D, pl->Do, pl->pad);
 }
 
 bool ranges_overlap(const void *a, int64_t na, const void *b, int64_t nb) {
@@ -153,14 +163,18 @@ struct FusedLaunch {
 
 bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     const FusedVariant *v = pl->fused;
-    const int P = v->P, Q = v->Q, K = v->K, TAPS = v->TAPS, LO = v->LO;
+    const int PY = v->PY, QY = v->QY, PX = v->PX, QX = v->QX, K = v->K, TAPS = v->TAPS, LO = v->LO;
     const int ESZ = esize(pl->dtype), A = 16 / ESZ;
-    const int HI = ((P - 1) * Q) / P + LO + TAPS - 1;
-    const int Lw = HI - LO + 1;
-    const int Cc = Lw > Q ? Lw - Q : 0;
-    const int Ff = Lw - Cc;
+    // y-period window (rows): L rows, C carried to the next period, F fresh
+    const int HIy = ((PY - 1) * QY) / PY + LO + TAPS - 1;
+    const int Ly = HIy - LO + 1;
+    const int Cc = Ly > QY ? Ly - QY : 0;
+    const int Ff = Ly - Cc;
+    // x-period window (columns)
+    const int HIx = ((PX - 1) * QX) / PX + LO + TAPS - 1;
+    const int Lw = HIx - LO + 1;
     const int NT = 32 * kFusedConsumerWarps;
-    const int KP = K * P;
+    const int KP = K * PX;
     FusedArgs &a = L.a;
     std::memset(&a, 0, sizeof(a));
     a.in = g.in;
@@ -179,17 +193,17 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     a.pad = pl->pad;
     a.nch = (int32_t)((g.Wo + KP - 1) / KP);
     a.SR = std::max(Ff, Cc);
-    const int WIN = (K - 1) * Q + Lw;
+    const int WIN = (K - 1) * QX + Lw;
     // right margin: every window read stays inside the row slot (allocation);
     // only the columns kept outputs' own taps reach are written (rfix)
-    const int64_t reach_all = (int64_t)(a.nch - 1) * K * Q + LO + WIN;  // one past the last window column
+    const int64_t reach_all = (int64_t)(a.nch - 1) * K * QX + LO + WIN;  // one past the last window column
     const int64_t ralloc = std::max<int64_t>(0, reach_all - g.W);
-    const int64_t reach_kept = ((g.Wo - 1) * Q) / P + LO + TAPS;       // one past the last kept tap
+    const int64_t reach_kept = ((g.Wo - 1) * QX) / PX + LO + TAPS;     // one past the last kept tap
     a.rfix = (int32_t)std::max<int64_t>(0, std::min<int64_t>(reach_kept - g.W, ralloc));
     const int budget = 110 * 1024;              // two CTAs per SM
     // shared row: [A-element margin][loaded columns][right margin], 16-B multiple
     auto seg_pitch_for = [&](int cpt) {
-        int64_t elems = std::min<int64_t>(g.W, (int64_t)cpt * K * Q - Q + Lw + 2 * A);
+        int64_t elems = std::min<int64_t>(g.W, (int64_t)cpt * K * QX - QX + Lw + 2 * A);
         elems = (elems + A - 1) / A * A + A + (ralloc + A - 1) / A * A;
         return (int)(elems * ESZ);
     };
@@ -201,10 +215,10 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     for (int64_t nt = min_tiles; nt <= std::min<int64_t>(a.nch, min_tiles + 64); ++nt) {
         // G = 1: one flush per y-period, two full-period staging slots;
         // G = 2: two flushes per period, slots of ceil(P/2) rows (half the smem)
-        for (int Gf = 1; Gf <= (P >= 2 ? 2 : 1); ++Gf) {
+        for (int Gf = 1; Gf <= (PY >= 2 ? 2 : 1); ++Gf) {
             FusedArgs c = a;
             c.G = Gf;
-            c.JM = Gf == 2 ? (P + 1) / 2 : P;
+            c.JM = Gf == 2 ? (PY + 1) / 2 : PY;
             c.CPT = (int32_t)((a.nch + nt - 1) / nt);
             c.ntile = (int32_t)((a.nch + c.CPT - 1) / c.CPT);
             if (nt > min_tiles && c.ntile != nt) continue;
@@ -240,15 +254,15 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     if (best_score < 0) return false;
     a = best;
     if (ESZ == 2 && a.ntile == 1 && (g.out_plane_stride & 1) && g.planes > 1) a.plane_even = (int32_t)((g.planes + 1) / 2);
-    a.iy_first = (int32_t)(g.out_row0 / P);
-    a.iy_last = (int32_t)((g.out_row0 + g.out_nrows - 1) / P);
+    a.iy_first = (int32_t)(g.out_row0 / PY);
+    a.iy_last = (int32_t)((g.out_row0 + g.out_nrows - 1) / PY);
     const int nper = a.iy_last - a.iy_first + 1;
     const int resident = pl->sm_count * 2;
     const int64_t base_tasks = ((int64_t)a.nseg + a.NS - 1) / a.NS;
     int nbands = 1;
     if (base_tasks < 4 * resident) {
         const int want = (int)((4 * resident + base_tasks - 1) / base_tasks);
-        const int min_pb = std::max(2, (4 * Cc + Q - 1) / std::max(1, Q));  // warm-up <= ~25%
+        const int min_pb = std::max(2, (4 * Cc + QY - 1) / std::max(1, QY));  // warm-up <= ~25%
         nbands = std::max(1, std::min(want, nper / min_pb));
     }
     if (const char *e = std::getenv("FCFS_DEBUG_NBANDS")) nbands = std::max(1, std::min(nper, std::atoi(e)));
@@ -262,16 +276,30 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     if (const char *e = std::getenv("FCFS_DEBUG_S")) a.S = std::max(2, std::min(a.S, std::atoi(e)));
     L.smem = 256 + a.S * a.stage_bytes + 128 + 2 * a.slot_bytes;
     std::snprintf(L.desc, sizeof(L.desc),
-                  "{\"kernel\": \"fused_separable\", \"P\": %d, \"Q\": %d, \"taps\": %d, \"K\": %d, \"NS\": %d, "
+                  "{\"kernel\": \"fused_separable\", \"PY\": %d, \"QY\": %d, \"PX\": %d, \"QX\": %d, \"taps\": %d, "
+                  "\"K\": %d, \"NS\": %d, "
                   "\"CPT\": %d, \"nch\": %d, \"ntile\": %d, \"nseg\": %d, \"S\": %d, \"SR\": %d, \"seg_pitch\": %d, "
                   "\"stage_bytes\": %d, \"out_pitch\": %d, \"slot_bytes\": %d, \"rfix\": %d, \"periods\": %d, "
                   "\"PB\": %d, \"nbands\": %d, \"ntasks\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, "
                   "\"busy_threads\": %d, \"flush_groups\": %d}",
-                  P, Q, TAPS, K, a.NS, a.CPT, a.nch, a.ntile, a.nseg, a.S, a.SR, a.seg_pitch, a.stage_bytes,
+                  PY, QY, PX, QX, TAPS, K, a.NS, a.CPT, a.nch, a.ntile, a.nseg, a.S, a.SR, a.seg_pitch, a.stage_bytes,
                   a.out_pitch, a.slot_bytes, a.rfix, nper, a.PB, a.nbands, a.ntasks, L.grid, kFusedThreads, L.smem,
                   a.NS * a.CPT, a.G);
     if (std::getenv("FCFS_DEBUG_PRINT")) std::fprintf(stderr, "%s\n", L.desc);
     return true;
+}
+
+// 1D plans: every row of every plane is an independent signal, so a whole-row
+// run is one plane of planes * H rows (long columns of rows keep the kernels'
+// row bands full however small H is).
+void fold_rows_1d(const fcfs_plan_s *pl, RunGeom &g) {
+    if (!pl->is1d || g.in_row0 != 0 || g.in_nrows != pl->H || g.out_row0 != 0 || g.out_nrows != pl->Ho) return;
+    const int64_t rows = g.planes * pl->H;
+    if (rows >= INT32_MAX || g.planes == 1) return;
+    g.H = g.Ho = g.in_nrows = g.out_nrows = rows;
+    g.planes = 1;
+    g.in_plane_stride = rows * pl->W;
+    g.out_plane_stride = rows * pl->Wo;
 }
 
 fcfs_status check_device(const fcfs_plan_s *pl) {
@@ -288,20 +316,29 @@ fcfs_status check_device(const fcfs_plan_s *pl) {
 // feasible shared-memory geometry (fused).  Fills L for the fused kernel.
 int select_kernel(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     int kernel = pl->kernel;
-    if (kernel == 1 && (g.planes * g.out_nrows >= INT32_MAX || pl->Ho * pl->q >= INT32_MAX)) kernel = 0;
+    if (kernel == 1 && (g.planes * g.Do * g.out_nrows >= INT32_MAX || pl->Ho * pl->qy >= INT32_MAX ||
+                        pl->Wo * pl->q >= INT32_MAX || pl->Do * pl->qz >= INT32_MAX))
+        kernel = 0;
     if (kernel == 2) {
+        // 3D plans reach the fused kernel only with an identity slice factor:
+        // then every slice is an independent 2D plane
+        RunGeom g2 = g;
+        g2.planes = g.planes * g.D;
+        g2.D = g2.Do = 1;
+        g2.in_plane_stride = g.in_nrows * pl->W;
+        g2.out_plane_stride = g.out_nrows * pl->Wo;
         if ((reinterpret_cast<uintptr_t>(g.in) & 15) ||
-            g.planes * std::max(g.in_nrows * pl->W, g.out_nrows * pl->Wo) > INT32_MAX * 16LL || !plan_fused(pl, g, L))
+            g2.planes * std::max(g.in_nrows * pl->W, g.out_nrows * pl->Wo) > INT32_MAX * 16LL || !plan_fused(pl, g2, L))
             kernel = 0;
     }
     if (kernel == 1) {
-        const int64_t rows = g.planes * g.out_nrows;
+        const int64_t rows = g.planes * g.Do * g.out_nrows;
         std::snprintf(L.desc, sizeof(L.desc),
                       "{\"kernel\": \"nearest_gather\", \"rows\": %lld, \"grid\": %lld, \"block\": 256, "
                       "\"outputs_per_lane_iter\": 8}",
                       (long long)rows, (long long)std::min<int64_t>((rows + 7) / 8, 148 * 8 * 4));
     } else if (kernel == 0) {
-        const int64_t total = g.planes * g.out_nrows * pl->Wo;
+        const int64_t total = g.planes * g.Do * g.out_nrows * pl->Wo;
         std::snprintf(L.desc, sizeof(L.desc), "{\"kernel\": \"reference\", \"grid\": %lld, \"block\": 256}",
                       (long long)std::min<int64_t>((total + 255) / 256, 148 * 32));
     }
@@ -331,7 +368,8 @@ fcfs_status prepare(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t in_
     if (!in || !out) return FCFS_E_ARG;
     const int ESZ = esize(pl->dtype);
     const int64_t planes = N * pl->C;
-    const int64_t in_bytes = planes * in_nrows * pl->W * ESZ, out_bytes = planes * out_nrows * pl->Wo * ESZ;
+    const int64_t in_bytes = planes * pl->D * in_nrows * pl->W * ESZ,
+                  out_bytes = planes * pl->Do * out_nrows * pl->Wo * ESZ;
     if (ranges_overlap(in, in_bytes, out, out_bytes)) return FCFS_E_ARG;
     int64_t n0, n1;
     needed_rows(pl, out_row0, out_row0 + out_nrows, &n0, &n1);
@@ -343,6 +381,8 @@ fcfs_status prepare(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t in_
     g.in = in;
     g.out = out;
     g.planes = planes;
+    g.D = pl->D;
+    g.Do = pl->Do;
     g.H = pl->H;
     g.W = pl->W;
     g.Ho = pl->Ho;
@@ -351,9 +391,10 @@ fcfs_status prepare(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t in_
     g.in_nrows = in_nrows;
     g.out_row0 = out_row0;
     g.out_nrows = out_nrows;
-    g.in_plane_stride = in_nrows * pl->W;
-    g.out_plane_stride = out_nrows * pl->Wo;
+    g.in_plane_stride = pl->D * in_nrows * pl->W;
+    g.out_plane_stride = pl->Do * out_nrows * pl->Wo;
 
+    fold_rows_1d(pl, g);
     pr.in = in;
     pr.out = out;
     pr.in_bytes = in_bytes;
@@ -362,18 +403,26 @@ fcfs_status prepare(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t in_
     if (pr.kernel == 1) {
         NearestArgs &a = pr.na;
         a.g = g;
-        a.div_wo = make_fastdiv((uint32_t)pl->Wo);
-        a.div_rows = make_fastdiv((uint32_t)out_nrows);
-        a.div_p = make_fastdiv((uint32_t)pl->p);
-        a.p = pl->p;
-        a.q = pl->q;
+        a.div_rows = make_fastdiv((uint32_t)g.out_nrows);
+        a.div_do = make_fastdiv((uint32_t)pl->Do);
+        a.div_px = make_fastdiv((uint32_t)pl->p);
+        a.div_py = make_fastdiv((uint32_t)pl->py);
+        a.div_pz = make_fastdiv((uint32_t)pl->pz);
+        a.px = pl->p;
+        a.qx = pl->q;
+        a.py = pl->py;
+        a.qy = pl->qy;
+        a.pz = pl->pz;
+        a.qz = pl->qz;
         a.pad = pl->pad;
         a.is1d = pl->is1d;
         a.vec_ok = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
     } else if (pr.kernel == 0) {
         RefArgs &a = pr.ra;
         a.g = g;
-        a.t = pl->tab;
+        a.tx = pl->tab;
+        a.ty = pl->taby;
+        a.tz = pl->tabz;
         a.pad = pl->pad;
         a.is1d = pl->is1d;
     }
@@ -396,68 +445,74 @@ fcfs_status run_window(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t 
     return launch(pr, stream);
 }
 
-}  // namespace
-
-extern "C" {
-
-int fcfs_version(void) { return FCFS_VERSION; }
-
-const char *fcfs_status_str(fcfs_status s) {
-    switch (s) {
-    case FCFS_OK: return "ok";
-    case FCFS_E_ARG: return "invalid argument";
-    case FCFS_E_SHAPE: return "invalid shape or row window";
-    case FCFS_E_PAD: return "reflect padding cannot reach a needed tap";
-    case FCFS_E_UNSUPPORTED: return "unsupported configuration";
-    case FCFS_E_DEVICE: return "no CUDA device or wrong device";
-    case FCFS_E_CUDA: return "CUDA error";
-    case FCFS_E_NOMEM: return "out of host memory";
-    }
-    return "unknown status";
-}
-
-fcfs_status fcfs_plan_ex(int p, int q, int mode, int pad, int64_t C, int64_t H, int64_t W, int dtype,
-                         unsigned flags, fcfs_plan_t *out) {
-    if (!out) return FCFS_E_ARG;
-    if (p < 1 || q < 1) return FCFS_E_ARG;
-    {
-        const int64_t g0 = gcd64(p, q);
-        if (p / g0 > FCFS_MAX_FACTOR || q / g0 > FCFS_MAX_FACTOR) return FCFS_E_ARG;
+// Validate a job and build its plan.  rank 1-3 spatial dimensions, outermost
+// first (D, H, W), each with its own factor p[d]/q[d] (§4.2).  fcfs_plan_ex is
+// rank 2 with equal factors; FCFS_FLAG_1D (rank 2 only) scales W alone and
+// keeps the H rows as independent signals (the same as rank 1).
+fcfs_status make_plan(int rank, const int *pd, const int *qd, int mode, int pad, int64_t C, const int64_t *dims,
+                      int dtype, unsigned flags, fcfs_plan_t *out) {
+    if (!out || rank < 1 || rank > 3) return FCFS_E_ARG;
+    int rp[3], rq[3];
+    for (int d = 0; d < rank; ++d) {
+        if (pd[d] < 1 || qd[d] < 1) return FCFS_E_ARG;
+        const int64_t g0 = gcd64(pd[d], qd[d]);
+        if (pd[d] / g0 > FCFS_MAX_FACTOR || qd[d] / g0 > FCFS_MAX_FACTOR) return FCFS_E_ARG;
+        rp[d] = (int)(pd[d] / g0);
+        rq[d] = (int)(qd[d] / g0);
+        if (dims[d] < 1 || dims[d] > INT32_MAX) return FCFS_E_ARG;
     }
     if (mode < FCFS_NEAREST || mode > FCFS_BICUBIC || pad < FCFS_PAD_ZERO || pad > FCFS_PAD_REFLECT) return FCFS_E_ARG;
     if (dtype < FCFS_F32 || dtype > FCFS_BF16) return FCFS_E_ARG;
-    if (C < 1 || H < 1 || W < 1 || H > INT32_MAX || W > INT32_MAX) return FCFS_E_ARG;
+    if (C < 1) return FCFS_E_ARG;
     const unsigned known = FCFS_FLAG_1D | FCFS_FLAG_EXTENT_FLOOR | FCFS_FLAG_FORCE_REFERENCE;
     if (flags & ~known) return FCFS_E_ARG;
+    if ((flags & FCFS_FLAG_1D) && rank != 2) return FCFS_E_ARG;
     fcfs_plan_s *pl = new (std::nothrow) fcfs_plan_s;
     if (!pl) return FCFS_E_NOMEM;
     std::memset(pl, 0, sizeof(*pl));
-    const int64_t g = gcd64(p, q);
-    pl->p = (int)(p / g);
-    pl->q = (int)(q / g);
+    pl->rank = (flags & FCFS_FLAG_1D) ? 1 : rank;
+    pl->is1d = (rank == 1 || (flags & FCFS_FLAG_1D)) ? 1 : 0;
+    pl->p = rp[rank - 1];
+    pl->q = rq[rank - 1];
+    pl->py = pl->qy = pl->pz = pl->qz = 1;
+    if (rank >= 2 && !pl->is1d) {
+        pl->py = rp[rank - 2];
+        pl->qy = rq[rank - 2];
+    }
+    if (rank == 3) {
+        pl->pz = rp[0];
+        pl->qz = rq[0];
+    }
     pl->mode = mode;
     pl->pad = pad;
     pl->dtype = dtype;
     pl->flags = flags;
     pl->C = C;
-    pl->H = H;
-    pl->W = W;
-    pl->is1d = (flags & FCFS_FLAG_1D) ? 1 : 0;
+    pl->W = dims[rank - 1];
+    pl->H = rank >= 2 ? dims[rank - 2] : 1;
+    pl->D = rank == 3 ? dims[0] : 1;
     const bool fl = (flags & FCFS_FLAG_EXTENT_FLOOR) != 0;
-    pl->Wo = extent(W, pl->p, pl->q, fl);
-    pl->Ho = pl->is1d ? H : extent(H, pl->p, pl->q, fl);
-    if (pl->Ho < 1 || pl->Wo < 1 || pl->Ho > INT32_MAX || pl->Wo > INT32_MAX) {
+    pl->Wo = extent(pl->W, pl->p, pl->q, fl);
+    pl->Ho = pl->is1d ? pl->H : extent(pl->H, pl->py, pl->qy, fl);
+    pl->Do = rank == 3 ? extent(pl->D, pl->pz, pl->qz, fl) : 1;
+    if (pl->Ho < 1 || pl->Wo < 1 || pl->Do < 1 || pl->Ho > INT32_MAX || pl->Wo > INT32_MAX || pl->Do > INT32_MAX) {
         delete pl;
         return FCFS_E_SHAPE;
     }
     phase_table(pl->tab, pl->p, pl->q, mode);
+    phase_table(pl->taby, pl->py, pl->qy, mode);
+    phase_table(pl->tabz, pl->pz, pl->qz, mode);
     if (pad == FCFS_PAD_REFLECT) {
         int64_t vmin, vmax;
-        tap_range(pl, 0, pl->Wo, &vmin, &vmax);
-        bool ok = reflect_ok(vmin, vmax, W);
+        tap_range(pl->tab, 0, pl->Wo, &vmin, &vmax);
+        bool ok = reflect_ok(vmin, vmax, pl->W);
         if (!pl->is1d) {
-            tap_range(pl, 0, pl->Ho, &vmin, &vmax);
-            ok = ok && reflect_ok(vmin, vmax, H);
+            tap_range(pl->taby, 0, pl->Ho, &vmin, &vmax);
+            ok = ok && reflect_ok(vmin, vmax, pl->H);
+        }
+        if (rank == 3) {
+            tap_range(pl->tabz, 0, pl->Do, &vmin, &vmax);
+            ok = ok && reflect_ok(vmin, vmax, pl->D);
         }
         if (!ok) {
             delete pl;
@@ -469,12 +524,17 @@ fcfs_status fcfs_plan_ex(int p, int q, int mode, int pad, int64_t C, int64_t H, 
     if (!(flags & FCFS_FLAG_FORCE_REFERENCE)) {
         if (mode == FCFS_NEAREST) {
             pl->kernel = 1;
-        } else if (!pl->is1d && (W * esize(dtype)) % 16 == 0) {
-            pl->fused = fused_lookup(dtype, pl->p, pl->q, pl->tab.ntaps);
-            // the variant's compile-time weights must be this plan's table, bit for bit
+        } else if ((pl->W * esize(dtype)) % 16 == 0 && pl->pz == 1 && pl->qz == 1) {
+            // separable fused kernel: rows by py/qy (1/1 for 1D rows), columns by p/q
+            pl->fused = fused_lookup(dtype, pl->py, pl->qy, pl->p, pl->q, pl->tab.ntaps);
+            // the variant's compile-time weights must be this plan's tables, bit for bit
             for (int j = 0; pl->fused && j < pl->p; ++j)
                 for (int t = 0; t < pl->tab.ntaps; ++t)
-                    if (std::memcmp(&pl->fused->wtab[4 * j + t], &pl->tab.w[j][t], sizeof(float)) != 0)
+                    if (std::memcmp(&pl->fused->wtab_x[4 * j + t], &pl->tab.w[j][t], sizeof(float)) != 0)
+                        pl->fused = nullptr;
+            for (int j = 0; pl->fused && j < pl->py; ++j)
+                for (int t = 0; t < pl->taby.ntaps; ++t)
+                    if (std::memcmp(&pl->fused->wtab_y[4 * j + t], &pl->taby.w[j][t], sizeof(float)) != 0)
                         pl->fused = nullptr;
             if (pl->fused) pl->kernel = 2;
         }
@@ -500,6 +560,39 @@ fcfs_status fcfs_plan_ex(int p, int q, int mode, int pad, int64_t C, int64_t H, 
     }
     *out = pl;
     return FCFS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fcfs_version(void) { return FCFS_VERSION; }
+
+const char *fcfs_status_str(fcfs_status s) {
+    switch (s) {
+    case FCFS_OK: return "ok";
+    case FCFS_E_ARG: return "invalid argument";
+    case FCFS_E_SHAPE: return "invalid shape or row window";
+    case FCFS_E_PAD: return "reflect padding cannot reach a needed tap";
+    case FCFS_E_UNSUPPORTED: return "unsupported configuration";
+    case FCFS_E_DEVICE: return "no CUDA device or wrong device";
+    case FCFS_E_CUDA: return "CUDA error";
+    case FCFS_E_NOMEM: return "out of host memory";
+    }
+    return "unknown status";
+}
+
+fcfs_status fcfs_plan_ex(int p, int q, int mode, int pad, int64_t C, int64_t H, int64_t W, int dtype,
+                         unsigned flags, fcfs_plan_t *out) {
+    const int pd[2] = {p, p}, qd[2] = {q, q};
+    const int64_t dims[2] = {H, W};
+    return make_plan(2, pd, qd, mode, pad, C, dims, dtype, flags, out);
+}
+
+fcfs_status fcfs_plan_nd(int rank, const int *p, const int *q, int mode, int pad, int64_t C, const int64_t *dims,
+                         int dtype, unsigned flags, fcfs_plan_t *out) {
+    if ((flags & FCFS_FLAG_1D) || !p || !q || !dims) return FCFS_E_ARG;
+    return make_plan(rank, p, q, mode, pad, C, dims, dtype, flags, out);
 }
 
 fcfs_status fcfs_plan(int p, int q, int mode, int pad, int64_t C, int64_t H, int64_t W, int dtype, fcfs_plan_t *out) {
@@ -533,8 +626,8 @@ fcfs_status fcfs_strip_rows(fcfs_plan_t pl, int64_t own0, int64_t own1, int64_t 
         m1 = own1;
     } else {
         // smallest m with floor(m*q/p) >= own  <=>  m >= own*p/q
-        m0 = own0 == 0 ? 0 : (own0 * pl->p + pl->q - 1) / pl->q;
-        m1 = own1 == pl->H ? pl->Ho : (own1 * pl->p + pl->q - 1) / pl->q;
+        m0 = own0 == 0 ? 0 : (own0 * pl->py + pl->qy - 1) / pl->qy;
+        m1 = own1 == pl->H ? pl->Ho : (own1 * pl->py + pl->qy - 1) / pl->qy;
         m0 = std::min(m0, pl->Ho);
         m1 = std::max(m0, std::min(m1, pl->Ho));
     }
@@ -611,8 +704,8 @@ fcfs_status fcfs_run_host(fcfs_plan_t pl, const void *host_in, void *host_out, i
     fcfs_status st = check_device(pl);
     if (st != FCFS_OK) return st;
     const int ESZ = esize(pl->dtype);
-    const size_t in_bytes = (size_t)(N * pl->C * pl->H * pl->W * ESZ);
-    const size_t out_bytes = (size_t)(N * pl->C * pl->Ho * pl->Wo * ESZ);
+    const size_t in_bytes = (size_t)(N * pl->C * pl->D * pl->H * pl->W * ESZ);
+    const size_t out_bytes = (size_t)(N * pl->C * pl->Do * pl->Ho * pl->Wo * ESZ);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (cudaMemcpyAsync(dev_in, host_in, in_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) {
         cudaGetLastError();
@@ -645,6 +738,35 @@ fcfs_status fcfs_plan_info(fcfs_plan_t pl, fcfs_plan_info_t *info) {
     info->kernel = pl->kernel;
     info->device = pl->device;
     info->in_rows_referenced = pl->rows_ref;
+    info->rank = pl->rank;
+    const int pp[3] = {pl->pz, pl->py, pl->p}, qq[3] = {pl->qz, pl->qy, pl->q};
+    const int64_t dd[3] = {pl->D, pl->H, pl->W}, oo[3] = {pl->Do, pl->Ho, pl->Wo};
+    for (int d = 0; d < 3; ++d) info->pd[d] = info->qd[d] = 1, info->dims[d] = info->odims[d] = 1;
+    for (int d = 0; d < pl->rank; ++d) {
+        const int s = 3 - pl->rank + d;
+        info->pd[d] = pp[s];
+        info->qd[d] = qq[s];
+        info->dims[d] = dd[s];
+        info->odims[d] = oo[s];
+    }
+    return FCFS_OK;
+}
+
+fcfs_status fcfs_output_dims(fcfs_plan_t pl, int64_t *odims) {
+    if (!pl || !odims) return FCFS_E_ARG;
+    const int64_t oo[3] = {pl->Do, pl->Ho, pl->Wo};
+    for (int d = 0; d < pl->rank; ++d) odims[d] = oo[3 - pl->rank + d];
+    return FCFS_OK;
+}
+
+fcfs_status fcfs_phase_table_dim(fcfs_plan_t pl, int dim, float *w, int *base) {
+    if (!pl || !w || !base || dim < 0 || dim >= pl->rank) return FCFS_E_ARG;
+    const PhaseTable *tabs[3] = {&pl->tabz, &pl->taby, &pl->tab};
+    const PhaseTable &t = *tabs[3 - pl->rank + dim];
+    for (int j = 0; j < t.p; ++j) {
+        base[j] = t.base[j];
+        for (int k = 0; k < 4; ++k) w[4 * j + k] = t.w[j][k];
+    }
     return FCFS_OK;
 }
 
@@ -658,6 +780,8 @@ fcfs_status fcfs_launch_info(fcfs_plan_t pl, int64_t N, int64_t out_row0, int64_
     g.in = nullptr;  // assumed 16-B aligned
     g.out = nullptr;
     g.planes = N * pl->C;
+    g.D = pl->D;
+    g.Do = pl->Do;
     g.H = pl->H;
     g.W = pl->W;
     g.Ho = pl->Ho;
@@ -666,8 +790,9 @@ fcfs_status fcfs_launch_info(fcfs_plan_t pl, int64_t N, int64_t out_row0, int64_
     g.in_nrows = std::max<int64_t>(1, n1 - n0);
     g.out_row0 = out_row0;
     g.out_nrows = out_nrows;
-    g.in_plane_stride = g.in_nrows * pl->W;
-    g.out_plane_stride = out_nrows * pl->Wo;
+    g.in_plane_stride = pl->D * g.in_nrows * pl->W;
+    g.out_plane_stride = pl->Do * out_nrows * pl->Wo;
+    fold_rows_1d(pl, g);
     FusedLaunch L;
     select_kernel(pl, g, L);
     std::snprintf(buf, (size_t)buflen, "%s", L.desc);
@@ -686,7 +811,7 @@ fcfs_status fcfs_phase_table(fcfs_plan_t pl, float *w, int *base) {
 fcfs_status fcfs_compulsory_bytes(fcfs_plan_t pl, int64_t N, int64_t *bytes) {
     if (!pl || !bytes || N < 0) return FCFS_E_ARG;
     const int ESZ = esize(pl->dtype);
-    *bytes = N * pl->C * (pl->rows_ref * pl->W + pl->Ho * pl->Wo) * ESZ;
+    *bytes = N * pl->C * (pl->rows_ref * pl->W + pl->Do * pl->Ho * pl->Wo) * ESZ;
     return FCFS_OK;
 }
 

@@ -39,8 +39,26 @@ class Plan:
         if extent not in ("paper", "floor"):
             raise ValueError(extent)
         h = ctypes.c_void_p()
-        check(_lib.lib.fcfs_plan_ex(p, q, _lib.MODES[mode], _lib.PADS[pad], C, H, W, _lib.DTYPES[dtype], flags,
-                                    ctypes.byref(h)), "fcfs_plan_ex")
+        if isinstance(p, (tuple, list)):  # per-dimension factors: the ND form (§4.2)
+            if is1d:
+                raise ValueError("per-dimension plans express 1D as rank 1")
+            R = len(p)
+            if isinstance(H, (tuple, list)):  # Plan.nd: the spatial dims, outermost first
+                dims = tuple(int(v) for v in H)
+            elif R == 2:
+                dims = (int(H), int(W))
+            elif R == 1:
+                dims = (int(W),)
+            else:
+                raise ValueError("rank-3 plans take dims=(D, H, W) (Plan.nd)")
+            if len(q) != R or len(dims) != R:
+                raise ValueError("p, q and dims need one entry per spatial dimension")
+            check(_lib.lib.fcfs_plan_nd(R, (ctypes.c_int * R)(*p), (ctypes.c_int * R)(*q), _lib.MODES[mode],
+                                        _lib.PADS[pad], C, (ctypes.c_int64 * R)(*dims), _lib.DTYPES[dtype], flags,
+                                        ctypes.byref(h)), "fcfs_plan_nd")
+        else:
+            check(_lib.lib.fcfs_plan_ex(p, q, _lib.MODES[mode], _lib.PADS[pad], C, H, W, _lib.DTYPES[dtype], flags,
+                                        ctypes.byref(h)), "fcfs_plan_ex")
         self._h = h
         self.mode, self.pad, self.dtype, self.extent, self.is1d = mode, pad, dtype, extent, is1d
         info = _lib.PlanInfo()
@@ -48,12 +66,26 @@ class Plan:
         self.info = info
         self.p, self.q = info.p, info.q
         self.C, self.H, self.W, self.Ho, self.Wo = info.C, info.H, info.W, info.Ho, info.Wo
+        self.rank = info.rank
+        nd = isinstance(p, (tuple, list))
+        # spatial dims of the tensors run() takes: (H, W) for fcfs_plan_ex plans
+        # (FCFS_FLAG_1D included), the plan's own rank for ND plans
+        r = info.rank if nd else 2
+        self.dims = tuple(info.dims[:r]) if nd else (info.H, info.W)
+        self.odims = tuple(info.odims[:r]) if nd else (info.Ho, info.Wo)
+        self.factors = tuple(zip(info.pd[:info.rank], info.qd[:info.rank]))
 
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
             _lib.lib.fcfs_destroy(h)
             self._h = None
+
+    @classmethod
+    def nd(cls, p, q, mode="bilinear", pad="replicate", C=1, dims=(1,), dtype="float32", extent="paper",
+           force_reference=False):
+        """ND plan with per-dimension factors p[d]/q[d] over spatial dims (D, H, W order)."""
+        return cls(tuple(p), tuple(q), mode, pad, C, tuple(dims), 1, dtype, extent, False, force_reference)
 
     @property
     def handle(self):
@@ -114,14 +146,20 @@ class Plan:
         if tuple(t.shape) != tuple(shape):
             raise ValueError(f"{what} shape {tuple(t.shape)} != {tuple(shape)}")
 
+    def in_shape(self, N: int):
+        return (N, self.C) + self.dims
+
+    def out_shape(self, N: int):
+        return (N, self.C) + self.odims
+
     def run(self, x, out=None, stream=None):
-        """out[N, C, Ho, Wo] = FCFS(x[N, C, H, W]) on the current (or given) stream."""
+        """out[N, C, *odims] = FCFS(x[N, C, *dims]) on the current (or given) stream."""
         import torch
         N = x.shape[0]
-        self._check_tensor(x, (N, self.C, self.H, self.W), "input")
+        self._check_tensor(x, self.in_shape(N), "input")
         if out is None:
-            out = torch.empty((N, self.C, self.Ho, self.Wo), dtype=x.dtype, device=x.device)
-        self._check_tensor(out, (N, self.C, self.Ho, self.Wo), "output")
+            out = torch.empty(self.out_shape(N), dtype=x.dtype, device=x.device)
+        self._check_tensor(out, self.out_shape(N), "output")
         check(_lib.lib.fcfs_run(self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), N,
                                 self._stream(stream)), "fcfs_run")
         return out
@@ -129,11 +167,14 @@ class Plan:
     def run_rows(self, x_rows, in_row0: int, out_row0: int, out_nrows: int, out=None, stream=None):
         """Output rows [out_row0, out_row0+out_nrows) from input rows [in_row0, in_row0+x_rows.shape[2])."""
         import torch
-        N, in_nrows = x_rows.shape[0], x_rows.shape[2]
-        self._check_tensor(x_rows, (N, self.C, in_nrows, self.W), "input rows")
+        if len(self.dims) < 2:
+            raise ValueError("row windows need a plan with rows (rank >= 2)")
+        N, in_nrows = x_rows.shape[0], x_rows.shape[-2]
+        self._check_tensor(x_rows, (N, self.C) + self.dims[:-2] + (in_nrows, self.W), "input rows")
+        oshape = (N, self.C) + self.odims[:-2] + (out_nrows, self.Wo)
         if out is None:
-            out = torch.empty((N, self.C, out_nrows, self.Wo), dtype=x_rows.dtype, device=x_rows.device)
-        self._check_tensor(out, (N, self.C, out_nrows, self.Wo), "output rows")
+            out = torch.empty(oshape, dtype=x_rows.dtype, device=x_rows.device)
+        self._check_tensor(out, oshape, "output rows")
         check(_lib.lib.fcfs_run_rows(self._h, ctypes.c_void_p(x_rows.data_ptr()), in_row0, in_nrows,
                                      ctypes.c_void_p(out.data_ptr()), out_row0, out_nrows, N,
                                      self._stream(stream)), "fcfs_run_rows")
@@ -155,8 +196,8 @@ def run_batch(jobs, stream=None):
     arr = (_lib.Job * len(jobs))()
     for i, (pl, x, out) in enumerate(jobs):
         N = x.shape[0]
-        pl._check_tensor(x, (N, pl.C, pl.H, pl.W), "input")
-        pl._check_tensor(out, (N, pl.C, pl.Ho, pl.Wo), "output")
+        pl._check_tensor(x, pl.in_shape(N), "input")
+        pl._check_tensor(out, pl.out_shape(N), "output")
         arr[i] = _lib.Job(pl.handle.value, x.data_ptr(), out.data_ptr(), N)
     s = torch.cuda.current_stream() if stream is None else stream
     check(_lib.lib.fcfs_run_batch(ctypes.cast(arr, ctypes.c_void_p), len(jobs), ctypes.c_void_p(s.cuda_stream)),
@@ -166,6 +207,26 @@ def run_batch(jobs, stream=None):
 
 _cache: dict = {}
 _cache_lock = threading.Lock()
+
+
+def scale_nd(x, p, q, mode: str = "bilinear", pad: str = "replicate", extent: str = "paper", out=None,
+             stream=None):
+    """FCFS-resize the last len(p) axes of a CUDA tensor x (N, C, *dims) by the
+    per-dimension factors p[d]/q[d] (§4.2): rank 1 (W), 2 (H, W) or 3 (D, H, W)."""
+    import torch
+    R = len(p)
+    if x.dim() != R + 2:
+        raise ValueError(f"expected an (N, C, {R} spatial dims) tensor, got shape {tuple(x.shape)}")
+    x = x.contiguous()
+    with torch.cuda.device(x.device):
+        key = ("nd", tuple(p), tuple(q), mode, pad, x.shape[1], tuple(x.shape[2:]), _dtype_name(x.dtype), extent,
+               x.device.index)
+        with _cache_lock:
+            pl = _cache.get(key)
+            if pl is None:
+                pl = Plan.nd(p, q, mode, pad, x.shape[1], tuple(x.shape[2:]), _dtype_name(x.dtype), extent)
+                _cache[key] = pl
+        return pl.run(x, out=out, stream=stream)
 
 
 def get_plan(p, q, mode, pad, C, H, W, dtype, extent="paper", is1d=False, device=None) -> Plan:

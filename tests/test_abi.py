@@ -99,7 +99,7 @@ def test_unknown_enum_and_flags():
     assert _lib.lib.fcfs_plan_ex(3, 2, 0, 0, 1, 4, 4, 0, 1 << 20, ctypes.byref(h)) == 1
     assert _lib.lib.fcfs_plan_ex(3, 2, 0, 0, 1, 4, 4, 0, 0, None) == 1
     assert _lib.lib.fcfs_status_str(6).decode() == "CUDA error"
-    assert _lib.lib.fcfs_version() == 1
+    assert _lib.lib.fcfs_version() == 2
 
 
 def test_run_without_device_is_refused(fc):
@@ -132,8 +132,49 @@ def test_kernel_selection(fc):
     assert fc.Plan(2, 3, "nearest", "zero", 1, 512, 512).kernel == "nearest_gather"
     assert fc.Plan(27, 11, "bicubic", "replicate", 1, 64, 64).kernel == "reference"  # no fused variant
     assert fc.Plan(3, 2, "bilinear", "replicate", 1, 64, 101).kernel == "reference"  # row pitch not 16-B
-    assert fc.Plan(3, 2, "bilinear", "replicate", 1, 64, 64, is1d=True).kernel == "reference"
+    # 1D rows run the fused kernel with a 1/1 row factor (the "width-only" variants)
+    assert fc.Plan(3, 2, "bilinear", "replicate", 1, 64, 64, is1d=True).kernel == "fused_separable"
     assert fc.Plan(3, 2, "bilinear", "replicate", 1, 64, 64, force_reference=True).kernel == "reference"
+    # per-dimension factors (§4.2)
+    assert fc.Plan.nd((1, 3), (1, 4), "bicubic", "reflect", 3, (64, 64), "float16").kernel == "fused_separable"
+    assert fc.Plan.nd((5, 1), (3, 1), "bilinear", "zero", 3, (64, 64), "bfloat16").kernel == "fused_separable"
+    assert fc.Plan.nd((5, 3), (3, 4), "bilinear", "zero", 3, (64, 64)).kernel == "reference"  # no variant
+    assert fc.Plan.nd((2, 3, 5), (1, 2, 3), "nearest", "zero", 1, (8, 16, 16)).kernel == "nearest_gather"
+    assert fc.Plan.nd((2, 3, 3), (1, 2, 2), "bicubic", "zero", 1, (8, 16, 16)).kernel == "reference"
+    assert fc.Plan.nd((1, 3, 3), (1, 2, 2), "bicubic", "zero", 1, (8, 16, 16)).kernel == "fused_separable"
+    assert fc.Plan.nd([3], [2], "bilinear", "zero", 2, (64,)).kernel == "fused_separable"
+
+
+def test_nd_plan_shapes_and_tables(fc):
+    """Per-dimension extents, info fields and phase tables against the oracle."""
+    import oracle
+    for dims, p, q, mode in [((9, 17, 32), (3, 2, 5), (2, 3, 3), "bicubic"), ((40, 24), (5, 1), (3, 4), "bilinear"),
+                             ((101,), (2,), (3,), "nearest")]:
+        for ext in ("paper", "floor"):
+            pl = fc.Plan.nd(p, q, mode, "replicate", 2, dims, "float32", ext)
+            R = len(dims)
+            assert pl.rank == R and pl.dims == dims
+            assert pl.odims == oracle.output_dims_nd(dims, p, q, ext == "floor")
+            assert pl.factors == tuple(zip(p, q))
+            for d in range(R):
+                w = (ctypes.c_float * (4 * p[d]))()
+                b = (ctypes.c_int * p[d])()
+                assert fc._lib.lib.fcfs_phase_table_dim(pl.handle, d, w, b) == 0
+                for j in range(p[d]):
+                    first, ow = oracle.phase_taps(mode, p[d], q[d], j)
+                    assert b[j] == (j * q[d]) // p[d]
+                    np.testing.assert_array_equal(np.float32(ow), np.float32(list(w)[4 * j: 4 * j + len(ow)]))
+            od = (ctypes.c_int64 * R)()
+            assert fc._lib.lib.fcfs_output_dims(pl.handle, od) == 0 and tuple(od) == pl.odims
+            assert fc._lib.lib.fcfs_phase_table_dim(pl.handle, R, w, b) == 1  # FCFS_E_ARG
+    # rank outside 1..3, 1D flag with the ND form, reflect that cannot reach (D = 2, bicubic up)
+    h = ctypes.c_void_p()
+    one = (ctypes.c_int * 4)(1, 1, 1, 1)
+    dims4 = (ctypes.c_int64 * 4)(2, 2, 2, 2)
+    assert fc._lib.lib.fcfs_plan_nd(4, one, one, 1, 0, 1, dims4, 0, 0, ctypes.byref(h)) == 1
+    assert fc._lib.lib.fcfs_plan_nd(2, one, one, 1, 0, 1, dims4, 0, 1, ctypes.byref(h)) == 1
+    with pytest.raises(fc.FcfsError):
+        fc.Plan.nd((5, 1, 1), (2, 1, 1), "bicubic", "reflect", 1, (2, 8, 8))
 
 
 @pytest.mark.parametrize("name", ["C1a", "C1b", "C2a", "C2b", "C3", "C4a", "C4b", "C5"])
@@ -150,7 +191,7 @@ def test_launch_geometry(fc, name):
         return
     assert info["smem"] <= 113 * 1024 and info["S"] >= 2 and info["grid"] <= 296
     assert info["CPT"] * info["ntile"] >= info["nch"] and info["NS"] * info["CPT"] <= 256
-    assert info["nch"] * info["K"] * info["P"] >= pl.Wo
+    assert info["nch"] * info["K"] * info["PX"] >= pl.Wo
     assert info["PB"] * info["nbands"] >= info["periods"]
     assert info["ntasks"] == -(-info["nseg"] // info["NS"]) * info["nbands"]
     if name in ("C3", "C4a", "C4b", "C5"):
