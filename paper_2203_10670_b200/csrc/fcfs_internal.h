@@ -66,6 +66,8 @@ struct NearestArgs {     // nearest gather (one output row per warp pass slot)
 
 // Fused separable kernel (bilinear / bicubic), see fused.cuh for the layout.
 // A task = NS segments x one band of y-periods; a segment = (plane, column tile).
+constexpr int kZMax = 16;  // slice phases a fused 3D variant takes
+
 struct FusedArgs {
     const void *in;
     void *out;
@@ -94,6 +96,15 @@ struct FusedArgs {
     int32_t plane_even;  // > 0: segment order visits the even planes (this many) before the odd
                          // ones, so that 16-bit outputs whose plane size is odd keep one 4-B
                          // phase per task (packed staging stores without warp divergence)
+    int32_t row_pitch;   // bytes between the rows of a segment in a stage (= TZ * seg_pitch)
+    // 3D variants (TZ > 1): every plane has Do output slices from D input
+    // slices; output slice m_z combines the TZ input slices b_z + lo + t with
+    // the slice weights of phase j_z = m_z mod pz (reference contract: slices,
+    // then columns, then rows).  Segments are ordered slice-major.
+    int32_t D, Do, pz, qz;
+    int64_t in_slice_stride, out_slice_stride;  // elements between slices of a plane
+    float zw[kZMax][4];
+    int32_t zbase[kZMax];
 };
 
 // Several nearest jobs (same dtype) in one launch (fcfs_run_batch).
@@ -115,9 +126,10 @@ int launch_nearest_batch(int dtype, const NearestBatch &nb, void *stream);
 struct FusedVariant {
     const void *fn;
     int PY, QY, PX, QX, TAPS, LO, K;
+    int TZ;                        // 1: 2D planes; TAPS: 3D (slice taps combined in the kernel)
     const float *wtab_y, *wtab_x;  // the variant's compile-time phase weights, [4*j + t]
 };
-const FusedVariant *fused_lookup(int dtype, int py, int qy, int px, int qx, int ntaps);
+const FusedVariant *fused_lookup(int dtype, int py, int qy, int px, int qx, int ntaps, bool slices);
 int launch_fused(const FusedVariant *v, const FusedArgs &a, int grid, int block, int smem, void *stream);
 
 constexpr int kFusedConsumerWarps = 8;

@@ -149,7 +149,7 @@ __device__ __forceinline__ void store_row(T *sr, const float (&o)[KP], int nvali
 
 // Geometry of one segment (plane x column tile).
 struct SegGeo {
-    int plane, ch0, ch1, c0, c1, a0, a1;
+    int plane, mz, ch0, ch1, c0, c1, a0, a1;  // mz: output slice (3D variants), else 0
 };
 
 template <int P, int Q, int TAPS, int LO, int K, int ESZ>
@@ -159,9 +159,12 @@ __device__ __forceinline__ SegGeo seg_geo(const FusedArgs &a, int gs) {
     SegGeo s;
     const int k = gs / a.ntile;
     const int tile = gs - k * a.ntile;
+    // slice-major: consecutive segments share an output slice (3D; 0 in 2D)
+    s.mz = k / a.planes;
+    const int kp = k - s.mz * a.planes;
     // plane_even > 0: even planes first, then odd ones (a task's planes share
     // the 4-B phase of their output plane start; see FusedArgs::plane_even)
-    s.plane = a.plane_even ? (k < a.plane_even ? 2 * k : 2 * (k - a.plane_even) + 1) : k;
+    s.plane = a.plane_even ? (kp < a.plane_even ? 2 * kp : 2 * (kp - a.plane_even) + 1) : kp;
     s.ch0 = tile * a.CPT;
     s.ch1 = min(a.nch, s.ch0 + a.CPT);
     s.c0 = s.ch0 * K * P;
@@ -234,7 +237,13 @@ struct StageCursor {
     }
 };
 
-template <typename T, int PY, int QY, int PX, int QX, int TAPS, int LO, int K>
+// first input slice b_z + lo of output slice mz (3D variants)
+__device__ __forceinline__ int slice_base(const FusedArgs &a, int mz, int lo) {
+    const int jz = mz % a.pz;
+    return (mz / a.pz) * a.qz + a.zbase[jz] + lo;
+}
+
+template <typename T, int PY, int QY, int PX, int QX, int TAPS, int LO, int K, int TZ>
 __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __grid_constant__ FusedArgs a) {
     using GY = Geo<PY, QY, TAPS, LO>;  // rows: y-periods of PY output rows from QY input rows
     using GX = Geo<PX, QX, TAPS, LO>;  // columns: x-periods of PX outputs from QX inputs
@@ -250,6 +259,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     constexpr int PAR = (ESZ == 2 && (K * QX) % 2 == 0) ? ((LO % 2 + 2) % 2) : -1;
     static_assert(PX <= 16 && PY <= 16, "fused variants have p <= 16");
     static_assert(-LO <= A, "left margin too small");
+    static_assert(TZ == 1 || TZ == TAPS, "slice taps: none or the mode's");
 
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);   // TMA landed       (count 1 + tx)
@@ -280,13 +290,19 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 if (ci.seq >= (uint32_t)a.S) mbar_wait(&empty[ci.slot], ci.phase ^ 1);
                 int vf, nr;
                 ci.rows(vf, nr);
-                int nreal = 0;  // rows that are not zero padding
-                for (int r = 0; r < nr; ++r) nreal += !(a.pad == FCFS_PAD_ZERO && (vf + r < 0 || vf + r >= a.H));
                 SegGeo sg;
                 uint32_t seg_bytes = 0;
+                int z0 = 0;      // first input slice of this lane's segment (3D)
+                int nreal = 0;   // (row, slice) sub-rows of the stage that are not zero padding
                 if (lane < ci.b.nsg) {
                     sg = seg_geo<PX, QX, TAPS, LO, K, ESZ>(a, ci.b.group * a.NS + lane);
                     seg_bytes = (uint32_t)(sg.a1 - sg.a0) * ESZ;
+                    if constexpr (TZ > 1) z0 = slice_base(a, sg.mz, LO);
+                    for (int r = 0; r < nr; ++r)
+#pragma unroll
+                        for (int tz = 0; tz < TZ; ++tz)
+                            nreal += !(a.pad == FCFS_PAD_ZERO && (vf + r < 0 || vf + r >= a.H ||
+                                                                 (TZ > 1 && (z0 + tz < 0 || z0 + tz >= a.D))));
                 }
                 uint32_t tot = seg_bytes * (uint32_t)nreal;
 #pragma unroll
@@ -295,13 +311,23 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 __syncwarp();
                 if (lane < ci.b.nsg) {  // lane s issues the rows of segment s
                     const T *pin = static_cast<const T *>(a.in) + (int64_t)sg.plane * a.in_plane_stride + sg.a0;
-                    unsigned char *sbase = stages + ci.slot * a.stage_bytes + A * ESZ + lane * a.SR * a.seg_pitch;
+                    unsigned char *sbase = stages + ci.slot * a.stage_bytes + A * ESZ + lane * a.SR * a.row_pitch;
                     for (int r = 0; r < nr; ++r) {
                         const int v = vf + r;
                         if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;
                         // rows outside the window only feed masked outputs: clamp
                         const int src = min(max(pad_src32(v, a.H, a.pad) - a.in_row0, 0), a.in_nrows - 1);
-                        bulk_g2s(sbase + r * a.seg_pitch, pin + (int64_t)src * a.W, seg_bytes, &full[ci.slot], pol);
+#pragma unroll
+                        for (int tz = 0; tz < TZ; ++tz) {
+                            int64_t soff = 0;
+                            if constexpr (TZ > 1) {
+                                const int sl = z0 + tz;
+                                if (a.pad == FCFS_PAD_ZERO && (sl < 0 || sl >= a.D)) continue;
+                                soff = (int64_t)min(max(pad_src32(sl, a.D, a.pad), 0), a.D - 1) * a.in_slice_stride;
+                            }
+                            bulk_g2s(sbase + r * a.row_pitch + tz * a.seg_pitch, pin + soff + (int64_t)src * a.W,
+                                     seg_bytes, &full[ci.slot], pol);
+                        }
                     }
                 }
                 __syncwarp();
@@ -322,24 +348,36 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 int vf, nr;
                 cf.rows(vf, nr);
                 unsigned char *sbase = stages + cf.slot * a.stage_bytes;
-                const int pairs = cf.b.nsg * nr;
-                if (a.pad == FCFS_PAD_ZERO && (vf < 0 || vf + nr > a.H)) {
-                    // zero-padding rows (§3 Padding, zeros): written as zeros so
-                    // that consumers filter every row the same way
-                    const int n16 = a.seg_pitch / 16;
-                    for (int u = lane; u < pairs * n16; u += 32) {
-                        const int sr = u / n16, c16 = u - sr * n16;
-                        const int s = sr / nr, r = sr - s * nr;
-                        if (vf + r >= 0 && vf + r < a.H) continue;
-                        reinterpret_cast<uint4 *>(sbase + (s * a.SR + r) * a.seg_pitch)[c16] = make_uint4(0, 0, 0, 0);
+                const int pairs = cf.b.nsg * nr * TZ;  // (segment, row, slice) sub-rows
+                const int n16 = a.seg_pitch / 16;
+                if constexpr (TZ == 1) {
+                    if (a.pad == FCFS_PAD_ZERO && (vf < 0 || vf + nr > a.H)) {
+                        // zero-padding rows (§3 Padding, zeros): written as zeros so
+                        // that consumers filter every row the same way
+                        for (int u = lane; u < pairs * n16; u += 32) {
+                            const int sr = u / n16, c16 = u - sr * n16;
+                            const int s = sr / nr, r = sr - s * nr;
+                            if (vf + r >= 0 && vf + r < a.H) continue;
+                            reinterpret_cast<uint4 *>(sbase + (s * a.SR + r) * a.row_pitch)[c16] = make_uint4(0, 0, 0, 0);
+                        }
                     }
                 }
                 for (int u = lane; u < pairs; u += 32) {
-                    const int s = u / nr, r = u - s * nr;
+                    const int s = u / (nr * TZ), rz = u - s * (nr * TZ), r = rz / TZ, tz = rz - r * TZ;
                     const int v = vf + r;
-                    if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;
                     const SegGeo sg = seg_geo<PX, QX, TAPS, LO, K, ESZ>(a, cf.b.group * a.NS + s);
-                    T *row = reinterpret_cast<T *>(sbase + (s * a.SR + r) * a.seg_pitch) + A - sg.a0;  // row[c]
+                    unsigned char *sub = sbase + (s * a.SR + r) * a.row_pitch + tz * a.seg_pitch;
+                    if constexpr (TZ == 1) {
+                        if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;  // zeroed above
+                    } else {
+                        const int sl = slice_base(a, sg.mz, LO) + tz;
+                        if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H || sl < 0 || sl >= a.D)) {
+                            // zero-padding row or slice
+                            for (int c16 = 0; c16 < n16; ++c16) reinterpret_cast<uint4 *>(sub)[c16] = make_uint4(0, 0, 0, 0);
+                            continue;
+                        }
+                    }
+                    T *row = reinterpret_cast<T *>(sub) + A - sg.a0;  // row[c]
                     if (sg.a0 == 0) {
 #pragma unroll
                         for (int c = LO; c < 0; ++c) {
@@ -393,15 +431,24 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             chl = j - sgi * (a.CPT - 1);
         }
         const bool seg_ok = sgi < b.nsg;
-        SegGeo sg = {0, 0, 0, 0, 0, 0, 1};
+        SegGeo sg = {0, 0, 0, 0, 0, 0, 0, 1};
         if (seg_ok) sg = seg_geo<PX, QX, TAPS, LO, K, ESZ>(a, b.group * a.NS + sgi);
         const int chunk = last ? sg.ch1 - 1 : sg.ch0 + chl;
         const bool active = seg_ok && (last || chunk < sg.ch1 - 1);
         const int e0 = A + chunk * K * QX + LO - sg.a0;  // window start (element) in a shared row
         const int col = chunk * KP;
         const int nvalid = sg.c1 - col;  // outputs of this chunk inside the tile (>= KP: all)
-        const int in_off = sgi * a.SR * a.seg_pitch;
-        const int64_t plane_out = (int64_t)sg.plane * a.out_plane_stride;
+        const int in_off = sgi * a.SR * a.row_pitch;
+        const int64_t plane_out = (int64_t)sg.plane * a.out_plane_stride + (int64_t)sg.mz * a.out_slice_stride;
+        // slice weights of this segment's output slice (3D): phase j_z; j_z = 0 copies its base slice
+        float wz[TZ];
+        bool z_copy = true;
+        if constexpr (TZ > 1) {
+            const int jz = sg.mz % a.pz;
+            z_copy = jz == 0;
+#pragma unroll
+            for (int t = 0; t < TZ; ++t) wz[t] = a.zw[jz][t];
+        }
         // global byte address of output row out_row0, column c0 of this thread's segment, mod 16
         const uint32_t mis_row0 =
             (uint32_t)(reinterpret_cast<uintptr_t>(a.out) + (plane_out + (full_width ? 0 : sg.c0)) * ESZ) & 15;
@@ -411,15 +458,34 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         const int span_seg = full_width ? span_id : (b.nsg > 0 ? span_id % b.nsg : 0);
         const int span_row = full_width ? 0 : span_id / max(b.nsg, 1);
         const bool span_ok = full_width ? span_id < b.nsg : span_row < a.JM;
-        SegGeo sq = {0, 0, 0, 0, 0, 0, 1};
+        SegGeo sq = {0, 0, 0, 0, 0, 0, 0, 1};
         if (span_ok) sq = seg_geo<PX, QX, TAPS, LO, K, ESZ>(a, b.group * a.NS + span_seg);
-        T *const span_out = static_cast<T *>(a.out) + (int64_t)sq.plane * a.out_plane_stride;
+        T *const span_out =
+            static_cast<T *>(a.out) + (int64_t)sq.plane * a.out_plane_stride + (int64_t)sq.mz * a.out_slice_stride;
 
         // horizontal taps of one window row into a ring slot
         // (zero-padding rows arrive as zeros: +0 for every tap, as in the reference kernel)
         auto row_h = [&](float(&h)[KP], const unsigned char *srow) {
             float win[WIN];
-            load_win<T, WIN, PAR>(reinterpret_cast<const T *>(srow), e0, win);
+            if constexpr (TZ == 1) {
+                load_win<T, WIN, PAR>(reinterpret_cast<const T *>(srow), e0, win);
+            } else {
+                // slice taps first (contract: slices, columns, rows): the TZ
+                // sub-rows of this window row combine into one row
+                float acc[WIN], cp[WIN];
+#pragma unroll
+                for (int t = 0; t < TZ; ++t) {
+                    float sub[WIN];
+                    load_win<T, WIN, PAR>(reinterpret_cast<const T *>(srow + t * a.seg_pitch), e0, sub);
+#pragma unroll
+                    for (int i = 0; i < WIN; ++i) {
+                        acc[i] = t == 0 ? __fmul_rn(wz[0], sub[i]) : __fmaf_rn(wz[t], sub[i], acc[i]);
+                        if (t == -LO) cp[i] = sub[i];
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < WIN; ++i) win[i] = z_copy ? cp[i] : acc[i];
+            }
             if constexpr (K == 2) {
                 // phase jx of both x-periods shares its weights: packed pairs
 #pragma unroll
@@ -462,7 +528,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             if (active) {
                 const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
 #pragma unroll
-                for (int i = 0; i < C; ++i) row_h(hr[i % TAPS], sb + i * a.seg_pitch);
+                for (int i = 0; i < C; ++i) row_h(hr[i % TAPS], sb + i * a.row_pitch);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
@@ -592,7 +658,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
 #pragma unroll
             for (int r = C; r < L; ++r) {
-                if (active) row_h(hr[(RO + r) % TAPS], sb + (r - C) * a.seg_pitch);
+                if (active) row_h(hr[(RO + r) % TAPS], sb + (r - C) * a.row_pitch);
 #pragma unroll
                 for (int jy = 0; jy < PY; ++jy) {
                     if (GY::last_row(jy) == r) {

@@ -17,3 +17,7 @@
 #define FCFS_W_X(X) FCFS_NONUNIT_PAIRS(X##_W)
 // rows only (columns 1/1)
 #define FCFS_H_X(X) FCFS_NONUNIT_PAIRS(X##_H)
+// 3D volumes: isotropic rows/columns, any slice factor (run-time slice weights)
+#define FCFS_Z_PAIRS(Y) \
+    Y(1, 1) Y(2, 1) Y(1, 2) Y(3, 2) Y(2, 3) Y(4, 3) Y(3, 4) Y(5, 3) Y(3, 5) Y(5, 4) Y(4, 5)
+#define FCFS_Z_X(X) FCFS_Z_PAIRS(X##_Z)

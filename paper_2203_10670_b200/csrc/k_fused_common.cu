@@ -8,18 +8,25 @@
 
 namespace fcfs {
 
-extern const FusedVariant kFusedVariants_f32_iso[], kFusedVariants_f32_w[], kFusedVariants_f32_h[];
-extern const FusedVariant kFusedVariants_f16_iso[], kFusedVariants_f16_w[], kFusedVariants_f16_h[];
-extern const FusedVariant kFusedVariants_bf16_iso[], kFusedVariants_bf16_w[], kFusedVariants_bf16_h[];
+extern const FusedVariant kFusedVariants_f32_iso[], kFusedVariants_f32_w[], kFusedVariants_f32_h[],
+    kFusedVariants_f32_z[];
+extern const FusedVariant kFusedVariants_f16_iso[], kFusedVariants_f16_w[], kFusedVariants_f16_h[],
+    kFusedVariants_f16_z[];
+extern const FusedVariant kFusedVariants_bf16_iso[], kFusedVariants_bf16_w[], kFusedVariants_bf16_h[],
+    kFusedVariants_bf16_z[];
 
-const FusedVariant *fused_lookup(int dtype, int py, int qy, int px, int qx, int ntaps) {
-    const FusedVariant *sets[3][3] = {{kFusedVariants_f32_iso, kFusedVariants_f32_w, kFusedVariants_f32_h},
-                                      {kFusedVariants_f16_iso, kFusedVariants_f16_w, kFusedVariants_f16_h},
-                                      {kFusedVariants_bf16_iso, kFusedVariants_bf16_w, kFusedVariants_bf16_h}};
+// slices: a 3D plan whose slice factor is not 1/1 (variants combining slice taps)
+const FusedVariant *fused_lookup(int dtype, int py, int qy, int px, int qx, int ntaps, bool slices) {
+    const FusedVariant *sets[3][4] = {
+        {kFusedVariants_f32_iso, kFusedVariants_f32_w, kFusedVariants_f32_h, kFusedVariants_f32_z},
+        {kFusedVariants_f16_iso, kFusedVariants_f16_w, kFusedVariants_f16_h, kFusedVariants_f16_z},
+        {kFusedVariants_bf16_iso, kFusedVariants_bf16_w, kFusedVariants_bf16_h, kFusedVariants_bf16_z}};
     if (dtype < 0 || dtype > 2) return nullptr;
     for (const FusedVariant *tab : sets[dtype])
         for (const FusedVariant *v = tab; v->fn; ++v)
-            if (v->PY == py && v->QY == qy && v->PX == px && v->QX == qx && v->TAPS == ntaps) return v;
+            if (v->PY == py && v->QY == qy && v->PX == px && v->QX == qx && v->TAPS == ntaps &&
+                (v->TZ > 1) == slices)
+                return v;
     return nullptr;
 }
 

@@ -1,4 +1,4 @@
-// Fused separable FCFS kernels: element type float, factor set "w" (fused_pairs.h).
+// Fused separable FCFS kernels: element type float, factor set "z" (3D) (fused_pairs.h).
 #include "fused_inst.cuh"
 
 #define V_ISO(P, Q) FCFS_BOTH_MODES(float, P, Q, P, Q)
@@ -6,5 +6,5 @@
 #define V_H(P, Q) FCFS_BOTH_MODES(float, P, Q, 1, 1)
 #define V_Z(P, Q) FCFS_BOTH_MODES_Z(float, P, Q, P, Q)
 namespace fcfs {
-extern const FusedVariant kFusedVariants_f32_w[] = {FCFS_W_X(V){nullptr, 0, 0, 0, 0, 0, 0, 0, 0, nullptr, nullptr}};
+extern const FusedVariant kFusedVariants_f32_z[] = {FCFS_Z_X(V){nullptr, 0, 0, 0, 0, 0, 0, 0, 0, nullptr, nullptr}};
 }  // namespace fcfs

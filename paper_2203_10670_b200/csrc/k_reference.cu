@@ -5,50 +5,45 @@
 // dimension d with factor p_d/q_d, output m_d = p_d*i + j_d has base
 // b_d = q_d*i + base_d[j_d] (§3.1.1, reading Z1), and
 //
-//   hx(s, r) = x~[s][r][b_x]                                   if j_x == 0 (fraction 0)
-//            = w_x[j_x][0]*x~[s][r][b_x+lo] (+fma) ... (+fma) w_x[j_x][T-1]*x~[s][r][b_x+lo+T-1]
-//            = 0                                               if slice s or row r is zero padding
-//   hz(r)    = hx(b_z, r)                                      if j_z == 0 (always in 2D)
-//            = w_z[j_z][0]*hx(b_z+lo, r) (+fma) ... w_z[j_z][T-1]*hx(b_z+lo+T-1, r)
-//   out      = hz(b_y)                                         if j_y == 0
-//            = w_y[j_y][0]*hz(b_y+lo) (+fma) ... w_y[j_y][T-1]*hz(b_y+lo+T-1)
+//   xz(r, c) = x~[b_z][r][c]                                   if j_z == 0 (always in 2D)
+//            = w_z[j_z][0]*x~[b_z+lo][r][c] (+fma) ... (+fma) w_z[j_z][T-1]*x~[b_z+lo+T-1][r][c]
+//   hx(r)    = xz(r, b_x)                                      if j_x == 0 (fraction 0)
+//            = w_x[j_x][0]*xz(r, b_x+lo) (+fma) ... w_x[j_x][T-1]*xz(r, b_x+lo+T-1)
+//   out      = hx(b_y)                                         if j_y == 0
+//            = w_y[j_y][0]*hx(b_y+lo) (+fma) ... w_y[j_y][T-1]*hx(b_y+lo+T-1)
 //
-// (fp32, __fmul_rn then __fmaf_rn in tap order: x first, then the slice
-// dimension, then rows; §4.2's kernels are outer products, so any order is the
-// same real number -- this one is the contract).  Nearest (one tap) is a pure
-// copy.  1D plans (FCFS_FLAG_1D) take out = hx(0, m_y).
+// with x~ = 0 wherever a slice, row or column index is zero padding (fp32,
+// __fmul_rn then __fmaf_rn in tap order: slices first, then columns, then
+// rows; §4.2's kernels are outer products, so any order is the same real
+// number -- this one is the contract).  Nearest (one tap) is a pure copy.  1D
+// plans (FCFS_FLAG_1D) take out = hx(m_y).
 #include "device_common.cuh"
 
 namespace fcfs {
 
+// slice pass at (row r, column c), virtual indices, padding applied
 template <typename T>
-__device__ __forceinline__ float xval(const T *__restrict__ row, int64_t c, int64_t W, int pad) {
-    int64_t s = pad_src(c, W, pad);
-    return s < 0 ? 0.0f : DT<T>::to_f(row[s]);
-}
-
-// horizontal pass of input row r of slice sl (virtual indices; padding applied)
-template <typename T>
-__device__ __forceinline__ float hxval(const T *__restrict__ plane, const RefArgs &a, int64_t sl, int64_t r, int jx,
-                                       int64_t bx) {
+__device__ __forceinline__ float xzval(const T *__restrict__ plane, const RefArgs &a, int jz, int64_t bz, int64_t r,
+                                       int64_t c) {
     const RunGeom &g = a.g;
-    if (a.pad == FCFS_PAD_ZERO && (r < 0 || r >= g.H || sl < 0 || sl >= g.D)) return 0.0f;
-    const int64_t ss = pad_src(sl, g.D, a.pad);
-    const int64_t rs = pad_src(r, g.H, a.pad) - g.in_row0;
-    const T *row = plane + (ss * g.in_nrows + rs) * g.W;
-    if (jx == 0 || a.tx.ntaps == 1) return xval(row, bx, g.W, a.pad);
-    float v = __fmul_rn(a.tx.w[jx][0], xval(row, bx + a.tx.lo, g.W, a.pad));
-    for (int t = 1; t < a.tx.ntaps; ++t) v = __fmaf_rn(a.tx.w[jx][t], xval(row, bx + a.tx.lo + t, g.W, a.pad), v);
+    auto at = [&](int64_t sl) -> float {
+        const int64_t ss = pad_src(sl, g.D, a.pad), rs = pad_src(r, g.H, a.pad), cs = pad_src(c, g.W, a.pad);
+        if (ss < 0 || rs < 0 || cs < 0) return 0.0f;
+        return DT<T>::to_f(plane[(ss * g.in_nrows + rs - g.in_row0) * g.W + cs]);
+    };
+    if (jz == 0 || a.tz.ntaps == 1) return at(bz);
+    float v = __fmul_rn(a.tz.w[jz][0], at(bz + a.tz.lo));
+    for (int t = 1; t < a.tz.ntaps; ++t) v = __fmaf_rn(a.tz.w[jz][t], at(bz + a.tz.lo + t), v);
     return v;
 }
 
-// slice-dimension pass at row r (identity in 2D: j_z = 0, b_z = 0)
+// column pass of row r
 template <typename T>
-__device__ __forceinline__ float hzval(const T *__restrict__ plane, const RefArgs &a, int jz, int64_t bz, int64_t r,
+__device__ __forceinline__ float hxval(const T *__restrict__ plane, const RefArgs &a, int jz, int64_t bz, int64_t r,
                                        int jx, int64_t bx) {
-    if (jz == 0 || a.tz.ntaps == 1) return hxval(plane, a, bz, r, jx, bx);
-    float v = __fmul_rn(a.tz.w[jz][0], hxval(plane, a, bz + a.tz.lo, r, jx, bx));
-    for (int t = 1; t < a.tz.ntaps; ++t) v = __fmaf_rn(a.tz.w[jz][t], hxval(plane, a, bz + a.tz.lo + t, r, jx, bx), v);
+    if (jx == 0 || a.tx.ntaps == 1) return xzval(plane, a, jz, bz, r, bx);
+    float v = __fmul_rn(a.tx.w[jx][0], xzval(plane, a, jz, bz, r, bx + a.tx.lo));
+    for (int t = 1; t < a.tx.ntaps; ++t) v = __fmaf_rn(a.tx.w[jx][t], xzval(plane, a, jz, bz, r, bx + a.tx.lo + t), v);
     return v;
 }
 
@@ -72,16 +67,16 @@ __global__ void __launch_bounds__(256) fcfs_reference_kernel(const __grid_consta
         const int64_t bz = (mz / a.tz.p) * a.tz.q + a.tz.base[jz];
         float out;
         if (a.is1d) {
-            out = hxval(src, a, 0, my, jx, bx);
+            out = hxval(src, a, 0, 0, my, jx, bx);
         } else {
             const int jy = (int)(my % a.ty.p);
             const int64_t by = (my / a.ty.p) * a.ty.q + a.ty.base[jy];
             if (jy == 0 || a.ty.ntaps == 1) {
-                out = hzval(src, a, jz, bz, by, jx, bx);
+                out = hxval(src, a, jz, bz, by, jx, bx);
             } else {
-                out = __fmul_rn(a.ty.w[jy][0], hzval(src, a, jz, bz, by + a.ty.lo, jx, bx));
+                out = __fmul_rn(a.ty.w[jy][0], hxval(src, a, jz, bz, by + a.ty.lo, jx, bx));
                 for (int k = 1; k < a.ty.ntaps; ++k)
-                    out = __fmaf_rn(a.ty.w[jy][k], hzval(src, a, jz, bz, by + a.ty.lo + k, jx, bx), out);
+                    out = __fmaf_rn(a.ty.w[jy][k], hxval(src, a, jz, bz, by + a.ty.lo + k, jx, bx), out);
             }
         }
         static_cast<T *>(g.out)[plane * g.out_plane_stride + (mz * g.out_nrows + lr) * g.Wo + mx] = DT<T>::from_f(out);

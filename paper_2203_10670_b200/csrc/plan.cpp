@@ -163,7 +163,7 @@ struct FusedLaunch {
 
 bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     const FusedVariant *v = pl->fused;
-    const int PY = v->PY, QY = v->QY, PX = v->PX, QX = v->QX, K = v->K, TAPS = v->TAPS, LO = v->LO;
+    const int PY = v->PY, QY = v->QY, PX = v->PX, QX = v->QX, K = v->K, TAPS = v->TAPS, LO = v->LO, TZ = v->TZ;
     const int ESZ = esize(pl->dtype), A = 16 / ESZ;
     // y-period window (rows): L rows, C carried to the next period, F fresh
     const int HIy = ((PY - 1) * QY) / PY + LO + TAPS - 1;
@@ -191,6 +191,19 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     a.out_nrows = (int32_t)g.out_nrows;
     a.planes = (int32_t)g.planes;
     a.pad = pl->pad;
+    a.D = (int32_t)g.D;
+    a.Do = (int32_t)g.Do;
+    a.pz = a.qz = 1;
+    if (TZ > 1) {
+        a.pz = pl->pz;
+        a.qz = pl->qz;
+        a.in_slice_stride = g.in_nrows * g.W;
+        a.out_slice_stride = g.out_nrows * g.Wo;
+        for (int j = 0; j < pl->pz; ++j) {
+            a.zbase[j] = pl->tabz.base[j];
+            for (int t = 0; t < 4; ++t) a.zw[j][t] = pl->tabz.w[j][t];
+        }
+    }
     a.nch = (int32_t)((g.Wo + KP - 1) / KP);
     a.SR = std::max(Ff, Cc);
     const int WIN = (K - 1) * QX + Lw;
@@ -222,14 +235,15 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
             c.CPT = (int32_t)((a.nch + nt - 1) / nt);
             c.ntile = (int32_t)((a.nch + c.CPT - 1) / c.CPT);
             if (nt > min_tiles && c.ntile != nt) continue;
-            const int64_t nseg = g.planes * c.ntile;
+            const int64_t nseg = g.planes * g.Do * c.ntile;  // (output slice, plane, column tile)
             if (nseg > INT32_MAX) continue;
             c.nseg = (int32_t)nseg;
             const int span_cap = c.ntile == 1 ? 16 : 16 / c.JM;  // copy-out spans per flush <= 16
             c.NS = (int32_t)std::min<int64_t>(std::min(NT / c.CPT, span_cap), nseg);
             if (c.NS < 1) continue;
             c.seg_pitch = seg_pitch_for(c.CPT);
-            c.stage_bytes = c.NS * c.SR * c.seg_pitch;
+            c.row_pitch = TZ * c.seg_pitch;
+            c.stage_bytes = c.NS * c.SR * c.row_pitch;
             if (c.ntile == 1) {
                 c.out_pitch = (int)(((int64_t)c.JM * g.Wo * ESZ + 16 + 15) / 16 * 16);
                 c.slot_bytes = c.NS * c.out_pitch;
@@ -253,7 +267,8 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     }
     if (best_score < 0) return false;
     a = best;
-    if (ESZ == 2 && a.ntile == 1 && (g.out_plane_stride & 1) && g.planes > 1) a.plane_even = (int32_t)((g.planes + 1) / 2);
+    if (TZ == 1 && ESZ == 2 && a.ntile == 1 && (g.out_plane_stride & 1) && g.planes > 1)
+        a.plane_even = (int32_t)((g.planes + 1) / 2);
     a.iy_first = (int32_t)(g.out_row0 / PY);
     a.iy_last = (int32_t)((g.out_row0 + g.out_nrows - 1) / PY);
     const int nper = a.iy_last - a.iy_first + 1;
@@ -276,13 +291,13 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     if (const char *e = std::getenv("FCFS_DEBUG_S")) a.S = std::max(2, std::min(a.S, std::atoi(e)));
     L.smem = 256 + a.S * a.stage_bytes + 128 + 2 * a.slot_bytes;
     std::snprintf(L.desc, sizeof(L.desc),
-                  "{\"kernel\": \"fused_separable\", \"PY\": %d, \"QY\": %d, \"PX\": %d, \"QX\": %d, \"taps\": %d, "
+                  "{\"kernel\": \"fused_separable\", \"PY\": %d, \"QY\": %d, \"PX\": %d, \"QX\": %d, \"TZ\": %d, \"taps\": %d, "
                   "\"K\": %d, \"NS\": %d, "
                   "\"CPT\": %d, \"nch\": %d, \"ntile\": %d, \"nseg\": %d, \"S\": %d, \"SR\": %d, \"seg_pitch\": %d, "
                   "\"stage_bytes\": %d, \"out_pitch\": %d, \"slot_bytes\": %d, \"rfix\": %d, \"periods\": %d, "
                   "\"PB\": %d, \"nbands\": %d, \"ntasks\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, "
                   "\"busy_threads\": %d, \"flush_groups\": %d}",
-                  PY, QY, PX, QX, TAPS, K, a.NS, a.CPT, a.nch, a.ntile, a.nseg, a.S, a.SR, a.seg_pitch, a.stage_bytes,
+                  PY, QY, PX, QX, TZ, TAPS, K, a.NS, a.CPT, a.nch, a.ntile, a.nseg, a.S, a.SR, a.seg_pitch, a.stage_bytes,
                   a.out_pitch, a.slot_bytes, a.rfix, nper, a.PB, a.nbands, a.ntasks, L.grid, kFusedThreads, L.smem,
                   a.NS * a.CPT, a.G);
     if (std::getenv("FCFS_DEBUG_PRINT")) std::fprintf(stderr, "%s\n", L.desc);
@@ -323,12 +338,14 @@ int select_kernel(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
         // 3D plans reach the fused kernel only with an identity slice factor:
         // then every slice is an independent 2D plane
         RunGeom g2 = g;
-        g2.planes = g.planes * g.D;
-        g2.D = g2.Do = 1;
-        g2.in_plane_stride = g.in_nrows * pl->W;
-        g2.out_plane_stride = g.out_nrows * pl->Wo;
+        if (pl->fused->TZ == 1) {
+            g2.planes = g.planes * g.D;
+            g2.D = g2.Do = 1;
+            g2.in_plane_stride = g.in_nrows * pl->W;
+            g2.out_plane_stride = g.out_nrows * pl->Wo;
+        }
         if ((reinterpret_cast<uintptr_t>(g.in) & 15) ||
-            g2.planes * std::max(g.in_nrows * pl->W, g.out_nrows * pl->Wo) > INT32_MAX * 16LL || !plan_fused(pl, g2, L))
+            g2.planes * std::max(g2.D, g2.Do) * std::max(g.in_nrows * pl->W, g.out_nrows * pl->Wo) > INT32_MAX * 16LL || !plan_fused(pl, g2, L))
             kernel = 0;
     }
     if (kernel == 1) {
@@ -524,9 +541,12 @@ fcfs_status make_plan(int rank, const int *pd, const int *qd, int mode, int pad,
     if (!(flags & FCFS_FLAG_FORCE_REFERENCE)) {
         if (mode == FCFS_NEAREST) {
             pl->kernel = 1;
-        } else if ((pl->W * esize(dtype)) % 16 == 0 && pl->pz == 1 && pl->qz == 1) {
-            // separable fused kernel: rows by py/qy (1/1 for 1D rows), columns by p/q
-            pl->fused = fused_lookup(dtype, pl->py, pl->qy, pl->p, pl->q, pl->tab.ntaps);
+        } else if ((pl->W * esize(dtype)) % 16 == 0 && pl->pz <= kZMax) {
+            // separable fused kernel: rows by py/qy (1/1 for 1D rows), columns by
+            // p/q; 3D plans with a slice factor other than 1/1 take the variants
+            // that combine slice taps (run-time slice weights)
+            const bool slices = !(pl->pz == 1 && pl->qz == 1);
+            pl->fused = fused_lookup(dtype, pl->py, pl->qy, pl->p, pl->q, pl->tab.ntaps, slices);
             // the variant's compile-time weights must be this plan's tables, bit for bit
             for (int j = 0; pl->fused && j < pl->p; ++j)
                 for (int t = 0; t < pl->tab.ntaps; ++t)

@@ -140,7 +140,10 @@ def test_kernel_selection(fc):
     assert fc.Plan.nd((5, 1), (3, 1), "bilinear", "zero", 3, (64, 64), "bfloat16").kernel == "fused_separable"
     assert fc.Plan.nd((5, 3), (3, 4), "bilinear", "zero", 3, (64, 64)).kernel == "reference"  # no variant
     assert fc.Plan.nd((2, 3, 5), (1, 2, 3), "nearest", "zero", 1, (8, 16, 16)).kernel == "nearest_gather"
-    assert fc.Plan.nd((2, 3, 3), (1, 2, 2), "bicubic", "zero", 1, (8, 16, 16)).kernel == "reference"
+    assert fc.Plan.nd((2, 3, 3), (1, 2, 2), "bicubic", "zero", 1, (8, 16, 16)).kernel == "fused_separable"
+    assert fc.Plan.nd((7, 5, 5), (3, 3, 3), "bilinear", "zero", 1, (8, 16, 16)).kernel == "fused_separable"
+    assert fc.Plan.nd((2, 3, 5), (1, 2, 3), "bicubic", "zero", 1, (8, 16, 16)).kernel == "reference"  # y != x
+    assert fc.Plan.nd((17, 3, 3), (5, 2, 2), "bicubic", "zero", 1, (8, 16, 16)).kernel == "reference"  # pz > 16
     assert fc.Plan.nd((1, 3, 3), (1, 2, 2), "bicubic", "zero", 1, (8, 16, 16)).kernel == "fused_separable"
     assert fc.Plan.nd([3], [2], "bilinear", "zero", 2, (64,)).kernel == "fused_separable"
 

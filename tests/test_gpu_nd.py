@@ -85,6 +85,19 @@ def test_volumes_3d(mode, dtype):
         check(x, p, q, mode, ["zero", "replicate", "reflect"][i])
 
 
+@pytest.mark.parametrize("mode", ["bilinear", "bicubic"])
+@pytest.mark.parametrize("dtype", ["float32", "float16", "bfloat16"])
+def test_volumes_3d_fused_slice_taps(mode, dtype):
+    """3D plans whose slice factor is not 1/1 run the fused variants that combine
+    the slice taps in the kernel; bitwise equal to the reference kernel."""
+    x = make_x(49, (2, 3, 11, 30, 72), dtype)
+    for i, (p, q) in enumerate([((3, 2, 2), (2, 3, 3)), ((5, 3, 3), (7, 2, 2)), ((2, 4, 4), (1, 3, 3)),
+                                ((11, 5, 5), (4, 4, 4))]):
+        for ext in ("floor", "paper"):
+            check(x, p, q, mode, ["zero", "replicate", "reflect"][(i + (ext == "paper")) % 3], extent=ext,
+                  expect_kernel="fused_separable")
+
+
 def test_volume_identity_slice_factor_runs_fused():
     x = make_x(44, (2, 3, 5, 40, 64), "float16")
     pl = check(x, (1, 5, 5), (1, 3, 3), "bicubic", "reflect", expect_kernel="fused_separable")
