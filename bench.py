@@ -144,7 +144,10 @@ def oracle_sample_run(cfgs, planes_per_cfg: int):
             continue
         x = synth.make_values(cfg, 0, n_img)
         t0 = time.perf_counter()
-        y = oracle.staged(x, cfg.p, cfg.q, cfg.mode, cfg.pad, floor_extent=cfg.floor_extent, is1d=cfg.is1d)
+        if cfg.nd:
+            y = oracle.staged_nd(x, cfg.pd, cfg.qd, cfg.mode, cfg.pad, floor_extent=cfg.floor_extent)
+        else:
+            y = oracle.staged(x, cfg.p, cfg.q, cfg.mode, cfg.pad, floor_extent=cfg.floor_extent, is1d=cfg.is1d)
         secs += time.perf_counter() - t0
         outs += y.size
         parts.append(f"{cfg.name}: {n_img * cfg.C} of {cfg.planes} planes")
@@ -197,6 +200,13 @@ def run_reference(args):
     return 0
 
 
+def make_plan(fc, cfg):
+    ext = "floor" if cfg.floor_extent else "paper"
+    if cfg.nd:
+        return fc.Plan.nd(cfg.pd, cfg.qd, cfg.mode, cfg.pad, cfg.C, cfg.dims, cfg.dtype, ext)
+    return fc.Plan(cfg.p, cfg.q, cfg.mode, cfg.pad, cfg.C, cfg.H, cfg.W, cfg.dtype, ext, cfg.is1d)
+
+
 # --------------------------------------------------------------------------- GPU leg
 def main():
     args = parse()
@@ -224,11 +234,13 @@ def main():
     l2 = getattr(props, "L2_cache_size", 126 * 2 ** 20) or 126 * 2 ** 20
     launches = []
     for cfg in cfgs:
-        pl = fc.Plan(cfg.p, cfg.q, cfg.mode, cfg.pad, cfg.C, cfg.H, cfg.W, cfg.dtype,
-                     "floor" if cfg.floor_extent else "paper", cfg.is1d)
+        pl = make_plan(fc, cfg)
         x = synth.make_input(cfg, batch_offset=rank * cfg.N)
+        n_out = 1
+        for d in pl.out_shape(cfg.N):
+            n_out *= d
         launches.append({"cfg": cfg, "plan": pl, "x_host": x, "bytes": pl.compulsory_bytes(cfg.N),
-                         "outputs": cfg.N * cfg.C * pl.Ho * pl.Wo})
+                         "outputs": n_out})
     # input/output buffers per rotation set; several launches may share one input
     set_bytes = 0
     host_inputs = {}
@@ -244,8 +256,8 @@ def main():
     R = max(1, min(R, int(0.8 * free // set_bytes)))
     dev_inputs = {k: [v.to(dev) for _ in range(R)] for k, v in host_inputs.items()}
     for L in launches:
-        L["outs"] = [torch.empty((L["cfg"].N, L["cfg"].C, L["plan"].Ho, L["plan"].Wo), dtype=L["x_host"].dtype,
-                                 device=dev) for _ in range(R)]
+        L["outs"] = [torch.empty(L["plan"].out_shape(L["cfg"].N), dtype=L["x_host"].dtype, device=dev)
+                     for _ in range(R)]
     torch.cuda.synchronize(dev)
 
     # kernel launches of a step: nearest-gather launches of one dtype share one
@@ -376,9 +388,11 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": DTYPE_TAG[cfgs[0].dtype], "data": "synthetic",
         "config": {"workload": args.workload, "launches": [
-            {"name": L["cfg"].name, "shape": [L["cfg"].N, L["cfg"].C, L["cfg"].H, L["cfg"].W],
-             "factor": f"{L['cfg'].p}/{L['cfg'].q}", "mode": L["cfg"].mode, "pad": L["cfg"].pad,
-             "dtype": L["cfg"].dtype, "out": [L["plan"].Ho, L["plan"].Wo], "kernel": L["plan"].kernel,
+            {"name": L["cfg"].name, "shape": [L["cfg"].N, L["cfg"].C, *L["cfg"].dims],
+             "factor": (f"{L['cfg'].p}/{L['cfg'].q}" if not L["cfg"].nd else
+                        " x ".join(f"{a}/{b}" for a, b in zip(L["cfg"].pd, L["cfg"].qd))),
+             "mode": L["cfg"].mode, "pad": L["cfg"].pad,
+             "dtype": L["cfg"].dtype, "out": list(L["plan"].odims), "kernel": L["plan"].kernel,
              "compulsory_bytes_alone": L["bytes"],
              "avg_launch_us": per_group_ms[next(gi for gi, g in enumerate(groups) if i in g)] * 1e3,
              "shares_launch_with": [launches[j]["cfg"].name for g in groups if i in g for j in g if j != i]}

@@ -49,8 +49,12 @@ struct Geo {
     static constexpr int L = HI - LO + 1;                          // window rows/cols of one period
     static constexpr int C = L > Q ? L - Q : 0;                    // rows carried to the next period
     static constexpr int F = L - C;                                // fresh rows per period
+    // phase j has fraction 0: its output is the tap at offset 0, exactly (phase
+    // 0 always; every phase of an unreduced identity factor R/R, which the
+    // variant tables use for 1/1 dimensions so that a period holds R outputs)
+    static __host__ __device__ constexpr bool frac0(int j) { return (j * Q) % P == 0; }
     // window row after which output row j of the period is complete
-    static __host__ __device__ constexpr int last_row(int j) { return j == 0 ? -LO : base(j) + TAPS - 1; }
+    static __host__ __device__ constexpr int last_row(int j) { return frac0(j) ? base(j) - LO : base(j) + TAPS - 1; }
 };
 
 // Phase weights as compile-time constants (folded into the FMAs as
@@ -490,9 +494,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 // phase jx of both x-periods shares its weights: packed pairs
 #pragma unroll
                 for (int jx = 0; jx < PX; ++jx) {
-                    if (jx == 0) {  // fraction 0: the tap at offset 0, exactly
-                        h[0] = win[-LO];
-                        h[PX] = win[QX - LO];
+                    if (GX::frac0(jx)) {  // fraction 0: the tap at offset 0, exactly
+                        h[jx] = win[GX::base(jx) - LO];
+                        h[PX + jx] = win[QX + GX::base(jx) - LO];
                     } else {
                         const int bb = GX::base(jx);
                         float2 v2 = fmul2_rn(WX::w(jx, 0), make_float2(win[bb], win[QX + bb]));
@@ -509,8 +513,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
 #pragma unroll
                     for (int jx = 0; jx < PX; ++jx) {
                         float v2;
-                        if (jx == 0) {
-                            v2 = win[k * QX - LO];  // fraction 0: the tap at offset 0, exactly
+                        if (GX::frac0(jx)) {
+                            v2 = win[k * QX + GX::base(jx) - LO];  // fraction 0: the tap at offset 0, exactly
                         } else {
                             const int bb = k * QX + GX::base(jx);
                             v2 = __fmul_rn(WX::w(jx, 0), win[bb]);
@@ -576,9 +580,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                     if (my < b.my_lo || my >= b.my_hi) return;
                 }
                 float o[KP];
-                if (jy == 0) {
+                if (GY::frac0(jy)) {  // fraction 0: the tap row at offset 0, exactly
 #pragma unroll
-                    for (int c = 0; c < KP; ++c) o[c] = hr[(RO - LO) % TAPS][c];
+                    for (int c = 0; c < KP; ++c) o[c] = hr[(RO + GY::base(jy) - LO) % TAPS][c];
                 } else {
                     const int bb = GY::base(jy);
                     constexpr int H2 = KP / 2;  // columns c and c + H2 share the row weights
@@ -705,10 +709,12 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     if (span_e == 0) bulk_wait0();
 }
 
-// periods per thread chunk: 2 for 16-bit data with odd q (odd word stride), else 1
-template <typename T, int Q>
+// x-periods per thread chunk: 2 for 16-bit data with odd q (odd word stride,
+// static window parity) and for narrow periods (p <= 3, even q: a thread then
+// owns 2p >= 4 columns and the horizontal taps pair up), else 1
+template <typename T, int PX, int QX>
 constexpr int fused_k() {
-    return (sizeof(T) == 2 && (Q % 2) == 1) ? 2 : 1;
+    return ((sizeof(T) == 2 && (QX % 2) == 1) || (PX <= 3 && (QX % 2) == 0 && PX != QX)) ? 2 : 1;
 }
 
 }  // namespace fcfs

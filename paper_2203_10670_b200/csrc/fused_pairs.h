@@ -13,9 +13,9 @@
     Y(7, 5) Y(5, 7) Y(4, 7) Y(7, 4) Y(5, 2) Y(2, 5)
 // isotropic p/q in both dimensions
 #define FCFS_ISO_X(X) FCFS_ISO_PAIRS(X##_ISO)
-// columns only (rows 1/1: 1D rows and width-only resizes)
+// columns only (rows 1/1, as the unreduced 4/4: 1D rows and width-only resizes)
 #define FCFS_W_X(X) FCFS_NONUNIT_PAIRS(X##_W)
-// rows only (columns 1/1)
+// rows only (columns 1/1, as the unreduced 8/8)
 #define FCFS_H_X(X) FCFS_NONUNIT_PAIRS(X##_H)
 // 3D volumes: isotropic rows/columns, any slice factor (run-time slice weights)
 #define FCFS_Z_PAIRS(Y) \

@@ -15,6 +15,11 @@ extern const FusedVariant kFusedVariants_f16_iso[], kFusedVariants_f16_w[], kFus
 extern const FusedVariant kFusedVariants_bf16_iso[], kFusedVariants_bf16_w[], kFusedVariants_bf16_h[],
     kFusedVariants_bf16_z[];
 
+// A variant's factor serves a plan's reduced factor p/q when they are equal, or
+// when p/q = 1/1 and the variant uses an unreduced identity R/R (R outputs per
+// period; every phase has fraction 0 and is an exact copy, as in the plan).
+static bool dim_match(int vp, int vq, int p, int q) { return (vp == p && vq == q) || (p == 1 && q == 1 && vp == vq); }
+
 // slices: a 3D plan whose slice factor is not 1/1 (variants combining slice taps)
 const FusedVariant *fused_lookup(int dtype, int py, int qy, int px, int qx, int ntaps, bool slices) {
     const FusedVariant *sets[3][4] = {
@@ -24,7 +29,7 @@ const FusedVariant *fused_lookup(int dtype, int py, int qy, int px, int qx, int 
     if (dtype < 0 || dtype > 2) return nullptr;
     for (const FusedVariant *tab : sets[dtype])
         for (const FusedVariant *v = tab; v->fn; ++v)
-            if (v->PY == py && v->QY == qy && v->PX == px && v->QX == qx && v->TAPS == ntaps &&
+            if (dim_match(v->PY, v->QY, py, qy) && dim_match(v->PX, v->QX, px, qx) && v->TAPS == ntaps &&
                 (v->TZ > 1) == slices)
                 return v;
     return nullptr;

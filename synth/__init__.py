@@ -99,10 +99,24 @@ class Config:
     floor_extent: bool = True
     is1d: bool = False
     seed: int = SEED_BASE
+    D: int = 1                       # slices (3D volumes); the tensor is N x C x D x H x W
+    pd: tuple | None = None          # per-dimension factors (outermost first): an ND plan (§4.2)
+    qd: tuple | None = None
 
     @property
     def planes(self) -> int:
         return self.N * self.C
+
+    @property
+    def nd(self) -> bool:
+        return self.pd is not None
+
+    @property
+    def dims(self) -> tuple:
+        """spatial dims of the input tensor (after N, C)"""
+        if not self.nd:
+            return (self.H, self.W)
+        return ((self.D,) if len(self.pd) == 3 else ()) + ((self.H,) if len(self.pd) >= 2 else ()) + (self.W,)
 
 
 # BASELINE.json "configs" (index 0..4); a config with two factors is two launches.
@@ -120,6 +134,18 @@ CONFIGS = {
     "C5": Config("C5", 1, 1, 32768, 32768, "float32", "field", 3, 5, "bicubic", "replicate", seed=SEED_BASE + 5),
 }
 
+# Per-dimension factors and 3D volumes (not BASELINE.json
+# configs): a 16:9 -> 4:3 width-only resize of config 4's frames, a trilinear
+# 3/2 volume and a bicubic 5/3 bf16 feature volume.
+CONFIGS.update({
+    "A1": Config("A1", 8, 3, 2160, 3840, "float16", "uniform_f16grid", 3, 4, "bilinear", "replicate",
+                 seed=SEED_BASE + 21, pd=(1, 3), qd=(1, 4)),
+    "V1": Config("V1", 4, 1, 256, 256, "float32", "uniform", 3, 2, "bilinear", "replicate", seed=SEED_BASE + 22,
+                 D=128, pd=(3, 3, 3), qd=(2, 2, 2)),
+    "V2": Config("V2", 2, 8, 128, 128, "bfloat16", "normal", 5, 3, "bicubic", "reflect", seed=SEED_BASE + 23,
+                 D=64, pd=(5, 5, 5), qd=(3, 3, 3)),
+})
+
 # bench workloads: a step = one pass over one batch, every launch of the config
 WORKLOADS = {
     "C1": ["C1a", "C1b"],
@@ -127,6 +153,9 @@ WORKLOADS = {
     "C3": ["C3"],
     "C4": ["C4a", "C4b"],
     "C5": ["C5"],
+    "A1": ["A1"],
+    "V1": ["V1"],
+    "V2": ["V2"],
 }
 
 
@@ -142,10 +171,11 @@ def make_values(cfg: Config, n0: int = 0, n1: int | None = None, rows: tuple[int
         assert cfg.N == 1 and cfg.C == 1
         return field_f32(cfg.seed + batch_offset, cfg.H, cfg.W, r0, r1).reshape(1, 1, r1 - r0, cfg.W)
     gen = {"uniform": uniform_f32, "uniform_f16grid": uniform_f16grid, "normal": normal_f32}[cfg.values]
-    plane = cfg.H * cfg.W
+    plane = cfg.D * cfg.H * cfg.W
     if (r0, r1) == (0, cfg.H):  # contiguous global index range
         off = (batch_offset + n0) * cfg.C * plane
-        return gen(cfg.seed, nb * cfg.C * plane, off).reshape(nb, cfg.C, cfg.H, cfg.W)
+        return gen(cfg.seed, nb * cfg.C * plane, off).reshape((nb, cfg.C) + cfg.dims)
+    assert cfg.D == 1
     out = np.empty((nb, cfg.C, r1 - r0, cfg.W), np.float32)
     for b in range(nb):
         for c in range(cfg.C):
