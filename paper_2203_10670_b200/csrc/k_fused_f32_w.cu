@@ -2,7 +2,7 @@
 #include "fused_inst.cuh"
 
 #define V_ISO(P, Q) FCFS_BOTH_MODES(float, P, Q, P, Q)
-#define V_W(P, Q) FCFS_BOTH_MODES(float, 4, 4, P, Q)
+#define V_W(P, Q) FCFS_BOTH_MODES(float, 8, 8, P, Q)
 #define V_H(P, Q) FCFS_BOTH_MODES(float, P, Q, 8, 8)
 #define V_Z(P, Q) FCFS_BOTH_MODES_Z(float, P, Q, P, Q)
 namespace fcfs {

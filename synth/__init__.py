@@ -135,11 +135,14 @@ CONFIGS = {
 }
 
 # Per-dimension factors and 3D volumes (not BASELINE.json
-# configs): a 16:9 -> 4:3 width-only resize of config 4's frames, a trilinear
+# configs): a 16:9 -> 4:3 width-only resize of config 4's frames (A1), a
+# height-only bicubic 5/3 stretch of the same frames (A2), a trilinear
 # 3/2 volume and a bicubic 5/3 bf16 feature volume.
 CONFIGS.update({
     "A1": Config("A1", 8, 3, 2160, 3840, "float16", "uniform_f16grid", 3, 4, "bilinear", "replicate",
                  seed=SEED_BASE + 21, pd=(1, 3), qd=(1, 4)),
+    "A2": Config("A2", 8, 3, 2160, 3840, "float16", "uniform_f16grid", 5, 3, "bicubic", "replicate",
+                 seed=SEED_BASE + 24, pd=(5, 1), qd=(3, 1)),
     "V1": Config("V1", 4, 1, 256, 256, "float32", "uniform", 3, 2, "bilinear", "replicate", seed=SEED_BASE + 22,
                  D=128, pd=(3, 3, 3), qd=(2, 2, 2)),
     "V2": Config("V2", 2, 8, 128, 128, "bfloat16", "normal", 5, 3, "bicubic", "reflect", seed=SEED_BASE + 23,
@@ -154,6 +157,7 @@ WORKLOADS = {
     "C4": ["C4a", "C4b"],
     "C5": ["C5"],
     "A1": ["A1"],
+    "A2": ["A2"],
     "V1": ["V1"],
     "V2": ["V2"],
 }

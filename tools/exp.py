@@ -21,11 +21,14 @@ def time_cfg(name, reps, env):
         del os.environ[k]
     os.environ.update(env)
     c = synth.CONFIGS[name]
-    pl = fc.Plan(c.p, c.q, c.mode, c.pad, c.C, c.H, c.W, c.dtype, "floor", c.is1d)
+    if c.nd:
+        pl = fc.Plan.nd(c.pd, c.qd, c.mode, c.pad, c.C, c.dims, c.dtype, "floor")
+    else:
+        pl = fc.Plan(c.p, c.q, c.mode, c.pad, c.C, c.H, c.W, c.dtype, "floor", c.is1d)
     x = synth.make_input(c).cuda()
     R = max(2, min(8, int(4 * 126e6 // (x.numel() * x.element_size() * 2)) + 1))
     xs = [x.clone() for _ in range(R)]
-    ys = [torch.empty((c.N, c.C, pl.Ho, pl.Wo), dtype=x.dtype, device="cuda") for _ in range(R)]
+    ys = [torch.empty(pl.out_shape(c.N), dtype=x.dtype, device="cuda") for _ in range(R)]
     for i in range(3):
         pl.run(xs[i % R], out=ys[i % R])
     torch.cuda.synchronize()
