@@ -202,7 +202,7 @@ typedef struct {
     int64_t C, H, W, Ho, Wo;
     int ntaps;              /* taps per dimension: 1, 2 or 4 */
     int lo;                 /* first tap offset relative to floor(m*q/p): 0 or -1 */
-    int kernel;             /* variant fcfs_run uses: 0 reference, 1 nearest gather, 2 fused separable */
+    int kernel;             /* variant fcfs_run uses: 0 reference, 1 nearest gather, 2 fused separable, 3 tiled */
     int device;             /* CUDA device recorded at plan time, -1 if none */
     int64_t in_rows_referenced; /* input rows (of D x H) some kept output's tap reads with a nonzero weight */
     int rank;               /* spatial rank (1 for FCFS_FLAG_1D plans) */

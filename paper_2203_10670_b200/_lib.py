@@ -68,7 +68,7 @@ FLAG_EXTENT_FLOOR = 1 << 1
 FLAG_FORCE_REFERENCE = 1 << 8
 STATUS = {0: "FCFS_OK", 1: "FCFS_E_ARG", 2: "FCFS_E_SHAPE", 3: "FCFS_E_PAD", 4: "FCFS_E_UNSUPPORTED",
           5: "FCFS_E_DEVICE", 6: "FCFS_E_CUDA", 7: "FCFS_E_NOMEM"}
-KERNELS = {0: "reference", 1: "nearest_gather", 2: "fused_separable"}
+KERNELS = {0: "reference", 1: "nearest_gather", 2: "fused_separable", 3: "tiled"}
 
 
 class FcfsError(RuntimeError):

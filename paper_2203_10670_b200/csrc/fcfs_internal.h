@@ -42,6 +42,14 @@ struct RefArgs {         // reference kernel: one thread per output
     int is1d;
 };
 
+struct TileArgs {        // tiled kernel (k_tile.cu): output tiles with a shared-memory window
+    RunGeom g;
+    PhaseTable tx, ty;
+    int pad, is1d;
+    int TH, TW;          // output tile rows / columns
+    int xs_cap;          // floats reserved for the input window (hidden buffer follows)
+};
+
 // 32-bit division by a run-time invariant divisor (n < 2^31).
 struct FastDiv {
     uint32_t d, m, s;
@@ -119,6 +127,7 @@ struct NearestBatch {
 int launch_reference(int dtype, const RefArgs &a, void *stream);
 int launch_nearest(int dtype, const NearestArgs &a, void *stream);
 int launch_nearest_batch(int dtype, const NearestBatch &nb, void *stream);
+int launch_tile(int dtype, const TileArgs &a, int grid, int smem, void *stream);
 
 // Fused: the variant table.  fused_lookup returns an opaque kernel handle or
 // nullptr when (dtype, py/qy, px/qx, ntaps) has no compiled instantiation; K

@@ -27,7 +27,7 @@ struct fcfs_plan_s {
     int64_t C, D, H, W, Do, Ho, Wo;
     int is1d;                 // rows are independent 1D signals (FCFS_FLAG_1D, rank 1)
     PhaseTable tab, taby, tabz;  // per-dimension phase tables: W, H, D
-    int kernel;  // 0 reference, 1 nearest, 2 fused
+    int kernel;  // 0 reference, 1 nearest, 2 fused, 3 tiled
     const FusedVariant *fused;
     int device;
     int64_t rows_ref;
@@ -326,7 +326,9 @@ fcfs_status check_device(const fcfs_plan_s *pl) {
     return FCFS_OK;
 }
 
-// The kernel a run uses (0 reference, 1 nearest gather, 2 fused) after the
+bool plan_tile(const fcfs_plan_s *pl, const RunGeom &g0, TileArgs &a, int &grid, int &smem, char *desc, int dlen);
+
+// The kernel a run uses (0 reference, 1 nearest gather, 2 fused, 3 tiled) after the
 // run-time checks: 32-bit index ranges (gather), 16-B-aligned input and a
 // feasible shared-memory geometry (fused).  Fills L for the fused kernel.
 int select_kernel(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
@@ -346,7 +348,12 @@ int select_kernel(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
         }
         if ((reinterpret_cast<uintptr_t>(g.in) & 15) ||
             g2.planes * std::max(g2.D, g2.Do) * std::max(g.in_nrows * pl->W, g.out_nrows * pl->Wo) > INT32_MAX * 16LL || !plan_fused(pl, g2, L))
-            kernel = 0;
+            kernel = (pl->pz == 1 && pl->qz == 1) ? 3 : 0;  // tiled when the slice factor allows it
+    }
+    if (kernel == 3) {
+        TileArgs ta;
+        int grid, smem;
+        if (!plan_tile(pl, g, ta, grid, smem, L.desc, sizeof(L.desc))) kernel = 0;
     }
     if (kernel == 1) {
         const int64_t rows = g.planes * g.Do * g.out_nrows;
@@ -362,12 +369,62 @@ int select_kernel(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     return kernel;
 }
 
+// Tiled-kernel geometry: the largest output tile (TH x TW) whose input window
+// and hidden buffer fit 48 KB of shared memory (4 CTAs per SM).
+bool plan_tile(const fcfs_plan_s *pl, const RunGeom &g0, TileArgs &a, int &grid, int &smem, char *desc, int dlen) {
+    RunGeom g = g0;
+    if (g.D > 1) {  // slices with a 1/1 factor: independent planes
+        g.planes *= g.D;
+        g.D = g.Do = 1;
+        g.in_plane_stride = g.in_nrows * g.W;
+        g.out_plane_stride = g.out_nrows * g.Wo;
+    }
+    a.g = g;
+    a.tx = pl->tab;
+    a.ty = pl->taby;
+    a.pad = pl->pad;
+    a.is1d = pl->is1d;
+    const int T = pl->tab.ntaps;
+    auto span = [&](int n, int p, int q) { return (int)(((int64_t)(n - 1) * q + p - 1) / p + q + T + 1); };
+    const int budget = 48 * 1024 / 4;  // floats
+    int bestTH = 0, bestTW = 0, bestNR = 0, bestNC = 0;
+    for (int TW : {256, 128, 64, 32, 16, 8, 4, 2, 1}) {
+        for (int TH : {64, 32, 16, 8, 4, 2, 1}) {
+            const int NR = pl->is1d ? TH : span(TH, pl->py, pl->qy);
+            const int NC = span(TW, pl->p, pl->q);
+            if ((int64_t)NR * NC + (int64_t)NR * TW > budget) continue;
+            const int TWe = (int)std::min<int64_t>(TW, g.Wo), THe = (int)std::min<int64_t>(TH, g.out_nrows);
+            if ((int64_t)THe * TWe > (int64_t)bestTH * bestTW || ((int64_t)THe * TWe == (int64_t)bestTH * bestTW && TW > bestTW)) {
+                bestTH = THe;
+                bestTW = TWe;
+                bestNR = NR;
+                bestNC = NC;
+            }
+        }
+    }
+    if (bestTH == 0) return false;
+    a.TH = bestTH;
+    a.TW = bestTW;
+    a.xs_cap = (bestNR * bestNC + 3) / 4 * 4;
+    smem = (a.xs_cap + bestNR * bestTW) * 4;
+    const int64_t ntiles = g.planes * ((g.out_nrows + a.TH - 1) / a.TH) * ((g.Wo + a.TW - 1) / a.TW);
+    grid = (int)std::min<int64_t>(ntiles, (int64_t)pl->sm_count * 4);
+    if (desc)
+        std::snprintf(desc, (size_t)dlen,
+                      "{\"kernel\": \"tiled\", \"TH\": %d, \"TW\": %d, \"window\": [%d, %d], \"tiles\": %lld, "
+                      "\"grid\": %d, \"block\": 256, \"smem\": %d}",
+                      a.TH, a.TW, bestNR, bestNC, (long long)ntiles, grid, smem);
+    return true;
+}
+
 // A validated launch: which kernel, with what arguments.
 struct Prepared {
     fcfs_plan_t pl;
     int kernel;  // -1: nothing to do
     NearestArgs na;
     RefArgs ra;
+    TileArgs ta;
+    int tgrid, tsmem;
     FusedLaunch L;
     const void *in;
     void *out;
@@ -434,6 +491,8 @@ fcfs_status prepare(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t in_
         a.pad = pl->pad;
         a.is1d = pl->is1d;
         a.vec_ok = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    } else if (pr.kernel == 3) {
+        plan_tile(pl, g, pr.ta, pr.tgrid, pr.tsmem, nullptr, 0);
     } else if (pr.kernel == 0) {
         RefArgs &a = pr.ra;
         a.g = g;
@@ -450,6 +509,7 @@ fcfs_status launch(const Prepared &pr, void *stream) {
     int rc = 0;
     if (pr.kernel == 1) rc = launch_nearest(pr.pl->dtype, pr.na, stream);
     else if (pr.kernel == 2) rc = launch_fused(pr.pl->fused, pr.L.a, pr.L.grid, kFusedThreads, pr.L.smem, stream);
+    else if (pr.kernel == 3) rc = launch_tile(pr.pl->dtype, pr.ta, pr.tgrid, pr.tsmem, stream);
     else if (pr.kernel == 0) rc = launch_reference(pr.pl->dtype, pr.ra, stream);
     return rc == 0 ? FCFS_OK : FCFS_E_CUDA;
 }
@@ -558,6 +618,9 @@ fcfs_status make_plan(int rank, const int *pd, const int *qd, int mode, int pad,
                         pl->fused = nullptr;
             if (pl->fused) pl->kernel = 2;
         }
+        // separable plans without a fused variant: the tiled kernel (2D planes;
+        // 3D with a 1/1 slice factor as N*C*D planes)
+        if (pl->kernel == 0 && mode != FCFS_NEAREST && pl->pz == 1 && pl->qz == 1) pl->kernel = 3;
     }
     pl->rows_ref = rows_referenced(pl);
     int dev = -1;

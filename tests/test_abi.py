@@ -130,15 +130,15 @@ def test_phase_table_matches_oracle_weights(fc, mode, p, q):
 def test_kernel_selection(fc):
     assert fc.Plan(5, 3, "bicubic", "reflect", 1, 128, 128, "bfloat16").kernel == "fused_separable"
     assert fc.Plan(2, 3, "nearest", "zero", 1, 512, 512).kernel == "nearest_gather"
-    assert fc.Plan(27, 11, "bicubic", "replicate", 1, 64, 64).kernel == "reference"  # no fused variant
-    assert fc.Plan(3, 2, "bilinear", "replicate", 1, 64, 101).kernel == "reference"  # row pitch not 16-B
+    assert fc.Plan(27, 11, "bicubic", "replicate", 1, 64, 64).kernel == "tiled"  # no fused variant
+    assert fc.Plan(3, 2, "bilinear", "replicate", 1, 64, 101).kernel == "tiled"  # row pitch not 16-B
     # 1D rows run the fused kernel with a 1/1 row factor (the "width-only" variants)
     assert fc.Plan(3, 2, "bilinear", "replicate", 1, 64, 64, is1d=True).kernel == "fused_separable"
     assert fc.Plan(3, 2, "bilinear", "replicate", 1, 64, 64, force_reference=True).kernel == "reference"
     # per-dimension factors (§4.2)
     assert fc.Plan.nd((1, 3), (1, 4), "bicubic", "reflect", 3, (64, 64), "float16").kernel == "fused_separable"
     assert fc.Plan.nd((5, 1), (3, 1), "bilinear", "zero", 3, (64, 64), "bfloat16").kernel == "fused_separable"
-    assert fc.Plan.nd((5, 3), (3, 4), "bilinear", "zero", 3, (64, 64)).kernel == "reference"  # no variant
+    assert fc.Plan.nd((5, 3), (3, 4), "bilinear", "zero", 3, (64, 64)).kernel == "tiled"  # no variant
     assert fc.Plan.nd((2, 3, 5), (1, 2, 3), "nearest", "zero", 1, (8, 16, 16)).kernel == "nearest_gather"
     assert fc.Plan.nd((2, 3, 3), (1, 2, 2), "bicubic", "zero", 1, (8, 16, 16)).kernel == "fused_separable"
     assert fc.Plan.nd((7, 5, 5), (3, 3, 3), "bilinear", "zero", 1, (8, 16, 16)).kernel == "fused_separable"

@@ -303,3 +303,22 @@ def test_streams_and_concurrency():
         b = pl.run(x)
     torch.cuda.synchronize()
     assert torch.equal(a, ref) and torch.equal(b, ref)
+
+
+@pytest.mark.parametrize("mode", ["bilinear", "bicubic"])
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_tiled_kernel_paper_factors(mode, dtype):
+    """Factors without a fused variant (the paper's §6 factors 2/11 and 27/11,
+    PAPER.md:289-300, and others) run the tiled kernel: many tiles with ragged
+    edges, bitwise equal to the reference kernel and within the bar of the oracle."""
+    for i, (p, q) in enumerate([(2, 11), (27, 11), (9, 7), (1, 6), (11, 4), (13, 10)]):
+        pad = ["zero", "replicate", "reflect"][i % 3]
+        x = _rand_input(2000 + i, (1, 2, 157, 229), dtype)
+        pl = Plan(p, q, mode, pad, 2, 157, 229, dtype, "floor")
+        assert pl.kernel == "tiled"
+        y = pl.run(x.to(DEV))
+        yr = Plan(p, q, mode, pad, 2, 157, 229, dtype, "floor", force_reference=True).run(x.to(DEV))
+        assert torch.equal(y.cpu().view(torch.uint8), yr.cpu().view(torch.uint8)), f"{p}/{q} {mode} {pad} kernels"
+        xr = oracle_input(x)
+        ref = oracle.staged(xr, p, q, mode, pad, floor_extent=True)
+        compare(y, ref, dtype, mode, float(xr.max() - xr.min()), f"tiled {p}/{q} {mode} {pad} {dtype}")
