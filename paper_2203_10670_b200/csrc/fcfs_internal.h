@@ -47,7 +47,9 @@ struct TileArgs {        // tiled kernel (k_tile.cu): output tiles with a shared
     PhaseTable tx, ty;
     int pad, is1d;
     int TH, TW;          // output tile rows / columns
-    int xs_cap;          // floats reserved for the input window (hidden buffer follows)
+    int row_slots;       // window rows: 1 = one slot per (output row, tap), 0 = the contiguous range
+    int nr_cap, nc_cap;  // window rows / columns reserved (row pitch of the window = nc_cap)
+    int xs_cap;          // floats reserved for the window (= nr_cap * nc_cap)
 };
 
 // 32-bit division by a run-time invariant divisor (n < 2^31).

@@ -709,12 +709,19 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     if (span_e == 0) bulk_wait0();
 }
 
-// x-periods per thread chunk: 2 for 16-bit data with odd q (odd word stride,
-// static window parity) and for narrow periods (p <= 3, even q: a thread then
-// owns 2p >= 4 columns and the horizontal taps pair up), else 1
+// x-periods per thread chunk (K outputs-periods of PX columns), a measured
+// table (tools/paper_sweep.py, tools/exp.py): 16-bit data with odd q needs an
+// even K (odd word stride: conflict-free shared loads, static window parity);
+// otherwise narrow periods take several periods so that a thread owns ~8
+// columns, and wide ones stay at 1 where a larger register ring costs more than
+// it saves (7/4 bicubic, 4/7).
 template <typename T, int PX, int QX>
 constexpr int fused_k() {
-    return ((sizeof(T) == 2 && (QX % 2) == 1) || (PX <= 3 && (QX % 2) == 0 && PX != QX)) ? 2 : 1;
+    if (sizeof(T) == 2 && (QX % 2) == 1) return 2;
+    if (PX == 1) return QX <= 2 ? 8 : 2;
+    if (PX == 2) return 4;
+    if (PX == 3) return (sizeof(T) == 2 || QX <= 2) ? 2 : 3;
+    return QX <= 3 ? 2 : 1;
 }
 
 }  // namespace fcfs

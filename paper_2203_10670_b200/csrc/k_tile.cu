@@ -2,93 +2,142 @@
 // per-dimension p, q <= 64: e.g. the paper's §6 factors 2/11 and 27/11,
 // PAPER.md:289-300), 2D planes (3D with a 1/1 slice factor as planes).
 //
-// A CTA takes output tiles (TH rows x TW columns of one plane) in a persistent
-// loop.  Per tile:
-//   1. the input window the tile's taps reach (virtual rows r_lo..r_hi,
-//      columns c_lo..c_hi, padding applied at the global border) is read
-//      coalesced into shared memory as fp32;
+// A CTA (8 warps) takes output tiles (TH rows x TW columns of one plane) in a
+// persistent loop.  Per tile:
+//   0. per output column: phase j_x and window column of its base tap; per
+//      output row: phase j_y and the window row of its first tap;
+//   1. the input rows the tile's taps reach, restricted to the tile's column
+//      window, are read coalesced into shared memory as fp32 (padding applied
+//      at the global border).  Window rows are either the contiguous virtual
+//      row range (up-scaling: neighbouring output rows share rows) or one slot
+//      per (output row, tap) (strong down-scaling: rows no tap reaches are
+//      never read -- e.g. 2/11 reads 4 of every 11 rows);
 //   2. the horizontal pass of every window row for the tile's output columns
-//      goes to a second shared buffer (the p-phase hidden values of §3.1.1
-//      for those columns, never in HBM);
+//      goes to a second shared buffer (the hidden values of §3.1.1 for those
+//      columns, never in HBM);
 //   3. the vertical pass writes the outputs, coalesced along the row.
-// Phase weights come from the plan's run-time tables.  The arithmetic is the
-// reference kernel's operation sequence (k_reference.cu: fraction-0 phases
-// copy, else __fmul_rn then __fmaf_rn in tap order, x then y), so the two
-// agree bit for bit.
+// Warps own rows and lanes columns (no integer division in the loops); the
+// phase weights sit in shared memory (lanes index them by their own phase).
+// The arithmetic is the reference kernel's operation sequence (k_reference.cu:
+// fraction-0 phases copy, else __fmul_rn then __fmaf_rn in tap order, x then
+// y), so the two agree bit for bit.
 #include "device_common.cuh"
 
 namespace fcfs {
 
+constexpr int kTileWarps = 8;
+
 template <typename T>
-__global__ void __launch_bounds__(256) fcfs_tile_kernel(const __grid_constant__ TileArgs a) {
+__global__ void __launch_bounds__(32 * kTileWarps) fcfs_tile_kernel(const __grid_constant__ TileArgs a) {
     extern __shared__ __align__(16) float tsm[];
     const RunGeom &g = a.g;
     const PhaseTable &tx = a.tx, &ty = a.ty;
-    const int T_ = tx.ntaps, lo = tx.lo;  // same mode in both dimensions
-    const int64_t tiles_y = (g.out_nrows + a.TH - 1) / a.TH, tiles_x = (g.Wo + a.TW - 1) / a.TW;
+    const int T_ = tx.ntaps, lo = tx.lo;  // one mode for both dimensions
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // shared layout: weights, per-column and per-row info, window, hidden
+    float *wx = tsm;                               // [px][4]
+    float *wy = wx + 4 * kPMax;                    // [py][4]
+    int *colj = reinterpret_cast<int *>(wy + 4 * kPMax);  // [TW] phase (bit 31: fraction 0)
+    int *colb = colj + a.TW;                       // [TW] window column of the base tap
+    int *rowj = colb + a.TW;                       // [TH] phase (bit 31: fraction 0)
+    int *rowb = rowj + a.TH;                       // [TH] window row of the first tap
+    int *rsrc = rowb + a.TH;                       // [NRcap] source row of window row (-1: zero)
+    float *xs = reinterpret_cast<float *>(rsrc + a.nr_cap);  // [NRcap][NCcap]
+    float *hs = xs + a.xs_cap;                     // [NRcap][TW]
+    for (int i = threadIdx.x; i < 4 * kPMax; i += blockDim.x) {
+        wx[i] = tx.w[i >> 2][i & 3];
+        wy[i] = ty.w[i >> 2][i & 3];
+    }
+    const int tiles_y = (int)((g.out_nrows + a.TH - 1) / a.TH), tiles_x = (int)((g.Wo + a.TW - 1) / a.TW);
     const int64_t ntiles = g.planes * tiles_y * tiles_x;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t tx_i = tile % tiles_x;
+        const int tx_i = (int)(tile % tiles_x);
         const int64_t rest = tile / tiles_x;
-        const int64_t ty_i = rest % tiles_y, plane = rest / tiles_y;
-        const int64_t my0 = g.out_row0 + ty_i * a.TH, my1 = min(my0 + a.TH, g.out_row0 + g.out_nrows);
-        const int64_t mx0 = tx_i * a.TW, mx1 = min(mx0 + (int64_t)a.TW, g.Wo);
-        // window (virtual indices) the tile's taps reach
-        const int64_t r_lo = a.is1d ? my0 : (my0 / ty.p) * ty.q + ty.base[my0 % ty.p] + lo;
-        const int64_t r_hi = a.is1d ? my1 - 1 : ((my1 - 1) / ty.p) * ty.q + ty.base[(my1 - 1) % ty.p] + lo + T_ - 1;
-        const int64_t c_lo = (mx0 / tx.p) * tx.q + tx.base[mx0 % tx.p] + lo;
-        const int64_t c_hi = ((mx1 - 1) / tx.p) * tx.q + tx.base[(mx1 - 1) % tx.p] + lo + T_ - 1;
-        const int NR = (int)(r_hi - r_lo + 1), NC = (int)(c_hi - c_lo + 1), NW = (int)(mx1 - mx0);
-        float *xs = tsm;                    // [NR][NC] input window (fp32)
-        float *hs = tsm + a.xs_cap;         // [NR][NW] horizontal pass
+        const int ty_i = (int)(rest % tiles_y);
+        const int64_t plane = rest / tiles_y;
+        const int my0 = (int)g.out_row0 + ty_i * a.TH, my1 = min(my0 + a.TH, (int)(g.out_row0 + g.out_nrows));
+        const int mx0 = tx_i * a.TW, mx1 = min(mx0 + a.TW, (int)g.Wo);
+        const int NH = my1 - my0, NW = mx1 - mx0;
+        const int c_lo = (mx0 / tx.p) * tx.q + tx.base[mx0 % tx.p] + lo;
+        const int c_hi = ((mx1 - 1) / tx.p) * tx.q + tx.base[(mx1 - 1) % tx.p] + lo + T_ - 1;
+        const int NC = c_hi - c_lo + 1;
+        // window rows: contiguous [r_lo, ...] or one slot per (output row, tap)
+        const int r_lo = a.is1d ? my0 : (my0 / ty.p) * ty.q + ty.base[my0 % ty.p] + lo;
+        const int r_hi = a.is1d ? my1 - 1 : ((my1 - 1) / ty.p) * ty.q + ty.base[(my1 - 1) % ty.p] + lo + T_ - 1;
+        const bool slots = a.row_slots && !a.is1d;
+        const int NR = slots ? NH * T_ : r_hi - r_lo + 1;
+        __syncthreads();  // the previous tile's readers are done with every buffer
+        for (int k = threadIdx.x; k < NW; k += blockDim.x) {
+            const int m = mx0 + k, j = m % tx.p;
+            colj[k] = j | (((j * tx.q) % tx.p == 0 || T_ == 1) ? (int)0x80000000 : 0);
+            colb[k] = (m / tx.p) * tx.q + tx.base[j] - c_lo;
+        }
+        for (int rr = threadIdx.x; rr < NH; rr += blockDim.x) {
+            const int m = my0 + rr;
+            if (a.is1d) {
+                rowj[rr] = (int)0x80000000;
+                rowb[rr] = rr;  // copy of window row rr (lo taps absent)
+            } else {
+                const int j = m % ty.p, b = (m / ty.p) * ty.q + ty.base[j];  // virtual base row
+                rowj[rr] = j | (((j * ty.q) % ty.p == 0 || T_ == 1) ? (int)0x80000000 : 0);
+                rowb[rr] = slots ? rr * T_ : b + lo - r_lo;  // window row of tap 0 (the copy is tap -lo)
+                if (slots)
+                    for (int t = 0; t < T_; ++t) {
+                        const int v = b + lo + t;
+                        rsrc[rr * T_ + t] = pad_src32(v, (int)g.H, a.pad);
+                    }
+            }
+        }
+        if (!slots)
+            for (int i = threadIdx.x; i < NR; i += blockDim.x)
+                rsrc[i] = a.is1d ? r_lo + i : pad_src32(r_lo + i, (int)g.H, a.pad);
+        __syncthreads();
+        // 1. window (fp32), padding applied
         const T *src = static_cast<const T *>(g.in) + plane * g.in_plane_stride;
-        __syncthreads();  // previous tile's readers are done
-        // 1. window, padding applied (zero padding -> 0)
-        for (int i = threadIdx.x; i < NR * NC; i += blockDim.x) {
-            const int r = i / NC, c = i - r * NC;
-            const int64_t rs = a.is1d ? r_lo + r : pad_src(r_lo + r, g.H, a.pad);
-            const int64_t cs = pad_src(c_lo + c, g.W, a.pad);
-            float v = 0.0f;
-            if (rs >= 0 && cs >= 0) v = DT<T>::to_f(src[(rs - g.in_row0) * g.W + cs]);
-            xs[i] = v;
+        for (int i = warp; i < NR; i += kTileWarps) {
+            const int rs = rsrc[i];
+            const T *row = src + (int64_t)(rs - (int)g.in_row0) * g.W;
+            float *xr = xs + i * a.nc_cap;
+            for (int c = lane; c < NC; c += 32) {
+                const int cs = pad_src32(c_lo + c, (int)g.W, a.pad);
+                xr[c] = (rs >= 0 && cs >= 0) ? DT<T>::to_f(row[cs]) : 0.0f;
+            }
         }
         __syncthreads();
-        // 2. horizontal pass: window row r, output column m
-        for (int i = threadIdx.x; i < NR * NW; i += blockDim.x) {
-            const int r = i / NW, k = i - r * NW;
-            const int64_t m = mx0 + k;
-            const int jx = (int)(m % tx.p);
-            const int bx = (int)((m / tx.p) * tx.q + tx.base[jx] - c_lo);  // window column of the base tap
-            const float *row = xs + r * NC;
-            float v;
-            if ((jx * tx.q) % tx.p == 0 || T_ == 1) {
-                v = row[bx];
-            } else {
-                v = __fmul_rn(tx.w[jx][0], row[bx + lo]);
-                for (int t = 1; t < T_; ++t) v = __fmaf_rn(tx.w[jx][t], row[bx + lo + t], v);
+        // 2. horizontal pass
+        for (int i = warp; i < NR; i += kTileWarps) {
+            const float *xr = xs + i * a.nc_cap;
+            float *hr = hs + i * a.TW;
+            for (int k = lane; k < NW; k += 32) {
+                const int cj = colj[k], b = colb[k];
+                float v;
+                if (cj < 0) {
+                    v = xr[b];
+                } else {
+                    const float *w = wx + 4 * cj;
+                    v = __fmul_rn(w[0], xr[b + lo]);
+                    for (int t = 1; t < T_; ++t) v = __fmaf_rn(w[t], xr[b + lo + t], v);
+                }
+                hr[k] = v;
             }
-            hs[i] = v;
         }
         __syncthreads();
         // 3. vertical pass -> outputs
         T *dst = static_cast<T *>(g.out) + plane * g.out_plane_stride;
-        for (int i = threadIdx.x; i < (int)(my1 - my0) * NW; i += blockDim.x) {
-            const int rr = i / NW, k = i - rr * NW;
-            const int64_t my = my0 + rr;
-            float v;
-            if (a.is1d) {
-                v = hs[(int)(my - r_lo) * NW + k];
-            } else {
-                const int jy = (int)(my % ty.p);
-                const int by = (int)((my / ty.p) * ty.q + ty.base[jy] - r_lo);  // window row of the base tap
-                if ((jy * ty.q) % ty.p == 0 || T_ == 1) {
-                    v = hs[by * NW + k];
+        for (int rr = warp; rr < NH; rr += kTileWarps) {
+            const int rj = rowj[rr], b = rowb[rr];
+            T *orow = dst + (int64_t)(my0 + rr - (int)g.out_row0) * g.Wo + mx0;
+            for (int k = lane; k < NW; k += 32) {
+                float v;
+                if (rj < 0) {
+                    v = hs[(b - (a.is1d ? 0 : lo)) * a.TW + k];
                 } else {
-                    v = __fmul_rn(ty.w[jy][0], hs[(by + lo) * NW + k]);
-                    for (int t = 1; t < T_; ++t) v = __fmaf_rn(ty.w[jy][t], hs[(by + lo + t) * NW + k], v);
+                    const float *w = wy + 4 * (rj & 0x7fffffff);
+                    v = __fmul_rn(w[0], hs[b * a.TW + k]);
+                    for (int t = 1; t < T_; ++t) v = __fmaf_rn(w[t], hs[(b + t) * a.TW + k], v);
                 }
+                orow[k] = DT<T>::from_f(v);
             }
-            dst[(my - g.out_row0) * g.Wo + mx0 + k] = DT<T>::from_f(v);
         }
     }
 }
@@ -106,7 +155,7 @@ int launch_tile(int dtype, const TileArgs &a, int grid, int smem, void *stream) 
     }
     TileArgs local = a;
     void *args[] = {&local};
-    cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(256), args, (size_t)smem, s);
+    cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(32 * kTileWarps), args, (size_t)smem, s);
     if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();
 }

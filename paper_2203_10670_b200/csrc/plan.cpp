@@ -385,35 +385,48 @@ bool plan_tile(const fcfs_plan_s *pl, const RunGeom &g0, TileArgs &a, int &grid,
     a.pad = pl->pad;
     a.is1d = pl->is1d;
     const int T = pl->tab.ntaps;
+    // window extent of n consecutive outputs (an upper bound over tile positions)
     auto span = [&](int n, int p, int q) { return (int)(((int64_t)(n - 1) * q + p - 1) / p + q + T + 1); };
-    const int budget = 48 * 1024 / 4;  // floats
-    int bestTH = 0, bestTW = 0, bestNR = 0, bestNC = 0;
+    const int budget = 48 * 1024;  // bytes: 4 CTAs per SM
+    int bestTH = 0, bestTW = 0, bestNR = 0, bestNC = 0, bestSlots = 0;
     for (int TW : {256, 128, 64, 32, 16, 8, 4, 2, 1}) {
         for (int TH : {64, 32, 16, 8, 4, 2, 1}) {
-            const int NR = pl->is1d ? TH : span(TH, pl->py, pl->qy);
-            const int NC = span(TW, pl->p, pl->q);
-            if ((int64_t)NR * NC + (int64_t)NR * TW > budget) continue;
+            int NR = TH, slots = 0;
+            if (!pl->is1d) {
+                NR = span(TH, pl->py, pl->qy);
+                if (TH * T < NR) {  // strong down-scaling: one row slot per (output row, tap)
+                    NR = TH * T;
+                    slots = 1;
+                }
+            }
+            const int NC = (span(TW, pl->p, pl->q) + 3) / 4 * 4;
+            const int64_t bytes = 4 * (8 * kPMax + 2 * TW + 2 * TH + NR) + 4 * ((int64_t)NR * NC + (int64_t)NR * TW);
+            if (bytes > budget) continue;
             const int TWe = (int)std::min<int64_t>(TW, g.Wo), THe = (int)std::min<int64_t>(TH, g.out_nrows);
             if ((int64_t)THe * TWe > (int64_t)bestTH * bestTW || ((int64_t)THe * TWe == (int64_t)bestTH * bestTW && TW > bestTW)) {
                 bestTH = THe;
                 bestTW = TWe;
                 bestNR = NR;
                 bestNC = NC;
+                bestSlots = slots;
             }
         }
     }
     if (bestTH == 0) return false;
     a.TH = bestTH;
     a.TW = bestTW;
-    a.xs_cap = (bestNR * bestNC + 3) / 4 * 4;
-    smem = (a.xs_cap + bestNR * bestTW) * 4;
+    a.row_slots = bestSlots;
+    a.nr_cap = bestNR;
+    a.nc_cap = bestNC;
+    a.xs_cap = bestNR * bestNC;
+    smem = 4 * (8 * kPMax + 2 * a.TW + 2 * a.TH + a.nr_cap) + 4 * (a.xs_cap + a.nr_cap * a.TW);
     const int64_t ntiles = g.planes * ((g.out_nrows + a.TH - 1) / a.TH) * ((g.Wo + a.TW - 1) / a.TW);
     grid = (int)std::min<int64_t>(ntiles, (int64_t)pl->sm_count * 4);
     if (desc)
         std::snprintf(desc, (size_t)dlen,
-                      "{\"kernel\": \"tiled\", \"TH\": %d, \"TW\": %d, \"window\": [%d, %d], \"tiles\": %lld, "
-                      "\"grid\": %d, \"block\": 256, \"smem\": %d}",
-                      a.TH, a.TW, bestNR, bestNC, (long long)ntiles, grid, smem);
+                      "{\"kernel\": \"tiled\", \"TH\": %d, \"TW\": %d, \"window\": [%d, %d], \"row_slots\": %d, "
+                      "\"tiles\": %lld, \"grid\": %d, \"block\": 256, \"smem\": %d}",
+                      a.TH, a.TW, bestNR, bestNC, a.row_slots, (long long)ntiles, grid, smem);
     return true;
 }
 
