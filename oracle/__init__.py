@@ -76,6 +76,8 @@ def _load():
                        i32, dp, i32]
             lib.fcfs_oracle_staged_nd.argtypes = nd_args
             lib.fcfs_oracle_direct_nd.argtypes = nd_args
+            lib.fcfs_oracle_adjoint_nd.argtypes = [dp, i64, i32, ctypes.POINTER(i64), ctypes.POINTER(i32),
+                                                   ctypes.POINTER(i32), i32, i32, i32, dp, i32]
             lib.fcfs_oracle_output_dims_nd.argtypes = [i32, ctypes.POINTER(i64), ctypes.POINTER(i32),
                                                        ctypes.POINTER(i32), i32, ctypes.POINTER(i64)]
             _lib = lib
@@ -259,6 +261,24 @@ def direct_nd(x, p, q, mode="bilinear", pad="replicate", floor_extent=False, ran
     """Per-output direct evaluation of the ND interpolation formula (independent code)."""
     R = rank if rank is not None else (len(p) if hasattr(p, "__len__") else 2)
     return _run_nd(_load().fcfs_oracle_direct_nd, x, p, q, R, mode, pad, floor_extent, nthreads)
+
+
+def adjoint_nd(g, dims, p, q, mode="bilinear", pad="replicate", floor_extent=False, nthreads=0):
+    """A^T g for the ND layer A of (dims, p, q, mode, pad): the input gradient
+    (backward pass).  g: (..., *odims); returns (..., *dims), double."""
+    R = len(dims)
+    pp, qq = _nd_params(p, q, R)
+    odims = output_dims_nd(dims, p, q, floor_extent)
+    ga = np.ascontiguousarray(g, dtype=np.float64)
+    if tuple(ga.shape[ga.ndim - R:]) != tuple(odims):
+        raise ValueError(f"gradient shape {ga.shape} does not end with the output dims {odims}")
+    lead = ga.shape[: ga.ndim - R]
+    planes = int(np.prod(lead)) if lead else 1
+    out = np.empty((planes,) + tuple(dims))
+    rc = _load().fcfs_oracle_adjoint_nd(_dptr(ga), planes, R, (ctypes.c_int64 * R)(*dims), pp, qq, MODES[mode],
+                                        PADS[pad], int(floor_extent), _dptr(out), nthreads)
+    _chk(rc, "adjoint_nd")
+    return out.reshape(tuple(lead) + tuple(dims))
 
 
 # ---------------------------------------------------------------- rounding

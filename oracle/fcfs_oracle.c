@@ -881,3 +881,131 @@ int fcfs_oracle_direct_nd(const void *x, int in_kind, int64_t planes, int R, con
     }
     return ORC_OK;
 }
+
+/* ===========================================================================
+ * ADJOINT (backward pass; §7 "the
+ * ability to learn weights" needs gradients through the layer).  FCFS is
+ * linear, y = A x (one plane); the input gradient of a loss L is
+ * dL/dx = A^T dL/dy.  The staged layer is A = crop . shuffle . conv . pad, so
+ * A^T = pad^T . conv^T . shuffle^T . crop^T, each step transposed literally
+ * and applied in reverse order:
+ *   crop^T    : embed g (the output extents) in the zero-extended shuffled array;
+ *   shuffle^T : the inverse permutation of the ND pixelshuffle (§4.1);
+ *   conv^T    : transposed strided conv: xp[q*i + t] += hid[c][i] * k_c[t];
+ *   pad^T     : every padded position adds into the source element it copies
+ *               (replicate / reflect), zero padding drops out.
+ * ===========================================================================*/
+static int adjoint_plane_nd(const double *g, const orc_ndjob *jb, double *out) {
+    const int R = jb->R;
+    int lo[ORC_RMAX] = {0, 0, 0}, T[ORC_RMAX] = {1, 1, 1}, P[ORC_RMAX] = {1, 1, 1}, Q[ORC_RMAX] = {1, 1, 1};
+    int64_t nh[ORC_RMAX] = {1, 1, 1}, PD[ORC_RMAX] = {1, 1, 1}, NO[ORC_RMAX] = {1, 1, 1}, NI[ORC_RMAX] = {1, 1, 1};
+    const int o = ORC_RMAX - R;
+    for (int d = 0; d < R; ++d) {
+        int hi;
+        phase_window(jb->mode, jb->p[d], jb->q[d], &lo[o + d], &hi);
+        T[o + d] = hi - lo[o + d] + 1;
+        P[o + d] = jb->p[d];
+        Q[o + d] = jb->q[d];
+        NO[o + d] = jb->no[d];
+        NI[o + d] = jb->n[d];
+        nh[o + d] = (jb->no[d] + jb->p[d] - 1) / jb->p[d];
+        PD[o + d] = (nh[o + d] - 1) * jb->q[d] + T[o + d];
+    }
+    const int64_t S0 = (int64_t)P[0] * nh[0], S1 = (int64_t)P[1] * nh[1], S2 = (int64_t)P[2] * nh[2];
+    const int nch = P[0] * P[1] * P[2];
+    const int64_t nhid = nh[0] * nh[1] * nh[2];
+    double *sh = (double *)calloc((size_t)(S0 * S1 * S2), sizeof(double));
+    double *hid = (double *)malloc(sizeof(double) * (size_t)nch * nhid);
+    double *xp = (double *)calloc((size_t)(PD[0] * PD[1] * PD[2]), sizeof(double));
+    double *k1[ORC_RMAX];
+    for (int s = 0; s < ORC_RMAX; ++s) k1[s] = (double *)malloc(sizeof(double) * (size_t)P[s] * T[s]);
+    int err = ORC_OK;
+    if (!sh || !hid || !xp || !k1[0] || !k1[1] || !k1[2]) { err = ORC_E_NOMEM; goto done; }
+    for (int s = 0; s < ORC_RMAX; ++s)
+        for (int j = 0; j < P[s]; ++j) {
+            if (s < o) { k1[s][0] = 1.0; continue; }
+            phase_kernel_1d(jb->mode, P[s], Q[s], j, lo[s], T[s], k1[s] + (size_t)j * T[s]);
+        }
+    /* crop^T */
+    for (int64_t i0 = 0; i0 < NO[0]; ++i0)
+        for (int64_t i1 = 0; i1 < NO[1]; ++i1)
+            for (int64_t i2 = 0; i2 < NO[2]; ++i2)
+                sh[(i0 * S1 + i1) * S2 + i2] = g[(i0 * NO[1] + i1) * NO[2] + i2];
+    /* shuffle^T: hid[c, i/r] = sh[i], c = ((i0 mod r0) r1 + i1 mod r1) r2 + i2 mod r2 */
+    for (int64_t i0 = 0; i0 < S0; ++i0)
+        for (int64_t i1 = 0; i1 < S1; ++i1)
+            for (int64_t i2 = 0; i2 < S2; ++i2) {
+                const int64_t c = ((i0 % P[0]) * P[1] + i1 % P[1]) * P[2] + i2 % P[2];
+                hid[((c * nh[0] + i0 / P[0]) * nh[1] + i1 / P[1]) * nh[2] + i2 / P[2]] = sh[(i0 * S1 + i1) * S2 + i2];
+            }
+    /* conv^T: every hidden value spreads over its window with the channel's kernel */
+    for (int j0 = 0; j0 < P[0]; ++j0)
+        for (int j1 = 0; j1 < P[1]; ++j1)
+            for (int j2 = 0; j2 < P[2]; ++j2) {
+                const int ch = (j0 * P[1] + j1) * P[2] + j2;
+                const double *ka = k1[0] + (size_t)j0 * T[0], *kb = k1[1] + (size_t)j1 * T[1],
+                             *kc = k1[2] + (size_t)j2 * T[2];
+                for (int64_t i0 = 0; i0 < nh[0]; ++i0)
+                    for (int64_t i1 = 0; i1 < nh[1]; ++i1)
+                        for (int64_t i2 = 0; i2 < nh[2]; ++i2) {
+                            const double h = hid[(((int64_t)ch * nh[0] + i0) * nh[1] + i1) * nh[2] + i2];
+                            for (int t0 = 0; t0 < T[0]; ++t0)
+                                for (int t1 = 0; t1 < T[1]; ++t1)
+                                    for (int t2 = 0; t2 < T[2]; ++t2)
+                                        xp[((Q[0] * i0 + t0) * PD[1] + Q[1] * i1 + t1) * PD[2] + Q[2] * i2 + t2] +=
+                                            h * (ka[t0] * kb[t1] * kc[t2]);
+                        }
+            }
+    /* pad^T: padded position v (virtual index lo + a) adds into the element it copies */
+    for (int64_t i = 0; i < NI[0] * NI[1] * NI[2]; ++i) out[i] = 0.0;
+    for (int64_t a0 = 0; a0 < PD[0]; ++a0)
+        for (int64_t a1 = 0; a1 < PD[1]; ++a1)
+            for (int64_t a2 = 0; a2 < PD[2]; ++a2) {
+                const int64_t v[ORC_RMAX] = {lo[0] + a0, lo[1] + a1, lo[2] + a2};
+                int64_t idx = 0, s;
+                int zero = 0;
+                for (int d = 0; d < ORC_RMAX; ++d) {
+                    if (d < o) continue;  /* unused dimension: index 0 */
+                    int k = pad_index(v[d], NI[d], jb->pad, &s);
+                    if (k == 0) { zero = 1; break; }
+                    if (k < 0) s = v[d] < 0 ? 0 : NI[d] - 1;  /* unreachable by kept outputs: weight 0 */
+                    idx = idx * NI[d] + s;
+                }
+                if (!zero) out[idx] += xp[(a0 * PD[1] + a1) * PD[2] + a2];
+            }
+done:
+    free(sh);
+    free(hid);
+    free(xp);
+    for (int s = 0; s < ORC_RMAX; ++s) free(k1[s]);
+    return err;
+}
+
+/* Adjoint entry point: g is planes x odims (fcfs_oracle_output_dims_nd), out
+ * planes x dims; the job is the forward job (factors of the forward layer). */
+int fcfs_oracle_adjoint_nd(const double *g, int64_t planes, int R, const int64_t *dims, const int *p, const int *q,
+                           int mode, int pad, int floor_ext, double *out, int nthreads) {
+    orc_ndjob jb;
+    int rc = make_ndjob(R, dims, p, q, mode, pad, floor_ext, &jb);
+    if (rc) return rc;
+    int64_t nin = 1, nout = 1;
+    for (int d = 0; d < R; ++d) {
+        nin *= jb.n[d];
+        nout *= jb.no[d];
+    }
+    int bad = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+    for (int64_t pl = 0; pl < planes; ++pl) {
+        int e = adjoint_plane_nd(g + pl * nout, &jb, out + pl * nin);
+        if (e) {
+#ifdef _OPENMP
+#pragma omp atomic write
+#endif
+            bad = e;
+        }
+    }
+    return bad;
+}
