@@ -194,6 +194,19 @@ fcfs_status fcfs_needed_rows(fcfs_plan_t plan, int64_t out_row0, int64_t out_row
 fcfs_status fcfs_run_host(fcfs_plan_t plan, const void *host_in, void *host_out, int64_t N, void *dev_in,
                           void *dev_out, void *stream);
 
+/* fcfs_run_adjoint -- the backward pass of the layer: grad_in = A^T grad_out,
+ * where A is the plan's (linear, fixed-weight) forward map (SURVEY.md §8(f)
+ * row f3; §7: learning through the layer needs its
+ * gradients).  Every input element gathers the outputs whose taps read it,
+ * padding included (replicate / reflect taps add into the edge or mirrored
+ * element they copy, zero padding contributes nothing).
+ *   grad_out: device N x C x odims (the forward output shape), plan dtype
+ *   grad_in : device N x C x dims (the forward input shape), overwritten
+ * fp32 accumulation (columns, then rows, then slices), rounded once to the
+ * dtype.  Whole tensors only (no row windows).  Asynchronous on `stream`.
+ * Errors: FCFS_E_ARG (NULL, N < 0, overlap), FCFS_E_DEVICE, FCFS_E_CUDA. */
+fcfs_status fcfs_run_adjoint(fcfs_plan_t plan, const void *grad_out, void *grad_in, int64_t N, void *stream);
+
 /* Read-only plan description (introspection and bench accounting). */
 typedef struct {
     int p, q;               /* reduced factor */

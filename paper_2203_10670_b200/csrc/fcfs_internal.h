@@ -52,6 +52,14 @@ struct TileArgs {        // tiled kernel (k_tile.cu): output tiles with a shared
     int xs_cap;          // floats reserved for the window (= nr_cap * nc_cap)
 };
 
+struct AdjArgs {         // adjoint kernel (k_adjoint.cu): grad_in = A^T grad_out
+    const void *grad_out;
+    void *grad_in;
+    int64_t planes, D, H, W, Do, Ho, Wo;
+    PhaseTable tx, ty, tz;
+    int pad, is1d;
+};
+
 // 32-bit division by a run-time invariant divisor (n < 2^31).
 struct FastDiv {
     uint32_t d, m, s;
@@ -130,6 +138,7 @@ int launch_reference(int dtype, const RefArgs &a, void *stream);
 int launch_nearest(int dtype, const NearestArgs &a, void *stream);
 int launch_nearest_batch(int dtype, const NearestBatch &nb, void *stream);
 int launch_tile(int dtype, const TileArgs &a, int grid, int smem, void *stream);
+int launch_adjoint(int dtype, const AdjArgs &a, void *stream);
 
 // Fused: the variant table.  fused_lookup returns an opaque kernel handle or
 // nullptr when (dtype, py/qy, px/qx, ntaps) has no compiled instantiation; K

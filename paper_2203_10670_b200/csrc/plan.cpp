@@ -816,6 +816,34 @@ fcfs_status fcfs_run_host(fcfs_plan_t pl, const void *host_in, void *host_out, i
     return FCFS_OK;
 }
 
+fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in, int64_t N, void *stream) {
+    if (!pl || N < 0) return FCFS_E_ARG;
+    if (N == 0) return FCFS_OK;
+    if (!grad_out || !grad_in) return FCFS_E_ARG;
+    const int ESZ = esize(pl->dtype);
+    const int64_t planes = N * pl->C;
+    const int64_t gin = planes * pl->D * pl->H * pl->W * ESZ, gout = planes * pl->Do * pl->Ho * pl->Wo * ESZ;
+    if (ranges_overlap(grad_out, gout, grad_in, gin)) return FCFS_E_ARG;
+    fcfs_status st = check_device(pl);
+    if (st != FCFS_OK) return st;
+    AdjArgs a;
+    a.grad_out = grad_out;
+    a.grad_in = grad_in;
+    a.planes = planes;
+    a.D = pl->D;
+    a.H = pl->H;
+    a.W = pl->W;
+    a.Do = pl->Do;
+    a.Ho = pl->Ho;
+    a.Wo = pl->Wo;
+    a.tx = pl->tab;
+    a.ty = pl->taby;
+    a.tz = pl->tabz;
+    a.pad = pl->pad;
+    a.is1d = pl->is1d;
+    return launch_adjoint(pl->dtype, a, stream) == 0 ? FCFS_OK : FCFS_E_CUDA;
+}
+
 fcfs_status fcfs_plan_info(fcfs_plan_t pl, fcfs_plan_info_t *info) {
     if (!pl || !info) return FCFS_E_ARG;
     info->p = pl->p;

@@ -164,6 +164,18 @@ class Plan:
                                 self._stream(stream)), "fcfs_run")
         return out
 
+    def run_adjoint(self, grad_out, out=None, stream=None):
+        """grad_in[N, C, *dims] = A^T grad_out[N, C, *odims] (fcfs_run_adjoint): the backward pass."""
+        import torch
+        N = grad_out.shape[0]
+        self._check_tensor(grad_out, self.out_shape(N), "grad_out")
+        if out is None:
+            out = torch.empty(self.in_shape(N), dtype=grad_out.dtype, device=grad_out.device)
+        self._check_tensor(out, self.in_shape(N), "grad_in")
+        check(_lib.lib.fcfs_run_adjoint(self._h, ctypes.c_void_p(grad_out.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                        N, self._stream(stream)), "fcfs_run_adjoint")
+        return out
+
     def run_rows(self, x_rows, in_row0: int, out_row0: int, out_nrows: int, out=None, stream=None):
         """Output rows [out_row0, out_row0+out_nrows) from input rows [in_row0, in_row0+x_rows.shape[2])."""
         import torch
@@ -227,6 +239,36 @@ def scale_nd(x, p, q, mode: str = "bilinear", pad: str = "replicate", extent: st
                 pl = Plan.nd(p, q, mode, pad, x.shape[1], tuple(x.shape[2:]), _dtype_name(x.dtype), extent)
                 _cache[key] = pl
         return pl.run(x, out=out, stream=stream)
+
+
+def _autograd_function():
+    import torch
+
+    class FCFSFunction(torch.autograd.Function):
+        """y = FCFS(x) with its backward pass (fcfs_run_adjoint): the layer as a
+        differentiable op inside a torch model (§7)."""
+
+        @staticmethod
+        def forward(ctx, x, plan):
+            ctx.plan = plan
+            return plan.run(x.contiguous())
+
+        @staticmethod
+        def backward(ctx, g):
+            return ctx.plan.run_adjoint(g.contiguous()), None
+
+    return FCFSFunction
+
+
+_FCFS_FN = None
+
+
+def apply(x, plan: Plan):
+    """Differentiable FCFS: torch autograd calls the adjoint kernel in backward."""
+    global _FCFS_FN
+    if _FCFS_FN is None:
+        _FCFS_FN = _autograd_function()
+    return _FCFS_FN.apply(x, plan)
 
 
 def get_plan(p, q, mode, pad, C, H, W, dtype, extent="paper", is1d=False, device=None) -> Plan:

@@ -198,7 +198,10 @@ def test_launch_geometry(fc, name):
     assert info["PB"] * info["nbands"] >= info["periods"]
     assert info["ntasks"] == -(-info["nseg"] // info["NS"]) * info["nbands"]
     if name in ("C3", "C4a", "C4b", "C5"):
-        assert info["busy_threads"] >= 0.85 * 256
+        # C5 (fp32 3/5, K = 3: 45 input columns x 5 fresh rows per thread) is
+        # bound by the shared-memory budget instead: 146 threads, measured faster
+        # than 253 threads at K = 1 (1012 vs 1044 us)
+        assert info["busy_threads"] >= (0.55 if name == "C5" else 0.85) * 256
         assert info["ntasks"] >= 296  # every SM slot has work
 
 
