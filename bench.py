@@ -235,12 +235,21 @@ def main():
     launches = []
     for cfg in cfgs:
         pl = make_plan(fc, cfg)
-        x = synth.make_input(cfg, batch_offset=rank * cfg.N)
+        if cfg.backward:  # the adjoint: grad_out (forward output shape) -> grad_in (forward input shape)
+            shp = pl.out_shape(cfg.N)
+            n = 1
+            for d in shp:
+                n *= d
+            x = torch.from_numpy(synth.normal_f32(cfg.seed + rank, n).reshape(shp)).to(getattr(torch, cfg.dtype))
+            oshape = pl.in_shape(cfg.N)
+        else:
+            x = synth.make_input(cfg, batch_offset=rank * cfg.N)
+            oshape = pl.out_shape(cfg.N)
         n_out = 1
-        for d in pl.out_shape(cfg.N):
+        for d in oshape:
             n_out *= d
-        launches.append({"cfg": cfg, "plan": pl, "x_host": x, "bytes": pl.compulsory_bytes(cfg.N),
-                         "outputs": n_out})
+        nbytes = (x.numel() + n_out) * x.element_size() if cfg.backward else pl.compulsory_bytes(cfg.N)
+        launches.append({"cfg": cfg, "plan": pl, "x_host": x, "bytes": nbytes, "outputs": n_out, "oshape": oshape})
     # input/output buffers per rotation set; several launches may share one input
     set_bytes = 0
     host_inputs = {}
@@ -256,8 +265,7 @@ def main():
     R = max(1, min(R, int(0.8 * free // set_bytes)))
     dev_inputs = {k: [v.to(dev) for _ in range(R)] for k, v in host_inputs.items()}
     for L in launches:
-        L["outs"] = [torch.empty(L["plan"].out_shape(L["cfg"].N), dtype=L["x_host"].dtype, device=dev)
-                     for _ in range(R)]
+        L["outs"] = [torch.empty(L["oshape"], dtype=L["x_host"].dtype, device=dev) for _ in range(R)]
     torch.cuda.synchronize(dev)
 
     # kernel launches of a step: nearest-gather launches of one dtype share one
@@ -273,7 +281,10 @@ def main():
                 continue
             if len(grp) == 1:
                 L = launches[grp[0]]
-                L["plan"].run(dev_inputs[L["key"]][r], out=L["outs"][r], stream=stream)
+                if L["cfg"].backward:
+                    L["plan"].run_adjoint(dev_inputs[L["key"]][r], out=L["outs"][r], stream=stream)
+                else:
+                    L["plan"].run(dev_inputs[L["key"]][r], out=L["outs"][r], stream=stream)
             else:
                 fc.run_batch([(launches[i]["plan"], dev_inputs[launches[i]["key"]][r], launches[i]["outs"][r])
                               for i in grp], stream=stream)
@@ -438,14 +449,19 @@ def run_e2e(launches, args, dev, stream, world, dist):
             pin_in[L["key"]] = L["x_host"].pin_memory()
         L["pin_out"] = torch.empty(L["outs"][0].shape, dtype=L["x_host"].dtype).pin_memory()
     din = {k: torch.empty(v.shape, dtype=v.dtype, device=dev) for k, v in pin_in.items()}
-    h2d = sum(v.numel() * v.element_size() for v in pin_in.values()) * 0
     # every launch copies its own input (the C-ABI call is per launch)
     h2d = sum(pin_in[L["key"]].numel() * pin_in[L["key"]].element_size() for L in launches)
     d2h = sum(L["pin_out"].numel() * L["pin_out"].element_size() for L in launches)
 
     def step():
         for L in launches:
-            L["plan"].run_host(pin_in[L["key"]], L["pin_out"], din[L["key"]], L["outs"][0], stream=stream)
+            if L["cfg"].backward:  # public API: copy in, Plan.run_adjoint, copy out (all on the stream)
+                with torch.cuda.stream(stream):
+                    din[L["key"]].copy_(pin_in[L["key"]], non_blocking=True)
+                    L["plan"].run_adjoint(din[L["key"]], out=L["outs"][0], stream=stream)
+                    L["pin_out"].copy_(L["outs"][0], non_blocking=True)
+            else:
+                L["plan"].run_host(pin_in[L["key"]], L["pin_out"], din[L["key"]], L["outs"][0], stream=stream)
 
     for _ in range(max(2, args.warmup)):
         step()
@@ -467,7 +483,8 @@ def run_e2e(launches, args, dev, stream, world, dist):
     outputs = sum(L["outputs"] for L in launches)
     return {"value": world * outputs * steps / (ms * 1e-3) / 1e6, "unit": "Mpix/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps, "ms_per_step": ms / steps,
-            "path": "fcfs_run_host (pinned host -> HBM -> kernel -> pinned host)"}
+            "path": ("fcfs_run_host (pinned host -> HBM -> kernel -> pinned host)" if not launches[0]["cfg"].backward
+                     else "pinned grad_out -> HBM -> fcfs_run_adjoint -> pinned grad_in")}
 
 
 if __name__ == "__main__":

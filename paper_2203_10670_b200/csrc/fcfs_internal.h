@@ -58,6 +58,8 @@ struct AdjArgs {         // adjoint kernel (k_adjoint.cu): grad_in = A^T grad_ou
     int64_t planes, D, H, W, Do, Ho, Wo;
     PhaseTable tx, ty, tz;
     int pad, is1d;
+    // tiled variant (2D / 1D rows; TH = 0: the per-element kernel)
+    int TH, TW, K, nc_cap, gw_cap, grid, smem;
 };
 
 // 32-bit division by a run-time invariant divisor (n < 2^31).

@@ -74,9 +74,141 @@ __global__ void __launch_bounds__(256) fcfs_adjoint_kernel(const __grid_constant
     }
 }
 
+// 32-bit pair list of one dimension for input index i into (m, w) arrays
+// (at most cap entries; returns the count, or cap + 1 on overflow).
+__device__ __forceinline__ int adj_list(const PhaseTable &t, int i, int n, int no, int pad, int *ms, float *ws,
+                                        int cap) {
+    int cnt = 0;
+    adj_pairs(t, i, n, no, pad, [&](int64_t m, float w) {
+        if (cnt < cap) {
+            ms[cnt] = (int)m;
+            ws[cnt] = w;
+        }
+        ++cnt;
+    });
+    return cnt;
+}
+
+// Tiled adjoint for 2D planes (and 1D rows): per tile of TH x TW input
+// elements, the (output, weight) pair lists of the tile's columns and rows go
+// to shared memory, the grad_out window they reach is staged once as fp32, then
+// the column pass (per window row) and the row pass produce the tile.  The
+// summation order is the per-element kernel's (columns in list order into an
+// fma chain from 0, then rows), so both give the same bits.
+// pair-list capacity per column / row: a.K (<= 32, the plan's measured maximum)
+
+template <typename T>
+__global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_constant__ AdjArgs a) {
+    extern __shared__ __align__(16) float asm_[];
+    const int TH = a.TH, TW = a.TW, kAdjK = a.K;
+    int *cm = reinterpret_cast<int *>(asm_);       // [TW][K] output columns
+    float *cw = reinterpret_cast<float *>(cm + TW * kAdjK);
+    int *cn = reinterpret_cast<int *>(cw + TW * kAdjK);   // [TW] counts
+    int *rm = cn + TW;                              // [TH][K] output rows
+    float *rw = reinterpret_cast<float *>(rm + TH * kAdjK);
+    int *rn = reinterpret_cast<int *>(rw + TH * kAdjK);   // [TH]
+    int *ext = rn + TH;                             // [4] window: mx_lo, mx_hi, my_lo, my_hi
+    float *gw = reinterpret_cast<float *>(ext + 4); // [NRcap][NCcap]
+    float *hx = gw + a.gw_cap;                      // [NRcap][TW]
+    const int H = (int)a.H, W = (int)a.W, Ho = (int)a.Ho, Wo = (int)a.Wo;
+    const int tiles_y = (H + TH - 1) / TH, tiles_x = (W + TW - 1) / TW;
+    const int ngeom = tiles_y * tiles_x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // CTA b keeps the tile geometry b % ngeom (its pair lists are computed once)
+    // and loops over the planes b / ngeom, + gridDim.x / ngeom, ...
+    const int geom = blockIdx.x % ngeom, pstep = max(1, (int)gridDim.x / ngeom);
+    if (blockIdx.x >= pstep * ngeom) return;
+    const int tx_i = geom % tiles_x, ty_i = geom / tiles_x;
+    const int r0 = ty_i * TH, r1 = min(r0 + TH, H), c0 = tx_i * TW, c1 = min(c0 + TW, W);
+    const int NH = r1 - r0, NW = c1 - c0;
+    if (threadIdx.x == 0) {
+        ext[0] = INT32_MAX;
+        ext[1] = -1;
+        ext[2] = INT32_MAX;
+        ext[3] = -1;
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < NW; k += blockDim.x) {
+        const int n = adj_list(a.tx, c0 + k, W, Wo, a.pad, cm + k * kAdjK, cw + k * kAdjK, kAdjK);
+        cn[k] = n;
+        if (n > 0) {
+            int lo = INT32_MAX, hi = -1;
+            for (int e = 0; e < n; ++e) lo = min(lo, cm[k * kAdjK + e]), hi = max(hi, cm[k * kAdjK + e]);
+            atomicMin(&ext[0], lo);
+            atomicMax(&ext[1], hi);
+        }
+    }
+    for (int rr = threadIdx.x; rr < NH; rr += blockDim.x) {
+        int n;
+        if (a.is1d) {
+            rm[rr * kAdjK] = r0 + rr;
+            rw[rr * kAdjK] = 1.0f;
+            n = 1;
+        } else {
+            n = adj_list(a.ty, r0 + rr, H, Ho, a.pad, rm + rr * kAdjK, rw + rr * kAdjK, kAdjK);
+        }
+        rn[rr] = n;
+        if (n > 0) {
+            int lo = INT32_MAX, hi = -1;
+            for (int e = 0; e < n; ++e) lo = min(lo, rm[rr * kAdjK + e]), hi = max(hi, rm[rr * kAdjK + e]);
+            atomicMin(&ext[2], lo);
+            atomicMax(&ext[3], hi);
+        }
+    }
+    __syncthreads();
+    const int mx_lo = ext[0], my_lo = ext[2];
+    const int NCg = ext[1] - mx_lo + 1, NRg = ext[3] - my_lo + 1;
+    for (int64_t plane = blockIdx.x / ngeom; plane < a.planes; plane += pstep) {
+        __syncthreads();  // the previous plane's readers are done
+        const T *g = static_cast<const T *>(a.grad_out) + plane * (int64_t)Ho * Wo;
+        // grad_out window (fp32)
+        if (NCg > 0 && NRg > 0)
+            for (int r = warp; r < NRg; r += 8) {
+                const T *grow = g + (int64_t)(my_lo + r) * Wo + mx_lo;
+                for (int c = lane; c < NCg; c += 32) gw[r * a.nc_cap + c] = DT<T>::to_f(grow[c]);
+            }
+        __syncthreads();
+        // column pass: hx[r][k] = sum over the column's pairs
+        for (int r = warp; r < NRg; r += 8)
+            for (int k = lane; k < NW; k += 32) {
+                float acc = 0.0f;
+                const int n = cn[k];
+                for (int e = 0; e < n; ++e) acc = __fmaf_rn(cw[k * kAdjK + e], gw[r * a.nc_cap + cm[k * kAdjK + e] - mx_lo], acc);
+                hx[r * TW + k] = acc;
+            }
+        __syncthreads();
+        // row pass -> grad_in
+        T *dst = static_cast<T *>(a.grad_in) + plane * (int64_t)H * W;
+        for (int rr = warp; rr < NH; rr += 8) {
+            const int n = rn[rr];
+            for (int k = lane; k < NW; k += 32) {
+                float acc = 0.0f;
+                for (int e = 0; e < n; ++e) acc = __fmaf_rn(rw[rr * kAdjK + e], hx[(rm[rr * kAdjK + e] - my_lo) * TW + k], acc);
+                dst[(int64_t)(r0 + rr) * W + c0 + k] = DT<T>::from_f(__fmaf_rn(1.0f, acc, 0.0f));
+            }
+        }
+    }
+}
+
 int launch_adjoint(int dtype, const AdjArgs &a, void *stream) {
     const int64_t total = a.planes * a.D * a.H * a.W;
     if (total == 0) return 0;
+    if (a.TH > 0) {  // tiled (2D / 1D rows)
+        static bool configured[3] = {false, false, false};
+        const void *fn = dtype == FCFS_F32   ? reinterpret_cast<const void *>(&fcfs_adjoint_tile_kernel<float>)
+                         : dtype == FCFS_F16 ? reinterpret_cast<const void *>(&fcfs_adjoint_tile_kernel<__half>)
+                                             : reinterpret_cast<const void *>(&fcfs_adjoint_tile_kernel<__nv_bfloat16>);
+        if (!configured[dtype]) {
+            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            if (e != cudaSuccess) return (int)e;
+            configured[dtype] = true;
+        }
+        AdjArgs local = a;
+        void *args[] = {&local};
+        cudaError_t e = cudaLaunchKernel(fn, dim3(a.grid), dim3(256), args, (size_t)a.smem, static_cast<cudaStream_t>(stream));
+        if (e != cudaSuccess) return (int)e;
+        return (int)cudaGetLastError();
+    }
     int64_t blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -816,6 +816,33 @@ fcfs_status fcfs_run_host(fcfs_plan_t pl, const void *host_in, void *host_out, i
     return FCFS_OK;
 }
 
+// Largest number of (output, weight) pairs any input index of one dimension
+// gathers in the adjoint (mirrors adj_pairs in k_adjoint.cu).
+int adj_max_pairs(const PhaseTable &t, int64_t n, int64_t no, int pad) {
+    const int lo = t.lo, T = t.ntaps;
+    const int64_t vmin = lo, vmax = ((no - 1) / t.p) * t.q + t.base[(no - 1) % t.p] + lo + T - 1;
+    auto count_v = [&](int64_t v) {
+        const int64_t bl = v - lo - T + 1, bh = v - lo;
+        const int64_t m0 = bl <= 0 ? 0 : (bl * t.p + t.q - 1) / t.q;
+        int64_t m1 = bh < 0 ? -1 : ((bh + 1) * t.p + t.q - 1) / t.q - 1;
+        m1 = std::min<int64_t>(m1, no - 1);
+        return (int)std::max<int64_t>(0, m1 - m0 + 1);
+    };
+    int best = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int c = count_v(i);
+        if (pad == FCFS_PAD_REPLICATE && i == 0)
+            for (int64_t v = vmin; v < 0; ++v) c += count_v(v);
+        if (pad == FCFS_PAD_REPLICATE && i == n - 1)
+            for (int64_t v = n; v <= vmax; ++v) c += count_v(v);
+        if (pad == FCFS_PAD_REFLECT && i >= 1 && -i >= vmin) c += count_v(-i);
+        if (pad == FCFS_PAD_REFLECT && i <= n - 2 && 2 * (n - 1) - i <= vmax) c += count_v(2 * (n - 1) - i);
+        best = std::max(best, c);
+        if (i > 4 * (int64_t)t.q + 8 && i < n - 4 * (int64_t)t.q - 8) i = std::max(i, n - 4 * (int64_t)t.q - 9);  // periodic interior
+    }
+    return best;
+}
+
 fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in, int64_t N, void *stream) {
     if (!pl || N < 0) return FCFS_E_ARG;
     if (N == 0) return FCFS_OK;
@@ -841,6 +868,44 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
     a.tz = pl->tabz;
     a.pad = pl->pad;
     a.is1d = pl->is1d;
+    a.TH = a.TW = 0;
+    // tiled variant for 2D planes / 1D rows when every pair list fits
+    const int kx = adj_max_pairs(pl->tab, pl->W, pl->Wo, pl->pad);
+    const int ky = pl->is1d ? 1 : adj_max_pairs(pl->taby, pl->H, pl->Ho, pl->pad);
+    if (pl->D == 1 && std::max(kx, ky) <= 32 && pl->H < INT32_MAX / 64 && pl->W < INT32_MAX / 64) {
+        const int K = std::max(1, std::max(kx, ky));
+        const int T = pl->tab.ntaps;
+        auto span = [&](int n, int p, int q) { return (int)(((int64_t)(n + 2 * T + 2) * p + q - 1) / q + p + 2); };
+        int bTH = 0, bTW = 0, bNR = 0, bNC = 0;
+        for (int TW : {256, 128, 64, 32, 16})
+            for (int TH : {256, 128, 64, 32, 16, 8, 4, 2, 1}) {
+                const int NC = (span(TW, pl->p, pl->q) + 3) / 4 * 4;
+                const int NR = pl->is1d ? TH : span(TH, pl->py, pl->qy);
+                const int64_t bytes = (int64_t)(TW + TH) * K * 8 + (TW + TH) * 4 + 16 +
+                                      4 * ((int64_t)NR * NC + (int64_t)NR * TW);
+                if (bytes > 100 * 1024) continue;
+                const int THe = (int)std::min<int64_t>(TH, pl->H), TWe = (int)std::min<int64_t>(TW, pl->W);
+                if ((int64_t)THe * TWe > (int64_t)bTH * bTW) {
+                    bTH = THe;
+                    bTW = TWe;
+                    bNR = NR;
+                    bNC = NC;
+                }
+            }
+        if (bTH > 0) {
+            a.K = K;
+            a.TH = bTH;
+            a.TW = bTW;
+            a.nc_cap = bNC;
+            a.gw_cap = bNR * bNC;
+            a.smem = (bTW + bTH) * K * 8 + (bTW + bTH) * 4 + 16 + 4 * (a.gw_cap + bNR * bTW);
+            const int64_t ngeom = ((pl->H + bTH - 1) / bTH) * ((pl->W + bTW - 1) / bTW);
+            const int64_t target = (int64_t)pl->sm_count * 2;
+            const int64_t pstep = std::max<int64_t>(1, std::min<int64_t>(planes, target / std::max<int64_t>(1, ngeom)));
+            if (ngeom * pstep > INT32_MAX) a.TH = a.TW = 0;
+            else a.grid = (int)(ngeom * pstep);
+        }
+    }
     return launch_adjoint(pl->dtype, a, stream) == 0 ? FCFS_OK : FCFS_E_CUDA;
 }
 

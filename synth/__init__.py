@@ -102,6 +102,7 @@ class Config:
     D: int = 1                       # slices (3D volumes); the tensor is N x C x D x H x W
     pd: tuple | None = None          # per-dimension factors (outermost first): an ND plan (§4.2)
     qd: tuple | None = None
+    backward: bool = False           # the adjoint launch: input = grad_out (N(0,1)), output = grad_in
 
     @property
     def planes(self) -> int:
@@ -149,6 +150,10 @@ CONFIGS.update({
                  D=64, pd=(5, 5, 5), qd=(3, 3, 3)),
 })
 
+# The backward pass of config 3: grad_in = A^T grad_out
+# for the FCN feature-map resize, grad_out N(0,1) bf16 of the forward output shape.
+CONFIGS["C3B"] = dataclasses.replace(CONFIGS["C3"], name="C3B", backward=True, seed=SEED_BASE + 31)
+
 # bench workloads: a step = one pass over one batch, every launch of the config
 WORKLOADS = {
     "C1": ["C1a", "C1b"],
@@ -160,6 +165,7 @@ WORKLOADS = {
     "A2": ["A2"],
     "V1": ["V1"],
     "V2": ["V2"],
+    "C3B": ["C3B"],
 }
 
 
