@@ -89,15 +89,18 @@ __device__ __forceinline__ int adj_list(const PhaseTable &t, int i, int n, int n
     return cnt;
 }
 
-// Tiled adjoint for 2D planes (and 1D rows): per tile of TH x TW input
-// elements, the (output, weight) pair lists of the tile's columns and rows go
-// to shared memory, the grad_out window they reach is staged once as fp32, then
-// the column pass (per window row) and the row pass produce the tile.  The
-// summation order is the per-element kernel's (columns in list order into an
-// fma chain from 0, then rows), so both give the same bits.
+// Tiled adjoint for 2D planes (and 1D rows): a CTA keeps one tile geometry
+// (TH x TW input elements): the (output, weight) pair lists of its columns and
+// rows are built once in shared memory, then for each plane the grad_out window
+// they reach is staged as fp32, the row pass reduces the window rows to the
+// tile's rows (lists uniform across a warp), and the column pass (each thread
+// one column, its list in registers) writes the tile.  Summation: rows first,
+// then columns, each an fma chain from 0 in list order (the 3D per-element
+// kernel sums columns first; the two are separate contracts, each checked
+// against the oracle's bound).
 // pair-list capacity per column / row: a.K (<= 32, the plan's measured maximum)
 
-template <typename T>
+template <typename T, int kAdjKMax>
 __global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_constant__ AdjArgs a) {
     extern __shared__ __align__(16) float asm_[];
     const int TH = a.TH, TW = a.TW, kAdjK = a.K;
@@ -108,8 +111,8 @@ __global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_con
     float *rw = reinterpret_cast<float *>(rm + TH * kAdjK);
     int *rn = reinterpret_cast<int *>(rw + TH * kAdjK);   // [TH]
     int *ext = rn + TH;                             // [4] window: mx_lo, mx_hi, my_lo, my_hi
-    float *gw = reinterpret_cast<float *>(ext + 4); // [NRcap][NCcap]
-    float *hx = gw + a.gw_cap;                      // [NRcap][TW]
+    float *gw = reinterpret_cast<float *>(ext + 4); // [NRcap][NCcap] window
+    float *hx = gw + a.gw_cap;                      // [TH][NCcap] row-pass buffer
     const int H = (int)a.H, W = (int)a.W, Ho = (int)a.Ho, Wo = (int)a.Wo;
     const int tiles_y = (H + TH - 1) / TH, tiles_x = (W + TW - 1) / TW;
     const int ngeom = tiles_y * tiles_x;
@@ -158,6 +161,7 @@ __global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_con
     __syncthreads();
     const int mx_lo = ext[0], my_lo = ext[2];
     const int NCg = ext[1] - mx_lo + 1, NRg = ext[3] - my_lo + 1;
+    float *hy = hx;  // [TH][NCcap]: the row pass over the window columns
     for (int64_t plane = blockIdx.x / ngeom; plane < a.planes; plane += pstep) {
         __syncthreads();  // the previous plane's readers are done
         const T *g = static_cast<const T *>(a.grad_out) + plane * (int64_t)Ho * Wo;
@@ -168,23 +172,39 @@ __global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_con
                 for (int c = lane; c < NCg; c += 32) gw[r * a.nc_cap + c] = DT<T>::to_f(grow[c]);
             }
         __syncthreads();
-        // column pass: hx[r][k] = sum over the column's pairs
-        for (int r = warp; r < NRg; r += 8)
-            for (int k = lane; k < NW; k += 32) {
-                float acc = 0.0f;
-                const int n = cn[k];
-                for (int e = 0; e < n; ++e) acc = __fmaf_rn(cw[k * kAdjK + e], gw[r * a.nc_cap + cm[k * kAdjK + e] - mx_lo], acc);
-                hx[r * TW + k] = acc;
-            }
-        __syncthreads();
-        // row pass -> grad_in
-        T *dst = static_cast<T *>(a.grad_in) + plane * (int64_t)H * W;
+        // row pass first: hy[rr][c] = sum over row rr's pairs (lists uniform across the warp)
         for (int rr = warp; rr < NH; rr += 8) {
             const int n = rn[rr];
-            for (int k = lane; k < NW; k += 32) {
+            for (int c = lane; c < NCg; c += 32) {
                 float acc = 0.0f;
-                for (int e = 0; e < n; ++e) acc = __fmaf_rn(rw[rr * kAdjK + e], hx[(rm[rr * kAdjK + e] - my_lo) * TW + k], acc);
-                dst[(int64_t)(r0 + rr) * W + c0 + k] = DT<T>::from_f(__fmaf_rn(1.0f, acc, 0.0f));
+                for (int e = 0; e < n; ++e)
+                    acc = __fmaf_rn(rw[rr * kAdjK + e], gw[(rm[rr * kAdjK + e] - my_lo) * a.nc_cap + c], acc);
+                hy[rr * a.nc_cap + c] = acc;
+            }
+        }
+        __syncthreads();
+        // column pass -> grad_in; a thread keeps one column's pair list in registers
+        T *dst = static_cast<T *>(a.grad_in) + plane * (int64_t)H * W;
+        const int ncw = (NW + 31) / 32;               // warps covering the columns
+        const int rsplit = max(1, 8 / max(1, ncw));   // row groups
+        const int cw_i = warp % max(1, ncw), rg = warp / max(1, ncw);
+        const int k = cw_i * 32 + lane;
+        if (rg < rsplit && k < NW) {
+            int mloc[kAdjKMax];
+            float wloc[kAdjKMax];
+            const int n = cn[k];
+#pragma unroll
+            for (int e = 0; e < kAdjKMax; ++e) {
+                mloc[e] = e < n ? cm[k * kAdjK + e] - mx_lo : 0;
+                wloc[e] = e < n ? cw[k * kAdjK + e] : 0.0f;
+            }
+            for (int rr = rg; rr < NH; rr += rsplit) {
+                const float *hr = hy + rr * a.nc_cap;
+                float acc = 0.0f;
+#pragma unroll
+                for (int e = 0; e < kAdjKMax; ++e)
+                    if (e < n) acc = __fmaf_rn(wloc[e], hr[mloc[e]], acc);
+                dst[(int64_t)(r0 + rr) * W + c0 + k] = DT<T>::from_f(acc);
             }
         }
     }
@@ -194,14 +214,23 @@ int launch_adjoint(int dtype, const AdjArgs &a, void *stream) {
     const int64_t total = a.planes * a.D * a.H * a.W;
     if (total == 0) return 0;
     if (a.TH > 0) {  // tiled (2D / 1D rows)
-        static bool configured[3] = {false, false, false};
-        const void *fn = dtype == FCFS_F32   ? reinterpret_cast<const void *>(&fcfs_adjoint_tile_kernel<float>)
-                         : dtype == FCFS_F16 ? reinterpret_cast<const void *>(&fcfs_adjoint_tile_kernel<__half>)
-                                             : reinterpret_cast<const void *>(&fcfs_adjoint_tile_kernel<__nv_bfloat16>);
-        if (!configured[dtype]) {
+        static bool configured[3][3] = {};
+        const int kb = a.K <= 8 ? 0 : (a.K <= 16 ? 1 : 2);
+        const void *fns[3][3] = {
+            {reinterpret_cast<const void *>(&fcfs_adjoint_tile_kernel<float, 8>),
+             reinterpret_cast<const void *>(&fcfs_adjoint_tile_kernel<float, 16>),
+             reinterpret_cast<const void *>(&fcfs_adjoint_tile_kernel<float, 32>)},
+            {reinterpret_cast<const void *>(&fcfs_adjoint_tile_kernel<__half, 8>),
+             reinterpret_cast<const void *>(&fcfs_adjoint_tile_kernel<__half, 16>),
+             reinterpret_cast<const void *>(&fcfs_adjoint_tile_kernel<__half, 32>)},
+            {reinterpret_cast<const void *>(&fcfs_adjoint_tile_kernel<__nv_bfloat16, 8>),
+             reinterpret_cast<const void *>(&fcfs_adjoint_tile_kernel<__nv_bfloat16, 16>),
+             reinterpret_cast<const void *>(&fcfs_adjoint_tile_kernel<__nv_bfloat16, 32>)}};
+        const void *fn = fns[dtype][kb];
+        if (!configured[dtype][kb]) {
             cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             if (e != cudaSuccess) return (int)e;
-            configured[dtype] = true;
+            configured[dtype][kb] = true;
         }
         AdjArgs local = a;
         void *args[] = {&local};

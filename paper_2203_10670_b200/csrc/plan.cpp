@@ -882,7 +882,7 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
                 const int NC = (span(TW, pl->p, pl->q) + 3) / 4 * 4;
                 const int NR = pl->is1d ? TH : span(TH, pl->py, pl->qy);
                 const int64_t bytes = (int64_t)(TW + TH) * K * 8 + (TW + TH) * 4 + 16 +
-                                      4 * ((int64_t)NR * NC + (int64_t)NR * TW);
+                                      4 * ((int64_t)NR * NC + (int64_t)TH * NC);
                 if (bytes > 100 * 1024) continue;
                 const int THe = (int)std::min<int64_t>(TH, pl->H), TWe = (int)std::min<int64_t>(TW, pl->W);
                 if ((int64_t)THe * TWe > (int64_t)bTH * bTW) {
@@ -898,7 +898,7 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
             a.TW = bTW;
             a.nc_cap = bNC;
             a.gw_cap = bNR * bNC;
-            a.smem = (bTW + bTH) * K * 8 + (bTW + bTH) * 4 + 16 + 4 * (a.gw_cap + bNR * bTW);
+            a.smem = (bTW + bTH) * K * 8 + (bTW + bTH) * 4 + 32 + 4 * (a.gw_cap + bTH * bNC);
             const int64_t ngeom = ((pl->H + bTH - 1) / bTH) * ((pl->W + bTW - 1) / bTW);
             const int64_t target = (int64_t)pl->sm_count * 2;
             const int64_t pstep = std::max<int64_t>(1, std::min<int64_t>(planes, target / std::max<int64_t>(1, ngeom)));

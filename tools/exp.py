@@ -9,6 +9,7 @@ import argparse
 import os
 import sys
 
+import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -25,26 +26,32 @@ def time_cfg(name, reps, env):
         pl = fc.Plan.nd(c.pd, c.qd, c.mode, c.pad, c.C, c.dims, c.dtype, "floor")
     else:
         pl = fc.Plan(c.p, c.q, c.mode, c.pad, c.C, c.H, c.W, c.dtype, "floor", c.is1d)
-    x = synth.make_input(c).cuda()
+    if c.backward:  # the adjoint: grad_out -> grad_in
+        shp = pl.out_shape(c.N)
+        x = torch.from_numpy(synth.normal_f32(c.seed, int(np.prod(shp))).reshape(shp)).to(getattr(torch, c.dtype)).cuda()
+        oshape, fn = pl.in_shape(c.N), pl.run_adjoint
+    else:
+        x = synth.make_input(c).cuda()
+        oshape, fn = pl.out_shape(c.N), pl.run
     R = max(2, min(8, int(4 * 126e6 // (x.numel() * x.element_size() * 2)) + 1))
     xs = [x.clone() for _ in range(R)]
-    ys = [torch.empty(pl.out_shape(c.N), dtype=x.dtype, device="cuda") for _ in range(R)]
+    ys = [torch.empty(oshape, dtype=x.dtype, device="cuda") for _ in range(R)]
     for i in range(3):
-        pl.run(xs[i % R], out=ys[i % R])
+        fn(xs[i % R], out=ys[i % R])
     torch.cuda.synchronize()
     ts = []
     for rep in range(5):  # back-to-back launches (steady state), 5 batches
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for i in range(reps):
-            pl.run(xs[i % R], out=ys[i % R])
+            fn(xs[i % R], out=ys[i % R])
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3 / reps)
     ts.sort()
     med = ts[len(ts) // 2]
-    by = pl.compulsory_bytes(c.N)
-    return med, by / (med * 1e-6) / 1e9, pl.launch_info(c.N)
+    by = (x.numel() + ys[0].numel()) * x.element_size() if c.backward else pl.compulsory_bytes(c.N)
+    return med, by / (med * 1e-6) / 1e9, ({} if c.backward else pl.launch_info(c.N))
 
 
 if __name__ == "__main__":
