@@ -157,6 +157,15 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     return p;
 }
 
+// Programmatic dependent launch (the library launches its kernels with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel waits for the
+// previous grid of the stream before touching global memory, and lets the next
+// grid launch once it has no more work, so launch latency and grid ramp-up
+// overlap the previous grid's tail.  Without a programmatic predecessor the
+// wait returns at once (ordinary stream order).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // named barrier among `count` threads (id != 0)
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");

@@ -135,6 +135,10 @@ struct NearestBatch {
     NearestArgs job[kMaxBatchJobs];
 };
 
+// cudaLaunchKernelEx with programmatic stream serialization (kernels pair it
+// with pdl_wait / pdl_launch_dependents).  Defined in k_fused_common.cu.
+int launch_pdl(const void *fn, int grid, int block, void **args, int smem, void *stream);
+
 // Launchers (host functions defined in the .cu files).  Return cudaError_t as int.
 int launch_reference(int dtype, const RefArgs &a, void *stream);
 int launch_nearest(int dtype, const NearestArgs &a, void *stream);

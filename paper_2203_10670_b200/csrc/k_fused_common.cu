@@ -1,6 +1,7 @@
 // Fused-variant lookup and launch.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <set>
 
@@ -50,8 +51,21 @@ int launch_fused(const FusedVariant *v, const FusedArgs &a, int grid, int block,
     }
     FusedArgs local = a;
     void *args[] = {&local};
-    cudaError_t e = cudaLaunchKernel(v->fn, dim3(grid), dim3(block), args, (size_t)smem,
-                                     static_cast<cudaStream_t>(stream));
+    return launch_pdl(v->fn, grid, block, args, smem, stream);
+}
+
+int launch_pdl(const void *fn, int grid, int block, void **args, int smem, void *stream) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = std::getenv("FCFS_NO_PDL") ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
     if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();
 }

@@ -22,6 +22,7 @@ namespace fcfs {
 
 template <typename T, int U, int RPW, int MINB>
 __global__ void __launch_bounds__(256, MINB) fcfs_nearest_kernel(const __grid_constant__ NearestBatch nb) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const uint32_t warp0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(256, MINB) fcfs_nearest_kernel(const __grid_co
             }
         }
     }
+    pdl_launch_dependents();
 }
 
 template <typename T, int U, int RPW, int MINB>
@@ -90,7 +92,10 @@ static void launch_nearest_v(NearestBatch nb, cudaStream_t s) {
     }
     int64_t blocks = ((int64_t)nb.pass_prefix[nb.njobs] + 7) / 8;  // 8 warps per block
     if (blocks > 148 * MINB) blocks = 148 * MINB;                    // one resident wave, warps loop
-    if (blocks > 0) fcfs_nearest_kernel<T, U, RPW, MINB><<<(int)blocks, 256, 0, s>>>(nb);
+    if (blocks > 0) {
+        void *args[] = {&nb};
+        launch_pdl(reinterpret_cast<const void *>(&fcfs_nearest_kernel<T, U, RPW, MINB>), (int)blocks, 256, args, 0, s);
+    }
 }
 
 // Variants (U columns per lane per pass, RPW rows per pass, CTAs per SM);

@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(32 * kTileWarps) fcfs_tile_kernel(const __grid
         wx[i] = tx.w[i >> 2][i & 3];
         wy[i] = ty.w[i >> 2][i & 3];
     }
+    pdl_wait();
     const int tiles_y = (int)((g.out_nrows + a.TH - 1) / a.TH), tiles_x = (int)((g.Wo + a.TW - 1) / a.TW);
     const int64_t ntiles = g.planes * tiles_y * tiles_x;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(32 * kTileWarps) fcfs_tile_kernel(const __grid
             }
         }
     }
+    pdl_launch_dependents();
 }
 
 int launch_tile(int dtype, const TileArgs &a, int grid, int smem, void *stream) {
@@ -155,9 +157,7 @@ int launch_tile(int dtype, const TileArgs &a, int grid, int smem, void *stream) 
     }
     TileArgs local = a;
     void *args[] = {&local};
-    cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(32 * kTileWarps), args, (size_t)smem, s);
-    if (e != cudaSuccess) return (int)e;
-    return (int)cudaGetLastError();
+    return launch_pdl(fn, grid, 32 * kTileWarps, args, smem, s);
 }
 
 }  // namespace fcfs
