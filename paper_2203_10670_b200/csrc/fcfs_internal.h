@@ -1,6 +1,8 @@
 // Internal declarations shared by the plan builder (plan.cpp) and the
 // kernels (*.cu).  Not part of the ABI.
 #pragma once
+#include <cuda.h>  // CUtensorMap (TMA descriptor passed in the fused kernel's parameters)
+
 #include <cstdint>
 
 #include "fcfs.h"
@@ -89,6 +91,13 @@ struct NearestArgs {     // nearest gather (one output row per warp pass slot)
 constexpr int kZMax = 16;  // slice phases a fused 3D variant takes
 
 struct FusedArgs {
+    // 4D tiled TMA descriptor of the input (columns, rows, slices, planes), used
+    // when use_tmap: one box of box_w columns x SR rows x TZ slices per segment
+    // and stage lands the stage's rows of that segment in one copy
+    alignas(64) CUtensorMap tmap;
+    int32_t use_tmap, box_w;
+    int32_t seg_block;   // bytes of one segment's block in a stage (TZ x SR rows, 128-B aligned)
+    int32_t slice_pitch; // bytes between the slices of a segment block (= SR * seg_pitch)
     const void *in;
     void *out;
     int64_t in_plane_stride, out_plane_stride;
@@ -116,7 +125,7 @@ struct FusedArgs {
     int32_t plane_even;  // > 0: segment order visits the even planes (this many) before the odd
                          // ones, so that 16-bit outputs whose plane size is odd keep one 4-B
                          // phase per task (packed staging stores without warp divergence)
-    int32_t row_pitch;   // bytes between the rows of a segment in a stage (= TZ * seg_pitch)
+    int32_t row_pitch;   // bytes between the rows of a segment block (= seg_pitch)
     // 3D variants (TZ > 1): every plane has Do output slices from D input
     // slices; output slice m_z combines the TZ input slices b_z + lo + t with
     // the slice weights of phase j_z = m_z mod pz (reference contract: slices,

@@ -299,24 +299,37 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 uint32_t seg_bytes = 0;
                 int z0 = 0;      // first input slice of this lane's segment (3D)
                 int nreal = 0;   // (row, slice) sub-rows of the stage that are not zero padding
+                bool box = false;  // one TMA box for the segment's whole block
+                uint32_t tot = 0;
                 if (lane < ci.b.nsg) {
                     sg = seg_geo<PX, QX, TAPS, LO, K, ESZ>(a, ci.b.group * a.NS + lane);
                     seg_bytes = (uint32_t)(sg.a1 - sg.a0) * ESZ;
                     if constexpr (TZ > 1) z0 = slice_base(a, sg.mz, LO);
-                    for (int r = 0; r < nr; ++r)
+                    // a box copies rows / slices as they are (out of bounds: zeros), so it
+                    // serves zero padding everywhere and the other modes away from the border
+                    box = a.use_tmap && (a.pad == FCFS_PAD_ZERO ||
+                                         (vf >= 0 && vf + nr <= a.H && (TZ == 1 || (z0 >= 0 && z0 + TZ <= a.D))));
+                    if (box) {
+                        tot = (uint32_t)(a.box_w * ESZ * a.SR * TZ);
+                    } else {
+                        for (int r = 0; r < nr; ++r)
 #pragma unroll
-                        for (int tz = 0; tz < TZ; ++tz)
-                            nreal += !(a.pad == FCFS_PAD_ZERO && (vf + r < 0 || vf + r >= a.H ||
-                                                                 (TZ > 1 && (z0 + tz < 0 || z0 + tz >= a.D))));
+                            for (int tz = 0; tz < TZ; ++tz)
+                                nreal += !(a.pad == FCFS_PAD_ZERO && (vf + r < 0 || vf + r >= a.H ||
+                                                                     (TZ > 1 && (z0 + tz < 0 || z0 + tz >= a.D))));
+                        tot = seg_bytes * (uint32_t)nreal;
+                    }
                 }
-                uint32_t tot = seg_bytes * (uint32_t)nreal;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
                 if (lane == 0) mbar_arrive_expect_tx(&full[ci.slot], tot);
                 __syncwarp();
-                if (lane < ci.b.nsg) {  // lane s issues the rows of segment s
+                if (lane < ci.b.nsg && box) {  // lane s: one box for segment s
+                    tma_load_4d(stages + ci.slot * a.stage_bytes + lane * a.seg_block, &a.tmap, sg.a0 - A,
+                                vf - a.in_row0, z0, sg.plane, &full[ci.slot], pol);
+                } else if (lane < ci.b.nsg) {  // lane s issues the rows of segment s
                     const T *pin = static_cast<const T *>(a.in) + (int64_t)sg.plane * a.in_plane_stride + sg.a0;
-                    unsigned char *sbase = stages + ci.slot * a.stage_bytes + A * ESZ + lane * a.SR * a.row_pitch;
+                    unsigned char *sbase = stages + ci.slot * a.stage_bytes + A * ESZ + lane * a.seg_block;
                     for (int r = 0; r < nr; ++r) {
                         const int v = vf + r;
                         if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;
@@ -330,7 +343,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                                 if (a.pad == FCFS_PAD_ZERO && (sl < 0 || sl >= a.D)) continue;
                                 soff = (int64_t)min(max(pad_src32(sl, a.D, a.pad), 0), a.D - 1) * a.in_slice_stride;
                             }
-                            bulk_g2s(sbase + r * a.row_pitch + tz * a.seg_pitch, pin + soff + (int64_t)src * a.W,
+                            bulk_g2s(sbase + r * a.row_pitch + tz * a.slice_pitch, pin + soff + (int64_t)src * a.W,
                                      seg_bytes, &full[ci.slot], pol);
                         }
                     }
@@ -364,7 +377,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                             const int sr = u / n16, c16 = u - sr * n16;
                             const int s = sr / nr, r = sr - s * nr;
                             if (vf + r >= 0 && vf + r < a.H) continue;
-                            reinterpret_cast<uint4 *>(sbase + (s * a.SR + r) * a.row_pitch)[c16] = make_uint4(0, 0, 0, 0);
+                            reinterpret_cast<uint4 *>(sbase + s * a.seg_block + r * a.row_pitch)[c16] = make_uint4(0, 0, 0, 0);
                         }
                     }
                 }
@@ -372,7 +385,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                     const int s = u / (nr * TZ), rz = u - s * (nr * TZ), r = rz / TZ, tz = rz - r * TZ;
                     const int v = vf + r;
                     const SegGeo sg = seg_geo<PX, QX, TAPS, LO, K, ESZ>(a, cf.b.group * a.NS + s);
-                    unsigned char *sub = sbase + (s * a.SR + r) * a.row_pitch + tz * a.seg_pitch;
+                    unsigned char *sub = sbase + s * a.seg_block + r * a.row_pitch + tz * a.slice_pitch;
                     if constexpr (TZ == 1) {
                         if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;  // zeroed above
                     } else {
@@ -445,7 +458,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         const int e0 = A + chunk * K * QX + LO - sg.a0;  // window start (element) in a shared row
         const int col = chunk * KP;
         const int nvalid = sg.c1 - col;  // outputs of this chunk inside the tile (>= KP: all)
-        const int in_off = sgi * a.SR * a.row_pitch;
+        const int in_off = sgi * a.seg_block;
         const int64_t plane_out = (int64_t)sg.plane * a.out_plane_stride + (int64_t)sg.mz * a.out_slice_stride;
         // slice weights of this segment's output slice (3D): phase j_z; j_z = 0 copies its base slice
         float wz[TZ];
@@ -483,7 +496,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
 #pragma unroll
                 for (int t = 0; t < TZ; ++t) {
                     float sub[WIN];
-                    load_win<T, WIN, PAR>(reinterpret_cast<const T *>(srow + t * a.seg_pitch), e0, sub);
+                    load_win<T, WIN, PAR>(reinterpret_cast<const T *>(srow + t * a.slice_pitch), e0, sub);
 #pragma unroll
                     for (int i = 0; i < WIN; ++i) {
                         acc[i] = t == 0 ? __fmul_rn(wz[0], sub[i]) : __fmaf_rn(wz[t], sub[i], acc[i]);

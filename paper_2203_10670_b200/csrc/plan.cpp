@@ -4,6 +4,7 @@
 // output extent (§5.1), strip ownership, compulsory-byte accounting, kernel
 // selection and launch geometry.  No device memory is ever allocated here.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -161,6 +162,37 @@ struct FusedLaunch {
     char desc[768];
 };
 
+// 4D tiled TMA descriptor of the run's input: (columns, rows of the window,
+// slices, planes), box (box_w, SR, TZ, 1), out-of-bounds zero fill.
+bool encode_input_map(const fcfs_plan_s *pl, const RunGeom &g, FusedArgs &a, int TZ) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        cudaGetLastError();
+    }
+    if (!encode) return false;
+    const int ESZ = esize(pl->dtype);
+    const CUtensorMapDataType dt = pl->dtype == FCFS_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                   : pl->dtype == FCFS_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                           : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    const int64_t slices = TZ > 1 ? g.D : 1;
+    cuuint64_t dims[4] = {(cuuint64_t)g.W, (cuuint64_t)g.in_nrows, (cuuint64_t)slices, (cuuint64_t)g.planes};
+    cuuint64_t strides[3] = {(cuuint64_t)(g.W * ESZ), (cuuint64_t)(g.in_nrows * g.W * ESZ),
+                             (cuuint64_t)(g.in_plane_stride * ESZ)};
+    cuuint32_t box[4] = {(cuuint32_t)a.box_w, (cuuint32_t)a.SR, (cuuint32_t)TZ, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode(&a.tmap, dt, 4, const_cast<void *>(g.in), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     const FusedVariant *v = pl->fused;
     const int PY = v->PY, QY = v->QY, PX = v->PX, QX = v->QX, K = v->K, TAPS = v->TAPS, LO = v->LO, TZ = v->TZ;
@@ -242,8 +274,10 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
             c.NS = (int32_t)std::min<int64_t>(std::min(NT / c.CPT, span_cap), nseg);
             if (c.NS < 1) continue;
             c.seg_pitch = seg_pitch_for(c.CPT);
-            c.row_pitch = TZ * c.seg_pitch;
-            c.stage_bytes = c.NS * c.SR * c.row_pitch;
+            c.row_pitch = c.seg_pitch;                                   // segment block: [slice][row][col]
+            c.slice_pitch = c.SR * c.seg_pitch;
+            c.seg_block = (TZ * c.slice_pitch + 127) / 128 * 128;        // 128-B aligned (TMA box destination)
+            c.stage_bytes = c.NS * c.seg_block;
             if (c.ntile == 1) {
                 c.out_pitch = (int)(((int64_t)c.JM * g.Wo * ESZ + 16 + 15) / 16 * 16);
                 c.slot_bytes = c.NS * c.out_pitch;
@@ -257,7 +291,11 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
             c.S = S;
             const double util = (double)c.NS * c.CPT / NT;
             // one flush per period is cheaper; deep enough input ring first
-            const double score = util * (S >= 3 ? 1.0 : 0.9) * (Gf == 1 ? 1.0 : 0.97) - 0.001 * (double)c.ntile;
+            // a segment narrow enough for one TMA box per stage (<= 256 elements) issues
+            // one copy instead of SR * TZ row copies
+            const double boxb = (c.seg_pitch / ESZ <= 256 && !std::getenv("FCFS_NO_TMA")) ? 1.04 : 1.0;
+            const double score =
+                util * boxb * (S >= 3 ? 1.0 : 0.9) * (Gf == 1 ? 1.0 : 0.97) - 0.001 * (double)c.ntile;
             if (score > best_score) {
                 best_score = score;
                 best = c;
@@ -290,16 +328,21 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     if (const char *e = std::getenv("FCFS_DEBUG_GRID")) L.grid = std::max(1, std::min(L.grid, std::atoi(e)));
     if (const char *e = std::getenv("FCFS_DEBUG_S")) a.S = std::max(2, std::min(a.S, std::atoi(e)));
     L.smem = 256 + a.S * a.stage_bytes + 128 + 2 * a.slot_bytes;
+    // one TMA box per segment and stage when the block is narrow enough (box dims <= 256)
+    a.box_w = a.seg_pitch / ESZ;
+    a.use_tmap = 0;
+    if (a.box_w <= 256 && a.SR <= 256 && !std::getenv("FCFS_NO_TMA") && g.in != nullptr)
+        a.use_tmap = encode_input_map(pl, g, a, TZ) ? 1 : 0;
     std::snprintf(L.desc, sizeof(L.desc),
                   "{\"kernel\": \"fused_separable\", \"PY\": %d, \"QY\": %d, \"PX\": %d, \"QX\": %d, \"TZ\": %d, \"taps\": %d, "
                   "\"K\": %d, \"NS\": %d, "
                   "\"CPT\": %d, \"nch\": %d, \"ntile\": %d, \"nseg\": %d, \"S\": %d, \"SR\": %d, \"seg_pitch\": %d, "
                   "\"stage_bytes\": %d, \"out_pitch\": %d, \"slot_bytes\": %d, \"rfix\": %d, \"periods\": %d, "
                   "\"PB\": %d, \"nbands\": %d, \"ntasks\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, "
-                  "\"busy_threads\": %d, \"flush_groups\": %d}",
+                  "\"busy_threads\": %d, \"flush_groups\": %d, \"tma_box\": %d}",
                   PY, QY, PX, QX, TZ, TAPS, K, a.NS, a.CPT, a.nch, a.ntile, a.nseg, a.S, a.SR, a.seg_pitch, a.stage_bytes,
                   a.out_pitch, a.slot_bytes, a.rfix, nper, a.PB, a.nbands, a.ntasks, L.grid, kFusedThreads, L.smem,
-                  a.NS * a.CPT, a.G);
+                  a.NS * a.CPT, a.G, (a.box_w <= 256 && a.SR <= 256) ? a.box_w : 0);
     if (std::getenv("FCFS_DEBUG_PRINT")) std::fprintf(stderr, "%s\n", L.desc);
     return true;
 }

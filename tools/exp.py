@@ -18,7 +18,7 @@ import paper_2203_10670_b200 as fc  # noqa: E402
 
 
 def time_cfg(name, reps, env):
-    for k in [k for k in os.environ if k.startswith("FCFS_DEBUG_")]:
+    for k in [k for k in os.environ if k.startswith("FCFS_DEBUG_") or k.startswith("FCFS_NO_")]:
         del os.environ[k]
     os.environ.update(env)
     c = synth.CONFIGS[name]
