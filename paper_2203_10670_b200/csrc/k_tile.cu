@@ -99,9 +99,17 @@ __global__ void __launch_bounds__(32 * kTileWarps) fcfs_tile_kernel(const __grid
             const int rs = rsrc[i];
             const T *row = src + (int64_t)(rs - (int)g.in_row0) * g.W;
             float *xr = xs + i * a.nc_cap;
-            for (int c = lane; c < NC; c += 32) {
-                const int cs = pad_src32(c_lo + c, (int)g.W, a.pad);
-                xr[c] = (rs >= 0 && cs >= 0) ? DT<T>::to_f(row[cs]) : 0.0f;
+            for (int c0 = lane; c0 < NC; c0 += 128) {  // 4 loads in flight per lane
+                float v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int c = c0 + 32 * u;
+                    const int cs = pad_src32(c_lo + c, (int)g.W, a.pad);
+                    v[u] = (c < NC && rs >= 0 && cs >= 0) ? DT<T>::to_f(row[cs]) : 0.0f;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (c0 + 32 * u < NC) xr[c0 + 32 * u] = v[u];
             }
         }
         __syncthreads();
