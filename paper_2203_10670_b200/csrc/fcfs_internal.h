@@ -96,6 +96,8 @@ struct FusedArgs {
     // and stage lands the stage's rows of that segment in one copy
     alignas(64) CUtensorMap tmap;
     int32_t use_tmap, box_w;
+    int32_t sw_load;     // rows are copied by the issue warp (input pitch / start not 16-B aligned)
+    const void *in_end;  // one past the input tensor (software copies never read past it)
     int32_t seg_block;   // bytes of one segment's block in a stage (TZ x SR rows, 128-B aligned)
     int32_t slice_pitch; // bytes between the slices of a segment block (= SR * seg_pitch)
     const void *in;

@@ -86,6 +86,108 @@ struct PhaseW {
     static constexpr Table tab = table();
 };
 
+// ---------------------------------------------------------------------------
+// Geometry of one dimension as the fused kernel runs it: P outputs and Q inputs
+// per period, TAPS taps per phase starting at window offset base(j) (window
+// start = Q*i + LO), weights w(j, t).
+//   forward (ADJ = false): the layer itself (Geo, PhaseW above);
+//   adjoint (ADJ = true): A^T of the forward factor P0/Q0 (backward pass,
+//     DESIGN.md reading Z21).  Input element v = Q0*k + r receives the forward
+//     outputs m whose taps read it: floor(m Q0/P0) + LO0 + t = v, a contiguous
+//     run m in [P0*k + m0(r), P0*k + m1(r)] -- so A^T is itself a polyphase op
+//     with Q0 phases, stride P0 and run-length taps, weight = the forward tap
+//     (a fraction-0 forward phase contributes only its copy tap, weight 1).
+//     Its input (grad_out) is zero outside the forward extent.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr long long fdivll(long long a, long long b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+__host__ __device__ constexpr long long cdivll(long long a, long long b) { return -fdivll(-a, b); }
+
+template <int P0, int Q0, int T0, int LO0, bool ADJ>
+struct GeoSel;
+
+template <int P0, int Q0, int T0, int LO0>
+struct GeoSel<P0, Q0, T0, LO0, false> {
+    using G = Geo<P0, Q0, T0, LO0>;
+    static constexpr int P = P0, Q = Q0, TAPS = T0, LO = LO0;
+    static constexpr int HI = G::HI, L = G::L, C = G::C, F = G::F;
+    static __host__ __device__ constexpr int base(int j) { return G::base(j); }
+    static __host__ __device__ constexpr bool frac0(int j) { return G::frac0(j); }
+    static __host__ __device__ constexpr int last_row(int j) { return G::last_row(j); }
+    static __host__ __device__ constexpr float w(int j, int t) { return PhaseW<P0, Q0, T0>::w(j, t); }
+};
+
+template <int P0, int Q0, int T0, int LO0>
+struct GeoSel<P0, Q0, T0, LO0, true> {
+    static __host__ __device__ constexpr int m0(int r) { return (int)cdivll((long long)(r - LO0 - T0 + 1) * P0, Q0); }
+    static __host__ __device__ constexpr int m1(int r) { return (int)cdivll((long long)(r - LO0 + 1) * P0, Q0) - 1; }
+    static __host__ __device__ constexpr int taps_max() {
+        int t = 1;
+        for (int r = 0; r < Q0; ++r) t = (m1(r) - m0(r) + 1) > t ? (m1(r) - m0(r) + 1) : t;
+        return t;
+    }
+    static constexpr int P = Q0, Q = P0, TAPS = taps_max(), LO = m0(0);
+    static __host__ __device__ constexpr int base(int r) { return m0(r) - LO; }
+    static __host__ __device__ constexpr int hi() {
+        int h = -(1 << 30);
+        for (int r = 0; r < Q0; ++r) h = (base(r) + TAPS - 1) > h ? (base(r) + TAPS - 1) : h;
+        return h + LO;
+    }
+    static constexpr int HI = hi();
+    static constexpr int L = HI - LO + 1;
+    static constexpr int C = L > Q ? L - Q : 0;
+    static constexpr int F = L - C;
+    static __host__ __device__ constexpr bool frac0(int) { return false; }
+    static __host__ __device__ constexpr int last_row(int r) { return base(r) + TAPS - 1; }
+    static __host__ __device__ constexpr float w(int r, int e) {
+        const int m = m0(r) + e;  // forward output offset relative to P0 * k
+        if (m > m1(r)) return 0.0f;
+        const int j = (int)(m - fdivll(m, P0) * P0);
+        const int b = (int)fdivll((long long)m * Q0, P0);  // its base relative to Q0 * k
+        const int t = r - LO0 - b;                          // the tap that reads element r
+        if (t < 0 || t >= T0) return 0.0f;
+        if (((long long)j * Q0) % P0 == 0) return t == -LO0 ? 1.0f : 0.0f;  // fraction-0 phase: copy tap
+        return PhaseW<P0, Q0, T0>::w(j, t);
+    }
+};
+
+// Copy nbytes from src (any alignment of the element type, at least 2 B) to
+// dst (16-B aligned) with the 32 lanes of a warp: 16-B loads of the aligned
+// superset of the source, shifted into place in registers, 16-B stores (the
+// last chunk may write up to 15 bytes past nbytes: the row slot's margin).
+// Loads never pass `end` (the end of the source tensor).
+__device__ __forceinline__ void copy_realign(unsigned char *dst, const unsigned char *src, int nbytes, int lane,
+                                             const unsigned char *end) {
+    const uintptr_t s0 = reinterpret_cast<uintptr_t>(src);
+    const uintptr_t base = s0 & ~(uintptr_t)15;
+    const int d = (int)(s0 & 15), q = d >> 2, sh = 8 * (d & 3);
+    const int nchunk = (nbytes + 15) >> 4;
+    const uintptr_t e = reinterpret_cast<uintptr_t>(end);
+    for (int i = lane; i < nchunk; i += 32) {
+        const uintptr_t c0 = base + 16 * (uintptr_t)i;
+        uint4 lo = make_uint4(0, 0, 0, 0), hi = make_uint4(0, 0, 0, 0);
+        if (c0 + 16 <= e) lo = __ldg(reinterpret_cast<const uint4 *>(c0));
+        if (d != 0 && c0 + 32 <= e) hi = __ldg(reinterpret_cast<const uint4 *>(c0 + 16));
+        if (c0 + 16 > e || (d != 0 && c0 + 32 > e)) {  // the tensor's last bytes: word by word
+            uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int k = 0; k < 8; ++k)
+                if (c0 + 4 * k + 4 <= e) w[k] = *reinterpret_cast<const uint32_t *>(c0 + 4 * k);
+                else if (c0 + 4 * k + 2 <= e) w[k] = *reinterpret_cast<const unsigned short *>(c0 + 4 * k);
+            lo = make_uint4(w[0], w[1], w[2], w[3]);
+            hi = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+        const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+        uint32_t a5[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) a5[k] = q == 0 ? w[k] : q == 1 ? w[k + 1] : q == 2 ? w[k + 2] : w[k + 3];
+        uint4 o;
+        o.x = sh ? __funnelshift_r(a5[0], a5[1], sh) : a5[0];
+        o.y = sh ? __funnelshift_r(a5[1], a5[2], sh) : a5[1];
+        o.z = sh ? __funnelshift_r(a5[2], a5[3], sh) : a5[2];
+        o.w = sh ? __funnelshift_r(a5[3], a5[4], sh) : a5[3];
+        *reinterpret_cast<uint4 *>(dst + 16 * i) = o;
+    }
+}
+
 template <typename T> struct HalfBits;
 template <> struct HalfBits<__half> {
     static __device__ __forceinline__ float f(uint32_t b) { return __half2float(__ushort_as_half((unsigned short)b)); }
@@ -156,9 +258,9 @@ struct SegGeo {
     int plane, mz, ch0, ch1, c0, c1, a0, a1;  // mz: output slice (3D variants), else 0
 };
 
-template <int P, int Q, int TAPS, int LO, int K, int ESZ>
+template <typename G, int K, int ESZ>
 __device__ __forceinline__ SegGeo seg_geo(const FusedArgs &a, int gs) {
-    using G = Geo<P, Q, TAPS, LO>;
+    constexpr int P = G::P, Q = G::Q, LO = G::LO;
     constexpr int A = 16 / ESZ;
     SegGeo s;
     const int k = gs / a.ntile;
@@ -199,7 +301,7 @@ __device__ __forceinline__ BandInfo band_info(const FusedArgs &a, int task) {
 }
 
 // Producer-side stage cursor: (task, stage k) of a CTA's sequence of stages.
-template <int P, int Q, int TAPS, int LO>
+template <typename G>
 struct StageCursor {
     int task, k, nst, slot;
     uint32_t phase, seq;
@@ -214,8 +316,8 @@ struct StageCursor {
     }
     __device__ __forceinline__ void load(const FusedArgs &a) {
         if (task < a.ntasks) {
-            b = band_info<P>(a, task);
-            nst = (Geo<P, Q, TAPS, LO>::C > 0 ? 1 : 0) + (b.iy1 - b.iy0);
+            b = band_info<G::P>(a, task);
+            nst = (G::C > 0 ? 1 : 0) + (b.iy1 - b.iy0);
         }
     }
     __device__ __forceinline__ void next(const FusedArgs &a) {
@@ -229,13 +331,12 @@ struct StageCursor {
     }
     // virtual rows [vf, vf + nr) of the stage
     __device__ __forceinline__ void rows(int &vf, int &nr) const {
-        using G = Geo<P, Q, TAPS, LO>;
         if (G::C > 0 && k == 0) {
-            vf = Q * b.iy0 + LO;
+            vf = G::Q * b.iy0 + G::LO;
             nr = G::C;
         } else {
             const int iy = b.iy0 + k - (G::C > 0 ? 1 : 0);
-            vf = Q * iy + LO + G::C;
+            vf = G::Q * iy + G::LO + G::C;
             nr = G::F;
         }
     }
@@ -247,12 +348,16 @@ __device__ __forceinline__ int slice_base(const FusedArgs &a, int mz, int lo) {
     return (mz / a.pz) * a.qz + a.zbase[jz] + lo;
 }
 
-template <typename T, int PY, int QY, int PX, int QX, int TAPS, int LO, int K, int TZ>
+template <typename T, int PY0, int QY0, int PX0, int QX0, int T0, int LO0, int K, int TZ, bool ADJ = false>
 __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __grid_constant__ FusedArgs a) {
-    using GY = Geo<PY, QY, TAPS, LO>;  // rows: y-periods of PY output rows from QY input rows
-    using GX = Geo<PX, QX, TAPS, LO>;  // columns: x-periods of PX outputs from QX inputs
-    using WY = PhaseW<PY, QY, TAPS>;
-    using WX = PhaseW<PX, QX, TAPS>;
+    // forward: the layer of factors PY0/QY0 (rows) and PX0/QX0 (columns), T0 taps
+    // from LO0; ADJ: its adjoint (the same kernel running A^T's polyphase form)
+    using GY = GeoSel<PY0, QY0, T0, LO0, ADJ>;  // rows: y-periods of PY output rows from QY input rows
+    using GX = GeoSel<PX0, QX0, T0, LO0, ADJ>;  // columns: x-periods of PX outputs from QX inputs
+    using WY = GY;
+    using WX = GX;
+    constexpr int PY = GY::P, QY = GY::Q, PX = GX::P, QX = GX::Q;
+    constexpr int TY = GY::TAPS, TX = GX::TAPS, LOX = GX::LO;
     constexpr int L = GY::L, C = GY::C;  // window rows per period, rows carried to the next
     constexpr int KP = K * PX;
     constexpr int WIN = (K - 1) * QX + GX::L;
@@ -260,10 +365,12 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     constexpr int A = 16 / ESZ;  // left margin (elements)
     constexpr int NCT = 32 * kFusedConsumerWarps;
     // element parity of every window start (16-bit types), when it is static
-    constexpr int PAR = (ESZ == 2 && (K * QX) % 2 == 0) ? ((LO % 2 + 2) % 2) : -1;
+    constexpr int PAR = (ESZ == 2 && (K * QX) % 2 == 0) ? ((LOX % 2 + 2) % 2) : -1;
     static_assert(PX <= 16 && PY <= 16, "fused variants have p <= 16");
-    static_assert(-LO <= A, "left margin too small");
-    static_assert(TZ == 1 || TZ == TAPS, "slice taps: none or the mode's");
+    static_assert(TZ == 1 || (TZ == T0 && !ADJ), "slice taps: none or the mode's (forward only)");
+    if constexpr (-LOX > A) {
+        return;  // adjoint geometry whose first tap reaches past the left margin: never selected (variant ok = 0)
+    } else {
 
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);   // TMA landed       (count 1 + tx)
@@ -288,10 +395,48 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         // ------------------------------------------------------- producer: issue
         // a stage's bulk loads as soon as the consumers have freed its slot
         const uint64_t pol = policy_evict_first();
-        StageCursor<PY, QY, TAPS, LO> ci;
+        StageCursor<GY> ci;
         ci.start(a);
         while (ci.task < a.ntasks) {
-            {
+            if (a.sw_load) {
+                // software copy (rows whose pitch or start is not 16-B aligned): the
+                // warp copies each (row, slice) sub-row's columns [a0, a1) into the
+                // stage with 16-B loads of the aligned superset, realigned in registers
+                if (ci.seq >= (uint32_t)a.S) mbar_wait(&empty[ci.slot], ci.phase ^ 1);
+                int vf, nr;
+                ci.rows(vf, nr);
+                for (int s = 0; s < ci.b.nsg; ++s) {
+                    const SegGeo sg = seg_geo<GX, K, ESZ>(a, ci.b.group * a.NS + s);
+                    int z0 = 0;
+                    if constexpr (TZ > 1) z0 = slice_base(a, sg.mz, LO0);
+                    const int nbytes = (sg.a1 - sg.a0) * ESZ;
+                    for (int r = 0; r < nr; ++r) {
+                        const int v = vf + r;
+                        if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;  // zeroed by warp 1
+                        const int src = min(max(pad_src32(v, a.H, a.pad) - a.in_row0, 0), a.in_nrows - 1);
+#pragma unroll
+                        for (int tz = 0; tz < TZ; ++tz) {
+                            int64_t soff = 0;
+                            if constexpr (TZ > 1) {
+                                const int sl = z0 + tz;
+                                if (a.pad == FCFS_PAD_ZERO && (sl < 0 || sl >= a.D)) continue;
+                                soff = (int64_t)min(max(pad_src32(sl, a.D, a.pad), 0), a.D - 1) * a.in_slice_stride;
+                            }
+                            const unsigned char *src0 = reinterpret_cast<const unsigned char *>(
+                                static_cast<const T *>(a.in) + (int64_t)sg.plane * a.in_plane_stride + soff +
+                                (int64_t)src * a.W + sg.a0);
+                            unsigned char *dst = stages + ci.slot * a.stage_bytes + A * ESZ + s * a.seg_block +
+                                                 r * a.row_pitch + tz * a.slice_pitch;
+                            copy_realign(dst, src0, nbytes, lane, static_cast<const unsigned char *>(a.in_end));
+                        }
+                    }
+                }
+                __threadfence_block();  // every lane's stage stores before the release below
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[ci.slot]);  // release: the stage's rows are written
+                __syncwarp();
+                ci.next(a);
+            } else {
                 if (ci.seq >= (uint32_t)a.S) mbar_wait(&empty[ci.slot], ci.phase ^ 1);
                 int vf, nr;
                 ci.rows(vf, nr);
@@ -302,9 +447,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 bool box = false;  // one TMA box for the segment's whole block
                 uint32_t tot = 0;
                 if (lane < ci.b.nsg) {
-                    sg = seg_geo<PX, QX, TAPS, LO, K, ESZ>(a, ci.b.group * a.NS + lane);
+                    sg = seg_geo<GX, K, ESZ>(a, ci.b.group * a.NS + lane);
                     seg_bytes = (uint32_t)(sg.a1 - sg.a0) * ESZ;
-                    if constexpr (TZ > 1) z0 = slice_base(a, sg.mz, LO);
+                    if constexpr (TZ > 1) z0 = slice_base(a, sg.mz, LO0);
                     // a box copies rows / slices as they are (out of bounds: zeros), so it
                     // serves zero padding everywhere and the other modes away from the border
                     box = a.use_tmap && (a.pad == FCFS_PAD_ZERO ||
@@ -359,7 +504,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         // ------------------------------------------- producer: padding + release
         // once a stage's bytes have landed, write the padding columns the kept
         // outputs read into the row margins and hand the stage to the consumers
-        StageCursor<PY, QY, TAPS, LO> cf;
+        StageCursor<GY> cf;
         cf.start(a);
         while (cf.task < a.ntasks) {
             mbar_wait(&full[cf.slot], cf.phase);
@@ -384,12 +529,12 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 for (int u = lane; u < pairs; u += 32) {
                     const int s = u / (nr * TZ), rz = u - s * (nr * TZ), r = rz / TZ, tz = rz - r * TZ;
                     const int v = vf + r;
-                    const SegGeo sg = seg_geo<PX, QX, TAPS, LO, K, ESZ>(a, cf.b.group * a.NS + s);
+                    const SegGeo sg = seg_geo<GX, K, ESZ>(a, cf.b.group * a.NS + s);
                     unsigned char *sub = sbase + s * a.seg_block + r * a.row_pitch + tz * a.slice_pitch;
                     if constexpr (TZ == 1) {
                         if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;  // zeroed above
                     } else {
-                        const int sl = slice_base(a, sg.mz, LO) + tz;
+                        const int sl = slice_base(a, sg.mz, LO0) + tz;
                         if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H || sl < 0 || sl >= a.D)) {
                             // zero-padding row or slice
                             for (int c16 = 0; c16 < n16; ++c16) reinterpret_cast<uint4 *>(sub)[c16] = make_uint4(0, 0, 0, 0);
@@ -399,7 +544,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                     T *row = reinterpret_cast<T *>(sub) + A - sg.a0;  // row[c]
                     if (sg.a0 == 0) {
 #pragma unroll
-                        for (int c = LO; c < 0; ++c) {
+                        for (int c = LOX; c < 0; ++c) {
                             const int sc = pad_src32(c, a.W, a.pad);
                             row[c] = sc < 0 ? DT<T>::from_f(0.0f) : row[min(sc, sg.a1 - 1)];
                         }
@@ -428,10 +573,11 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     const int RS = full_width ? rowb : a.out_pitch;          // staging row stride
     const uint32_t R16 = full_width ? 0u : rowb16;          // per-row shift increment (tiled)
     constexpr int kJM = (PY + 1) / 2;                        // first row of flush group 1 (plan: JM)
-    float hr[TAPS][KP];  // ring of horizontally filtered window rows (see `period`)
+    float hr[TY][KP];  // ring of horizontally filtered window rows (see `period`)
     // Unrolling the period loop over the ring offsets removes the carry copies
     // but multiplies the loop body; worth it only for small register rings.
-    constexpr bool kRingUnroll = KP * TAPS <= 24;  // (40, C3's ring, measured 160 -> 210 us)
+    constexpr int U0 = TY / cgcd(QY, TY);  // ring offsets before the cycle repeats
+    constexpr bool kRingUnroll = KP * TY <= 24 && (U0 == 1 || U0 == 2 || U0 == 4);  // (40, C3's ring: 160 -> 210 us)
     int slot = 0;
     uint32_t phase = 0;
     uint32_t fk = 0;     // flush counter: staging slot = fk & 1
@@ -452,10 +598,10 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         }
         const bool seg_ok = sgi < b.nsg;
         SegGeo sg = {0, 0, 0, 0, 0, 0, 0, 1};
-        if (seg_ok) sg = seg_geo<PX, QX, TAPS, LO, K, ESZ>(a, b.group * a.NS + sgi);
+        if (seg_ok) sg = seg_geo<GX, K, ESZ>(a, b.group * a.NS + sgi);
         const int chunk = last ? sg.ch1 - 1 : sg.ch0 + chl;
         const bool active = seg_ok && (last || chunk < sg.ch1 - 1);
-        const int e0 = A + chunk * K * QX + LO - sg.a0;  // window start (element) in a shared row
+        const int e0 = A + chunk * K * QX + LOX - sg.a0;  // window start (element) in a shared row
         const int col = chunk * KP;
         const int nvalid = sg.c1 - col;  // outputs of this chunk inside the tile (>= KP: all)
         const int in_off = sgi * a.seg_block;
@@ -479,7 +625,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         const int span_row = full_width ? 0 : span_id / max(b.nsg, 1);
         const bool span_ok = full_width ? span_id < b.nsg : span_row < a.JM;
         SegGeo sq = {0, 0, 0, 0, 0, 0, 0, 1};
-        if (span_ok) sq = seg_geo<PX, QX, TAPS, LO, K, ESZ>(a, b.group * a.NS + span_seg);
+        if (span_ok) sq = seg_geo<GX, K, ESZ>(a, b.group * a.NS + span_seg);
         T *const span_out =
             static_cast<T *>(a.out) + (int64_t)sq.plane * a.out_plane_stride + (int64_t)sq.mz * a.out_slice_stride;
 
@@ -500,7 +646,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
 #pragma unroll
                     for (int i = 0; i < WIN; ++i) {
                         acc[i] = t == 0 ? __fmul_rn(wz[0], sub[i]) : __fmaf_rn(wz[t], sub[i], acc[i]);
-                        if (t == -LO) cp[i] = sub[i];
+                        if (t == -LO0) cp[i] = sub[i];
                     }
                 }
 #pragma unroll
@@ -511,13 +657,13 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
 #pragma unroll
                 for (int jx = 0; jx < PX; ++jx) {
                     if (GX::frac0(jx)) {  // fraction 0: the tap at offset 0, exactly
-                        h[jx] = win[GX::base(jx) - LO];
-                        h[PX + jx] = win[QX + GX::base(jx) - LO];
+                        h[jx] = win[GX::base(jx) - LOX];
+                        h[PX + jx] = win[QX + GX::base(jx) - LOX];
                     } else {
                         const int bb = GX::base(jx);
                         float2 v2 = fmul2_rn(WX::w(jx, 0), make_float2(win[bb], win[QX + bb]));
 #pragma unroll
-                        for (int tp = 1; tp < TAPS; ++tp)
+                        for (int tp = 1; tp < TX; ++tp)
                             v2 = ffma2_rn(WX::w(jx, tp), make_float2(win[bb + tp], win[QX + bb + tp]), v2);
                         h[jx] = v2.x;
                         h[PX + jx] = v2.y;
@@ -530,12 +676,12 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                     for (int jx = 0; jx < PX; ++jx) {
                         float v2;
                         if (GX::frac0(jx)) {
-                            v2 = win[k * QX + GX::base(jx) - LO];  // fraction 0: the tap at offset 0, exactly
+                            v2 = win[k * QX + GX::base(jx) - LOX];  // fraction 0: the tap at offset 0, exactly
                         } else {
                             const int bb = k * QX + GX::base(jx);
                             v2 = __fmul_rn(WX::w(jx, 0), win[bb]);
 #pragma unroll
-                            for (int tp = 1; tp < TAPS; ++tp) v2 = __fmaf_rn(WX::w(jx, tp), win[bb + tp], v2);
+                            for (int tp = 1; tp < TX; ++tp) v2 = __fmaf_rn(WX::w(jx, tp), win[bb + tp], v2);
                         }
                         h[k * PX + jx] = v2;
                     }
@@ -548,16 +694,16 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             if (active) {
                 const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
 #pragma unroll
-                for (int i = 0; i < C; ++i) row_h(hr[i % TAPS], sb + i * a.row_pitch);
+                for (int i = 0; i < C; ++i) row_h(hr[i % TY], sb + i * a.row_pitch);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
             if (++slot == a.S) { slot = 0; phase ^= 1; }
         }
 
-        // One y-period with window row r in ring slot (RO + r) % TAPS.  The next
+        // One y-period with window row r in ring slot (RO + r) % TY.  The next
         // period's rows 0..C-1 are this period's rows QY..L-1, so its offset is
-        // RO + QY: the loop below is unrolled over the TAPS / gcd(QY, TAPS) ring
+        // RO + QY: the loop below is unrolled over the TY / gcd(QY, TY) ring
         // offsets and no row is ever copied between ring slots.
         auto period = [&](auto ro_c, const int iy) {
             constexpr int RO = decltype(ro_c)::value;
@@ -598,25 +744,25 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 float o[KP];
                 if (GY::frac0(jy)) {  // fraction 0: the tap row at offset 0, exactly
 #pragma unroll
-                    for (int c = 0; c < KP; ++c) o[c] = hr[(RO + GY::base(jy) - LO) % TAPS][c];
+                    for (int c = 0; c < KP; ++c) o[c] = hr[(RO + GY::base(jy) - GY::LO) % TY][c];
                 } else {
                     const int bb = GY::base(jy);
                     constexpr int H2 = KP / 2;  // columns c and c + H2 share the row weights
 #pragma unroll
                     for (int c = 0; c < H2; ++c) {
-                        float2 v2 = fmul2_rn(WY::w(jy, 0), make_float2(hr[(RO + bb) % TAPS][c], hr[(RO + bb) % TAPS][c + H2]));
+                        float2 v2 = fmul2_rn(WY::w(jy, 0), make_float2(hr[(RO + bb) % TY][c], hr[(RO + bb) % TY][c + H2]));
 #pragma unroll
-                        for (int tp = 1; tp < TAPS; ++tp)
+                        for (int tp = 1; tp < TY; ++tp)
                             v2 = ffma2_rn(WY::w(jy, tp),
-                                          make_float2(hr[(RO + bb + tp) % TAPS][c], hr[(RO + bb + tp) % TAPS][c + H2]), v2);
+                                          make_float2(hr[(RO + bb + tp) % TY][c], hr[(RO + bb + tp) % TY][c + H2]), v2);
                         o[c] = v2.x;
                         o[c + H2] = v2.y;
                     }
                     if constexpr (KP % 2 == 1) {
-                        float v1 = __fmul_rn(WY::w(jy, 0), hr[(RO + bb) % TAPS][KP - 1]);
+                        float v1 = __fmul_rn(WY::w(jy, 0), hr[(RO + bb) % TY][KP - 1]);
 #pragma unroll
-                        for (int tp = 1; tp < TAPS; ++tp)
-                            v1 = __fmaf_rn(WY::w(jy, tp), hr[(RO + bb + tp) % TAPS][KP - 1], v1);
+                        for (int tp = 1; tp < TY; ++tp)
+                            v1 = __fmaf_rn(WY::w(jy, tp), hr[(RO + bb + tp) % TY][KP - 1], v1);
                         o[KP - 1] = v1;
                     }
                 }
@@ -678,7 +824,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
 #pragma unroll
             for (int r = C; r < L; ++r) {
-                if (active) row_h(hr[(RO + r) % TAPS], sb + (r - C) * a.row_pitch);
+                if (active) row_h(hr[(RO + r) % TY], sb + (r - C) * a.row_pitch);
 #pragma unroll
                 for (int jy = 0; jy < PY; ++jy) {
                     if (GY::last_row(jy) == r) {
@@ -690,40 +836,41 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
             if (++slot == a.S) { slot = 0; phase ^= 1; }
-            if constexpr (!kRingUnroll && C > 0 && (QY % TAPS) != 0) {
+            if constexpr (!kRingUnroll && C > 0 && (QY % TY) != 0) {
                 // carry window rows QY..L-1 -> rows 0..C-1 of the next period
                 float tmp[C][KP];
 #pragma unroll
                 for (int i = 0; i < C; ++i)
 #pragma unroll
-                    for (int c = 0; c < KP; ++c) tmp[i][c] = hr[(QY + i) % TAPS][c];
+                    for (int c = 0; c < KP; ++c) tmp[i][c] = hr[(QY + i) % TY][c];
 #pragma unroll
                 for (int i = 0; i < C; ++i)
 #pragma unroll
-                    for (int c = 0; c < KP; ++c) hr[i % TAPS][c] = tmp[i][c];
+                    for (int c = 0; c < KP; ++c) hr[i % TY][c] = tmp[i][c];
             }
             flush(a.G - 1);
             fk += a.G;
         };
         // ring offsets before the cycle repeats (1: the carried rows are copied)
-        constexpr int U = kRingUnroll ? TAPS / cgcd(QY, TAPS) : 1;
+        constexpr int U = kRingUnroll ? U0 : 1;
         for (int iy = b.iy0; iy < b.iy1;) {
             period(std::integral_constant<int, 0>{}, iy);
             if (++iy >= b.iy1) break;
             if constexpr (U > 1) {
-                period(std::integral_constant<int, (QY % TAPS)>{}, iy);
+                period(std::integral_constant<int, (QY % TY)>{}, iy);
                 if (++iy >= b.iy1) break;
             }
             if constexpr (U > 2) {
-                period(std::integral_constant<int, ((2 * QY) % TAPS)>{}, iy);
+                period(std::integral_constant<int, ((2 * QY) % TY)>{}, iy);
                 if (++iy >= b.iy1) break;
-                period(std::integral_constant<int, ((3 * QY) % TAPS)>{}, iy);
+                period(std::integral_constant<int, ((3 * QY) % TY)>{}, iy);
                 ++iy;
             }
         }
     }
     pdl_launch_dependents();
     if (span_e == 0) bulk_wait0();
+    }
 }
 
 // x-periods per thread chunk (K outputs-periods of PX columns), a measured

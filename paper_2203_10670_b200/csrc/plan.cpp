@@ -247,9 +247,12 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     a.rfix = (int32_t)std::max<int64_t>(0, std::min<int64_t>(reach_kept - g.W, ralloc));
     const int budget = 110 * 1024;              // two CTAs per SM
     // shared row: [A-element margin][loaded columns][right margin], 16-B multiple
+    // rows copied by the issue warp (input pitch or start not 16-B aligned) may
+    // write up to 15 bytes past a row's columns: one more margin of A elements
+    const bool sw = ((g.W * ESZ) % 16 != 0) || (reinterpret_cast<uintptr_t>(g.in) & 15) != 0;
     auto seg_pitch_for = [&](int cpt) {
         int64_t elems = std::min<int64_t>(g.W, (int64_t)cpt * K * QX - QX + Lw + 2 * A);
-        elems = (elems + A - 1) / A * A + A + (ralloc + A - 1) / A * A;
+        elems = (elems + A - 1) / A * A + A + (ralloc + A - 1) / A * A + (sw ? A : 0);
         return (int)(elems * ESZ);
     };
     // geometry search: segments of CPT chunks (one plane x one column tile), NS
@@ -293,7 +296,7 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
             // one flush per period is cheaper; deep enough input ring first
             // a segment narrow enough for one TMA box per stage (<= 256 elements) issues
             // one copy instead of SR * TZ row copies
-            const double boxb = (c.seg_pitch / ESZ <= 256 && !std::getenv("FCFS_NO_TMA")) ? 1.04 : 1.0;
+            const double boxb = (!sw && c.seg_pitch / ESZ <= 256 && !std::getenv("FCFS_NO_TMA")) ? 1.04 : 1.0;
             const double score =
                 util * boxb * (S >= 3 ? 1.0 : 0.9) * (Gf == 1 ? 1.0 : 0.97) - 0.001 * (double)c.ntile;
             if (score > best_score) {
@@ -331,7 +334,9 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     // one TMA box per segment and stage when the block is narrow enough (box dims <= 256)
     a.box_w = a.seg_pitch / ESZ;
     a.use_tmap = 0;
-    if (a.box_w <= 256 && a.SR <= 256 && !std::getenv("FCFS_NO_TMA") && g.in != nullptr)
+    a.sw_load = sw ? 1 : 0;
+    a.in_end = static_cast<const unsigned char *>(g.in) + g.planes * g.in_plane_stride * ESZ;
+    if (!sw && a.box_w <= 256 && a.SR <= 256 && !std::getenv("FCFS_NO_TMA") && g.in != nullptr)
         a.use_tmap = encode_input_map(pl, g, a, TZ) ? 1 : 0;
     std::snprintf(L.desc, sizeof(L.desc),
                   "{\"kernel\": \"fused_separable\", \"PY\": %d, \"QY\": %d, \"PX\": %d, \"QX\": %d, \"TZ\": %d, \"taps\": %d, "
@@ -389,7 +394,7 @@ int select_kernel(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
             g2.in_plane_stride = g.in_nrows * pl->W;
             g2.out_plane_stride = g.out_nrows * pl->Wo;
         }
-        if ((reinterpret_cast<uintptr_t>(g.in) & 15) ||
+        if ((reinterpret_cast<uintptr_t>(g.in) % esize(pl->dtype)) ||
             g2.planes * std::max(g2.D, g2.Do) * std::max(g.in_nrows * pl->W, g.out_nrows * pl->Wo) > INT32_MAX * 16LL || !plan_fused(pl, g2, L))
             kernel = (pl->pz == 1 && pl->qz == 1) ? 3 : 0;  // tiled when the slice factor allows it
     }
@@ -657,7 +662,7 @@ fcfs_status make_plan(int rank, const int *pd, const int *qd, int mode, int pad,
     if (!(flags & FCFS_FLAG_FORCE_REFERENCE)) {
         if (mode == FCFS_NEAREST) {
             pl->kernel = 1;
-        } else if ((pl->W * esize(dtype)) % 16 == 0 && pl->pz <= kZMax) {
+        } else if (pl->pz <= kZMax) {
             // separable fused kernel: rows by py/qy (1/1 for 1D rows), columns by
             // p/q; 3D plans with a slice factor other than 1/1 take the variants
             // that combine slice taps (run-time slice weights)

@@ -131,7 +131,7 @@ def test_kernel_selection(fc):
     assert fc.Plan(5, 3, "bicubic", "reflect", 1, 128, 128, "bfloat16").kernel == "fused_separable"
     assert fc.Plan(2, 3, "nearest", "zero", 1, 512, 512).kernel == "nearest_gather"
     assert fc.Plan(27, 11, "bicubic", "replicate", 1, 64, 64).kernel == "tiled"  # no fused variant
-    assert fc.Plan(3, 2, "bilinear", "replicate", 1, 64, 101).kernel == "tiled"  # row pitch not 16-B
+    assert fc.Plan(3, 2, "bilinear", "replicate", 1, 64, 101).kernel == "fused_separable"  # unaligned pitch: software row copies
     # 1D rows run the fused kernel with a 1/1 row factor (the "width-only" variants)
     assert fc.Plan(3, 2, "bilinear", "replicate", 1, 64, 64, is1d=True).kernel == "fused_separable"
     assert fc.Plan(3, 2, "bilinear", "replicate", 1, 64, 64, force_reference=True).kernel == "reference"
