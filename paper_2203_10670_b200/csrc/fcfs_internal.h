@@ -62,6 +62,7 @@ struct AdjArgs {         // adjoint kernel (k_adjoint.cu): grad_in = A^T grad_ou
     int pad, is1d;
     // tiled variant (2D / 1D rows; TH = 0: the per-element kernel)
     int TH, TW, K, nc_cap, gw_cap, grid, smem;
+    int R0, RH, C0, RW;  // the region of grad_in the tiled kernel writes (rows, columns)
 };
 
 // 32-bit division by a run-time invariant divisor (n < 2^31).
@@ -162,11 +163,17 @@ int launch_adjoint(int dtype, const AdjArgs &a, void *stream);
 // (x-periods per thread chunk) is reported.
 struct FusedVariant {
     const void *fn;
-    int PY, QY, PX, QX, TAPS, LO, K;
+    int PY, QY, PX, QX, TAPS, LO, K;  // the forward layer's factors and taps
     int TZ;                        // 1: 2D planes; TAPS: 3D (slice taps combined in the kernel)
-    const float *wtab_y, *wtab_x;  // the variant's compile-time phase weights, [4*j + t]
+    const float *wtab_y, *wtab_x;  // the forward layer's compile-time phase weights, [4*j + t]
+    int adj;                       // 1: the kernel runs the adjoint A^T of that layer
+    int ok;                        // 0: never selected (adjoint whose first tap passes the left margin)
+    // geometry the kernel runs (GeoSel): [0..3] rows P, Q, TAPS, LO; [4..7] columns;
+    // [8..23] rows' per-phase base offsets; [24..39] columns'
+    const int *geo;
 };
 const FusedVariant *fused_lookup(int dtype, int py, int qy, int px, int qx, int ntaps, bool slices);
+const FusedVariant *fused_lookup_adjoint(int dtype, int py, int qy, int px, int qx, int ntaps);
 int launch_fused(const FusedVariant *v, const FusedArgs &a, int grid, int block, int smem, void *stream);
 
 constexpr int kFusedConsumerWarps = 8;

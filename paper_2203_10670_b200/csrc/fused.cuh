@@ -150,44 +150,6 @@ struct GeoSel<P0, Q0, T0, LO0, true> {
     }
 };
 
-// Copy nbytes from src (any alignment of the element type, at least 2 B) to
-// dst (16-B aligned) with the 32 lanes of a warp: 16-B loads of the aligned
-// superset of the source, shifted into place in registers, 16-B stores (the
-// last chunk may write up to 15 bytes past nbytes: the row slot's margin).
-// Loads never pass `end` (the end of the source tensor).
-__device__ __forceinline__ void copy_realign(unsigned char *dst, const unsigned char *src, int nbytes, int lane,
-                                             const unsigned char *end) {
-    const uintptr_t s0 = reinterpret_cast<uintptr_t>(src);
-    const uintptr_t base = s0 & ~(uintptr_t)15;
-    const int d = (int)(s0 & 15), q = d >> 2, sh = 8 * (d & 3);
-    const int nchunk = (nbytes + 15) >> 4;
-    const uintptr_t e = reinterpret_cast<uintptr_t>(end);
-    for (int i = lane; i < nchunk; i += 32) {
-        const uintptr_t c0 = base + 16 * (uintptr_t)i;
-        uint4 lo = make_uint4(0, 0, 0, 0), hi = make_uint4(0, 0, 0, 0);
-        if (c0 + 16 <= e) lo = __ldg(reinterpret_cast<const uint4 *>(c0));
-        if (d != 0 && c0 + 32 <= e) hi = __ldg(reinterpret_cast<const uint4 *>(c0 + 16));
-        if (c0 + 16 > e || (d != 0 && c0 + 32 > e)) {  // the tensor's last bytes: word by word
-            uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int k = 0; k < 8; ++k)
-                if (c0 + 4 * k + 4 <= e) w[k] = *reinterpret_cast<const uint32_t *>(c0 + 4 * k);
-                else if (c0 + 4 * k + 2 <= e) w[k] = *reinterpret_cast<const unsigned short *>(c0 + 4 * k);
-            lo = make_uint4(w[0], w[1], w[2], w[3]);
-            hi = make_uint4(w[4], w[5], w[6], w[7]);
-        }
-        const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-        uint32_t a5[5];
-#pragma unroll
-        for (int k = 0; k < 5; ++k) a5[k] = q == 0 ? w[k] : q == 1 ? w[k + 1] : q == 2 ? w[k + 2] : w[k + 3];
-        uint4 o;
-        o.x = sh ? __funnelshift_r(a5[0], a5[1], sh) : a5[0];
-        o.y = sh ? __funnelshift_r(a5[1], a5[2], sh) : a5[1];
-        o.z = sh ? __funnelshift_r(a5[2], a5[3], sh) : a5[2];
-        o.w = sh ? __funnelshift_r(a5[3], a5[4], sh) : a5[3];
-        *reinterpret_cast<uint4 *>(dst + 16 * i) = o;
-    }
-}
-
 template <typename T> struct HalfBits;
 template <> struct HalfBits<__half> {
     static __device__ __forceinline__ float f(uint32_t b) { return __half2float(__ushort_as_half((unsigned short)b)); }
@@ -342,6 +304,32 @@ struct StageCursor {
     }
 };
 
+// Software-aligned rows (FusedArgs::sw_load).  sw_src: the address of element
+// a0 of virtual row v (slice sl) of segment sg, false for a zero-padding row or
+// slice; rows outside the window are clamped (they only feed masked outputs).
+template <typename T>
+__device__ __forceinline__ bool sw_src_t(const FusedArgs &a, const SegGeo &sg, int v, int sl, int tz_taps,
+                                         const unsigned char *&src0) {
+    if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) return false;
+    int64_t soff = 0;
+    if (tz_taps > 1) {
+        if (a.pad == FCFS_PAD_ZERO && (sl < 0 || sl >= a.D)) return false;
+        soff = (int64_t)min(max(pad_src32(sl, a.D, a.pad), 0), a.D - 1) * a.in_slice_stride;
+    }
+    const int src = min(max(pad_src32(v, a.H, a.pad) - a.in_row0, 0), a.in_nrows - 1);
+    src0 = reinterpret_cast<const unsigned char *>(static_cast<const T *>(a.in) + (int64_t)sg.plane * a.in_plane_stride +
+                                                   soff + (int64_t)src * a.W + sg.a0);
+    return true;
+}
+// bytes of the 16-B-aligned superset of [src0, src0 + nbytes), never past the
+// input's end (a truncated tail is completed by aligned_row)
+__device__ __forceinline__ uint32_t aligned_row_bytes(const FusedArgs &a, const unsigned char *src0, int nbytes) {
+    const uintptr_t s0 = reinterpret_cast<uintptr_t>(src0), base = s0 & ~(uintptr_t)15;
+    uintptr_t end = (s0 + nbytes + 15) & ~(uintptr_t)15;
+    const uintptr_t lim = reinterpret_cast<uintptr_t>(a.in_end) & ~(uintptr_t)15;
+    if (end > lim) end = lim > base ? lim : base;
+    return (uint32_t)(end - base);
+}
 // first input slice b_z + lo of output slice mz (3D variants)
 __device__ __forceinline__ int slice_base(const FusedArgs &a, int mz, int lo) {
     const int jz = mz % a.pz;
@@ -372,6 +360,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         return;  // adjoint geometry whose first tap reaches past the left margin: never selected (variant ok = 0)
     } else {
 
+    auto sw_src = [&](const FusedArgs &fa, const SegGeo &sg, int v, int sl, const unsigned char *&src0) {
+        return sw_src_t<T>(fa, sg, v, sl, TZ, src0);
+    };
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);   // TMA landed       (count 1 + tx)
     uint64_t *ready = full + 8;                             // padding written  (count 32)
@@ -399,41 +390,43 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         ci.start(a);
         while (ci.task < a.ntasks) {
             if (a.sw_load) {
-                // software copy (rows whose pitch or start is not 16-B aligned): the
-                // warp copies each (row, slice) sub-row's columns [a0, a1) into the
-                // stage with 16-B loads of the aligned superset, realigned in registers
+                // rows whose pitch or start is not 16-B aligned: each (row, slice)
+                // sub-row's 16-B-aligned superset lands 16 B into its row slot by a
+                // bulk copy; the padding warp then shifts it into place (aligned_row)
                 if (ci.seq >= (uint32_t)a.S) mbar_wait(&empty[ci.slot], ci.phase ^ 1);
                 int vf, nr;
                 ci.rows(vf, nr);
-                for (int s = 0; s < ci.b.nsg; ++s) {
-                    const SegGeo sg = seg_geo<GX, K, ESZ>(a, ci.b.group * a.NS + s);
-                    int z0 = 0;
+                SegGeo sg;
+                int z0 = 0;
+                uint32_t tot = 0;
+                if (lane < ci.b.nsg) {
+                    sg = seg_geo<GX, K, ESZ>(a, ci.b.group * a.NS + lane);
                     if constexpr (TZ > 1) z0 = slice_base(a, sg.mz, LO0);
-                    const int nbytes = (sg.a1 - sg.a0) * ESZ;
-                    for (int r = 0; r < nr; ++r) {
-                        const int v = vf + r;
-                        if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;  // zeroed by warp 1
-                        const int src = min(max(pad_src32(v, a.H, a.pad) - a.in_row0, 0), a.in_nrows - 1);
+                    for (int r = 0; r < nr; ++r)
 #pragma unroll
                         for (int tz = 0; tz < TZ; ++tz) {
-                            int64_t soff = 0;
-                            if constexpr (TZ > 1) {
-                                const int sl = z0 + tz;
-                                if (a.pad == FCFS_PAD_ZERO && (sl < 0 || sl >= a.D)) continue;
-                                soff = (int64_t)min(max(pad_src32(sl, a.D, a.pad), 0), a.D - 1) * a.in_slice_stride;
-                            }
-                            const unsigned char *src0 = reinterpret_cast<const unsigned char *>(
-                                static_cast<const T *>(a.in) + (int64_t)sg.plane * a.in_plane_stride + soff +
-                                (int64_t)src * a.W + sg.a0);
-                            unsigned char *dst = stages + ci.slot * a.stage_bytes + A * ESZ + s * a.seg_block +
-                                                 r * a.row_pitch + tz * a.slice_pitch;
-                            copy_realign(dst, src0, nbytes, lane, static_cast<const unsigned char *>(a.in_end));
+                            const unsigned char *src0;
+                            if (sw_src(a, sg, vf + r, z0 + tz, src0)) tot += aligned_row_bytes(a, src0, (sg.a1 - sg.a0) * ESZ);
                         }
-                    }
                 }
-                __threadfence_block();  // every lane's stage stores before the release below
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+                if (lane == 0) mbar_arrive_expect_tx(&full[ci.slot], tot);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&full[ci.slot]);  // release: the stage's rows are written
+                if (lane < ci.b.nsg) {
+                    for (int r = 0; r < nr; ++r)
+#pragma unroll
+                        for (int tz = 0; tz < TZ; ++tz) {
+                            const unsigned char *src0;
+                            if (!sw_src(a, sg, vf + r, z0 + tz, src0)) continue;
+                            const uint32_t bytes = aligned_row_bytes(a, src0, (sg.a1 - sg.a0) * ESZ);
+                            if (bytes == 0) continue;
+                            unsigned char *dst = stages + ci.slot * a.stage_bytes + lane * a.seg_block + r * a.row_pitch +
+                                                 tz * a.slice_pitch + 16;
+                            bulk_g2s(dst, reinterpret_cast<const void *>(reinterpret_cast<uintptr_t>(src0) & ~(uintptr_t)15),
+                                     bytes, &full[ci.slot], pol);
+                        }
+                }
                 __syncwarp();
                 ci.next(a);
             } else {
@@ -512,6 +505,80 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 int vf, nr;
                 cf.rows(vf, nr);
                 unsigned char *sbase = stages + cf.slot * a.stage_bytes;
+                if (a.sw_load) {  // shift every sub-row's aligned superset into place, 4 sub-rows per pass
+                    const int nsub = cf.b.nsg * nr * TZ;
+                    for (int g0 = 0; g0 < nsub; g0 += 4) {
+                        unsigned char *rowp[4];
+                        const unsigned char *srcp[4];
+                        int nb[4], dd[4];
+                        uint32_t len[4];
+                        bool ok[4];
+                        int maxch = 0;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int id = g0 + u;
+                            ok[u] = false;
+                            nb[u] = 0;
+                            dd[u] = 0;
+                            len[u] = 0;
+                            rowp[u] = nullptr;
+                            srcp[u] = nullptr;
+                            if (id < nsub) {
+                                const int sidx = id / (nr * TZ), rz = id - sidx * (nr * TZ), r = rz / TZ, tz = rz - r * TZ;
+                                const SegGeo sg = seg_geo<GX, K, ESZ>(a, cf.b.group * a.NS + sidx);
+                                int z0 = 0;
+                                if constexpr (TZ > 1) z0 = slice_base(a, sg.mz, LO0);
+                                const unsigned char *src0;
+                                if (sw_src(a, sg, vf + r, z0 + tz, src0)) {
+                                    ok[u] = true;
+                                    nb[u] = (sg.a1 - sg.a0) * ESZ;
+                                    srcp[u] = src0;
+                                    dd[u] = (int)(reinterpret_cast<uintptr_t>(src0) & 15);
+                                    len[u] = aligned_row_bytes(a, src0, nb[u]);
+                                    rowp[u] = sbase + sidx * a.seg_block + r * a.row_pitch + tz * a.slice_pitch;
+                                    maxch = max(maxch, (nb[u] + 15) >> 4);
+                                }
+                            }
+                        }
+                        for (int c0 = 0; c0 < maxch; c0 += 32) {  // left to right: read a pass, then write it
+                            uint4 o[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int c = c0 + lane;
+                                o[u] = make_uint4(0, 0, 0, 0);
+                                if (ok[u] && dd[u] != 0 && c < ((nb[u] + 15) >> 4)) {
+                                    const uint4 lo = *reinterpret_cast<const uint4 *>(rowp[u] + 16 + 16 * c);
+                                    const uint4 hi = *reinterpret_cast<const uint4 *>(rowp[u] + 32 + 16 * c);
+                                    const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+                                    const int q = dd[u] >> 2, sh = 8 * (dd[u] & 3);
+                                    uint32_t a5[5];
+#pragma unroll
+                                    for (int k = 0; k < 5; ++k)
+                                        a5[k] = q == 0 ? w[k] : q == 1 ? w[k + 1] : q == 2 ? w[k + 2] : w[k + 3];
+                                    o[u].x = sh ? __funnelshift_r(a5[0], a5[1], sh) : a5[0];
+                                    o[u].y = sh ? __funnelshift_r(a5[1], a5[2], sh) : a5[1];
+                                    o[u].z = sh ? __funnelshift_r(a5[2], a5[3], sh) : a5[2];
+                                    o[u].w = sh ? __funnelshift_r(a5[3], a5[4], sh) : a5[3];
+                                }
+                            }
+                            __syncwarp();
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int c = c0 + lane;
+                                if (ok[u] && dd[u] != 0 && c < ((nb[u] + 15) >> 4))
+                                    *reinterpret_cast<uint4 *>(rowp[u] + 16 + 16 * c) = o[u];
+                            }
+                            __syncwarp();
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)  // a truncated tail (the input's last row): 2-byte reads
+                            if (ok[u])
+                                for (int bb = max((int)len[u] - dd[u], 0) + 2 * lane; bb < nb[u]; bb += 64)
+                                    *reinterpret_cast<unsigned short *>(rowp[u] + 16 + bb) =
+                                        *reinterpret_cast<const unsigned short *>(srcp[u] + bb);
+                        __syncwarp();
+                    }
+                }
                 const int pairs = cf.b.nsg * nr * TZ;  // (segment, row, slice) sub-rows
                 const int n16 = a.seg_pitch / 16;
                 if constexpr (TZ == 1) {

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_con
     float *gw = reinterpret_cast<float *>(ext + 4); // [NRcap][NCcap] window
     float *hx = gw + a.gw_cap;                      // [TH][NCcap] row-pass buffer
     const int H = (int)a.H, W = (int)a.W, Ho = (int)a.Ho, Wo = (int)a.Wo;
-    const int tiles_y = (H + TH - 1) / TH, tiles_x = (W + TW - 1) / TW;
+    const int tiles_y = (a.RH + TH - 1) / TH, tiles_x = (a.RW + TW - 1) / TW;  // tiles of the region
     const int ngeom = tiles_y * tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // CTA b keeps the tile geometry b % ngeom (its pair lists are computed once)
@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_con
     const int geom = blockIdx.x % ngeom, pstep = max(1, (int)gridDim.x / ngeom);
     if (blockIdx.x >= pstep * ngeom) return;
     const int tx_i = geom % tiles_x, ty_i = geom / tiles_x;
-    const int r0 = ty_i * TH, r1 = min(r0 + TH, H), c0 = tx_i * TW, c1 = min(c0 + TW, W);
+    const int r0 = a.R0 + ty_i * TH, r1 = min(r0 + TH, a.R0 + a.RH), c0 = a.C0 + tx_i * TW,
+              c1 = min(c0 + TW, a.C0 + a.RW);
     const int NH = r1 - r0, NW = c1 - c0;
     if (threadIdx.x == 0) {
         ext[0] = INT32_MAX;

@@ -6,5 +6,5 @@
 #define V_H(P, Q) FCFS_BOTH_MODES(__nv_bfloat16, P, Q, 8, 8)
 #define V_Z(P, Q) FCFS_BOTH_MODES_Z(__nv_bfloat16, P, Q, P, Q)
 namespace fcfs {
-extern const FusedVariant kFusedVariants_bf16_w[] = {FCFS_W_X(V){nullptr, 0, 0, 0, 0, 0, 0, 0, 0, nullptr, nullptr}};
+extern const FusedVariant kFusedVariants_bf16_w[] = {FCFS_W_X(V){nullptr, 0, 0, 0, 0, 0, 0, 0, 0, nullptr, nullptr, 0, 0, nullptr}};
 }  // namespace fcfs

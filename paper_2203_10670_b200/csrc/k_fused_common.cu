@@ -15,6 +15,16 @@ extern const FusedVariant kFusedVariants_f16_iso[], kFusedVariants_f16_w[], kFus
     kFusedVariants_f16_z[];
 extern const FusedVariant kFusedVariants_bf16_iso[], kFusedVariants_bf16_w[], kFusedVariants_bf16_h[],
     kFusedVariants_bf16_z[];
+extern const FusedVariant kFusedVariants_f32_adj[], kFusedVariants_f16_adj[], kFusedVariants_bf16_adj[];
+
+// The adjoint (backward pass) variant of the 2D layer (py/qy, px/qx): exact factors.
+const FusedVariant *fused_lookup_adjoint(int dtype, int py, int qy, int px, int qx, int ntaps) {
+    const FusedVariant *sets[3] = {kFusedVariants_f32_adj, kFusedVariants_f16_adj, kFusedVariants_bf16_adj};
+    if (dtype < 0 || dtype > 2) return nullptr;
+    for (const FusedVariant *v = sets[dtype]; v->fn; ++v)
+        if (v->ok && v->PY == py && v->QY == qy && v->PX == px && v->QX == qx && v->TAPS == ntaps) return v;
+    return nullptr;
+}
 
 // A variant's factor serves a plan's reduced factor p/q when they are equal, or
 // when p/q = 1/1 and the variant uses an unreduced identity R/R (R outputs per

@@ -1,0 +1,7 @@
+// Fused separable FCFS kernels: element type __half, the adjoint (backward pass) set (fused_pairs.h).
+#include "fused_inst.cuh"
+
+#define V_ADJ(P, Q) FCFS_BOTH_MODES_ADJ(__half, P, Q, P, Q)
+namespace fcfs {
+extern const FusedVariant kFusedVariants_f16_adj[] = {FCFS_ADJ_X(V){nullptr, 0, 0, 0, 0, 0, 0, 0, 0, nullptr, nullptr, 0, 0, nullptr}};
+}  // namespace fcfs

@@ -6,5 +6,5 @@
 #define V_H(P, Q) FCFS_BOTH_MODES(float, P, Q, 8, 8)
 #define V_Z(P, Q) FCFS_BOTH_MODES_Z(float, P, Q, P, Q)
 namespace fcfs {
-extern const FusedVariant kFusedVariants_f32_h[] = {FCFS_H_X(V){nullptr, 0, 0, 0, 0, 0, 0, 0, 0, nullptr, nullptr}};
+extern const FusedVariant kFusedVariants_f32_h[] = {FCFS_H_X(V){nullptr, 0, 0, 0, 0, 0, 0, 0, 0, nullptr, nullptr, 0, 0, nullptr}};
 }  // namespace fcfs

@@ -193,18 +193,27 @@ bool encode_input_map(const fcfs_plan_s *pl, const RunGeom &g, FusedArgs &a, int
     return r == CUDA_SUCCESS;
 }
 
-bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
-    const FusedVariant *v = pl->fused;
-    const int PY = v->PY, QY = v->QY, PX = v->PX, QX = v->QX, K = v->K, TAPS = v->TAPS, LO = v->LO, TZ = v->TZ;
+// v: the variant (default the plan's); pad: the input's padding mode (the
+// adjoint's input, grad_out, is zero outside the forward extent).
+bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L, const FusedVariant *v = nullptr,
+                int pad = -1) {
+    if (!v) v = pl->fused;
+    if (pad < 0) pad = pl->pad;
+    // geometry the kernel runs (forward, or the adjoint's polyphase form): FusedVariant::geo
+    const int *geo = v->geo;
+    const int PY = geo[0], QY = geo[1], TY = geo[2], LOY = geo[3];
+    const int PX = geo[4], QX = geo[5], TX = geo[6], LOX = geo[7];
+    const int K = v->K, TZ = v->TZ;
     const int ESZ = esize(pl->dtype), A = 16 / ESZ;
     // y-period window (rows): L rows, C carried to the next period, F fresh
-    const int HIy = ((PY - 1) * QY) / PY + LO + TAPS - 1;
-    const int Ly = HIy - LO + 1;
+    int HIy = -(1 << 30), HIx = -(1 << 30);
+    for (int j = 0; j < PY; ++j) HIy = std::max(HIy, geo[8 + j] + TY - 1 + LOY);
+    for (int j = 0; j < PX; ++j) HIx = std::max(HIx, geo[24 + j] + TX - 1 + LOX);
+    const int Ly = HIy - LOY + 1;
     const int Cc = Ly > QY ? Ly - QY : 0;
     const int Ff = Ly - Cc;
     // x-period window (columns)
-    const int HIx = ((PX - 1) * QX) / PX + LO + TAPS - 1;
-    const int Lw = HIx - LO + 1;
+    const int Lw = HIx - LOX + 1;
     const int NT = 32 * kFusedConsumerWarps;
     const int KP = K * PX;
     FusedArgs &a = L.a;
@@ -222,7 +231,7 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     a.out_row0 = (int32_t)g.out_row0;
     a.out_nrows = (int32_t)g.out_nrows;
     a.planes = (int32_t)g.planes;
-    a.pad = pl->pad;
+    a.pad = pad;
     a.D = (int32_t)g.D;
     a.Do = (int32_t)g.Do;
     a.pz = a.qz = 1;
@@ -241,9 +250,10 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     const int WIN = (K - 1) * QX + Lw;
     // right margin: every window read stays inside the row slot (allocation);
     // only the columns kept outputs' own taps reach are written (rfix)
-    const int64_t reach_all = (int64_t)(a.nch - 1) * K * QX + LO + WIN;  // one past the last window column
+    const int64_t reach_all = (int64_t)(a.nch - 1) * K * QX + LOX + WIN;  // one past the last window column
     const int64_t ralloc = std::max<int64_t>(0, reach_all - g.W);
-    const int64_t reach_kept = ((g.Wo - 1) * QX) / PX + LO + TAPS;     // one past the last kept tap
+    const int64_t reach_kept =  // one past the last kept output's last tap
+        ((g.Wo - 1) / PX) * QX + LOX + geo[24 + (int)((g.Wo - 1) % PX)] + TX;
     a.rfix = (int32_t)std::max<int64_t>(0, std::min<int64_t>(reach_kept - g.W, ralloc));
     const int budget = 110 * 1024;              // two CTAs per SM
     // shared row: [A-element margin][loaded columns][right margin], 16-B multiple
@@ -252,7 +262,7 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     const bool sw = ((g.W * ESZ) % 16 != 0) || (reinterpret_cast<uintptr_t>(g.in) & 15) != 0;
     auto seg_pitch_for = [&](int cpt) {
         int64_t elems = std::min<int64_t>(g.W, (int64_t)cpt * K * QX - QX + Lw + 2 * A);
-        elems = (elems + A - 1) / A * A + A + (ralloc + A - 1) / A * A + (sw ? A : 0);
+        elems = (elems + A - 1) / A * A + A + (ralloc + A - 1) / A * A + (sw ? 2 * A : 0);
         return (int)(elems * ESZ);
     };
     // geometry search: segments of CPT chunks (one plane x one column tile), NS
@@ -344,10 +354,10 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
                   "\"CPT\": %d, \"nch\": %d, \"ntile\": %d, \"nseg\": %d, \"S\": %d, \"SR\": %d, \"seg_pitch\": %d, "
                   "\"stage_bytes\": %d, \"out_pitch\": %d, \"slot_bytes\": %d, \"rfix\": %d, \"periods\": %d, "
                   "\"PB\": %d, \"nbands\": %d, \"ntasks\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, "
-                  "\"busy_threads\": %d, \"flush_groups\": %d, \"tma_box\": %d}",
-                  PY, QY, PX, QX, TZ, TAPS, K, a.NS, a.CPT, a.nch, a.ntile, a.nseg, a.S, a.SR, a.seg_pitch, a.stage_bytes,
+                  "\"busy_threads\": %d, \"flush_groups\": %d, \"tma_box\": %d, \"tma\": %d}",
+                  PY, QY, PX, QX, TZ, TX, K, a.NS, a.CPT, a.nch, a.ntile, a.nseg, a.S, a.SR, a.seg_pitch, a.stage_bytes,
                   a.out_pitch, a.slot_bytes, a.rfix, nper, a.PB, a.nbands, a.ntasks, L.grid, kFusedThreads, L.smem,
-                  a.NS * a.CPT, a.G, (a.box_w <= 256 && a.SR <= 256) ? a.box_w : 0);
+                  a.NS * a.CPT, a.G, (a.box_w <= 256 && a.SR <= 256) ? a.box_w : 0, a.use_tmap);
     if (std::getenv("FCFS_DEBUG_PRINT")) std::fprintf(stderr, "%s\n", L.desc);
     return true;
 }
@@ -917,10 +927,15 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
     a.pad = pl->pad;
     a.is1d = pl->is1d;
     a.TH = a.TW = 0;
-    // tiled variant for 2D planes / 1D rows when every pair list fits
+    a.R0 = a.C0 = 0;
+    a.RH = (int)std::min<int64_t>(pl->H, INT32_MAX);
+    a.RW = (int)std::min<int64_t>(pl->W, INT32_MAX);
+    // tiled kernel over the region (R0, RH, C0, RW) when every pair list fits
     const int kx = adj_max_pairs(pl->tab, pl->W, pl->Wo, pl->pad);
     const int ky = pl->is1d ? 1 : adj_max_pairs(pl->taby, pl->H, pl->Ho, pl->pad);
-    if (pl->D == 1 && std::max(kx, ky) <= 32 && pl->H < INT32_MAX / 64 && pl->W < INT32_MAX / 64) {
+    const bool tiled_ok = pl->D == 1 && std::max(kx, ky) <= 32 && pl->H < INT32_MAX / 64 && pl->W < INT32_MAX / 64;
+    auto plan_tiles = [&](AdjArgs &b) {
+        b.TH = b.TW = 0;
         const int K = std::max(1, std::max(kx, ky));
         const int T = pl->tab.ntaps;
         auto span = [&](int n, int p, int q) { return (int)(((int64_t)(n + 2 * T + 2) * p + q - 1) / q + p + 2); };
@@ -932,7 +947,7 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
                 const int64_t bytes = (int64_t)(TW + TH) * K * 8 + (TW + TH) * 4 + 16 +
                                       4 * ((int64_t)NR * NC + (int64_t)TH * NC);
                 if (bytes > 100 * 1024) continue;
-                const int THe = (int)std::min<int64_t>(TH, pl->H), TWe = (int)std::min<int64_t>(TW, pl->W);
+                const int THe = std::min(TH, b.RH), TWe = std::min(TW, b.RW);
                 if ((int64_t)THe * TWe > (int64_t)bTH * bTW) {
                     bTH = THe;
                     bTW = TWe;
@@ -940,20 +955,85 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
                     bNC = NC;
                 }
             }
-        if (bTH > 0) {
-            a.K = K;
-            a.TH = bTH;
-            a.TW = bTW;
-            a.nc_cap = bNC;
-            a.gw_cap = bNR * bNC;
-            a.smem = (bTW + bTH) * K * 8 + (bTW + bTH) * 4 + 32 + 4 * (a.gw_cap + bTH * bNC);
-            const int64_t ngeom = ((pl->H + bTH - 1) / bTH) * ((pl->W + bTW - 1) / bTW);
-            const int64_t target = (int64_t)pl->sm_count * 2;
-            const int64_t pstep = std::max<int64_t>(1, std::min<int64_t>(planes, target / std::max<int64_t>(1, ngeom)));
-            if (ngeom * pstep > INT32_MAX) a.TH = a.TW = 0;
-            else a.grid = (int)(ngeom * pstep);
+        if (bTH == 0) return;
+        b.K = K;
+        b.TH = bTH;
+        b.TW = bTW;
+        b.nc_cap = bNC;
+        b.gw_cap = bNR * bNC;
+        b.smem = (bTW + bTH) * K * 8 + (bTW + bTH) * 4 + 32 + 4 * (b.gw_cap + bTH * bNC);
+        const int64_t ngeom = (int64_t)((b.RH + bTH - 1) / bTH) * ((b.RW + bTW - 1) / bTW);
+        // resident CTAs: shared memory (227 KB per SM) and 2048 threads per SM
+        const int per_sm = std::max(1, std::min(8, (227 * 1024) / (b.smem + 1024)));
+        const int64_t target = (int64_t)pl->sm_count * per_sm;
+        const int64_t pstep = std::max<int64_t>(1, std::min<int64_t>(planes, target / std::max<int64_t>(1, ngeom)));
+        if (ngeom * pstep > INT32_MAX) b.TH = b.TW = 0;
+        else b.grid = (int)(ngeom * pstep);
+    };
+    // 2D: the fused kernel runs A^T's polyphase form over grad_out (zero outside
+    // the forward extent) -- exact wherever no padding image folds in; the
+    // replicate / reflect border bands are then rewritten by the tiled kernel
+    const FusedVariant *v = nullptr;
+    if (pl->mode != FCFS_NEAREST && pl->D == 1 && !pl->is1d && !(pl->flags & FCFS_FLAG_FORCE_REFERENCE) &&
+        !std::getenv("FCFS_NO_FUSED_ADJOINT"))
+        v = fused_lookup_adjoint(pl->dtype, pl->py, pl->qy, pl->p, pl->q, pl->tab.ntaps);
+    // grad_out rows that are not 16-B aligned would take the fused kernel's
+    // software-realigned load path, slower than the tiled kernel
+    const bool go_aligned = (pl->Wo * ESZ) % 16 == 0 && (reinterpret_cast<uintptr_t>(grad_out) & 15) == 0;
+    if (v && (tiled_ok || pl->pad == FCFS_PAD_ZERO) && (go_aligned || !tiled_ok || std::getenv("FCFS_FUSED_ADJOINT_SW"))) {
+        RunGeom g;
+        g.in = grad_out;
+        g.out = grad_in;
+        g.planes = planes;
+        g.D = g.Do = 1;
+        g.H = pl->Ho;
+        g.W = pl->Wo;
+        g.Ho = pl->H;
+        g.Wo = pl->W;
+        g.in_row0 = 0;
+        g.in_nrows = pl->Ho;
+        g.out_row0 = 0;
+        g.out_nrows = pl->H;
+        g.in_plane_stride = pl->Ho * pl->Wo;
+        g.out_plane_stride = pl->H * pl->W;
+        FusedLaunch L;
+        if (planes * std::max(pl->Ho * pl->Wo, pl->H * pl->W) <= INT32_MAX * 16LL &&
+            plan_fused(pl, g, L, v, FCFS_PAD_ZERO)) {
+            if (launch_fused(v, L.a, L.grid, kFusedThreads, L.smem, stream) != 0) return FCFS_E_CUDA;
+            if (pl->pad == FCFS_PAD_ZERO || std::getenv("FCFS_DEBUG_NO_BANDS")) return FCFS_OK;
+            // border bands: indices that receive padding images (Z21)
+            auto bands = [&](const PhaseTable &t, int64_t n, int64_t no, int64_t &bl, int64_t &br) {
+                const int64_t vmin = t.lo, vmax = ((no - 1) / t.p) * t.q + t.base[(no - 1) % t.p] + t.lo + t.ntaps - 1;
+                bl = vmin < 0 ? std::min<int64_t>(n, -vmin + 1) : 0;
+                br = vmax > n - 1 ? std::min<int64_t>(n, vmax - n + 2) : 0;
+            };
+            int64_t bly, bry, blx, brx;
+            bands(pl->taby, pl->H, pl->Ho, bly, bry);
+            bands(pl->tab, pl->W, pl->Wo, blx, brx);
+            struct Region { int64_t r0, rh, c0, rw; };
+            Region regs[4];
+            int nreg = 0;
+            if (bly + bry >= pl->H || blx + brx >= pl->W) {
+                regs[nreg++] = {0, pl->H, 0, pl->W};
+            } else {
+                if (bly) regs[nreg++] = {0, bly, 0, pl->W};
+                if (bry) regs[nreg++] = {pl->H - bry, bry, 0, pl->W};
+                if (blx) regs[nreg++] = {bly, pl->H - bly - bry, 0, blx};
+                if (brx) regs[nreg++] = {bly, pl->H - bly - bry, pl->W - brx, brx};
+            }
+            for (int i = 0; i < nreg; ++i) {
+                AdjArgs b = a;
+                b.R0 = (int)regs[i].r0;
+                b.RH = (int)regs[i].rh;
+                b.C0 = (int)regs[i].c0;
+                b.RW = (int)regs[i].rw;
+                plan_tiles(b);
+                if (launch_adjoint(pl->dtype, b, stream) != 0) return FCFS_E_CUDA;
+            }
+            return FCFS_OK;
         }
     }
+    if (tiled_ok) plan_tiles(a);
     return launch_adjoint(pl->dtype, a, stream) == 0 ? FCFS_OK : FCFS_E_CUDA;
 }
 

@@ -21,7 +21,14 @@ def time_cfg(name, reps, env):
     for k in [k for k in os.environ if k.startswith("FCFS_DEBUG_") or k.startswith("FCFS_NO_")]:
         del os.environ[k]
     os.environ.update(env)
+    import dataclasses
+    hw = None
+    if "@" in name:  # NAME@HxW: the config at another image size (2D configs)
+        name, hw = name.split("@")
     c = synth.CONFIGS[name]
+    if hw:
+        h, w = (int(v) for v in hw.split("x"))
+        c = dataclasses.replace(c, H=h, W=w)
     if c.nd:
         pl = fc.Plan.nd(c.pd, c.qd, c.mode, c.pad, c.C, c.dims, c.dtype, "floor")
     else:
