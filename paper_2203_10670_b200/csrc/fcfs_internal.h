@@ -61,8 +61,14 @@ struct AdjArgs {         // adjoint kernel (k_adjoint.cu): grad_in = A^T grad_ou
     PhaseTable tx, ty, tz;
     int pad, is1d;
     // tiled variant (2D / 1D rows; TH = 0: the per-element kernel)
-    int TH, TW, K, nc_cap, gw_cap, grid, smem;
+    int TH, TW, K, nc_cap, gw_cap, grid, smem, PB;
     int R0, RH, C0, RW;  // the region of grad_in the tiled kernel writes (rows, columns)
+    // several regions in one tiled launch (border bands): region k owns CTAs
+    // [cta0, cta0 + ncta) with its own tile geometry; nreg = 0: the fields above
+    struct Region {
+        int R0, RH, C0, RW, TH, TW, nc_cap, gw_cap, cta0, ncta, PB;  // PB: planes per CTA iteration
+    } reg[4];
+    int nreg;
 };
 
 // 32-bit division by a run-time invariant divisor (n < 2^31).

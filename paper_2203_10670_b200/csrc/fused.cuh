@@ -369,6 +369,11 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     uint64_t *empty = full + 16;                            // consumers done   (count 8 warps)
     unsigned char *stages = smem + 256;
     unsigned char *obuf = stages + a.S * a.stage_bytes + 128;
+    // adjoint variants with unaligned rows (sw_load): the consumers read every
+    // sub-row where its aligned superset landed, shifted by dtab's element count
+    // (slot, segment, row) -- no realignment pass (TZ == 1)
+    constexpr bool kShift = ADJ && TZ == 1;
+    unsigned char *dtab = obuf + 2 * a.slot_bytes;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -406,7 +411,11 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
 #pragma unroll
                         for (int tz = 0; tz < TZ; ++tz) {
                             const unsigned char *src0;
-                            if (sw_src(a, sg, vf + r, z0 + tz, src0)) tot += aligned_row_bytes(a, src0, (sg.a1 - sg.a0) * ESZ);
+                            const bool real = sw_src(a, sg, vf + r, z0 + tz, src0);
+                            if (real) tot += aligned_row_bytes(a, src0, (sg.a1 - sg.a0) * ESZ);
+                            if constexpr (kShift)
+                                dtab[(ci.slot * a.NS + lane) * a.SR + r] =
+                                    real ? (unsigned char)((reinterpret_cast<uintptr_t>(src0) & 15) / ESZ) : 0;
                         }
                 }
 #pragma unroll
@@ -505,7 +514,22 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 int vf, nr;
                 cf.rows(vf, nr);
                 unsigned char *sbase = stages + cf.slot * a.stage_bytes;
-                if (a.sw_load) {  // shift every sub-row's aligned superset into place, 4 sub-rows per pass
+                if (kShift && a.sw_load) {
+                    // a truncated tail (the input's last row): the bytes past the
+                    // last aligned 16 B, with 2-byte reads
+                    for (int u = lane; u < cf.b.nsg * nr; u += 32) {
+                        const int sidx = u / nr, r = u - sidx * nr;
+                        const SegGeo sg = seg_geo<GX, K, ESZ>(a, cf.b.group * a.NS + sidx);
+                        const unsigned char *src0;
+                        if (!sw_src(a, sg, vf + r, 0, src0)) continue;
+                        const int nb = (sg.a1 - sg.a0) * ESZ, d = (int)(reinterpret_cast<uintptr_t>(src0) & 15);
+                        const int len = (int)aligned_row_bytes(a, src0, nb);
+                        unsigned char *rowp = sbase + sidx * a.seg_block + r * a.row_pitch + 16 + d;
+                        for (int bb = max(len - d, 0); bb < nb; bb += 2)
+                            *reinterpret_cast<unsigned short *>(rowp + bb) = *reinterpret_cast<const unsigned short *>(src0 + bb);
+                    }
+                    __syncwarp();
+                } else if (a.sw_load) {  // shift every sub-row's aligned superset into place, 4 sub-rows per pass
                     const int nsub = cf.b.nsg * nr * TZ;
                     for (int g0 = 0; g0 < nsub; g0 += 4) {
                         unsigned char *rowp[4];
@@ -609,6 +633,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                         }
                     }
                     T *row = reinterpret_cast<T *>(sub) + A - sg.a0;  // row[c]
+                    if constexpr (kShift)
+                        if (a.sw_load) row += dtab[(cf.slot * a.NS + s) * a.SR + r];
                     if (sg.a0 == 0) {
 #pragma unroll
                         for (int c = LOX; c < 0; ++c) {
@@ -698,9 +724,14 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
 
         // horizontal taps of one window row into a ring slot
         // (zero-padding rows arrive as zeros: +0 for every tap, as in the reference kernel)
-        auto row_h = [&](float(&h)[KP], const unsigned char *srow) {
+        auto row_h = [&](float(&h)[KP], const unsigned char *srow, int sl, int ridx) {
             float win[WIN];
-            if constexpr (TZ == 1) {
+            if constexpr (kShift) {
+                if (a.sw_load)
+                    load_win<T, WIN, -1>(reinterpret_cast<const T *>(srow), e0 + dtab[(sl * a.NS + sgi) * a.SR + ridx], win);
+                else
+                    load_win<T, WIN, PAR>(reinterpret_cast<const T *>(srow), e0, win);
+            } else if constexpr (TZ == 1) {
                 load_win<T, WIN, PAR>(reinterpret_cast<const T *>(srow), e0, win);
             } else {
                 // slice taps first (contract: slices, columns, rows): the TZ
@@ -761,7 +792,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             if (active) {
                 const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
 #pragma unroll
-                for (int i = 0; i < C; ++i) row_h(hr[i % TY], sb + i * a.row_pitch);
+                for (int i = 0; i < C; ++i) row_h(hr[i % TY], sb + i * a.row_pitch, slot, i);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
@@ -891,7 +922,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             const unsigned char *sb = stages + slot * a.stage_bytes + in_off;
 #pragma unroll
             for (int r = C; r < L; ++r) {
-                if (active) row_h(hr[(RO + r) % TY], sb + (r - C) * a.row_pitch);
+                if (active) row_h(hr[(RO + r) % TY], sb + (r - C) * a.row_pitch, slot, r - C);
 #pragma unroll
                 for (int jy = 0; jy < PY; ++jy) {
                     if (GY::last_row(jy) == r) {

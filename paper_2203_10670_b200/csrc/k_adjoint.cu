@@ -103,7 +103,14 @@ __device__ __forceinline__ int adj_list(const PhaseTable &t, int i, int n, int n
 template <typename T, int kAdjKMax>
 __global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_constant__ AdjArgs a) {
     extern __shared__ __align__(16) float asm_[];
-    const int TH = a.TH, TW = a.TW, kAdjK = a.K;
+    int rk = 0;  // this CTA's region
+    while (rk + 1 < a.nreg && (int)blockIdx.x >= a.reg[rk + 1].cta0) ++rk;
+    const AdjArgs::Region R = a.nreg ? a.reg[rk]
+                                     : AdjArgs::Region{a.R0, a.RH, a.C0, a.RW, a.TH, a.TW, a.nc_cap, a.gw_cap, 0,
+                                                       (int)gridDim.x, a.PB};
+    const int bid = (int)blockIdx.x - R.cta0;
+    const int nc_cap = R.nc_cap;
+    const int TH = R.TH, TW = R.TW, kAdjK = a.K;
     int *cm = reinterpret_cast<int *>(asm_);       // [TW][K] output columns
     float *cw = reinterpret_cast<float *>(cm + TW * kAdjK);
     int *cn = reinterpret_cast<int *>(cw + TW * kAdjK);   // [TW] counts
@@ -111,19 +118,19 @@ __global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_con
     float *rw = reinterpret_cast<float *>(rm + TH * kAdjK);
     int *rn = reinterpret_cast<int *>(rw + TH * kAdjK);   // [TH]
     int *ext = rn + TH;                             // [4] window: mx_lo, mx_hi, my_lo, my_hi
-    float *gw = reinterpret_cast<float *>(ext + 4); // [NRcap][NCcap] window
-    float *hx = gw + a.gw_cap;                      // [TH][NCcap] row-pass buffer
+    float *gw = reinterpret_cast<float *>(ext + 4); // [PB][NRcap][NCcap] windows
+    float *hx = gw + max(1, R.PB) * R.gw_cap;       // [PB][TH][NCcap] row-pass buffer (after PB windows)
     const int H = (int)a.H, W = (int)a.W, Ho = (int)a.Ho, Wo = (int)a.Wo;
-    const int tiles_y = (a.RH + TH - 1) / TH, tiles_x = (a.RW + TW - 1) / TW;  // tiles of the region
+    const int tiles_y = (R.RH + TH - 1) / TH, tiles_x = (R.RW + TW - 1) / TW;  // tiles of the region
     const int ngeom = tiles_y * tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // CTA b keeps the tile geometry b % ngeom (its pair lists are computed once)
-    // and loops over the planes b / ngeom, + gridDim.x / ngeom, ...
-    const int geom = blockIdx.x % ngeom, pstep = max(1, (int)gridDim.x / ngeom);
-    if (blockIdx.x >= pstep * ngeom) return;
+    // and loops over the planes b / ngeom, + ncta / ngeom, ...
+    const int geom = bid % ngeom, pstep = max(1, R.ncta / ngeom);
+    if (bid >= pstep * ngeom) return;
     const int tx_i = geom % tiles_x, ty_i = geom / tiles_x;
-    const int r0 = a.R0 + ty_i * TH, r1 = min(r0 + TH, a.R0 + a.RH), c0 = a.C0 + tx_i * TW,
-              c1 = min(c0 + TW, a.C0 + a.RW);
+    const int r0 = R.R0 + ty_i * TH, r1 = min(r0 + TH, R.R0 + R.RH), c0 = R.C0 + tx_i * TW,
+              c1 = min(c0 + TW, R.C0 + R.RW);
     const int NH = r1 - r0, NW = c1 - c0;
     if (threadIdx.x == 0) {
         ext[0] = INT32_MAX;
@@ -162,30 +169,72 @@ __global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_con
     __syncthreads();
     const int mx_lo = ext[0], my_lo = ext[2];
     const int NCg = ext[1] - mx_lo + 1, NRg = ext[3] - my_lo + 1;
-    float *hy = hx;  // [TH][NCcap]: the row pass over the window columns
-    for (int64_t plane = blockIdx.x / ngeom; plane < a.planes; plane += pstep) {
-        __syncthreads();  // the previous plane's readers are done
-        const T *g = static_cast<const T *>(a.grad_out) + plane * (int64_t)Ho * Wo;
-        // grad_out window (fp32)
-        if (NCg > 0 && NRg > 0)
-            for (int r = warp; r < NRg; r += 8) {
-                const T *grow = g + (int64_t)(my_lo + r) * Wo + mx_lo;
-                for (int c = lane; c < NCg; c += 32) gw[r * a.nc_cap + c] = DT<T>::to_f(grow[c]);
+    float *hy = hx;  // [PB][TH][NCcap]: the row pass over the window columns
+    const int PB = max(1, R.PB), gstride = R.gw_cap, hstride = TH * nc_cap;
+    // CTA planes: groups of PB consecutive planes, group bid / ngeom, + pstep, ...
+    for (int64_t p0 = (int64_t)(bid / ngeom) * PB; p0 < a.planes; p0 += (int64_t)pstep * PB) {
+        const int nP = (int)(a.planes - p0 < PB ? a.planes - p0 : PB);
+        __syncthreads();  // the previous planes' readers are done
+        const T *g0 = static_cast<const T *>(a.grad_out) + p0 * (int64_t)Ho * Wo;
+        // grad_out windows (fp32); narrow windows are flattened over (plane, row,
+        // column) so that every thread keeps loads in flight
+        if (NCg >= 64 && NRg > 0) {
+            for (int rp = warp; rp < nP * NRg; rp += 8) {
+                const int pp = rp / NRg, r = rp - pp * NRg;
+                const T *grow = g0 + (int64_t)pp * Ho * Wo + (int64_t)(my_lo + r) * Wo + mx_lo;
+                for (int c = lane; c < NCg; c += 32) gw[pp * gstride + r * nc_cap + c] = DT<T>::to_f(grow[c]);
             }
-        __syncthreads();
-        // row pass first: hy[rr][c] = sum over row rr's pairs (lists uniform across the warp)
-        for (int rr = warp; rr < NH; rr += 8) {
-            const int n = rn[rr];
-            for (int c = lane; c < NCg; c += 32) {
-                float acc = 0.0f;
-                for (int e = 0; e < n; ++e)
-                    acc = __fmaf_rn(rw[rr * kAdjK + e], gw[(rm[rr * kAdjK + e] - my_lo) * a.nc_cap + c], acc);
-                hy[rr * a.nc_cap + c] = acc;
+        } else if (NCg > 0 && NRg > 0) {
+            const int per = NRg * NCg, tot = nP * per;
+#pragma unroll 4
+            for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+                const int pp = idx / per, rc = idx - pp * per, r = rc / NCg, c = rc - r * NCg;
+                gw[pp * gstride + r * nc_cap + c] =
+                    DT<T>::to_f(g0[(int64_t)pp * Ho * Wo + (int64_t)(my_lo + r) * Wo + mx_lo + c]);
             }
         }
         __syncthreads();
-        // column pass -> grad_in; a thread keeps one column's pair list in registers
-        T *dst = static_cast<T *>(a.grad_in) + plane * (int64_t)H * W;
+        // row pass first: hy[rr][c] = sum over row rr's pairs (wide windows: lists uniform across a warp)
+        if (NCg >= 64) {
+            for (int rp = warp; rp < nP * NH; rp += 8) {
+                const int pp = rp / NH, rr = rp - pp * NH;
+                const int n = rn[rr];
+                const float *gp = gw + pp * gstride;
+                for (int c = lane; c < NCg; c += 32) {
+                    float acc = 0.0f;
+                    for (int e = 0; e < n; ++e)
+                        acc = __fmaf_rn(rw[rr * kAdjK + e], gp[(rm[rr * kAdjK + e] - my_lo) * nc_cap + c], acc);
+                    hy[pp * hstride + rr * nc_cap + c] = acc;
+                }
+            }
+        } else {
+            const int per = NH * NCg;
+            for (int idx = threadIdx.x; idx < nP * per; idx += blockDim.x) {
+                const int pp = idx / per, rc = idx - pp * per, rr = rc / NCg, c = rc - rr * NCg;
+                const int n = rn[rr];
+                const float *gp = gw + pp * gstride;
+                float acc = 0.0f;
+                for (int e = 0; e < n; ++e)
+                    acc = __fmaf_rn(rw[rr * kAdjK + e], gp[(rm[rr * kAdjK + e] - my_lo) * nc_cap + c], acc);
+                hy[pp * hstride + rr * nc_cap + c] = acc;
+            }
+        }
+        __syncthreads();
+        // column pass -> grad_in
+        T *dst0 = static_cast<T *>(a.grad_in) + p0 * (int64_t)H * W;
+        if (NW < 32) {  // narrow tile (border bands): one thread per (plane, row, column), lists from shared memory
+            const int per = NH * NW;
+            for (int idx = threadIdx.x; idx < nP * per; idx += blockDim.x) {
+                const int pp = idx / per, rc = idx - pp * per, rr = rc / NW, kk = rc - rr * NW;
+                const float *hr = hy + pp * hstride + rr * nc_cap - mx_lo;
+                const int n = cn[kk];
+                float acc = 0.0f;
+                for (int e = 0; e < n; ++e) acc = __fmaf_rn(cw[kk * kAdjK + e], hr[cm[kk * kAdjK + e]], acc);
+                dst0[(int64_t)pp * H * W + (int64_t)(r0 + rr) * W + c0 + kk] = DT<T>::from_f(acc);
+            }
+            continue;
+        }
+        // a thread keeps one column's pair list in registers
         const int ncw = (NW + 31) / 32;               // warps covering the columns
         const int rsplit = max(1, 8 / max(1, ncw));   // row groups
         const int cw_i = warp % max(1, ncw), rg = warp / max(1, ncw);
@@ -199,13 +248,14 @@ __global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_con
                 mloc[e] = e < n ? cm[k * kAdjK + e] - mx_lo : 0;
                 wloc[e] = e < n ? cw[k * kAdjK + e] : 0.0f;
             }
-            for (int rr = rg; rr < NH; rr += rsplit) {
-                const float *hr = hy + rr * a.nc_cap;
+            for (int rp = rg; rp < nP * NH; rp += rsplit) {
+                const int pp = rp / NH, rr = rp - pp * NH;
+                const float *hr = hy + pp * hstride + rr * nc_cap;
                 float acc = 0.0f;
 #pragma unroll
                 for (int e = 0; e < kAdjKMax; ++e)
                     if (e < n) acc = __fmaf_rn(wloc[e], hr[mloc[e]], acc);
-                dst[(int64_t)(r0 + rr) * W + c0 + k] = DT<T>::from_f(acc);
+                dst0[(int64_t)pp * H * W + (int64_t)(r0 + rr) * W + c0 + k] = DT<T>::from_f(acc);
             }
         }
     }

@@ -260,6 +260,8 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L, const F
     // rows copied by the issue warp (input pitch or start not 16-B aligned) may
     // write up to 15 bytes past a row's columns: one more margin of A elements
     const bool sw = ((g.W * ESZ) % 16 != 0) || (reinterpret_cast<uintptr_t>(g.in) & 15) != 0;
+    const int dtab_bytes = 8 * 16 * 32;  // adjoint sw rows: element shift per (slot <= 8, segment <= 16, row)
+    if (sw && a.SR > 32) return false;
     auto seg_pitch_for = [&](int cpt) {
         int64_t elems = std::min<int64_t>(g.W, (int64_t)cpt * K * QX - QX + Lw + 2 * A);
         elems = (elems + A - 1) / A * A + A + (ralloc + A - 1) / A * A + (sw ? 2 * A : 0);
@@ -298,7 +300,7 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L, const F
                 c.out_pitch = ((c.CPT * KP * ESZ + 16) + 15) / 16 * 16;
                 c.slot_bytes = c.NS * c.JM * c.out_pitch;
             }
-            const int fixed = 256 + 128 + 2 * c.slot_bytes;
+            const int fixed = 256 + 128 + 2 * c.slot_bytes + (sw ? dtab_bytes : 0);
             const int S = std::min(8, (budget - fixed) / std::max(1, c.stage_bytes));
             if (S < 2) continue;
             c.S = S;
@@ -340,7 +342,7 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L, const F
     L.grid = (int)std::min<int64_t>(ntasks, resident);
     if (const char *e = std::getenv("FCFS_DEBUG_GRID")) L.grid = std::max(1, std::min(L.grid, std::atoi(e)));
     if (const char *e = std::getenv("FCFS_DEBUG_S")) a.S = std::max(2, std::min(a.S, std::atoi(e)));
-    L.smem = 256 + a.S * a.stage_bytes + 128 + 2 * a.slot_bytes;
+    L.smem = 256 + a.S * a.stage_bytes + 128 + 2 * a.slot_bytes + (sw ? dtab_bytes : 0);
     // one TMA box per segment and stage when the block is narrow enough (box dims <= 256)
     a.box_w = a.seg_pitch / ESZ;
     a.use_tmap = 0;
@@ -927,6 +929,8 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
     a.pad = pl->pad;
     a.is1d = pl->is1d;
     a.TH = a.TW = 0;
+    a.nreg = 0;
+    a.PB = 1;
     a.R0 = a.C0 = 0;
     a.RH = (int)std::min<int64_t>(pl->H, INT32_MAX);
     a.RW = (int)std::min<int64_t>(pl->W, INT32_MAX);
@@ -934,21 +938,26 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
     const int kx = adj_max_pairs(pl->tab, pl->W, pl->Wo, pl->pad);
     const int ky = pl->is1d ? 1 : adj_max_pairs(pl->taby, pl->H, pl->Ho, pl->pad);
     const bool tiled_ok = pl->D == 1 && std::max(kx, ky) <= 32 && pl->H < INT32_MAX / 64 && pl->W < INT32_MAX / 64;
-    auto plan_tiles = [&](AdjArgs &b) {
+    // band: a border region (small tiles, several planes per CTA iteration)
+    auto plan_tiles = [&](AdjArgs &b, bool band) {
         b.TH = b.TW = 0;
+        b.PB = 1;
         const int K = std::max(1, std::max(kx, ky));
         const int T = pl->tab.ntaps;
         auto span = [&](int n, int p, int q) { return (int)(((int64_t)(n + 2 * T + 2) * p + q - 1) / q + p + 2); };
         int bTH = 0, bTW = 0, bNR = 0, bNC = 0;
+        int64_t bbytes = 0;
         for (int TW : {256, 128, 64, 32, 16})
             for (int TH : {256, 128, 64, 32, 16, 8, 4, 2, 1}) {
-                const int NC = (span(TW, pl->p, pl->q) + 3) / 4 * 4;
-                const int NR = pl->is1d ? TH : span(TH, pl->py, pl->qy);
-                const int64_t bytes = (int64_t)(TW + TH) * K * 8 + (TW + TH) * 4 + 16 +
-                                      4 * ((int64_t)NR * NC + (int64_t)TH * NC);
-                if (bytes > 100 * 1024) continue;
-                const int THe = std::min(TH, b.RH), TWe = std::min(TW, b.RW);
-                if ((int64_t)THe * TWe > (int64_t)bTH * bTW) {
+                const int THe = std::min(TH, b.RH), TWe = std::min(TW, b.RW);  // a region narrower than the tile
+                const int NC = (span(TWe, pl->p, pl->q) + 3) / 4 * 4;
+                const int NR = pl->is1d ? THe : span(THe, pl->py, pl->qy);
+                const int64_t bytes = (int64_t)(TWe + THe) * K * 8 + (TWe + THe) * 4 + 16 +
+                                      4 * ((int64_t)NR * NC + (int64_t)THe * NC);
+                if (bytes > (band ? 40 : 100) * 1024) continue;
+                if ((int64_t)THe * TWe > (int64_t)bTH * bTW ||
+                    (band && (int64_t)THe * TWe == (int64_t)bTH * bTW && bytes < bbytes)) {
+                    bbytes = bytes;
                     bTH = THe;
                     bTW = TWe;
                     bNR = NR;
@@ -961,12 +970,15 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
         b.TW = bTW;
         b.nc_cap = bNC;
         b.gw_cap = bNR * bNC;
-        b.smem = (bTW + bTH) * K * 8 + (bTW + bTH) * 4 + 32 + 4 * (b.gw_cap + bTH * bNC);
+        const int lists = (bTW + bTH) * K * 8 + (bTW + bTH) * 4 + 32, per_plane = 4 * (b.gw_cap + bTH * bNC);
+        if (band) b.PB = std::max(1, std::min(8, (48 * 1024 - lists) / per_plane));
+        b.smem = lists + b.PB * per_plane;
         const int64_t ngeom = (int64_t)((b.RH + bTH - 1) / bTH) * ((b.RW + bTW - 1) / bTW);
         // resident CTAs: shared memory (227 KB per SM) and 2048 threads per SM
         const int per_sm = std::max(1, std::min(8, (227 * 1024) / (b.smem + 1024)));
         const int64_t target = (int64_t)pl->sm_count * per_sm;
-        const int64_t pstep = std::max<int64_t>(1, std::min<int64_t>(planes, target / std::max<int64_t>(1, ngeom)));
+        const int64_t groups = (planes + b.PB - 1) / b.PB;
+        const int64_t pstep = std::max<int64_t>(1, std::min<int64_t>(groups, target / std::max<int64_t>(1, ngeom)));
         if (ngeom * pstep > INT32_MAX) b.TH = b.TW = 0;
         else b.grid = (int)(ngeom * pstep);
     };
@@ -977,10 +989,7 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
     if (pl->mode != FCFS_NEAREST && pl->D == 1 && !pl->is1d && !(pl->flags & FCFS_FLAG_FORCE_REFERENCE) &&
         !std::getenv("FCFS_NO_FUSED_ADJOINT"))
         v = fused_lookup_adjoint(pl->dtype, pl->py, pl->qy, pl->p, pl->q, pl->tab.ntaps);
-    // grad_out rows that are not 16-B aligned would take the fused kernel's
-    // software-realigned load path, slower than the tiled kernel
-    const bool go_aligned = (pl->Wo * ESZ) % 16 == 0 && (reinterpret_cast<uintptr_t>(grad_out) & 15) == 0;
-    if (v && (tiled_ok || pl->pad == FCFS_PAD_ZERO) && (go_aligned || !tiled_ok || std::getenv("FCFS_FUSED_ADJOINT_SW"))) {
+    if (v && (tiled_ok || pl->pad == FCFS_PAD_ZERO)) {
         RunGeom g;
         g.in = grad_out;
         g.out = grad_in;
@@ -1021,19 +1030,30 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
                 if (blx) regs[nreg++] = {bly, pl->H - bly - bry, 0, blx};
                 if (brx) regs[nreg++] = {bly, pl->H - bly - bry, pl->W - brx, brx};
             }
+            // every band in one launch: region i owns a contiguous range of CTAs
+            AdjArgs all = a;
+            all.nreg = nreg;
+            all.grid = 0;
+            all.smem = 0;
             for (int i = 0; i < nreg; ++i) {
                 AdjArgs b = a;
                 b.R0 = (int)regs[i].r0;
                 b.RH = (int)regs[i].rh;
                 b.C0 = (int)regs[i].c0;
                 b.RW = (int)regs[i].rw;
-                plan_tiles(b);
-                if (launch_adjoint(pl->dtype, b, stream) != 0) return FCFS_E_CUDA;
+                plan_tiles(b, true);
+                if (b.TH == 0) return FCFS_E_CUDA;  // tiled_ok: every region has a geometry
+                all.reg[i] = {b.R0, b.RH, b.C0, b.RW, b.TH, b.TW, b.nc_cap, b.gw_cap, all.grid, b.grid, b.PB};
+                all.K = b.K;
+                all.TH = b.TH;
+                all.grid += b.grid;
+                all.smem = std::max(all.smem, b.smem);
             }
+            if (nreg && launch_adjoint(pl->dtype, all, stream) != 0) return FCFS_E_CUDA;
             return FCFS_OK;
         }
     }
-    if (tiled_ok) plan_tiles(a);
+    if (tiled_ok) plan_tiles(a, false);
     return launch_adjoint(pl->dtype, a, stream) == 0 ? FCFS_OK : FCFS_E_CUDA;
 }
 
