@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_con
             }
         } else if (NCg > 0 && NRg > 0) {
             const int per = NRg * NCg, tot = nP * per;
-#pragma unroll 4
+#pragma unroll 8
             for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
                 const int pp = idx / per, rc = idx - pp * per, r = rc / NCg, c = rc - r * NCg;
                 gw[pp * gstride + r * nc_cap + c] =

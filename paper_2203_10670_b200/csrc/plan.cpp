@@ -903,6 +903,36 @@ int adj_max_pairs(const PhaseTable &t, int64_t n, int64_t no, int pad) {
     return best;
 }
 
+// Widest grad_out window (outputs m, max - min + 1) that the adjoint pair lists
+// of any tile [i0, i0 + te) of the region [r0, r0 + rn) of one dimension reach.
+int adj_window(const PhaseTable &t, int64_t n, int64_t no, int pad, int64_t r0, int64_t rn, int te) {
+    const int lo = t.lo, T = t.ntaps;
+    const int64_t vmin = lo, vmax = ((no - 1) / t.p) * t.q + t.base[(no - 1) % t.p] + lo + T - 1;
+    int64_t mlo = INT64_MAX, mhi = -1;
+    auto span_v = [&](int64_t v) {
+        const int64_t bl = v - lo - T + 1, bh = v - lo;
+        const int64_t m0 = bl <= 0 ? 0 : (bl * t.p + t.q - 1) / t.q;
+        const int64_t m1 = std::min<int64_t>(bh < 0 ? -1 : ((bh + 1) * t.p + t.q - 1) / t.q - 1, no - 1);
+        if (m1 >= m0) mlo = std::min(mlo, m0), mhi = std::max(mhi, m1);
+    };
+    int best = 1;
+    for (int64_t i0 = r0; i0 < r0 + rn; i0 += te) {
+        mlo = INT64_MAX;
+        mhi = -1;
+        for (int64_t i = i0; i < std::min(r0 + rn, i0 + te); ++i) {
+            span_v(i);
+            if (pad == FCFS_PAD_REPLICATE && i == 0)
+                for (int64_t v = vmin; v < 0; ++v) span_v(v);
+            if (pad == FCFS_PAD_REPLICATE && i == n - 1)
+                for (int64_t v = n; v <= vmax; ++v) span_v(v);
+            if (pad == FCFS_PAD_REFLECT && i >= 1 && -i >= vmin) span_v(-i);
+            if (pad == FCFS_PAD_REFLECT && i <= n - 2 && 2 * (n - 1) - i <= vmax) span_v(2 * (n - 1) - i);
+        }
+        if (mhi >= mlo) best = std::max<int64_t>(best, mhi - mlo + 1);
+    }
+    return best;
+}
+
 fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in, int64_t N, void *stream) {
     if (!pl || N < 0) return FCFS_E_ARG;
     if (N == 0) return FCFS_OK;
@@ -946,7 +976,13 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
         const int T = pl->tab.ntaps;
         auto span = [&](int n, int p, int q) { return (int)(((int64_t)(n + 2 * T + 2) * p + q - 1) / q + p + 2); };
         int bTH = 0, bTW = 0, bNR = 0, bNC = 0;
-        int64_t bbytes = 0;
+        if (band) {  // border bands: the region's own width (<= 256) x up to 64 rows, exact windows
+            bTW = std::min(b.RW, 256);
+            bTH = std::min(b.RH, 64);
+            bNC = (adj_window(pl->tab, pl->W, pl->Wo, pl->pad, b.C0, b.RW, bTW) + 3) / 4 * 4;
+            bNR = pl->is1d ? bTH : adj_window(pl->taby, pl->H, pl->Ho, pl->pad, b.R0, b.RH, bTH);
+        }
+        if (!band)
         for (int TW : {256, 128, 64, 32, 16})
             for (int TH : {256, 128, 64, 32, 16, 8, 4, 2, 1}) {
                 const int THe = std::min(TH, b.RH), TWe = std::min(TW, b.RW);  // a region narrower than the tile
@@ -954,10 +990,8 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
                 const int NR = pl->is1d ? THe : span(THe, pl->py, pl->qy);
                 const int64_t bytes = (int64_t)(TWe + THe) * K * 8 + (TWe + THe) * 4 + 16 +
                                       4 * ((int64_t)NR * NC + (int64_t)THe * NC);
-                if (bytes > (band ? 40 : 100) * 1024) continue;
-                if ((int64_t)THe * TWe > (int64_t)bTH * bTW ||
-                    (band && (int64_t)THe * TWe == (int64_t)bTH * bTW && bytes < bbytes)) {
-                    bbytes = bytes;
+                if (bytes > 100 * 1024) continue;
+                if ((int64_t)THe * TWe > (int64_t)bTH * bTW) {
                     bTH = THe;
                     bTW = TWe;
                     bNR = NR;
@@ -971,7 +1005,7 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
         b.nc_cap = bNC;
         b.gw_cap = bNR * bNC;
         const int lists = (bTW + bTH) * K * 8 + (bTW + bTH) * 4 + 32, per_plane = 4 * (b.gw_cap + bTH * bNC);
-        if (band) b.PB = std::max(1, std::min(8, (48 * 1024 - lists) / per_plane));
+        if (band) b.PB = std::max(1, std::min(8, (72 * 1024 - lists) / per_plane));
         b.smem = lists + b.PB * per_plane;
         const int64_t ngeom = (int64_t)((b.RH + bTH - 1) / bTH) * ((b.RW + bTW - 1) / bTW);
         // resident CTAs: shared memory (227 KB per SM) and 2048 threads per SM
