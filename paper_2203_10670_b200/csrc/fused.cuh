@@ -369,10 +369,10 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     uint64_t *empty = full + 16;                            // consumers done   (count 8 warps)
     unsigned char *stages = smem + 256;
     unsigned char *obuf = stages + a.S * a.stage_bytes + 128;
-    // adjoint variants with unaligned rows (sw_load): the consumers read every
-    // sub-row where its aligned superset landed, shifted by dtab's element count
-    // (slot, segment, row) -- no realignment pass (TZ == 1)
-    constexpr bool kShift = ADJ && TZ == 1;
+    // unaligned rows (sw_load, TZ == 1): the consumers read every sub-row where
+    // its aligned superset landed, shifted by dtab's element count (slot,
+    // segment, row) -- no realignment pass; 3D variants realign in the padding warp
+    constexpr bool kShift = TZ == 1;
     unsigned char *dtab = obuf + 2 * a.slot_bytes;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -658,6 +658,10 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     }
 
     // ---------------------------------------------------------------- consumers
+    // (SW: rows read in place at a per-row element shift; a separate copy of the
+    // consumer code so that aligned runs keep compile-time parities)
+    auto consumers = [&](auto sw_c) {
+    constexpr bool SW = decltype(sw_c)::value;
     const int ctid = threadIdx.x - 64;
     const int span_id = ctid >> 4, span_e = ctid & 15;  // copy-out roles
     const int rowb = a.Wo * ESZ;
@@ -726,11 +730,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
         // (zero-padding rows arrive as zeros: +0 for every tap, as in the reference kernel)
         auto row_h = [&](float(&h)[KP], const unsigned char *srow, int sl, int ridx) {
             float win[WIN];
-            if constexpr (kShift) {
-                if (a.sw_load)
-                    load_win<T, WIN, -1>(reinterpret_cast<const T *>(srow), e0 + dtab[(sl * a.NS + sgi) * a.SR + ridx], win);
-                else
-                    load_win<T, WIN, PAR>(reinterpret_cast<const T *>(srow), e0, win);
+            if constexpr (SW) {
+                load_win<T, WIN, -1>(reinterpret_cast<const T *>(srow), e0 + dtab[(sl * a.NS + sgi) * a.SR + ridx], win);
             } else if constexpr (TZ == 1) {
                 load_win<T, WIN, PAR>(reinterpret_cast<const T *>(srow), e0, win);
             } else {
@@ -968,6 +969,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     }
     pdl_launch_dependents();
     if (span_e == 0) bulk_wait0();
+    };
+    if (kShift && a.sw_load) consumers(std::true_type{});
+    else consumers(std::false_type{});
     }
 }
 
