@@ -286,8 +286,14 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L, const F
             if (nseg > INT32_MAX) continue;
             c.nseg = (int32_t)nseg;
             const int span_cap = c.ntile == 1 ? 16 : 16 / c.JM;  // copy-out spans per flush <= 16
-            c.NS = (int32_t)std::min<int64_t>(std::min(NT / c.CPT, span_cap), nseg);
-            if (c.NS < 1) continue;
+            int ns_max = (int)std::min<int64_t>(std::min(NT / c.CPT, span_cap), nseg);
+            if (const char *e = std::getenv("FCFS_DEBUG_NSMAX")) ns_max = std::max(1, std::min<int>(ns_max, std::atoi(e)));
+            if (ns_max < 1) continue;
+            const FusedArgs c_base = c;
+            // 3D: fewer segments per task buy a deeper stage ring (see `depth`)
+            for (int ns = ns_max; ns >= (TZ > 1 ? 1 : ns_max); --ns) {
+            FusedArgs c = c_base;
+            c.NS = ns;
             c.seg_pitch = seg_pitch_for(c.CPT);
             c.row_pitch = c.seg_pitch;                                   // segment block: [slice][row][col]
             c.slice_pitch = c.SR * c.seg_pitch;
@@ -309,11 +315,17 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L, const F
             // a segment narrow enough for one TMA box per stage (<= 256 elements) issues
             // one copy instead of SR * TZ row copies
             const double boxb = (!sw && c.seg_pitch / ESZ <= 256 && !std::getenv("FCFS_NO_TMA")) ? 1.04 : 1.0;
+            // ring depth: a 3D stage carries TZ slices per row and takes the
+            // consumers several times longer -- latency hiding needs >= 4 stages
+            // (V2: NS 11 / S 2 -> NS 6 / S 4 is 180 -> 162 us despite half the
+            // consumer threads idle)
+            const double depth = TZ > 1 ? (S >= 4 ? 1.0 : S == 3 ? 0.6 : 0.5) : (S >= 3 ? 1.0 : 0.9);
             const double score =
-                util * boxb * (S >= 3 ? 1.0 : 0.9) * (Gf == 1 ? 1.0 : 0.97) - 0.001 * (double)c.ntile;
+                util * boxb * depth * (Gf == 1 ? 1.0 : 0.97) - 0.001 * (double)c.ntile;
             if (score > best_score) {
                 best_score = score;
                 best = c;
+            }
             }
         }
         if (best_score > 0.96) break;
