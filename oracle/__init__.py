@@ -80,6 +80,7 @@ def _load():
                                                    ctypes.POINTER(i32), i32, i32, i32, dp, i32]
             lib.fcfs_oracle_output_dims_nd.argtypes = [i32, ctypes.POINTER(i64), ctypes.POINTER(i32),
                                                        ctypes.POINTER(i32), i32, ctypes.POINTER(i64)]
+            lib.fcfs_oracle_weight_grad.argtypes = [vp, i32, i64, i64, i64, dp, i32, i32, i32, i32, i32, i32, dp, dp]
             _lib = lib
     return _lib
 
@@ -279,6 +280,32 @@ def adjoint_nd(g, dims, p, q, mode="bilinear", pad="replicate", floor_extent=Fal
                                         PADS[pad], int(floor_extent), _dptr(out), nthreads)
     _chk(rc, "adjoint_nd")
     return out.reshape(tuple(lead) + tuple(dims))
+
+
+def weight_grad(x, g, p, q, mode="bilinear", pad="replicate", floor_extent=False, is1d=False):
+    """Gradient of sum(y * g) with respect to the layer's learnable weights
+    (reading Z22: each output channel's own taps), summed over all planes.
+
+    x: (..., H, W) float32 or float64; g: (..., Ho, Wo) (the layer output's shape).
+    Returns (grad, abs_sum), both double of shape (py, px, nty, ntx) -- 2D: (p, p,
+    taps, taps); 1D flag: (1, p, 1, taps) -- abs_sum the same sums of |g| |x|.
+    """
+    xa, kind = _as_input(x)
+    H, W = xa.shape[-2], xa.shape[-1]
+    planes = int(np.prod(xa.shape[:-2])) if xa.ndim > 2 else 1
+    Ho, Wo = output_shape(H, W, p, q, floor_extent, is1d)
+    ga = np.ascontiguousarray(g, dtype=np.float64)
+    if ga.size != planes * Ho * Wo:
+        raise ValueError(f"gradient of {ga.size} elements, expected {planes} x {Ho} x {Wo}")
+    from math import gcd
+    pr = p // gcd(p, q)
+    nt = {"nearest": 1, "bilinear": 2, "bicubic": 4}[mode]
+    shape = (1, pr, 1, nt) if is1d else (pr, pr, nt, nt)
+    out, ab = np.zeros(shape), np.zeros(shape)
+    rc = _load().fcfs_oracle_weight_grad(xa.ctypes.data, kind, planes, H, W, _dptr(ga), p, q, MODES[mode],
+                                         PADS[pad], int(floor_extent), int(is1d), _dptr(out), _dptr(ab))
+    _chk(rc, "weight_grad")
+    return out, ab
 
 
 # ---------------------------------------------------------------- rounding

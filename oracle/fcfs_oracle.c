@@ -1009,3 +1009,123 @@ int fcfs_oracle_adjoint_nd(const double *g, int64_t planes, int R, const int64_t
     }
     return bad;
 }
+
+/* ---------------------------------------------------------------------------
+ * WEIGHT GRADIENT ("learnable weights ... the weight
+ * gradient is a per-phase reduction"; the paper's §7 future work, PAPER.md:
+ * 310-314, makes the layer's kernel_weights W trainable -- it defines no
+ * backward).  Reading Z22: the learnable parameters of output channel (jy, jx)
+ * are its own taps (the nonzero support of the fixed kernel: ntaps x ntaps
+ * entries at the phase's tap offsets, §5.2); entries outside stay zero.
+ *
+ * The literal backward of the staged 2D layer (staged_plane_2d), per plane:
+ *   1. pad: the same materialised padded plane x_pad;
+ *   2. crop^T then pixelshuffle^-1: the hidden-layer gradient
+ *        gh[jy*p + jx][iy][ix] = g[p*iy + jy][p*ix + jx]  (0 past the extent);
+ *   3. conv2d weight gradient over the full T x T window:
+ *        dK[c][a][b] = sum_{iy, ix} gh[c][iy][ix] * x_pad[q*iy + a][q*ix + b];
+ *   4. the phase's support: out[jy][jx][ty][tx] = dK[jy*p+jx][fy - lo + ty][fx - lo + tx],
+ *      f = the phase's first tap offset (fcfs_oracle_phase_taps).
+ * Summed over planes.  abs_out: the same sums of |gh| * |x_pad| (the scale of
+ * a floating-point bound).  1D flag: rows are signals; out is (1, p, 1, nt).
+ * g: double [planes][Ho][Wo]; out, abs_out: double [py][px][nty][ntx].
+ * -------------------------------------------------------------------------*/
+static int wgrad_plane(const orc_src *s, const orc_job *jb, int64_t plane, const double *g, double *dK,
+                       double *dKabs, int T, int lo) {
+    int p = jb->p, q = jb->q, err = 0;
+    int64_t nhy = jb->is1d ? 1 : (jb->Ho + p - 1) / p, nix = (jb->Wo + p - 1) / p;
+    int64_t rows = jb->is1d ? jb->H : 1;
+    int py = jb->is1d ? 1 : p, qy = jb->is1d ? 1 : q, Ty = jb->is1d ? 1 : T, loy = jb->is1d ? 0 : lo;
+    int64_t PR = (nhy - 1) * qy + Ty, PC = (nix - 1) * q + T;
+    double *xp = (double *)malloc(sizeof(double) * PR * PC);
+    if (!xp) return ORC_E_NOMEM;
+    for (int64_t row = 0; row < rows; ++row) {
+        /* 1. pad (2D: the plane; 1D: row `row`) */
+        for (int64_t a = 0; a < PR; ++a)
+            for (int64_t b = 0; b < PC; ++b) {
+                int e = 0;
+                int64_t vr = jb->is1d ? row : loy + a, vc = lo + b;
+                double v;
+                if (jb->is1d) {
+                    int64_t sc;
+                    int k = pad_index(vc, s->W, jb->pad, &sc);
+                    if (k < 0) { /* unreachable by kept outputs: clamped edge */
+                        sc = vc < 0 ? 0 : s->W - 1;
+                        k = 1;
+                    }
+                    v = k == 0 ? 0.0 : src_at(s, plane, row, sc);
+                } else {
+                    v = padded_at(s, jb, plane, vr, vc, &e);
+                    if (e == ORC_E_PAD) {
+                        int64_t rr = vr < 0 ? 0 : (vr >= s->H ? s->H - 1 : vr);
+                        int64_t cc = vc < 0 ? 0 : (vc >= s->W ? s->W - 1 : vc);
+                        e = 0;
+                        v = padded_at(s, jb, plane, rr, cc, &e);
+                    }
+                    if (e) { err = e; goto done; }
+                }
+                xp[a * PC + b] = v;
+            }
+        /* 2.-3. hidden gradient and the conv weight gradient */
+        for (int jy = 0; jy < py; ++jy)
+            for (int jx = 0; jx < p; ++jx) {
+                double *k = dK + (size_t)(jy * p + jx) * Ty * T;
+                double *ka = dKabs + (size_t)(jy * p + jx) * Ty * T;
+                for (int64_t iy = 0; iy < nhy; ++iy)
+                    for (int64_t ix = 0; ix < nix; ++ix) {
+                        int64_t my = jb->is1d ? row : py * iy + jy, mx = (int64_t)p * ix + jx;
+                        if ((!jb->is1d && my >= jb->Ho) || mx >= jb->Wo) continue; /* crop^T: zero */
+                        double gh = g[(my)*jb->Wo + mx];
+                        for (int a = 0; a < Ty; ++a)
+                            for (int b = 0; b < T; ++b) {
+                                double xv = xp[(qy * iy + a) * PC + q * ix + b];
+                                k[a * T + b] += gh * xv;
+                                ka[a * T + b] += fabs(gh) * fabs(xv);
+                            }
+                    }
+            }
+    }
+done:
+    free(xp);
+    return err;
+}
+
+int fcfs_oracle_weight_grad(const void *x, int in_kind, int64_t planes, int64_t H, int64_t W, const double *g,
+                            int p, int q, int mode, int pad, int floor_ext, int is1d, double *out,
+                            double *abs_out) {
+    orc_job jb;
+    int rc = make_job(H, W, p, q, mode, pad, floor_ext, is1d, &jb);
+    if (rc) return rc;
+    rc = check_reach(&jb);
+    if (rc) return rc;
+    int lo, hi;
+    phase_window(mode, jb.p, jb.q, &lo, &hi);
+    int T = hi - lo + 1, Ty = is1d ? 1 : T, py = is1d ? 1 : jb.p;
+    size_t nk = (size_t)py * jb.p * Ty * T;
+    double *dK = (double *)calloc(nk, sizeof(double)), *dKa = (double *)calloc(nk, sizeof(double));
+    if (!dK || !dKa) { free(dK); free(dKa); return ORC_E_NOMEM; }
+    orc_src s = {x, in_kind, H, W, 0, H, H * W};
+    for (int64_t pl = 0; pl < planes && !rc; ++pl)
+        rc = wgrad_plane(&s, &jb, pl, g + pl * jb.Ho * jb.Wo, dK, dKa, T, lo);
+    if (!rc) {
+        double w[4];
+        int fy = 0, fx = 0;
+        int nt = fcfs_oracle_phase_taps(mode, jb.p, jb.q, 0, &fx, w), nty = is1d ? 1 : nt;
+        for (int jy = 0; jy < py; ++jy)
+            for (int jx = 0; jx < jb.p; ++jx) {
+                if (!is1d) fcfs_oracle_phase_taps(mode, jb.p, jb.q, jy, &fy, w);
+                fcfs_oracle_phase_taps(mode, jb.p, jb.q, jx, &fx, w);
+                int oy = is1d ? 0 : fy - lo, ox = fx - lo;
+                for (int ty = 0; ty < nty; ++ty)
+                    for (int tx = 0; tx < nt; ++tx) {
+                        size_t src = ((size_t)(jy * jb.p + jx) * Ty + oy + ty) * T + ox + tx;
+                        size_t dst = ((size_t)(jy * jb.p + jx) * nty + ty) * nt + tx;
+                        out[dst] = dK[src];
+                        if (abs_out) abs_out[dst] = dKa[src];
+                    }
+            }
+    }
+    free(dK);
+    free(dKa);
+    return rc;
+}
