@@ -207,6 +207,29 @@ fcfs_status fcfs_run_host(fcfs_plan_t plan, const void *host_in, void *host_out,
  * Errors: FCFS_E_ARG (NULL, N < 0, overlap), FCFS_E_DEVICE, FCFS_E_CUDA. */
 fcfs_status fcfs_run_adjoint(fcfs_plan_t plan, const void *grad_out, void *grad_in, int64_t N, void *stream);
 
+/* fcfs_weight_grad_shape / fcfs_run_weight_grad -- the gradient of the
+ * layer with respect to its learnable weights ("the
+ * weight gradient is a per-phase reduction"; §7 makes the
+ * kernel_weights trainable).  Reading Z22: the parameters of
+ * output channel (jy, jx) are its own taps -- ty < nty rows, tx < ntx columns
+ * at the phase's tap offsets (§5.2; zero-weight taps of fraction-0 phases
+ * included) -- so
+ *   grad_w[jy][jx][ty][tx] = sum over n, c and the outputs (my, mx) with
+ *     my mod py = jy, mx mod px = jx of
+ *     grad_out[n][c][my][mx] * x~[n][c][floor(my qy/py) + fy_jy + ty][floor(mx qx/px) + fx_jx + tx]
+ * with x~ the padded input (§3 Padding) and f_j the phase's first tap offset.
+ *   shape : dims[4] = (py, px, nty, ntx); 1D / rank-1 plans (1, p, 1, taps)
+ *   x        : device N x C x H x W (the forward input), plan dtype
+ *   grad_out : device N x C x Ho x Wo (the forward output's gradient), plan dtype
+ *   grad_w   : device fp32, prod(dims) elements, overwritten (zeroed, then
+ *              accumulated; fp32 partial sums added atomically, so the last
+ *              bits may differ between runs)
+ * Asynchronous on `stream`.  Errors: FCFS_E_ARG (NULL, N < 0),
+ * FCFS_E_UNSUPPORTED (rank-3 plans), FCFS_E_DEVICE, FCFS_E_CUDA. */
+fcfs_status fcfs_weight_grad_shape(fcfs_plan_t plan, int64_t *dims);
+fcfs_status fcfs_run_weight_grad(fcfs_plan_t plan, const void *x, const void *grad_out, float *grad_w, int64_t N,
+                                 void *stream);
+
 /* Read-only plan description (introspection and bench accounting). */
 typedef struct {
     int p, q;               /* reduced factor */

@@ -48,6 +48,8 @@ SIGNATURES = {
     "fcfs_needed_rows": (i32, [vp, i64, i64, P64, P64]),
     "fcfs_run_host": (i32, [vp, vp, vp, i64, vp, vp, vp]),
     "fcfs_run_adjoint": (i32, [vp, vp, vp, i64, vp]),
+    "fcfs_weight_grad_shape": (i32, [vp, P64]),
+    "fcfs_run_weight_grad": (i32, [vp, vp, vp, vp, i64, vp]),
     "fcfs_plan_info": (i32, [vp, ctypes.POINTER(PlanInfo)]),
     "fcfs_launch_info": (i32, [vp, i64, i64, i64, ctypes.c_char_p, i64]),
     "fcfs_phase_table": (i32, [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int)]),

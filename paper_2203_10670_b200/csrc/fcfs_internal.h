@@ -162,6 +162,22 @@ int launch_reference(int dtype, const RefArgs &a, void *stream);
 int launch_nearest(int dtype, const NearestArgs &a, void *stream);
 int launch_nearest_batch(int dtype, const NearestBatch &nb, void *stream);
 int launch_tile(int dtype, const TileArgs &a, int grid, int smem, void *stream);
+// Weight gradient (k_wgrad.cu): grad_w[jy][jx][ty][tx] over the phases' own taps.
+struct WgradArgs {
+    const void *x, *g;
+    float *gw;
+    int64_t planes;
+    int H, W, Ho, Wo, pad;
+    int px, qx, ntx, py, qy, nty;  // columns / rows (1D: rows 1/1, one tap)
+    int fx[kPMax], fy[kPMax];      // first tap offset of each phase (virtual index - floor(m q / p))
+    int fx_min, fy_min;            // smallest first offsets: the tile origins
+    int xb, yb;                    // x-periods / y-periods per task
+    int nxb, nyb;                  // tasks per plane: x bands, y bands
+    int64_t ntasks;
+    int xrows, xcols, grows, gcols;  // shared tiles: x (fp32, padded) and grad_out (fp32)
+    int npairs;                    // py * px (lanes take 32 per grid.y slice)
+};
+int launch_wgrad(int dtype, const WgradArgs &a, int grid, int smem, void *stream);
 int launch_adjoint(int dtype, const AdjArgs &a, void *stream);
 
 // Fused: the variant table.  fused_lookup returns an opaque kernel handle or

@@ -1,0 +1,117 @@
+// Weight gradient of the layer's learnable taps (SURVEY.md §8(f) row f3,
+// reading Z22): for output channel (jy, jx) and its own taps (ty, tx),
+//   grad_w[jy][jx][ty][tx] = sum over planes and outputs m = (my, mx) of that
+//   phase of grad_out[m] * x~[floor(my qy/py) + fy_jy + ty][floor(mx qx/px) + fx_jx + tx]
+// (x~ the padded input, §3 Padding).  A reduction: grad_out and x are each
+// read once from HBM into shared-memory tiles (fp32, padding applied); a warp
+// walks the tile's periods and lane l owns phase pair (pair0 + l), so all
+// lanes of a period read overlapping x windows (mostly broadcast shared
+// loads) and lane l keeps its ntx x nty partial sums in registers across all
+// of the CTA's tasks.  At the end the 8 warps' sums are added in shared
+// memory and one atomicAdd per weight and CTA lands in grad_w (pre-zeroed by
+// the host).  fp32 throughout; the order of the atomics is not fixed, so
+// runs may differ in the last bits (the parity bar is an error bound).
+#include "device_common.cuh"
+
+namespace fcfs {
+
+template <typename T, int NT>
+__global__ void __launch_bounds__(256) fcfs_wgrad_kernel(const __grid_constant__ WgradArgs a) {
+    extern __shared__ __align__(16) float wsm[];
+    float *xs = wsm;                          // [xrows][xcols]
+    float *gs = wsm + a.xrows * a.xcols;      // [grows][gcols]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pair = blockIdx.y * 32 + lane;
+    const bool own = pair < a.npairs;
+    const int jy = own ? pair / a.px : 0, jx = own ? pair - (pair / a.px) * a.px : 0;
+    const int oy = a.fy[jy] - a.fy_min, ox = a.fx[jx] - a.fx_min;  // window offsets in the tiles
+    float acc[NT][NT];
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int k = 0; k < NT; ++k) acc[i][k] = 0.0f;
+    const int nty = a.nty;
+    for (int64_t task = blockIdx.x; task < a.ntasks; task += gridDim.x) {
+        const int64_t plane = task / (a.nyb * a.nxb);
+        const int tb = (int)(task - plane * a.nyb * a.nxb);
+        const int by = tb / a.nxb, bx = tb - by * a.nxb;
+        const int iy0 = by * a.yb, ix0 = bx * a.xb;
+        const int ny = min(a.yb, (a.Ho + a.py - 1) / a.py - iy0), nx = min(a.xb, (a.Wo + a.px - 1) / a.px - ix0);
+        const int vr0 = iy0 * a.qy + a.fy_min, vc0 = ix0 * a.qx + a.fx_min;  // tile origins (virtual)
+        const int my0 = iy0 * a.py, mx0 = ix0 * a.px;
+        const T *xp = static_cast<const T *>(a.x) + plane * (int64_t)a.H * a.W;
+        const T *gp = static_cast<const T *>(a.g) + plane * (int64_t)a.Ho * a.Wo;
+        __syncthreads();  // the previous task's readers are done
+        const int xr = (ny - 1) * a.qy + (a.xrows - (a.yb - 1) * a.qy), xc = (nx - 1) * a.qx + (a.xcols - (a.xb - 1) * a.qx);
+        for (int idx = threadIdx.x; idx < xr * xc; idx += blockDim.x) {
+            const int r = idx / xc, c = idx - r * xc;
+            const int sr = pad_src32(vr0 + r, a.H, a.pad), sc = pad_src32(vc0 + c, a.W, a.pad);
+            // reflect positions one bounce cannot reach feed no kept output (plan check): clamp
+            const int rr = min(max(sr, 0), a.H - 1), cc = min(max(sc, 0), a.W - 1);
+            xs[r * a.xcols + c] = (sr < 0 || sc < 0) && a.pad == FCFS_PAD_ZERO ? 0.0f
+                                                                                : DT<T>::to_f(xp[(int64_t)rr * a.W + cc]);
+        }
+        const int gr = ny * a.py, gc = nx * a.px;
+        for (int idx = threadIdx.x; idx < gr * gc; idx += blockDim.x) {
+            const int r = idx / gc, c = idx - r * gc;
+            const int my = my0 + r, mx = mx0 + c;
+            gs[r * a.gcols + c] = (my < a.Ho && mx < a.Wo) ? DT<T>::to_f(gp[(int64_t)my * a.Wo + mx]) : 0.0f;
+        }
+        __syncthreads();
+        if (own) {
+            for (int it = warp; it < ny * nx; it += 8) {
+                const int iy = it / nx, ix = it - iy * nx;
+                const float gv = gs[(iy * a.py + jy) * a.gcols + ix * a.px + jx];
+                const float *xw = xs + (iy * a.qy + oy) * a.xcols + ix * a.qx + ox;
+#pragma unroll
+                for (int ty = 0; ty < NT; ++ty) {
+                    if (ty < nty) {
+#pragma unroll
+                        for (int tx = 0; tx < NT; ++tx) acc[ty][tx] = __fmaf_rn(gv, xw[ty * a.xcols + tx], acc[ty][tx]);
+                    }
+                }
+            }
+        }
+    }
+    // the 8 warps' partial sums of each pair, then one atomic per weight
+    __syncthreads();
+    float *red = wsm;  // [8][32][NT*NT]
+#pragma unroll
+    for (int ty = 0; ty < NT; ++ty)
+#pragma unroll
+        for (int tx = 0; tx < NT; ++tx) red[(warp * 32 + lane) * NT * NT + ty * NT + tx] = acc[ty][tx];
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 32 * NT * NT; idx += blockDim.x) {
+        const int l = idx / (NT * NT), e = idx - l * (NT * NT);
+        const int pr = blockIdx.y * 32 + l, ty = e / NT, tx = e - ty * NT;
+        if (pr >= a.npairs || ty >= nty) continue;
+        float s = 0.0f;
+        for (int w = 0; w < 8; ++w) s += red[(w * 32 + l) * NT * NT + e];
+        atomicAdd(&a.gw[((int64_t)pr * nty + ty) * a.ntx + tx], s);
+    }
+}
+
+int launch_wgrad(int dtype, const WgradArgs &a, int grid, int smem, void *stream) {
+    const int nt = a.ntx, gy = (a.npairs + 31) / 32;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const void *fn = nullptr;
+#define FCFS_WG(TT)                                                                               \
+    fn = nt == 1 ? reinterpret_cast<const void *>(&fcfs_wgrad_kernel<TT, 1>)                      \
+                 : (nt == 2 ? reinterpret_cast<const void *>(&fcfs_wgrad_kernel<TT, 2>)           \
+                            : reinterpret_cast<const void *>(&fcfs_wgrad_kernel<TT, 4>));
+    switch (dtype) {
+    case FCFS_F32: FCFS_WG(float) break;
+    case FCFS_F16: FCFS_WG(__half) break;
+    default: FCFS_WG(__nv_bfloat16) break;
+    }
+#undef FCFS_WG
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return (int)e;
+    WgradArgs local = a;
+    void *args[] = {&local};
+    e = cudaLaunchKernel(fn, dim3(grid, gy), dim3(256), args, (size_t)smem, s);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaGetLastError();
+}
+
+}  // namespace fcfs

@@ -1103,6 +1103,100 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
     return launch_adjoint(pl->dtype, a, stream) == 0 ? FCFS_OK : FCFS_E_CUDA;
 }
 
+// Weight gradient (reading Z22): shape (py, px, nty, ntx); 1D / rank 1: (1, p, 1, taps).
+fcfs_status fcfs_weight_grad_shape(fcfs_plan_t pl, int64_t *dims) {
+    if (!pl || !dims) return FCFS_E_ARG;
+    if (pl->rank == 3) return FCFS_E_UNSUPPORTED;
+    const bool rows1 = pl->is1d || pl->rank == 1;
+    dims[0] = rows1 ? 1 : pl->py;
+    dims[1] = pl->p;
+    dims[2] = rows1 ? 1 : pl->taby.ntaps;
+    dims[3] = pl->tab.ntaps;
+    return FCFS_OK;
+}
+
+fcfs_status fcfs_run_weight_grad(fcfs_plan_t pl, const void *x, const void *grad_out, float *grad_w, int64_t N,
+                                 void *stream) {
+    if (!pl || N < 0) return FCFS_E_ARG;
+    int64_t shp[4];
+    fcfs_status st = fcfs_weight_grad_shape(pl, shp);
+    if (st != FCFS_OK) return st;
+    if (!grad_w) return FCFS_E_ARG;
+    st = check_device(pl);
+    if (st != FCFS_OK) return st;
+    const int64_t nw = shp[0] * shp[1] * shp[2] * shp[3];
+    if (cudaMemsetAsync(grad_w, 0, nw * sizeof(float), static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return FCFS_E_CUDA;
+    if (N == 0) return FCFS_OK;
+    if (!x || !grad_out) return FCFS_E_ARG;
+    if (pl->H >= INT32_MAX / 64 || pl->W >= INT32_MAX / 64) return FCFS_E_UNSUPPORTED;
+    const bool rows1 = pl->is1d || pl->rank == 1;
+    WgradArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.x = x;
+    a.g = grad_out;
+    a.gw = grad_w;
+    a.planes = N * pl->C;
+    a.H = (int)pl->H;
+    a.W = (int)pl->W;
+    a.Ho = (int)(rows1 ? pl->H : pl->Ho);
+    a.Wo = (int)pl->Wo;
+    a.pad = pl->pad;
+    a.px = pl->p;
+    a.qx = pl->q;
+    a.ntx = pl->tab.ntaps;
+    a.fx_min = 1 << 30;
+    int fx_max = -(1 << 30), fy_max = -(1 << 30);
+    for (int j = 0; j < a.px; ++j) {
+        a.fx[j] = pl->tab.base[j] + pl->tab.lo;
+        a.fx_min = std::min(a.fx_min, a.fx[j]);
+        fx_max = std::max(fx_max, a.fx[j]);
+    }
+    if (rows1) {
+        a.py = a.qy = a.nty = 1;
+        a.fy[0] = 0;
+        a.fy_min = fy_max = 0;
+    } else {
+        a.py = pl->py;
+        a.qy = pl->qy;
+        a.nty = pl->taby.ntaps;
+        a.fy_min = 1 << 30;
+        for (int j = 0; j < a.py; ++j) {
+            a.fy[j] = pl->taby.base[j] + pl->taby.lo;
+            a.fy_min = std::min(a.fy_min, a.fy[j]);
+            fy_max = std::max(fy_max, a.fy[j]);
+        }
+    }
+    a.npairs = a.py * a.px;
+    const int span_x = fx_max + a.ntx - a.fx_min, span_y = fy_max + a.nty - a.fy_min;
+    const int nix = (a.Wo + a.px - 1) / a.px, niy = (a.Ho + a.py - 1) / a.py;
+    const int budget = 48 * 1024;  // 4 CTAs per SM
+    a.yb = 0;
+    for (a.xb = std::min(nix, 64); a.xb >= 1 && a.yb == 0; a.xb = a.xb > 1 ? a.xb / 2 : 0) {
+        a.xcols = (a.xb - 1) * a.qx + span_x;
+        a.gcols = a.xb * a.px;
+        for (int yb = std::min(niy, 64); yb >= 1; --yb) {
+            const int xrows = (yb - 1) * a.qy + span_y;
+            if (4 * ((int64_t)xrows * a.xcols + (int64_t)yb * a.py * a.gcols) <= budget) {
+                a.yb = yb;
+                a.xrows = xrows;
+                a.grows = yb * a.py;
+                break;
+            }
+        }
+        if (a.yb) break;
+    }
+    if (a.yb == 0) return FCFS_E_UNSUPPORTED;
+    a.nxb = (nix + a.xb - 1) / a.xb;
+    a.nyb = (niy + a.yb - 1) / a.yb;
+    a.ntasks = a.planes * a.nyb * a.nxb;
+    const int nt = a.ntx;
+    const int smem = std::max(4 * (a.xrows * a.xcols + a.grows * a.gcols), 8 * 32 * nt * nt * 4);
+    const int per_sm = std::max(1, std::min(8, (227 * 1024) / (smem + 1024)));
+    const int grid = (int)std::min<int64_t>(a.ntasks, (int64_t)pl->sm_count * per_sm);
+    return launch_wgrad(pl->dtype, a, grid, smem, stream) == 0 ? FCFS_OK : FCFS_E_CUDA;
+}
+
 fcfs_status fcfs_plan_info(fcfs_plan_t pl, fcfs_plan_info_t *info) {
     if (!pl || !info) return FCFS_E_ARG;
     info->p = pl->p;

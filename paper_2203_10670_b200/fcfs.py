@@ -176,6 +176,30 @@ class Plan:
                                         N, self._stream(stream)), "fcfs_run_adjoint")
         return out
 
+    def weight_grad_shape(self):
+        """(py, px, nty, ntx) of the learnable taps (fcfs_weight_grad_shape; reading Z22)."""
+        d = (ctypes.c_int64 * 4)()
+        check(_lib.lib.fcfs_weight_grad_shape(self._h, d), "fcfs_weight_grad_shape")
+        return tuple(d)
+
+    def run_weight_grad(self, x, grad_out, out=None, stream=None):
+        """d(sum y * grad_out)/dW over the learnable taps, fp32 (fcfs_run_weight_grad)."""
+        import torch
+        N = x.shape[0]
+        self._check_tensor(x, self.in_shape(N), "x")
+        self._check_tensor(grad_out, self.out_shape(N), "grad_out")
+        if grad_out.dtype != x.dtype:
+            raise ValueError("x and grad_out must share the plan dtype")
+        shp = self.weight_grad_shape()
+        if out is None:
+            out = torch.empty(shp, dtype=torch.float32, device=x.device)
+        if tuple(out.shape) != shp or out.dtype != torch.float32 or not out.is_contiguous():
+            raise ValueError(f"grad_w must be a contiguous float32 tensor of shape {shp}")
+        check(_lib.lib.fcfs_run_weight_grad(self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(grad_out.data_ptr()),
+                                            ctypes.c_void_p(out.data_ptr()), N, self._stream(stream)),
+              "fcfs_run_weight_grad")
+        return out
+
     def run_rows(self, x_rows, in_row0: int, out_row0: int, out_nrows: int, out=None, stream=None):
         """Output rows [out_row0, out_row0+out_nrows) from input rows [in_row0, in_row0+x_rows.shape[2])."""
         import torch
