@@ -127,10 +127,27 @@ def physical_gpu_index(local_rank: int) -> int:
 def oracle_sample_run(cfgs, planes_per_cfg: int):
     """Run the oracle (staged, as it stands) on `planes_per_cfg` planes of every
     launch of the workload; returns (outputs, seconds, description)."""
+    import numpy as np
     import oracle
     outs, secs, parts = 0, 0.0, []
     for cfg in cfgs:
         n_img = max(1, min(cfg.N, -(-planes_per_cfg // cfg.C)))
+        if cfg.backward or cfg.wgrad:  # the oracle's adjoint / weight gradient on whole planes
+            n_img = max(1, min(cfg.N, -(-planes_per_cfg // cfg.C)))
+            pl_sh = (n_img, cfg.C) + tuple(oracle.output_dims_nd(cfg.dims, (cfg.p,) * 2, (cfg.q,) * 2,
+                                                                 cfg.floor_extent))
+            g = synth.normal_f32(cfg.seed, int(np.prod(pl_sh))).reshape(pl_sh)
+            t0 = time.perf_counter()
+            if cfg.backward:
+                oracle.adjoint_nd(g, cfg.dims, (cfg.p,) * 2, (cfg.q,) * 2, cfg.mode, cfg.pad, cfg.floor_extent)
+            else:
+                x = synth.make_values(cfg, 0, n_img)
+                oracle.weight_grad(x, g, cfg.p, cfg.q, cfg.mode, cfg.pad, floor_extent=cfg.floor_extent)
+            secs += time.perf_counter() - t0
+            outs += g.size
+            parts.append(f"{cfg.name}: {'adjoint' if cfg.backward else 'weight gradient'} of "
+                         f"{n_img * cfg.C} of {cfg.planes} planes")
+            continue
         if cfg.values == "field":
             rows = (0, min(cfg.H, 600))
             x = synth.make_values(cfg, 0, 1, rows=rows)
@@ -169,8 +186,10 @@ def cpu_baseline(cfgs, budget_s=10.0):
         tot_o += o
         tot_s += s
         reps += 1
-    return {"value": tot_o / tot_s / 1e6, "unit": "Mpix/s", "cores": cores, "kind": "oracle",
-            "sample": f"staged C oracle (double, OpenMP {cores} threads) on {desc}, {reps} passes; {tot_s:.1f} s"}
+    threads = 1 if all(c.wgrad for c in cfgs) else cores  # the weight-gradient oracle is single-threaded
+    return {"value": tot_o / tot_s / 1e6, "unit": "Mpix/s", "cores": threads, "kind": "oracle",
+            "sample": f"C oracle (double, {threads} thread{'s' if threads > 1 else ''}) on {desc}, {reps} passes; "
+                      f"{tot_s:.1f} s"}
 
 
 def run_reference(args):
@@ -193,11 +212,20 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": DTYPE_TAG[cfgs[0].dtype], "data": "synthetic",
             "config": {"workload": args.workload, "launches": [c.name for c in cfgs]},
-            "cpu_baseline": {"value": value, "unit": "Mpix/s", "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": "Mpix/s",
+                             "cores": 1 if all(c.wgrad for c in cfgs) else cores, "kind": "oracle",
                              "sample": f"each step: {desc}"},
             "e2e": {"value": value, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def kernel_name(L):
+    if L["cfg"].backward:
+        return "fused_adjoint (+ border bands for replicate/reflect)"
+    if L["cfg"].wgrad:
+        return "weight_grad"
+    return L["plan"].kernel
 
 
 def make_plan(fc, cfg):
@@ -249,7 +277,13 @@ def main():
         for d in oshape:
             n_out *= d
         nbytes = (x.numel() + n_out) * x.element_size() if cfg.backward else pl.compulsory_bytes(cfg.N)
-        launches.append({"cfg": cfg, "plan": pl, "x_host": x, "bytes": nbytes, "outputs": n_out, "oshape": oshape})
+        g_host = None
+        if cfg.wgrad:  # weight gradient: inputs x and grad_out (the output's shape); "outputs" = grad_out pixels
+            g_host = torch.from_numpy(synth.normal_f32(cfg.seed + 7 + rank, n_out).reshape(oshape)).to(
+                getattr(torch, cfg.dtype))
+            nbytes = (x.numel() + n_out) * x.element_size()
+        launches.append({"cfg": cfg, "plan": pl, "x_host": x, "bytes": nbytes, "outputs": n_out, "oshape": oshape,
+                         "g_host": g_host})
     # input/output buffers per rotation set; several launches may share one input
     set_bytes = 0
     host_inputs = {}
@@ -265,7 +299,11 @@ def main():
     R = max(1, min(R, int(0.8 * free // set_bytes)))
     dev_inputs = {k: [v.to(dev) for _ in range(R)] for k, v in host_inputs.items()}
     for L in launches:
-        L["outs"] = [torch.empty(L["oshape"], dtype=L["x_host"].dtype, device=dev) for _ in range(R)]
+        if L["cfg"].wgrad:
+            L["g_dev"] = [L["g_host"].to(dev) for _ in range(R)]
+            L["outs"] = [torch.empty(L["plan"].weight_grad_shape(), dtype=torch.float32, device=dev) for _ in range(R)]
+        else:
+            L["outs"] = [torch.empty(L["oshape"], dtype=L["x_host"].dtype, device=dev) for _ in range(R)]
     torch.cuda.synchronize(dev)
 
     # kernel launches of a step: nearest-gather launches of one dtype share one
@@ -283,6 +321,8 @@ def main():
                 L = launches[grp[0]]
                 if L["cfg"].backward:
                     L["plan"].run_adjoint(dev_inputs[L["key"]][r], out=L["outs"][r], stream=stream)
+                elif L["cfg"].wgrad:
+                    L["plan"].run_weight_grad(dev_inputs[L["key"]][r], L["g_dev"][r], out=L["outs"][r], stream=stream)
                 else:
                     L["plan"].run(dev_inputs[L["key"]][r], out=L["outs"][r], stream=stream)
             else:
@@ -318,7 +358,9 @@ def main():
     for w in range(args.warmup):  # eager warm-up (also configures the kernels)
         step(w % R)
     torch.cuda.synchronize(dev)
+    n_launch0 = fc.kernel_launches()
     graph = capture(args.steps)
+    n_launches = fc.kernel_launches() - n_launch0  # the library's kernels captured in the timed graph
     with torch.cuda.stream(stream):
         graph.replay()  # graph warm-up (upload)
     torch.cuda.synchronize(dev)
@@ -403,7 +445,7 @@ def main():
              "factor": (f"{L['cfg'].p}/{L['cfg'].q}" if not L["cfg"].nd else
                         " x ".join(f"{a}/{b}" for a, b in zip(L["cfg"].pd, L["cfg"].qd))),
              "mode": L["cfg"].mode, "pad": L["cfg"].pad,
-             "dtype": L["cfg"].dtype, "out": list(L["plan"].odims), "kernel": L["plan"].kernel,
+             "dtype": L["cfg"].dtype, "out": list(L["plan"].odims), "kernel": kernel_name(L),
              "compulsory_bytes_alone": L["bytes"],
              "avg_launch_us": per_group_ms[next(gi for gi, g in enumerate(groups) if i in g)] * 1e3,
              "shares_launch_with": [launches[j]["cfg"].name for g in groups if i in g for j in g if j != i]}
@@ -418,14 +460,14 @@ def main():
         "achieved_GBps_step": bytes_per_step / (ms_per_step * 1e-3) / 1e9,
         "frac_of_8TBps_step": bytes_per_step / (ms_per_step * 1e-3) / 8e12,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": launches[groups[dom][0]]["plan"].kernel, "launch": dom_name,
+                     "traffic": traffic, "kernel": kernel_name(launches[groups[dom][0]]), "launch": dom_name,
                      "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs" if peak_kind == "measured" else
                      "fallback 6.65 TB/s (B200_PROFILING.md)",
                      "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_us": dom_ms * 1e3,
                      "timing": ("timed region: CUDA events around one CUDA-graph replay of exactly K steps "
                                 "(the library's launches captured on the launching stream); per-launch average = "
                                 "region / K when a step is one launch, else a graph of K launches of that kernel")},
-        "gpu_launches": args.steps * len(groups),
+        "gpu_launches": n_launches,
         "clocks": clocks,
     }
     if e2e is not None:
@@ -447,10 +489,13 @@ def run_e2e(launches, args, dev, stream, world, dist):
     for L in launches:
         if L["key"] not in pin_in:
             pin_in[L["key"]] = L["x_host"].pin_memory()
-        L["pin_out"] = torch.empty(L["outs"][0].shape, dtype=L["x_host"].dtype).pin_memory()
+        L["pin_out"] = torch.empty(L["outs"][0].shape, dtype=L["outs"][0].dtype).pin_memory()
     din = {k: torch.empty(v.shape, dtype=v.dtype, device=dev) for k, v in pin_in.items()}
+    pin_g = {L["key"]: L["g_host"].pin_memory() for L in launches if L["cfg"].wgrad}
+    gdev = {k: torch.empty(v.shape, dtype=v.dtype, device=dev) for k, v in pin_g.items()}
     # every launch copies its own input (the C-ABI call is per launch)
-    h2d = sum(pin_in[L["key"]].numel() * pin_in[L["key"]].element_size() for L in launches)
+    h2d = sum(pin_in[L["key"]].numel() * pin_in[L["key"]].element_size() for L in launches) + \
+        sum(v.numel() * v.element_size() for v in pin_g.values())
     d2h = sum(L["pin_out"].numel() * L["pin_out"].element_size() for L in launches)
 
     def step():
@@ -459,6 +504,12 @@ def run_e2e(launches, args, dev, stream, world, dist):
                 with torch.cuda.stream(stream):
                     din[L["key"]].copy_(pin_in[L["key"]], non_blocking=True)
                     L["plan"].run_adjoint(din[L["key"]], out=L["outs"][0], stream=stream)
+                    L["pin_out"].copy_(L["outs"][0], non_blocking=True)
+            elif L["cfg"].wgrad:  # copy x and grad_out in, Plan.run_weight_grad, copy grad_w out
+                with torch.cuda.stream(stream):
+                    din[L["key"]].copy_(pin_in[L["key"]], non_blocking=True)
+                    gdev[L["key"]].copy_(pin_g[L["key"]], non_blocking=True)
+                    L["plan"].run_weight_grad(din[L["key"]], gdev[L["key"]], out=L["outs"][0], stream=stream)
                     L["pin_out"].copy_(L["outs"][0], non_blocking=True)
             else:
                 L["plan"].run_host(pin_in[L["key"]], L["pin_out"], din[L["key"]], L["outs"][0], stream=stream)
@@ -483,8 +534,9 @@ def run_e2e(launches, args, dev, stream, world, dist):
     outputs = sum(L["outputs"] for L in launches)
     return {"value": world * outputs * steps / (ms * 1e-3) / 1e6, "unit": "Mpix/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps, "ms_per_step": ms / steps,
-            "path": ("fcfs_run_host (pinned host -> HBM -> kernel -> pinned host)" if not launches[0]["cfg"].backward
-                     else "pinned grad_out -> HBM -> fcfs_run_adjoint -> pinned grad_in")}
+            "path": ("pinned grad_out -> HBM -> fcfs_run_adjoint -> pinned grad_in" if launches[0]["cfg"].backward else
+                     "pinned x, grad_out -> HBM -> fcfs_run_weight_grad -> pinned grad_w" if launches[0]["cfg"].wgrad
+                     else "fcfs_run_host (pinned host -> HBM -> kernel -> pinned host)")}
 
 
 if __name__ == "__main__":

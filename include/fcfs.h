@@ -230,6 +230,11 @@ fcfs_status fcfs_weight_grad_shape(fcfs_plan_t plan, int64_t *dims);
 fcfs_status fcfs_run_weight_grad(fcfs_plan_t plan, const void *x, const void *grad_out, float *grad_w, int64_t N,
                                  void *stream);
 
+/* fcfs_kernel_launches -- the number of kernels this process's library has
+ * launched (enqueued or captured into a CUDA graph) so far: the bench's
+ * launch count is the difference around a capture.  Thread-safe. */
+uint64_t fcfs_kernel_launches(void);
+
 /* Read-only plan description (introspection and bench accounting). */
 typedef struct {
     int p, q;               /* reduced factor */

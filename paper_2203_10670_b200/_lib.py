@@ -57,6 +57,7 @@ SIGNATURES = {
     "fcfs_destroy": (None, [vp]),
     "fcfs_status_str": (ctypes.c_char_p, [i32]),
     "fcfs_version": (i32, []),
+    "fcfs_kernel_launches": (ctypes.c_uint64, []),
 }
 for _name, (_res, _args) in SIGNATURES.items():
     _f = getattr(lib, _name)

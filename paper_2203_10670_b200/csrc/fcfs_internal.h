@@ -178,6 +178,8 @@ struct WgradArgs {
     int npairs;                    // py * px (lanes take 32 per grid.y slice)
 };
 int launch_wgrad(int dtype, const WgradArgs &a, int grid, int smem, void *stream);
+// every successful kernel launch of the library (fcfs_kernel_launches)
+void count_launch();
 int launch_adjoint(int dtype, const AdjArgs &a, void *stream);
 
 // Fused: the variant table.  fused_lookup returns an opaque kernel handle or

@@ -287,6 +287,7 @@ int launch_adjoint(int dtype, const AdjArgs &a, void *stream) {
         void *args[] = {&local};
         cudaError_t e = cudaLaunchKernel(fn, dim3(a.grid), dim3(256), args, (size_t)a.smem, static_cast<cudaStream_t>(stream));
         if (e != cudaSuccess) return (int)e;
+        count_launch();
         return (int)cudaGetLastError();
     }
     int64_t blocks = (total + 255) / 256;
@@ -297,6 +298,7 @@ int launch_adjoint(int dtype, const AdjArgs &a, void *stream) {
     case FCFS_F16: fcfs_adjoint_kernel<__half><<<(int)blocks, 256, 0, s>>>(a); break;
     default: fcfs_adjoint_kernel<__nv_bfloat16><<<(int)blocks, 256, 0, s>>>(a); break;
     }
+    count_launch();
     return (int)cudaGetLastError();
 }
 

@@ -77,6 +77,7 @@ int launch_pdl(const void *fn, int grid, int block, void **args, int smem, void 
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
     if (e != cudaSuccess) return (int)e;
+    count_launch();
     return (int)cudaGetLastError();
 }
 

@@ -94,6 +94,7 @@ int launch_reference(int dtype, const RefArgs &a, void *stream) {
     case FCFS_F16: fcfs_reference_kernel<__half><<<(int)blocks, 256, 0, s>>>(a); break;
     default: fcfs_reference_kernel<__nv_bfloat16><<<(int)blocks, 256, 0, s>>>(a); break;
     }
+    count_launch();
     return (int)cudaGetLastError();
 }
 

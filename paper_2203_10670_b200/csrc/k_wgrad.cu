@@ -15,7 +15,7 @@
 
 namespace fcfs {
 
-template <typename T, int NT>
+template <typename T, int NT, int NTY>
 __global__ void __launch_bounds__(256) fcfs_wgrad_kernel(const __grid_constant__ WgradArgs a) {
     extern __shared__ __align__(16) float wsm[];
     float *xs = wsm;                          // [xrows][xcols]
@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(256) fcfs_wgrad_kernel(const __grid_constant__
     for (int i = 0; i < NT; ++i)
 #pragma unroll
         for (int k = 0; k < NT; ++k) acc[i][k] = 0.0f;
-    const int nty = a.nty;
+    constexpr int nty = NTY;  // rows of taps: NT (2D) or 1 (1D rows)
     for (int64_t task = blockIdx.x; task < a.ntasks; task += gridDim.x) {
         const int64_t plane = task / (a.nyb * a.nxb);
         const int tb = (int)(task - plane * a.nyb * a.nxb);
@@ -43,32 +43,68 @@ __global__ void __launch_bounds__(256) fcfs_wgrad_kernel(const __grid_constant__
         const T *gp = static_cast<const T *>(a.g) + plane * (int64_t)a.Ho * a.Wo;
         __syncthreads();  // the previous task's readers are done
         const int xr = (ny - 1) * a.qy + (a.xrows - (a.yb - 1) * a.qy), xc = (nx - 1) * a.qx + (a.xcols - (a.xb - 1) * a.qx);
-        for (int idx = threadIdx.x; idx < xr * xc; idx += blockDim.x) {
-            const int r = idx / xc, c = idx - r * xc;
-            const int sr = pad_src32(vr0 + r, a.H, a.pad), sc = pad_src32(vc0 + c, a.W, a.pad);
+        // padded x tile: a warp per row, lanes across columns (coalesced); the
+        // padding index map only where the tile leaves the image
+        const bool cols_in = vc0 >= 0 && vc0 + xc <= a.W;
+        for (int r = warp; r < xr; r += 8) {
+            const int sr = pad_src32(vr0 + r, a.H, a.pad);
             // reflect positions one bounce cannot reach feed no kept output (plan check): clamp
-            const int rr = min(max(sr, 0), a.H - 1), cc = min(max(sc, 0), a.W - 1);
-            xs[r * a.xcols + c] = (sr < 0 || sc < 0) && a.pad == FCFS_PAD_ZERO ? 0.0f
-                                                                                : DT<T>::to_f(xp[(int64_t)rr * a.W + cc]);
+            const int rr = min(max(sr, 0), a.H - 1);
+            const T *xrow = xp + (int64_t)rr * a.W;
+            float *srow = xs + r * a.xcols;
+            if (sr < 0 && a.pad == FCFS_PAD_ZERO) {
+                for (int c = lane; c < xc; c += 32) srow[c] = 0.0f;
+            } else if (cols_in) {
+#pragma unroll 4
+                for (int c = lane; c < xc; c += 32) srow[c] = DT<T>::to_f(xrow[vc0 + c]);
+            } else {
+                for (int c = lane; c < xc; c += 32) {
+                    const int sc = pad_src32(vc0 + c, a.W, a.pad);
+                    srow[c] = sc < 0 && a.pad == FCFS_PAD_ZERO ? 0.0f : DT<T>::to_f(xrow[min(max(sc, 0), a.W - 1)]);
+                }
+            }
         }
         const int gr = ny * a.py, gc = nx * a.px;
-        for (int idx = threadIdx.x; idx < gr * gc; idx += blockDim.x) {
-            const int r = idx / gc, c = idx - r * gc;
-            const int my = my0 + r, mx = mx0 + c;
-            gs[r * a.gcols + c] = (my < a.Ho && mx < a.Wo) ? DT<T>::to_f(gp[(int64_t)my * a.Wo + mx]) : 0.0f;
+        for (int r = warp; r < gr; r += 8) {
+            const int my = my0 + r;
+            float *srow = gs + r * a.gcols;
+            const T *grow = gp + (int64_t)my * a.Wo + mx0;
+            const int cval = my < a.Ho ? min(gc, a.Wo - mx0) : 0;  // columns inside the output
+#pragma unroll 4
+            for (int c = lane; c < gc; c += 32) srow[c] = c < cval ? DT<T>::to_f(grow[c]) : 0.0f;
         }
         __syncthreads();
         if (own) {
-            for (int it = warp; it < ny * nx; it += 8) {
-                const int iy = it / nx, ix = it - iy * nx;
-                const float gv = gs[(iy * a.py + jy) * a.gcols + ix * a.px + jx];
-                const float *xw = xs + (iy * a.qy + oy) * a.xcols + ix * a.qx + ox;
+            // one period's products into the lane's partial sums: x rows r0..r3 of its window
+            auto item = [&](float gv, const float *xw) {
 #pragma unroll
-                for (int ty = 0; ty < NT; ++ty) {
-                    if (ty < nty) {
+                for (int ty = 0; ty < NTY; ++ty) {
+                    const float *xr_ = xw + ty * a.xcols;
+                    if constexpr (NT % 2 == 0) {  // packed pairs (FFMA2: each lane one RN fma)
 #pragma unroll
-                        for (int tx = 0; tx < NT; ++tx) acc[ty][tx] = __fmaf_rn(gv, xw[ty * a.xcols + tx], acc[ty][tx]);
+                        for (int tx = 0; tx < NT; tx += 2) {
+                            const float2 r2 = ffma2_rn(gv, make_float2(xr_[tx], xr_[tx + 1]),
+                                                       make_float2(acc[ty][tx], acc[ty][tx + 1]));
+                            acc[ty][tx] = r2.x;
+                            acc[ty][tx + 1] = r2.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int tx = 0; tx < NT; ++tx) acc[ty][tx] = __fmaf_rn(gv, xr_[tx], acc[ty][tx]);
                     }
+                }
+            };
+            if (nx >= 8) {  // warp w: periods ix = w, w + 8, ... of every period row
+                const int gstep = 8 * a.px, xstep = 8 * a.qx;
+                for (int iy = 0; iy < ny; ++iy) {
+                    const float *gq = gs + (iy * a.py + jy) * a.gcols + warp * a.px + jx;
+                    const float *xq = xs + (iy * a.qy + oy) * a.xcols + warp * a.qx + ox;
+                    for (int ix = warp; ix < nx; ix += 8, gq += gstep, xq += xstep) item(*gq, xq);
+                }
+            } else {
+                for (int it = warp; it < ny * nx; it += 8) {
+                    const int iy = it / nx, ix = it - iy * nx;
+                    item(gs[(iy * a.py + jy) * a.gcols + ix * a.px + jx], xs + (iy * a.qy + oy) * a.xcols + ix * a.qx + ox);
                 }
             }
         }
@@ -95,10 +131,12 @@ int launch_wgrad(int dtype, const WgradArgs &a, int grid, int smem, void *stream
     const int nt = a.ntx, gy = (a.npairs + 31) / 32;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const void *fn = nullptr;
-#define FCFS_WG(TT)                                                                               \
-    fn = nt == 1 ? reinterpret_cast<const void *>(&fcfs_wgrad_kernel<TT, 1>)                      \
-                 : (nt == 2 ? reinterpret_cast<const void *>(&fcfs_wgrad_kernel<TT, 2>)           \
-                            : reinterpret_cast<const void *>(&fcfs_wgrad_kernel<TT, 4>));
+#define FCFS_WG(TT)                                                                                          \
+    fn = nt == 1   ? reinterpret_cast<const void *>(&fcfs_wgrad_kernel<TT, 1, 1>)                            \
+         : nt == 2 ? (a.nty == 1 ? reinterpret_cast<const void *>(&fcfs_wgrad_kernel<TT, 2, 1>)              \
+                                 : reinterpret_cast<const void *>(&fcfs_wgrad_kernel<TT, 2, 2>))             \
+                   : (a.nty == 1 ? reinterpret_cast<const void *>(&fcfs_wgrad_kernel<TT, 4, 1>)              \
+                                 : reinterpret_cast<const void *>(&fcfs_wgrad_kernel<TT, 4, 4>));
     switch (dtype) {
     case FCFS_F32: FCFS_WG(float) break;
     case FCFS_F16: FCFS_WG(__half) break;
@@ -111,6 +149,7 @@ int launch_wgrad(int dtype, const WgradArgs &a, int grid, int smem, void *stream
     void *args[] = {&local};
     e = cudaLaunchKernel(fn, dim3(grid, gy), dim3(256), args, (size_t)smem, s);
     if (e != cudaSuccess) return (int)e;
+    count_launch();
     return (int)cudaGetLastError();
 }
 

@@ -7,6 +7,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -18,6 +19,11 @@
 #include "fcfs_internal.h"
 
 using namespace fcfs;
+
+namespace fcfs {
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace fcfs
 
 struct fcfs_plan_s {
     int rank;                 // spatial rank as created: 1, 2 or 3 (fcfs_plan_ex: 2, or 1 with FCFS_FLAG_1D)
@@ -1170,7 +1176,8 @@ fcfs_status fcfs_run_weight_grad(fcfs_plan_t pl, const void *x, const void *grad
     a.npairs = a.py * a.px;
     const int span_x = fx_max + a.ntx - a.fx_min, span_y = fy_max + a.nty - a.fy_min;
     const int nix = (a.Wo + a.px - 1) / a.px, niy = (a.Ho + a.py - 1) / a.py;
-    const int budget = 48 * 1024;  // 4 CTAs per SM
+    int budget = 26 * 1024;  // 8 CTAs per SM: other CTAs compute while one stages its tiles
+    if (const char *e = std::getenv("FCFS_DEBUG_WG_BUDGET")) budget = std::atoi(e) * 1024;
     a.yb = 0;
     for (a.xb = std::min(nix, 64); a.xb >= 1 && a.yb == 0; a.xb = a.xb > 1 ? a.xb / 2 : 0) {
         a.xcols = (a.xb - 1) * a.qx + span_x;
@@ -1196,6 +1203,8 @@ fcfs_status fcfs_run_weight_grad(fcfs_plan_t pl, const void *x, const void *grad
     const int grid = (int)std::min<int64_t>(a.ntasks, (int64_t)pl->sm_count * per_sm);
     return launch_wgrad(pl->dtype, a, grid, smem, stream) == 0 ? FCFS_OK : FCFS_E_CUDA;
 }
+
+uint64_t fcfs_kernel_launches(void) { return fcfs::g_launches.load(std::memory_order_relaxed); }
 
 fcfs_status fcfs_plan_info(fcfs_plan_t pl, fcfs_plan_info_t *info) {
     if (!pl || !info) return FCFS_E_ARG;

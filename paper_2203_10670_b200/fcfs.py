@@ -225,6 +225,11 @@ class Plan:
         return out_host
 
 
+def kernel_launches() -> int:
+    """Kernels the library has launched (or captured into graphs) in this process (fcfs_kernel_launches)."""
+    return int(_lib.lib.fcfs_kernel_launches())
+
+
 def run_batch(jobs, stream=None):
     """Run [(plan, x, out), ...] (independent jobs) with fcfs_run_batch: compatible
     jobs share kernel launches.  Outputs must be preallocated."""

@@ -103,6 +103,7 @@ class Config:
     pd: tuple | None = None          # per-dimension factors (outermost first): an ND plan (§4.2)
     qd: tuple | None = None
     backward: bool = False           # the adjoint launch: input = grad_out (N(0,1)), output = grad_in
+    wgrad: bool = False              # the weight gradient: inputs x (the config's) and grad_out (N(0,1))
 
     @property
     def planes(self) -> int:
@@ -153,6 +154,9 @@ CONFIGS.update({
 # The backward pass of config 3: grad_in = A^T grad_out
 # for the FCN feature-map resize, grad_out N(0,1) bf16 of the forward output shape.
 CONFIGS["C3B"] = dataclasses.replace(CONFIGS["C3"], name="C3B", backward=True, seed=SEED_BASE + 31)
+# ... and the gradient of its learnable taps (reading Z22): x of config 3 and a
+# N(0,1) bf16 grad_out of the forward output shape -> 5 x 5 x 4 x 4 fp32
+CONFIGS["C3W"] = dataclasses.replace(CONFIGS["C3"], name="C3W", wgrad=True, seed=SEED_BASE + 32)
 
 # bench workloads: a step = one pass over one batch, every launch of the config
 WORKLOADS = {
@@ -166,6 +170,7 @@ WORKLOADS = {
     "V1": ["V1"],
     "V2": ["V2"],
     "C3B": ["C3B"],
+    "C3W": ["C3W"],
 }
 
 

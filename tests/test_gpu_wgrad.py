@@ -119,3 +119,21 @@ def test_weight_grad_exact_on_integer_inputs(dtype):
         ref, ab = oracle.weight_grad(oracle_input(x), g.double().numpy(), p, q, mode, pad, floor_extent=True)
         assert ab.max() < 2 ** 24
         assert np.array_equal(gw.cpu().double().numpy(), ref), (p, q, mode, pad, dtype)
+
+
+def test_kernel_launch_counter():
+    """fcfs_kernel_launches counts the library's kernels (the bench's gpu_launches):
+    one per forward run, one per weight gradient, two for a replicate-padded 2D
+    adjoint (fused interior + border bands)."""
+    pl = Plan(5, 3, "bicubic", "replicate", 2, 40, 48, "float32", "floor")
+    x = torch.from_numpy(synth.normal_f32(30, 2 * 2 * 40 * 48).reshape(2, 2, 40, 48)).to(DEV)
+    n0 = fc.kernel_launches()
+    y = pl.run(x)
+    assert fc.kernel_launches() - n0 == 1
+    n0 = fc.kernel_launches()
+    pl.run_weight_grad(x, y)
+    assert fc.kernel_launches() - n0 == 1
+    n0 = fc.kernel_launches()
+    pl.run_adjoint(y)
+    assert fc.kernel_launches() - n0 == 2
+    torch.cuda.synchronize()

@@ -33,6 +33,30 @@ def time_cfg(name, reps, env):
         pl = fc.Plan.nd(c.pd, c.qd, c.mode, c.pad, c.C, c.dims, c.dtype, "floor")
     else:
         pl = fc.Plan(c.p, c.q, c.mode, c.pad, c.C, c.H, c.W, c.dtype, "floor", c.is1d)
+    if c.wgrad:  # the weight gradient: (x, grad_out) -> grad_w
+        x = synth.make_input(c).cuda()
+        shp = pl.out_shape(c.N)
+        g = torch.from_numpy(synth.normal_f32(c.seed + 7, int(np.prod(shp))).reshape(shp)).to(getattr(torch, c.dtype)).cuda()
+        R = max(2, min(8, int(4 * 126e6 // ((x.numel() + g.numel()) * x.element_size())) + 1))
+        xs = [x.clone() for _ in range(R)]
+        gs = [g.clone() for _ in range(R)]
+        gw = torch.empty(pl.weight_grad_shape(), device="cuda")
+        fn = lambda i: pl.run_weight_grad(xs[i % R], gs[i % R], out=gw)
+        for i in range(3):
+            fn(i)
+        torch.cuda.synchronize()
+        ts = []
+        for rep in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for i in range(reps):
+                fn(i)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3 / reps)
+        ts.sort()
+        med = ts[len(ts) // 2]
+        return med, (x.numel() + g.numel()) * x.element_size() / (med * 1e-6) / 1e9, {}
     if c.backward:  # the adjoint: grad_out -> grad_in
         shp = pl.out_shape(c.N)
         x = torch.from_numpy(synth.normal_f32(c.seed, int(np.prod(shp))).reshape(shp)).to(getattr(torch, c.dtype)).cuda()
