@@ -12,17 +12,17 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 [ -n "$ONLY_FULL" ] && { NO_BENCH=1; }
 if [ -z "$NO_BENCH" ]; then
 timeout 600 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo "bench default rc=$?"
-for w in ${WL:-C2 C3 C4 C5 A1 A2 V1 V2 C3B}; do
+for w in ${WL:-C2 C3 C4 C5 A1 A2 V1 V2 C3B C3W}; do
   timeout 600 python bench.py --workload $w --no-cpu-baseline > $O/bench_$w.json 2> $O/bench_$w.err; echo "bench $w rc=$?"
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err; echo "bench reference rc=$?"
 fi
-for w in ${NW:-C2 C3 C4 C5 A1 V1 V2 C3B}; do
+for w in ${NW:-C2 C3 C4 C5 A1 V1 V2 C3B C3W}; do
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_$w.csv \
   python bench.py --workload $w --steps 2 --warmup 3 --soak-s 0 --no-e2e --no-cpu-baseline > $O/ncu_launch_$w.log 2>&1; echo "ncu launches $w rc=$?"
 done
 [ -n "$NO_FULL" ] && exit 0
-for w in ${NW:-C2 C3 C4 C5 A1 V1 V2 C3B}; do
+for w in ${NW:-C2 C3 C4 C5 A1 V1 V2 C3B C3W}; do
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fcfs -s 4 -c 2 -o $O/full_$w -f \
   python bench.py --workload $w --steps 2 --warmup 3 --soak-s 0 --no-e2e --no-cpu-baseline > $O/ncu_full_$w.log 2>&1; echo "ncu full $w rc=$?"
   # summaries on the box (raw reports exceed the copy-back limit); keep the SASS mix too
