@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--impl", default="fcfs", choices=["fcfs", "reference"])
     ap.add_argument("--soak-s", type=float, default=1.0, help="untimed steady-state run before warm-up (clocks)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--halo", default="nccl", choices=["nccl", "peer"],
+                    help="C5 row strips at N > 1: NCCL send/recv halo, or in-kernel peer reads (symmetric memory)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 

@@ -186,6 +186,24 @@ fcfs_status fcfs_strip_rows(fcfs_plan_t plan, int64_t own_in_row0, int64_t own_i
 fcfs_status fcfs_needed_rows(fcfs_plan_t plan, int64_t out_row0, int64_t out_row1, int64_t *need_row0,
                              int64_t *need_row1);
 
+/* fcfs_run_rows_segments -- output rows [out_row0, out_row0 + out_nrows) of a
+ * 2D plan from input rows held in up to 3 disjoint row windows instead of one
+ * contiguous buffer: window k holds global rows [seg_row0[k], seg_row0[k] +
+ * seg_nrows[k]) of all N x C planes (N x C x seg_nrows[k] x W, the plan dtype).
+ * The kernel reads every row from the window that holds it, so a row-strip
+ * rank can take its halo rows straight out of its neighbours' strips through
+ * peer (NVLink) pointers, with no copy or send/recv (
+ * the halo of §8(e)).  One thread per output (the reference kernel: the same
+ * arithmetic contract as every other path, so strips assembled this way equal
+ * the single-launch image bit for bit).  Asynchronous on `stream`; the caller
+ * orders the windows' writes before the launch (e.g. a device barrier).
+ * Errors: FCFS_E_ARG (NULL, nseg outside 1..3, windows outside [0, H) or
+ * overlapping), FCFS_E_UNSUPPORTED (rank != 2 or 1D), FCFS_E_SHAPE (a needed
+ * row in no window), FCFS_E_DEVICE, FCFS_E_CUDA. */
+fcfs_status fcfs_run_rows_segments(fcfs_plan_t plan, int nseg, const void *const *seg_rows, const int64_t *seg_row0,
+                                   const int64_t *seg_nrows, void *out_rows, int64_t out_row0, int64_t out_nrows,
+                                   int64_t N, void *stream);
+
 /* fcfs_run_host -- the end-to-end call with HOST buffers: copies host_in
  * (N x C x H x W, ideally pinned) to dev_in, runs, copies dev_out to
  * host_out (N x C x Ho x Wo), all asynchronously on stream.  dev_in/dev_out

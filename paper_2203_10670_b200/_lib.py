@@ -43,6 +43,7 @@ SIGNATURES = {
     "fcfs_output_shape": (i32, [vp, P64, P64]),
     "fcfs_run": (i32, [vp, vp, vp, i64, vp]),
     "fcfs_run_rows": (i32, [vp, vp, i64, i64, vp, i64, i64, i64, vp]),
+    "fcfs_run_rows_segments": (i32, [vp, i32, ctypes.POINTER(vp), P64, P64, vp, i64, i64, i64, vp]),
     "fcfs_run_batch": (i32, [vp, i32, vp]),
     "fcfs_strip_rows": (i32, [vp, i64, i64, P64, P64, P64, P64]),
     "fcfs_needed_rows": (i32, [vp, i64, i64, P64, P64]),

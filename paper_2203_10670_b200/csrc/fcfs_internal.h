@@ -42,6 +42,11 @@ struct RefArgs {         // reference kernel: one thread per output
     PhaseTable tx, ty, tz;  // W, H, D dimensions (ty unused with is1d, tz the identity in 2D)
     int pad;
     int is1d;
+    // nseg > 0 (2D, fcfs_run_rows_segments): input rows come from nseg row windows
+    // (each N*C planes of seg_nrows rows, possibly another GPU's memory) instead of g.in
+    int nseg;
+    const void *seg_in[3];
+    int64_t seg_row0[3], seg_nrows[3];
 };
 
 struct TileArgs {        // tiled kernel (k_tile.cu): output tiles with a shared-memory window

@@ -16,7 +16,9 @@
 // __fmul_rn then __fmaf_rn in tap order: slices first, then columns, then
 // rows; §4.2's kernels are outer products, so any order is the same real
 // number -- this one is the contract).  Nearest (one tap) is a pure copy.  1D
-// plans (FCFS_FLAG_1D) take out = hx(m_y).
+// plans (FCFS_FLAG_1D) take out = hx(m_y).  With row segments (RefArgs::nseg,
+// fcfs_run_rows_segments) each input row is read from the window holding it --
+// e.g. a neighbour GPU's strip through a peer pointer.
 #include "device_common.cuh"
 
 namespace fcfs {
@@ -24,11 +26,17 @@ namespace fcfs {
 // slice pass at (row r, column c), virtual indices, padding applied
 template <typename T>
 __device__ __forceinline__ float xzval(const T *__restrict__ plane, const RefArgs &a, int jz, int64_t bz, int64_t r,
-                                       int64_t c) {
+                                       int64_t c, int64_t pidx) {
     const RunGeom &g = a.g;
     auto at = [&](int64_t sl) -> float {
         const int64_t ss = pad_src(sl, g.D, a.pad), rs = pad_src(r, g.H, a.pad), cs = pad_src(c, g.W, a.pad);
         if (ss < 0 || rs < 0 || cs < 0) return 0.0f;
+        if (a.nseg > 0) {  // row windows (2D): the one holding global row rs
+            int k = 0;
+            while (k + 1 < a.nseg && !(rs >= a.seg_row0[k] && rs < a.seg_row0[k] + a.seg_nrows[k])) ++k;
+            const T *sp = static_cast<const T *>(a.seg_in[k]) + pidx * a.seg_nrows[k] * g.W;
+            return DT<T>::to_f(sp[(rs - a.seg_row0[k]) * g.W + cs]);
+        }
         return DT<T>::to_f(plane[(ss * g.in_nrows + rs - g.in_row0) * g.W + cs]);
     };
     if (jz == 0 || a.tz.ntaps == 1) return at(bz);
@@ -40,10 +48,11 @@ __device__ __forceinline__ float xzval(const T *__restrict__ plane, const RefArg
 // column pass of row r
 template <typename T>
 __device__ __forceinline__ float hxval(const T *__restrict__ plane, const RefArgs &a, int jz, int64_t bz, int64_t r,
-                                       int jx, int64_t bx) {
-    if (jx == 0 || a.tx.ntaps == 1) return xzval(plane, a, jz, bz, r, bx);
-    float v = __fmul_rn(a.tx.w[jx][0], xzval(plane, a, jz, bz, r, bx + a.tx.lo));
-    for (int t = 1; t < a.tx.ntaps; ++t) v = __fmaf_rn(a.tx.w[jx][t], xzval(plane, a, jz, bz, r, bx + a.tx.lo + t), v);
+                                       int jx, int64_t bx, int64_t pidx) {
+    if (jx == 0 || a.tx.ntaps == 1) return xzval(plane, a, jz, bz, r, bx, pidx);
+    float v = __fmul_rn(a.tx.w[jx][0], xzval(plane, a, jz, bz, r, bx + a.tx.lo, pidx));
+    for (int t = 1; t < a.tx.ntaps; ++t)
+        v = __fmaf_rn(a.tx.w[jx][t], xzval(plane, a, jz, bz, r, bx + a.tx.lo + t, pidx), v);
     return v;
 }
 
@@ -60,23 +69,23 @@ __global__ void __launch_bounds__(256) fcfs_reference_kernel(const __grid_consta
         const int64_t mz = t % g.Do;
         const int64_t plane = t / g.Do;
         const int64_t my = g.out_row0 + lr;
-        const T *src = static_cast<const T *>(g.in) + plane * g.in_plane_stride;
+        const T *src = a.nseg > 0 ? nullptr : static_cast<const T *>(g.in) + plane * g.in_plane_stride;
         const int jx = (int)(mx % a.tx.p);
         const int64_t bx = (mx / a.tx.p) * a.tx.q + a.tx.base[jx];
         const int jz = (int)(mz % a.tz.p);
         const int64_t bz = (mz / a.tz.p) * a.tz.q + a.tz.base[jz];
         float out;
         if (a.is1d) {
-            out = hxval(src, a, 0, 0, my, jx, bx);
+            out = hxval(src, a, 0, 0, my, jx, bx, plane);
         } else {
             const int jy = (int)(my % a.ty.p);
             const int64_t by = (my / a.ty.p) * a.ty.q + a.ty.base[jy];
             if (jy == 0 || a.ty.ntaps == 1) {
-                out = hxval(src, a, jz, bz, by, jx, bx);
+                out = hxval(src, a, jz, bz, by, jx, bx, plane);
             } else {
-                out = __fmul_rn(a.ty.w[jy][0], hxval(src, a, jz, bz, by + a.ty.lo, jx, bx));
+                out = __fmul_rn(a.ty.w[jy][0], hxval(src, a, jz, bz, by + a.ty.lo, jx, bx, plane));
                 for (int k = 1; k < a.ty.ntaps; ++k)
-                    out = __fmaf_rn(a.ty.w[jy][k], hxval(src, a, jz, bz, by + a.ty.lo + k, jx, bx), out);
+                    out = __fmaf_rn(a.ty.w[jy][k], hxval(src, a, jz, bz, by + a.ty.lo + k, jx, bx, plane), out);
             }
         }
         static_cast<T *>(g.out)[plane * g.out_plane_stride + (mz * g.out_nrows + lr) * g.Wo + mx] = DT<T>::from_f(out);

@@ -586,6 +586,7 @@ fcfs_status prepare(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t in_
         plan_tile(pl, g, pr.ta, pr.tgrid, pr.tsmem, nullptr, 0);
     } else if (pr.kernel == 0) {
         RefArgs &a = pr.ra;
+        std::memset(&a, 0, sizeof(a));
         a.g = g;
         a.tx = pl->tab;
         a.ty = pl->taby;
@@ -788,6 +789,60 @@ fcfs_status fcfs_run(fcfs_plan_t pl, const void *in, void *out, int64_t N, void 
 fcfs_status fcfs_run_rows(fcfs_plan_t pl, const void *in_rows, int64_t in_row0, int64_t in_nrows, void *out_rows,
                           int64_t out_row0, int64_t out_nrows, int64_t N, void *stream) {
     return run_window(pl, in_rows, in_row0, in_nrows, out_rows, out_row0, out_nrows, N, stream);
+}
+
+fcfs_status fcfs_run_rows_segments(fcfs_plan_t pl, int nseg, const void *const *seg_rows, const int64_t *seg_row0,
+                                   const int64_t *seg_nrows, void *out_rows, int64_t out_row0, int64_t out_nrows,
+                                   int64_t N, void *stream) {
+    if (!pl || nseg < 1 || nseg > 3 || !seg_rows || !seg_row0 || !seg_nrows) return FCFS_E_ARG;
+    if (pl->rank != 2 || pl->is1d) return FCFS_E_UNSUPPORTED;
+    for (int k = 0; k < nseg; ++k) {
+        if (!seg_rows[k] || seg_row0[k] < 0 || seg_nrows[k] < 1 || seg_row0[k] + seg_nrows[k] > pl->H) return FCFS_E_ARG;
+        for (int j = 0; j < k; ++j)  // windows are disjoint
+            if (seg_row0[k] < seg_row0[j] + seg_nrows[j] && seg_row0[j] < seg_row0[k] + seg_nrows[k]) return FCFS_E_ARG;
+    }
+    if (out_row0 < 0 || out_nrows < 0 || out_row0 + out_nrows > pl->Ho) return FCFS_E_ARG;
+    if (N < 0) return FCFS_E_ARG;
+    if (N == 0 || out_nrows == 0) return FCFS_OK;
+    if (!out_rows) return FCFS_E_ARG;
+    // every needed row lies in some window (the windows' union is read row by row)
+    int64_t n0, n1;
+    needed_rows(pl, out_row0, out_row0 + out_nrows, &n0, &n1);
+    for (int64_t r = n0; r < n1; ++r) {
+        bool in = false;
+        for (int k = 0; k < nseg && !in; ++k) in = r >= seg_row0[k] && r < seg_row0[k] + seg_nrows[k];
+        if (!in) return FCFS_E_SHAPE;
+    }
+    fcfs_status st = check_device(pl);
+    if (st != FCFS_OK) return st;
+    RefArgs a;
+    std::memset(&a, 0, sizeof(a));
+    RunGeom &g = a.g;
+    g.in = seg_rows[0];
+    g.out = out_rows;
+    g.planes = N * pl->C;
+    g.D = g.Do = 1;
+    g.H = pl->H;
+    g.W = pl->W;
+    g.Ho = pl->Ho;
+    g.Wo = pl->Wo;
+    g.in_row0 = seg_row0[0];
+    g.in_nrows = seg_nrows[0];
+    g.out_row0 = out_row0;
+    g.out_nrows = out_nrows;
+    g.in_plane_stride = seg_nrows[0] * pl->W;
+    g.out_plane_stride = out_nrows * pl->Wo;
+    a.tx = pl->tab;
+    a.ty = pl->taby;
+    a.tz = pl->tabz;
+    a.pad = pl->pad;
+    a.nseg = nseg;
+    for (int k = 0; k < nseg; ++k) {
+        a.seg_in[k] = seg_rows[k];
+        a.seg_row0[k] = seg_row0[k];
+        a.seg_nrows[k] = seg_nrows[k];
+    }
+    return launch_reference(pl->dtype, a, stream) == 0 ? FCFS_OK : FCFS_E_CUDA;
 }
 
 fcfs_status fcfs_strip_rows(fcfs_plan_t pl, int64_t own0, int64_t own1, int64_t *out0, int64_t *out1, int64_t *need0,

@@ -15,6 +15,15 @@ Two shardings:
 
 The exchange plan is pure host logic (tested on CPU with gloo, world size 2);
 all arithmetic runs in libfcfs.so.
+
+Transport "peer" (in-kernel NVLink halo): every rank's
+strip lives in symmetric memory (torch.distributed._symmetric_memory); the
+boundary output rows are computed by one launch that reads the halo rows
+straight out of the neighbours' strips through peer pointers
+(fcfs_run_rows_segments) -- no send/recv, no copy, no halo buffer -- after a
+device-side barrier on the stream.  The window logic (peer_windows) is host
+logic, tested on CPU; the kernel's multi-window reads are tested on one GPU
+with local buffers standing in for the peers.
 """
 from __future__ import annotations
 
@@ -111,6 +120,32 @@ def exchange(local, lay: StripLayout, group=None):
     return works, staged
 
 
+def peer_windows(plan, rank: int, world: int):
+    """Row windows a rank reads in peer mode: its own strip and every
+    neighbour strip that holds one of its needed rows, as (peer rank, row0,
+    row1) over whole strips (a strip is one contiguous N x C x rows x W
+    tensor).  Pure host logic."""
+    lay = strip_layout(plan, rank, world)
+    wins = [(rank, lay.own0, lay.own1)]
+    for t in lay.recvs:
+        o0, o1 = own_rows(plan.H, t.peer, world)
+        if (t.peer, o0, o1) not in wins:
+            wins.append((t.peer, o0, o1))
+    if len(wins) > 3:
+        raise ValueError("a strip needs rows of more than two neighbours (strips thinner than the halo)")
+    return lay, wins
+
+
+def boundary_ranges(lay: StripLayout):
+    """Output rows of a strip outside its interior (they read halo rows)."""
+    i0, i1 = lay.interior
+    if lay.out1 <= lay.out0:
+        return []
+    if i1 <= i0:
+        return [(lay.out0, lay.out1)]
+    return [r for r in ((lay.out0, i0), (i1, lay.out1)) if r[1] > r[0]]
+
+
 def finish_exchange(works, staged):
     for w in works:
         w.wait()
@@ -119,11 +154,64 @@ def finish_exchange(works, staged):
 
 
 class StripRunner:
-    """Run one FCFS plan over a row-strip-sharded image on this rank's GPU."""
+    """Run one FCFS plan over a row-strip-sharded image on this rank's GPU.
 
-    def __init__(self, plan, rank: int, world: int, group=None):
-        self.plan, self.group = plan, group
+    transport "nccl": halo rows by send/recv into the local buffer (own rows +
+    halo); "peer": the local buffer is this rank's strip in symmetric memory and
+    the boundary rows read the neighbours' strips in place (setup_peer)."""
+
+    def __init__(self, plan, rank: int, world: int, group=None, transport: str = "nccl"):
+        if transport not in ("nccl", "peer"):
+            raise ValueError(transport)
+        self.plan, self.group, self.rank, self.world = plan, group, rank, world
+        self.transport = transport
         self.lay = strip_layout(plan, rank, world)
+        self.hdl = None
+
+    def setup_peer(self, N: int, dtype, device):
+        """Allocate this rank's strip in symmetric memory (the same allocation
+        size on every rank: the largest strip) and map the neighbour strips this
+        rank reads.  Returns the local strip (N, C, own rows, W) to fill."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        pl = self.plan
+        lay, wins = peer_windows(pl, self.rank, self.world)
+        rows_max = max(own_rows(pl.H, r, self.world)[1] - own_rows(pl.H, r, self.world)[0] for r in range(self.world))
+        group = self.group or dist.group.WORLD
+        buf = symm_mem.empty((N, pl.C, rows_max, pl.W), dtype=dtype, device=device)
+        self.hdl = symm_mem.rendezvous(buf, group.group_name if hasattr(group, "group_name") else group)
+        own = lay.own1 - lay.own0
+        self.local = buf[:, :, :own] if own < rows_max else buf
+        if not self.local.is_contiguous():  # N * C > 1 with a short strip: a contiguous prefix view
+            self.local = buf.view(-1)[: N * pl.C * own * pl.W].view(N, pl.C, own, pl.W)
+        self.windows = []
+        for peer, r0, r1 in wins:
+            t = self.local if peer == self.rank else self.hdl.get_buffer(peer, (N, pl.C, r1 - r0, pl.W), dtype)
+            self.windows.append((t, r0))
+        return self.local
+
+    def run_peer(self, out):
+        """Peer transport: barrier (the neighbours' strips are written and my
+        previous reads of theirs are done), interior rows from my strip (fused
+        kernel), boundary rows from my strip + the neighbours' (one launch)."""
+        lay, pl = self.lay, self.plan
+        self.hdl.barrier()
+        if lay.out1 <= lay.out0:
+            return out
+        i0, i1 = lay.interior
+        if i1 > i0:
+            dst = out[:, :, i0 - lay.out0:i1 - lay.out0]
+            if dst.is_contiguous():
+                pl.run_rows(self.local, lay.own0, i0, i1 - i0, out=dst)
+            else:
+                dst.copy_(pl.run_rows(self.local, lay.own0, i0, i1 - i0))
+        for m0, m1 in boundary_ranges(lay):
+            dst = out[:, :, m0 - lay.out0:m1 - lay.out0]
+            if dst.is_contiguous():
+                pl.run_rows_segments(self.windows, m0, m1 - m0, out=dst)
+            else:
+                dst.copy_(pl.run_rows_segments(self.windows, m0, m1 - m0))
+        return out
 
     def alloc_local(self, N: int, dtype, device):
         import torch
@@ -185,15 +273,21 @@ def bench_strips(args, cfg, rank, world, dev, metric):
     from bench import ClockSampler, DTYPE_TAG, peaks, physical_gpu_index
 
     pl = fc.Plan(cfg.p, cfg.q, cfg.mode, cfg.pad, cfg.C, cfg.H, cfg.W, cfg.dtype, "floor")
-    sr = StripRunner(pl, rank, world)
+    halo = getattr(args, "halo", "nccl")
+    sr = StripRunner(pl, rank, world, transport=halo)
     lay = sr.lay
     x_own = synth.make_input(cfg, rows=(lay.own0, lay.own1)).to(dev)
     stream = torch.cuda.current_stream(dev)
     R = 3  # rotating local/output buffers (each >= 4 x 32768 x 4 KB)
-    locs = [sr.alloc_local(1, x_own.dtype, dev) for _ in range(R)]
     outs = [sr.alloc_out(1, x_own.dtype, dev) for _ in range(R)]
-    for l in locs:
-        sr.own_view(l).copy_(x_own)
+    if halo == "peer":  # one symmetric-memory strip per rank; neighbours read it in place
+        sr.setup_peer(1, x_own.dtype, dev).copy_(x_own)
+        locs = [None] * R
+        sr.run = lambda local, out: sr.run_peer(out)
+    else:
+        locs = [sr.alloc_local(1, x_own.dtype, dev) for _ in range(R)]
+        for l in locs:
+            sr.own_view(l).copy_(x_own)
     torch.cuda.synchronize(dev)
     sampler = ClockSampler(physical_gpu_index(int(os.environ.get("LOCAL_RANK", "0"))))
     sampler.start()
@@ -210,10 +304,12 @@ def bench_strips(args, cfg, rank, world, dev, metric):
     dist.barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_launch0 = fc.kernel_launches()
     e0.record(stream)
     for s in range(args.steps):
         sr.run(locs[s % R], outs[s % R])
     e1.record(stream)
+    n_launches = fc.kernel_launches() - n_launch0
     torch.cuda.synchronize(dev)
     t1 = time.time()
     dist.barrier()
@@ -236,13 +332,15 @@ def bench_strips(args, cfg, rank, world, dev, metric):
             "data": "synthetic",
             "config": {"workload": "C5", "shape": [1, 1, cfg.H, cfg.W], "factor": f"{cfg.p}/{cfg.q}",
                        "mode": cfg.mode, "pad": cfg.pad, "out": [pl.Ho, pl.Wo],
-                       "parallelism": f"row strips x{world}, NCCL halo send/recv, interior overlapped",
+                       "parallelism": (f"row strips x{world}, NCCL halo send/recv, interior overlapped" if halo == "nccl"
+                                       else f"row strips x{world}, halo rows read in-kernel from the neighbours' "
+                                            "symmetric-memory strips (peer pointers), device barrier per step"),
                        "l2": "working set per rank > L2; 3 rotating buffer sets"},
             "achieved_GBps_step": total_bytes / (ms_step * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
                          "note": "per-rank bytes / max-over-ranks step time (exchange included)"},
-            "gpu_launches": args.steps * 3, "clocks": clocks}
+            "gpu_launches": n_launches, "clocks": clocks}
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

@@ -176,6 +176,30 @@ class Plan:
                                         N, self._stream(stream)), "fcfs_run_adjoint")
         return out
 
+    def run_rows_segments(self, windows, out_row0: int, out_nrows: int, out=None, stream=None):
+        """Output rows [out_row0, out_row0+out_nrows) from up to 3 row windows
+        [(tensor (N, C, nrows, W), global row0), ...] -- e.g. neighbour strips read
+        in place through peer pointers (fcfs_run_rows_segments)."""
+        import torch
+        if not 1 <= len(windows) <= 3:
+            raise ValueError("1 to 3 row windows")
+        N = windows[0][0].shape[0]
+        ptrs, r0s, nrs = [], [], []
+        for t, r0 in windows:
+            self._check_tensor(t, (N, self.C, t.shape[2], self.W), "row window")
+            ptrs.append(t.data_ptr())
+            r0s.append(r0)
+            nrs.append(t.shape[2])
+        oshape = (N, self.C, out_nrows, self.Wo)
+        if out is None:
+            out = torch.empty(oshape, dtype=windows[0][0].dtype, device=windows[0][0].device)
+        self._check_tensor(out, oshape, "output rows")
+        n = len(windows)
+        check(_lib.lib.fcfs_run_rows_segments(self._h, n, (ctypes.c_void_p * n)(*ptrs), (ctypes.c_int64 * n)(*r0s),
+                                              (ctypes.c_int64 * n)(*nrs), ctypes.c_void_p(out.data_ptr()), out_row0,
+                                              out_nrows, N, self._stream(stream)), "fcfs_run_rows_segments")
+        return out
+
     def weight_grad_shape(self):
         """(py, px, nty, ntx) of the learnable taps (fcfs_weight_grad_shape; reading Z22)."""
         d = (ctypes.c_int64 * 4)()

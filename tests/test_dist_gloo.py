@@ -96,3 +96,36 @@ def test_strip_exchange_gloo(world, case):
     for r in results:
         for peer, r0, r1 in r["sent"]:
             assert abs(peer - r["rank"]) == 1 and 0 < r1 - r0 <= 2
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_peer_windows_cover_and_reproduce(case):
+    """Peer transport: the windows a rank reads -- its own
+    strip and whole neighbour strips -- cover every input row its output rows
+    need, number at most 3, and the oracle evaluated on exactly those rows
+    (the strips concatenated in row order) reproduces the whole image's rows."""
+    import oracle
+    import synth
+    import paper_2203_10670_b200 as fc
+    from paper_2203_10670_b200.dist import boundary_ranges, own_rows, peer_windows
+    p, q, mode, pad, H, W, N, C = case
+    pl = fc.Plan(p, q, mode, pad, C, H, W, "float32", "floor")
+    cfg = synth.Config("peer", N, C, H, W, "float32", "uniform", p, q, mode, pad, seed=4343)
+    full = synth.make_values(cfg)
+    whole = oracle.direct(full, p, q, mode, pad, floor_extent=True)
+    for world in (2, 3, 5):
+        for rank in range(world):
+            lay, wins = peer_windows(pl, rank, world)
+            assert 1 <= len(wins) <= 3 and wins[0] == (rank, lay.own0, lay.own1)
+            for peer, r0, r1 in wins:
+                assert (r0, r1) == own_rows(H, peer, world)
+            if lay.out1 <= lay.out0:
+                continue
+            rows = sorted((r0, r1) for _, r0, r1 in wins)
+            lo, hi = rows[0][0], rows[-1][1]
+            assert all(rows[k][1] == rows[k + 1][0] for k in range(len(rows) - 1))  # adjacent strips
+            assert lo <= lay.need0 and lay.need1 <= hi
+            for m0, m1 in boundary_ranges(lay):
+                mine = oracle.direct(full[:, :, lo:hi], p, q, mode, pad, floor_extent=True, rows=(m0, m1), H=H,
+                                     row0=lo)
+                assert np.array_equal(mine, whole[:, :, m0:m1]), (world, rank, m0, m1)

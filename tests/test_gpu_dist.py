@@ -73,3 +73,53 @@ def test_strip_layouts_reproduce_whole_image(G):
                 out[:, :, a - lay.out0:b - lay.out0] = pl.run_rows(local, lay.loc0, a, b - a)
         parts.append(out)
     assert torch.equal(torch.cat(parts, dim=2), whole)
+
+
+def test_run_rows_segments_equals_contiguous_rows():
+    """fcfs_run_rows_segments (the peer-halo launch) with three
+    separate buffers standing in for a rank's strip and its neighbours' strips:
+    bit-identical to the rows of the single launch (one arithmetic contract)."""
+    import paper_2203_10670_b200 as fc
+    from paper_2203_10670_b200._lib import FcfsError
+    for (p, q, mode, pad, dtype, N, C) in [(3, 5, "bicubic", "replicate", "float32", 1, 1),
+                                           (5, 3, "bicubic", "reflect", "bfloat16", 2, 3),
+                                           (7, 5, "bilinear", "zero", "float16", 1, 2)]:
+        H, W = 301, 257
+        pl = fc.Plan(p, q, mode, pad, C, H, W, dtype, "floor")
+        x = torch.from_numpy(synth.normal_f32(55, N * C * H * W).reshape(N, C, H, W)).to(getattr(torch, dtype)).cuda()
+        whole = pl.run(x)
+        cuts = [0, 97, 205, H]
+        strips = [(x[:, :, a:b].contiguous(), a) for a, b in zip(cuts[:-1], cuts[1:])]
+        for s in range(3):
+            o0, o1, n0, n1 = pl.strip_rows(cuts[s], cuts[s + 1])
+            wins = [strips[s]] + [strips[k] for k in (s - 1, s + 1) if 0 <= k < 3]
+            got = pl.run_rows_segments(wins, o0, o1 - o0)
+            assert torch.equal(got.view(torch.uint8), whole[:, :, o0:o1].contiguous().view(torch.uint8)), (p, q, s)
+        # a needed row in no window / overlapping windows
+        o0, o1, n0, n1 = pl.strip_rows(97, 205)
+        with pytest.raises(FcfsError) as e:
+            pl.run_rows_segments([strips[1]], o0, o1 - o0)
+        assert e.value.name == "FCFS_E_SHAPE"
+        with pytest.raises(FcfsError) as e:
+            pl.run_rows_segments([strips[1], (x[:, :, 90:100].contiguous(), 90)], o0, o1 - o0)
+        assert e.value.name == "FCFS_E_ARG"
+
+
+def test_strip_runner_peer_transport_world1(pg):
+    """The symmetric-memory setup and run path of the peer transport on one GPU
+    (world 1: no neighbours, every row interior) equals the single launch."""
+    import paper_2203_10670_b200 as fc
+    from paper_2203_10670_b200.dist import StripRunner
+    try:
+        import torch.distributed._symmetric_memory  # noqa: F401
+    except Exception as e:  # pragma: no cover
+        pytest.skip(f"symmetric memory unavailable: {e}")
+    pl = fc.Plan(3, 5, "bicubic", "replicate", 1, 600, 512, "float32", "floor")
+    x = torch.from_numpy(synth.normal_f32(56, 600 * 512).reshape(1, 1, 600, 512)).cuda()
+    sr = StripRunner(pl, 0, 1, transport="peer")
+    local = sr.setup_peer(1, torch.float32, torch.device("cuda", 0))
+    local.copy_(x)
+    out = sr.alloc_out(1, torch.float32, torch.device("cuda", 0))
+    sr.run_peer(out)
+    torch.cuda.synchronize()
+    assert torch.equal(out, pl.run(x))
