@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define FCFS_VERSION 2
+#define FCFS_VERSION 3
 #define FCFS_MAX_FACTOR 64 /* p and q (after gcd reduction) must be <= 64 */
 
 typedef struct fcfs_plan_s *fcfs_plan_t;
