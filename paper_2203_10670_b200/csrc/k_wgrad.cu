@@ -31,6 +31,31 @@ __global__ void __launch_bounds__(256) fcfs_wgrad_kernel(const __grid_constant__
 #pragma unroll
         for (int k = 0; k < NT; ++k) acc[i][k] = 0.0f;
     constexpr int nty = NTY;  // rows of taps: NT (2D) or 1 (1D rows)
+    // L2 prefetch of a task's x and grad_out rows (one row per thread): the
+    // synchronous tile staging of the next task then hits L2
+    auto prefetch = [&](int64_t task) {
+        if (task >= a.ntasks) return;
+        const int64_t plane = task / (a.nyb * a.nxb);
+        const int tb = (int)(task - plane * a.nyb * a.nxb);
+        const int by = tb / a.nxb, bx = tb - by * a.nxb;
+        const int iy0 = by * a.yb, ix0 = bx * a.xb;
+        const int ny = min(a.yb, (a.Ho + a.py - 1) / a.py - iy0), nx = min(a.xb, (a.Wo + a.px - 1) / a.px - ix0);
+        const int xr = (ny - 1) * a.qy + (a.xrows - (a.yb - 1) * a.qy), xc = (nx - 1) * a.qx + (a.xcols - (a.xb - 1) * a.qx);
+        const int gr = ny * a.py, gc = nx * a.px;
+        const int t = threadIdx.x;
+        if (t < xr) {
+            const int r = min(max(iy0 * a.qy + a.fy_min + t, 0), a.H - 1);
+            const int c0 = max(ix0 * a.qx + a.fx_min, 0), c1 = min(ix0 * a.qx + a.fx_min + xc, a.W);
+            prefetch_l2(static_cast<const T *>(a.x) + plane * (int64_t)a.H * a.W + (int64_t)r * a.W + c0,
+                        (int64_t)(c1 - c0) * sizeof(T));
+        } else if (t < xr + gr) {
+            const int my = iy0 * a.py + t - xr;
+            if (my < a.Ho)
+                prefetch_l2(static_cast<const T *>(a.g) + plane * (int64_t)a.Ho * a.Wo + (int64_t)my * a.Wo + ix0 * a.px,
+                            (int64_t)min(gc, a.Wo - ix0 * a.px) * sizeof(T));
+        }
+    };
+    prefetch(blockIdx.x);
     for (int64_t task = blockIdx.x; task < a.ntasks; task += gridDim.x) {
         const int64_t plane = task / (a.nyb * a.nxb);
         const int tb = (int)(task - plane * a.nyb * a.nxb);
@@ -74,6 +99,7 @@ __global__ void __launch_bounds__(256) fcfs_wgrad_kernel(const __grid_constant__
             for (int c = lane; c < gc; c += 32) srow[c] = c < cval ? DT<T>::to_f(grow[c]) : 0.0f;
         }
         __syncthreads();
+        prefetch(task + gridDim.x);
         if (own) {
             // one period's products into the lane's partial sums: x rows r0..r3 of its window
             auto item = [&](float gv, const float *xw) {

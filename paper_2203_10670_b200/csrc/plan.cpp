@@ -1231,7 +1231,7 @@ fcfs_status fcfs_run_weight_grad(fcfs_plan_t pl, const void *x, const void *grad
     a.npairs = a.py * a.px;
     const int span_x = fx_max + a.ntx - a.fx_min, span_y = fy_max + a.nty - a.fy_min;
     const int nix = (a.Wo + a.px - 1) / a.px, niy = (a.Ho + a.py - 1) / a.py;
-    int budget = 26 * 1024;  // 8 CTAs per SM: other CTAs compute while one stages its tiles
+    int budget = 48 * 1024;  // 4 CTAs per SM (tiles prefetched into L2 one task ahead)
     if (const char *e = std::getenv("FCFS_DEBUG_WG_BUDGET")) budget = std::atoi(e) * 1024;
     a.yb = 0;
     for (a.xb = std::min(nix, 64); a.xb >= 1 && a.yb == 0; a.xb = a.xb > 1 ? a.xb / 2 : 0) {
