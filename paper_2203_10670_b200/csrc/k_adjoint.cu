@@ -194,6 +194,17 @@ __global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_con
             }
         }
         __syncthreads();
+        {  // L2 prefetch of the next plane group's windows (its staging then hits L2)
+            const int64_t q0 = p0 + (int64_t)pstep * PB;
+            const int nq = (int)(a.planes - q0 < PB ? a.planes - q0 : PB);
+            if (q0 < a.planes && NCg > 0)
+                for (int idx = threadIdx.x; idx < nq * NRg; idx += blockDim.x) {
+                    const int pp = idx / NRg, r = idx - pp * NRg;
+                    prefetch_l2(static_cast<const T *>(a.grad_out) + (q0 + pp) * (int64_t)Ho * Wo +
+                                    (int64_t)(my_lo + r) * Wo + mx_lo,
+                                (int64_t)NCg * sizeof(T));
+                }
+        }
         // row pass first: hy[rr][c] = sum over row rr's pairs (wide windows: lists uniform across a warp)
         if (NCg >= 64) {
             for (int rp = warp; rp < nP * NH; rp += 8) {
