@@ -31,3 +31,14 @@ def test_workloads_are_known_configs():
     for name, launches in synth.WORKLOADS.items():
         for l in launches:
             assert l in synth.CONFIGS, (name, l)
+
+
+def test_oracle_legs_of_the_backward_workloads():
+    """The cpu_baseline / --impl reference legs of C3B and C3W time the oracle's
+    adjoint and weight gradient (not the forward) on a sample of whole planes."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import synth
+    for name, what in (("C3B", "adjoint"), ("C3W", "weight gradient")):
+        outs, secs, desc = bench.oracle_sample_run([synth.CONFIGS[name]], 1)
+        assert outs == synth.CONFIGS[name].C * 213 * 213 and secs > 0 and what in desc, (name, desc)
