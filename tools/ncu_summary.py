@@ -93,6 +93,7 @@ def summarise(rep, out, traffic_key=None, title=None):
     lines = [f"# {title or os.path.basename(rep)}", "", f"Source report: `{os.path.basename(rep)}` "
              "(`ncu --set full --clock-control none --import-source on`, one launch).", ""]
     traffic = None
+    per_name = {}  # a launch group of several kernels (C3B: fused adjoint + bands): their sum
     for d in kernels:
         name = d.get("Kernel Name", "?")
         lines += [f"## `{name}`", "", "| metric | value |", "|---|---|"]
@@ -111,7 +112,8 @@ def summarise(rep, out, traffic_key=None, title=None):
         wu = scale.get(units.get("dram__bytes_write.sum", "byte").lower(), 1)
         du = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}.get(units.get("gpu__time_duration.sum", "").lower(), 1e-6)
         tot = rd * ru + wr * wu
-        traffic = tot
+        per_name.setdefault(name, tot)
+        traffic = sum(per_name.values())
         lines.append(f"| DRAM read+write per launch | {tot / 1e6:.3f} MB |")
         if dur == dur and dur > 0:
             lines.append(f"| achieved DRAM bandwidth (under ncu, cold) | {tot / (dur * du) / 1e9:.1f} GB/s |")
