@@ -27,12 +27,13 @@ namespace fcfs {
 
 constexpr int kTileWarps = 8;
 
-template <typename T>
+template <typename T, int NT>
 __global__ void __launch_bounds__(32 * kTileWarps) fcfs_tile_kernel(const __grid_constant__ TileArgs a) {
     extern __shared__ __align__(16) float tsm[];
     const RunGeom &g = a.g;
     const PhaseTable &tx = a.tx, &ty = a.ty;
-    const int T_ = tx.ntaps, lo = tx.lo;  // one mode for both dimensions
+    constexpr int T_ = NT;  // taps per dimension (the mode's: 2 or 4), compile-time: unrolled tap loops
+    const int lo = tx.lo;   // one mode for both dimensions
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // shared layout: weights, per-column and per-row info, window, hidden
     float *wx = tsm;                               // [px][4]
@@ -125,6 +126,7 @@ __global__ void __launch_bounds__(32 * kTileWarps) fcfs_tile_kernel(const __grid
                 } else {
                     const float *w = wx + 4 * cj;
                     v = __fmul_rn(w[0], xr[b + lo]);
+#pragma unroll
                     for (int t = 1; t < T_; ++t) v = __fmaf_rn(w[t], xr[b + lo + t], v);
                 }
                 hr[k] = v;
@@ -142,8 +144,10 @@ __global__ void __launch_bounds__(32 * kTileWarps) fcfs_tile_kernel(const __grid
                     v = hs[(b - (a.is1d ? 0 : lo)) * a.TW + k];
                 } else {
                     const float *w = wy + 4 * (rj & 0x7fffffff);
-                    v = __fmul_rn(w[0], hs[b * a.TW + k]);
-                    for (int t = 1; t < T_; ++t) v = __fmaf_rn(w[t], hs[(b + t) * a.TW + k], v);
+                    const float *hb = hs + b * a.TW + k;
+                    v = __fmul_rn(w[0], hb[0]);
+#pragma unroll
+                    for (int t = 1; t < T_; ++t) v = __fmaf_rn(w[t], hb[t * a.TW], v);
                 }
                 orow[k] = DT<T>::from_f(v);
             }
@@ -153,15 +157,21 @@ __global__ void __launch_bounds__(32 * kTileWarps) fcfs_tile_kernel(const __grid
 }
 
 int launch_tile(int dtype, const TileArgs &a, int grid, int smem, void *stream) {
-    static bool configured[3] = {false, false, false};
+    static bool configured[3][2] = {};
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const void *fn = dtype == FCFS_F32   ? reinterpret_cast<const void *>(&fcfs_tile_kernel<float>)
-                     : dtype == FCFS_F16 ? reinterpret_cast<const void *>(&fcfs_tile_kernel<__half>)
-                                         : reinterpret_cast<const void *>(&fcfs_tile_kernel<__nv_bfloat16>);
-    if (!configured[dtype]) {
+    const int k4 = a.tx.ntaps == 4 ? 1 : 0;  // bilinear (2 taps) or bicubic (4)
+    const void *fns[3][2] = {{reinterpret_cast<const void *>(&fcfs_tile_kernel<float, 2>),
+                              reinterpret_cast<const void *>(&fcfs_tile_kernel<float, 4>)},
+                             {reinterpret_cast<const void *>(&fcfs_tile_kernel<__half, 2>),
+                              reinterpret_cast<const void *>(&fcfs_tile_kernel<__half, 4>)},
+                             {reinterpret_cast<const void *>(&fcfs_tile_kernel<__nv_bfloat16, 2>),
+                              reinterpret_cast<const void *>(&fcfs_tile_kernel<__nv_bfloat16, 4>)}};
+    const void *fn = fns[dtype][k4];
+    if (a.tx.ntaps != 2 && a.tx.ntaps != 4) return (int)cudaErrorInvalidValue;
+    if (!configured[dtype][k4]) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (e != cudaSuccess) return (int)e;
-        configured[dtype] = true;
+        configured[dtype][k4] = true;
     }
     TileArgs local = a;
     void *args[] = {&local};
