@@ -114,22 +114,27 @@ __global__ void __launch_bounds__(32 * kTileWarps) fcfs_tile_kernel(const __grid
             }
         }
         __syncthreads();
-        // 2. horizontal pass
-        for (int i = warp; i < NR; i += kTileWarps) {
-            const float *xr = xs + i * a.nc_cap;
-            float *hr = hs + i * a.TW;
-            for (int k = lane; k < NW; k += 32) {
-                const int cj = colj[k], b = colb[k];
-                float v;
-                if (cj < 0) {
-                    v = xr[b];
-                } else {
-                    const float *w = wx + 4 * cj;
-                    v = __fmul_rn(w[0], xr[b + lo]);
+        // 2. horizontal pass: a lane keeps one output column's phase, base and
+        // weights in registers across the window rows of its warp
+        for (int k = lane; k < NW; k += 32) {
+            const int cj = colj[k];
+            const bool copy = cj < 0;
+            float w[T_];
 #pragma unroll
-                    for (int t = 1; t < T_; ++t) v = __fmaf_rn(w[t], xr[b + lo + t], v);
+            for (int t = 0; t < T_; ++t) w[t] = copy ? 0.0f : wx[4 * cj + t];
+            const float *xk = xs + colb[k] + (copy ? 0 : lo) + warp * a.nc_cap;
+            float *hk = hs + k + warp * a.TW;
+            const int xstep = kTileWarps * a.nc_cap, hstep = kTileWarps * a.TW;
+            for (int i = warp; i < NR; i += kTileWarps, xk += xstep, hk += hstep) {
+                float v;
+                if (copy) {
+                    v = xk[0];
+                } else {
+                    v = __fmul_rn(w[0], xk[0]);
+#pragma unroll
+                    for (int t = 1; t < T_; ++t) v = __fmaf_rn(w[t], xk[t], v);
                 }
-                hr[k] = v;
+                *hk = v;
             }
         }
         __syncthreads();
@@ -137,19 +142,22 @@ __global__ void __launch_bounds__(32 * kTileWarps) fcfs_tile_kernel(const __grid
         T *dst = static_cast<T *>(g.out) + plane * g.out_plane_stride;
         for (int rr = warp; rr < NH; rr += kTileWarps) {
             const int rj = rowj[rr], b = rowb[rr];
-            T *orow = dst + (int64_t)(my0 + rr - (int)g.out_row0) * g.Wo + mx0;
-            for (int k = lane; k < NW; k += 32) {
-                float v;
-                if (rj < 0) {
-                    v = hs[(b - (a.is1d ? 0 : lo)) * a.TW + k];
-                } else {
-                    const float *w = wy + 4 * (rj & 0x7fffffff);
-                    const float *hb = hs + b * a.TW + k;
-                    v = __fmul_rn(w[0], hb[0]);
+            const bool copy = rj < 0;  // warp-uniform
+            float w[T_];
 #pragma unroll
-                    for (int t = 1; t < T_; ++t) v = __fmaf_rn(w[t], hb[t * a.TW], v);
+            for (int t = 0; t < T_; ++t) w[t] = copy ? 0.0f : wy[4 * (rj & 0x7fffffff) + t];
+            T *op = dst + (int64_t)(my0 + rr - (int)g.out_row0) * g.Wo + mx0 + lane;
+            const float *hb = hs + (copy ? b - (a.is1d ? 0 : lo) : b) * a.TW + lane;
+            const int TW = a.TW;
+            if (copy) {
+                for (int k = lane; k < NW; k += 32, hb += 32, op += 32) *op = DT<T>::from_f(hb[0]);
+            } else {
+                for (int k = lane; k < NW; k += 32, hb += 32, op += 32) {
+                    float v = __fmul_rn(w[0], hb[0]);
+#pragma unroll
+                    for (int t = 1; t < T_; ++t) v = __fmaf_rn(w[t], hb[t * TW], v);
+                    *op = DT<T>::from_f(v);
                 }
-                orow[k] = DT<T>::from_f(v);
             }
         }
     }
