@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--impl", default="fcfs", choices=["fcfs", "reference"])
     ap.add_argument("--soak-s", type=float, default=1.0, help="untimed steady-state run before warm-up (clocks)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cold", action="store_true", help="skip the cold-L2 single-step median/min (SURVEY 8d)")
+    ap.add_argument("--cold-reps", type=int, default=100)
     ap.add_argument("--halo", default="nccl", choices=["nccl", "peer"],
                     help="C5 row strips at N > 1: NCCL send/recv halo, or in-kernel peer reads (symmetric memory)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -434,6 +436,26 @@ def main():
     except Exception:
         pass
 
+    # SURVEY §8(d) single-launch protocol: cold L2 (a > L2 buffer written before
+    # each repeat), CUDA events around one eager step, median and min
+    cold = None
+    if not args.no_cold:
+        flush = torch.empty(int(2 * l2) // 4, dtype=torch.float32, device=dev)
+        ts = []
+        with torch.cuda.stream(stream):
+            for r in range(args.cold_reps):
+                flush.fill_(float(r))
+                c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                c0.record(stream)
+                step(r % R)
+                c1.record(stream)
+                c1.synchronize()
+                ts.append(c0.elapsed_time(c1) * 1e3)
+        del flush
+        ts.sort()
+        cold = {"median_us": ts[len(ts) // 2], "min_us": ts[0], "repeats": len(ts),
+                "protocol": "L2 flushed (2x L2 written) before each repeat; CUDA events around one eager step"}
+
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(launches, args, dev, stream, world, dist)
@@ -470,6 +492,7 @@ def main():
                                 "(the library's launches captured on the launching stream); per-launch average = "
                                 "region / K when a step is one launch, else a graph of K launches of that kernel")},
         "gpu_launches": n_launches,
+        "single_launch_cold_l2": cold,
         "clocks": clocks,
     }
     if e2e is not None:
