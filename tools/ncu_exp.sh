@@ -1,3 +1,4 @@
+# usage: bash tools/ncu_exp.sh <config[@HxW]> <out tag> [kernel regex] -- ncu --set full of one launch (tools/exp.py), summarised
 # usage: bash tools/_ncu_one.sh <config> <tag> [kernel regex]
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 mkdir -p gpurun_out/$2

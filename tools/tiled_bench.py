@@ -1,3 +1,4 @@
+"""Per-image time of the tiled kernel on the paper sweep's 27/11 and 2/11 factors (16 x 3 x 1024^2 fp32; developer tool)."""
 import sys, torch
 sys.path.insert(0, "/root/repo")
 import paper_2203_10670_b200 as fc
