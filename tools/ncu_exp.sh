@@ -1,5 +1,4 @@
 # usage: bash tools/ncu_exp.sh <config[@HxW]> <out tag> [kernel regex] -- ncu --set full of one launch (tools/exp.py), summarised
-# usage: bash tools/_ncu_one.sh <config> <tag> [kernel regex]
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 mkdir -p gpurun_out/$2
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:${3:-fcfs} -s 2 -c 1 -o gpurun_out/$2/rep -f python tools/exp.py $1 --reps 1 > gpurun_out/$2/log 2>&1

@@ -1,6 +1,7 @@
 """Per-image time of the tiled kernel on the paper sweep's 27/11 and 2/11 factors (16 x 3 x 1024^2 fp32; developer tool)."""
 import sys, torch
-sys.path.insert(0, "/root/repo")
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2203_10670_b200 as fc
 for (p, q, mode) in [(27, 11, "bilinear"), (27, 11, "bicubic"), (2, 11, "bilinear"), (2, 11, "bicubic")]:
     pl = fc.Plan(p, q, mode, "replicate", 3, 1024, 1024, "float32", "floor")
