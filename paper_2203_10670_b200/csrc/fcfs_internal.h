@@ -57,6 +57,7 @@ struct TileArgs {        // tiled kernel (k_tile.cu): output tiles with a shared
     int row_slots;       // window rows: 1 = one slot per (output row, tap), 0 = the contiguous range
     int nr_cap, nc_cap;  // window rows / columns reserved (row pitch of the window = nc_cap)
     int xs_cap;          // floats reserved for the window (= nr_cap * nc_cap)
+    int col_direct;      // strong down-scaling in both dimensions: no window; the horizontal pass reads its taps from HBM/L2
 };
 
 struct AdjArgs {         // adjoint kernel (k_adjoint.cu): grad_in = A^T grad_out

@@ -94,8 +94,9 @@ __global__ void __launch_bounds__(32 * kTileWarps) fcfs_tile_kernel(const __grid
             for (int i = threadIdx.x; i < NR; i += blockDim.x)
                 rsrc[i] = a.is1d ? r_lo + i : pad_src32(r_lo + i, (int)g.H, a.pad);
         __syncthreads();
-        // 1. window (fp32), padding applied
+        // 1. window (fp32), padding applied (col_direct: none -- phase 2 reads its taps)
         const T *src = static_cast<const T *>(g.in) + plane * g.in_plane_stride;
+        if (!a.col_direct)
         for (int i = warp; i < NR; i += kTileWarps) {
             const int rs = rsrc[i];
             const T *row = src + (int64_t)(rs - (int)g.in_row0) * g.W;
@@ -113,9 +114,45 @@ __global__ void __launch_bounds__(32 * kTileWarps) fcfs_tile_kernel(const __grid
                     if (c0 + 32 * u < NC) xr[c0 + 32 * u] = v[u];
             }
         }
-        __syncthreads();
+        if (!a.col_direct) __syncthreads();
         // 2. horizontal pass: a lane keeps one output column's phase, base and
         // weights in registers across the window rows of its warp
+        if (a.col_direct) {
+            // strong down-scaling (a window row holds ~q/p columns per output): each
+            // lane loads its column's taps straight from global memory (L1/L2),
+            // row after row -- no window staging, no barrier before the pass; the
+            // values and the operation order are the staged path's
+            for (int k = lane; k < NW; k += 32) {
+                const int cj = colj[k];
+                const bool copy = cj < 0;
+                float w[T_];
+                int cs[T_];
+#pragma unroll
+                for (int t = 0; t < T_; ++t) {
+                    w[t] = copy ? 0.0f : wx[4 * cj + t];
+                    cs[t] = pad_src32(c_lo + colb[k] + (copy ? 0 : lo) + t, (int)g.W, a.pad);
+                }
+                float *hk = hs + k + warp * a.TW;
+                const int hstep = kTileWarps * a.TW;
+#pragma unroll 4
+                for (int i = warp; i < NR; i += kTileWarps, hk += hstep) {
+                    const int rs = rsrc[i];
+                    const T *row = src + (int64_t)(rs - (int)g.in_row0) * g.W;
+                    float xv[T_];
+#pragma unroll
+                    for (int t = 0; t < T_; ++t) xv[t] = (rs >= 0 && cs[t] >= 0) ? DT<T>::to_f(row[cs[t]]) : 0.0f;
+                    float v;
+                    if (copy) {
+                        v = xv[0];
+                    } else {
+                        v = __fmul_rn(w[0], xv[0]);
+#pragma unroll
+                        for (int t = 1; t < T_; ++t) v = __fmaf_rn(w[t], xv[t], v);
+                    }
+                    *hk = v;
+                }
+            }
+        } else
         for (int k = lane; k < NW; k += 32) {
             const int cj = colj[k];
             const bool copy = cj < 0;

@@ -467,6 +467,10 @@ bool plan_tile(const fcfs_plan_s *pl, const RunGeom &g0, TileArgs &a, int &grid,
     auto span = [&](int n, int p, int q) { return (int)(((int64_t)(n - 1) * q + p - 1) / p + q + T + 1); };
     const int budget = 48 * 1024;  // bytes: 4 CTAs per SM
     int bestTH = 0, bestTW = 0, bestNR = 0, bestNC = 0, bestSlots = 0;
+    double best_score = -1.0;
+    // the largest tile, unless it leaves the resident CTAs without work: small
+    // images (2/11 of 1024^2: 186^2 outputs per plane) need more, smaller tiles
+    const double want_tiles = 2.0 * pl->sm_count * 4;
     for (int TW : {256, 128, 64, 32, 16, 8, 4, 2, 1}) {
         for (int TH : {64, 32, 16, 8, 4, 2, 1}) {
             int NR = TH, slots = 0;
@@ -481,7 +485,10 @@ bool plan_tile(const fcfs_plan_s *pl, const RunGeom &g0, TileArgs &a, int &grid,
             const int64_t bytes = 4 * (8 * kPMax + 2 * TW + 2 * TH + NR) + 4 * ((int64_t)NR * NC + (int64_t)NR * TW);
             if (bytes > budget) continue;
             const int TWe = (int)std::min<int64_t>(TW, g.Wo), THe = (int)std::min<int64_t>(TH, g.out_nrows);
-            if ((int64_t)THe * TWe > (int64_t)bestTH * bestTW || ((int64_t)THe * TWe == (int64_t)bestTH * bestTW && TW > bestTW)) {
+            const double nt = (double)g.planes * (double)((g.out_nrows + THe - 1) / THe) * (double)((g.Wo + TWe - 1) / TWe);
+            const double score = (double)THe * TWe * std::min(1.0, nt / want_tiles) + 1e-3 * TW;
+            if (score > best_score) {
+                best_score = score;
                 bestTH = THe;
                 bestTW = TWe;
                 bestNR = NR;
@@ -497,6 +504,9 @@ bool plan_tile(const fcfs_plan_s *pl, const RunGeom &g0, TileArgs &a, int &grid,
     a.nr_cap = bestNR;
     a.nc_cap = bestNC;
     a.xs_cap = bestNR * bestNC;
+    // rows by slots and columns strongly down-scaled too: the taps are a small
+    // fraction of the window's columns -- read them directly instead
+    a.col_direct = bestSlots && bestNC > bestTW * T && !std::getenv("FCFS_DEBUG_TILE_WINDOW");
     smem = 4 * (8 * kPMax + 2 * a.TW + 2 * a.TH + a.nr_cap) + 4 * (a.xs_cap + a.nr_cap * a.TW);
     const int64_t ntiles = g.planes * ((g.out_nrows + a.TH - 1) / a.TH) * ((g.Wo + a.TW - 1) / a.TW);
     grid = (int)std::min<int64_t>(ntiles, (int64_t)pl->sm_count * 4);
