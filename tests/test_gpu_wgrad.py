@@ -137,3 +137,17 @@ def test_kernel_launch_counter():
     pl.run_adjoint(y)
     assert fc.kernel_launches() - n0 == 2
     torch.cuda.synchronize()
+
+
+def test_weight_grad_rank1_plan_equals_1d_rows():
+    """A rank-1 plan (plan_nd with one factor) has the 1D flag's weights (1, p, 1, taps)."""
+    for mode in ("bilinear", "bicubic"):
+        pl = Plan.nd((5,), (3,), mode, "reflect", 3, (97,), "float32", "floor")
+        assert pl.weight_grad_shape() == (1, 5, 1, {"bilinear": 2, "bicubic": 4}[mode])
+        x = torch.from_numpy(synth.normal_f32(40, 2 * 3 * 97).reshape(2, 3, 97))
+        g = torch.from_numpy(synth.normal_f32(41, 2 * 3 * pl.odims[0]).reshape(2, 3, pl.odims[0]))
+        gw = pl.run_weight_grad(x.to(DEV), g.to(DEV))
+        ref, ab = oracle.weight_grad(x.numpy()[:, :, None, :], g.double().numpy()[:, :, None, :], 5, 3, mode, "reflect",
+                                     floor_extent=True, is1d=True)
+        n = g.numel()
+        assert (np.abs(gw.cpu().double().numpy() - ref) <= (n + 8) * 2.0 ** -24 * ab + 1e-30).all()
