@@ -278,7 +278,9 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L, const F
     const int64_t min_tiles = (a.nch + NT - 1) / NT;
     double best_score = -1.0;
     FusedArgs best = a;
-    for (int64_t nt = min_tiles; nt <= std::min<int64_t>(a.nch, min_tiles + 64); ++nt) {
+    int64_t nt_lo = min_tiles, nt_hi = std::min<int64_t>(a.nch, min_tiles + 64);
+    if (const char *e = std::getenv("FCFS_DEBUG_NTILE")) nt_lo = nt_hi = std::max<int64_t>(min_tiles, std::min<int64_t>(a.nch, std::atoi(e)));
+    for (int64_t nt = nt_lo; nt <= nt_hi; ++nt) {
         // G = 1: one flush per y-period, two full-period staging slots;
         // G = 2: two flushes per period, slots of ceil(P/2) rows (half the smem)
         for (int Gf = 1; Gf <= (PY >= 2 ? 2 : 1); ++Gf) {
