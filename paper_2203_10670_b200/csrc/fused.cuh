@@ -38,6 +38,17 @@
 
 #include "device_common.cuh"
 
+// ring-offset unroll of the period loop: register rings up to this many floats
+#ifndef FCFS_RING_UNROLL_MAX
+#define FCFS_RING_UNROLL_MAX 24
+#endif
+// between unrolled periods (experiments: keeps ptxas from interleaving them)
+#ifdef FCFS_EXP_PERIOD_FENCE
+#define FCFS_PERIOD_FENCE() asm volatile("" ::: "memory")
+#else
+#define FCFS_PERIOD_FENCE() ((void)0)
+#endif
+
 namespace fcfs {
 
 __host__ __device__ constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
@@ -674,7 +685,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     // Unrolling the period loop over the ring offsets removes the carry copies
     // but multiplies the loop body; worth it only for small register rings.
     constexpr int U0 = TY / cgcd(QY, TY);  // ring offsets before the cycle repeats
-    constexpr bool kRingUnroll = KP * TY <= 24 && (U0 == 1 || U0 == 2 || U0 == 4);  // (40, C3's ring: 160 -> 210 us)
+    constexpr bool kRingUnroll = KP * TY <= FCFS_RING_UNROLL_MAX && (U0 == 1 || U0 == 2 || U0 == 4);  // (40, C3's ring: 160 -> 210 us)
     int slot = 0;
     uint32_t phase = 0;
     uint32_t fk = 0;     // flush counter: staging slot = fk & 1
@@ -956,12 +967,15 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             period(std::integral_constant<int, 0>{}, iy);
             if (++iy >= b.iy1) break;
             if constexpr (U > 1) {
+                FCFS_PERIOD_FENCE();
                 period(std::integral_constant<int, (QY % TY)>{}, iy);
                 if (++iy >= b.iy1) break;
             }
             if constexpr (U > 2) {
+                FCFS_PERIOD_FENCE();
                 period(std::integral_constant<int, ((2 * QY) % TY)>{}, iy);
                 if (++iy >= b.iy1) break;
+                FCFS_PERIOD_FENCE();
                 period(std::integral_constant<int, ((3 * QY) % TY)>{}, iy);
                 ++iy;
             }
