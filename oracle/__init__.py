@@ -81,6 +81,8 @@ def _load():
             lib.fcfs_oracle_output_dims_nd.argtypes = [i32, ctypes.POINTER(i64), ctypes.POINTER(i32),
                                                        ctypes.POINTER(i32), i32, ctypes.POINTER(i64)]
             lib.fcfs_oracle_weight_grad.argtypes = [vp, i32, i64, i64, i64, dp, i32, i32, i32, i32, i32, i32, dp, dp]
+            lib.fcfs_oracle_weight_grad_2d.argtypes = [vp, i32, i64, i64, i64, dp, i32, i32, i32, i32, i32, i32, i32,
+                                                       dp, dp]
             _lib = lib
     return _lib
 
@@ -305,6 +307,27 @@ def weight_grad(x, g, p, q, mode="bilinear", pad="replicate", floor_extent=False
     rc = _load().fcfs_oracle_weight_grad(xa.ctypes.data, kind, planes, H, W, _dptr(ga), p, q, MODES[mode],
                                          PADS[pad], int(floor_extent), int(is1d), _dptr(out), _dptr(ab))
     _chk(rc, "weight_grad")
+    return out, ab
+
+
+def weight_grad_2d(x, g, p, q, mode="bilinear", pad="replicate", floor_extent=False):
+    """weight_grad for a 2D layer with a factor per dimension: p = (py, px), q = (qy, qx).
+    Returns (grad, abs_sum) of shape (py, px, taps, taps) (reduced factors)."""
+    from math import gcd
+    xa, kind = _as_input(x)
+    H, W = xa.shape[-2], xa.shape[-1]
+    planes = int(np.prod(xa.shape[:-2])) if xa.ndim > 2 else 1
+    (py, px), (qy, qx) = p, q
+    Ho, Wo = output_extent(H, py, qy, floor_extent), output_extent(W, px, qx, floor_extent)
+    ga = np.ascontiguousarray(g, dtype=np.float64)
+    if ga.size != planes * Ho * Wo:
+        raise ValueError(f"gradient of {ga.size} elements, expected {planes} x {Ho} x {Wo}")
+    nt = {"nearest": 1, "bilinear": 2, "bicubic": 4}[mode]
+    shape = (py // gcd(py, qy), px // gcd(px, qx), nt, nt)
+    out, ab = np.zeros(shape), np.zeros(shape)
+    rc = _load().fcfs_oracle_weight_grad_2d(xa.ctypes.data, kind, planes, H, W, _dptr(ga), py, qy, px, qx,
+                                            MODES[mode], PADS[pad], int(floor_extent), _dptr(out), _dptr(ab))
+    _chk(rc, "weight_grad_2d")
     return out, ab
 
 

@@ -1129,3 +1129,94 @@ int fcfs_oracle_weight_grad(const void *x, int in_kind, int64_t planes, int64_t 
     free(dKa);
     return rc;
 }
+
+/* The same weight gradient for a 2D layer with its own factor per dimension
+ * (§4.2: "the scale factor can differ per dimension"): rows
+ * py/qy, columns px/qx, each dimension with its own phase window; the
+ * literal backward of the staged layer as above.  out, abs_out: [py][px][nt][nt]
+ * (reduced factors).  Used to pin the GPU's anisotropic weight gradient. */
+int fcfs_oracle_weight_grad_2d(const void *x, int in_kind, int64_t planes, int64_t H, int64_t W, const double *g,
+                               int py, int qy, int px, int qx, int mode, int pad, int floor_ext, double *out,
+                               double *abs_out) {
+    if (py < 1 || qy < 1 || px < 1 || qx < 1 || py > ORC_PMAX || qy > ORC_PMAX || px > ORC_PMAX || qx > ORC_PMAX)
+        return ORC_E_ARG;
+    if (mode < 0 || mode > 2 || pad < 0 || pad > 2 || H < 1 || W < 1) return ORC_E_ARG;
+    int64_t gy = orc_gcd(py, qy), gx = orc_gcd(px, qx);
+    py /= (int)gy; qy /= (int)gy; px /= (int)gx; qx /= (int)gx;
+    int64_t Ho, Wo;
+    fcfs_oracle_output_extent(H, py, qy, floor_ext, &Ho);
+    fcfs_oracle_output_extent(W, px, qx, floor_ext, &Wo);
+    if (Ho < 1 || Wo < 1) return ORC_E_SHAPE;
+    int loy, hiy, lox, hix;
+    phase_window(mode, py, qy, &loy, &hiy);
+    phase_window(mode, px, qx, &lox, &hix);
+    int Ty = hiy - loy + 1, Tx = hix - lox + 1;
+    double w[4];
+    int f0, fl, nt = fcfs_oracle_phase_taps(mode, px, qx, 0, &f0, w);
+    /* reflect reach (as check_reach, per dimension) */
+    if (pad == ORC_PAD_REFLECT) {
+        int64_t dims_[2] = {H, W}, outs_[2] = {Ho, Wo};
+        int ps_[2] = {py, px}, qs_[2] = {qy, qx};
+        for (int d = 0; d < 2; ++d) {
+            int64_t mlast = outs_[d] - 1, s;
+            fcfs_oracle_phase_taps(mode, ps_[d], qs_[d], 0, &f0, w);
+            int n2 = fcfs_oracle_phase_taps(mode, ps_[d], qs_[d], (int)(mlast % ps_[d]), &fl, w);
+            int64_t vmin = f0, vmax = (int64_t)qs_[d] * (mlast / ps_[d]) + fl + n2 - 1;
+            if (vmin < 0 && pad_index(vmin, dims_[d], ORC_PAD_REFLECT, &s) < 0) return ORC_E_PAD;
+            if (vmax > dims_[d] - 1 && pad_index(vmax, dims_[d], ORC_PAD_REFLECT, &s) < 0) return ORC_E_PAD;
+        }
+    }
+    int64_t nhy = (Ho + py - 1) / py, nix = (Wo + px - 1) / px;
+    int64_t PR = (nhy - 1) * qy + Ty, PC = (nix - 1) * qx + Tx;
+    size_t nk = (size_t)py * px * Ty * Tx;
+    double *xp = (double *)malloc(sizeof(double) * PR * PC);
+    double *dK = (double *)calloc(nk, sizeof(double)), *dKa = (double *)calloc(nk, sizeof(double));
+    if (!xp || !dK || !dKa) { free(xp); free(dK); free(dKa); return ORC_E_NOMEM; }
+    orc_src s = {x, in_kind, H, W, 0, H, H * W};
+    for (int64_t pl = 0; pl < planes; ++pl) {
+        /* 1. pad */
+        for (int64_t a = 0; a < PR; ++a)
+            for (int64_t b = 0; b < PC; ++b) {
+                int64_t vr = loy + a, vc = lox + b, sr, sc;
+                int kr = pad_index(vr, H, pad, &sr), kc = pad_index(vc, W, pad, &sc);
+                if (kr < 0) { sr = vr < 0 ? 0 : H - 1; kr = 1; } /* unreachable by kept outputs: clamped */
+                if (kc < 0) { sc = vc < 0 ? 0 : W - 1; kc = 1; }
+                xp[a * PC + b] = (kr == 0 || kc == 0) ? 0.0 : src_at(&s, pl, sr, sc);
+            }
+        /* 2.-3. crop^T, pixelshuffle^-1, conv2d weight gradient */
+        const double *gp = g + pl * Ho * Wo;
+        for (int jy = 0; jy < py; ++jy)
+            for (int jx = 0; jx < px; ++jx)
+                for (int64_t iy = 0; iy < nhy; ++iy)
+                    for (int64_t ix = 0; ix < nix; ++ix) {
+                        int64_t my = (int64_t)py * iy + jy, mx = (int64_t)px * ix + jx;
+                        if (my >= Ho || mx >= Wo) continue;
+                        double gh = gp[my * Wo + mx];
+                        double *k = dK + (size_t)(jy * px + jx) * Ty * Tx, *ka = dKa + (size_t)(jy * px + jx) * Ty * Tx;
+                        for (int a = 0; a < Ty; ++a)
+                            for (int b = 0; b < Tx; ++b) {
+                                double xv = xp[(qy * iy + a) * PC + qx * ix + b];
+                                k[a * Tx + b] += gh * xv;
+                                ka[a * Tx + b] += fabs(gh) * fabs(xv);
+                            }
+                    }
+    }
+    /* 4. the phases' own taps */
+    for (int jy = 0; jy < py; ++jy)
+        for (int jx = 0; jx < px; ++jx) {
+            int fy, fx;
+            fcfs_oracle_phase_taps(mode, py, qy, jy, &fy, w);
+            fcfs_oracle_phase_taps(mode, px, qx, jx, &fx, w);
+            for (int ty = 0; ty < nt; ++ty)
+                for (int tx = 0; tx < nt; ++tx) {
+                    size_t src = ((size_t)(jy * px + jx) * Ty + fy - loy + ty) * Tx + fx - lox + tx;
+                    size_t dst = ((size_t)(jy * px + jx) * nt + ty) * nt + tx;
+                    out[dst] = dK[src];
+                    if (abs_out) abs_out[dst] = dKa[src];
+                }
+        }
+    free(xp);
+    free(dK);
+    free(dKa);
+    return ORC_OK;
+}

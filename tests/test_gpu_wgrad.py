@@ -151,3 +151,23 @@ def test_weight_grad_rank1_plan_equals_1d_rows():
                                      floor_extent=True, is1d=True)
         n = g.numel()
         assert (np.abs(gw.cpu().double().numpy() - ref) <= (n + 8) * 2.0 ** -24 * ab + 1e-30).all()
+
+
+@pytest.mark.parametrize("mode", ["nearest", "bilinear", "bicubic"])
+def test_weight_grad_anisotropic(mode):
+    """Per-dimension factors (plan_nd, §4.2): the GPU's anisotropic weight
+    gradient against the oracle's (pinned to torch autograd with stride (qy, qx))."""
+    for i, (p, q, pad, dtype) in enumerate([((5, 2), (3, 7), "replicate", "float32"),
+                                            ((3, 4), (2, 3), "reflect", "bfloat16"),
+                                            ((2, 7), (5, 4), "zero", "float32")]):
+        H, W = 41, 66
+        pl = Plan.nd(p, q, mode, pad, 3, (H, W), dtype, "floor")
+        x = torch.from_numpy(synth.normal_f32(60 + i, 2 * 3 * H * W).reshape(2, 3, H, W)).to(getattr(torch, dtype))
+        oshape = pl.out_shape(2)
+        g = torch.from_numpy(synth.normal_f32(70 + i, int(np.prod(oshape))).reshape(oshape)).to(getattr(torch, dtype))
+        gw = pl.run_weight_grad(x.to(DEV), g.to(DEV))
+        torch.cuda.synchronize()
+        ref, ab = oracle.weight_grad_2d(oracle_input(x), g.double().numpy(), p, q, mode, pad, floor_extent=True)
+        assert tuple(gw.shape) == ref.shape, (gw.shape, ref.shape)
+        tol = (g.numel() + 8) * 2.0 ** -24 * ab + 1e-30
+        assert (np.abs(gw.cpu().double().numpy() - ref) <= tol).all(), (p, q, mode, pad, dtype)

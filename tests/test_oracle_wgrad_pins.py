@@ -107,3 +107,63 @@ def test_weight_grad_1d_and_linearity():
                     v = -v if v < 0 else (2 * 39 - v if v > 39 else v)
                     ref[0, j, 0, t] += (g1[..., m] * x[..., v]).sum()
         np.testing.assert_allclose(a1, ref, rtol=0, atol=1e-11)
+
+
+def torch_layer_wgrad_2d(x, g, p, q, mode, pad, ext):
+    """torch float64 autograd through the anisotropic layer: F.pad -> F.conv2d
+    (stride (qy, qx), a (py*px, 1, Ty, Tx) weight) -> pixelshuffle by (py, px)
+    as reshape/permute -> crop; the weight's .grad read at each phase's taps."""
+    import torch
+    import torch.nn.functional as F
+    (py, px), (qy, qx) = p, q
+    N, H, W = x.shape
+    Ho, Wo = oracle.output_extent(H, py, qy, ext), oracle.output_extent(W, px, qx, ext)
+    def win(pp, qq):
+        firsts = [oracle.phase_taps(mode, pp, qq, j)[0] for j in range(pp)]
+        nt = len(oracle.phase_taps(mode, pp, qq, 0)[1])
+        lo, hi = min(firsts), max(firsts) + nt - 1
+        return firsts, lo, hi - lo + 1, nt
+    fy, loy, Ty, nt = win(py, qy)
+    fx, lox, Tx, _ = win(px, qx)
+    k = np.zeros((py * px, 1, Ty, Tx))
+    for jy in range(py):
+        for jx in range(px):
+            wy = oracle.phase_taps(mode, py, qy, jy)[1]
+            wx = oracle.phase_taps(mode, px, qx, jx)[1]
+            k[jy * px + jx, 0, fy[jy] - loy:fy[jy] - loy + nt, fx[jx] - lox:fx[jx] - lox + nt] = np.outer(wy, wx)
+    w = torch.from_numpy(k).requires_grad_(True)
+    nhy, nhx = -(-Ho // py), -(-Wo // px)
+    padb, padr = (nhy - 1) * qy + Ty - H + loy, (nhx - 1) * qx + Tx - W + lox
+    xt = torch.from_numpy(x)[:, None]
+    if padb < 0:
+        xt, padb = xt[..., : H + padb, :], 0
+    if padr < 0:
+        xt, padr = xt[..., :, : W + padr], 0
+    tmode = {"zero": "constant", "replicate": "replicate", "reflect": "reflect"}[pad]
+    h = F.conv2d(F.pad(xt, (-lox, padr, -loy, padb), mode=tmode), w, stride=(qy, qx))  # (N, py*px, nhy, nhx)
+    y = h.reshape(N, py, px, nhy, nhx).permute(0, 3, 1, 4, 2).reshape(N, nhy * py, nhx * px)[:, :Ho, :Wo]
+    (y * torch.from_numpy(g)).sum().backward()
+    gw = w.grad.numpy()[:, 0]
+    out = np.empty((py, px, nt, nt))
+    for jy in range(py):
+        for jx in range(px):
+            out[jy, jx] = gw[jy * px + jx, fy[jy] - loy:fy[jy] - loy + nt, fx[jx] - lox:fx[jx] - lox + nt]
+    return out
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("pad", PADS)
+def test_weight_grad_2d_anisotropic_equals_torch_autograd(mode, pad):
+    for n, (p, q, ext) in enumerate([((5, 2), (3, 7), False), ((3, 4), (2, 3), True), ((2, 7), (5, 4), True),
+                                      ((4, 1), (1, 3), False)]):
+        H, W = 17, 23
+        x = rnd(200 + n, (2, H, W))
+        Ho, Wo = oracle.output_extent(H, p[0], q[0], ext), oracle.output_extent(W, p[1], q[1], ext)
+        g = rnd(220 + n, (2, Ho, Wo))
+        try:
+            ours, ab = oracle.weight_grad_2d(x, g, p, q, mode, pad, floor_extent=ext)
+        except oracle.OracleError as e:
+            assert pad == "reflect" and e.code == -2
+            continue
+        ref = torch_layer_wgrad_2d(x, g, p, q, mode, pad, ext)
+        np.testing.assert_allclose(ours, ref, rtol=0, atol=1e-12, err_msg=f"{p}/{q} {mode} {pad}")
