@@ -348,3 +348,21 @@ def test_unaligned_rows_fused(pad):
         compare(y, ref, dtype, "bicubic", float(xr.max() - xr.min()), f"unaligned {p}/{q} {pad} {dtype} {H}x{W}+{off}")
         yr = Plan(p, q, "bicubic", pad, C, H, W, dtype, "floor", force_reference=True).run(x)
         assert torch.equal(y.view(torch.uint8), yr.view(torch.uint8)), (p, q, pad, dtype, W, off)
+
+
+def test_unaligned_strips_equal_whole_image():
+    """Row strips of an image whose rows are not 16-B aligned (the fused kernel's
+    in-place shifted reads with a row window) reproduce the single launch."""
+    for (p, q, mode, pad, dtype) in [(5, 3, "bicubic", "reflect", "bfloat16"), (3, 5, "bicubic", "replicate", "float16"),
+                                     (7, 4, "bilinear", "zero", "float32")]:
+        H, W = 331, 641
+        x = _rand_input(19, (2, 2, H, W), dtype).to(DEV)
+        pl = Plan(p, q, mode, pad, 2, H, W, dtype, "floor")
+        assert pl.launch_info(2)["kernel"] == "fused_separable"
+        whole = pl.run(x)
+        parts = []
+        for g in range(3):
+            own0, own1 = g * H // 3, (g + 1) * H // 3
+            o0, o1, n0, n1 = pl.strip_rows(own0, own1)
+            parts.append(pl.run_rows(x[:, :, n0:n1].contiguous(), n0, o0, o1 - o0))
+        assert torch.equal(torch.cat(parts, dim=2).view(torch.uint8), whole.view(torch.uint8)), (p, q, dtype)
