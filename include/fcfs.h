@@ -220,8 +220,12 @@ fcfs_status fcfs_run_host(fcfs_plan_t plan, const void *host_in, void *host_out,
  * element they copy, zero padding contributes nothing).
  *   grad_out: device N x C x odims (the forward output shape), plan dtype
  *   grad_in : device N x C x dims (the forward input shape), overwritten
- * fp32 accumulation (columns, then rows, then slices), rounded once to the
- * dtype.  Whole tensors only (no row windows).  Asynchronous on `stream`.
+ * 2D bilinear/bicubic: the fused kernel runs A^T's polyphase form (q phases
+ * per period of p inputs) over grad_out; with replicate / reflect padding a
+ * second launch rewrites the border rows/columns that receive padding images.
+ * fp32 accumulation in a fixed order per element (reading Z21),
+ * rounded once to the dtype.  Whole tensors only (no row windows).
+ * Asynchronous on `stream`.
  * Errors: FCFS_E_ARG (NULL, N < 0, overlap), FCFS_E_DEVICE, FCFS_E_CUDA. */
 fcfs_status fcfs_run_adjoint(fcfs_plan_t plan, const void *grad_out, void *grad_in, int64_t N, void *stream);
 
