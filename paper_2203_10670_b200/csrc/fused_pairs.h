@@ -6,11 +6,11 @@
 #define FCFS_ISO_PAIRS(Y) \
     Y(1, 1) Y(2, 1) Y(3, 1) Y(4, 1) Y(1, 2) Y(1, 3) Y(1, 4) \
     Y(3, 2) Y(2, 3) Y(4, 3) Y(3, 4) Y(5, 3) Y(3, 5) Y(5, 4) Y(4, 5) \
-    Y(7, 5) Y(5, 7) Y(4, 7) Y(7, 4) Y(5, 2) Y(2, 5)
+    Y(7, 5) Y(5, 7) Y(4, 7) Y(7, 4) Y(5, 2) Y(2, 5) Y(2, 11)
 #define FCFS_NONUNIT_PAIRS(Y) \
     Y(2, 1) Y(3, 1) Y(4, 1) Y(1, 2) Y(1, 3) Y(1, 4) \
     Y(3, 2) Y(2, 3) Y(4, 3) Y(3, 4) Y(5, 3) Y(3, 5) Y(5, 4) Y(4, 5) \
-    Y(7, 5) Y(5, 7) Y(4, 7) Y(7, 4) Y(5, 2) Y(2, 5)
+    Y(7, 5) Y(5, 7) Y(4, 7) Y(7, 4) Y(5, 2) Y(2, 5) Y(2, 11)
 // isotropic p/q in both dimensions
 #define FCFS_ISO_X(X) FCFS_ISO_PAIRS(X##_ISO)
 // columns only (rows 1/1, as the unreduced 4/4: 1D rows and width-only resizes)

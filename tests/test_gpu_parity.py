@@ -308,14 +308,16 @@ def test_streams_and_concurrency():
 @pytest.mark.parametrize("mode", ["bilinear", "bicubic"])
 @pytest.mark.parametrize("dtype", DTYPES)
 def test_tiled_kernel_paper_factors(mode, dtype):
-    """Factors without a fused variant (the paper's §6 factors 2/11 and 27/11,
-    PAPER.md:289-300, and others) run the tiled kernel: many tiles with ragged
-    edges, bitwise equal to the reference kernel and within the bar of the oracle."""
-    for i, (p, q) in enumerate([(2, 11), (27, 11), (9, 7), (1, 6), (11, 4), (13, 10)]):
+    """Factors without a fused variant (the paper's §6 factor 27/11,
+    PAPER.md:289-300, strong down-scaling 2/13 -- the direct-tap mode -- and
+    others) run the tiled kernel; 2/11 (the paper's other §6 factor) has a fused
+    variant.  Many tiles with ragged edges, bitwise equal to the reference kernel
+    and within the bar of the oracle."""
+    for i, (p, q) in enumerate([(2, 13), (27, 11), (9, 7), (1, 6), (11, 4), (13, 10), (2, 11)]):
         pad = ["zero", "replicate", "reflect"][i % 3]
         x = _rand_input(2000 + i, (1, 2, 157, 229), dtype)
         pl = Plan(p, q, mode, pad, 2, 157, 229, dtype, "floor")
-        assert pl.kernel == "tiled"
+        assert pl.kernel == ("fused_separable" if (p, q) == (2, 11) else "tiled"), (p, q, pl.kernel)
         y = pl.run(x.to(DEV))
         yr = Plan(p, q, mode, pad, 2, 157, 229, dtype, "floor", force_reference=True).run(x.to(DEV))
         assert torch.equal(y.cpu().view(torch.uint8), yr.cpu().view(torch.uint8)), f"{p}/{q} {mode} {pad} kernels"
