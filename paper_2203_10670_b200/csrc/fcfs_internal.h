@@ -58,6 +58,8 @@ struct TileArgs {        // tiled kernel (k_tile.cu): output tiles with a shared
     int nr_cap, nc_cap;  // window rows / columns reserved (row pitch of the window = nc_cap)
     int xs_cap;          // floats reserved for the window (= nr_cap * nc_cap)
     int col_direct;      // strong down-scaling in both dimensions: no window; the horizontal pass reads its taps from HBM/L2
+    // multiply-shift divisors (FastDiv: d, m, s): phases px, py; tiles per row / per plane
+    uint32_t fdx[3], fdy[3], fdtx[3], fdty[3];
 };
 
 struct AdjArgs {         // adjoint kernel (k_adjoint.cu): grad_in = A^T grad_out

@@ -51,28 +51,40 @@ __global__ void __launch_bounds__(32 * kTileWarps) fcfs_tile_kernel(const __grid
     }
     pdl_wait();
     const int tiles_y = (int)((g.out_nrows + a.TH - 1) / a.TH), tiles_x = (int)((g.Wo + a.TW - 1) / a.TW);
-    const int64_t ntiles = g.planes * tiles_y * tiles_x;
+    const int64_t ntiles = g.planes * tiles_y * tiles_x;  // < 2^31 (plan)
+    const FastDiv fdx{a.fdx[0], a.fdx[1], a.fdx[2]}, fdy{a.fdy[0], a.fdy[1], a.fdy[2]};
+    const FastDiv fdtx{a.fdtx[0], a.fdtx[1], a.fdtx[2]}, fdty{a.fdty[0], a.fdty[1], a.fdty[2]};
+    // base (floor(m q / p)) and phase of output m along x / y: multiply-shift, no division
+    auto bx = [&](int m, int &j) { const int i = (int)fdiv((uint32_t)m, fdx); j = m - i * tx.p; return i * tx.q + tx.base[j]; };
+    auto by = [&](int m, int &j) { const int i = (int)fdiv((uint32_t)m, fdy); j = m - i * ty.p; return i * ty.q + ty.base[j]; };
+    int cached_tx = -1;  // column tables of the column tile last built (a CTA keeps its column tile: grid % tiles_x == 0)
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int tx_i = (int)(tile % tiles_x);
-        const int64_t rest = tile / tiles_x;
-        const int ty_i = (int)(rest % tiles_y);
-        const int64_t plane = rest / tiles_y;
+        const uint32_t t32 = (uint32_t)tile, rest = fdiv(t32, fdtx);
+        const int tx_i = (int)(t32 - rest * (uint32_t)tiles_x);
+        const uint32_t plane32 = fdiv(rest, fdty);
+        const int ty_i = (int)(rest - plane32 * (uint32_t)tiles_y);
+        const int64_t plane = plane32;
         const int my0 = (int)g.out_row0 + ty_i * a.TH, my1 = min(my0 + a.TH, (int)(g.out_row0 + g.out_nrows));
         const int mx0 = tx_i * a.TW, mx1 = min(mx0 + a.TW, (int)g.Wo);
         const int NH = my1 - my0, NW = mx1 - mx0;
-        const int c_lo = (mx0 / tx.p) * tx.q + tx.base[mx0 % tx.p] + lo;
-        const int c_hi = ((mx1 - 1) / tx.p) * tx.q + tx.base[(mx1 - 1) % tx.p] + lo + T_ - 1;
+        int jt;
+        const int c_lo = bx(mx0, jt) + lo;
+        const int c_hi = bx(mx1 - 1, jt) + lo + T_ - 1;
         const int NC = c_hi - c_lo + 1;
         // window rows: contiguous [r_lo, ...] or one slot per (output row, tap)
-        const int r_lo = a.is1d ? my0 : (my0 / ty.p) * ty.q + ty.base[my0 % ty.p] + lo;
-        const int r_hi = a.is1d ? my1 - 1 : ((my1 - 1) / ty.p) * ty.q + ty.base[(my1 - 1) % ty.p] + lo + T_ - 1;
+        const int r_lo = a.is1d ? my0 : by(my0, jt) + lo;
+        const int r_hi = a.is1d ? my1 - 1 : by(my1 - 1, jt) + lo + T_ - 1;
         const bool slots = a.row_slots && !a.is1d;
         const int NR = slots ? NH * T_ : r_hi - r_lo + 1;
         __syncthreads();  // the previous tile's readers are done with every buffer
-        for (int k = threadIdx.x; k < NW; k += blockDim.x) {
-            const int m = mx0 + k, j = m % tx.p;
-            colj[k] = j | (((j * tx.q) % tx.p == 0 || T_ == 1) ? (int)0x80000000 : 0);
-            colb[k] = (m / tx.p) * tx.q + tx.base[j] - c_lo;
+        if (tx_i != cached_tx) {  // (CTA-uniform)
+            cached_tx = tx_i;
+            for (int k = threadIdx.x; k < NW; k += blockDim.x) {
+                int j;
+                const int b = bx(mx0 + k, j);
+                colj[k] = j | (((j * tx.q) % tx.p == 0 || T_ == 1) ? (int)0x80000000 : 0);
+                colb[k] = b - c_lo;
+            }
         }
         for (int rr = threadIdx.x; rr < NH; rr += blockDim.x) {
             const int m = my0 + rr;
@@ -80,7 +92,8 @@ __global__ void __launch_bounds__(32 * kTileWarps) fcfs_tile_kernel(const __grid
                 rowj[rr] = (int)0x80000000;
                 rowb[rr] = rr;  // copy of window row rr (lo taps absent)
             } else {
-                const int j = m % ty.p, b = (m / ty.p) * ty.q + ty.base[j];  // virtual base row
+                int j;
+                const int b = by(m, j);  // virtual base row
                 rowj[rr] = j | (((j * ty.q) % ty.p == 0 || T_ == 1) ? (int)0x80000000 : 0);
                 rowb[rr] = slots ? rr * T_ : b + lo - r_lo;  // window row of tap 0 (the copy is tap -lo)
                 if (slots)

@@ -510,8 +510,22 @@ bool plan_tile(const fcfs_plan_s *pl, const RunGeom &g0, TileArgs &a, int &grid,
     // fraction of the window's columns -- read them directly instead
     a.col_direct = bestSlots && bestNC > bestTW * T && !std::getenv("FCFS_DEBUG_TILE_WINDOW");
     smem = 4 * (8 * kPMax + 2 * a.TW + 2 * a.TH + a.nr_cap) + 4 * (a.xs_cap + a.nr_cap * a.TW);
-    const int64_t ntiles = g.planes * ((g.out_nrows + a.TH - 1) / a.TH) * ((g.Wo + a.TW - 1) / a.TW);
+    const int64_t tiles_x = (g.Wo + a.TW - 1) / a.TW, tiles_y = (g.out_nrows + a.TH - 1) / a.TH;
+    const int64_t ntiles = g.planes * tiles_y * tiles_x;
+    if (ntiles >= INT32_MAX || g.Wo >= INT32_MAX / 2 || g.out_row0 + g.out_nrows >= INT32_MAX / 2) return false;
     grid = (int)std::min<int64_t>(ntiles, (int64_t)pl->sm_count * 4);
+    // a CTA keeps one column tile (its column tables are built once): grid % tiles_x == 0
+    if (grid >= tiles_x && grid < ntiles) grid -= (int)(grid % tiles_x);
+    auto fd = [](uint32_t *dst, uint32_t d) {
+        const FastDiv f = make_fastdiv(d);
+        dst[0] = f.d;
+        dst[1] = f.m;
+        dst[2] = f.s;
+    };
+    fd(a.fdx, (uint32_t)pl->tab.p);
+    fd(a.fdy, (uint32_t)pl->taby.p);
+    fd(a.fdtx, (uint32_t)tiles_x);
+    fd(a.fdty, (uint32_t)tiles_y);
     if (desc)
         std::snprintf(desc, (size_t)dlen,
                       "{\"kernel\": \"tiled\", \"TH\": %d, \"TW\": %d, \"window\": [%d, %d], \"row_slots\": %d, "
