@@ -184,6 +184,7 @@ struct WgradArgs {
     int64_t ntasks;
     int xrows, xcols, grows, gcols;  // shared tiles: x (fp32, padded) and grad_out (fp32)
     int npairs;                    // py * px (lanes take 32 per grid.y slice)
+    uint32_t fd_tasks[3], fd_nxb[3];  // FastDiv (d, m, s) of nyb * nxb and nxb (task -> plane, band; tasks < 2^31)
 };
 int launch_wgrad(int dtype, const WgradArgs &a, int grid, int smem, void *stream);
 // every successful kernel launch of the library (fcfs_kernel_launches)

@@ -31,13 +31,15 @@ __global__ void __launch_bounds__(256) fcfs_wgrad_kernel(const __grid_constant__
 #pragma unroll
         for (int k = 0; k < NT; ++k) acc[i][k] = 0.0f;
     constexpr int nty = NTY;  // rows of taps: NT (2D) or 1 (1D rows)
+    const FastDiv fd_tasks{a.fd_tasks[0], a.fd_tasks[1], a.fd_tasks[2]}, fd_nxb{a.fd_nxb[0], a.fd_nxb[1], a.fd_nxb[2]};
     // L2 prefetch of a task's x and grad_out rows (one row per thread): the
     // synchronous tile staging of the next task then hits L2
     auto prefetch = [&](int64_t task) {
         if (task >= a.ntasks) return;
-        const int64_t plane = task / (a.nyb * a.nxb);
-        const int tb = (int)(task - plane * a.nyb * a.nxb);
-        const int by = tb / a.nxb, bx = tb - by * a.nxb;
+        const uint32_t plane32 = fdiv((uint32_t)task, fd_tasks);
+        const int64_t plane = plane32;
+        const int tb = (int)((uint32_t)task - plane32 * (uint32_t)(a.nyb * a.nxb));
+        const int by = (int)fdiv((uint32_t)tb, fd_nxb), bx = tb - by * a.nxb;
         const int iy0 = by * a.yb, ix0 = bx * a.xb;
         const int ny = min(a.yb, (a.Ho + a.py - 1) / a.py - iy0), nx = min(a.xb, (a.Wo + a.px - 1) / a.px - ix0);
         const int xr = (ny - 1) * a.qy + (a.xrows - (a.yb - 1) * a.qy), xc = (nx - 1) * a.qx + (a.xcols - (a.xb - 1) * a.qx);
@@ -57,9 +59,10 @@ __global__ void __launch_bounds__(256) fcfs_wgrad_kernel(const __grid_constant__
     };
     prefetch(blockIdx.x);
     for (int64_t task = blockIdx.x; task < a.ntasks; task += gridDim.x) {
-        const int64_t plane = task / (a.nyb * a.nxb);
-        const int tb = (int)(task - plane * a.nyb * a.nxb);
-        const int by = tb / a.nxb, bx = tb - by * a.nxb;
+        const uint32_t plane32 = fdiv((uint32_t)task, fd_tasks);
+        const int64_t plane = plane32;
+        const int tb = (int)((uint32_t)task - plane32 * (uint32_t)(a.nyb * a.nxb));
+        const int by = (int)fdiv((uint32_t)tb, fd_nxb), bx = tb - by * a.nxb;
         const int iy0 = by * a.yb, ix0 = bx * a.xb;
         const int ny = min(a.yb, (a.Ho + a.py - 1) / a.py - iy0), nx = min(a.xb, (a.Wo + a.px - 1) / a.px - ix0);
         const int vr0 = iy0 * a.qy + a.fy_min, vc0 = ix0 * a.qx + a.fx_min;  // tile origins (virtual)

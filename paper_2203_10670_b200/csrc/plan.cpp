@@ -1278,6 +1278,12 @@ fcfs_status fcfs_run_weight_grad(fcfs_plan_t pl, const void *x, const void *grad
     a.nxb = (nix + a.xb - 1) / a.xb;
     a.nyb = (niy + a.yb - 1) / a.yb;
     a.ntasks = a.planes * a.nyb * a.nxb;
+    if (a.ntasks >= INT32_MAX) return FCFS_E_UNSUPPORTED;
+    {
+        const FastDiv f1 = make_fastdiv((uint32_t)(a.nyb * a.nxb)), f2 = make_fastdiv((uint32_t)a.nxb);
+        a.fd_tasks[0] = f1.d, a.fd_tasks[1] = f1.m, a.fd_tasks[2] = f1.s;
+        a.fd_nxb[0] = f2.d, a.fd_nxb[1] = f2.m, a.fd_nxb[2] = f2.s;
+    }
     const int nt = a.ntx;
     const int smem = std::max(4 * (a.xrows * a.xcols + a.grows * a.gcols), 8 * 32 * nt * nt * 4);
     const int per_sm = std::max(1, std::min(8, (227 * 1024) / (smem + 1024)));
