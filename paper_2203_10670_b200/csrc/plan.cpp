@@ -1104,7 +1104,11 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
         b.nc_cap = bNC;
         b.gw_cap = bNR * bNC;
         const int lists = (bTW + bTH) * K * 8 + (bTW + bTH) * 4 + 32, per_plane = 4 * (b.gw_cap + bTH * bNC);
-        if (band) b.PB = std::max(1, std::min(8, (72 * 1024 - lists) / per_plane));
+        int band_kb = 72;
+        if (const char *e = std::getenv("FCFS_DEBUG_BAND_KB")) band_kb = std::max(8, std::atoi(e));
+        int pb_max = 8;
+        if (const char *e = std::getenv("FCFS_DEBUG_BAND_PB")) pb_max = std::max(1, std::atoi(e));
+        if (band) b.PB = std::max(1, std::min(pb_max, (band_kb * 1024 - lists) / per_plane));
         b.smem = lists + b.PB * per_plane;
         const int64_t ngeom = (int64_t)((b.RH + bTH - 1) / bTH) * ((b.RW + bTW - 1) / bTW);
         // resident CTAs: shared memory (227 KB per SM) and 2048 threads per SM
