@@ -220,6 +220,15 @@ def run_reference(args):
                              "cores": 1 if all(c.wgrad for c in cfgs) else cores, "kind": "oracle",
                              "sample": f"each step: {desc}"},
             "e2e": {"value": value, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if args.workload == "C1":  # the 1-thread oracle time of config 0 ("well under a second")
+        import oracle
+        one = {}
+        for c in cfgs:
+            x = synth.make_values(c)
+            t0 = time.perf_counter()
+            oracle.staged(x, c.p, c.q, c.mode, c.pad, floor_extent=c.floor_extent, is1d=c.is1d, nthreads=1)
+            one[c.name] = time.perf_counter() - t0
+        line["oracle_1thread_s"] = one
     print(json.dumps(line), flush=True)
     return 0
 

@@ -42,3 +42,20 @@ def test_oracle_legs_of_the_backward_workloads():
     for name, what in (("C3B", "adjoint"), ("C3W", "weight gradient")):
         outs, secs, desc = bench.oracle_sample_run([synth.CONFIGS[name]], 1)
         assert outs == synth.CONFIGS[name].C * 213 * 213 and secs > 0 and what in desc, (name, desc)
+
+
+def test_config1_oracle_single_thread_well_under_a_second():
+    """BASELINE.json config 0: 'CPU oracle runs in well under a second' -- the
+    staged oracle on C1a (48x64 bilinear 3/2) and C1b (1D 101 nearest 2/3) on
+    one thread (report a 1-thread time for C1a/C1b)."""
+    import time
+    sys.path.insert(0, ROOT)
+    import oracle
+    import synth
+    for name in ("C1a", "C1b"):
+        c = synth.CONFIGS[name]
+        x = synth.make_values(c)
+        t0 = time.perf_counter()
+        oracle.staged(x, c.p, c.q, c.mode, c.pad, floor_extent=c.floor_extent, is1d=c.is1d, nthreads=1)
+        dt = time.perf_counter() - t0
+        assert dt < 0.5, (name, dt)
