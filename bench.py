@@ -517,47 +517,59 @@ def main():
 
 def run_e2e(launches, args, dev, stream, world, dist):
     """Same metric through the public host-buffer call (fcfs_run_host): every step
-    copies its inputs H2D from pinned memory, runs, and reads the outputs D2H."""
+    copies its inputs H2D from pinned memory, runs, and reads the outputs D2H.
+    Consecutive steps alternate between two streams with their own device and
+    pinned output buffers, so one step's D2H overlaps the next step's H2D (the
+    two copy engines), as a pipelined caller would use the API."""
     import torch
     pin_in = {}
     for L in launches:
         if L["key"] not in pin_in:
             pin_in[L["key"]] = L["x_host"].pin_memory()
-        L["pin_out"] = torch.empty(L["outs"][0].shape, dtype=L["outs"][0].dtype).pin_memory()
-    din = {k: torch.empty(v.shape, dtype=v.dtype, device=dev) for k, v in pin_in.items()}
+        L["pin_outs"] = [torch.empty(L["outs"][0].shape, dtype=L["outs"][0].dtype).pin_memory() for _ in range(2)]
+        L["pin_out"] = L["pin_outs"][0]
+    dins = [{k: torch.empty(v.shape, dtype=v.dtype, device=dev) for k, v in pin_in.items()} for _ in range(2)]
     pin_g = {L["key"]: L["g_host"].pin_memory() for L in launches if L["cfg"].wgrad}
-    gdev = {k: torch.empty(v.shape, dtype=v.dtype, device=dev) for k, v in pin_g.items()}
+    gdevs = [{k: torch.empty(v.shape, dtype=v.dtype, device=dev) for k, v in pin_g.items()} for _ in range(2)]
+    streams = [stream, torch.cuda.Stream(dev)]
     # every launch copies its own input (the C-ABI call is per launch)
     h2d = sum(pin_in[L["key"]].numel() * pin_in[L["key"]].element_size() for L in launches) + \
         sum(v.numel() * v.element_size() for v in pin_g.values())
     d2h = sum(L["pin_out"].numel() * L["pin_out"].element_size() for L in launches)
 
-    def step():
+    def step(k):
+        i = k % 2
+        st, din, gdev = streams[i], dins[i], gdevs[i]
         for L in launches:
+            out_d, out_h = L["outs"][i % len(L["outs"])], L["pin_outs"][i]
             if L["cfg"].backward:  # public API: copy in, Plan.run_adjoint, copy out (all on the stream)
-                with torch.cuda.stream(stream):
+                with torch.cuda.stream(st):
                     din[L["key"]].copy_(pin_in[L["key"]], non_blocking=True)
-                    L["plan"].run_adjoint(din[L["key"]], out=L["outs"][0], stream=stream)
-                    L["pin_out"].copy_(L["outs"][0], non_blocking=True)
+                    L["plan"].run_adjoint(din[L["key"]], out=out_d, stream=st)
+                    out_h.copy_(out_d, non_blocking=True)
             elif L["cfg"].wgrad:  # copy x and grad_out in, Plan.run_weight_grad, copy grad_w out
-                with torch.cuda.stream(stream):
+                with torch.cuda.stream(st):
                     din[L["key"]].copy_(pin_in[L["key"]], non_blocking=True)
                     gdev[L["key"]].copy_(pin_g[L["key"]], non_blocking=True)
-                    L["plan"].run_weight_grad(din[L["key"]], gdev[L["key"]], out=L["outs"][0], stream=stream)
-                    L["pin_out"].copy_(L["outs"][0], non_blocking=True)
+                    L["plan"].run_weight_grad(din[L["key"]], gdev[L["key"]], out=out_d, stream=st)
+                    out_h.copy_(out_d, non_blocking=True)
             else:
-                L["plan"].run_host(pin_in[L["key"]], L["pin_out"], din[L["key"]], L["outs"][0], stream=stream)
+                L["plan"].run_host(pin_in[L["key"]], out_h, din[L["key"]], out_d, stream=st)
 
-    for _ in range(max(2, args.warmup)):
-        step()
+    for k in range(max(2, args.warmup)):
+        step(k)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     steps = max(1, min(args.steps, 50))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(steps):
-        step()
+    streams[1].wait_event(e0)
+    for k in range(steps):
+        step(k)
+    done1 = torch.cuda.Event()
+    done1.record(streams[1])
+    stream.wait_event(done1)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
@@ -570,7 +582,8 @@ def run_e2e(launches, args, dev, stream, world, dist):
             "d2h_bytes_per_step": d2h, "steps": steps, "ms_per_step": ms / steps,
             "path": ("pinned grad_out -> HBM -> fcfs_run_adjoint -> pinned grad_in" if launches[0]["cfg"].backward else
                      "pinned x, grad_out -> HBM -> fcfs_run_weight_grad -> pinned grad_w" if launches[0]["cfg"].wgrad
-                     else "fcfs_run_host (pinned host -> HBM -> kernel -> pinned host)")}
+                     else "fcfs_run_host (pinned host -> HBM -> kernel -> pinned host)") +
+                    "; steps alternate between two streams (D2H of one overlaps H2D of the next)"}
 
 
 if __name__ == "__main__":
