@@ -467,7 +467,7 @@ def main():
 
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(launches, args, dev, stream, world, dist)
+        e2e = run_e2e(launches, args, dev, stream, world, dist, fc=fc, groups=groups)
 
     line = {
         "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": world, "steps": args.steps,
@@ -515,7 +515,7 @@ def main():
     return 0
 
 
-def run_e2e(launches, args, dev, stream, world, dist):
+def run_e2e(launches, args, dev, stream, world, dist, fc=None, groups=None):
     """Same metric through the public host-buffer call (fcfs_run_host): every step
     copies its inputs H2D from pinned memory, runs, and reads the outputs D2H.
     Consecutive steps alternate between two streams with their own device and
@@ -532,14 +532,36 @@ def run_e2e(launches, args, dev, stream, world, dist):
     pin_g = {L["key"]: L["g_host"].pin_memory() for L in launches if L["cfg"].wgrad}
     gdevs = [{k: torch.empty(v.shape, dtype=v.dtype, device=dev) for k, v in pin_g.items()} for _ in range(2)]
     streams = [stream, torch.cuda.Stream(dev)]
-    # every launch copies its own input (the C-ABI call is per launch)
-    h2d = sum(pin_in[L["key"]].numel() * pin_in[L["key"]].element_size() for L in launches) + \
-        sum(v.numel() * v.element_size() for v in pin_g.values())
+    # a workload of several forward launches over one batch (C2, C4: two factors)
+    # copies the batch in once per step and runs every launch on it (run_batch
+    # where the launches share a kernel launch); single launches use the
+    # one-call host path
+    batched = (groups is not None and fc is not None and len(launches) > 1 and
+               not any(L["cfg"].backward or L["cfg"].wgrad for L in launches))
+    if batched:
+        h2d = sum(v.numel() * v.element_size() for v in pin_in.values())
+    else:
+        h2d = sum(pin_in[L["key"]].numel() * pin_in[L["key"]].element_size() for L in launches) + \
+            sum(v.numel() * v.element_size() for v in pin_g.values())
     d2h = sum(L["pin_out"].numel() * L["pin_out"].element_size() for L in launches)
 
     def step(k):
         i = k % 2
         st, din, gdev = streams[i], dins[i], gdevs[i]
+        if batched:  # copy the batch in once, one fcfs_run_batch launch, copy every output back
+            with torch.cuda.stream(st):
+                for key, v in pin_in.items():
+                    din[key].copy_(v, non_blocking=True)
+                for grp in groups:
+                    if len(grp) > 1:
+                        fc.run_batch([(launches[j]["plan"], din[launches[j]["key"]],
+                                       launches[j]["outs"][i % len(launches[j]["outs"])]) for j in grp], stream=st)
+                    else:
+                        L = launches[grp[0]]
+                        L["plan"].run(din[L["key"]], out=L["outs"][i % len(L["outs"])], stream=st)
+                for L in launches:
+                    L["pin_outs"][i].copy_(L["outs"][i % len(L["outs"])], non_blocking=True)
+            return
         for L in launches:
             out_d, out_h = L["outs"][i % len(L["outs"])], L["pin_outs"][i]
             if L["cfg"].backward:  # public API: copy in, Plan.run_adjoint, copy out (all on the stream)
@@ -580,7 +602,9 @@ def run_e2e(launches, args, dev, stream, world, dist):
     outputs = sum(L["outputs"] for L in launches)
     return {"value": world * outputs * steps / (ms * 1e-3) / 1e6, "unit": "Mpix/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps, "ms_per_step": ms / steps,
-            "path": ("pinned grad_out -> HBM -> fcfs_run_adjoint -> pinned grad_in" if launches[0]["cfg"].backward else
+            "path": ("pinned batch -> HBM once -> every factor's launch (fcfs_run_batch / fcfs_run) -> pinned outputs"
+                     if batched else
+                     "pinned grad_out -> HBM -> fcfs_run_adjoint -> pinned grad_in" if launches[0]["cfg"].backward else
                      "pinned x, grad_out -> HBM -> fcfs_run_weight_grad -> pinned grad_w" if launches[0]["cfg"].wgrad
                      else "fcfs_run_host (pinned host -> HBM -> kernel -> pinned host)") +
                     "; steps alternate between two streams (D2H of one overlaps H2D of the next)"}
