@@ -984,8 +984,12 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     pdl_launch_dependents();
     if (span_e == 0) bulk_wait0();
     };
-    if (kShift && a.sw_load) consumers(std::true_type{});
-    else consumers(std::false_type{});
+    if constexpr (kShift) {  // (3D variants: no shifted copy of the consumer code)
+        if (a.sw_load) consumers(std::true_type{});
+        else consumers(std::false_type{});
+    } else {
+        consumers(std::false_type{});
+    }
     }
 }
 
