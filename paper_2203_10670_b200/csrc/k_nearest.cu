@@ -107,9 +107,9 @@ static void launch_nearest_t(const NearestBatch &nb, cudaStream_t s) {
     case 1: launch_nearest_v<T, 8, 2, 4>(nb, s); break;
     case 2: launch_nearest_v<T, 8, 4, 4>(nb, s); break;
     case 3: launch_nearest_v<T, 16, 1, 4>(nb, s); break;
-    case 4: launch_nearest_v<T, 12, 2, 3>(nb, s); break;
+    case 4: launch_nearest_v<T, 12, 2, 4>(nb, s); break;
     case 5: launch_nearest_v<T, 12, 4, 2>(nb, s); break;
-    default: launch_nearest_v<T, 12, 2, 4>(nb, s); break;
+    default: launch_nearest_v<T, 12, 2, 3>(nb, s); break;  // 3 CTAs/SM: C2 -4% vs 4 (tools/nearest_ab.py)
     }
 }
 

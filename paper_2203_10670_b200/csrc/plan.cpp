@@ -439,8 +439,8 @@ int select_kernel(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
         const int64_t rows = g.planes * g.Do * g.out_nrows;
         std::snprintf(L.desc, sizeof(L.desc),
                       "{\"kernel\": \"nearest_gather\", \"rows\": %lld, \"grid\": %lld, \"block\": 256, "
-                      "\"outputs_per_lane_iter\": 8}",
-                      (long long)rows, (long long)std::min<int64_t>((rows + 7) / 8, 148 * 8 * 4));
+                      "\"rows_per_warp_pass\": 2, \"columns_per_lane_pass\": 12}",
+                      (long long)rows, (long long)std::min<int64_t>(((rows + 1) / 2 + 7) / 8, (int64_t)pl->sm_count * 3));
     } else if (kernel == 0) {
         const int64_t total = g.planes * g.Do * g.out_nrows * pl->Wo;
         std::snprintf(L.desc, sizeof(L.desc), "{\"kernel\": \"reference\", \"grid\": %lld, \"block\": 256}",
