@@ -1077,7 +1077,9 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
         int bTH = 0, bTW = 0, bNR = 0, bNC = 0;
         if (band) {  // border bands: the region's own width (<= 256) x up to 64 rows, exact windows
             bTW = std::min(b.RW, 256);
-            bTH = std::min(b.RH, 64);
+            int band_th = 64;
+            if (const char *e = std::getenv("FCFS_DEBUG_BAND_TH")) band_th = std::max(1, std::atoi(e));
+            bTH = std::min(b.RH, band_th);
             bNC = (adj_window(pl->tab, pl->W, pl->Wo, pl->pad, b.C0, b.RW, bTW) + 3) / 4 * 4;
             bNR = pl->is1d ? bTH : adj_window(pl->taby, pl->H, pl->Ho, pl->pad, b.R0, b.RH, bTH);
         }
