@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define FCFS_VERSION 3
+#define FCFS_VERSION 4
 #define FCFS_MAX_FACTOR 64 /* p and q (after gcd reduction) must be <= 64 */
 
 typedef struct fcfs_plan_s *fcfs_plan_t;
@@ -283,6 +283,14 @@ fcfs_status fcfs_plan_info(fcfs_plan_t plan, fcfs_plan_info_t *info);
  * FCFS_E_ARG. */
 fcfs_status fcfs_launch_info(fcfs_plan_t plan, int64_t N, int64_t out_row0, int64_t out_nrows, char *buf,
                              int64_t buflen);
+
+/* fcfs_adjoint_info -- host-only description (JSON, as fcfs_launch_info) of
+ * the launches fcfs_run_adjoint would make for N images with 16-B-aligned
+ * buffers: {"kernel": "fused_adjoint", PY/QY/PX/QX (the forward factors),
+ * "taps", "bands" (border regions rewritten by the second launch),
+ * "launches"}, or {"kernel": "tiled_adjoint" | "reference_adjoint"}.
+ * Errors: FCFS_E_ARG. */
+fcfs_status fcfs_adjoint_info(fcfs_plan_t plan, int64_t N, char *buf, int64_t buflen);
 
 /* The fp32 phase table of the W dimension: for phase j in [0, p), weights
  * w[4*j + t] (t < ntaps; unused entries 0) and base offsets base[j] =

@@ -1032,16 +1032,21 @@ int adj_window(const PhaseTable &t, int64_t n, int64_t no, int pad, int64_t r0, 
     return best;
 }
 
-fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in, int64_t N, void *stream) {
+// The backward pass: launches on `stream`, or -- info != nullptr -- only
+// describes the launches it would make (fcfs_adjoint_info) as JSON.
+static fcfs_status adjoint_impl(fcfs_plan_t pl, const void *grad_out, void *grad_in, int64_t N, void *stream,
+                                char *info, int64_t infolen) {
     if (!pl || N < 0) return FCFS_E_ARG;
-    if (N == 0) return FCFS_OK;
-    if (!grad_out || !grad_in) return FCFS_E_ARG;
+    if (N == 0 && !info) return FCFS_OK;
     const int ESZ = esize(pl->dtype);
     const int64_t planes = N * pl->C;
-    const int64_t gin = planes * pl->D * pl->H * pl->W * ESZ, gout = planes * pl->Do * pl->Ho * pl->Wo * ESZ;
-    if (ranges_overlap(grad_out, gout, grad_in, gin)) return FCFS_E_ARG;
-    fcfs_status st = check_device(pl);
-    if (st != FCFS_OK) return st;
+    if (!info) {
+        if (!grad_out || !grad_in) return FCFS_E_ARG;
+        const int64_t gin = planes * pl->D * pl->H * pl->W * ESZ, gout = planes * pl->Do * pl->Ho * pl->Wo * ESZ;
+        if (ranges_overlap(grad_out, gout, grad_in, gin)) return FCFS_E_ARG;
+        fcfs_status st = check_device(pl);
+        if (st != FCFS_OK) return st;
+    }
     AdjArgs a;
     a.grad_out = grad_out;
     a.grad_in = grad_in;
@@ -1147,8 +1152,16 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
         FusedLaunch L;
         if (planes * std::max(pl->Ho * pl->Wo, pl->H * pl->W) <= INT32_MAX * 16LL &&
             plan_fused(pl, g, L, v, FCFS_PAD_ZERO)) {
-            if (launch_fused(v, L.a, L.grid, kFusedThreads, L.smem, stream) != 0) return FCFS_E_CUDA;
-            if (pl->pad == FCFS_PAD_ZERO || std::getenv("FCFS_DEBUG_NO_BANDS")) return FCFS_OK;
+            const bool no_bands = pl->pad == FCFS_PAD_ZERO || std::getenv("FCFS_DEBUG_NO_BANDS");
+            if (info) {
+                if (no_bands)
+                    std::snprintf(info, (size_t)infolen, "{\"kernel\": \"fused_adjoint\", \"PY\": %d, \"QY\": %d, "
+                                  "\"PX\": %d, \"QX\": %d, \"taps\": %d, \"bands\": 0, \"launches\": 1}",
+                                  v->PY, v->QY, v->PX, v->QX, v->TAPS);
+            } else if (launch_fused(v, L.a, L.grid, kFusedThreads, L.smem, stream) != 0) {
+                return FCFS_E_CUDA;
+            }
+            if (no_bands) return FCFS_OK;
             // border bands: indices that receive padding images (Z21)
             auto bands = [&](const PhaseTable &t, int64_t n, int64_t no, int64_t &bl, int64_t &br) {
                 const int64_t vmin = t.lo, vmax = ((no - 1) / t.p) * t.q + t.base[(no - 1) % t.p] + t.lo + t.ntaps - 1;
@@ -1188,12 +1201,32 @@ fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in
                 all.grid += b.grid;
                 all.smem = std::max(all.smem, b.smem);
             }
+            if (info) {
+                std::snprintf(info, (size_t)infolen, "{\"kernel\": \"fused_adjoint\", \"PY\": %d, \"QY\": %d, "
+                              "\"PX\": %d, \"QX\": %d, \"taps\": %d, \"bands\": %d, \"launches\": %d}",
+                              v->PY, v->QY, v->PX, v->QX, v->TAPS, nreg, 1 + (nreg ? 1 : 0));
+                return FCFS_OK;
+            }
             if (nreg && launch_adjoint(pl->dtype, all, stream) != 0) return FCFS_E_CUDA;
             return FCFS_OK;
         }
     }
     if (tiled_ok) plan_tiles(a, false);
+    if (info) {
+        std::snprintf(info, (size_t)infolen, "{\"kernel\": \"%s\", \"launches\": 1}",
+                      a.TH > 0 ? "tiled_adjoint" : "reference_adjoint");
+        return FCFS_OK;
+    }
     return launch_adjoint(pl->dtype, a, stream) == 0 ? FCFS_OK : FCFS_E_CUDA;
+}
+
+fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in, int64_t N, void *stream) {
+    return adjoint_impl(pl, grad_out, grad_in, N, stream, nullptr, 0);
+}
+
+fcfs_status fcfs_adjoint_info(fcfs_plan_t pl, int64_t N, char *buf, int64_t buflen) {
+    if (!pl || !buf || buflen < 2 || N < 1) return FCFS_E_ARG;
+    return adjoint_impl(pl, nullptr, nullptr, N, nullptr, buf, buflen);
 }
 
 // Weight gradient (reading Z22): shape (py, px, nty, ntx); 1D / rank 1: (1, p, 1, taps).

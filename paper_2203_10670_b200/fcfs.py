@@ -123,6 +123,13 @@ class Plan:
         check(_lib.lib.fcfs_launch_info(self._h, N, out_row0, n, buf, 1024), "fcfs_launch_info")
         return json.loads(buf.value.decode())
 
+    def adjoint_info(self, N: int) -> dict:
+        """The launches run_adjoint would make (host only, fcfs_adjoint_info)."""
+        import json
+        buf = ctypes.create_string_buffer(1024)
+        check(_lib.lib.fcfs_adjoint_info(self._h, N, buf, 1024), "fcfs_adjoint_info")
+        return json.loads(buf.value.decode())
+
     def needed_rows(self, out0: int, out1: int):
         """Input rows [need0, need1) that output rows [out0, out1) read."""
         a, b = ctypes.c_int64(), ctypes.c_int64()
@@ -240,9 +247,31 @@ class Plan:
                                      self._stream(stream)), "fcfs_run_rows")
         return out
 
+    def _check_host(self, t, shape, what):
+        import torch
+        if not isinstance(t, torch.Tensor) or t.device.type != "cpu":
+            raise TypeError(f"{what} must be a CPU tensor")
+        if _dtype_name(t.dtype) != self.dtype:
+            raise TypeError(f"{what} dtype {t.dtype} does not match the plan's {self.dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{what} must be contiguous")
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{what} shape {tuple(t.shape)} != {tuple(shape)}")
+        if not t.is_pinned():
+            import warnings
+            warnings.warn(f"{what} is not pinned: the copy is synchronous and slower", stacklevel=3)
+
     def run_host(self, x_host, out_host, dev_in, dev_out, stream=None):
-        """End-to-end call with host buffers (H2D copy, run, D2H copy on the stream)."""
+        """End-to-end call with host buffers (fcfs_run_host): H2D copy of x_host
+        into dev_in, the run into dev_out, D2H copy into out_host, all enqueued on
+        the stream.  out_host holds the result only after that stream has
+        synchronised.  Host tensors: contiguous CPU (pinned for async copies);
+        device tensors: contiguous CUDA; all of the plan dtype and shapes."""
         N = x_host.shape[0]
+        self._check_host(x_host, self.in_shape(N), "x_host")
+        self._check_host(out_host, self.out_shape(N), "out_host")
+        self._check_tensor(dev_in, self.in_shape(N), "dev_in")
+        self._check_tensor(dev_out, self.out_shape(N), "dev_out")
         check(_lib.lib.fcfs_run_host(self._h, ctypes.c_void_p(x_host.data_ptr()), ctypes.c_void_p(out_host.data_ptr()),
                                      N, ctypes.c_void_p(dev_in.data_ptr()), ctypes.c_void_p(dev_out.data_ptr()),
                                      self._stream(stream)), "fcfs_run_host")

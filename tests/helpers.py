@@ -30,15 +30,22 @@ def fp32_error_bound(mode: str, x_absmax: float) -> float:
     return 2.0 ** -20 * WSUM[mode] ** 2 * x_absmax
 
 
+RELAXED_MAX_FRAC = 1e-3  # relaxed (reading Z18) elements allowed per comparison, as a fraction of its outputs
+
+
 def compare(gpu: torch.Tensor, ref64: np.ndarray, dtype: str, mode: str, x_range: float, what: str = "",
-            x_absmax: float | None = None):
+            x_absmax: float | None = None, report: list | None = None):
     """Assert the BASELINE.json bar: nearest bit-exact; fp32 within 1e-5 * range;
     fp16/bf16 within 1 ulp of the oracle's fp32 result rounded to the dtype.
 
-    Reading Z18: where the exact result lies so close to zero that
-    the fp32 accumulation the bar prescribes cannot resolve 1 ulp of the dtype,
-    an element also passes if |gpu - exact| <= 1 dtype-spacing + the fp32 error
-    bound (fp32_error_bound).  The count of such elements is returned."""
+    Reading Z18: an element more than 1 ulp off still passes only
+    if the exact value is so close to zero that the fp32 accumulation the bar
+    prescribes cannot resolve one ulp of the dtype there -- one dtype spacing
+    at the exact value <= 2 E, E = fp32_error_bound(mode, max|x|) -- and then
+    only within |gpu - exact| <= spacing + E.  x_absmax is max|x| of the input
+    (required for 16-bit interpolating modes).  Returns the number of relaxed
+    elements (appended to `report` as (what, n, size) when given); more than
+    RELAXED_MAX_FRAC of the outputs relaxed fails."""
     gpu = gpu.cpu()
     ref64 = np.asarray(ref64, dtype=np.float64).reshape(tuple(gpu.shape))
     if dtype == "float32":
@@ -49,28 +56,39 @@ def compare(gpu: torch.Tensor, ref64: np.ndarray, dtype: str, mode: str, x_range
         else:
             err = np.abs(g - ref64).max() if g.size else 0.0
             assert err <= TOL_F32 * max(x_range, 1e-30), f"{what}: max abs err {err} > {TOL_F32} * {x_range}"
-        return
+        return 0
     ref = oracle.round_to(ref64, dtype)
     ref_t = ref if isinstance(ref, torch.Tensor) else torch.from_numpy(ref)
     gb, rb = to_bits16(gpu), to_bits16(ref_t)
     if mode == "nearest":
         np.testing.assert_array_equal(gb, rb, err_msg=what)
-        return
+        return 0
+    assert x_absmax is not None, "16-bit parity needs max|x| (reading Z18)"
     d = np.abs(ordered16(gb) - ordered16(rb))
     bad = d > 1
-    n_near_zero = 0
+    n_relaxed = 0
     if bad.any():
-        xa = x_range if x_absmax is None else x_absmax
-        g64 = gpu.to(torch.float64).numpy()
-        nxt = torch.from_numpy(((rb + 1) & 0xFFFF).astype(np.int16).view(np.int16)).view(ref_t.dtype)
-        spacing = np.abs(nxt.to(torch.float64).numpy() - ref_t.to(torch.float64).numpy())
-        ok2 = np.abs(g64 - ref64) <= spacing + fp32_error_bound(mode, xa)
-        n_near_zero = int((bad & ok2).sum())
-        bad &= ~ok2
-    assert not bad.any(), (f"{what}: {int(d[bad].max())} ulp at {np.unravel_index(np.argmax(np.where(bad, d, -1)), d.shape)}"
-                           f" gpu={gpu.flatten()[np.argmax(np.where(bad, d, -1))]} exact="
-                           f"{ref64.flatten()[np.argmax(np.where(bad, d, -1))]}")
-    return n_near_zero
+        E = fp32_error_bound(mode, x_absmax)
+        idx = np.nonzero(bad.ravel())[0]
+        g64 = gpu.to(torch.float64).numpy().ravel()[idx]
+        e64 = ref64.ravel()[idx]
+        r16 = ref_t.reshape(-1)[torch.from_numpy(idx)]
+        rbits = rb.ravel()[idx]
+        nxt = torch.from_numpy(((rbits + 1) & 0xFFFF).astype(np.int16)).view(ref_t.dtype)
+        spacing = np.abs(nxt.to(torch.float64).numpy() - r16.to(torch.float64).numpy())
+        ok2 = (spacing <= 2 * E) & (np.abs(g64 - e64) <= spacing + E)
+        n_relaxed = int(ok2.sum())
+        bad.ravel()[idx[ok2]] = False
+    if bad.any():
+        k = int(np.argmax(np.where(bad, d, -1)))
+        raise AssertionError(f"{what}: {int(d.ravel()[k])} ulp at {np.unravel_index(k, d.shape)} "
+                             f"gpu={float(gpu.reshape(-1)[k])} exact={ref64.ravel()[k]}")
+    if report is not None:
+        report.append((what, n_relaxed, int(d.size)))
+    if n_relaxed:
+        print(f"[Z18] {what}: {n_relaxed} of {d.size} elements relaxed")
+    assert n_relaxed <= RELAXED_MAX_FRAC * max(d.size, 1), f"{what}: {n_relaxed} relaxed elements of {d.size}"
+    return n_relaxed
 
 
 def oracle_input(x_cpu: torch.Tensor) -> np.ndarray:

@@ -4,8 +4,8 @@ Bar (BASELINE.json north_star): nearest bit-exact; fp32 max abs error <=
 1e-5 x input range; fp16/bf16 within 1 ulp of the oracle's fp32 result rounded
 to the dtype.  Full-size configs are checked on sampled outputs (plus whole
 border rows/columns) computed one by one by the oracle's direct evaluator, on
-every output of whole planes by the staged oracle, and on every output against
-the reference kernel (bitwise: both kernels share one arithmetic contract).
+every output by the staged oracle (in chunks of planes), and on every output
+against the reference kernel (bitwise: both kernels share one arithmetic contract).
 """
 import itertools
 import zlib
@@ -36,12 +36,16 @@ def run_cfg(cfg: synth.Config, x_dev, force_reference=False):
     return pl, y
 
 
-def check_full_config(cfg: synth.Config, n_points=60000, whole_planes=(0,)):
+def check_full_config(cfg: synth.Config, n_points=60000, chunk_planes=256):
+    """Every output of a BASELINE config against the staged oracle (in chunks of
+    planes), sampled outputs against the direct evaluator, and every output
+    against the reference kernel (bitwise).  Returns (plan, relaxed Z18 count)."""
     x = synth.make_input(cfg)
     xd = x.to(DEV)
     pl, y = run_cfg(cfg, xd)
     xr = oracle_input(x)
     rng = float(xr.max() - xr.min())
+    amax = float(np.abs(xr).max())
     planes = cfg.planes
     Ho, Wo = pl.output_shape()
     assert tuple(y.shape) == (cfg.N, cfg.C, Ho, Wo)
@@ -52,16 +56,21 @@ def check_full_config(cfg: synth.Config, n_points=60000, whole_planes=(0,)):
     ref = oracle.direct_points(xr.reshape(planes, cfg.H, cfg.W), pts, cfg.p, cfg.q, cfg.mode, cfg.pad, **ext)
     got = y.reshape(planes, Ho, Wo)[torch.from_numpy(pts[:, 0]), torch.from_numpy(pts[:, 1]),
                                     torch.from_numpy(pts[:, 2])]
-    compare(got, ref, cfg.dtype, cfg.mode, rng, f"{cfg.name} sampled")
-    # (2) whole planes, staged oracle
-    for pli in whole_planes:
-        ref = oracle.staged(xr.reshape(planes, cfg.H, cfg.W)[pli], cfg.p, cfg.q, cfg.mode, cfg.pad, **ext)
-        compare(y.reshape(planes, Ho, Wo)[pli], ref, cfg.dtype, cfg.mode, rng, f"{cfg.name} plane {pli}")
+    compare(got, ref, cfg.dtype, cfg.mode, rng, f"{cfg.name} sampled", x_absmax=amax)
+    # (2) every output, staged oracle (all outputs of C1-C4)
+    yc = y.reshape(planes, Ho, Wo).cpu()
+    xp = xr.reshape(planes, cfg.H, cfg.W)
+    relaxed = 0
+    for p0 in range(0, planes, chunk_planes):
+        p1 = min(planes, p0 + chunk_planes)
+        ref = oracle.staged(xp[p0:p1], cfg.p, cfg.q, cfg.mode, cfg.pad, **ext)
+        relaxed += compare(yc[p0:p1], ref, cfg.dtype, cfg.mode, rng, f"{cfg.name} planes {p0}:{p1}", x_absmax=amax)
+    print(f"{cfg.name}: every output ({planes * Ho * Wo}) checked against the oracle, {relaxed} relaxed (Z18)")
     # (3) every output: fused/gather kernel == reference kernel, bitwise
     _, yr = run_cfg(cfg, xd, force_reference=True)
     assert torch.equal(y.view(torch.int16 if cfg.dtype != "float32" else torch.int32),
                        yr.view(torch.int16 if cfg.dtype != "float32" else torch.int32)), f"{cfg.name}: kernels differ"
-    return pl
+    return pl, relaxed
 
 
 @pytest.mark.parametrize("name", ["C1a", "C1b"])
@@ -71,7 +80,7 @@ def test_config1_every_output(name):
     pl, y = run_cfg(cfg, x.to(DEV))
     ref = oracle.staged(oracle_input(x), cfg.p, cfg.q, cfg.mode, cfg.pad, floor_extent=cfg.floor_extent,
                         is1d=cfg.is1d)
-    compare(y, ref, cfg.dtype, cfg.mode, float(x.max() - x.min()), name)
+    compare(y, ref, cfg.dtype, cfg.mode, float(x.max() - x.min()), name, x_absmax=float(x.abs().max()))
     assert tuple(y.shape[-2:]) == {"C1a": (72, 96), "C1b": (1, 67)}[name]
 
 
@@ -86,17 +95,18 @@ def test_config2_nearest_bit_exact_every_output(name):
 
 
 def test_config3_bicubic_bf16():
-    pl = check_full_config(synth.CONFIGS["C3"], whole_planes=(0, 4095))
+    pl, relaxed = check_full_config(synth.CONFIGS["C3"])
+    assert relaxed <= 1e-5 * 4096 * 213 * 213
     assert pl.kernel == "fused_separable" and pl.output_shape() == (213, 213)
 
 
 @pytest.mark.parametrize("name", ["C4a", "C4b"])
 def test_config4_bilinear_fp16(name):
-    pl = check_full_config(synth.CONFIGS[name], whole_planes=(5,))
+    pl, relaxed = check_full_config(synth.CONFIGS[name], chunk_planes=4)
     assert pl.kernel == "fused_separable"
 
 
-def test_config5_giant_image_sampled():
+def test_config5_giant_image_every_output():
     cfg = synth.CONFIGS["C5"]
     x = synth.make_input(cfg)
     xd = x.to(DEV)
@@ -121,6 +131,17 @@ def test_config5_giant_image_sampled():
         ref = oracle.direct(xr[0, 0, lo:hi], 3, 5, "bicubic", "replicate", floor_extent=True, rows=(r0, r0 + 1),
                             H=cfg.H, row0=lo)
         compare(y[0, 0, r0:r0 + 1], ref, "float32", "bicubic", rng, f"C5 row {r0}")
+    # every output, staged oracle in blocks of output rows (all C5
+    # outputs when host RAM allows; the image is never padded whole in double)
+    yc = y.reshape(19660, 19660).cpu().numpy()
+    for r0 in range(0, 19660, 2048):
+        r1 = min(19660, r0 + 2048)
+        # the staged layer's union window of hidden positions i = m div 3: rows [5i - 1, 5i + 5]
+        n0, n1 = max(0, 5 * (r0 // 3) - 1), min(cfg.H, 5 * ((r1 - 1) // 3) + 6)
+        ref = oracle.staged(xr[0, 0, n0:n1], cfg.p, cfg.q, cfg.mode, cfg.pad, floor_extent=True, rows=(r0, r1),
+                            H=cfg.H, row0=n0)
+        err = float(np.abs(yc[r0:r1].astype(np.float64) - ref).max())
+        assert err <= 1e-5 * rng, f"C5 rows {r0}:{r1}: max abs err {err}"
     # every output: fused == reference, bitwise
     _, yr = run_cfg(cfg, xd, force_reference=True)
     assert torch.equal(y.view(torch.int32), yr.view(torch.int32))
@@ -160,7 +181,8 @@ def test_sweep_every_output(mode, pad):
         torch.cuda.synchronize()
         xr = oracle_input(x)
         ref = oracle.staged(xr, p, q, mode, pad, floor_extent=(ext == "floor"))
-        compare(y, ref, dtype, mode, float(xr.max() - xr.min()), f"{p}/{q} {mode} {pad} {dtype} {ext} {H}x{W}")
+        compare(y, ref, dtype, mode, float(xr.max() - xr.min()), f"{p}/{q} {mode} {pad} {dtype} {ext} {H}x{W}",
+                x_absmax=float(np.abs(xr).max()))
         yr = Plan(p, q, mode, pad, C, H, W, dtype, ext, force_reference=True).run(x.to(DEV))
         assert torch.equal(y.cpu().view(torch.uint8), yr.cpu().view(torch.uint8)), f"{p}/{q} {mode} {pad} kernels"
 
@@ -172,7 +194,8 @@ def test_1d_rows(mode):
         pl = Plan(p, q, mode, "replicate", 3, 5, 101, dtype, "floor", is1d=True)
         y = pl.run(x.to(DEV))
         ref = oracle.staged(oracle_input(x), p, q, mode, "replicate", floor_extent=True, is1d=True)
-        compare(y, ref, dtype, mode, float(x.float().max() - x.float().min()), f"1d {p}/{q} {dtype}")
+        compare(y, ref, dtype, mode, float(x.float().max() - x.float().min()), f"1d {p}/{q} {dtype}",
+                x_absmax=float(x.float().abs().max()))
 
 
 def test_identity_bit_exact():
@@ -226,7 +249,8 @@ def test_misaligned_and_odd_pitch_buffers():
         pl = Plan(5, 3, "bicubic", "reflect", 2, 50, 64, dtype, "floor")
         y = pl.run(x)
         ref = oracle.staged(oracle_input(x.cpu()), 5, 3, "bicubic", "reflect", floor_extent=True)
-        compare(y, ref, dtype, "bicubic", float(x.float().max() - x.float().min()), f"misaligned {dtype}")
+        compare(y, ref, dtype, "bicubic", float(x.float().max() - x.float().min()), f"misaligned {dtype}",
+                x_absmax=float(x.float().abs().max()))
         out_base = torch.empty(y.numel() + 1, dtype=y.dtype, device=DEV)
         y2 = out_base[1:].view(y.shape)
         pl.run(x, out=y2)
@@ -270,6 +294,17 @@ def test_run_host_end_to_end():
     pl.run_host(x, out, din, dout)
     torch.cuda.synchronize()
     assert torch.equal(out.view(torch.int16), pl.run(x.to(DEV)).cpu().view(torch.int16))
+    # every buffer is validated before anything is enqueued
+    with pytest.raises(TypeError):
+        pl.run_host(x.float(), out, din, dout)
+    with pytest.raises(ValueError):
+        pl.run_host(x, out[:, :, :212], din, dout)
+    with pytest.raises(ValueError):
+        pl.run_host(x, out, din, dout[:1])
+    with pytest.raises(TypeError):
+        pl.run_host(x, out, din.cpu(), dout)
+    with pytest.raises(TypeError):
+        pl.run_host(x.to(DEV), out, din, dout)
 
 
 def test_run_batch_matches_single_runs():
@@ -323,7 +358,8 @@ def test_tiled_kernel_paper_factors(mode, dtype):
         assert torch.equal(y.cpu().view(torch.uint8), yr.cpu().view(torch.uint8)), f"{p}/{q} {mode} {pad} kernels"
         xr = oracle_input(x)
         ref = oracle.staged(xr, p, q, mode, pad, floor_extent=True)
-        compare(y, ref, dtype, mode, float(xr.max() - xr.min()), f"tiled {p}/{q} {mode} {pad} {dtype}")
+        compare(y, ref, dtype, mode, float(xr.max() - xr.min()), f"tiled {p}/{q} {mode} {pad} {dtype}",
+                x_absmax=float(np.abs(xr).max()))
 
 
 @pytest.mark.parametrize("pad", ["zero", "replicate", "reflect"])
@@ -347,7 +383,8 @@ def test_unaligned_rows_fused(pad):
             assert pl.launch_info(N)["kernel"] == "fused_separable", (p, q, dtype, W)
         xr = oracle_input(x.cpu())
         ref = oracle.staged(xr, p, q, "bicubic", pad, floor_extent=True)
-        compare(y, ref, dtype, "bicubic", float(xr.max() - xr.min()), f"unaligned {p}/{q} {pad} {dtype} {H}x{W}+{off}")
+        compare(y, ref, dtype, "bicubic", float(xr.max() - xr.min()), f"unaligned {p}/{q} {pad} {dtype} {H}x{W}+{off}",
+                x_absmax=float(np.abs(xr).max()))
         yr = Plan(p, q, "bicubic", pad, C, H, W, dtype, "floor", force_reference=True).run(x)
         assert torch.equal(y.view(torch.uint8), yr.view(torch.uint8)), (p, q, pad, dtype, W, off)
 
