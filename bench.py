@@ -6,10 +6,13 @@ HBM GB/s vs 8 TB/s, 1/2/4/8 B200).
     torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU, NCCL)
 
 A step is one pass of the whole hot path over one batch: every launch of the
-workload (C2 = nearest 2/3 and 3/4 on 16x3x512^2 fp32, BASELINE.json
-configs[1]).  Batched workloads scale weakly: every rank scales its own batch,
-no data-path collective.  C5 (one 32768^2 image) shards by row strips with an
-NCCL halo exchange when N > 1 (paper_2203_10670_b200.dist).
+workload.  The default workload is C5 (BASELINE.json configs[4]: one
+32768^2 fp32 image, bicubic 3/5), the largest single-GPU configuration: the
+metric names no config, so the headline is measured on the largest one.  At
+N > 1 C5 shards by row strips with an NCCL halo exchange (strong scaling,
+paper_2203_10670_b200.dist); batched workloads (C2 16, C3 64, C4 8 images)
+give each rank its share of the batch (--split batch, strong scaling, no
+data-path collective) or a whole batch of its own (--split weak).
 
 Prints ONE JSON line on rank 0.  Inputs are resident in HBM before the timed
 region; between steps the input/output buffers rotate over a set larger than
@@ -19,6 +22,8 @@ launching stream, max over ranks.
 from __future__ import annotations
 
 import argparse
+import dataclasses
+import datetime
 import json
 import os
 import statistics
@@ -41,7 +46,10 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="C2", choices=sorted(synth.WORKLOADS))
+    ap.add_argument("--workload", default="C5", choices=sorted(synth.WORKLOADS))
+    ap.add_argument("--split", default="batch", choices=["batch", "weak"],
+                    help="batched workloads at N > 1: 'batch' gives rank r its share of the config's N images "
+                         "(SURVEY 8(e), strong scaling); 'weak' gives every rank a whole batch of its own")
     ap.add_argument("--impl", default="fcfs", choices=["fcfs", "reference"])
     ap.add_argument("--soak-s", type=float, default=1.0, help="untimed steady-state run before warm-up (clocks)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -50,6 +58,7 @@ def parse():
     ap.add_argument("--halo", default="nccl", choices=["nccl", "peer"],
                     help="C5 row strips at N > 1: NCCL send/recv halo, or in-kernel peer reads (symmetric memory)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-strips", action="store_true", help="C5: the row-strip path even at N = 1 (testing)")
     return ap.parse_args()
 
 
@@ -117,6 +126,42 @@ class ClockSampler:
                 "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
 
 
+def batch_share(n: int, rank: int, world: int):
+    """Images [a, b) of an n-image batch that rank `rank` of `world` scales
+    (--split batch): contiguous, disjoint, covering [0, n)."""
+    return rank * n // world, (rank + 1) * n // world
+
+
+def provenance():
+    """What ran where: the git commit when the tree has one (gpurun copies omit
+    .git), a hash of the product sources and bench.py, the host CPU."""
+    import glob
+    import hashlib
+    out = {}
+    try:
+        out["git_sha"] = subprocess.run(["git", "-C", ROOT, "rev-parse", "HEAD"], capture_output=True, text=True,
+                                        timeout=10).stdout.strip() or None
+    except Exception:
+        out["git_sha"] = None
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(ROOT, "paper_2203_10670_b200", "csrc", "*")) +
+                   glob.glob(os.path.join(ROOT, "include", "*.h")) + [os.path.join(ROOT, "bench.py")])
+    for f in files:
+        with open(f, "rb") as fh:
+            h.update(os.path.basename(f).encode() + fh.read())
+    out["src_sha16"] = h.hexdigest()[:16]
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    out["host_cpu"] = {"model": model, "cores": os.cpu_count()}
+    return out
+
+
 def physical_gpu_index(local_rank: int) -> int:
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     if vis:
@@ -128,9 +173,11 @@ def physical_gpu_index(local_rank: int) -> int:
 
 
 # --------------------------------------------------------------------------- CPU oracle leg
-def oracle_sample_run(cfgs, planes_per_cfg: int):
+def oracle_sample_run(cfgs, planes_per_cfg: int, keep: list | None = None):
     """Run the oracle (staged, as it stands) on `planes_per_cfg` planes of every
-    launch of the workload; returns (outputs, seconds, description)."""
+    launch of the workload; returns (outputs, seconds, description).  keep: a
+    list that receives (config name, what, oracle result) of every sample, for
+    the parity check of the GPU result on the same sample."""
     import numpy as np
     import oracle
     outs, secs, parts = 0, 0.0, []
@@ -143,11 +190,13 @@ def oracle_sample_run(cfgs, planes_per_cfg: int):
             g = synth.normal_f32(cfg.seed, int(np.prod(pl_sh))).reshape(pl_sh)
             t0 = time.perf_counter()
             if cfg.backward:
-                oracle.adjoint_nd(g, cfg.dims, (cfg.p,) * 2, (cfg.q,) * 2, cfg.mode, cfg.pad, cfg.floor_extent)
+                y = oracle.adjoint_nd(g, cfg.dims, (cfg.p,) * 2, (cfg.q,) * 2, cfg.mode, cfg.pad, cfg.floor_extent)
             else:
                 x = synth.make_values(cfg, 0, n_img)
-                oracle.weight_grad(x, g, cfg.p, cfg.q, cfg.mode, cfg.pad, floor_extent=cfg.floor_extent)
+                y = oracle.weight_grad(x, g, cfg.p, cfg.q, cfg.mode, cfg.pad, floor_extent=cfg.floor_extent)
             secs += time.perf_counter() - t0
+            if keep is not None and cfg.backward:
+                keep.append((cfg.name, ("images", 0, n_img), y))
             outs += g.size
             parts.append(f"{cfg.name}: {'adjoint' if cfg.backward else 'weight gradient'} of "
                          f"{n_img * cfg.C} of {cfg.planes} planes")
@@ -160,6 +209,8 @@ def oracle_sample_run(cfgs, planes_per_cfg: int):
             t0 = time.perf_counter()
             y = oracle.staged(x[0], cfg.p, cfg.q, cfg.mode, cfg.pad, floor_extent=True, rows=Ho_rows, H=cfg.H)
             secs += time.perf_counter() - t0
+            if keep is not None:
+                keep.append((cfg.name, ("rows",) + Ho_rows, y))
             outs += y.size
             parts.append(f"{cfg.name}: output rows {Ho_rows[0]}..{Ho_rows[1]} of 1 plane")
             continue
@@ -170,20 +221,28 @@ def oracle_sample_run(cfgs, planes_per_cfg: int):
         else:
             y = oracle.staged(x, cfg.p, cfg.q, cfg.mode, cfg.pad, floor_extent=cfg.floor_extent, is1d=cfg.is1d)
         secs += time.perf_counter() - t0
+        if keep is not None:
+            keep.append((cfg.name, ("images", 0, n_img), y))
         outs += y.size
         parts.append(f"{cfg.name}: {n_img * cfg.C} of {cfg.planes} planes")
     return outs, secs, "; ".join(parts)
 
 
-def cpu_baseline(cfgs, budget_s=10.0):
+def cpu_baseline(cfgs, budget_s=10.0, gpu_result=None):
     """The oracle as it stands on this host's cores: a sample of the workload
-    grown (then repeated) until it has run about budget_s seconds."""
+    grown (then repeated) until it has run about budget_s seconds.
+
+    gpu_result(config name, what) -> the timed GPU path's output on the same
+    sample (a CPU tensor): the line then also carries the sample's parity
+    against the oracle (BASELINE.json bar; the tests check every output)."""
     cores = os.cpu_count() or 1
     planes = max(1, cores)
-    outs, secs, desc = oracle_sample_run(cfgs, planes)
+    keep = []
+    outs, secs, desc = oracle_sample_run(cfgs, planes, keep)
     while secs < budget_s / 8 and not all(planes >= c.planes for c in cfgs):
         planes *= 4
-        outs, secs, desc = oracle_sample_run(cfgs, planes)
+        keep = []
+        outs, secs, desc = oracle_sample_run(cfgs, planes, keep)
     tot_o, tot_s, reps = outs, secs, 1
     while tot_s < budget_s and reps < 1000:
         o, s, _ = oracle_sample_run(cfgs, planes)
@@ -191,9 +250,59 @@ def cpu_baseline(cfgs, budget_s=10.0):
         tot_s += s
         reps += 1
     threads = 1 if all(c.wgrad for c in cfgs) else cores  # the weight-gradient oracle is single-threaded
-    return {"value": tot_o / tot_s / 1e6, "unit": "Mpix/s", "cores": threads, "kind": "oracle",
-            "sample": f"C oracle (double, {threads} thread{'s' if threads > 1 else ''}) on {desc}, {reps} passes; "
-                      f"{tot_s:.1f} s"}
+    res = {"value": tot_o / tot_s / 1e6, "unit": "Mpix/s", "cores": threads, "kind": "oracle",
+           "sample": f"C oracle (double, {threads} thread{'s' if threads > 1 else ''}) on {desc}, {reps} passes; "
+                     f"{tot_s:.1f} s"}
+    if gpu_result is not None and keep:
+        res["parity"] = [sample_parity(cfg_by_name(cfgs, name), what, ref, gpu_result(name, what))
+                         for name, what, ref in keep]
+    return res
+
+
+def cfg_by_name(cfgs, name):
+    return next(c for c in cfgs if c.name == name)
+
+
+def sample_parity(cfg, what, ref, gpu):
+    """The GPU output of one oracle sample against the BASELINE.json bar:
+    nearest bit-exact, fp32 max abs error <= 1e-5 x input range, 16-bit
+    ordered-ulp distance from the oracle rounded to the dtype (elements > 1 ulp
+    counted; the tests apply reading Z18 to those)."""
+    import numpy as np
+    import torch
+    import oracle
+    gpu, x_range = gpu
+    ref = np.asarray(ref, dtype=np.float64)
+    if what[0] == "images" and gpu.shape[0] < ref.shape[0]:  # a rank's share of the batch holds fewer images
+        ref = ref[:gpu.shape[0]]
+    ref = ref.reshape(tuple(gpu.shape))
+    out = {"config": cfg.name, "sample": list(what), "outputs": int(ref.size)}
+    if cfg.backward:
+        out.update(max_abs_err=float(np.abs(gpu.double().numpy() - ref).max()), max_abs_ref=float(np.abs(ref).max()))
+        return out
+    if cfg.dtype == "float32":
+        r = torch.from_numpy(ref.astype(np.float32))
+    else:
+        r = oracle.round_to(ref, cfg.dtype)
+        r = r if isinstance(r, torch.Tensor) else torch.from_numpy(r)
+    ib = torch.int32 if cfg.dtype == "float32" else torch.int16
+    if cfg.mode == "nearest":
+        n = int((gpu.contiguous().view(ib) != r.contiguous().view(ib)).sum())
+        out.update(bit_mismatches=n, within_bar=n == 0)
+        return out
+    err = float(np.abs(gpu.double().numpy() - ref).max())
+    out["max_abs_err"] = err
+    if cfg.dtype == "float32":
+        tol = 1e-5 * x_range
+        out.update(tol=tol, within_bar=err <= tol)
+        return out
+
+    def ordered(t):
+        b = t.contiguous().view(torch.int16).numpy().astype(np.int32) & 0xFFFF
+        return np.where(b & 0x8000, -(b & 0x7FFF), b & 0x7FFF)
+    d = np.abs(ordered(gpu) - ordered(r))
+    out.update(max_ulp=int(d.max()), over_1ulp=int((d > 1).sum()))
+    return out
 
 
 def run_reference(args):
@@ -262,19 +371,28 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(minutes=10))
     import paper_2203_10670_b200 as fc
 
     cfgs = [synth.CONFIGS[n] for n in synth.WORKLOADS[args.workload]]
-    if args.workload == "C5" and world > 1:
-        from paper_2203_10670_b200 import dist as fdist
-        return fdist.bench_strips(args, cfgs[0], rank, world, dev, METRIC)
+    if args.workload == "C5" and (world > 1 or args.force_strips):
+        return bench_strips(args, cfgs[0], rank, world, dev)
+    # --split batch (N > 1): rank r scales images [r N / G, (r + 1) N / G) of the
+    # config's batch; --split weak: a whole batch of its own
+    split = world > 1 and args.split == "batch"
 
     stream = torch.cuda.Stream(dev)  # every launch of the run goes to this stream (also the graph capture stream)
     props = torch.cuda.get_device_properties(dev)
     l2 = getattr(props, "L2_cache_size", 126 * 2 ** 20) or 126 * 2 ** 20
     launches = []
-    for cfg in cfgs:
+    for gcfg in cfgs:
+        cfg = gcfg
+        img0, img1 = 0, gcfg.N
+        if split:
+            img0, img1 = batch_share(gcfg.N, rank, world)
+            if img1 <= img0:
+                raise SystemExit(f"--split batch: {gcfg.name} has {gcfg.N} images for {world} ranks")
+            cfg = dataclasses.replace(gcfg, N=img1 - img0)
         pl = make_plan(fc, cfg)
         if cfg.backward:  # the adjoint: grad_out (forward output shape) -> grad_in (forward input shape)
             shp = pl.out_shape(cfg.N)
@@ -284,7 +402,8 @@ def main():
             x = torch.from_numpy(synth.normal_f32(cfg.seed + rank, n).reshape(shp)).to(getattr(torch, cfg.dtype))
             oshape = pl.in_shape(cfg.N)
         else:
-            x = synth.make_input(cfg, batch_offset=rank * cfg.N)
+            x = (synth.make_input(gcfg, img0, img1) if split else
+                 synth.make_input(cfg, batch_offset=rank * cfg.N))
             oshape = pl.out_shape(cfg.N)
         n_out = 1
         for d in oshape:
@@ -407,6 +526,11 @@ def main():
     sampler.stop()
 
     outputs_per_step = sum(L["outputs"] for L in launches)
+    total_outputs = outputs_per_step * world  # every rank's outputs of one step (uneven batch shares summed)
+    if world > 1:
+        t = torch.tensor([outputs_per_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        total_outputs = float(t.item())
     # algorithmic bytes of a launch group: every output byte once plus every
     # input row some job of the group reads once (jobs of one launch that scale
     # the same input share its rows: C2a and C2b read the batch once)
@@ -431,7 +555,7 @@ def main():
 
     bytes_per_step = sum(group_bytes(g) for g in groups)
     ms_per_step = elapsed_ms / args.steps
-    value = world * outputs_per_step * args.steps / (elapsed_ms * 1e-3) / 1e6
+    value = total_outputs * args.steps / (elapsed_ms * 1e-3) / 1e6
     peak, peak_kind = peaks()
     dom = max(range(len(groups)), key=lambda gi: per_group_ms[gi])  # dominant kernel launch
     dom_ms = per_group_ms[dom]
@@ -467,11 +591,12 @@ def main():
 
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(launches, args, dev, stream, world, dist, fc=fc, groups=groups)
+        e2e = run_e2e(launches, args, dev, stream, world, dist, fc=fc, groups=groups, total_outputs=total_outputs)
 
     line = {
         "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if split else "weak",
         "vs_baseline": None, "dtype": DTYPE_TAG[cfgs[0].dtype], "data": "synthetic",
         "config": {"workload": args.workload, "launches": [
             {"name": L["cfg"].name, "shape": [L["cfg"].N, L["cfg"].C, *L["cfg"].dims],
@@ -485,7 +610,8 @@ def main():
             for i, L in enumerate(launches)],
             "launch_info": [dict(launches[g[0]]["plan"].launch_info(launches[g[0]]["cfg"].N),
                                  jobs=[launches[i]["cfg"].name for i in g]) for g in groups],
-            "per_rank_batch": "own batch per rank (weak scaling)",
+            "per_rank_batch": (f"rank {rank}: images of the config's batch split {world} ways (strong scaling)"
+                               if split else "own batch per rank (weak scaling)"),
             "l2": f"rotating {R} buffer sets of {set_bytes / 2**20:.0f} MiB (> 4x {l2 / 2**20:.0f} MiB L2); no flush",
             "soak_s": args.soak_s, "parallelism": f"dp{world}",
             "timing": "CUDA graph of K steps replayed once between CUDA events (steady-state launches)"},
@@ -503,11 +629,20 @@ def main():
         "gpu_launches": n_launches,
         "single_launch_cold_l2": cold,
         "clocks": clocks,
+        "provenance": provenance(),
     }
     if e2e is not None:
         line["e2e"] = e2e
     if rank == 0 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfgs)
+        def gpu_result(name, what):
+            L = next(L for L in launches if L["cfg"].name == name)
+            o = L["outs"][0]  # every rotation set holds the same input, so any set's output
+            x = dev_inputs[L["key"]][0]
+            rng = float((x.max() - x.min()).float().item()) if not L["cfg"].wgrad else 1.0
+            if what[0] == "rows":
+                return o[:, :, what[1]:what[2]].cpu(), rng
+            return o[what[1]:min(what[2], o.shape[0])].cpu(), rng
+        line["cpu_baseline"] = cpu_baseline(cfgs, gpu_result=gpu_result)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -515,7 +650,183 @@ def main():
     return 0
 
 
-def run_e2e(launches, args, dev, stream, world, dist, fc=None, groups=None):
+def bench_strips(args, cfg, rank, world, dev):
+    """--workload C5 at N > 1 (or --force-strips): the 32768^2 image in row
+    strips (paper_2203_10670_b200.dist.StripRunner), the halo exchange inside
+    the timed region.  Strong scaling (fixed total image).  The K steps are
+    captured in one CUDA graph (kernels + NCCL send/recv) when every rank's
+    capture succeeds, else timed eagerly (the line says which)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2203_10670_b200 as fc
+    from paper_2203_10670_b200.dist import StripRunner
+
+    pl = make_plan(fc, cfg)
+    esz = {"float32": 4, "float16": 2, "bfloat16": 2}[cfg.dtype]
+    halo = args.halo
+    sr = StripRunner(pl, rank, world, transport=halo)
+    lay = sr.lay
+    x_host = synth.make_input(cfg, rows=(lay.own0, lay.own1))
+    x_own = x_host.to(dev)
+    stream = torch.cuda.Stream(dev)
+    R = 3  # rotating local/output buffers (each >= 4 x 32768 x 4 KB)
+    outs = [sr.alloc_out(1, x_own.dtype, dev) for _ in range(R)]
+    if halo == "peer":  # one symmetric-memory strip per rank; neighbours read it in place
+        sr.setup_peer(1, x_own.dtype, dev).copy_(x_own)
+        locs = [None] * R
+
+        def run(k):
+            sr.run_peer(outs[k % R])
+    else:
+        locs = [sr.alloc_local(1, x_own.dtype, dev) for _ in range(R)]
+        for buf in locs:
+            sr.own_view(buf).copy_(x_own)
+
+        def run(k):
+            sr.run(locs[k % R], outs[k % R])
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(physical_gpu_index(int(os.environ.get("LOCAL_RANK", "0"))))
+    sampler.start()
+    t0 = time.time()
+    k = 0
+    with torch.cuda.stream(stream):
+        while time.time() - t0 < args.soak_s:
+            run(k)
+            k += 1
+            if k % 20 == 0:
+                torch.cuda.synchronize(dev)
+        for w in range(args.warmup):
+            run(w)
+    torch.cuda.synchronize(dev)
+    # one CUDA graph of the K steps (every rank must capture, or none replays)
+    graph, how = None, "eager"
+    n_launch0 = fc.kernel_launches()
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for st in range(args.steps):
+                run(st)
+        graph, how = g, "cuda_graph"
+    except Exception as e:  # noqa: BLE001 -- reported in the line, timed eagerly instead
+        how = f"eager (graph capture failed: {type(e).__name__}: {str(e)[:120]})"
+        torch.cuda.synchronize(dev)
+    n_launches = fc.kernel_launches() - n_launch0
+    if world > 1:
+        ok = torch.tensor([1.0 if graph is not None else 0.0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() < 1.0 and graph is not None:
+            graph, how = None, "eager (another rank's graph capture failed)"
+    if graph is not None:
+        with torch.cuda.stream(stream):
+            graph.replay()  # upload / warm-up
+    else:
+        n_launch0 = fc.kernel_launches()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        if graph is not None:
+            graph.replay()
+        else:
+            for st in range(args.steps):
+                run(st)
+        e1.record(stream)
+    if graph is None:
+        n_launches = fc.kernel_launches() - n_launch0
+    torch.cuda.synchronize(dev)
+    t1 = time.time()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clocks = sampler.summary(t0, t1)
+    sampler.stop()
+    outputs = pl.Ho * pl.Wo
+    total_bytes = pl.compulsory_bytes(1)
+    ms_step = ms / args.steps
+    peak, kind = peaks()
+    # per-rank algorithmic bytes: own output rows + own + halo input rows
+    rank_bytes = ((lay.out1 - lay.out0) * pl.Wo + (lay.loc1 - lay.loc0) * pl.W) * esz
+    achieved = rank_bytes / (ms_step * 1e-3) / 1e9
+
+    # e2e: every step copies this rank's strip in from pinned memory, runs the
+    # strip step (exchange + kernels) and reads its output rows back
+    e2e = None
+    if not args.no_e2e:
+        pin_in = x_host.pin_memory()
+        pin_out = torch.empty(outs[0].shape, dtype=outs[0].dtype).pin_memory()
+        tgt = sr.local if halo == "peer" else sr.own_view(locs[0])
+        steps = max(1, min(args.steps, 20))
+        with torch.cuda.stream(stream):
+            for k in range(2):
+                tgt.copy_(pin_in, non_blocking=True)
+                run(0)
+                pin_out.copy_(outs[0], non_blocking=True)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            f0.record(stream)
+            for k in range(steps):
+                tgt.copy_(pin_in, non_blocking=True)
+                run(0)
+                pin_out.copy_(outs[0], non_blocking=True)
+            f1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": outputs * steps / (ems * 1e-3) / 1e6, "unit": "Mpix/s",
+               "h2d_bytes_per_step": pin_in.numel() * esz, "d2h_bytes_per_step": pin_out.numel() * esz,
+               "steps": steps, "ms_per_step": ems / steps,
+               "path": "per rank: pinned own strip -> HBM -> strip step (halo exchange + fcfs_run_rows) -> "
+                       "pinned own output rows (bytes per rank)"}
+
+    line = {"metric": METRIC, "value": outputs * args.steps / (ms * 1e-3) / 1e6, "unit": "Mpix/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": DTYPE_TAG[cfg.dtype],
+            "data": "synthetic",
+            "config": {"workload": "C5", "shape": [1, 1, cfg.H, cfg.W], "factor": f"{cfg.p}/{cfg.q}",
+                       "mode": cfg.mode, "pad": cfg.pad, "out": [pl.Ho, pl.Wo],
+                       "parallelism": (f"row strips x{world}, NCCL halo send/recv, interior overlapped" if halo == "nccl"
+                                       else f"row strips x{world}, halo rows read in-kernel from the neighbours' "
+                                            "symmetric-memory strips (peer pointers), device barriers per step"),
+                       "rank0_rows": {"own_in": [lay.own0, lay.own1], "out": [lay.out0, lay.out1]},
+                       "l2": "working set per rank > L2; 3 rotating buffer sets",
+                       "timing": how},
+            "achieved_GBps_step": total_bytes / (ms_step * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "peak_source": f"{kind} MEASURED_PEAKS.json hbm_gbs",
+                         "note": "rank-0 bytes (own output rows + own and halo input rows) / max-over-ranks step "
+                                 "time (exchange included)"},
+            "gpu_launches": n_launches, "clocks": clocks, "provenance": provenance()}
+    if e2e is not None:
+        line["e2e"] = e2e
+    if rank == 0 and not args.no_cpu_baseline:
+        def gpu_result(name, what):
+            assert what[0] == "rows" and lay.out0 <= what[1] and what[2] <= lay.out1
+            rng = float((x_own.max() - x_own.min()).item())  # rank 0's rows: the sample reads only those
+            return outs[0][:, :, what[1] - lay.out0:what[2] - lay.out0].cpu(), rng
+        line["cpu_baseline"] = cpu_baseline([cfg], gpu_result=gpu_result)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(launches, args, dev, stream, world, dist, fc=None, groups=None, total_outputs=None):
     """Same metric through the public host-buffer call (fcfs_run_host): every step
     copies its inputs H2D from pinned memory, runs, and reads the outputs D2H.
     Consecutive steps alternate between two streams with their own device and
@@ -529,6 +840,11 @@ def run_e2e(launches, args, dev, stream, world, dist, fc=None, groups=None):
         L["pin_outs"] = [torch.empty(L["outs"][0].shape, dtype=L["outs"][0].dtype).pin_memory() for _ in range(2)]
         L["pin_out"] = L["pin_outs"][0]
     dins = [{k: torch.empty(v.shape, dtype=v.dtype, device=dev) for k, v in pin_in.items()} for _ in range(2)]
+    # device outputs of their own per stream (never shared with the other stream)
+    douts = [[torch.empty(L["outs"][0].shape, dtype=L["outs"][0].dtype, device=dev) for L in launches]
+             for _ in range(2)]
+    for li, L in enumerate(launches):
+        L["e2e_outs"] = [douts[0][li], douts[1][li]]
     pin_g = {L["key"]: L["g_host"].pin_memory() for L in launches if L["cfg"].wgrad}
     gdevs = [{k: torch.empty(v.shape, dtype=v.dtype, device=dev) for k, v in pin_g.items()} for _ in range(2)]
     streams = [stream, torch.cuda.Stream(dev)]
@@ -554,16 +870,16 @@ def run_e2e(launches, args, dev, stream, world, dist, fc=None, groups=None):
                     din[key].copy_(v, non_blocking=True)
                 for grp in groups:
                     if len(grp) > 1:
-                        fc.run_batch([(launches[j]["plan"], din[launches[j]["key"]],
-                                       launches[j]["outs"][i % len(launches[j]["outs"])]) for j in grp], stream=st)
+                        fc.run_batch([(launches[j]["plan"], din[launches[j]["key"]], launches[j]["e2e_outs"][i])
+                                      for j in grp], stream=st)
                     else:
                         L = launches[grp[0]]
-                        L["plan"].run(din[L["key"]], out=L["outs"][i % len(L["outs"])], stream=st)
+                        L["plan"].run(din[L["key"]], out=L["e2e_outs"][i], stream=st)
                 for L in launches:
-                    L["pin_outs"][i].copy_(L["outs"][i % len(L["outs"])], non_blocking=True)
+                    L["pin_outs"][i].copy_(L["e2e_outs"][i], non_blocking=True)
             return
         for L in launches:
-            out_d, out_h = L["outs"][i % len(L["outs"])], L["pin_outs"][i]
+            out_d, out_h = L["e2e_outs"][i], L["pin_outs"][i]
             if L["cfg"].backward:  # public API: copy in, Plan.run_adjoint, copy out (all on the stream)
                 with torch.cuda.stream(st):
                     din[L["key"]].copy_(pin_in[L["key"]], non_blocking=True)
@@ -599,8 +915,8 @@ def run_e2e(launches, args, dev, stream, world, dist, fc=None, groups=None):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    outputs = sum(L["outputs"] for L in launches)
-    return {"value": world * outputs * steps / (ms * 1e-3) / 1e6, "unit": "Mpix/s", "h2d_bytes_per_step": h2d,
+    outputs = total_outputs if total_outputs is not None else world * sum(L["outputs"] for L in launches)
+    return {"value": outputs * steps / (ms * 1e-3) / 1e6, "unit": "Mpix/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps, "ms_per_step": ms / steps,
             "path": ("pinned batch -> HBM once -> every factor's launch (fcfs_run_batch / fcfs_run) -> pinned outputs"
                      if batched else

@@ -28,7 +28,6 @@ with local buffers standing in for the peers.
 from __future__ import annotations
 
 import dataclasses
-import os
 
 
 @dataclasses.dataclass
@@ -191,11 +190,19 @@ class StripRunner:
         return self.local
 
     def run_peer(self, out):
-        """Peer transport: barrier (the neighbours' strips are written and my
-        previous reads of theirs are done), interior rows from my strip (fused
-        kernel), boundary rows from my strip + the neighbours' (one launch)."""
+        """Peer transport: barrier (the neighbours' strips are written), interior
+        rows from my strip (fused kernel), boundary rows from my strip + the
+        neighbours' (one launch), barrier (every neighbour's reads of my strip
+        are done).  The local strip may be refilled once run_peer has returned
+        (stream order): no neighbour reads it any more."""
         lay, pl = self.lay, self.plan
         self.hdl.barrier()
+        self._compute_peer(out)
+        self.hdl.barrier()  # write-after-read: my strip stays untouched until the neighbours have read it
+        return out
+
+    def _compute_peer(self, out):
+        lay, pl = self.lay, self.plan
         if lay.out1 <= lay.out0:
             return out
         i0, i1 = lay.interior
@@ -257,91 +264,3 @@ class StripRunner:
         else:
             tmp = pl.run_rows(local, lay.loc0, m0, m1 - m0)
             dst.copy_(tmp)
-
-
-def bench_strips(args, cfg, rank, world, dev, metric):
-    """bench.py --workload C5 at N > 1: the 32768^2 image in row strips, halo
-    exchange inside the timed region.  Strong scaling (fixed total image)."""
-    import json
-    import time
-
-    import torch
-    import torch.distributed as dist
-
-    import synth
-    import paper_2203_10670_b200 as fc
-    from bench import ClockSampler, DTYPE_TAG, peaks, physical_gpu_index
-
-    pl = fc.Plan(cfg.p, cfg.q, cfg.mode, cfg.pad, cfg.C, cfg.H, cfg.W, cfg.dtype, "floor")
-    halo = getattr(args, "halo", "nccl")
-    sr = StripRunner(pl, rank, world, transport=halo)
-    lay = sr.lay
-    x_own = synth.make_input(cfg, rows=(lay.own0, lay.own1)).to(dev)
-    stream = torch.cuda.current_stream(dev)
-    R = 3  # rotating local/output buffers (each >= 4 x 32768 x 4 KB)
-    outs = [sr.alloc_out(1, x_own.dtype, dev) for _ in range(R)]
-    if halo == "peer":  # one symmetric-memory strip per rank; neighbours read it in place
-        sr.setup_peer(1, x_own.dtype, dev).copy_(x_own)
-        locs = [None] * R
-        sr.run = lambda local, out: sr.run_peer(out)
-    else:
-        locs = [sr.alloc_local(1, x_own.dtype, dev) for _ in range(R)]
-        for l in locs:
-            sr.own_view(l).copy_(x_own)
-    torch.cuda.synchronize(dev)
-    sampler = ClockSampler(physical_gpu_index(int(os.environ.get("LOCAL_RANK", "0"))))
-    sampler.start()
-    t0 = time.time()
-    k = 0
-    while time.time() - t0 < args.soak_s:
-        sr.run(locs[k % R], outs[k % R])
-        k += 1
-        if k % 20 == 0:
-            torch.cuda.synchronize(dev)
-    for w in range(args.warmup):
-        sr.run(locs[w % R], outs[w % R])
-    torch.cuda.synchronize(dev)
-    dist.barrier()
-    torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n_launch0 = fc.kernel_launches()
-    e0.record(stream)
-    for s in range(args.steps):
-        sr.run(locs[s % R], outs[s % R])
-    e1.record(stream)
-    n_launches = fc.kernel_launches() - n_launch0
-    torch.cuda.synchronize(dev)
-    t1 = time.time()
-    dist.barrier()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    clocks = sampler.summary(t0, t1)
-    sampler.stop()
-    outputs = pl.Ho * pl.Wo
-    total_bytes = pl.compulsory_bytes(1)
-    ms_step = ms / args.steps
-    peak, kind = peaks()
-    # per-rank algorithmic bytes: own output rows + own + halo input rows
-    rank_bytes = ((lay.out1 - lay.out0) * pl.Wo + (lay.loc1 - lay.loc0) * pl.W) * 4
-    achieved = rank_bytes / (ms_step * 1e-3) / 1e9
-    line = {"metric": metric, "value": outputs * args.steps / (ms * 1e-3) / 1e6, "unit": "Mpix/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": DTYPE_TAG[cfg.dtype],
-            "data": "synthetic",
-            "config": {"workload": "C5", "shape": [1, 1, cfg.H, cfg.W], "factor": f"{cfg.p}/{cfg.q}",
-                       "mode": cfg.mode, "pad": cfg.pad, "out": [pl.Ho, pl.Wo],
-                       "parallelism": (f"row strips x{world}, NCCL halo send/recv, interior overlapped" if halo == "nccl"
-                                       else f"row strips x{world}, halo rows read in-kernel from the neighbours' "
-                                            "symmetric-memory strips (peer pointers), device barrier per step"),
-                       "l2": "working set per rank > L2; 3 rotating buffer sets"},
-            "achieved_GBps_step": total_bytes / (ms_step * 1e-3) / 1e9,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "note": "per-rank bytes / max-over-ranks step time (exchange included)"},
-            "gpu_launches": n_launches, "clocks": clocks}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    dist.destroy_process_group()
-    return 0

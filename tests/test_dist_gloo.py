@@ -129,3 +129,58 @@ def test_peer_windows_cover_and_reproduce(case):
                 mine = oracle.direct(full[:, :, lo:hi], p, q, mode, pad, floor_extent=True, rows=(m0, m1), H=H,
                                      row0=lo)
                 assert np.array_equal(mine, whole[:, :, m0:m1]), (world, rank, m0, m1)
+
+
+def _batch_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import bench
+        import synth
+        res = {"rank": rank, "ok": True, "msg": "", "shares": {}}
+        for name in ("C2a", "C3", "C4a"):
+            cfg = synth.CONFIGS[name]
+            a, b = bench.batch_share(cfg.N, rank, world)
+            # every rank's images, gathered: they must tile [0, N) exactly once
+            t = torch.tensor([a, b], dtype=torch.int64)
+            allv = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+            dist.all_gather(allv, t)
+            spans = sorted(tuple(int(x) for x in v) for v in allv)
+            if spans[0][0] != 0 or spans[-1][1] != cfg.N or any(s[1] != n[0] for s, n in zip(spans, spans[1:])):
+                res.update(ok=False, msg=f"{name}: spans {spans}")
+            # a rank's slice of the synthetic batch equals the same images of the whole batch
+            if b > a:
+                c1 = synth.Config(name, cfg.N, 1, 8, 8, "float32", cfg.values, cfg.p, cfg.q, cfg.mode, cfg.pad,
+                                  seed=cfg.seed)
+                whole = synth.make_values(c1)
+                if not np.array_equal(synth.make_values(c1, a, b), whole[a:b]):
+                    res.update(ok=False, msg=f"{name}: slice differs")
+            res["shares"][name] = (a, b)
+        out_q.put(res)
+    except Exception as e:  # report, do not hang the peers
+        out_q.put({"rank": rank, "ok": False, "msg": repr(e)})
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_batch_split_partition_gloo(world):
+    """bench.py --split batch: rank r scales images [rN/G, (r+1)N/G)
+    -- the shares cover each config's batch exactly (C2 16, C3 64, C4 8 images)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    results = [q.get(timeout=180) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+    for r in results:
+        assert r["ok"], r
+    if world == 8:  # C4: one image per rank at G = 8 (SURVEY 8(e))
+        assert sorted(r["shares"]["C4a"] for r in results) == [(i, i + 1) for i in range(8)]

@@ -23,7 +23,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 METRICS = [
-    ("gpu__time_duration.sum", "duration (us)"),
+    ("gpu__time_duration.sum", "duration"),
     ("dram__bytes_read.sum", "DRAM read (MB)"),
     ("dram__bytes_write.sum", "DRAM write (MB)"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput (% of peak)"),
@@ -110,7 +110,8 @@ def summarise(rep, out, traffic_key=None, title=None):
         scale = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}
         ru = scale.get(units.get("dram__bytes_read.sum", "byte").lower(), 1)
         wu = scale.get(units.get("dram__bytes_write.sum", "byte").lower(), 1)
-        du = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}.get(units.get("gpu__time_duration.sum", "").lower(), 1e-6)
+        du = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
+              "s": 1.0}[units.get("gpu__time_duration.sum", "").strip().lower()]
         tot = rd * ru + wr * wu
         per_name.setdefault(name, tot)
         traffic = sum(per_name.values())
