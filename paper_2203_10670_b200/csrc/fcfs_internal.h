@@ -99,6 +99,7 @@ struct NearestArgs {     // nearest gather (one output row per warp pass slot)
     FastDiv div_rows, div_do, div_px, div_py, div_pz;
     int px, qx, py, qy, pz, qz, pad, is1d;
     int vec_ok;          // output base 16-B aligned
+    int sm_count;        // the device's SMs (grid sizing)
 };
 
 // Fused separable kernel (bilinear / bicubic), see fused.cuh for the layout.
@@ -157,7 +158,7 @@ struct FusedArgs {
 constexpr int kMaxBatchJobs = 8;
 struct NearestBatch {
     int njobs;
-    uint32_t pass_prefix[kMaxBatchJobs + 1];  // filled by the launcher
+    int64_t pass_prefix[kMaxBatchJobs + 1];   // filled by the launcher (int64: no wrap over many jobs)
     NearestArgs job[kMaxBatchJobs];
 };
 
@@ -169,6 +170,8 @@ int launch_pdl(const void *fn, int grid, int block, void **args, int smem, void 
 int launch_reference(int dtype, const RefArgs &a, void *stream);
 int launch_nearest(int dtype, const NearestArgs &a, void *stream);
 int launch_nearest_batch(int dtype, const NearestBatch &nb, void *stream);
+// the row-staged nearest kernel serves this job (k_nearest.cu)
+bool nearest_rows_job_ok(const RunGeom &g, int is1d, int qx, int qy, int esz);
 int launch_tile(int dtype, const TileArgs &a, int grid, int smem, void *stream);
 // Weight gradient (k_wgrad.cu): grad_w[jy][jx][ty][tx] over the phases' own taps.
 struct WgradArgs {

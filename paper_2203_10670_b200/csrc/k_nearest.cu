@@ -4,29 +4,401 @@
 //     out[m_z][m_y][m_x] = x~[floor(m_z*q_z/p_z)][floor(m_y*q_y/p_y)][floor(m_x*q_x/p_x)]
 // with no arithmetic on the value (bit-exact; -0, NaN and Inf pass through).
 //
-// Layout: a warp handles RPW output rows per pass (grid-stride over the
-// passes of every job of the launch); the lanes sweep the columns, 32
-// consecutive outputs per instruction, so every load instruction reads a short
-// contiguous run of the source row and every store instruction writes 32
-// consecutive outputs (coalesced whatever the row pitch).  All RPW x U loads of
-// a pass are issued before the first store (memory-level parallelism for a
-// latency-bound gather); registers are bounded so that 32+ warps stay resident
-// per SM.  Source columns use a 32-bit multiply-shift division; source rows
-// that no output references are never read.  One launch can carry several
-// jobs (fcfs_run_batch: e.g. the levels of a multi-scale pyramid of one batch).
+// Two kernels:
+//
+// * fcfs_nearest_rows_kernel (2D whole images, 16-B aligned input rows; the
+//   common case, BASELINE config 2).  Input-row centric: a work item is one
+//   input row of one plane.  A producer lane streams every REFERENCED row
+//   (rows no output reads are never loaded) into a ring of shared-memory slots
+//   with one bulk async copy each (TMA engine, mbarrier complete_tx); the
+//   consumer warp that owns the item emits every output row of every job of
+//   the launch that reads this row (the jobs of one launch share the input --
+//   e.g. C2's 2/3 and 3/4 -- so a shared row is loaded once).  Output rows
+//   leave as 16-B vector stores (st.global.v4) with a scalar head/tail for the
+//   row's own alignment; each lane gathers its vector's elements from the
+//   staged row by a multiply-shift column map.
+//
+// * fcfs_nearest_kernel (everything else: 3D, row windows, unaligned rows).  A
+//   warp handles RPW output rows per pass (grid-stride over the passes of
+//   every job of the launch); the lanes sweep the columns, 32 consecutive
+//   outputs per instruction (coalesced whatever the row pitch).  All RPW x U
+//   loads of a pass are issued before the first store.
+#include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "device_common.cuh"
 
 namespace fcfs {
 
+// ---------------------------------------------------------------------------
+// Row-staged gather
+// ---------------------------------------------------------------------------
+struct NearestRowJob {
+    void *out;
+    int32_t Ho, Wo, py, qy, px, qx, pad;
+    FastDiv div_px, div_py, div_qy;
+    int32_t tab_off;  // byte offset of the job's column tables in shared memory
+};
+struct NearestRowsArgs {
+    const void *in;
+    int32_t H, W, row_bytes, slot_pitch, log2Sw, tab_bytes;  // Sw = 1 << log2Sw slots per consumer warp
+    int32_t pf_dist;  // L2 prefetch distance (items), 0: none
+    int32_t nitems;  // planes * H
+    FastDiv div_H;
+    int32_t njobs;
+    NearestRowJob job[kMaxBatchJobs];
+};
+constexpr int kRowsConsumerWarps = 15;
+constexpr int kRowsThreads = 32 * (1 + kRowsConsumerWarps);
+constexpr int kRowsSlotsMax = 64;  // consumer warps x slots per warp
+constexpr int kRowsHdr = 2048;    // shared-memory header: full[64], empty[64] mbarriers, item[64]
+
+// output rows [m0, m1) of a job whose source row is r (rows whose source lies
+// past the last input row -- padding -- belong to r = H - 1)
+__device__ __forceinline__ void job_rows(int H, const NearestRowJob &jb, int r, int &m0, int &m1) {
+    // ceil(r py / qy) .. ceil((r + 1) py / qy); (H + 1) * 64 < 2^31 (host check)
+    m0 = (int)fdiv((uint32_t)(r * jb.py + jb.qy - 1), jb.div_qy);
+    m1 = r == H - 1 ? jb.Ho : min(jb.Ho, (int)fdiv((uint32_t)((r + 1) * jb.py + jb.qy - 1), jb.div_qy));
+}
+__device__ __forceinline__ bool referenced(const NearestRowsArgs &a, int r) {
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < kMaxBatchJobs; ++j) {
+        if (j < a.njobs) {
+            int m0, m1;
+            job_rows(a.H, a.job[j], r, m0, m1);
+            any |= m0 < m1;
+        }
+    }
+    return any;
+}
+
+// entries per head shift of a job's column table (16-B multiple: vector loads)
+__host__ __device__ constexpr int tab_n(int Wo, int V) { return (Wo + V + 7) / 8 * 8; }
+
+// Column tables (built once per CTA): for every job and every head shift h in
+// [0, V) (V = elements per 16 B; an output row whose first 16-B boundary is h
+// elements in), entry i holds the byte offset inside a staged row of the
+// source element of output column h + i (§4.2 per-dimension factor p_x/q_x,
+// floor rule; the padding mode applied; a zero-padding column points at the
+// zero element kept just past every staged row).  Vector v of such a row then
+// reads its V offsets with one shared load.
+template <typename T>
+__device__ __forceinline__ void build_tables(const NearestRowsArgs &a, unsigned char *smem, int tid, int nthr) {
+    constexpr int V = 16 / sizeof(T);
+#pragma unroll 1
+    for (int j = 0; j < a.njobs; ++j) {
+        const NearestRowJob &jb = a.job[j];
+        const int n = tab_n(jb.Wo, V);  // entries per head shift
+        uint16_t *tab = reinterpret_cast<uint16_t *>(smem + jb.tab_off);
+        for (int e = tid; e < V * n; e += nthr) {
+            const int h = e / n, c = h + (e - h * n);
+            int off = a.row_bytes;  // the zero element
+            if (c < jb.Wo) {
+                const uint32_t nn = (uint32_t)c * (uint32_t)jb.qx;
+                int sc = (int)fdiv(nn, jb.div_px);
+                if (sc >= a.W) sc = pad_src32(sc, a.W, jb.pad);
+                if (sc >= 0) off = sc * (int)sizeof(T);
+            }
+            tab[e] = (uint16_t)off;
+        }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t lds_el(const unsigned char *row, uint32_t off) {
+    if constexpr (sizeof(T) == 4) return *reinterpret_cast<const uint32_t *>(row + off);
+    else return *reinterpret_cast<const uint16_t *>(row + off);
+}
+
+// Output row `orow` (Wo elements) from the staged row `srow` through the job's tables.
+template <typename T>
+__device__ __forceinline__ void emit_row_tab(const unsigned char *srow, const uint16_t *tabs, int Wo, T *orow,
+                                             int lane) {
+    constexpr int V = 16 / sizeof(T);
+    const int n = tab_n(Wo, V);
+    const int h = min(Wo, (int)(((16u - (uint32_t)(reinterpret_cast<uintptr_t>(orow) & 15u)) & 15u) / sizeof(T)));
+    const int nvec = (Wo - h) / V;
+    const int tail0 = h + nvec * V;
+    const uint16_t *t0 = tabs;              // head shift 0: column c at entry c
+    const uint16_t *th = tabs + (h % V) * n;  // this row's head shift
+    if (lane < h) {
+        const uint32_t v = lds_el<T>(srow, t0[lane]);
+        if constexpr (sizeof(T) == 4) reinterpret_cast<uint32_t *>(orow)[lane] = v;
+        else reinterpret_cast<uint16_t *>(orow)[lane] = (uint16_t)v;
+    }
+    if (lane < Wo - tail0) {
+        const uint32_t v = lds_el<T>(srow, t0[tail0 + lane]);
+        if constexpr (sizeof(T) == 4) reinterpret_cast<uint32_t *>(orow)[tail0 + lane] = v;
+        else reinterpret_cast<uint16_t *>(orow)[tail0 + lane] = (uint16_t)v;
+    }
+    uint4 *vout = reinterpret_cast<uint4 *>(orow + h);
+#pragma unroll 4
+    for (int v = lane; v < nvec; v += 32) {
+        uint32_t w[4];
+        if constexpr (sizeof(T) == 4) {
+            const uint2 o = *reinterpret_cast<const uint2 *>(th + 4 * v);
+            w[0] = lds_el<T>(srow, o.x & 0xffffu);
+            w[1] = lds_el<T>(srow, o.x >> 16);
+            w[2] = lds_el<T>(srow, o.y & 0xffffu);
+            w[3] = lds_el<T>(srow, o.y >> 16);
+        } else {
+            const uint4 o = *reinterpret_cast<const uint4 *>(th + 8 * v);
+            const uint32_t oo[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                w[e] = __byte_perm(lds_el<T>(srow, oo[e] & 0xffffu), lds_el<T>(srow, oo[e] >> 16), 0x5410);
+        }
+        vout[v] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+// A row that is none of the staged ones (reflect padding past the last row):
+// element by element from global memory (rare; or zeros).
+template <typename T>
+__device__ __forceinline__ void emit_row_global(const NearestRowsArgs &a, const NearestRowJob &jb, const T *src,
+                                                bool zero, T *orow, int lane) {
+    for (int c = lane; c < jb.Wo; c += 32) {
+        int sc = (int)fdiv((uint32_t)c * (uint32_t)jb.qx, jb.div_px);
+        if (sc >= a.W) sc = pad_src32(sc, a.W, jb.pad);
+        orow[c] = (zero || sc < 0) ? DT<T>::from_f(0.0f) : src[sc];
+    }
+}
+
+// Slot of the CTA's k-th staged row: consumer warp k mod CW owns it, in that
+// warp's own ring of Sw slots (use u = k div CW).  Every slot has exactly one
+// consumer that waits on its uses in order, so no waiter can ever be two
+// mbarrier phases ahead of the slot.
+struct RowSlot {
+    int slot;
+    uint32_t use;  // the slot's use index (parity = (use >> log2Sw) & 1 of the per-slot sequence)
+};
+__device__ __forceinline__ RowSlot row_slot(uint32_t k, int log2Sw) {
+    const uint32_t w = k % kRowsConsumerWarps, u = k / kRowsConsumerWarps;
+    RowSlot r;
+    r.slot = (int)(w << log2Sw) + (int)(u & ((1u << log2Sw) - 1u));
+    r.use = u >> log2Sw;
+    return r;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRowsThreads, 2) fcfs_nearest_rows_kernel(const __grid_constant__ NearestRowsArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);  // slot landed (or holds an end marker)
+    uint64_t *empty = full + kRowsSlotsMax;               // slot consumed
+    int32_t *item = reinterpret_cast<int32_t *>(empty + kRowsSlotsMax);  // the slot's item (-1: end of the CTA's items)
+    unsigned char *ring = smem + kRowsHdr + a.tab_bytes;
+    const int Sw = 1 << a.log2Sw;
+    const int nslots = kRowsConsumerWarps * Sw;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nslots; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_fence_init();
+    }
+    if (warp > 0) {  // consumers: column tables and the zero elements (parameters only: before the grid dependency)
+        const int ctid = threadIdx.x - 32;
+        build_tables<T>(a, smem + kRowsHdr, ctid, 32 * kRowsConsumerWarps);
+        for (int s = ctid; s < nslots; s += 32 * kRowsConsumerWarps)  // the zero element past every staged row
+            *reinterpret_cast<uint4 *>(ring + s * a.slot_pitch + a.row_bytes) = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+    pdl_wait();
+    if (warp == 0) {
+        // ---------------------------------------------- producer (one warp):
+        // the CTA's items are a contiguous range (DRAM page locality); the lanes
+        // take B items at a time, the referenced rows go to the next slots in
+        // item order (one bulk copy per lane), then one end marker per consumer
+        // warp.  B <= slots: a lane's slot was last used by an item of an
+        // earlier batch (no lane waits on a slot another lane of its batch fills).
+        const uint64_t pol = policy_evict_first();
+        const int it0 = (int)((int64_t)blockIdx.x * a.nitems / gridDim.x);
+        const int it1 = (int)((int64_t)(blockIdx.x + 1) * a.nitems / gridDim.x);
+        const int B = min(32, nslots);
+        uint32_t k0 = 0;  // rows staged so far
+        for (int base = it0; base < it1 + kRowsConsumerWarps; base += B) {
+            const int it = base + lane;
+            bool use = false, end = false;
+            if (lane >= B) {
+            } else if (it < it1) {
+                const int plane = (int)fdiv((uint32_t)it, a.div_H);
+                use = referenced(a, it - plane * a.H);
+            } else {
+                end = it - it1 < kRowsConsumerWarps;  // the end markers follow the last item
+            }
+            const uint32_t mask = __ballot_sync(0xffffffffu, use || end);
+            if (a.pf_dist > 0 && lane < B) {  // L2 prefetch of a referenced row pf_dist items ahead
+                const int ip = it + a.pf_dist;
+                if (ip < it1) {
+                    const int pp = (int)fdiv((uint32_t)ip, a.div_H);
+                    if (referenced(a, ip - pp * a.H))
+                        prefetch_l2(static_cast<const unsigned char *>(a.in) + (int64_t)ip * a.row_bytes, a.row_bytes);
+                }
+            }
+            if (use || end) {
+                const uint32_t k = k0 + __popc(mask & ((1u << lane) - 1u));
+                const RowSlot rs = row_slot(k, a.log2Sw);
+                if (rs.use > 0) mbar_wait(&empty[rs.slot], (rs.use - 1) & 1u);
+                item[rs.slot] = use ? it : -1;
+                if (use) {
+                    mbar_arrive_expect_tx(&full[rs.slot], (uint32_t)a.row_bytes);
+                    bulk_g2s(ring + rs.slot * a.slot_pitch,
+                             static_cast<const unsigned char *>(a.in) + (int64_t)it * a.row_bytes,
+                             (uint32_t)a.row_bytes, &full[rs.slot], pol);
+                } else {
+                    mbar_arrive(&full[rs.slot]);
+                }
+            }
+            k0 += __popc(mask);
+        }
+        pdl_launch_dependents();
+        return;
+    }
+    // ---------------------------------------------------- consumers
+    // warp cw takes the CTA's rows k = cw, cw + CW, ... (its own ring)
+    const int cw = warp - 1;
+    for (uint32_t k = (uint32_t)cw;; k += kRowsConsumerWarps) {
+        const RowSlot rs = row_slot(k, a.log2Sw);
+        const int slot = rs.slot;
+        mbar_wait(&full[slot], rs.use & 1u);
+        const int it = item[slot];
+        if (it < 0) break;
+        const int plane = (int)fdiv((uint32_t)it, a.div_H), r = it - plane * a.H;
+        const unsigned char *srow = ring + slot * a.slot_pitch;
+#pragma unroll
+        for (int j = 0; j < kMaxBatchJobs; ++j) {
+            if (j >= a.njobs) break;
+            const NearestRowJob &jb = a.job[j];
+            int m0, m1;
+            job_rows(a.H, jb, r, m0, m1);
+            const int Wo = jb.Wo;
+            const uint16_t *tabs = reinterpret_cast<const uint16_t *>(smem + kRowsHdr + jb.tab_off);
+            T *obase = static_cast<T *>(jb.out) + (int64_t)plane * jb.Ho * Wo;
+            for (int m = m0; m < m1; ++m) {
+                T *orow = obase + (int64_t)m * Wo;
+                const int sr = (int)fdiv((uint32_t)(m * jb.qy), jb.div_py);
+                const int sp = sr <= r ? r : pad_src32(sr, a.H, jb.pad);  // past the last row: the padding source
+                if (sp == r)
+                    emit_row_tab<T>(srow, tabs, Wo, orow, lane);
+                else
+                    emit_row_global<T>(a, jb, static_cast<const T *>(a.in) + ((int64_t)plane * a.H + max(sp, 0)) * a.W,
+                                       sp < 0, orow, lane);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+    pdl_launch_dependents();
+}
+
+// One job the row kernel serves: a 2D whole image (or 1D rows), 16-B aligned
+// input rows of at most 32 KB, 32-bit index ranges.
+bool nearest_rows_job_ok(const RunGeom &g, int is1d, int qx, int qy, int esz) {
+    (void)is1d;
+    (void)qy;
+    if (g.D != 1 || g.Do != 1 || g.in_row0 != 0 || g.in_nrows != g.H || g.out_row0 != 0 || g.out_nrows != g.Ho)
+        return false;
+    if ((int64_t)g.Wo * qx >= INT32_MAX || (int64_t)(g.Ho + 1) * 64 >= INT32_MAX || (g.H + 1) * 64 >= INT32_MAX)
+        return false;  // 32-bit multiply-shift index math (p, q <= 64)
+    if ((reinterpret_cast<uintptr_t>(g.out) % esz) != 0) return false;
+    const int64_t row_bytes = g.W * esz;
+    if ((reinterpret_cast<uintptr_t>(g.in) & 15) || (row_bytes & 15) || row_bytes > 12 * 1024) return false;
+    if (g.planes * g.H >= INT32_MAX || g.Wo < 1) return false;
+    if ((int64_t)(16 / esz) * (g.Wo + 16 / esz + 8) * 2 > 40 * 1024) return false;  // column tables
+    return true;
+}
+
+// The row kernel serves a batch whose jobs all qualify, share one input and
+// whose column tables fit together.
+static bool rows_ok(const NearestBatch &nb, int esz) {
+    const RunGeom &g0 = nb.job[0].g;
+    int64_t tab = 0;
+    for (int j = 0; j < nb.njobs; ++j) {
+        const NearestArgs &a = nb.job[j];
+        const RunGeom &g = a.g;
+        if (g.in != g0.in || g.planes != g0.planes || g.H != g0.H || g.W != g0.W) return false;
+        if (!nearest_rows_job_ok(g, a.is1d, a.qx, a.qy, esz)) return false;
+        tab += (int64_t)(16 / esz) * tab_n((int)g.Wo, 16 / esz) * 2;
+    }
+    const int64_t pitch = (g0.W * esz + 16 + 127) / 128 * 128;
+    return tab <= 48 * 1024 && kRowsHdr + (tab + 127) / 128 * 128 + kRowsConsumerWarps * pitch <= 200 * 1024;
+}
+
+template <typename T>
+static int launch_nearest_rows(const NearestBatch &nb, cudaStream_t s) {
+    constexpr int V = 16 / sizeof(T);
+    const RunGeom &g0 = nb.job[0].g;
+    NearestRowsArgs a;
+    a.in = g0.in;
+    a.H = (int32_t)g0.H;
+    a.W = (int32_t)g0.W;
+    a.row_bytes = (int32_t)(g0.W * sizeof(T));
+    a.slot_pitch = (a.row_bytes + 16 + 127) / 128 * 128;  // + the zero element
+    a.nitems = (int32_t)(g0.planes * g0.H);
+    a.div_H = make_fastdiv((uint32_t)g0.H);
+    a.njobs = nb.njobs;
+    int tab = 0;
+    for (int j = 0; j < nb.njobs; ++j) {
+        const NearestArgs &na = nb.job[j];
+        NearestRowJob &jb = a.job[j];
+        jb.out = na.g.out;
+        jb.Ho = (int32_t)na.g.Ho;
+        jb.Wo = (int32_t)na.g.Wo;
+        jb.py = na.is1d ? 1 : na.py;
+        jb.qy = na.is1d ? 1 : na.qy;
+        jb.px = na.px;
+        jb.qx = na.qx;
+        jb.pad = na.pad;
+        jb.div_px = make_fastdiv((uint32_t)na.px);
+        jb.div_py = make_fastdiv((uint32_t)jb.py);
+        jb.div_qy = make_fastdiv((uint32_t)jb.qy);
+        jb.tab_off = tab;
+        tab += V * tab_n(jb.Wo, V) * 2;
+    }
+    a.tab_bytes = (tab + 127) / 128 * 128;
+    // rings: a power of two of slots per consumer warp (<= 4: 60 slots) in
+    // ~100 KB with the tables (two CTAs per SM), else ~200 KB (one)
+    int ctas = 1;
+    if (const char *e = std::getenv("FCFS_DEBUG_NEAREST_CTAS")) ctas = std::max(1, std::min(2, std::atoi(e)));
+    const int budget = (ctas == 2 ? 100 : 200) * 1024;
+    int log2Sw = 2;
+    while (log2Sw > 0 && kRowsHdr + a.tab_bytes + kRowsConsumerWarps * (1 << log2Sw) * a.slot_pitch > budget)
+        --log2Sw;
+    if (kRowsHdr + a.tab_bytes + kRowsConsumerWarps * a.slot_pitch > budget) ctas = 1;
+    if (const char *e = std::getenv("FCFS_DEBUG_NEAREST_LOG2SW")) log2Sw = std::max(0, std::min(log2Sw, std::atoi(e)));
+    a.log2Sw = log2Sw;
+    a.pf_dist = kRowsConsumerWarps << log2Sw;  // one ring ahead
+    if (const char *e = std::getenv("FCFS_DEBUG_NEAREST_PF")) a.pf_dist = std::atoi(e);
+    const int smem = kRowsHdr + a.tab_bytes + kRowsConsumerWarps * (1 << log2Sw) * a.slot_pitch;
+    const int sms = nb.job[0].sm_count > 0 ? nb.job[0].sm_count : 148;
+    int grid = (int)std::min<int64_t>(a.nitems, (int64_t)sms * ctas);
+    if (const char *e = std::getenv("FCFS_DEBUG_NEAREST_GRID")) grid = std::max(1, std::min(grid, std::atoi(e)));
+    if (grid <= 0) return 0;
+    const void *fn = reinterpret_cast<const void *>(&fcfs_nearest_rows_kernel<T>);
+    static bool configured[3] = {false, false, false};
+    const int di = sizeof(T) == 4 ? 0 : (std::is_same<T, __half>::value ? 1 : 2);
+    if (!configured[di]) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+        if (e != cudaSuccess) return (int)e;
+        configured[di] = true;
+    }
+    void *args[] = {&a};
+    return launch_pdl(fn, grid, kRowsThreads, args, smem, s);
+}
+
+// ---------------------------------------------------------------------------
+// General gather
+// ---------------------------------------------------------------------------
 template <typename T, int U, int RPW, int MINB>
 __global__ void __launch_bounds__(256, MINB) fcfs_nearest_kernel(const __grid_constant__ NearestBatch nb) {
     pdl_wait();
     const int lane = threadIdx.x & 31;
-    const uint32_t warp0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t gp = warp0; gp < nb.pass_prefix[nb.njobs]; gp += nwarps) {
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t gp = warp0; gp < nb.pass_prefix[nb.njobs]; gp += nwarps) {
         int j = 0;
         while (j + 1 < nb.njobs && gp >= nb.pass_prefix[j + 1]) ++j;
         const NearestArgs &a = nb.job[j];
@@ -36,7 +408,7 @@ __global__ void __launch_bounds__(256, MINB) fcfs_nearest_kernel(const __grid_co
         const uint32_t qx = (uint32_t)a.qx;
         const T *__restrict__ in = static_cast<const T *>(g.in);
         T *__restrict__ out = static_cast<T *>(g.out);
-        const uint32_t rw0 = (gp - nb.pass_prefix[j]) * RPW;
+        const uint32_t rw0 = (uint32_t)(gp - nb.pass_prefix[j]) * RPW;
         const T *irow[RPW];
         T *orow[RPW];
         bool rd[RPW], wr[RPW];  // row reads its source / row exists
@@ -84,44 +456,67 @@ __global__ void __launch_bounds__(256, MINB) fcfs_nearest_kernel(const __grid_co
 }
 
 template <typename T, int U, int RPW, int MINB>
-static void launch_nearest_v(NearestBatch nb, cudaStream_t s) {
+static int launch_nearest_v(NearestBatch nb, cudaStream_t s) {
     nb.pass_prefix[0] = 0;
     for (int j = 0; j < nb.njobs; ++j) {
         const int64_t rows = nb.job[j].g.planes * nb.job[j].g.Do * nb.job[j].g.out_nrows;
-        nb.pass_prefix[j + 1] = nb.pass_prefix[j] + (uint32_t)((rows + RPW - 1) / RPW);
+        nb.pass_prefix[j + 1] = nb.pass_prefix[j] + (rows + RPW - 1) / RPW;
     }
-    int64_t blocks = ((int64_t)nb.pass_prefix[nb.njobs] + 7) / 8;  // 8 warps per block
-    if (blocks > 148 * MINB) blocks = 148 * MINB;                    // one resident wave, warps loop
-    if (blocks > 0) {
-        void *args[] = {&nb};
-        launch_pdl(reinterpret_cast<const void *>(&fcfs_nearest_kernel<T, U, RPW, MINB>), (int)blocks, 256, args, 0, s);
-    }
+    const int sms = nb.job[0].sm_count > 0 ? nb.job[0].sm_count : 148;
+    int64_t blocks = (nb.pass_prefix[nb.njobs] + 7) / 8;  // 8 warps per block
+    if (blocks > (int64_t)sms * MINB) blocks = (int64_t)sms * MINB;  // one resident wave, warps loop
+    if (blocks <= 0) return 0;
+    void *args[] = {&nb};
+    return launch_pdl(reinterpret_cast<const void *>(&fcfs_nearest_kernel<T, U, RPW, MINB>), (int)blocks, 256, args,
+                      0, s);
 }
 
 // Variants (U columns per lane per pass, RPW rows per pass, CTAs per SM);
 // FCFS_DEBUG_NEAREST selects one for tuning sweeps.
 template <typename T>
-static void launch_nearest_t(const NearestBatch &nb, cudaStream_t s) {
+static int launch_nearest_t(const NearestBatch &nb, cudaStream_t s) {
     const char *e = std::getenv("FCFS_DEBUG_NEAREST");
     switch (e ? std::atoi(e) : 0) {
-    case 1: launch_nearest_v<T, 8, 2, 4>(nb, s); break;
-    case 2: launch_nearest_v<T, 8, 4, 4>(nb, s); break;
-    case 3: launch_nearest_v<T, 16, 1, 4>(nb, s); break;
-    case 4: launch_nearest_v<T, 12, 2, 4>(nb, s); break;
-    case 5: launch_nearest_v<T, 12, 4, 2>(nb, s); break;
-    default: launch_nearest_v<T, 12, 2, 3>(nb, s); break;  // 3 CTAs/SM: C2 -4% vs 4 (tools/nearest_ab.py)
+    case 1: return launch_nearest_v<T, 8, 2, 4>(nb, s);
+    case 2: return launch_nearest_v<T, 8, 4, 4>(nb, s);
+    case 3: return launch_nearest_v<T, 16, 1, 4>(nb, s);
+    case 4: return launch_nearest_v<T, 12, 2, 4>(nb, s);
+    case 5: return launch_nearest_v<T, 12, 4, 2>(nb, s);
+    default: return launch_nearest_v<T, 12, 2, 3>(nb, s);  // 3 CTAs/SM: C2 -4% vs 4 (tools/nearest_ab.py)
     }
+}
+
+template <typename T>
+static int launch_batch_t(const NearestBatch &nb, cudaStream_t s) {
+    if (!std::getenv("FCFS_NO_NEAREST_ROWS") && rows_ok(nb, (int)sizeof(T))) return launch_nearest_rows<T>(nb, s);
+    // general kernel: jobs in launches whose pass counts stay below 2^31
+    NearestBatch cur;
+    cur.njobs = 0;
+    int64_t passes = 0;
+    for (int j = 0; j < nb.njobs; ++j) {
+        const int64_t p = (nb.job[j].g.planes * nb.job[j].g.Do * nb.job[j].g.out_nrows + 1) / 2;
+        if (cur.njobs > 0 && passes + p >= INT32_MAX) {
+            int rc = launch_nearest_t<T>(cur, s);
+            if (rc) return rc;
+            cur.njobs = 0;
+            passes = 0;
+        }
+        cur.job[cur.njobs++] = nb.job[j];
+        passes += p;
+    }
+    return cur.njobs ? launch_nearest_t<T>(cur, s) : 0;
 }
 
 int launch_nearest_batch(int dtype, const NearestBatch &nb, void *stream) {
     if (nb.njobs <= 0) return 0;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int rc;
     switch (dtype) {
-    case FCFS_F32: launch_nearest_t<float>(nb, s); break;
-    case FCFS_F16: launch_nearest_t<__half>(nb, s); break;
-    default: launch_nearest_t<__nv_bfloat16>(nb, s); break;
+    case FCFS_F32: rc = launch_batch_t<float>(nb, s); break;
+    case FCFS_F16: rc = launch_batch_t<__half>(nb, s); break;
+    default: rc = launch_batch_t<__nv_bfloat16>(nb, s); break;
     }
-    return (int)cudaGetLastError();
+    return rc ? rc : (int)cudaGetLastError();
 }
 
 int launch_nearest(int dtype, const NearestArgs &a, void *stream) {

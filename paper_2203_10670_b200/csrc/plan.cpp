@@ -437,10 +437,21 @@ int select_kernel(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     }
     if (kernel == 1) {
         const int64_t rows = g.planes * g.Do * g.out_nrows;
-        std::snprintf(L.desc, sizeof(L.desc),
-                      "{\"kernel\": \"nearest_gather\", \"rows\": %lld, \"grid\": %lld, \"block\": 256, "
-                      "\"rows_per_warp_pass\": 2, \"columns_per_lane_pass\": 12}",
-                      (long long)rows, (long long)std::min<int64_t>(((rows + 1) / 2 + 7) / 8, (int64_t)pl->sm_count * 3));
+        RunGeom gr = g;
+        if (!gr.in) gr.in = reinterpret_cast<const void *>(static_cast<uintptr_t>(256));  // launch_info: aligned
+        if (!gr.out) gr.out = reinterpret_cast<void *>(static_cast<uintptr_t>(256));
+        if (!std::getenv("FCFS_NO_NEAREST_ROWS") &&
+            nearest_rows_job_ok(gr, pl->is1d, pl->q, pl->qy, esize(pl->dtype)))
+            std::snprintf(L.desc, sizeof(L.desc),
+                          "{\"kernel\": \"nearest_gather\", \"variant\": \"rows_staged\", \"items\": %lld, "
+                          "\"grid\": %lld, \"block\": %d, \"consumer_warps\": 15}",
+                          (long long)(g.planes * g.H), (long long)std::min<int64_t>(g.planes * g.H, (int64_t)pl->sm_count),
+                          512);
+        else
+            std::snprintf(L.desc, sizeof(L.desc),
+                          "{\"kernel\": \"nearest_gather\", \"variant\": \"general\", \"rows\": %lld, "
+                          "\"grid\": %lld, \"block\": 256, \"rows_per_warp_pass\": 2, \"columns_per_lane_pass\": 12}",
+                          (long long)rows, (long long)std::min<int64_t>(((rows + 1) / 2 + 7) / 8, (int64_t)pl->sm_count * 3));
     } else if (kernel == 0) {
         const int64_t total = g.planes * g.Do * g.out_nrows * pl->Wo;
         std::snprintf(L.desc, sizeof(L.desc), "{\"kernel\": \"reference\", \"grid\": %lld, \"block\": 256}",
@@ -608,6 +619,7 @@ fcfs_status prepare(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t in_
         a.pad = pl->pad;
         a.is1d = pl->is1d;
         a.vec_ok = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+        a.sm_count = pl->sm_count;
     } else if (pr.kernel == 3) {
         plan_tile(pl, g, pr.ta, pr.tgrid, pr.tsmem, nullptr, 0);
     } else if (pr.kernel == 0) {
@@ -1400,6 +1412,10 @@ fcfs_status fcfs_launch_info(fcfs_plan_t pl, int64_t N, int64_t out_row0, int64_
     g.Wo = pl->Wo;
     g.in_row0 = n0;
     g.in_nrows = std::max<int64_t>(1, n1 - n0);
+    if (out_row0 == 0 && out_nrows == pl->Ho) {  // a whole-image run (fcfs_run) holds every input row
+        g.in_row0 = 0;
+        g.in_nrows = pl->H;
+    }
     g.out_row0 = out_row0;
     g.out_nrows = out_nrows;
     g.in_plane_stride = pl->D * g.in_nrows * pl->W;

@@ -77,7 +77,7 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and getattr(_lib, "lib", None) is not None:  # (not at interpreter shutdown)
             _lib.lib.fcfs_destroy(h)
             self._h = None
 

@@ -30,7 +30,11 @@ def fp32_error_bound(mode: str, x_absmax: float) -> float:
     return 2.0 ** -20 * WSUM[mode] ** 2 * x_absmax
 
 
-RELAXED_MAX_FRAC = 1e-3  # relaxed (reading Z18) elements allowed per comparison, as a fraction of its outputs
+# relaxed (reading Z18) elements allowed per comparison: a fraction of its
+# outputs, at least a few (small N(0,1) arrays: ~1e-3 of the values lie in the
+# band where fp32 cannot resolve a bf16 ulp)
+RELAXED_MAX_FRAC = 1e-3
+RELAXED_MIN_CAP = 4
 
 
 def compare(gpu: torch.Tensor, ref64: np.ndarray, dtype: str, mode: str, x_range: float, what: str = "",
@@ -87,7 +91,7 @@ def compare(gpu: torch.Tensor, ref64: np.ndarray, dtype: str, mode: str, x_range
         report.append((what, n_relaxed, int(d.size)))
     if n_relaxed:
         print(f"[Z18] {what}: {n_relaxed} of {d.size} elements relaxed")
-    assert n_relaxed <= RELAXED_MAX_FRAC * max(d.size, 1), f"{what}: {n_relaxed} relaxed elements of {d.size}"
+    assert n_relaxed <= max(RELAXED_MIN_CAP, RELAXED_MAX_FRAC * d.size), f"{what}: {n_relaxed} relaxed of {d.size}"
     return n_relaxed
 
 

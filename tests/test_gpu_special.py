@@ -9,7 +9,7 @@ out[my][mx] = x~[floor(my q / p)][floor(mx q / p)] with x~ the padded input
 NaNs with payloads, subnormals and the largest finite values; every output's
 bits must equal the gather's.  The fraction-0 outputs of bilinear/bicubic
 (output rows and columns that are multiples of p) are exact copies too
-(reading Z11): their bits are checked the same way (fp16 NaN payloads
+(reading Z11): their bits are checked the same way (16-bit NaN payloads
 excepted: that copy passes through fp32 registers).
 """
 import itertools
@@ -81,18 +81,21 @@ def gather(bits, dims, odims, factors, pad):
 
 
 @pytest.mark.parametrize("dtype", ["float32", "float16", "bfloat16"])
-def test_nearest_special_values_bit_exact(dtype):
+@pytest.mark.parametrize("W", [45, 48])
+def test_nearest_special_values_bit_exact(dtype, W):
+    """W = 48: 16-B rows (the row-staged kernel); W = 45: the general kernel."""
     ut = SPECIALS[dtype][0]
     n = 0
     for (p, q), pad, ext in itertools.product([(2, 3), (3, 4), (3, 2), (5, 3), (1, 1), (2, 1), (27, 11), (1, 4)],
                                               ["zero", "replicate", "reflect"], ["paper", "floor"]):
         n += 1
-        x = special_input(100 + n, (2, 3, 29, 45), dtype)
-        pl = Plan(p, q, "nearest", pad, 3, 29, 45, dtype, ext)
+        x = special_input(100 + n, (2, 3, 29, W), dtype)
+        pl = Plan(p, q, "nearest", pad, 3, 29, W, dtype, ext)
         assert pl.kernel == "nearest_gather"
+        assert pl.launch_info(2)["variant"] == ("rows_staged" if W == 48 else "general")
         y = pl.run(x.to(DEV))
         got = y.cpu().view(TORCH_INT[dtype]).numpy().view(ut)
-        exp = gather(x.view(TORCH_INT[dtype]).numpy().view(ut), (29, 45), (pl.Ho, pl.Wo), [(pl.p, pl.q)] * 2, pad)
+        exp = gather(x.view(TORCH_INT[dtype]).numpy().view(ut), (29, W), (pl.Ho, pl.Wo), [(pl.p, pl.q)] * 2, pad)
         assert np.array_equal(got, exp), f"{p}/{q} {pad} {ext} {dtype}: {int((got != exp).sum())} outputs differ"
 
 
@@ -125,13 +128,38 @@ def test_fraction0_outputs_are_exact_copies(mode):
         exp = gather(x.view(TORCH_INT[dtype]).numpy().view(ut), (40, 72), (pl.Ho, pl.Wo), [(p, q)] * 2, "replicate")
         sel = (slice(None), slice(None), slice(0, None, p), slice(0, None, p))
         g, e = got[sel], exp[sel]
-        if dtype == "float16":
-            # the copy goes through fp32 registers (cvt.f32.f16 / cvt.rn.f16.f32):
-            # every value and sign survives, a NaN stays a NaN but its payload may
-            # not (Z11); bf16 and fp32 conversions are bit shifts
-            nan_g = (g & 0x7C00) == 0x7C00
-            nan_g &= (g & 0x03FF) != 0
-            nan_e = ((e & 0x7C00) == 0x7C00) & ((e & 0x03FF) != 0)
+        if dtype != "float32":
+            # the copy goes through fp32 registers and the RNE store conversion
+            # (cvt.rn.f16.f32 / cvt.rn.bf16x2.f32): every value and sign
+            # survives, a NaN stays a NaN but its payload may not (Z11)
+            em, mm = (0x7C00, 0x03FF) if dtype == "float16" else (0x7F80, 0x007F)
+            nan_g = ((g & em) == em) & ((g & mm) != 0)
+            nan_e = ((e & em) == em) & ((e & mm) != 0)
             assert np.array_equal(nan_g, nan_e), f"{mode} {p}/{q} {dtype}: NaN positions"
             g, e = g[~nan_e], e[~nan_e]
         assert np.array_equal(g, e), f"{mode} {p}/{q} {dtype}"
+
+
+def test_nearest_row_kernel_equals_general_kernel(monkeypatch):
+    """The row-staged gather and the general gather (FCFS_NO_NEAREST_ROWS) give
+    the same bits on batches of jobs sharing one input: anisotropic factors,
+    up- and down-scaling, paper extent rows past the last input row (reflect:
+    rows read from global memory), several jobs in one launch."""
+    import paper_2203_10670_b200 as fc
+    for dtype in ("float32", "bfloat16"):
+        x = special_input(11, (3, 2, 77, 96), dtype).to(DEV)
+        plans = [Plan.nd(pq[0], pq[1], "nearest", pad, 2, (77, 96), dtype, ext)
+                 for pq, pad, ext in [(((2, 3), (3, 4)), "zero", "floor"), (((5, 7), (3, 2)), "reflect", "paper"),
+                                      (((3, 1), (4, 1)), "replicate", "paper"), (((1, 1), (1, 1)), "zero", "floor")]]
+        for pl in plans:
+            assert pl.launch_info(3)["variant"] == "rows_staged"
+        a = [torch.empty(pl.out_shape(3), dtype=x.dtype, device=DEV) for pl in plans]
+        b = [torch.empty_like(t) for t in a]
+        fc.run_batch([(pl, x, o) for pl, o in zip(plans, a)])
+        torch.cuda.synchronize()
+        monkeypatch.setenv("FCFS_NO_NEAREST_ROWS", "1")
+        fc.run_batch([(pl, x, o) for pl, o in zip(plans, b)])
+        torch.cuda.synchronize()
+        monkeypatch.delenv("FCFS_NO_NEAREST_ROWS")
+        for i, (u, v) in enumerate(zip(a, b)):
+            assert torch.equal(u.view(TORCH_INT[dtype]), v.view(TORCH_INT[dtype])), (dtype, i)
