@@ -50,7 +50,9 @@ def _compile(src: str, obj: str, verbose: bool) -> str:
     return r.stderr
 
 
-def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False, only: list | None = None) -> str:
+    """only: developer iteration -- recompile just these translation units (base
+    names, e.g. k_fused_bf16_pair) and relink, whatever the header times say."""
     os.makedirs(BUILD, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     hdr = max(os.path.getmtime(h) for h in _headers())
@@ -58,7 +60,10 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
     for s in srcs:
         o = os.path.join(BUILD, os.path.basename(s) + ".o")
         objs.append(o)
-        if force or _stale(o, s, hdr):
+        if only is not None:
+            if os.path.splitext(os.path.basename(s))[0] in only:
+                todo.append((s, o))
+        elif force or _stale(o, s, hdr):
             todo.append((s, o))
     if todo:
         with cf.ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 4) as ex:
@@ -82,5 +87,6 @@ if __name__ == "__main__":
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-j", type=int, default=None)
     ap.add_argument("-v", action="store_true", help="ptxas -v register/smem report")
+    ap.add_argument("--only", nargs="*", help="recompile only these translation units (developer iteration)")
     a = ap.parse_args()
-    print(build(a.force, a.j, a.v))
+    print(build(a.force, a.j, a.v, a.only))
