@@ -284,6 +284,8 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L, const F
         // G = 1: one flush per y-period, two full-period staging slots;
         // G = 2: two flushes per period, slots of ceil(P/2) rows (half the smem)
         for (int Gf = 1; Gf <= (PY >= 2 ? 2 : 1); ++Gf) {
+            if (const char *e = std::getenv("FCFS_DEBUG_G"))  // tuning / race tests: force the flush groups
+                if (std::atoi(e) != Gf && PY >= 2) continue;
             FusedArgs c = a;
             c.G = Gf;
             c.JM = Gf == 2 ? (PY + 1) / 2 : PY;

@@ -88,7 +88,7 @@ def hot_lines(rep, top=15):
     return [(k, 100 * inst[k] / I, 100 * stall[k] / S, src.get(k, "")) for k, _ in stall.most_common(top)]
 
 
-def summarise(rep, out, traffic_key=None, title=None):
+def summarise(rep, out, traffic_key=None, title=None, traffic_match=None):
     kernels, units = raw_rows(rep)
     lines = [f"# {title or os.path.basename(rep)}", "", f"Source report: `{os.path.basename(rep)}` "
              "(`ncu --set full --clock-control none --import-source on`, one launch).", ""]
@@ -113,8 +113,9 @@ def summarise(rep, out, traffic_key=None, title=None):
         du = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
               "s": 1.0}[units.get("gpu__time_duration.sum", "").strip().lower()]
         tot = rd * ru + wr * wu
-        per_name.setdefault(name, tot)
-        traffic = sum(per_name.values())
+        if traffic_match is None or traffic_match in name:  # (C4: only the dominant launch's kernel)
+            per_name.setdefault(name, tot)
+        traffic = sum(per_name.values()) if per_name else None
         lines.append(f"| DRAM read+write per launch | {tot / 1e6:.3f} MB |")
         if dur == dur and dur > 0:
             lines.append(f"| achieved DRAM bandwidth (under ncu, cold) | {tot / (dur * du) / 1e9:.1f} GB/s |")
@@ -166,10 +167,11 @@ if __name__ == "__main__":
     ap.add_argument("--out", required=True)
     ap.add_argument("--traffic-key")
     ap.add_argument("--title")
+    ap.add_argument("--traffic-match", help="only kernels whose name contains this count toward the traffic key")
     ap.add_argument("--launches")
     a = ap.parse_args()
     if a.launches:
         launches(a.launches, a.out)
     else:
-        summarise(a.report, a.out, a.traffic_key, a.title)
+        summarise(a.report, a.out, a.traffic_key, a.title, a.traffic_match)
     print(a.out)
