@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define FCFS_VERSION 4
+#define FCFS_VERSION 5
 #define FCFS_MAX_FACTOR 64 /* p and q (after gcd reduction) must be <= 64 */
 
 typedef struct fcfs_plan_s *fcfs_plan_t;
@@ -291,6 +291,12 @@ fcfs_status fcfs_launch_info(fcfs_plan_t plan, int64_t N, int64_t out_row0, int6
  * "launches"}, or {"kernel": "tiled_adjoint" | "reference_adjoint"}.
  * Errors: FCFS_E_ARG. */
 fcfs_status fcfs_adjoint_info(fcfs_plan_t plan, int64_t N, char *buf, int64_t buflen);
+
+/* fcfs_last_launch -- the JSON description (as fcfs_launch_info) of the most
+ * recent launch the calling host thread made through this library (run,
+ * run_rows, run_batch, run_rows_segments, run_adjoint); "{}" before any.
+ * Errors: FCFS_E_ARG. */
+fcfs_status fcfs_last_launch(char *buf, int64_t buflen);
 
 /* The fp32 phase table of the W dimension: for phase j in [0, p), weights
  * w[4*j + t] (t < ntaps; unused entries 0) and base offsets base[j] =

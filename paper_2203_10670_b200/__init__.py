@@ -10,6 +10,6 @@ Public API:
     dist                                      -- multi-GPU drivers (batch shards, row strips + NCCL halo)
 """
 from ._lib import FcfsError, LIB_PATH  # noqa: F401  (raises ImportError if libfcfs.so is missing)
-from .fcfs import Plan, apply, get_plan, kernel_launches, run_batch, scale, scale_nd  # noqa: F401
+from .fcfs import Plan, apply, get_plan, kernel_launches, last_launch, run_batch, scale, scale_nd  # noqa: F401
 
-__all__ = ["Plan", "apply", "get_plan", "kernel_launches", "run_batch", "scale", "scale_nd", "FcfsError", "LIB_PATH"]
+__all__ = ["Plan", "apply", "get_plan", "kernel_launches", "last_launch", "run_batch", "scale", "scale_nd", "FcfsError", "LIB_PATH"]

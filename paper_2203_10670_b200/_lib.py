@@ -54,6 +54,7 @@ SIGNATURES = {
     "fcfs_plan_info": (i32, [vp, ctypes.POINTER(PlanInfo)]),
     "fcfs_launch_info": (i32, [vp, i64, i64, i64, ctypes.c_char_p, i64]),
     "fcfs_adjoint_info": (i32, [vp, i64, ctypes.c_char_p, i64]),
+    "fcfs_last_launch": (i32, [ctypes.c_char_p, i64]),
     "fcfs_phase_table": (i32, [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int)]),
     "fcfs_compulsory_bytes": (i32, [vp, i64, P64]),
     "fcfs_destroy": (None, [vp]),

@@ -144,6 +144,12 @@ struct FusedArgs {
                          // ones, so that 16-bit outputs whose plane size is odd keep one 4-B
                          // phase per task (packed staging stores without warp divergence)
     int32_t row_pitch;   // bytes between the rows of a segment block (= seg_pitch)
+    // input rows from up to 3 row windows (fcfs_run_rows_segments; 2D, row copies,
+    // no TMA box): window k holds global rows [seg_row0[k], + seg_nrows[k]) of every
+    // plane; 0: the single window (in, in_row0, in_nrows)
+    int32_t nseg_in;
+    const void *seg_in[3];
+    int32_t seg_row0[3], seg_nrows[3];
     // 3D variants (TZ > 1): every plane has Do output slices from D input
     // slices; output slice m_z combines the TZ input slices b_z + lo + t with
     // the slice weights of phase j_z = m_z mod pz (reference contract: slices,

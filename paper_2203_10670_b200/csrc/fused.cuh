@@ -492,7 +492,17 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                         const int v = vf + r;
                         if (a.pad == FCFS_PAD_ZERO && (v < 0 || v >= a.H)) continue;
                         // rows outside the window only feed masked outputs: clamp
-                        const int src = min(max(pad_src32(v, a.H, a.pad) - a.in_row0, 0), a.in_nrows - 1);
+                        int src = min(max(pad_src32(v, a.H, a.pad) - a.in_row0, 0), a.in_nrows - 1);
+                        if constexpr (TZ == 1) {
+                            if (a.nseg_in > 0) {  // row windows (fcfs_run_rows_segments): the one holding the row
+                                const int gr = src + a.in_row0;
+                                int k = 0;
+                                while (k + 1 < a.nseg_in && (gr < a.seg_row0[k] || gr >= a.seg_row0[k] + a.seg_nrows[k])) ++k;
+                                const int lr = min(max(gr - a.seg_row0[k], 0), a.seg_nrows[k] - 1);
+                                pin = static_cast<const T *>(a.seg_in[k]) + (int64_t)sg.plane * a.seg_nrows[k] * a.W + sg.a0;
+                                src = lr;
+                            }
+                        }
 #pragma unroll
                         for (int tz = 0; tz < TZ; ++tz) {
                             int64_t soff = 0;

@@ -637,7 +637,12 @@ fcfs_status prepare(fcfs_plan_t pl, const void *in, int64_t in_row0, int64_t in_
     return FCFS_OK;
 }
 
+// the JSON description of the calling thread's most recent launch (fcfs_last_launch)
+thread_local char g_last_launch[768] = "{}";
+void note_launch(const char *desc) { std::snprintf(g_last_launch, sizeof(g_last_launch), "%s", desc); }
+
 fcfs_status launch(const Prepared &pr, void *stream) {
+    note_launch(pr.L.desc);
     int rc = 0;
     if (pr.kernel == 1) rc = launch_nearest(pr.pl->dtype, pr.na, stream);
     else if (pr.kernel == 2) rc = launch_fused(pr.pl->fused, pr.L.a, pr.L.grid, kFusedThreads, pr.L.smem, stream);
@@ -855,6 +860,49 @@ fcfs_status fcfs_run_rows_segments(fcfs_plan_t pl, int nseg, const void *const *
     }
     fcfs_status st = check_device(pl);
     if (st != FCFS_OK) return st;
+    const int ESZ = esize(pl->dtype);
+    // the fused kernel, its producer copying each input row from the window
+    // holding it (16-B aligned windows and rows; a few output rows per strip)
+    bool fused_ok = pl->kernel == 2 && pl->fused && pl->fused->TZ == 1 && pl->D == 1 && (pl->W * ESZ) % 16 == 0 &&
+                    !std::getenv("FCFS_SEGMENTS_REFERENCE");
+    for (int k = 0; k < nseg && fused_ok; ++k) fused_ok = (reinterpret_cast<uintptr_t>(seg_rows[k]) & 15) == 0;
+    if (fused_ok) {
+        int64_t lo = seg_row0[0], hi = seg_row0[0] + seg_nrows[0];
+        for (int k = 1; k < nseg; ++k) {
+            lo = std::min(lo, seg_row0[k]);
+            hi = std::max(hi, seg_row0[k] + seg_nrows[k]);
+        }
+        RunGeom g;
+        g.in = seg_rows[0];
+        g.out = out_rows;
+        g.planes = N * pl->C;
+        g.D = g.Do = 1;
+        g.H = pl->H;
+        g.W = pl->W;
+        g.Ho = pl->Ho;
+        g.Wo = pl->Wo;
+        g.in_row0 = lo;
+        g.in_nrows = hi - lo;
+        g.out_row0 = out_row0;
+        g.out_nrows = out_nrows;
+        g.in_plane_stride = seg_nrows[0] * pl->W;
+        g.out_plane_stride = out_nrows * pl->Wo;
+        FusedLaunch L;
+        if (g.planes * std::max(g.in_nrows * pl->W, out_nrows * pl->Wo) <= INT32_MAX * 16LL && plan_fused(pl, g, L)) {
+            L.a.use_tmap = 0;  // row copies: each from its own window
+            L.a.nseg_in = nseg;
+            for (int k = 0; k < nseg; ++k) {
+                L.a.seg_in[k] = seg_rows[k];
+                L.a.seg_row0[k] = (int32_t)seg_row0[k];
+                L.a.seg_nrows[k] = (int32_t)seg_nrows[k];
+            }
+            char d[800];
+            std::snprintf(d, sizeof(d), "{\"kernel\": \"fused_separable\", \"segments\": %d}", nseg);
+            note_launch(d);
+            return launch_fused(pl->fused, L.a, L.grid, kFusedThreads, L.smem, stream) == 0 ? FCFS_OK : FCFS_E_CUDA;
+        }
+    }
+    note_launch("{\"kernel\": \"reference\", \"segments\": 1}");
     RefArgs a;
     std::memset(&a, 0, sizeof(a));
     RunGeom &g = a.g;
@@ -1167,6 +1215,11 @@ static fcfs_status adjoint_impl(fcfs_plan_t pl, const void *grad_out, void *grad
         if (planes * std::max(pl->Ho * pl->Wo, pl->H * pl->W) <= INT32_MAX * 16LL &&
             plan_fused(pl, g, L, v, FCFS_PAD_ZERO)) {
             const bool no_bands = pl->pad == FCFS_PAD_ZERO || std::getenv("FCFS_DEBUG_NO_BANDS");
+            {
+                char d[256];
+                std::snprintf(d, sizeof(d), "{\"kernel\": \"fused_adjoint\", \"bands\": %d}", no_bands ? 0 : 1);
+                if (!info) note_launch(d);
+            }
             if (info) {
                 if (no_bands)
                     std::snprintf(info, (size_t)infolen, "{\"kernel\": \"fused_adjoint\", \"PY\": %d, \"QY\": %d, "
@@ -1231,11 +1284,18 @@ static fcfs_status adjoint_impl(fcfs_plan_t pl, const void *grad_out, void *grad
                       a.TH > 0 ? "tiled_adjoint" : "reference_adjoint");
         return FCFS_OK;
     }
+    note_launch(a.TH > 0 ? "{\"kernel\": \"tiled_adjoint\"}" : "{\"kernel\": \"reference_adjoint\"}");
     return launch_adjoint(pl->dtype, a, stream) == 0 ? FCFS_OK : FCFS_E_CUDA;
 }
 
 fcfs_status fcfs_run_adjoint(fcfs_plan_t pl, const void *grad_out, void *grad_in, int64_t N, void *stream) {
     return adjoint_impl(pl, grad_out, grad_in, N, stream, nullptr, 0);
+}
+
+fcfs_status fcfs_last_launch(char *buf, int64_t buflen) {
+    if (!buf || buflen < 2) return FCFS_E_ARG;
+    std::snprintf(buf, (size_t)buflen, "%s", g_last_launch);
+    return FCFS_OK;
 }
 
 fcfs_status fcfs_adjoint_info(fcfs_plan_t pl, int64_t N, char *buf, int64_t buflen) {

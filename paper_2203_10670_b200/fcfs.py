@@ -278,6 +278,14 @@ class Plan:
         return out_host
 
 
+def last_launch() -> dict:
+    """The calling thread's most recent launch (fcfs_last_launch): kernel and geometry."""
+    import json
+    buf = ctypes.create_string_buffer(1024)
+    check(_lib.lib.fcfs_last_launch(buf, 1024), "fcfs_last_launch")
+    return json.loads(buf.value.decode())
+
+
 def kernel_launches() -> int:
     """Kernels the library has launched (or captured into graphs) in this process (fcfs_kernel_launches)."""
     return int(_lib.lib.fcfs_kernel_launches())

@@ -99,7 +99,7 @@ def test_unknown_enum_and_flags():
     assert _lib.lib.fcfs_plan_ex(3, 2, 0, 0, 1, 4, 4, 0, 1 << 20, ctypes.byref(h)) == 1
     assert _lib.lib.fcfs_plan_ex(3, 2, 0, 0, 1, 4, 4, 0, 0, None) == 1
     assert _lib.lib.fcfs_status_str(6).decode() == "CUDA error"
-    assert _lib.lib.fcfs_version() == 4
+    assert _lib.lib.fcfs_version() == 5
 
 
 def test_run_without_device_is_refused(fc):

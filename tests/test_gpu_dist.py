@@ -105,6 +105,49 @@ def test_run_rows_segments_equals_contiguous_rows():
         assert e.value.name == "FCFS_E_ARG"
 
 
+def test_run_rows_segments_fused_against_oracle(monkeypatch):
+    """The peer-halo boundary launch runs the fused kernel --
+    its producer copies each input row from the window holding it -- on three
+    windows (own strip + both neighbours' strips): every output row checked
+    against the oracle's direct evaluator on exactly those rows (row0 = the
+    first window row), and bitwise equal to the reference kernel's segment
+    reads (FCFS_SEGMENTS_REFERENCE) and to the single launch."""
+    import numpy as np
+    import oracle
+    import paper_2203_10670_b200 as fc
+    from helpers import compare
+    for (p, q, mode, pad, dtype, N, C) in [(3, 5, "bicubic", "replicate", "float32", 1, 1),
+                                           (5, 3, "bicubic", "reflect", "bfloat16", 2, 3),
+                                           (7, 5, "bilinear", "zero", "float16", 1, 2),
+                                           (4, 7, "bilinear", "reflect", "float32", 1, 2)]:
+        H, W = 301, 256
+        pl = fc.Plan(p, q, mode, pad, C, H, W, dtype, "floor")
+        xv = synth.normal_f32(57, N * C * H * W).reshape(N, C, H, W)
+        x = torch.from_numpy(xv).to(getattr(torch, dtype)).cuda()
+        xr = x.float().cpu().numpy()
+        whole = pl.run(x)
+        cuts = [0, 97, 205, H]
+        strips = [(x[:, :, a:b].contiguous(), a) for a, b in zip(cuts[:-1], cuts[1:])]
+        for s in range(3):
+            o0, o1, n0, n1 = pl.strip_rows(cuts[s], cuts[s + 1])
+            wins = [strips[s]] + [strips[k] for k in (s - 1, s + 1) if 0 <= k < 3]
+            got = pl.run_rows_segments(wins, o0, o1 - o0)
+            torch.cuda.synchronize()
+            assert fc.last_launch() == {"kernel": "fused_separable", "segments": len(wins)}, fc.last_launch()
+            lo = min(r0 for _, r0 in wins)
+            hi = max(r0 + t.shape[2] for t, r0 in wins)
+            ref = oracle.direct(xr[:, :, lo:hi], p, q, mode, pad, floor_extent=True, rows=(o0, o1), H=H, row0=lo)
+            compare(got, ref, dtype, mode, float(xr.max() - xr.min()), f"segments {p}/{q} strip {s}",
+                    x_absmax=float(np.abs(xr).max()))
+            monkeypatch.setenv("FCFS_SEGMENTS_REFERENCE", "1")
+            got_ref = pl.run_rows_segments(wins, o0, o1 - o0)
+            torch.cuda.synchronize()
+            monkeypatch.delenv("FCFS_SEGMENTS_REFERENCE")
+            assert fc.last_launch()["kernel"] == "reference"
+            assert torch.equal(got.view(torch.uint8), got_ref.view(torch.uint8)), (p, q, s)
+            assert torch.equal(got.view(torch.uint8), whole[:, :, o0:o1].contiguous().view(torch.uint8)), (p, q, s)
+
+
 def test_strip_runner_peer_transport_world1(pg):
     """The symmetric-memory setup and run path of the peer transport on one GPU
     (world 1: no neighbours, every row interior) equals the single launch."""
