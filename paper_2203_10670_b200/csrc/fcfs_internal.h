@@ -196,6 +196,11 @@ struct WgradArgs {
     uint32_t fd_tasks[3], fd_nxb[3];  // FastDiv (d, m, s) of nyb * nxb and nxb (task -> plane, band; tasks < 2^31)
 };
 int launch_wgrad(int dtype, const WgradArgs &a, int grid, int smem, void *stream);
+// Row-blocked weight gradient (k_wgrad.cu) for the factor combinations it compiles:
+// WgradArgs with xb = x-chunks per row, yb = x-periods per chunk, grows = band rows,
+// xrows / xcols / gcols = tile sizes.
+bool wgrad_rows_available(int py, int qy, int px, int qx, int nt);
+int launch_wgrad_rows(int dtype, const WgradArgs &a, int grid, int smem, void *stream);
 // every successful kernel launch of the library (fcfs_kernel_launches)
 void count_launch();
 int launch_adjoint(int dtype, const AdjArgs &a, void *stream);

@@ -156,6 +156,218 @@ __global__ void __launch_bounds__(256) fcfs_wgrad_kernel(const __grid_constant__
     }
 }
 
+// ---------------------------------------------------------------------------
+// Row-blocked weight gradient (2D plans whose factors have a compiled entry;
+// the kernel above serves every other plan).  A task is a band of BR output
+// rows of one plane (all columns); thread (r, c) owns output row my0 + r and
+// the c-th run of XP x-periods of it.  The row fixes the row phase jy, so the
+// thread holds all NT x PX x NT partial sums of that phase -- acc[ty][jx][tx]
+// -- and per x-period loads the PX grad_out values and the NT x Lw input window
+// once (NT x Lw window elements serve all PX column phases: their taps
+// overlap) for NT x PX x NT FMAs, packed over tap-row pairs (ty, ty + 1):
+// the window is held as (row ty, row ty + 1) pairs straight from the shared
+// loads, each FFMA2 takes one grad_out value for both lanes.  Tiles are
+// staged in shared memory as fp32 with the padding applied; the next task's
+// rows are prefetched into L2.  At the end the partial sums go to a shared
+// [PY][PX][NT][NT] table (shared atomics) and then to grad_w (one global
+// atomic per weight and CTA).  fp32 throughout, sum order not fixed (Z22).
+// ---------------------------------------------------------------------------
+template <int P, int Q>
+struct WgPhase {
+    static __host__ __device__ constexpr int base(int j) { return (j * Q) / P; }
+};
+
+// shared tile layouts of the row-blocked kernel: input column xc sits at tile
+// column xc + kWgXOff (16-B aligned 4-element groups); grad_out rows are a flat
+// copy of the band's contiguous span, element e of the span at gs[e + shift]
+constexpr int kWgXOff = 4;
+
+template <typename T>
+__device__ __forceinline__ void cvt4(const T *src, float (&f)[4]) {  // 4 elements from an 8-B (16-bit) / 16-B load
+    if constexpr (sizeof(T) == 2) {
+        const uint2 w = *reinterpret_cast<const uint2 *>(src);
+        const T *e = reinterpret_cast<const T *>(&w);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) f[k] = DT<T>::to_f(e[k]);
+    } else {
+        const float4 w = *reinterpret_cast<const float4 *>(src);
+        f[0] = w.x, f[1] = w.y, f[2] = w.z, f[3] = w.w;
+    }
+}
+
+template <typename T, int PY, int QY, int PX, int QX, int NT>
+__global__ void __launch_bounds__(256, 2) fcfs_wgrad_rows_kernel(const __grid_constant__ WgradArgs a) {
+    constexpr int LO = NT == 4 ? -1 : 0;
+    constexpr int LW = WgPhase<PX, QX>::base(PX - 1) + NT;  // window columns of one x-period (all phases)
+    constexpr int NH = NT / 2;                               // tap-row pairs
+    extern __shared__ __align__(16) float wsm[];
+    const int XC = a.xcols, XR = a.xrows, BR = a.grows, XCH = a.xb, XP = a.yb;
+    float *xs = wsm;                  // [XR][XC] padded input rows of the band
+    float *gs = wsm + XR * XC;        // flat grad_out span of the band (+ alignment room)
+    float *gsum = gs + a.gcols;       // [PY][PX][NT][NT] the CTA's sums
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int r = tid / XCH, c = tid - (tid / XCH) * XCH;
+    const int nxp = (a.Wo + PX - 1) / PX;
+    const int ix0 = c * XP, ix1 = min(nxp, ix0 + XP);
+    const int xlo = LO, xhi = (nxp - 1) * QX + LW + LO;  // input columns the band's windows read
+    for (int i = tid; i < PY * PX * NT * NT; i += 256) gsum[i] = 0.0f;
+    float2 acc[NH][PX][NT];
+#pragma unroll
+    for (int h = 0; h < NH; ++h)
+#pragma unroll
+        for (int jx = 0; jx < PX; ++jx)
+#pragma unroll
+            for (int tx = 0; tx < NT; ++tx) acc[h][jx][tx] = make_float2(0.0f, 0.0f);
+    int jy_acc = -1;  // the row phase of the thread's sums (every band starts at a multiple of PY)
+    const int nbands = (a.Ho + BR - 1) / BR;
+    auto band_rows = [&](int64_t task, int64_t &plane, int &my0, int &vr0) {
+        plane = task / nbands;
+        my0 = (int)(task - plane * nbands) * BR;
+        vr0 = (my0 / PY) * QY + LO;
+    };
+    auto prefetch = [&](int64_t task) {
+        if (task >= a.ntasks) return;
+        int64_t plane;
+        int my0, vr0;
+        band_rows(task, plane, my0, vr0);
+        if (tid < XR) {
+            const int rr = min(max(vr0 + tid, 0), a.H - 1);
+            prefetch_l2(static_cast<const T *>(a.x) + (plane * a.H + rr) * (int64_t)a.W, (int64_t)a.W * sizeof(T));
+        } else if (tid == XR) {
+            const int m1 = min(a.Ho, my0 + BR);
+            prefetch_l2(static_cast<const T *>(a.g) + (plane * a.Ho + my0) * (int64_t)a.Wo,
+                        (int64_t)(m1 - my0) * a.Wo * sizeof(T));
+        }
+    };
+    prefetch(blockIdx.x);
+    for (int64_t task = blockIdx.x; task < a.ntasks; task += gridDim.x) {
+        int64_t plane;
+        int my0, vr0;
+        band_rows(task, plane, my0, vr0);
+        const T *xp = static_cast<const T *>(a.x) + plane * (int64_t)a.H * a.W;
+        __syncthreads();  // the previous task's readers are done
+        // padded input rows: a warp per row; the image columns as 4-element vectors
+        // (the host requires 16-B aligned rows), the few padding columns by the
+        // first lanes (the padding index map)
+        const int nv = a.W / 4;
+        for (int rr = warp; rr < XR; rr += 8) {
+            const int sr = pad_src32(vr0 + rr, a.H, a.pad);
+            float *srow = xs + rr * XC + kWgXOff;  // srow[xc]: input column xc
+            if (sr < 0) {  // a zero-padding row
+                for (int cc = xlo + lane; cc < xhi; cc += 32) srow[cc] = 0.0f;
+                continue;
+            }
+            const T *xrow = xp + (int64_t)min(sr, a.H - 1) * a.W;
+            for (int v = lane; v < nv; v += 32) {
+                float f[4];
+                cvt4<T>(xrow + 4 * v, f);
+                *reinterpret_cast<float4 *>(srow + 4 * v) = make_float4(f[0], f[1], f[2], f[3]);
+            }
+            const int npl = -xlo, npr = max(0, xhi - a.W);
+            if (lane < npl + npr) {  // padding columns [xlo, 0) and [W, xhi)
+                const int cc = lane < npl ? xlo + lane : a.W + (lane - npl);
+                const int sc = pad_src32(cc, a.W, a.pad);
+                srow[cc] = sc < 0 ? 0.0f : DT<T>::to_f(xrow[min(sc, a.W - 1)]);
+            }
+        }
+        // grad_out: the band's rows are one contiguous span; its 8-B (16-bit) /
+        // 16-B aligned superset lands flat, element e of the span at gs[e + shift]
+        const int m1 = min(a.Ho, my0 + BR);
+        const T *gspan = static_cast<const T *>(a.g) + (plane * a.Ho + my0) * (int64_t)a.Wo;
+        const int shift = (int)((reinterpret_cast<uintptr_t>(gspan) & (4 * sizeof(T) - 1)) / sizeof(T));
+        const int ng = (m1 - my0) * a.Wo + shift;
+        const T *gend = static_cast<const T *>(a.g) + a.planes * (int64_t)a.Ho * a.Wo;
+        for (int v = tid; 4 * v < ng; v += 256) {
+            const T *src = gspan - shift + 4 * v;  // (past the span's end: the next rows' bytes, never used)
+            float f[4];
+            if (src + 4 <= gend) {
+                cvt4<T>(src, f);
+            } else {  // the tensor's last elements: no read past its end
+#pragma unroll
+                for (int k = 0; k < 4; ++k) f[k] = src + k < gend ? DT<T>::to_f(src[k]) : 0.0f;
+            }
+            *reinterpret_cast<float4 *>(gs + 4 * v) = make_float4(f[0], f[1], f[2], f[3]);
+        }
+        __syncthreads();
+        prefetch(task + gridDim.x);
+        const int my = my0 + r;
+        if (r < BR && my < a.Ho && ix0 < ix1) {
+            const int jy = my % PY;
+            jy_acc = jy;
+            // the thread's first window row in the tile: floor(my QY / PY) + LO - vr0
+            const float *xrow = xs + ((my / PY) * QY + WgPhase<PY, QY>::base(jy) + LO - vr0) * XC + kWgXOff + ix0 * QX + LO;
+            const float *grow = gs + shift + r * a.Wo + ix0 * PX;
+            // the row's last x-period may end past the row (those grad_out values are zeros)
+            const int ixf = (a.Wo % PX) && ix1 == nxp ? ix1 - 1 : ix1;
+            auto step = [&](const float *xq, const float *gq, int nj) {
+                float gv[PX];
+#pragma unroll
+                for (int jx = 0; jx < PX; ++jx) gv[jx] = jx < nj ? gq[jx] : 0.0f;
+                float2 xw[NH][LW];
+#pragma unroll
+                for (int h = 0; h < NH; ++h)
+#pragma unroll
+                    for (int k = 0; k < LW; ++k) xw[h][k] = make_float2(xq[(2 * h) * XC + k], xq[(2 * h + 1) * XC + k]);
+#pragma unroll
+                for (int h = 0; h < NH; ++h)
+#pragma unroll
+                    for (int jx = 0; jx < PX; ++jx)
+#pragma unroll
+                        for (int tx = 0; tx < NT; ++tx)
+                            acc[h][jx][tx] = ffma2_rn(gv[jx], xw[h][WgPhase<PX, QX>::base(jx) + tx], acc[h][jx][tx]);
+            };
+            int ix = ix0;
+            for (; ix < ixf; ++ix, xrow += QX, grow += PX) step(xrow, grow, PX);
+            if (ix < ix1) step(xrow, grow, a.Wo - ix * PX);
+        }
+    }
+    // the thread's sums (one row phase) into the CTA table, then one atomic per weight
+    if (jy_acc >= 0) {
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+#pragma unroll
+            for (int jx = 0; jx < PX; ++jx)
+#pragma unroll
+                for (int tx = 0; tx < NT; ++tx) {
+                    float *e = gsum + ((jy_acc * PX + jx) * NT + 2 * h) * NT + tx;
+                    atomicAdd(e, acc[h][jx][tx].x);
+                    atomicAdd(e + NT, acc[h][jx][tx].y);
+                }
+    }
+    __syncthreads();
+    for (int i = tid; i < PY * PX * NT * NT; i += 256) atomicAdd(&a.gw[i], gsum[i]);
+}
+
+// The compiled (PY/QY, PX/QX, taps) entries of the row-blocked weight gradient.
+#define FCFS_WG_ROWS(Y) Y(5, 3, 4) Y(5, 3, 2) Y(3, 2, 4) Y(3, 2, 2) Y(2, 3, 4) Y(2, 3, 2) Y(3, 5, 4) Y(3, 5, 2)
+
+bool wgrad_rows_available(int py, int qy, int px, int qx, int nt) {
+#define FCFS_WG_AV(P, Q, N) if (py == P && qy == Q && px == P && qx == Q && nt == N) return true;
+    FCFS_WG_ROWS(FCFS_WG_AV)
+#undef FCFS_WG_AV
+    return false;
+}
+
+int launch_wgrad_rows(int dtype, const WgradArgs &a, int grid, int smem, void *stream) {
+    const void *fn = nullptr;
+#define FCFS_WG_PICK(P, Q, N)                                                                                   \
+    if (a.py == P && a.qy == Q && a.px == P && a.qx == Q && a.ntx == N)                                         \
+        fn = dtype == FCFS_F32   ? reinterpret_cast<const void *>(&fcfs_wgrad_rows_kernel<float, P, Q, P, Q, N>)  \
+             : dtype == FCFS_F16 ? reinterpret_cast<const void *>(&fcfs_wgrad_rows_kernel<__half, P, Q, P, Q, N>) \
+                                 : reinterpret_cast<const void *>(&fcfs_wgrad_rows_kernel<__nv_bfloat16, P, Q, P, Q, N>);
+    FCFS_WG_ROWS(FCFS_WG_PICK)
+#undef FCFS_WG_PICK
+    if (!fn) return (int)cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return (int)e;
+    WgradArgs local = a;
+    void *args[] = {&local};
+    e = cudaLaunchKernel(fn, dim3(grid), dim3(256), args, (size_t)smem, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return (int)e;
+    count_launch();
+    return (int)cudaGetLastError();
+}
+
 int launch_wgrad(int dtype, const WgradArgs &a, int grid, int smem, void *stream) {
     const int nt = a.ntx, gy = (a.npairs + 31) / 32;
     cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -1369,6 +1369,33 @@ fcfs_status fcfs_run_weight_grad(fcfs_plan_t pl, const void *x, const void *grad
     }
     a.npairs = a.py * a.px;
     const int span_x = fx_max + a.ntx - a.fx_min, span_y = fy_max + a.nty - a.fy_min;
+    // the row-blocked kernel: 2D isotropic plans with a compiled entry, tiles in ~100 KB
+    if (!rows1 && pl->D == 1 && a.ntx == a.nty && !std::getenv("FCFS_NO_WGRAD_ROWS") &&
+        (pl->W * esize(pl->dtype)) % 16 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(grad_out) & 15) == 0 &&
+        wgrad_rows_available(a.py, a.qy, a.px, a.qx, a.ntx)) {
+        WgradArgs b = a;
+        const int nxp = (b.Wo + b.px - 1) / b.px;
+        const int xch = std::max(1, std::min(8, (nxp + 11) / 12));  // x-chunks per row: ~12 x-periods each
+        int br = 256 / xch;
+        br -= br % b.py;  // a thread's rows keep one row phase across bands
+        if (br >= b.py) {
+            b.xb = xch;
+            b.yb = (nxp + xch - 1) / xch;
+            b.grows = br;
+            // input tile row: columns [fx_min, (nxp-1) qx + span_x + fx_min) at tile offset 4 + column, 4-aligned pitch
+            b.xcols = (4 + std::max<int>((int)b.W, (nxp - 1) * b.qx + span_x + b.fx_min) + 3) / 4 * 4 + 4;
+            b.gcols = (br * b.Wo + 8 + 3) / 4 * 4;  // the flat grad_out span + alignment room
+            b.xrows = ((br - 1) / b.py) * b.qy + span_y + 1;
+            const int64_t smem = 4 * ((int64_t)b.xrows * b.xcols + (int64_t)b.gcols + b.py * b.px * b.ntx * b.ntx);
+            const int64_t nbands = (b.Ho + br - 1) / br;
+            b.ntasks = b.planes * nbands;
+            if (smem <= 100 * 1024 && b.ntasks < INT32_MAX) {
+                const int grid = (int)std::min<int64_t>(b.ntasks, (int64_t)pl->sm_count * 2);
+                return launch_wgrad_rows(pl->dtype, b, grid, (int)smem, stream) == 0 ? FCFS_OK : FCFS_E_CUDA;
+            }
+        }
+    }
     const int nix = (a.Wo + a.px - 1) / a.px, niy = (a.Ho + a.py - 1) / a.py;
     int budget = 48 * 1024;  // 4 CTAs per SM (tiles prefetched into L2 one task ahead)
     if (const char *e = std::getenv("FCFS_DEBUG_WG_BUDGET")) budget = std::atoi(e) * 1024;
