@@ -201,6 +201,10 @@ int launch_wgrad(int dtype, const WgradArgs &a, int grid, int smem, void *stream
 // xrows / xcols / gcols = tile sizes.
 bool wgrad_rows_available(int py, int qy, int px, int qx, int nt);
 int launch_wgrad_rows(int dtype, const WgradArgs &a, int grid, int smem, void *stream);
+// Tensor-core weight gradient (16-bit inputs, the same compiled factors): WgradArgs with
+// grows = band rows (a multiple of py), xrows / xcols = input tile rows / pitch (elements),
+// gcols = grad_out tile pitch (elements).
+int launch_wgrad_mma(int dtype, const WgradArgs &a, int grid, int smem, void *stream);
 // every successful kernel launch of the library (fcfs_kernel_launches)
 void count_launch();
 int launch_adjoint(int dtype, const AdjArgs &a, void *stream);

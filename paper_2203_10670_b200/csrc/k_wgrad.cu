@@ -11,6 +11,8 @@
 // memory and one atomicAdd per weight and CTA lands in grad_w (pre-zeroed by
 // the host).  fp32 throughout; the order of the atomics is not fixed, so
 // runs may differ in the last bits (the parity bar is an error bound).
+#include <type_traits>
+
 #include "device_common.cuh"
 
 namespace fcfs {
@@ -338,6 +340,236 @@ __global__ void __launch_bounds__(256, 2) fcfs_wgrad_rows_kernel(const __grid_co
     for (int i = tid; i < PY * PX * NT * NT; i += 256) atomicAdd(&a.gw[i], gsum[i]);
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core weight gradient (16-bit inputs; compiled factors).  The
+// gradient is a contraction over the x-periods p = (plane, iy, ix):
+//   M[(jy, jx)][(a, b)] = sum_p g[iy PY + jy][ix PX + jx] * x~[iy QY + LO + a][ix QX + LO + b]
+// for the PY*PX phases and the LH x LW window of a period, and
+// grad_w[jy][jx][ty][tx] = M[(jy, jx)][(by(jy) + ty, bx(jx) + tx)].  So a warp
+// runs mma.sync m16n8k16 (bf16/fp16 products are exact in fp32, fp32
+// accumulation; reading Z22's bound) with K = 16 consecutive x-periods of one
+// period row: A (phases x periods) and B (periods x window positions) are
+// gathered from shared tiles of the raw 16-bit data, every thread's element
+// addresses a per-thread base plus compile-time offsets.  Zero columns past
+// the row's end (grad_out) make the last block's extra periods contribute
+// nothing.  The warps' accumulators are summed in shared memory and each
+// weight takes one global atomic per CTA.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    if constexpr (std::is_same<T, __nv_bfloat16>::value)
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+            "{%0, %1, %2, %3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+    else
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+            "{%0, %1, %2, %3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+template <typename T, int PY, int QY, int PX, int QX, int NT>
+__global__ void __launch_bounds__(256) fcfs_wgrad_mma_kernel(const __grid_constant__ WgradArgs a) {
+    constexpr int LO = NT == 4 ? -1 : 0;
+    constexpr int LH = WgPhase<PY, QY>::base(PY - 1) + NT, LW = WgPhase<PX, QX>::base(PX - 1) + NT;
+    constexpr int MP = PY * PX, MT = (MP + 15) / 16;   // phases, M tiles
+    constexpr int NN = LH * LW, NTL = (NN + 7) / 8;    // window positions, N tiles
+    constexpr int XO = 8;                              // tile column of input column 0 (16-B aligned rows)
+    static_assert(MT <= 2 && NTL <= 8, "tensor-core weight gradient: <= 32 phases, <= 64 window positions");
+    // shared memory: [0, 64) two mbarriers; two tile buffers of (x tile, flat grad_out span); the CTA's sums
+    extern __shared__ __align__(128) unsigned char wsm_raw[];
+    const int XR = a.xrows, XP = a.xcols, GP = a.gcols, BR = a.grows;
+    uint64_t *full = reinterpret_cast<uint64_t *>(wsm_raw);
+    const int bufb = (XR * XP + GP) * 2;  // bytes per buffer (16-B multiple: host)
+    auto xs_of = [&](int buf) { return reinterpret_cast<uint16_t *>(wsm_raw + 128 + buf * bufb); };
+    auto gs_of = [&](int buf) { return xs_of(buf) + XR * XP; };
+    float *dsum = reinterpret_cast<float *>(wsm_raw + 128 + 2 * bufb);  // [MT * 16][NTL * 8]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int nxp = (a.Wo + PX - 1) / PX, nxb = (nxp + 15) / 16;
+    const int yper = BR / PY;  // period rows per band
+    const int xhi = (nxb * 16 - 1) * QX + LW + LO;  // one past the last input column any block reads
+    const int nbands = (a.Ho + BR - 1) / BR;
+    const T *gend = static_cast<const T *>(a.g) + a.planes * (int64_t)a.Ho * a.Wo;
+    if (tid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_fence_init();
+    }
+    for (int i = tid; i < MT * 16 * NTL * 8; i += 256) dsum[i] = 0.0f;
+    // columns past the padded window region never change: zeros, once
+    for (int buf = 0; buf < 2; ++buf)
+        for (int i = tid; i < XR * (XP - (XO + xhi)); i += 256) {
+            const int rr = i / (XP - (XO + xhi)), cc = XO + xhi + (i - rr * (XP - (XO + xhi)));
+            xs_of(buf)[rr * XP + cc] = 0;
+        }
+    __syncthreads();
+    struct Band {
+        int64_t plane;
+        int my0, vr0, m1, gsh, nflat;
+    };
+    auto band = [&](int64_t task) {
+        Band bd;
+        bd.plane = task / nbands;
+        bd.my0 = (int)(task - bd.plane * nbands) * BR;
+        bd.vr0 = (bd.my0 / PY) * QY + LO;
+        bd.m1 = min(a.Ho, bd.my0 + BR);
+        const T *gspan = static_cast<const T *>(a.g) + (bd.plane * a.Ho + bd.my0) * (int64_t)a.Wo;
+        bd.gsh = (int)((reinterpret_cast<uintptr_t>(gspan) & 15) / sizeof(T));
+        // the span's 16-B aligned superset, never past the tensor's (16-B aligned) end
+        const int64_t want = ((int64_t)bd.gsh + (int64_t)(bd.m1 - bd.my0) * a.Wo + 7) / 8 * 8;
+        const int64_t avail = gend - (gspan - bd.gsh);
+        bd.nflat = (int)min(want, avail / 8 * 8);
+        return bd;
+    };
+    // warp 0: the bulk copies of a task's tiles into a buffer (image rows, lane per
+    // row; the grad_out span, lane 0)
+    auto issue = [&](int64_t task, int buf) {
+        fence_proxy_async_smem();  // the buffer's earlier generic writes (padding, zeros) before the copies
+        const Band bd = band(task);
+        const T *xp = static_cast<const T *>(a.x) + bd.plane * (int64_t)a.H * a.W;
+        uint32_t bytes = lane == 0 ? (uint32_t)bd.nflat * 2 : 0u;
+        for (int rr = lane; rr < XR; rr += 32) bytes += pad_src32(bd.vr0 + rr, a.H, a.pad) >= 0 ? (uint32_t)a.W * 2 : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+        if (lane == 0) mbar_arrive_expect_tx(&full[buf], bytes);
+        __syncwarp();
+        const uint64_t pol = policy_evict_first();
+        for (int rr = lane; rr < XR; rr += 32) {
+            const int sr = pad_src32(bd.vr0 + rr, a.H, a.pad);
+            if (sr >= 0) bulk_g2s(xs_of(buf) + rr * XP + XO, xp + (int64_t)min(sr, a.H - 1) * a.W, (uint32_t)a.W * 2, &full[buf], pol);
+        }
+        const T *gspan = static_cast<const T *>(a.g) + (bd.plane * a.Ho + bd.my0) * (int64_t)a.Wo;
+        if (lane == 0 && bd.nflat > 0) bulk_g2s(gs_of(buf), gspan - bd.gsh, (uint32_t)bd.nflat * 2, &full[buf], pol);
+    };
+    // per-thread gather bases (element offsets within a block's tiles)
+    int abase[2 * MT], bbase[NTL];
+#pragma unroll
+    for (int i = 0; i < 2 * MT; ++i) {
+        int m = gq + 8 * i;
+        m = m < MP ? m : 0;  // rows past the phases: any valid element (those rows of D are never read)
+        abase[i] = (m / PX) * a.Wo + (m % PX) + 2 * tq * PX;  // the flat span: row pitch Wo
+    }
+#pragma unroll
+    for (int j = 0; j < NTL; ++j) {
+        int n = 8 * j + gq;
+        n = n < NN ? n : 0;
+        bbase[j] = (n / LW) * XP + (n % LW) + XO + LO + 2 * tq * QX;
+    }
+    float d[MT][NTL][4];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NTL; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) d[i][j][e] = 0.0f;
+    if (warp == 0 && blockIdx.x < a.ntasks) issue(blockIdx.x, 0);
+    uint32_t phase[2] = {0u, 0u};
+    int buf = 0;
+    for (int64_t task = blockIdx.x; task < a.ntasks; task += gridDim.x, buf ^= 1) {
+        const Band bd = band(task);
+        mbar_wait(&full[buf], phase[buf]);
+        phase[buf] ^= 1u;
+        uint16_t *xs = xs_of(buf), *gs = gs_of(buf);
+        // padding: rows past the image (zero / replicate / reflect rows came as copies),
+        // padding columns, the grad_out rows past Ho in the last period row
+        {
+            const uint16_t *xp = reinterpret_cast<const uint16_t *>(static_cast<const T *>(a.x) + bd.plane * (int64_t)a.H * a.W);
+            const int nout = xhi - a.W - LO;  // padding columns [LO, 0) and [W, xhi)
+            for (int rr = warp; rr < XR; rr += 8) {  // a warp per row
+                const int sr = pad_src32(bd.vr0 + rr, a.H, a.pad);
+                uint16_t *srow = xs + rr * XP + XO;
+                if (sr < 0) {  // a zero-padding row (not copied)
+                    for (int v = lane; v < a.W / 8; v += 32) reinterpret_cast<uint4 *>(srow)[v] = make_uint4(0, 0, 0, 0);
+                }
+                const uint16_t *xrow = xp + (int64_t)min(max(sr, 0), a.H - 1) * a.W;
+                for (int u = lane; u < nout; u += 32) {
+                    const int xc = u < -LO ? LO + u : a.W + (u + LO);
+                    const int sc = pad_src32(xc, a.W, a.pad);
+                    srow[xc] = (sr < 0 || sc < 0) ? (uint16_t)0 : xrow[min(sc, a.W - 1)];
+                }
+            }
+            const int gz0 = bd.nflat, gz1 = bd.gsh + ((bd.m1 - bd.my0 + PY - 1) / PY) * PY * a.Wo + 16 * PX;
+            for (int i = gz0 + tid; i < min(gz1, GP); i += 256) gs[i] = 0;
+        }
+        __syncthreads();
+        // the next task's copies into the other buffer (its readers finished last iteration)
+        if (warp == 0 && task + gridDim.x < a.ntasks) issue(task + gridDim.x, buf ^ 1);
+        // K blocks of the band: (period row iy, x-block xb), warp-strided
+        int iy = 0, xb = warp;  // blocks (iy, xb) = warp, warp + 8, ... in row-major order
+        while (xb >= nxb) xb -= nxb, ++iy;
+        for (; iy < yper && bd.my0 + iy * PY < a.Ho;) {
+            const uint16_t *ga = gs + bd.gsh + iy * PY * a.Wo + xb * 16 * PX;
+            const uint16_t *xb_ = xs + iy * QY * XP + xb * 16 * QX;
+            uint32_t af[MT][4];
+            const bool rows_ok = bd.my0 + iy * PY + PY <= a.Ho;
+            if (xb + 1 < nxb && rows_ok) {
+#pragma unroll
+                for (int i = 0; i < MT; ++i) {
+                    const uint16_t *p0 = ga + abase[2 * i], *p1 = ga + abase[2 * i + 1];
+                    af[i][0] = (uint32_t)p0[0] | ((uint32_t)p0[PX] << 16);
+                    af[i][1] = (uint32_t)p1[0] | ((uint32_t)p1[PX] << 16);
+                    af[i][2] = (uint32_t)p0[8 * PX] | ((uint32_t)p0[9 * PX] << 16);
+                    af[i][3] = (uint32_t)p1[8 * PX] | ((uint32_t)p1[9 * PX] << 16);
+                }
+            } else {  // a row's last block or the plane's last period row: zeros past Wo / Ho
+                const int cmax = a.Wo - xb * 16 * PX;               // valid columns from the block's first
+                const int rmax = a.Ho - (bd.my0 + iy * PY);         // valid rows of the period row
+#pragma unroll
+                for (int i = 0; i < MT; ++i) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        int m = gq + 8 * (2 * i + h);
+                        m = m < MP ? m : 0;
+                        const int cb = (m % PX) + 2 * tq * PX;  // column of element k = 2t
+                        const bool row_in = (m / PX) < rmax;
+                        const uint16_t *p = ga + abase[2 * i + h];
+                        auto ld = [&](int koff) -> uint32_t {
+                            return row_in && cb + koff * PX < cmax ? (uint32_t)p[koff * PX] : 0u;
+                        };
+                        af[i][h] = ld(0) | (ld(1) << 16);
+                        af[i][2 + h] = ld(8) | (ld(9) << 16);
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) {
+                const uint16_t *q = xb_ + bbase[j];
+                const uint32_t bf[2] = {(uint32_t)q[0] | ((uint32_t)q[QX] << 16),
+                                        (uint32_t)q[8 * QX] | ((uint32_t)q[9 * QX] << 16)};
+#pragma unroll
+                for (int i = 0; i < MT; ++i) mma16816<T>(d[i][j], af[i], bf);
+            }
+            xb += 8;
+            while (xb >= nxb) xb -= nxb, ++iy;
+        }
+        __syncthreads();  // this buffer's readers are done before its next copies
+    }
+    // the warps' accumulators into the CTA table (C layout: rows g, g + 8; columns 2t, 2t + 1)
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) {
+            float *r0 = dsum + (16 * i + gq) * (NTL * 8) + 8 * j + 2 * tq;
+            float *r1 = r0 + 8 * (NTL * 8);
+            atomicAdd(r0, d[i][j][0]);
+            atomicAdd(r0 + 1, d[i][j][1]);
+            atomicAdd(r1, d[i][j][2]);
+            atomicAdd(r1 + 1, d[i][j][3]);
+        }
+    __syncthreads();
+    for (int idx = tid; idx < PY * PX * NT * NT; idx += 256) {
+        const int tx = idx % NT, ty = (idx / NT) % NT, jx = (idx / (NT * NT)) % PX, jy = idx / (NT * NT * PX);
+        const int m = jy * PX + jx, n = (WgPhase<PY, QY>::base(jy) + ty) * LW + WgPhase<PX, QX>::base(jx) + tx;
+        atomicAdd(&a.gw[idx], dsum[m * (NTL * 8) + n]);
+    }
+}
+
+int launch_wgrad_mma(int dtype, const WgradArgs &a, int grid, int smem, void *stream);
+
 // The compiled (PY/QY, PX/QX, taps) entries of the row-blocked weight gradient.
 #define FCFS_WG_ROWS(Y) Y(5, 3, 4) Y(5, 3, 2) Y(3, 2, 4) Y(3, 2, 2) Y(2, 3, 4) Y(2, 3, 2) Y(3, 5, 4) Y(3, 5, 2)
 
@@ -358,6 +590,25 @@ int launch_wgrad_rows(int dtype, const WgradArgs &a, int grid, int smem, void *s
     FCFS_WG_ROWS(FCFS_WG_PICK)
 #undef FCFS_WG_PICK
     if (!fn) return (int)cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return (int)e;
+    WgradArgs local = a;
+    void *args[] = {&local};
+    e = cudaLaunchKernel(fn, dim3(grid), dim3(256), args, (size_t)smem, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return (int)e;
+    count_launch();
+    return (int)cudaGetLastError();
+}
+
+int launch_wgrad_mma(int dtype, const WgradArgs &a, int grid, int smem, void *stream) {
+    const void *fn = nullptr;
+#define FCFS_WG_MMA(P, Q, N)                                                                                      \
+    if (a.py == P && a.qy == Q && a.px == P && a.qx == Q && a.ntx == N)                                           \
+        fn = dtype == FCFS_F16 ? reinterpret_cast<const void *>(&fcfs_wgrad_mma_kernel<__half, P, Q, P, Q, N>)    \
+                               : reinterpret_cast<const void *>(&fcfs_wgrad_mma_kernel<__nv_bfloat16, P, Q, P, Q, N>);
+    FCFS_WG_ROWS(FCFS_WG_MMA)
+#undef FCFS_WG_MMA
+    if (!fn || dtype == FCFS_F32) return (int)cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return (int)e;
     WgradArgs local = a;

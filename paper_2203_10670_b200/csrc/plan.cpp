@@ -1369,6 +1369,33 @@ fcfs_status fcfs_run_weight_grad(fcfs_plan_t pl, const void *x, const void *grad
     }
     a.npairs = a.py * a.px;
     const int span_x = fx_max + a.ntx - a.fx_min, span_y = fy_max + a.nty - a.fy_min;
+    // 16-bit data: the tensor-core kernel (mma.sync over 16 x-periods per K block)
+    if (!rows1 && pl->D == 1 && a.ntx == a.nty && pl->dtype != FCFS_F32 && !std::getenv("FCFS_NO_WGRAD_MMA") &&
+        (pl->W * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+        wgrad_rows_available(a.py, a.qy, a.px, a.qx, a.ntx) && a.py * a.px <= 32) {
+        WgradArgs b = a;
+        const int nxp = (b.Wo + b.px - 1) / b.px, nxb = (nxp + 15) / 16;
+        const int lh = pl->taby.base[b.py - 1] + b.nty, lw = pl->tab.base[b.px - 1] + b.ntx;
+        if (lh * lw <= 64) {
+            int br = std::max(b.py, 40 / b.py * b.py);  // band rows: a multiple of py
+            b.grows = br;
+            b.xrows = (br / b.py - 1) * b.qy + lh;
+            b.xcols = ((8 + (nxb * 16 - 1) * b.qx + lw + 8) + 7) / 8 * 8;
+            // the flat grad_out span (+ the 16-B alignment room and the last block's reads
+            // past the span: at most 16 periods)
+            b.gcols = (br * b.Wo + 8 + 16 * b.px + 16 + 7) / 8 * 8;
+            const int mt = (b.py * b.px + 15) / 16, ntl = (lh * lw + 7) / 8;
+            // two buffers of (x tile, grad_out span) for the bulk copies of the next task
+            const int64_t smem = 128 + 2 * 2 * ((int64_t)b.xrows * b.xcols + (int64_t)b.gcols) + 4 * mt * 16 * ntl * 8;
+            const int64_t nbands = (b.Ho + br - 1) / br;
+            b.ntasks = b.planes * nbands;
+            if (smem <= 110 * 1024 && b.ntasks < INT32_MAX && (b.W * 2) % 16 == 0) {
+                const int per_sm = std::max(1, std::min(4, (int)((227 * 1024) / (smem + 1024))));
+                const int grid = (int)std::min<int64_t>(b.ntasks, (int64_t)pl->sm_count * per_sm);
+                return launch_wgrad_mma(pl->dtype, b, grid, (int)smem, stream) == 0 ? FCFS_OK : FCFS_E_CUDA;
+            }
+        }
+    }
     // the row-blocked kernel: 2D isotropic plans with a compiled entry, tiles in ~100 KB
     if (!rows1 && pl->D == 1 && a.ntx == a.nty && !std::getenv("FCFS_NO_WGRAD_ROWS") &&
         (pl->W * esize(pl->dtype)) % 16 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
