@@ -347,7 +347,7 @@ def kernel_name(L):
         return "fused_adjoint (+ border bands for replicate/reflect)"
     if L["cfg"].wgrad:
         return "weight_grad"
-    return L["plan"].kernel
+    return L["plan"].launch_info(L["cfg"].N)["kernel"]  # the variant fcfs_run launches (fused_plane, ...)
 
 
 def make_plan(fc, cfg):

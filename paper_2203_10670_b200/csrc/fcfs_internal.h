@@ -230,4 +230,30 @@ int launch_fused(const FusedVariant *v, const FusedArgs &a, int grid, int block,
 constexpr int kFusedConsumerWarps = 8;
 constexpr int kFusedThreads = 32 * (2 + kFusedConsumerWarps);  // issuer warp, padding warp, consumers
 
+// Plane-resident fused kernel (plane.cuh): batches of small 2D planes, a whole
+// padded input plane per TMA box, one warp per band of y-periods across the
+// full output width (at most 32 column chunks).
+constexpr int kPlaneConsumerWarps = 8;  // 16 warps per SM at two CTAs (<= 128 registers per thread)
+constexpr int kPlaneThreads = 32 * kPlaneConsumerWarps;   // every warp computes; no producer warp
+struct PlaneArgs {
+    // 3D tiled TMA descriptor of the input (columns, rows, planes), box (BW, BH, 1);
+    // a box starts at column -16/esize and row row_lo (out of bounds: zero fill)
+    alignas(64) CUtensorMap tmap;
+    void *out;
+    int64_t out_plane_stride;  // elements between output planes (= Ho * Wo)
+    int32_t planes, H, W, Ho, Wo, pad;
+    int32_t BW, BH;            // plane buffer: row pitch (elements), rows
+    int32_t row_lo;            // virtual row of buffer row 0 (the first window row, <= 0)
+    int32_t plane_bytes;       // bytes of one plane buffer (128-B multiple)
+    int32_t nch;               // column chunks per output row (<= 32: one lane each)
+    int32_t nper;              // y-periods per plane
+    int32_t nunits;            // units of U periods (bands start at unit boundaries)
+    int32_t slot_bytes;        // one staging slot (a y-period's rows + spill, 16-B multiple)
+    int32_t lpad, rpad;        // margin columns the kept outputs read (left of 0 / from W on)
+    int32_t tpad, bpad;        // margin rows the kept outputs read (above 0 / from H on)
+};
+// The plane-resident variant of the 2D layer (py/qy, px/qx) with ntaps taps, or nullptr.
+const FusedVariant *plane_lookup(int dtype, int py, int qy, int px, int qx, int ntaps);
+int launch_plane(const FusedVariant *v, const PlaneArgs &a, int grid, int smem, void *stream);
+
 }  // namespace fcfs

@@ -23,3 +23,6 @@
 #define FCFS_Z_X(X) FCFS_Z_PAIRS(X##_Z)
 // adjoint (backward pass) of isotropic 2D layers
 #define FCFS_ADJ_X(X) FCFS_NONUNIT_PAIRS(X##_ADJ)
+// plane-resident kernel (plane.cuh): isotropic pairs for batches of small planes
+#define FCFS_PLANE_PAIRS(Y) \
+    Y(2, 1) Y(3, 2) Y(4, 3) Y(5, 3) Y(5, 4) Y(7, 5) Y(1, 2) Y(2, 3) Y(3, 4) Y(3, 5) Y(4, 5) Y(5, 7)

@@ -16,6 +16,16 @@ extern const FusedVariant kFusedVariants_f16_iso[], kFusedVariants_f16_w[], kFus
 extern const FusedVariant kFusedVariants_bf16_iso[], kFusedVariants_bf16_w[], kFusedVariants_bf16_h[],
     kFusedVariants_bf16_z[];
 extern const FusedVariant kFusedVariants_f32_adj[], kFusedVariants_f16_adj[], kFusedVariants_bf16_adj[];
+extern const FusedVariant kPlaneVariants_f32[], kPlaneVariants_f16[], kPlaneVariants_bf16[];
+
+// The plane-resident variant (plane.cuh) of the 2D layer (py/qy, px/qx): exact factors.
+const FusedVariant *plane_lookup(int dtype, int py, int qy, int px, int qx, int ntaps) {
+    const FusedVariant *sets[3] = {kPlaneVariants_f32, kPlaneVariants_f16, kPlaneVariants_bf16};
+    if (dtype < 0 || dtype > 2) return nullptr;
+    for (const FusedVariant *v = sets[dtype]; v->fn; ++v)
+        if (v->PY == py && v->QY == qy && v->PX == px && v->QX == qx && v->TAPS == ntaps) return v;
+    return nullptr;
+}
 
 // The adjoint (backward pass) variant of the 2D layer (py/qy, px/qx): exact factors.
 const FusedVariant *fused_lookup_adjoint(int dtype, int py, int qy, int px, int qx, int ntaps) {
@@ -62,6 +72,24 @@ int launch_fused(const FusedVariant *v, const FusedArgs &a, int grid, int block,
     FusedArgs local = a;
     void *args[] = {&local};
     return launch_pdl(v->fn, grid, block, args, smem, stream);
+}
+
+int launch_plane(const FusedVariant *v, const PlaneArgs &a, int grid, int smem, void *stream) {
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> configured;  // (fn, device)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!configured.count({v->fn, dev})) {
+            cudaError_t e = cudaFuncSetAttribute(v->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+            if (e != cudaSuccess) return (int)e;
+            configured.insert({v->fn, dev});
+        }
+    }
+    PlaneArgs local = a;
+    void *args[] = {&local};
+    return launch_pdl(v->fn, grid, kPlaneThreads, args, smem, stream);
 }
 
 int launch_pdl(const void *fn, int grid, int block, void **args, int smem, void *stream) {

@@ -36,6 +36,7 @@ struct fcfs_plan_s {
     PhaseTable tab, taby, tabz;  // per-dimension phase tables: W, H, D
     int kernel;  // 0 reference, 1 nearest, 2 fused, 3 tiled
     const FusedVariant *fused;
+    const FusedVariant *plane;  // plane-resident variant of `fused` (2D planes), or nullptr
     int device;
     int64_t rows_ref;
     int sm_count;
@@ -164,6 +165,7 @@ bool ranges_overlap(const void *a, int64_t na, const void *b, int64_t nb) {
 // ---------------------------------------------------------------- fused launch geometry
 struct FusedLaunch {
     FusedArgs a;
+    PlaneArgs pa;  // the plane-resident kernel (select_kernel returns 4)
     int grid, smem;
     char desc[768];
 };
@@ -386,6 +388,104 @@ bool plan_fused(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L, const F
     return true;
 }
 
+// Plane-resident geometry (plane.cuh): whole 2D planes of a batch (g after
+// slices are folded into planes), each padded input plane one TMA box of at
+// most 256 x 256 elements, at most 32 column chunks per output row, two CTAs
+// per SM.  False: the row-pipelined fused kernel runs.
+bool plan_plane(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
+    const FusedVariant *v = pl->plane;
+    if (!v || pl->is1d || g.D != 1 || g.Do != 1 || std::getenv("FCFS_NO_PLANE")) return false;
+    if (g.in_row0 != 0 || g.in_nrows != g.H || g.out_row0 != 0 || g.out_nrows != g.Ho) return false;
+    if (g.in_plane_stride != g.H * g.W || g.out_plane_stride != g.Ho * g.Wo) return false;
+    const int ESZ = esize(pl->dtype), A = 16 / ESZ;
+    if ((g.W * ESZ) % 16 != 0 || (reinterpret_cast<uintptr_t>(g.in) & 15) != 0) return false;
+    // at least two CTAs per SM, and planes of at least 16 KB: on smaller ones
+    // (bf16 64^2) the per-plane and per-band costs outweigh the gain
+    // (tools/plane_ab.py: 128^2 bf16 0.59-0.92x the row-pipelined kernel's
+    // time, 64^2 bf16 0.66-1.45x); FCFS_DEBUG_PLANE_MIN (tests) lowers both bars
+    int64_t min_planes = 2LL * pl->sm_count, min_bytes = 16384;
+    if (const char *e = std::getenv("FCFS_DEBUG_PLANE_MIN")) min_planes = std::atoll(e), min_bytes = 0;
+    if (g.planes < min_planes || g.planes > INT32_MAX / 2 || g.H * g.W * ESZ < min_bytes) return false;
+    const int *geo = v->geo;
+    const int PY = geo[0], QY = geo[1], TY = geo[2], LOY = geo[3];
+    const int PX = geo[4], QX = geo[5], TX = geo[6], LOX = geo[7];
+    const int K = v->K, KP = K * PX;
+    int HIy = -(1 << 30), HIx = -(1 << 30);
+    for (int j = 0; j < PY; ++j) HIy = std::max(HIy, geo[8 + j] + TY - 1 + LOY);
+    for (int j = 0; j < PX; ++j) HIx = std::max(HIx, geo[24 + j] + TX - 1 + LOX);
+    const int Ly = HIy - LOY + 1, Lx = HIx - LOX + 1;
+    PlaneArgs &a = L.pa;
+    std::memset(&a, 0, sizeof(a));
+    a.out = g.out;
+    a.out_plane_stride = g.out_plane_stride;
+    a.planes = (int32_t)g.planes;
+    a.H = (int32_t)g.H;
+    a.W = (int32_t)g.W;
+    a.Ho = (int32_t)g.Ho;
+    a.Wo = (int32_t)g.Wo;
+    a.pad = pl->pad;
+    a.nch = (int32_t)((g.Wo + KP - 1) / KP);
+    if (a.nch > 32) return false;
+    a.nper = (int32_t)((g.Ho + PY - 1) / PY);
+    const int R = QY * ((Ly + QY - 1) / QY), U = R / QY;
+    a.nunits = (a.nper + U - 1) / U;
+    a.row_lo = LOY;
+    a.BH = QY * (a.nper - 1) + Ly;  // window rows of every period, the last one's included
+    const int WIN = (K - 1) * QX + Lx;
+    const int64_t col_end = (int64_t)(a.nch - 1) * K * QX + LOX + WIN;  // one past the last column any lane reads
+    a.BW = (int32_t)((A + col_end + A - 1) / A * A);
+    if (a.BW > 256 || a.BH > 256) return false;
+    a.plane_bytes = (a.BW * a.BH * ESZ + 127) / 128 * 128;
+    const int64_t rowb = g.Wo * ESZ;
+    a.slot_bytes = (int32_t)((16 + PY * rowb + KP * ESZ + 15) / 16 * 16);
+    L.smem = 256 + 2 * a.plane_bytes + 2 * kPlaneConsumerWarps * a.slot_bytes;
+    if (L.smem > 112 * 1024) return false;  // two CTAs per SM
+    // margins the kept outputs read (written by the producer for replicate / reflect)
+    const int64_t reach_x = ((g.Wo - 1) / PX) * QX + LOX + geo[24 + (int)((g.Wo - 1) % PX)] + TX;
+    const int64_t reach_y = ((g.Ho - 1) / PY) * QY + LOY + geo[8 + (int)((g.Ho - 1) % PY)] + TY;
+    a.lpad = pl->pad == FCFS_PAD_ZERO ? 0 : -LOX;
+    a.rpad = pl->pad == FCFS_PAD_ZERO ? 0 : (int32_t)std::max<int64_t>(0, reach_x - g.W);
+    a.tpad = pl->pad == FCFS_PAD_ZERO ? 0 : -LOY;
+    a.bpad = pl->pad == FCFS_PAD_ZERO ? 0 : (int32_t)std::max<int64_t>(0, reach_y - g.H);
+    if (a.lpad > A || g.W + a.rpad > a.BW - A || g.H + a.bpad - a.row_lo > a.BH) return false;
+    L.grid = (int)std::min<int64_t>(g.planes, 2LL * pl->sm_count);
+    if (const char *e = std::getenv("FCFS_DEBUG_GRID")) L.grid = std::max(1, std::min(L.grid, std::atoi(e)));
+    if (g.in) {
+        static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+        static bool tried = false;
+        if (!tried) {
+            tried = true;
+            void *fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+                q == cudaDriverEntryPointSuccess)
+                encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+            cudaGetLastError();
+        }
+        if (!encode) return false;
+        const CUtensorMapDataType dt = pl->dtype == FCFS_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                       : pl->dtype == FCFS_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                               : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        cuuint64_t dims[3] = {(cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.planes};
+        cuuint64_t strides[2] = {(cuuint64_t)(g.W * ESZ), (cuuint64_t)(g.H * g.W * ESZ)};
+        cuuint32_t box[3] = {(cuuint32_t)a.BW, (cuuint32_t)a.BH, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        if (encode(&a.tmap, dt, 3, const_cast<void *>(g.in), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    std::snprintf(L.desc, sizeof(L.desc),
+                  "{\"kernel\": \"fused_plane\", \"PY\": %d, \"QY\": %d, \"PX\": %d, \"QX\": %d, \"taps\": %d, "
+                  "\"K\": %d, \"nch\": %d, \"periods\": %d, \"ring_phases\": %d, \"BW\": %d, \"BH\": %d, "
+                  "\"plane_bytes\": %d, \"slot_bytes\": %d, \"bands\": %d, \"grid\": %d, \"block\": %d, "
+                  "\"smem\": %d, \"busy_lanes\": %d, \"pads\": [%d, %d, %d, %d]}",
+                  PY, QY, PX, QX, TX, K, a.nch, a.nper, U, a.BW, a.BH, a.plane_bytes, a.slot_bytes,
+                  kPlaneConsumerWarps, L.grid, kPlaneThreads, L.smem, a.nch, a.tpad, a.bpad, a.lpad, a.rpad);
+    if (std::getenv("FCFS_DEBUG_PRINT")) std::fprintf(stderr, "%s\n", L.desc);
+    return true;
+}
+
 // 1D plans: every row of every plane is an independent signal, so a whole-row
 // run is one plane of planes * H rows (long columns of rows keep the kernels'
 // row bands full however small H is).
@@ -428,6 +528,7 @@ int select_kernel(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
             g2.in_plane_stride = g.in_nrows * pl->W;
             g2.out_plane_stride = g.out_nrows * pl->Wo;
         }
+        if (pl->fused->TZ == 1 && plan_plane(pl, g2, L)) return 4;
         if ((reinterpret_cast<uintptr_t>(g.in) % esize(pl->dtype)) ||
             g2.planes * std::max(g2.D, g2.Do) * std::max(g.in_nrows * pl->W, g.out_nrows * pl->Wo) > INT32_MAX * 16LL || !plan_fused(pl, g2, L))
             kernel = (pl->pz == 1 && pl->qz == 1) ? 3 : 0;  // tiled when the slice factor allows it
@@ -646,6 +747,7 @@ fcfs_status launch(const Prepared &pr, void *stream) {
     int rc = 0;
     if (pr.kernel == 1) rc = launch_nearest(pr.pl->dtype, pr.na, stream);
     else if (pr.kernel == 2) rc = launch_fused(pr.pl->fused, pr.L.a, pr.L.grid, kFusedThreads, pr.L.smem, stream);
+    else if (pr.kernel == 4) rc = launch_plane(pr.pl->plane, pr.L.pa, pr.L.grid, pr.L.smem, stream);
     else if (pr.kernel == 3) rc = launch_tile(pr.pl->dtype, pr.ta, pr.tgrid, pr.tsmem, stream);
     else if (pr.kernel == 0) rc = launch_reference(pr.pl->dtype, pr.ra, stream);
     return rc == 0 ? FCFS_OK : FCFS_E_CUDA;
@@ -735,6 +837,7 @@ fcfs_status make_plan(int rank, const int *pd, const int *qd, int mode, int pad,
     }
     pl->kernel = 0;
     pl->fused = nullptr;
+    pl->plane = nullptr;
     if (!(flags & FCFS_FLAG_FORCE_REFERENCE)) {
         if (mode == FCFS_NEAREST) {
             pl->kernel = 1;
@@ -754,6 +857,18 @@ fcfs_status make_plan(int rank, const int *pd, const int *qd, int mode, int pad,
                     if (std::memcmp(&pl->fused->wtab_y[4 * j + t], &pl->taby.w[j][t], sizeof(float)) != 0)
                         pl->fused = nullptr;
             if (pl->fused) pl->kernel = 2;
+            // batches of small planes: the plane-resident form of the same layer
+            if (pl->fused && !slices && !pl->is1d) {
+                pl->plane = plane_lookup(dtype, pl->py, pl->qy, pl->p, pl->q, pl->tab.ntaps);
+                for (int j = 0; pl->plane && j < pl->p; ++j)
+                    for (int t = 0; t < pl->tab.ntaps; ++t)
+                        if (std::memcmp(&pl->plane->wtab_x[4 * j + t], &pl->tab.w[j][t], sizeof(float)) != 0)
+                            pl->plane = nullptr;
+                for (int j = 0; pl->plane && j < pl->py; ++j)
+                    for (int t = 0; t < pl->taby.ntaps; ++t)
+                        if (std::memcmp(&pl->plane->wtab_y[4 * j + t], &pl->taby.w[j][t], sizeof(float)) != 0)
+                            pl->plane = nullptr;
+            }
         }
         // separable plans without a fused variant: the tiled kernel (2D planes;
         // 3D with a 1/1 slice factor as N*C*D planes)

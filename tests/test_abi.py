@@ -189,6 +189,15 @@ def test_launch_geometry(fc, name):
     c = synth.CONFIGS[name]
     pl = fc.Plan(c.p, c.q, c.mode, c.pad, c.C, c.H, c.W, c.dtype, "floor", c.is1d)
     info = pl.launch_info(c.N)
+    if info["kernel"] == "fused_plane":
+        # batches of small planes (C3): whole padded planes per TMA box, a warp per
+        # band across the full output width, two CTAs per SM
+        assert pl.kernel == "fused_separable"
+        assert info["smem"] <= 112 * 1024 and info["BW"] <= 256 and info["BH"] <= 256
+        assert info["nch"] <= 32 and info["nch"] * info["K"] * info["PX"] >= pl.Wo
+        assert info["grid"] == min(c.N * c.C, 296) and info["block"] == 256
+        assert info["BH"] >= (info["periods"] - 1) * info["QY"] + 1
+        return
     assert info["kernel"] == pl.kernel
     if info["kernel"] != "fused_separable":
         return
