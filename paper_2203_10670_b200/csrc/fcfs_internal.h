@@ -181,6 +181,11 @@ bool nearest_rows_job_ok(const RunGeom &g, int is1d, int qx, int qy, int esz);
 int launch_tile(int dtype, const TileArgs &a, int grid, int smem, void *stream);
 // Weight gradient (k_wgrad.cu): grad_w[jy][jx][ty][tx] over the phases' own taps.
 struct WgradArgs {
+    // tensor-core kernel: 3D tiled TMA descriptor of x (columns, rows, planes), box
+    // (xcols, xrows, 1) starting at column -8 (out-of-bounds zero fill)
+    alignas(64) CUtensorMap tmap_x;
+    int lpad, rpad, tpad, bpad;    // margin columns / rows kept outputs read (replicate / reflect)
+    int nbuf;                      // tile buffers (tasks in flight + 1), 2..4
     const void *x, *g;
     float *gw;
     int64_t planes;

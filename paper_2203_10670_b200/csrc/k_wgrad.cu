@@ -355,6 +355,15 @@ __global__ void __launch_bounds__(256, 2) fcfs_wgrad_rows_kernel(const __grid_co
 // nothing.  The warps' accumulators are summed in shared memory and each
 // weight takes one global atomic per CTA.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void wg_tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                               uint64_t *bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
 template <typename T>
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
     if constexpr (std::is_same<T, __nv_bfloat16>::value)
@@ -379,33 +388,27 @@ __global__ void __launch_bounds__(256) fcfs_wgrad_mma_kernel(const __grid_consta
     constexpr int NN = LH * LW, NTL = (NN + 7) / 8;    // window positions, N tiles
     constexpr int XO = 8;                              // tile column of input column 0 (16-B aligned rows)
     static_assert(MT <= 2 && NTL <= 8, "tensor-core weight gradient: <= 32 phases, <= 64 window positions");
-    // shared memory: [0, 64) two mbarriers; two tile buffers of (x tile, flat grad_out span); the CTA's sums
+    // shared memory: [0, 128) nbuf mbarriers; nbuf tile buffers of (x tile, flat grad_out span) -- the
+    // tasks in flight: a buffer's copies are issued nbuf - 1 tasks ahead --; the CTA's sums
     extern __shared__ __align__(128) unsigned char wsm_raw[];
     const int XR = a.xrows, XP = a.xcols, GP = a.gcols, BR = a.grows;
     uint64_t *full = reinterpret_cast<uint64_t *>(wsm_raw);
-    const int bufb = (XR * XP + GP) * 2;  // bytes per buffer (16-B multiple: host)
+    const int bufb = (XR * XP + GP) * 2;  // bytes per buffer (128-B multiple: host)
     auto xs_of = [&](int buf) { return reinterpret_cast<uint16_t *>(wsm_raw + 128 + buf * bufb); };
     auto gs_of = [&](int buf) { return xs_of(buf) + XR * XP; };
-    float *dsum = reinterpret_cast<float *>(wsm_raw + 128 + 2 * bufb);  // [MT * 16][NTL * 8]
+    const int NB = a.nbuf;
+    float *dsum = reinterpret_cast<float *>(wsm_raw + 128 + NB * bufb);  // [MT * 16][NTL * 8]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int gq = lane >> 2, tq = lane & 3;
     const int nxp = (a.Wo + PX - 1) / PX, nxb = (nxp + 15) / 16;
     const int yper = BR / PY;  // period rows per band
-    const int xhi = (nxb * 16 - 1) * QX + LW + LO;  // one past the last input column any block reads
     const int nbands = (a.Ho + BR - 1) / BR;
     const T *gend = static_cast<const T *>(a.g) + a.planes * (int64_t)a.Ho * a.Wo;
     if (tid == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
+        for (int b = 0; b < NB; ++b) mbar_init(&full[b], 1);
         mbar_fence_init();
     }
     for (int i = tid; i < MT * 16 * NTL * 8; i += 256) dsum[i] = 0.0f;
-    // columns past the padded window region never change: zeros, once
-    for (int buf = 0; buf < 2; ++buf)
-        for (int i = tid; i < XR * (XP - (XO + xhi)); i += 256) {
-            const int rr = i / (XP - (XO + xhi)), cc = XO + xhi + (i - rr * (XP - (XO + xhi)));
-            xs_of(buf)[rr * XP + cc] = 0;
-        }
     __syncthreads();
     struct Band {
         int64_t plane;
@@ -413,8 +416,9 @@ __global__ void __launch_bounds__(256) fcfs_wgrad_mma_kernel(const __grid_consta
     };
     auto band = [&](int64_t task) {
         Band bd;
-        bd.plane = task / nbands;
-        bd.my0 = (int)(task - bd.plane * nbands) * BR;
+        const int t32 = (int)task;  // tasks < 2^31 (host)
+        bd.plane = t32 / nbands;
+        bd.my0 = (t32 - (int)bd.plane * nbands) * BR;
         bd.vr0 = (bd.my0 / PY) * QY + LO;
         bd.m1 = min(a.Ho, bd.my0 + BR);
         const T *gspan = static_cast<const T *>(a.g) + (bd.plane * a.Ho + bd.my0) * (int64_t)a.Wo;
@@ -425,34 +429,37 @@ __global__ void __launch_bounds__(256) fcfs_wgrad_mma_kernel(const __grid_consta
         bd.nflat = (int)min(want, avail / 8 * 8);
         return bd;
     };
-    // warp 0: the bulk copies of a task's tiles into a buffer (image rows, lane per
-    // row; the grad_out span, lane 0)
+    // one thread: a task's x tile (ONE 3D TMA box: out-of-bounds zero fill = zero
+    // padding) and its grad_out span (one bulk copy) into a buffer
     auto issue = [&](int64_t task, int buf) {
-        fence_proxy_async_smem();  // the buffer's earlier generic writes (padding, zeros) before the copies
+        fence_proxy_async_smem();  // the buffer's earlier generic writes (margins, zeros) before the copies
         const Band bd = band(task);
-        const T *xp = static_cast<const T *>(a.x) + bd.plane * (int64_t)a.H * a.W;
-        uint32_t bytes = lane == 0 ? (uint32_t)bd.nflat * 2 : 0u;
-        for (int rr = lane; rr < XR; rr += 32) bytes += pad_src32(bd.vr0 + rr, a.H, a.pad) >= 0 ? (uint32_t)a.W * 2 : 0u;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
-        if (lane == 0) mbar_arrive_expect_tx(&full[buf], bytes);
-        __syncwarp();
         const uint64_t pol = policy_evict_first();
-        for (int rr = lane; rr < XR; rr += 32) {
-            const int sr = pad_src32(bd.vr0 + rr, a.H, a.pad);
-            if (sr >= 0) bulk_g2s(xs_of(buf) + rr * XP + XO, xp + (int64_t)min(sr, a.H - 1) * a.W, (uint32_t)a.W * 2, &full[buf], pol);
-        }
+        mbar_arrive_expect_tx(&full[buf], (uint32_t)(XR * XP * 2 + bd.nflat * 2));
+        wg_tma_load_3d(xs_of(buf), &a.tmap_x, -XO, bd.vr0, (int)bd.plane, &full[buf], pol);
         const T *gspan = static_cast<const T *>(a.g) + (bd.plane * a.Ho + bd.my0) * (int64_t)a.Wo;
-        if (lane == 0 && bd.nflat > 0) bulk_g2s(gs_of(buf), gspan - bd.gsh, (uint32_t)bd.nflat * 2, &full[buf], pol);
+        if (bd.nflat > 0) bulk_g2s(gs_of(buf), gspan - bd.gsh, (uint32_t)bd.nflat * 2, &full[buf], pol);
     };
     // per-thread gather bases (element offsets within a block's tiles)
     int abase[2 * MT], bbase[NTL];
+    // A elements of a row's last block past the output width: masked to zero (the
+    // block's other periods multiply finite x values)
+    uint32_t amask[MT][4];
 #pragma unroll
     for (int i = 0; i < 2 * MT; ++i) {
         int m = gq + 8 * i;
         m = m < MP ? m : 0;  // rows past the phases: any valid element (those rows of D are never read)
         abase[i] = (m / PX) * a.Wo + (m % PX) + 2 * tq * PX;  // the flat span: row pitch Wo
     }
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            int m = gq + 8 * (2 * i + (r & 1));
+            m = m < MP ? m : 0;
+            const int c0 = (nxb - 1) * 16 * PX + (m % PX) + (2 * tq + 8 * (r >> 1)) * PX;  // column of the low half
+            amask[i][r] = (c0 < a.Wo ? 0x0000ffffu : 0u) | (c0 + PX < a.Wo ? 0xffff0000u : 0u);
+        }
 #pragma unroll
     for (int j = 0; j < NTL; ++j) {
         int n = 8 * j + gq;
@@ -466,88 +473,89 @@ __global__ void __launch_bounds__(256) fcfs_wgrad_mma_kernel(const __grid_consta
         for (int j = 0; j < NTL; ++j)
 #pragma unroll
             for (int e = 0; e < 4; ++e) d[i][j][e] = 0.0f;
-    if (warp == 0 && blockIdx.x < a.ntasks) issue(blockIdx.x, 0);
-    uint32_t phase[2] = {0u, 0u};
-    int buf = 0;
-    for (int64_t task = blockIdx.x; task < a.ntasks; task += gridDim.x, buf ^= 1) {
+    if (tid == 0)
+        for (int k = 0; k < NB - 1; ++k)
+            if (blockIdx.x + (int64_t)k * gridDim.x < a.ntasks) issue(blockIdx.x + (int64_t)k * gridDim.x, k);
+    int n = 0;
+    for (int64_t task = blockIdx.x; task < a.ntasks; task += gridDim.x, ++n) {
+        const int buf = n % NB;
         const Band bd = band(task);
-        mbar_wait(&full[buf], phase[buf]);
-        phase[buf] ^= 1u;
+        mbar_wait(&full[buf], (uint32_t)((n / NB) & 1));
         uint16_t *xs = xs_of(buf), *gs = gs_of(buf);
-        // padding: rows past the image (zero / replicate / reflect rows came as copies),
-        // padding columns, the grad_out rows past Ho in the last period row
-        {
-            const uint16_t *xp = reinterpret_cast<const uint16_t *>(static_cast<const T *>(a.x) + bd.plane * (int64_t)a.H * a.W);
-            const int nout = xhi - a.W - LO;  // padding columns [LO, 0) and [W, xhi)
-            for (int rr = warp; rr < XR; rr += 8) {  // a warp per row
-                const int sr = pad_src32(bd.vr0 + rr, a.H, a.pad);
-                uint16_t *srow = xs + rr * XP + XO;
-                if (sr < 0) {  // a zero-padding row (not copied)
-                    for (int v = lane; v < a.W / 8; v += 32) reinterpret_cast<uint4 *>(srow)[v] = make_uint4(0, 0, 0, 0);
-                }
-                const uint16_t *xrow = xp + (int64_t)min(max(sr, 0), a.H - 1) * a.W;
-                for (int u = lane; u < nout; u += 32) {
-                    const int xc = u < -LO ? LO + u : a.W + (u + LO);
-                    const int sc = pad_src32(xc, a.W, a.pad);
-                    srow[xc] = (sr < 0 || sc < 0) ? (uint16_t)0 : xrow[min(sc, a.W - 1)];
-                }
+        // replicate / reflect margins the kept outputs read (§3 Padding): margin
+        // columns of the tile rows holding image rows, and the padding rows
+        if (a.pad != FCFS_PAD_ZERO) {
+            for (int rr = tid; rr < XR; rr += 256) {
+                const int v = bd.vr0 + rr;
+                if (v < 0 || v >= a.H) continue;
+                uint16_t *row = xs + rr * XP + XO;
+                for (int c = -a.lpad; c < 0; ++c) row[c] = row[pad_src32(c, a.W, a.pad)];
+                for (int c = a.W; c < a.W + a.rpad; ++c) row[c] = row[pad_src32(c, a.W, a.pad)];
             }
-            const int gz0 = bd.nflat, gz1 = bd.gsh + ((bd.m1 - bd.my0 + PY - 1) / PY) * PY * a.Wo + 16 * PX;
+            // padding rows, from their source image rows in global memory (a band's
+            // tile need not hold the source row: reflect at the bottom reaches up)
+            const uint16_t *xg = reinterpret_cast<const uint16_t *>(static_cast<const T *>(a.x) + bd.plane * (int64_t)a.H * a.W);
+            auto pad_row = [&](int rr) {
+                uint16_t *row = xs + rr * XP + XO;
+                const uint16_t *src = xg + (int64_t)pad_src32(bd.vr0 + rr, a.H, a.pad) * a.W;
+                for (int c = lane - a.lpad; c < a.W + a.rpad; c += 32) row[c] = src[pad_src32(c, a.W, a.pad)];
+            };
+            // tile rows of virtual rows [-tpad, 0) and [H, H + bpad)
+            for (int rr = max(0, -a.tpad - bd.vr0) + warp; rr < min(XR, -bd.vr0); rr += 8) pad_row(rr);
+            for (int rr = max(0, a.H - bd.vr0) + warp; rr < min(XR, a.H + a.bpad - bd.vr0); rr += 8) pad_row(rr);
+        }
+        if (bd.nflat < bd.gsh + (bd.m1 - bd.my0) * a.Wo) {
+            // the tensor's last elements past its last aligned 16 B (the bulk copy stops there)
+            const uint16_t *gspan = reinterpret_cast<const uint16_t *>(static_cast<const T *>(a.g) +
+                                                                       (bd.plane * a.Ho + bd.my0) * (int64_t)a.Wo);
+            for (int e = bd.nflat + tid; e < bd.gsh + (bd.m1 - bd.my0) * a.Wo; e += 256) gs[e] = gspan[e - bd.gsh];
+        }
+        {   // grad_out past the span (the last period row's rows past Ho -- the aligned copy may
+            // have brought the next plane's first elements there -- and reads past the span): zeros
+            const int gz0 = bd.gsh + (bd.m1 - bd.my0) * a.Wo, gz1 = bd.gsh + ((bd.m1 - bd.my0 + PY - 1) / PY) * PY * a.Wo + 16 * PX;
             for (int i = gz0 + tid; i < min(gz1, GP); i += 256) gs[i] = 0;
         }
         __syncthreads();
-        // the next task's copies into the other buffer (its readers finished last iteration)
-        if (warp == 0 && task + gridDim.x < a.ntasks) issue(task + gridDim.x, buf ^ 1);
-        // K blocks of the band: (period row iy, x-block xb), warp-strided
-        int iy = 0, xb = warp;  // blocks (iy, xb) = warp, warp + 8, ... in row-major order
-        while (xb >= nxb) xb -= nxb, ++iy;
-        for (; iy < yper && bd.my0 + iy * PY < a.Ho;) {
+        // task n + nbuf - 1's copies into the buffer task n - 1 used (its readers are done)
+        if (tid == 0 && task + (int64_t)(NB - 1) * gridDim.x < a.ntasks)
+            issue(task + (int64_t)(NB - 1) * gridDim.x, (n + NB - 1) % NB);
+        // K blocks of the band: (period row iy, x-block xb)
+        const int nrow = min(yper, (bd.m1 - bd.my0 + PY - 1) / PY);
+        const int nblk = nrow * nxb;
+        // this warp's contiguous share of the blocks, walked row by row (no division per block)
+        const int b0 = warp * nblk / 8, b1 = (warp + 1) * nblk / 8;
+        int iy = b0 / nxb, xb = b0 - iy * nxb;
+        for (int blk = b0; blk < b1; ++blk) {
             const uint16_t *ga = gs + bd.gsh + iy * PY * a.Wo + xb * 16 * PX;
             const uint16_t *xb_ = xs + iy * QY * XP + xb * 16 * QX;
             uint32_t af[MT][4];
-            const bool rows_ok = bd.my0 + iy * PY + PY <= a.Ho;
-            if (xb + 1 < nxb && rows_ok) {
 #pragma unroll
-                for (int i = 0; i < MT; ++i) {
-                    const uint16_t *p0 = ga + abase[2 * i], *p1 = ga + abase[2 * i + 1];
-                    af[i][0] = (uint32_t)p0[0] | ((uint32_t)p0[PX] << 16);
-                    af[i][1] = (uint32_t)p1[0] | ((uint32_t)p1[PX] << 16);
-                    af[i][2] = (uint32_t)p0[8 * PX] | ((uint32_t)p0[9 * PX] << 16);
-                    af[i][3] = (uint32_t)p1[8 * PX] | ((uint32_t)p1[9 * PX] << 16);
-                }
-            } else {  // a row's last block or the plane's last period row: zeros past Wo / Ho
-                const int cmax = a.Wo - xb * 16 * PX;               // valid columns from the block's first
-                const int rmax = a.Ho - (bd.my0 + iy * PY);         // valid rows of the period row
-#pragma unroll
-                for (int i = 0; i < MT; ++i) {
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        int m = gq + 8 * (2 * i + h);
-                        m = m < MP ? m : 0;
-                        const int cb = (m % PX) + 2 * tq * PX;  // column of element k = 2t
-                        const bool row_in = (m / PX) < rmax;
-                        const uint16_t *p = ga + abase[2 * i + h];
-                        auto ld = [&](int koff) -> uint32_t {
-                            return row_in && cb + koff * PX < cmax ? (uint32_t)p[koff * PX] : 0u;
-                        };
-                        af[i][h] = ld(0) | (ld(1) << 16);
-                        af[i][2 + h] = ld(8) | (ld(9) << 16);
-                    }
-                }
+            for (int i = 0; i < MT; ++i) {
+                const uint16_t *p0 = ga + abase[2 * i], *p1 = ga + abase[2 * i + 1];
+                af[i][0] = __byte_perm(p0[0], p0[PX], 0x5410);
+                af[i][1] = __byte_perm(p1[0], p1[PX], 0x5410);
+                af[i][2] = __byte_perm(p0[8 * PX], p0[9 * PX], 0x5410);
+                af[i][3] = __byte_perm(p1[8 * PX], p1[9 * PX], 0x5410);
             }
+            if (xb == nxb - 1) {  // a row's last block: columns past Wo are zero
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) af[i][r] &= amask[i][r];
+            }
+            if (++xb == nxb) xb = 0, ++iy;
 #pragma unroll
             for (int j = 0; j < NTL; ++j) {
                 const uint16_t *q = xb_ + bbase[j];
-                const uint32_t bf[2] = {(uint32_t)q[0] | ((uint32_t)q[QX] << 16),
-                                        (uint32_t)q[8 * QX] | ((uint32_t)q[9 * QX] << 16)};
+                const uint32_t bf[2] = {__byte_perm(q[0], q[QX], 0x5410), __byte_perm(q[8 * QX], q[9 * QX], 0x5410)};
 #pragma unroll
                 for (int i = 0; i < MT; ++i) mma16816<T>(d[i][j], af[i], bf);
             }
-            xb += 8;
-            while (xb >= nxb) xb -= nxb, ++iy;
         }
-        __syncthreads();  // this buffer's readers are done before its next copies
+        // (no barrier here: the next task's barrier also orders this task's reads
+        // before the copies that reuse this buffer, issued after it)
     }
+    __syncthreads();
     // the warps' accumulators into the CTA table (C layout: rows g, g + 8; columns 2t, 2t + 1)
 #pragma unroll
     for (int i = 0; i < MT; ++i)

@@ -1491,24 +1491,68 @@ fcfs_status fcfs_run_weight_grad(fcfs_plan_t pl, const void *x, const void *grad
         WgradArgs b = a;
         const int nxp = (b.Wo + b.px - 1) / b.px, nxb = (nxp + 15) / 16;
         const int lh = pl->taby.base[b.py - 1] + b.nty, lw = pl->tab.base[b.px - 1] + b.ntx;
-        if (lh * lw <= 64) {
-            int br = std::max(b.py, 40 / b.py * b.py);  // band rows: a multiple of py
+        const int LOw = pl->tab.lo;
+        // band rows (a multiple of py) and tile buffers: ~80 rows with as many buffers as
+        // fit (up to 4), else ~40 (C3W: 80 rows x 2 buffers 194 us, 40 x 4 271 us -- the
+        // per-task cost dominates)
+        for (int want : {80, 40}) {
+            if (lh * lw > 64) break;
+            int br = std::max(b.py, want / b.py * b.py);
             b.grows = br;
             b.xrows = (br / b.py - 1) * b.qy + lh;
-            b.xcols = ((8 + (nxb * 16 - 1) * b.qx + lw + 8) + 7) / 8 * 8;
+            b.xcols = ((8 + (nxb * 16 - 1) * b.qx + lw + 8) + 7) / 8 * 8;  // = the TMA box width
             // the flat grad_out span (+ the 16-B alignment room and the last block's reads
-            // past the span: at most 16 periods)
+            // past the span: at most 16 periods); a buffer is a 128-B multiple
             b.gcols = (br * b.Wo + 8 + 16 * b.px + 16 + 7) / 8 * 8;
+            while (((int64_t)b.xrows * b.xcols + b.gcols) * 2 % 128) b.gcols += 8;
             const int mt = (b.py * b.px + 15) / 16, ntl = (lh * lw + 7) / 8;
-            // two buffers of (x tile, grad_out span) for the bulk copies of the next task
-            const int64_t smem = 128 + 2 * 2 * ((int64_t)b.xrows * b.xcols + (int64_t)b.gcols) + 4 * mt * 16 * ntl * 8;
+            const int64_t bufb = 2 * ((int64_t)b.xrows * b.xcols + (int64_t)b.gcols), dsb = 4 * mt * 16 * ntl * 8;
+            b.nbuf = (int)std::min<int64_t>(4, (110 * 1024 - 128 - dsb) / bufb);
+            if (const char *e = std::getenv("FCFS_DEBUG_WG_NBUF")) b.nbuf = std::max(2, std::min(b.nbuf, std::atoi(e)));
+            if (b.nbuf < 2) continue;
+            const int64_t smem = 128 + b.nbuf * bufb + dsb;
             const int64_t nbands = (b.Ho + br - 1) / br;
             b.ntasks = b.planes * nbands;
-            if (smem <= 110 * 1024 && b.ntasks < INT32_MAX && (b.W * 2) % 16 == 0) {
-                const int per_sm = std::max(1, std::min(4, (int)((227 * 1024) / (smem + 1024))));
-                const int grid = (int)std::min<int64_t>(b.ntasks, (int64_t)pl->sm_count * per_sm);
-                return launch_wgrad_mma(pl->dtype, b, grid, (int)smem, stream) == 0 ? FCFS_OK : FCFS_E_CUDA;
+            if (smem > 110 * 1024 || b.ntasks >= INT32_MAX || b.xcols > 256 || b.xrows > 256) continue;
+            // margins the kept outputs read (replicate / reflect; zero padding = the box's fill)
+            const int64_t reach_x = ((b.Wo - 1) / b.px) * b.qx + pl->tab.base[(b.Wo - 1) % b.px] + LOw + b.ntx;
+            const int64_t reach_y = ((b.Ho - 1) / b.py) * b.qy + pl->taby.base[(b.Ho - 1) % b.py] + pl->taby.lo + b.nty;
+            b.lpad = pl->pad == FCFS_PAD_ZERO ? 0 : -LOw;
+            b.rpad = pl->pad == FCFS_PAD_ZERO ? 0 : (int)std::max<int64_t>(0, reach_x - b.W);
+            b.tpad = pl->pad == FCFS_PAD_ZERO ? 0 : -pl->taby.lo;
+            b.bpad = pl->pad == FCFS_PAD_ZERO ? 0 : (int)std::max<int64_t>(0, reach_y - b.H);
+            if (b.rpad > 8 || b.lpad > 8) continue;  // margins inside the tile's 16-B side groups
+            static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+            static bool tried = false;
+            if (!tried) {
+                tried = true;
+                void *fn = nullptr;
+                cudaDriverEntryPointQueryResult q;
+                if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+                    q == cudaDriverEntryPointSuccess)
+                    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+                cudaGetLastError();
             }
+            if (!encode) break;
+            const CUtensorMapDataType dt =
+                pl->dtype == FCFS_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+            cuuint64_t dims[3] = {(cuuint64_t)b.W, (cuuint64_t)b.H, (cuuint64_t)b.planes};
+            cuuint64_t strides[2] = {(cuuint64_t)(b.W * 2), (cuuint64_t)((int64_t)b.H * b.W * 2)};
+            cuuint32_t box[3] = {(cuuint32_t)b.xcols, (cuuint32_t)b.xrows, 1};
+            cuuint32_t estr[3] = {1, 1, 1};
+            if (encode(&b.tmap_x, dt, 3, const_cast<void *>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                break;
+            const int per_sm = std::max(1, std::min(4, (int)((227 * 1024) / (smem + 1024))));
+            const int grid = (int)std::min<int64_t>(b.ntasks, (int64_t)pl->sm_count * per_sm);
+            char d[256];
+            std::snprintf(d, sizeof(d),
+                          "{\"kernel\": \"weight_grad_tensor_core\", \"band_rows\": %d, \"buffers\": %d, \"grid\": %d, "
+                          "\"smem\": %lld}",
+                          br, b.nbuf, grid, (long long)smem);
+            note_launch(d);
+            return launch_wgrad_mma(pl->dtype, b, grid, (int)smem, stream) == 0 ? FCFS_OK : FCFS_E_CUDA;
         }
     }
     // the row-blocked kernel: 2D isotropic plans with a compiled entry, tiles in ~100 KB

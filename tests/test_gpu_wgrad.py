@@ -171,3 +171,38 @@ def test_weight_grad_anisotropic(mode):
         assert tuple(gw.shape) == ref.shape, (gw.shape, ref.shape)
         tol = (g.numel() + 8) * 2.0 ** -24 * ab + 1e-30
         assert (np.abs(gw.cpu().double().numpy() - ref) <= tol).all(), (p, q, mode, pad, dtype)
+
+
+@pytest.mark.parametrize("pad", ["zero", "replicate", "reflect"])
+def test_weight_grad_tensor_core_every_compiled_factor(pad, monkeypatch):
+    """The tensor-core kernel (16-bit inputs, 16-B aligned rows, the compiled
+    factors of FCFS_WG_ROWS in csrc/k_wgrad.cu) on ragged shapes -- output rows
+    not a multiple of the band or period, a row's last 16-period block partly
+    past the width (masked A fragments), margins of every padding mode from the
+    TMA box -- against the oracle at Z22's bound, and exactly on integer
+    inputs; fcfs_last_launch asserts the kernel that ran."""
+    cases = [(5, 3), (3, 2), (2, 3), (3, 5)]
+    for i, ((p, q), mode, dtype) in enumerate(itertools.product(cases, ["bilinear", "bicubic"],
+                                                                 ["bfloat16", "float16"])):
+        H, W = [(37, 72), (101, 64), (53, 136)][i % 3]
+        run_case(2, 3, H, W, p, q, mode, pad, dtype, extent=["floor", "paper"][i % 2], seed=40 + i)
+        assert fc.last_launch()["kernel"] == "weight_grad_tensor_core", (p, q, mode, dtype, fc.last_launch())
+    # integers: exact in any summation order; 2 and the default (4) tile buffers, many
+    # tasks per CTA (every buffer's mbarrier phase wraps)
+    pl = Plan(5, 3, "bicubic", pad, 3, 141, 80, "bfloat16", "floor")
+    oshape = pl.out_shape(40)
+    xi = np.floor(synth.uniform_f32(31, 40 * 3 * 141 * 80) * 7.0) - 3.0
+    gi = np.floor(synth.uniform_f32(32, int(np.prod(oshape))) * 7.0) - 3.0
+    x = torch.from_numpy(xi.reshape(40, 3, 141, 80).astype(np.float32)).to(torch.bfloat16)
+    g = torch.from_numpy(gi.reshape(oshape).astype(np.float32)).to(torch.bfloat16)
+    ref, _ = oracle.weight_grad(oracle_input(x), g.double().numpy(), 5, 3, "bicubic", pad, floor_extent=True)
+    for nbuf in ("2", None):
+        if nbuf:
+            monkeypatch.setenv("FCFS_DEBUG_WG_NBUF", nbuf)
+        else:
+            monkeypatch.delenv("FCFS_DEBUG_WG_NBUF", raising=False)
+        gw = pl.run_weight_grad(x.to(DEV), g.to(DEV))
+        torch.cuda.synchronize()
+        info = fc.last_launch()
+        assert info["kernel"] == "weight_grad_tensor_core" and (nbuf is None or info["buffers"] == 2), info
+        assert np.array_equal(gw.cpu().double().numpy(), ref), info
