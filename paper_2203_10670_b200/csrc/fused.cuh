@@ -397,6 +397,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
     }
     __syncthreads();
     pdl_wait();  // the previous grid of the stream (programmatic launch) has completed
+    // the next grid of the stream may start its prologue now: its own pdl_wait
+    // still waits for this grid to complete and its writes to be visible
+    pdl_launch_dependents();
 
     if (warp == 0) {
         // ------------------------------------------------------- producer: issue
@@ -520,7 +523,6 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
                 ci.next(a);
             }
         }
-        pdl_launch_dependents();
         return;
     }
     if (warp == 1) {
@@ -674,7 +676,6 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             mbar_arrive(&ready[cf.slot]);
             cf.next(a);
         }
-        pdl_launch_dependents();
         return;
     }
 
@@ -991,7 +992,6 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fcfs_fused_kernel(const __gr
             }
         }
     }
-    pdl_launch_dependents();
     if (span_e == 0) bulk_wait0();
     };
     if constexpr (kShift) {  // (3D variants: no shifted copy of the consumer code)

@@ -25,6 +25,7 @@
 //   loads of a pass are issued before the first store.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "device_common.cuh"
@@ -294,6 +295,97 @@ __global__ void __launch_bounds__(kRowsThreads, 2) fcfs_nearest_rows_kernel(cons
     pdl_launch_dependents();
 }
 
+// ---------------------------------------------------------------------------
+// Row gather without a producer warp (the default row kernel).  Every warp
+// computes: it takes the referenced input rows k = gw, gw + NW, ... (gw the
+// global warp index, NW the warps of the grid: at any moment the grid works on
+// one contiguous window of rows), copies each into one of its two shared row
+// buffers with per-lane 16-B async copies (cp.async.cg: no register staging,
+// L1 bypassed) -- the next row's copies are in flight while this row's output
+// rows are emitted -- and emits every output row of every job that reads it
+// exactly as the staged kernel does (column tables per CTA, 16-B vector
+// stores).  Compared with the staged kernel (one producer warp, per-slot
+// mbarriers, 15 consumer warps, one CTA per SM) it trades the mbarrier and
+// ring bookkeeping (~245 warp instructions per output row measured on C2) for
+// a cp.async group wait, and runs several CTAs per SM for latency hiding.
+// ---------------------------------------------------------------------------
+constexpr int kRowsAsyncWarps = 8;
+constexpr int kRowsAsyncThreads = 32 * kRowsAsyncWarps;
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <typename T>
+__global__ void __launch_bounds__(kRowsAsyncThreads, 4)
+    fcfs_nearest_rows_async_kernel(const __grid_constant__ NearestRowsArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char *ring = smem + a.tab_bytes;  // per warp: two row buffers of slot_pitch bytes
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // column tables and the zero element past every row buffer (parameters only:
+    // before the grid dependency)
+    build_tables<T>(a, smem, threadIdx.x, kRowsAsyncThreads);
+    for (int s = threadIdx.x; s < 2 * kRowsAsyncWarps; s += kRowsAsyncThreads)
+        *reinterpret_cast<uint4 *>(ring + s * a.slot_pitch + a.row_bytes) = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    pdl_wait();
+    pdl_launch_dependents();  // the next grid may start its prologue (its pdl_wait still waits for us)
+    const int nw = (int)gridDim.x * kRowsAsyncWarps;
+    unsigned char *const bufs = ring + warp * 2 * a.slot_pitch;
+    const int n16 = a.row_bytes >> 4;
+    const uint64_t pol = policy_evict_first();
+    // the next referenced item after `it` (stride nw), or nitems
+    auto next_ref = [&](int it) {
+        for (it += nw; it < a.nitems; it += nw) {
+            const int plane = (int)fdiv((uint32_t)it, a.div_H);
+            if (referenced(a, it - plane * a.H)) break;
+        }
+        return it < a.nitems ? it : a.nitems;
+    };
+    auto issue = [&](int it, unsigned char *dst) {
+        const unsigned char *src = static_cast<const unsigned char *>(a.in) + (int64_t)it * a.row_bytes;
+        for (int c = lane; c < n16; c += 32) cp_async16(dst + 16 * c, src + 16 * c, pol);
+    };
+    int it = next_ref((int)blockIdx.x * kRowsAsyncWarps + warp - nw);
+    if (it < a.nitems) issue(it, bufs);
+    cp_async_commit();
+    for (int k = 0; it < a.nitems; ++k) {
+        const int nxt = next_ref(it);
+        if (nxt < a.nitems) issue(nxt, bufs + ((k + 1) & 1) * a.slot_pitch);
+        cp_async_commit();
+        cp_async_wait1();  // this lane's copies of item `it` have landed
+        __syncwarp();      // ... and every lane's
+        const unsigned char *srow = bufs + (k & 1) * a.slot_pitch;
+        const int plane = (int)fdiv((uint32_t)it, a.div_H), r = it - plane * a.H;
+#pragma unroll
+        for (int j = 0; j < kMaxBatchJobs; ++j) {
+            if (j >= a.njobs) break;
+            const NearestRowJob &jb = a.job[j];
+            int m0, m1;
+            job_rows(a.H, jb, r, m0, m1);
+            const int Wo = jb.Wo;
+            const uint16_t *tabs = reinterpret_cast<const uint16_t *>(smem + jb.tab_off);
+            T *obase = static_cast<T *>(jb.out) + (int64_t)plane * jb.Ho * Wo;
+            for (int m = m0; m < m1; ++m) {
+                T *orow = obase + (int64_t)m * Wo;
+                const int sr = (int)fdiv((uint32_t)(m * jb.qy), jb.div_py);
+                const int sp = sr <= r ? r : pad_src32(sr, a.H, jb.pad);  // past the last row: the padding source
+                if (sp == r)
+                    emit_row_tab<T>(srow, tabs, Wo, orow, lane);
+                else
+                    emit_row_global<T>(a, jb, static_cast<const T *>(a.in) + ((int64_t)plane * a.H + max(sp, 0)) * a.W,
+                                       sp < 0, orow, lane);
+            }
+        }
+        __syncwarp();  // every lane is done with this buffer before the next issue refills it
+        it = nxt;
+    }
+}
+
 // One job the row kernel serves: a 2D whole image (or 1D rows), 16-B aligned
 // input rows of at most 32 KB, 32-bit index ranges.
 bool nearest_rows_job_ok(const RunGeom &g, int is1d, int qx, int qy, int esz) {
@@ -332,6 +424,7 @@ static int launch_nearest_rows(const NearestBatch &nb, cudaStream_t s) {
     constexpr int V = 16 / sizeof(T);
     const RunGeom &g0 = nb.job[0].g;
     NearestRowsArgs a;
+    std::memset(&a, 0, sizeof(a));
     a.in = g0.in;
     a.H = (int32_t)g0.H;
     a.W = (int32_t)g0.W;
@@ -359,6 +452,28 @@ static int launch_nearest_rows(const NearestBatch &nb, cudaStream_t s) {
         tab += V * tab_n(jb.Wo, V) * 2;
     }
     a.tab_bytes = (tab + 127) / 128 * 128;
+    const int sms0 = nb.job[0].sm_count > 0 ? nb.job[0].sm_count : 148;
+    {   // the async row kernel (default): 4 CTAs per SM when the tables and 16 row buffers fit
+        const int smem = a.tab_bytes + 2 * kRowsAsyncWarps * a.slot_pitch;
+        if (!std::getenv("FCFS_NEAREST_STAGED") && smem <= 56 * 1024) {
+            int per_sm = 4;
+            if (const char *e = std::getenv("FCFS_DEBUG_NEAREST_CTAS")) per_sm = std::max(1, std::min(4, std::atoi(e)));
+            int grid = (int)std::min<int64_t>(((int64_t)a.nitems + kRowsAsyncWarps - 1) / kRowsAsyncWarps,
+                                              (int64_t)sms0 * per_sm);
+            if (const char *e = std::getenv("FCFS_DEBUG_NEAREST_GRID")) grid = std::max(1, std::min(grid, std::atoi(e)));
+            if (grid <= 0) return 0;
+            const void *fn = reinterpret_cast<const void *>(&fcfs_nearest_rows_async_kernel<T>);
+            static bool configured[3] = {false, false, false};
+            const int di = sizeof(T) == 4 ? 0 : (std::is_same<T, __half>::value ? 1 : 2);
+            if (!configured[di]) {
+                cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * 1024);
+                if (e != cudaSuccess) return (int)e;
+                configured[di] = true;
+            }
+            void *args[] = {&a};
+            return launch_pdl(fn, grid, kRowsAsyncThreads, args, smem, s);
+        }
+    }
     // rings: a power of two of slots per consumer warp (<= 4: 60 slots) in
     // ~100 KB with the tables (two CTAs per SM), else ~200 KB (one)
     int ctas = 1;

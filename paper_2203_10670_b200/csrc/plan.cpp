@@ -545,11 +545,23 @@ int select_kernel(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
         if (!gr.out) gr.out = reinterpret_cast<void *>(static_cast<uintptr_t>(256));
         if (!std::getenv("FCFS_NO_NEAREST_ROWS") &&
             nearest_rows_job_ok(gr, pl->is1d, pl->q, pl->qy, esize(pl->dtype)))
-            std::snprintf(L.desc, sizeof(L.desc),
-                          "{\"kernel\": \"nearest_gather\", \"variant\": \"rows_staged\", \"items\": %lld, "
-                          "\"grid\": %lld, \"block\": %d, \"consumer_warps\": 15}",
-                          (long long)(g.planes * g.H), (long long)std::min<int64_t>(g.planes * g.H, (int64_t)pl->sm_count),
-                          512);
+        {
+            // the async row kernel (k_nearest.cu) unless FCFS_NEAREST_STAGED or its buffers do not
+            // fit (then the staged kernel); the launch decides, this mirrors it for launch_info
+            const bool staged = std::getenv("FCFS_NEAREST_STAGED") != nullptr ||
+                                (int64_t)(16 / esize(pl->dtype)) * (pl->Wo + 16 / esize(pl->dtype) + 8) * 2 + 16 * ((pl->W * esize(pl->dtype) + 16 + 127) / 128 * 128) > 56 * 1024;
+            const int64_t items = g.planes * g.H;
+            if (staged)
+                std::snprintf(L.desc, sizeof(L.desc),
+                              "{\"kernel\": \"nearest_gather\", \"variant\": \"rows_staged\", \"items\": %lld, "
+                              "\"grid\": %lld, \"block\": %d, \"consumer_warps\": 15}",
+                              (long long)items, (long long)std::min<int64_t>(items, (int64_t)pl->sm_count), 512);
+            else
+                std::snprintf(L.desc, sizeof(L.desc),
+                              "{\"kernel\": \"nearest_gather\", \"variant\": \"rows_async\", \"items\": %lld, "
+                              "\"grid\": %lld, \"block\": %d, \"warps\": 8}",
+                              (long long)items, (long long)std::min<int64_t>((items + 7) / 8, 4LL * pl->sm_count), 256);
+        }
         else
             std::snprintf(L.desc, sizeof(L.desc),
                           "{\"kernel\": \"nearest_gather\", \"variant\": \"general\", \"rows\": %lld, "

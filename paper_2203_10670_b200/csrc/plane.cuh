@@ -94,6 +94,9 @@ __global__ void __launch_bounds__(kPlaneThreads, 2) fcfs_plane_kernel(const __gr
     }
     __syncthreads();
     pdl_wait();  // the previous grid of the stream (programmatic launch) has completed
+    // the next grid of the stream may start its prologue now: its own pdl_wait
+    // still waits for this grid to complete and its writes to be visible
+    pdl_launch_dependents();
     if (threadIdx.x == 0) {
         if (nmine > 0) issue(0);
         if (nmine > 1) issue(1);
@@ -291,7 +294,6 @@ __global__ void __launch_bounds__(kPlaneThreads, 2) fcfs_plane_kernel(const __gr
             }
         }
     }
-    pdl_launch_dependents();
     if (lane == 0) bulk_wait0();
 }
 

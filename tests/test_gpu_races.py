@@ -98,16 +98,22 @@ def test_forward_schedules_identical_and_complete(case, monkeypatch):
 
 
 def test_nearest_row_ring_schedules(monkeypatch):
-    """The row-staged gather under every ring depth and grid: same bits, no gaps."""
+    """The row gathers (async and staged) under every ring depth and grid: same bits, no gaps."""
     x = x_of((4, 3, 200, 256), torch.float32, 5)
     plans = [Plan(2, 3, "nearest", "zero", 3, 200, 256, "float32", "floor"),
              Plan(3, 4, "nearest", "zero", 3, 200, 256, "float32", "floor"),
              Plan(7, 5, "nearest", "reflect", 3, 200, 256, "float32", "paper")]
     ref = None
-    for env in [{}, {"FCFS_DEBUG_NEAREST_LOG2SW": "0"}, {"FCFS_DEBUG_NEAREST_LOG2SW": "1"},
-                {"FCFS_DEBUG_NEAREST_GRID": "1"}, {"FCFS_DEBUG_NEAREST_GRID": "5"}, {"FCFS_NO_PDL": "1"},
-                {"FCFS_DEBUG_NEAREST_CTAS": "2"}]:
-        for k in ("FCFS_DEBUG_NEAREST_LOG2SW", "FCFS_DEBUG_NEAREST_GRID", "FCFS_NO_PDL", "FCFS_DEBUG_NEAREST_CTAS"):
+    # default: the async row kernel (two row buffers per warp); FCFS_NEAREST_STAGED: the
+    # producer-warp kernel with its slot rings
+    st = {"FCFS_NEAREST_STAGED": "1"}
+    for env in [{}, {"FCFS_DEBUG_NEAREST_GRID": "1"}, {"FCFS_DEBUG_NEAREST_GRID": "5"},
+                {"FCFS_DEBUG_NEAREST_CTAS": "1"}, {"FCFS_NO_PDL": "1"},
+                st, {**st, "FCFS_DEBUG_NEAREST_LOG2SW": "0"}, {**st, "FCFS_DEBUG_NEAREST_LOG2SW": "1"},
+                {**st, "FCFS_DEBUG_NEAREST_GRID": "1"}, {**st, "FCFS_DEBUG_NEAREST_GRID": "5"},
+                {**st, "FCFS_DEBUG_NEAREST_CTAS": "2"}]:
+        for k in ("FCFS_DEBUG_NEAREST_LOG2SW", "FCFS_DEBUG_NEAREST_GRID", "FCFS_NO_PDL", "FCFS_DEBUG_NEAREST_CTAS",
+                  "FCFS_NEAREST_STAGED"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)

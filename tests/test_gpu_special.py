@@ -92,7 +92,7 @@ def test_nearest_special_values_bit_exact(dtype, W):
         x = special_input(100 + n, (2, 3, 29, W), dtype)
         pl = Plan(p, q, "nearest", pad, 3, 29, W, dtype, ext)
         assert pl.kernel == "nearest_gather"
-        assert pl.launch_info(2)["variant"] == ("rows_staged" if W == 48 else "general")
+        assert pl.launch_info(2)["variant"] in (("rows_staged", "rows_async") if W == 48 else ("general",))
         y = pl.run(x.to(DEV))
         got = y.cpu().view(TORCH_INT[dtype]).numpy().view(ut)
         exp = gather(x.view(TORCH_INT[dtype]).numpy().view(ut), (29, W), (pl.Ho, pl.Wo), [(pl.p, pl.q)] * 2, pad)
@@ -152,7 +152,7 @@ def test_nearest_row_kernel_equals_general_kernel(monkeypatch):
                  for pq, pad, ext in [(((2, 3), (3, 4)), "zero", "floor"), (((5, 7), (3, 2)), "reflect", "paper"),
                                       (((3, 1), (4, 1)), "replicate", "paper"), (((1, 1), (1, 1)), "zero", "floor")]]
         for pl in plans:
-            assert pl.launch_info(3)["variant"] == "rows_staged"
+            assert pl.launch_info(3)["variant"] in ("rows_staged", "rows_async")
         a = [torch.empty(pl.out_shape(3), dtype=x.dtype, device=DEV) for pl in plans]
         b = [torch.empty_like(t) for t in a]
         fc.run_batch([(pl, x, o) for pl, o in zip(plans, a)])
