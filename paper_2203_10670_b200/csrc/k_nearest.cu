@@ -45,6 +45,7 @@ struct NearestRowsArgs {
     const void *in;
     int32_t H, W, row_bytes, slot_pitch, log2Sw, tab_bytes;  // Sw = 1 << log2Sw slots per consumer warp
     int32_t pf_dist;  // L2 prefetch distance (items), 0: none
+    int32_t list_bytes;  // async kernel: bytes of the referenced-row list (uint16 per row, H <= 8192)
     int32_t nitems;  // planes * H
     FastDiv div_H;
     int32_t njobs;
@@ -88,21 +89,23 @@ __host__ __device__ constexpr int tab_n(int Wo, int V) { return (Wo + V + 7) / 8
 template <typename T>
 __device__ __forceinline__ void build_tables(const NearestRowsArgs &a, unsigned char *smem, int tid, int nthr) {
     constexpr int V = 16 / sizeof(T);
+    // entry i of head shift h is column h + i: each column's offset is computed
+    // once and written into the V shifted copies (no division per entry)
 #pragma unroll 1
     for (int j = 0; j < a.njobs; ++j) {
         const NearestRowJob &jb = a.job[j];
         const int n = tab_n(jb.Wo, V);  // entries per head shift
         uint16_t *tab = reinterpret_cast<uint16_t *>(smem + jb.tab_off);
-        for (int e = tid; e < V * n; e += nthr) {
-            const int h = e / n, c = h + (e - h * n);
+        for (int c = tid; c < n + V - 1; c += nthr) {
             int off = a.row_bytes;  // the zero element
             if (c < jb.Wo) {
-                const uint32_t nn = (uint32_t)c * (uint32_t)jb.qx;
-                int sc = (int)fdiv(nn, jb.div_px);
+                int sc = (int)fdiv((uint32_t)c * (uint32_t)jb.qx, jb.div_px);
                 if (sc >= a.W) sc = pad_src32(sc, a.W, jb.pad);
                 if (sc >= 0) off = sc * (int)sizeof(T);
             }
-            tab[e] = (uint16_t)off;
+#pragma unroll
+            for (int h = 0; h < V; ++h)
+                if (c - h >= 0 && c - h < n) tab[h * n + c - h] = (uint16_t)off;
         }
     }
 }
@@ -114,7 +117,7 @@ __device__ __forceinline__ uint32_t lds_el(const unsigned char *row, uint32_t of
 }
 
 // Output row `orow` (Wo elements) from the staged row `srow` through the job's tables.
-template <typename T>
+template <typename T, bool CS = false>
 __device__ __forceinline__ void emit_row_tab(const unsigned char *srow, const uint16_t *tabs, int Wo, T *orow,
                                              int lane) {
     constexpr int V = 16 / sizeof(T);
@@ -151,7 +154,8 @@ __device__ __forceinline__ void emit_row_tab(const unsigned char *srow, const ui
             for (int e = 0; e < 4; ++e)
                 w[e] = __byte_perm(lds_el<T>(srow, oo[e] & 0xffffu), lds_el<T>(srow, oo[e] >> 16), 0x5410);
         }
-        vout[v] = make_uint4(w[0], w[1], w[2], w[3]);
+        if constexpr (CS) __stcs(vout + v, make_uint4(w[0], w[1], w[2], w[3]));  // streaming: evict first
+        else vout[v] = make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
@@ -318,53 +322,77 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src, uint64_t 
                  : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <typename T>
+// NB: row buffers per warp (NB - 1 rows in flight while one is emitted); CS: streaming output stores
+template <typename T, int NB, bool CS>
 __global__ void __launch_bounds__(kRowsAsyncThreads, 4)
     fcfs_nearest_rows_async_kernel(const __grid_constant__ NearestRowsArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    unsigned char *ring = smem + a.tab_bytes;  // per warp: two row buffers of slot_pitch bytes
+    // [column tables][referenced-row list][per warp: NB row buffers of slot_pitch bytes][count]
+    uint16_t *rlist = reinterpret_cast<uint16_t *>(smem + a.tab_bytes);
+    unsigned char *ring = smem + a.tab_bytes + a.list_bytes;
+    int *nref_s = reinterpret_cast<int *>(ring + NB * kRowsAsyncWarps * a.slot_pitch);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // column tables and the zero element past every row buffer (parameters only:
-    // before the grid dependency)
-    build_tables<T>(a, smem, threadIdx.x, kRowsAsyncThreads);
-    for (int s = threadIdx.x; s < 2 * kRowsAsyncWarps; s += kRowsAsyncThreads)
+    // parameters only (before the grid dependency): column tables, the zero
+    // element past every row buffer, and the list of the input rows some output
+    // row of some job reads (the same in every plane; the others are never loaded)
+    if (warp == 0) {
+        int cnt = 0;
+        for (int r0 = 0; r0 < a.H; r0 += 32) {
+            const int r = r0 + lane;
+            const bool ref = r < a.H && referenced(a, r);
+            const uint32_t m = __ballot_sync(0xffffffffu, ref);
+            if (ref) rlist[cnt + __popc(m & ((1u << lane) - 1u))] = (uint16_t)r;
+            cnt += __popc(m);
+        }
+        if (lane == 0) *nref_s = cnt;
+    } else {
+        build_tables<T>(a, smem, threadIdx.x - 32, kRowsAsyncThreads - 32);
+    }
+    for (int s = threadIdx.x; s < NB * kRowsAsyncWarps; s += kRowsAsyncThreads)
         *reinterpret_cast<uint4 *>(ring + s * a.slot_pitch + a.row_bytes) = make_uint4(0, 0, 0, 0);
     __syncthreads();
     pdl_wait();
     pdl_launch_dependents();  // the next grid may start its prologue (its pdl_wait still waits for us)
+    const int nref = *nref_s;
+    const int total = (int)fdiv((uint32_t)a.nitems, a.div_H) * nref;  // planes x referenced rows
     const int nw = (int)gridDim.x * kRowsAsyncWarps;
-    unsigned char *const bufs = ring + warp * 2 * a.slot_pitch;
+    unsigned char *const bufs = ring + warp * NB * a.slot_pitch;
     const int n16 = a.row_bytes >> 4;
     const uint64_t pol = policy_evict_first();
-    // the next referenced item after `it` (stride nw), or nitems
-    auto next_ref = [&](int it) {
-        for (it += nw; it < a.nitems; it += nw) {
-            const int plane = (int)fdiv((uint32_t)it, a.div_H);
-            if (referenced(a, it - plane * a.H)) break;
-        }
-        return it < a.nitems ? it : a.nitems;
+    // item j: plane j / nref, input row rlist[j % nref]
+    auto row_of = [&](int j, int &plane) {
+        plane = j / nref;
+        return (int)rlist[j - plane * nref];
     };
-    auto issue = [&](int it, unsigned char *dst) {
-        const unsigned char *src = static_cast<const unsigned char *>(a.in) + (int64_t)it * a.row_bytes;
+    auto issue = [&](int j, unsigned char *dst) {
+        int plane;
+        const int r = row_of(j, plane);
+        const unsigned char *src = static_cast<const unsigned char *>(a.in) + ((int64_t)plane * a.H + r) * a.row_bytes;
+#pragma unroll 4
         for (int c = lane; c < n16; c += 32) cp_async16(dst + 16 * c, src + 16 * c, pol);
     };
-    int it = next_ref((int)blockIdx.x * kRowsAsyncWarps + warp - nw);
-    if (it < a.nitems) issue(it, bufs);
-    cp_async_commit();
-    for (int k = 0; it < a.nitems; ++k) {
-        const int nxt = next_ref(it);
-        if (nxt < a.nitems) issue(nxt, bufs + ((k + 1) & 1) * a.slot_pitch);
-        cp_async_commit();
-        cp_async_wait1();  // this lane's copies of item `it` have landed
-        __syncwarp();      // ... and every lane's
-        const unsigned char *srow = bufs + (k & 1) * a.slot_pitch;
-        const int plane = (int)fdiv((uint32_t)it, a.div_H), r = it - plane * a.H;
+    // items in flight: the one emitted next, NB - 2 more, and the issue cursor NB - 1 ahead
+    const int j0 = (int)blockIdx.x * kRowsAsyncWarps + warp;
 #pragma unroll
-        for (int j = 0; j < kMaxBatchJobs; ++j) {
-            if (j >= a.njobs) break;
-            const NearestRowJob &jb = a.job[j];
+    for (int i = 0; i < NB - 1; ++i) {
+        if (j0 + i * nw < total) issue(j0 + i * nw, bufs + i * a.slot_pitch);
+        cp_async_commit();
+    }
+    for (int k = 0, j = j0; j < total; ++k, j += nw) {
+        const int jn = j + (NB - 1) * nw;
+        if (jn < total) issue(jn, bufs + ((k + NB - 1) % NB) * a.slot_pitch);
+        cp_async_commit();
+        cp_async_wait<NB - 1>();  // this lane's copies of item j have landed
+        __syncwarp();             // ... and every lane's
+        const unsigned char *srow = bufs + (k % NB) * a.slot_pitch;
+        int plane;
+        const int r = row_of(j, plane);
+#pragma unroll
+        for (int jj = 0; jj < kMaxBatchJobs; ++jj) {
+            if (jj >= a.njobs) break;
+            const NearestRowJob &jb = a.job[jj];
             int m0, m1;
             job_rows(a.H, jb, r, m0, m1);
             const int Wo = jb.Wo;
@@ -375,14 +403,13 @@ __global__ void __launch_bounds__(kRowsAsyncThreads, 4)
                 const int sr = (int)fdiv((uint32_t)(m * jb.qy), jb.div_py);
                 const int sp = sr <= r ? r : pad_src32(sr, a.H, jb.pad);  // past the last row: the padding source
                 if (sp == r)
-                    emit_row_tab<T>(srow, tabs, Wo, orow, lane);
+                    emit_row_tab<T, CS>(srow, tabs, Wo, orow, lane);
                 else
                     emit_row_global<T>(a, jb, static_cast<const T *>(a.in) + ((int64_t)plane * a.H + max(sp, 0)) * a.W,
                                        sp < 0, orow, lane);
             }
         }
         __syncwarp();  // every lane is done with this buffer before the next issue refills it
-        it = nxt;
     }
 }
 
@@ -453,23 +480,28 @@ static int launch_nearest_rows(const NearestBatch &nb, cudaStream_t s) {
     }
     a.tab_bytes = (tab + 127) / 128 * 128;
     const int sms0 = nb.job[0].sm_count > 0 ? nb.job[0].sm_count : 148;
-    {   // the async row kernel (default): 4 CTAs per SM when the tables and 16 row buffers fit
-        const int smem = a.tab_bytes + 2 * kRowsAsyncWarps * a.slot_pitch;
-        if (!std::getenv("FCFS_NEAREST_STAGED") && smem <= 56 * 1024) {
-            int per_sm = 4;
-            if (const char *e = std::getenv("FCFS_DEBUG_NEAREST_CTAS")) per_sm = std::max(1, std::min(4, std::atoi(e)));
+    {   // the async row kernel (default): NB row buffers per warp, as many CTAs per SM (<= 4)
+        // as the tables and buffers allow
+        int nb_ = 2, cs = 1;  // streaming stores measured 2% faster on C2
+        if (const char *e = std::getenv("FCFS_DEBUG_NEAREST_NBUF")) nb_ = std::max(2, std::min(4, std::atoi(e)));
+        if (const char *e = std::getenv("FCFS_DEBUG_NEAREST_CS")) cs = std::atoi(e) != 0;
+        a.list_bytes = (int32_t)((2 * g0.H + 127) / 128 * 128);
+        const int smem = a.tab_bytes + a.list_bytes + nb_ * kRowsAsyncWarps * a.slot_pitch + 16;
+        if (!std::getenv("FCFS_NEAREST_STAGED") && g0.H <= 8192 && smem <= 108 * 1024) {
+            int per_sm = std::min(4, 216 * 1024 / smem);
+            if (const char *e = std::getenv("FCFS_DEBUG_NEAREST_CTAS")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
             int grid = (int)std::min<int64_t>(((int64_t)a.nitems + kRowsAsyncWarps - 1) / kRowsAsyncWarps,
                                               (int64_t)sms0 * per_sm);
             if (const char *e = std::getenv("FCFS_DEBUG_NEAREST_GRID")) grid = std::max(1, std::min(grid, std::atoi(e)));
             if (grid <= 0) return 0;
-            const void *fn = reinterpret_cast<const void *>(&fcfs_nearest_rows_async_kernel<T>);
-            static bool configured[3] = {false, false, false};
-            const int di = sizeof(T) == 4 ? 0 : (std::is_same<T, __half>::value ? 1 : 2);
-            if (!configured[di]) {
-                cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * 1024);
-                if (e != cudaSuccess) return (int)e;
-                configured[di] = true;
-            }
+            const void *fn = nb_ == 2 ? (cs ? reinterpret_cast<const void *>(&fcfs_nearest_rows_async_kernel<T, 2, true>)
+                                            : reinterpret_cast<const void *>(&fcfs_nearest_rows_async_kernel<T, 2, false>))
+                           : nb_ == 3 ? (cs ? reinterpret_cast<const void *>(&fcfs_nearest_rows_async_kernel<T, 3, true>)
+                                            : reinterpret_cast<const void *>(&fcfs_nearest_rows_async_kernel<T, 3, false>))
+                                      : (cs ? reinterpret_cast<const void *>(&fcfs_nearest_rows_async_kernel<T, 4, true>)
+                                            : reinterpret_cast<const void *>(&fcfs_nearest_rows_async_kernel<T, 4, false>));
+            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 108 * 1024);
+            if (e != cudaSuccess) return (int)e;
             void *args[] = {&a};
             return launch_pdl(fn, grid, kRowsAsyncThreads, args, smem, s);
         }

@@ -548,8 +548,8 @@ int select_kernel(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
         {
             // the async row kernel (k_nearest.cu) unless FCFS_NEAREST_STAGED or its buffers do not
             // fit (then the staged kernel); the launch decides, this mirrors it for launch_info
-            const bool staged = std::getenv("FCFS_NEAREST_STAGED") != nullptr ||
-                                (int64_t)(16 / esize(pl->dtype)) * (pl->Wo + 16 / esize(pl->dtype) + 8) * 2 + 16 * ((pl->W * esize(pl->dtype) + 16 + 127) / 128 * 128) > 56 * 1024;
+            const bool staged = std::getenv("FCFS_NEAREST_STAGED") != nullptr || g.H > 8192 ||
+                                (int64_t)(16 / esize(pl->dtype)) * (pl->Wo + 16 / esize(pl->dtype) + 8) * 2 + 16 * ((pl->W * esize(pl->dtype) + 16 + 127) / 128 * 128) > 108 * 1024;
             const int64_t items = g.planes * g.H;
             if (staged)
                 std::snprintf(L.desc, sizeof(L.desc),
