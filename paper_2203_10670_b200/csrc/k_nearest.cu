@@ -332,30 +332,47 @@ __global__ void __launch_bounds__(kRowsAsyncThreads, 4)
     // [column tables][referenced-row list][per warp: NB row buffers of slot_pitch bytes][count]
     uint16_t *rlist = reinterpret_cast<uint16_t *>(smem + a.tab_bytes);
     unsigned char *ring = smem + a.tab_bytes + a.list_bytes;
-    int *nref_s = reinterpret_cast<int *>(ring + NB * kRowsAsyncWarps * a.slot_pitch);
+    uint32_t *hdr = reinterpret_cast<uint32_t *>(ring + NB * kRowsAsyncWarps * a.slot_pitch);  // nref, FastDiv(nref)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // parameters only (before the grid dependency): column tables, the zero
     // element past every row buffer, and the list of the input rows some output
-    // row of some job reads (the same in every plane; the others are never loaded)
+    // row of some job reads (the same in every plane; the others are never
+    // loaded).  The list: a flag byte per row (all threads), then one warp
+    // compacts the flags into the list's first half (it writes entry c < row r
+    // at byte 2c <= 2r, never over a flag at byte H + r' it has yet to read).
+    unsigned char *flags = smem + a.tab_bytes + a.H;
+    for (int r = threadIdx.x; r < a.H; r += kRowsAsyncThreads) flags[r] = referenced(a, r) ? 1 : 0;
+    build_tables<T>(a, smem, threadIdx.x, kRowsAsyncThreads);
+    __syncthreads();
     if (warp == 0) {
         int cnt = 0;
         for (int r0 = 0; r0 < a.H; r0 += 32) {
             const int r = r0 + lane;
-            const bool ref = r < a.H && referenced(a, r);
+            const bool ref = r < a.H && flags[r];
             const uint32_t m = __ballot_sync(0xffffffffu, ref);
+            __syncwarp();
             if (ref) rlist[cnt + __popc(m & ((1u << lane) - 1u))] = (uint16_t)r;
             cnt += __popc(m);
         }
-        if (lane == 0) *nref_s = cnt;
+        if (lane == 0) {  // multiply-shift divisor of cnt (fcfs_internal.h make_fastdiv)
+            uint32_t sh = 0;
+            while (sh < 32 && (1ull << sh) < (uint64_t)cnt) ++sh;
+            hdr[0] = (uint32_t)cnt;
+            hdr[1] = cnt > 0 ? (uint32_t)(((1ull << 32) * ((1ull << sh) - (uint64_t)cnt)) / (uint64_t)cnt + 1) : 0u;
+            hdr[2] = sh;
+        }
     } else {
-        build_tables<T>(a, smem, threadIdx.x - 32, kRowsAsyncThreads - 32);
+        for (int s = threadIdx.x - 32; s < NB * kRowsAsyncWarps; s += kRowsAsyncThreads - 32)
+            *reinterpret_cast<uint4 *>(ring + s * a.slot_pitch + a.row_bytes) = make_uint4(0, 0, 0, 0);
     }
-    for (int s = threadIdx.x; s < NB * kRowsAsyncWarps; s += kRowsAsyncThreads)
-        *reinterpret_cast<uint4 *>(ring + s * a.slot_pitch + a.row_bytes) = make_uint4(0, 0, 0, 0);
     __syncthreads();
     pdl_wait();
     pdl_launch_dependents();  // the next grid may start its prologue (its pdl_wait still waits for us)
-    const int nref = *nref_s;
+    const int nref = (int)hdr[0];
+    FastDiv div_nref;
+    div_nref.d = hdr[0];
+    div_nref.m = hdr[1];
+    div_nref.s = hdr[2];
     const int total = (int)fdiv((uint32_t)a.nitems, a.div_H) * nref;  // planes x referenced rows
     const int nw = (int)gridDim.x * kRowsAsyncWarps;
     unsigned char *const bufs = ring + warp * NB * a.slot_pitch;
@@ -363,7 +380,7 @@ __global__ void __launch_bounds__(kRowsAsyncThreads, 4)
     const uint64_t pol = policy_evict_first();
     // item j: plane j / nref, input row rlist[j % nref]
     auto row_of = [&](int j, int &plane) {
-        plane = j / nref;
+        plane = (int)fdiv((uint32_t)j, div_nref);
         return (int)rlist[j - plane * nref];
     };
     auto issue = [&](int j, unsigned char *dst) {
