@@ -261,4 +261,27 @@ struct PlaneArgs {
 const FusedVariant *plane_lookup(int dtype, int py, int qy, int px, int qx, int ntaps);
 int launch_plane(const FusedVariant *v, const PlaneArgs &a, int grid, int smem, void *stream);
 
+// Volumes of small slices (plane.cuh fcfs_plane3_kernel): a ring of S whole
+// padded input slices, a task = a run of output slices of one volume.
+constexpr int kPlane3MaxS = 8;
+struct Plane3Args {
+    // 4D tiled TMA descriptor of the input (columns, rows, slices, volumes), box (BW, BH, 1, 1);
+    // a box starts at column -16/esize, row row_lo and the (padded) slice
+    alignas(64) CUtensorMap tmap;
+    void *out;
+    int64_t out_plane_stride;  // elements between output volumes (= Do * Ho * Wo)
+    int64_t out_slice_stride;  // elements between output slices (= Ho * Wo)
+    int32_t H, W, Ho, Wo, pad;
+    int32_t D, Do, pz, qz;
+    int32_t BW, BH, row_lo, plane_bytes, nch, nper, slot_bytes;
+    int32_t lpad, rpad, tpad, bpad;
+    int32_t S;        // slice buffers (>= taps + 1)
+    int32_t chunks;   // tasks per volume (runs of output slices)
+    int32_t ntasks;   // volumes * chunks
+    float zw[kZMax][4];
+    int32_t zbase[kZMax];
+};
+const FusedVariant *plane3_lookup(int dtype, int py, int qy, int px, int qx, int ntaps);
+int launch_plane3(const FusedVariant *v, const Plane3Args &a, int grid, int smem, void *stream);
+
 }  // namespace fcfs

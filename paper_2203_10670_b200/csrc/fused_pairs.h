@@ -26,3 +26,7 @@
 // plane-resident kernel (plane.cuh): isotropic pairs for batches of small planes
 #define FCFS_PLANE_PAIRS(Y) \
     Y(2, 1) Y(3, 2) Y(4, 3) Y(5, 3) Y(5, 4) Y(7, 5) Y(1, 2) Y(2, 3) Y(3, 4) Y(3, 5) Y(4, 5) Y(5, 7)
+// slice-ring plane kernel (plane.cuh fcfs_plane3_kernel): isotropic row/column
+// pairs of 3D volumes with small slices (any slice factor, run-time slice weights)
+#define FCFS_PLANE3_PAIRS(Y) \
+    Y(2, 1) Y(3, 2) Y(4, 3) Y(5, 3) Y(5, 4) Y(1, 2) Y(2, 3) Y(3, 4) Y(3, 5) Y(4, 5)

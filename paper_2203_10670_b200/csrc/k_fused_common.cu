@@ -17,6 +17,16 @@ extern const FusedVariant kFusedVariants_bf16_iso[], kFusedVariants_bf16_w[], kF
     kFusedVariants_bf16_z[];
 extern const FusedVariant kFusedVariants_f32_adj[], kFusedVariants_f16_adj[], kFusedVariants_bf16_adj[];
 extern const FusedVariant kPlaneVariants_f32[], kPlaneVariants_f16[], kPlaneVariants_bf16[];
+extern const FusedVariant kPlane3Variants_f32[], kPlane3Variants_f16[], kPlane3Variants_bf16[];
+
+// The slice-ring variant (plane.cuh fcfs_plane3_kernel) of a 3D layer's rows/columns.
+const FusedVariant *plane3_lookup(int dtype, int py, int qy, int px, int qx, int ntaps) {
+    const FusedVariant *sets[3] = {kPlane3Variants_f32, kPlane3Variants_f16, kPlane3Variants_bf16};
+    if (dtype < 0 || dtype > 2) return nullptr;
+    for (const FusedVariant *v = sets[dtype]; v->fn; ++v)
+        if (v->PY == py && v->QY == qy && v->PX == px && v->QX == qx && v->TAPS == ntaps) return v;
+    return nullptr;
+}
 
 // The plane-resident variant (plane.cuh) of the 2D layer (py/qy, px/qx): exact factors.
 const FusedVariant *plane_lookup(int dtype, int py, int qy, int px, int qx, int ntaps) {
@@ -88,6 +98,24 @@ int launch_plane(const FusedVariant *v, const PlaneArgs &a, int grid, int smem, 
         }
     }
     PlaneArgs local = a;
+    void *args[] = {&local};
+    return launch_pdl(v->fn, grid, kPlaneThreads, args, smem, stream);
+}
+
+int launch_plane3(const FusedVariant *v, const Plane3Args &a, int grid, int smem, void *stream) {
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> configured;  // (fn, device)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!configured.count({v->fn, dev})) {
+            cudaError_t e = cudaFuncSetAttribute(v->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            if (e != cudaSuccess) return (int)e;
+            configured.insert({v->fn, dev});
+        }
+    }
+    Plane3Args local = a;
     void *args[] = {&local};
     return launch_pdl(v->fn, grid, kPlaneThreads, args, smem, stream);
 }

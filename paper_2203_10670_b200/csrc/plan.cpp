@@ -37,6 +37,7 @@ struct fcfs_plan_s {
     int kernel;  // 0 reference, 1 nearest, 2 fused, 3 tiled
     const FusedVariant *fused;
     const FusedVariant *plane;  // plane-resident variant of `fused` (2D planes), or nullptr
+    const FusedVariant *plane3; // slice-ring plane variant of `fused` (3D volumes with a slice factor), or nullptr
     int device;
     int64_t rows_ref;
     int sm_count;
@@ -166,6 +167,7 @@ bool ranges_overlap(const void *a, int64_t na, const void *b, int64_t nb) {
 struct FusedLaunch {
     FusedArgs a;
     PlaneArgs pa;  // the plane-resident kernel (select_kernel returns 4)
+    Plane3Args p3; // the slice-ring plane kernel (select_kernel returns 5)
     int grid, smem;
     char desc[768];
 };
@@ -486,6 +488,118 @@ bool plan_plane(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     return true;
 }
 
+// Slice-ring geometry (plane.cuh fcfs_plane3_kernel): 3D volumes whose padded
+// input slice fits one TMA box and whose shared memory holds at least taps + 1
+// of them next to the staging slots (one CTA per SM).  A task is a run of
+// output slices of one volume, the runs sized so that every SM gets work.
+// False: the row-pipelined 3D kernel runs.
+bool plan_plane3(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
+    const FusedVariant *v = pl->plane3;
+    if (!v || pl->is1d || std::getenv("FCFS_NO_PLANE3")) return false;
+    if (g.in_row0 != 0 || g.in_nrows != g.H || g.out_row0 != 0 || g.out_nrows != g.Ho) return false;
+    if (g.in_plane_stride != g.D * g.H * g.W || g.out_plane_stride != g.Do * g.Ho * g.Wo) return false;
+    const int ESZ = esize(pl->dtype), A = 16 / ESZ;
+    if ((g.W * ESZ) % 16 != 0 || (reinterpret_cast<uintptr_t>(g.in) & 15) != 0) return false;
+    if (g.planes > INT32_MAX / 4 || g.D > INT32_MAX / 4 || g.Do < 1) return false;
+    const int *geo = v->geo;
+    const int PY = geo[0], QY = geo[1], TY = geo[2], LOY = geo[3];
+    const int PX = geo[4], QX = geo[5], TX = geo[6], LOX = geo[7];
+    const int K = v->K, KP = K * PX;
+    int HIy = -(1 << 30), HIx = -(1 << 30);
+    for (int j = 0; j < PY; ++j) HIy = std::max(HIy, geo[8 + j] + TY - 1 + LOY);
+    for (int j = 0; j < PX; ++j) HIx = std::max(HIx, geo[24 + j] + TX - 1 + LOX);
+    const int Ly = HIy - LOY + 1, Lx = HIx - LOX + 1;
+    Plane3Args &a = L.p3;
+    std::memset(&a, 0, sizeof(a));
+    a.out = g.out;
+    a.out_plane_stride = g.out_plane_stride;
+    a.out_slice_stride = g.Ho * g.Wo;
+    a.H = (int32_t)g.H;
+    a.W = (int32_t)g.W;
+    a.Ho = (int32_t)g.Ho;
+    a.Wo = (int32_t)g.Wo;
+    a.pad = pl->pad;
+    a.D = (int32_t)g.D;
+    a.Do = (int32_t)g.Do;
+    a.pz = pl->pz;
+    a.qz = pl->qz;
+    for (int j = 0; j < pl->pz; ++j) {
+        a.zbase[j] = pl->tabz.base[j];
+        for (int t = 0; t < 4; ++t) a.zw[j][t] = pl->tabz.w[j][t];
+    }
+    a.nch = (int32_t)((g.Wo + KP - 1) / KP);
+    if (a.nch > 32) return false;
+    a.nper = (int32_t)((g.Ho + PY - 1) / PY);
+    a.row_lo = LOY;
+    a.BH = QY * (a.nper - 1) + Ly;
+    const int WIN = (K - 1) * QX + Lx;
+    const int64_t col_end = (int64_t)(a.nch - 1) * K * QX + LOX + WIN;
+    a.BW = (int32_t)((A + col_end + A - 1) / A * A);
+    if (a.BW > 256 || a.BH > 256) return false;
+    a.plane_bytes = (a.BW * a.BH * ESZ + 127) / 128 * 128;
+    const int64_t rowb = g.Wo * ESZ;
+    a.slot_bytes = (int32_t)((16 + PY * rowb + KP * ESZ + 15) / 16 * 16);
+    const int64_t fixed = 256 + 2 * kPlaneConsumerWarps * a.slot_bytes;
+    const int64_t budget = 227 * 1024;
+    a.S = (int32_t)std::min<int64_t>(kPlane3MaxS, (budget - fixed) / a.plane_bytes);
+    if (const char *e = std::getenv("FCFS_DEBUG_PLANE3_S")) a.S = std::min(a.S, std::atoi(e));
+    if (a.S < v->TAPS + 1) return false;
+    L.smem = (int)(fixed + a.S * a.plane_bytes);
+    const int64_t reach_x = ((g.Wo - 1) / PX) * QX + LOX + geo[24 + (int)((g.Wo - 1) % PX)] + TX;
+    const int64_t reach_y = ((g.Ho - 1) / PY) * QY + LOY + geo[8 + (int)((g.Ho - 1) % PY)] + TY;
+    a.lpad = pl->pad == FCFS_PAD_ZERO ? 0 : -LOX;
+    a.rpad = pl->pad == FCFS_PAD_ZERO ? 0 : (int32_t)std::max<int64_t>(0, reach_x - g.W);
+    a.tpad = pl->pad == FCFS_PAD_ZERO ? 0 : -LOY;
+    a.bpad = pl->pad == FCFS_PAD_ZERO ? 0 : (int32_t)std::max<int64_t>(0, reach_y - g.H);
+    if (a.lpad > A || g.W + a.rpad > a.BW - A || g.H + a.bpad - a.row_lo > a.BH) return false;
+    // runs of output slices: enough tasks for every SM, each run >= 4 output slices
+    // (a run re-reads the taps - 1 slices its first output slice shares with the previous run)
+    const int64_t sms = pl->sm_count > 0 ? pl->sm_count : 148;
+    int64_t chunks = std::max<int64_t>(1, sms / g.planes);  // tasks <= SMs: one wave
+    chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, g.Do / 4));
+    if (const char *e = std::getenv("FCFS_DEBUG_PLANE3_CHUNKS")) chunks = std::max(1, std::min((int)g.Do, std::atoi(e)));
+    a.chunks = (int32_t)chunks;
+    if (g.planes * chunks > INT32_MAX) return false;
+    a.ntasks = (int32_t)(g.planes * chunks);
+    L.grid = (int)std::min<int64_t>(a.ntasks, sms);
+    if (const char *e = std::getenv("FCFS_DEBUG_GRID")) L.grid = std::max(1, std::min(L.grid, std::atoi(e)));
+    if (g.in) {
+        static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+        static bool tried = false;
+        if (!tried) {
+            tried = true;
+            void *fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+                q == cudaDriverEntryPointSuccess)
+                encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+            cudaGetLastError();
+        }
+        if (!encode) return false;
+        const CUtensorMapDataType dt = pl->dtype == FCFS_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                       : pl->dtype == FCFS_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                               : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        cuuint64_t dims[4] = {(cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.D, (cuuint64_t)g.planes};
+        cuuint64_t strides[3] = {(cuuint64_t)(g.W * ESZ), (cuuint64_t)(g.H * g.W * ESZ),
+                                 (cuuint64_t)(g.D * g.H * g.W * ESZ)};
+        cuuint32_t box[4] = {(cuuint32_t)a.BW, (cuuint32_t)a.BH, 1, 1};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        if (encode(&a.tmap, dt, 4, const_cast<void *>(g.in), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    std::snprintf(L.desc, sizeof(L.desc),
+                  "{\"kernel\": \"fused_plane3\", \"PY\": %d, \"QY\": %d, \"PX\": %d, \"QX\": %d, \"taps\": %d, "
+                  "\"K\": %d, \"nch\": %d, \"periods\": %d, \"BW\": %d, \"BH\": %d, \"plane_bytes\": %d, "
+                  "\"S\": %d, \"slot_bytes\": %d, \"chunks\": %d, \"ntasks\": %d, \"grid\": %d, \"block\": %d, "
+                  "\"smem\": %d, \"busy_lanes\": %d, \"pads\": [%d, %d, %d, %d]}",
+                  PY, QY, PX, QX, TX, K, a.nch, a.nper, a.BW, a.BH, a.plane_bytes, a.S, a.slot_bytes, a.chunks,
+                  a.ntasks, L.grid, kPlaneThreads, L.smem, a.nch, a.tpad, a.bpad, a.lpad, a.rpad);
+    if (std::getenv("FCFS_DEBUG_PRINT")) std::fprintf(stderr, "%s\n", L.desc);
+    return true;
+}
+
 // 1D plans: every row of every plane is an independent signal, so a whole-row
 // run is one plane of planes * H rows (long columns of rows keep the kernels'
 // row bands full however small H is).
@@ -529,6 +643,7 @@ int select_kernel(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
             g2.out_plane_stride = g.out_nrows * pl->Wo;
         }
         if (pl->fused->TZ == 1 && plan_plane(pl, g2, L)) return 4;
+        if (pl->fused->TZ > 1 && plan_plane3(pl, g, L)) return 5;
         if ((reinterpret_cast<uintptr_t>(g.in) % esize(pl->dtype)) ||
             g2.planes * std::max(g2.D, g2.Do) * std::max(g.in_nrows * pl->W, g.out_nrows * pl->Wo) > INT32_MAX * 16LL || !plan_fused(pl, g2, L))
             kernel = (pl->pz == 1 && pl->qz == 1) ? 3 : 0;  // tiled when the slice factor allows it
@@ -760,6 +875,7 @@ fcfs_status launch(const Prepared &pr, void *stream) {
     if (pr.kernel == 1) rc = launch_nearest(pr.pl->dtype, pr.na, stream);
     else if (pr.kernel == 2) rc = launch_fused(pr.pl->fused, pr.L.a, pr.L.grid, kFusedThreads, pr.L.smem, stream);
     else if (pr.kernel == 4) rc = launch_plane(pr.pl->plane, pr.L.pa, pr.L.grid, pr.L.smem, stream);
+    else if (pr.kernel == 5) rc = launch_plane3(pr.pl->plane3, pr.L.p3, pr.L.grid, pr.L.smem, stream);
     else if (pr.kernel == 3) rc = launch_tile(pr.pl->dtype, pr.ta, pr.tgrid, pr.tsmem, stream);
     else if (pr.kernel == 0) rc = launch_reference(pr.pl->dtype, pr.ra, stream);
     return rc == 0 ? FCFS_OK : FCFS_E_CUDA;
@@ -850,6 +966,7 @@ fcfs_status make_plan(int rank, const int *pd, const int *qd, int mode, int pad,
     pl->kernel = 0;
     pl->fused = nullptr;
     pl->plane = nullptr;
+    pl->plane3 = nullptr;
     if (!(flags & FCFS_FLAG_FORCE_REFERENCE)) {
         if (mode == FCFS_NEAREST) {
             pl->kernel = 1;
@@ -870,6 +987,18 @@ fcfs_status make_plan(int rank, const int *pd, const int *qd, int mode, int pad,
                         pl->fused = nullptr;
             if (pl->fused) pl->kernel = 2;
             // batches of small planes: the plane-resident form of the same layer
+            // volumes of small slices: the slice-ring form
+            if (pl->fused && slices && !pl->is1d) {
+                pl->plane3 = plane3_lookup(dtype, pl->py, pl->qy, pl->p, pl->q, pl->tab.ntaps);
+                for (int j = 0; pl->plane3 && j < pl->p; ++j)
+                    for (int t = 0; t < pl->tab.ntaps; ++t)
+                        if (std::memcmp(&pl->plane3->wtab_x[4 * j + t], &pl->tab.w[j][t], sizeof(float)) != 0)
+                            pl->plane3 = nullptr;
+                for (int j = 0; pl->plane3 && j < pl->py; ++j)
+                    for (int t = 0; t < pl->taby.ntaps; ++t)
+                        if (std::memcmp(&pl->plane3->wtab_y[4 * j + t], &pl->taby.w[j][t], sizeof(float)) != 0)
+                            pl->plane3 = nullptr;
+            }
             if (pl->fused && !slices && !pl->is1d) {
                 pl->plane = plane_lookup(dtype, pl->py, pl->qy, pl->p, pl->q, pl->tab.ntaps);
                 for (int j = 0; pl->plane && j < pl->p; ++j)

@@ -297,4 +297,320 @@ __global__ void __launch_bounds__(kPlaneThreads, 2) fcfs_plane_kernel(const __gr
     if (lane == 0) bulk_wait0();
 }
 
+// ---------------------------------------------------------------------------
+// Volumes of small slices (3D layers, §4.2 per-dimension factors with a slice
+// factor pz/qz): the same plane-resident scheme over a RING of S input slices.
+// A task is a run of output slices [mz0, mz1) of one volume; output slice mz
+// combines the TZ input slices z0(mz) + t (virtual, padded at the volume's
+// ends: reflect / replicate remap the slice coordinate, zero padding lets the
+// 4D TMA box fall outside the tensor and fill zeros) with the run-time slice
+// weights of phase mz mod pz -- slice taps first, then columns, then rows,
+// the operation order of the row-pipelined 3D variants and the reference
+// kernel, so all three agree bit for bit.  The CTA's slices form one sequence
+// (task by task, each task's slices z0(mz0) .. z0(mz1 - 1) + TZ - 1 in order);
+// sequence element s lands in buffer s mod S (one 3D box per slice), and the
+// last of the 8 warps to finish with element s loads element s + S into it.
+// Warp w keeps band w of every output slice (a fixed band: it writes the
+// replicate / reflect margins of its band's rows once per slice, after the
+// slice lands, and no other warp reads them first).  One CTA per SM (S = 5
+// whole padded slices of 128^2 bf16 fill the shared memory).
+// ---------------------------------------------------------------------------
+
+template <typename T, int PY0, int QY0, int PX0, int QX0, int T0, int LO0, int K>
+__global__ void __launch_bounds__(kPlaneThreads, 1) fcfs_plane3_kernel(const __grid_constant__ Plane3Args a) {
+    using GY = GeoSel<PY0, QY0, T0, LO0, false>;
+    using GX = GeoSel<PX0, QX0, T0, LO0, false>;
+    constexpr int PY = GY::P, QY = GY::Q, PX = GX::P, QX = GX::Q;
+    constexpr int TY = GY::TAPS, TX = GX::TAPS, LOX = GX::LO;
+    constexpr int TZ = T0, LOZ = LO0;  // slice taps: the mode's
+    constexpr int L = GY::L, C = GY::C;
+    constexpr int KP = K * PX;
+    constexpr int WIN = (K - 1) * QX + GX::L;
+    constexpr int ESZ = sizeof(T);
+    constexpr int A = 16 / ESZ;
+    constexpr int PAR = (ESZ == 2 && (K * QX) % 2 == 0) ? ((LOX % 2 + 2) % 2) : -1;
+    constexpr int R = QY * ((L + QY - 1) / QY);
+    constexpr int U = R / QY;
+    static_assert(U <= 4, "ring phases");
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);  // [kPlane3MaxS] slice landed
+    int *done = reinterpret_cast<int *>(smem + 8 * kPlane3MaxS);  // [kPlane3MaxS] warps done with the element
+    unsigned char *pbuf = smem + 256;
+    unsigned char *obuf = pbuf + a.S * a.plane_bytes;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int S = a.S;
+    const uint32_t box_bytes = (uint32_t)(a.BW * a.BH * ESZ);
+    // first virtual input slice of output slice mz (§4.2: floor(mz qz / pz) + base of its phase + LO)
+    auto zfirst = [&](int mz) { return (mz / a.pz) * a.qz + a.zbase[mz % a.pz] + LOZ; };
+    // task t: volume, output slices [m0, m1), first slice, slice count
+    auto task_span = [&](int t, int &vol, int &m0, int &m1, int &zf, int &ns) {
+        vol = t / a.chunks;
+        const int c = t - vol * a.chunks;
+        m0 = (int)((int64_t)c * a.Do / a.chunks);
+        m1 = (int)((int64_t)(c + 1) * a.Do / a.chunks);
+        zf = zfirst(m0);
+        ns = m1 > m0 ? zfirst(m1 - 1) + TZ - zf : 0;
+    };
+    // sequence element s of this CTA -> (volume, virtual slice); false past the last task
+    auto locate = [&](uint32_t s, int &vol, int &zv) {
+        uint32_t base = 0;
+        for (int t = (int)blockIdx.x; t < a.ntasks; t += (int)gridDim.x) {
+            int m0, m1, zf, ns;
+            task_span(t, vol, m0, m1, zf, ns);
+            if (s < base + (uint32_t)ns) {
+                zv = zf + (int)(s - base);
+                return true;
+            }
+            base += (uint32_t)ns;
+        }
+        return false;
+    };
+    auto issue = [&](uint32_t s) {  // one elected thread
+        int vol, zv;
+        if (!locate(s, vol, zv)) return;
+        const int b = (int)(s % (uint32_t)S);
+        // zero padding: a slice outside [0, D) is a box outside the tensor (zero fill)
+        const int zs = a.pad == FCFS_PAD_ZERO ? zv : pad_src32(zv, a.D, a.pad);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full[b], box_bytes);
+        tma_load_4d(pbuf + b * a.plane_bytes, &a.tmap, -A, a.row_lo, zs, vol, &full[b], policy_evict_first());
+    };
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < S; ++b) {
+            mbar_init(&full[b], 1);
+            done[b] = 0;
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    pdl_wait();
+    pdl_launch_dependents();
+    if (threadIdx.x == 0)
+        for (int s = 0; s < S; ++s) issue((uint32_t)s);
+
+    const int chunk = min(lane, a.nch - 1);
+    const int e0 = A + chunk * K * QX + LOX;
+    const int rowb = a.Wo * ESZ;
+    const int col_b = chunk * KP * ESZ;
+    unsigned char *const slots = obuf + warp * 2 * a.slot_bytes;
+    float hr[R][KP];
+    uint32_t fk = 0;
+    // this warp's fixed band of y-periods and the buffer rows it reads
+    const int iy0 = warp * a.nper / kPlaneConsumerWarps, iy1 = (warp + 1) * a.nper / kPlaneConsumerWarps;
+    const int br0 = iy0 * QY, br1 = min(a.BH, (iy1 - 1) * QY + L);
+
+    // horizontal taps of one window row combined over the TZ slices of sl[]
+    auto row_h = [&](float(&h)[KP], const T *const (&sl)[TZ], int br, const float (&wz)[TZ], bool zcopy) {
+        float win[WIN];
+        {
+            float acc[WIN], cp[WIN];
+#pragma unroll
+            for (int t = 0; t < TZ; ++t) {
+                float sub[WIN];
+                load_win<T, WIN, PAR>(sl[t] + br * a.BW, e0, sub);
+#pragma unroll
+                for (int i = 0; i < WIN; ++i) {
+                    acc[i] = t == 0 ? __fmul_rn(wz[0], sub[i]) : __fmaf_rn(wz[t], sub[i], acc[i]);
+                    if (t == -LOZ) cp[i] = sub[i];
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < WIN; ++i) win[i] = zcopy ? cp[i] : acc[i];
+        }
+        if constexpr (K == 2) {
+#pragma unroll
+            for (int jx = 0; jx < PX; ++jx) {
+                if (GX::frac0(jx)) {
+                    h[jx] = win[GX::base(jx) - LOX];
+                    h[PX + jx] = win[QX + GX::base(jx) - LOX];
+                } else {
+                    const int bb = GX::base(jx);
+                    float2 v2 = fmul2_rn(GX::w(jx, 0), make_float2(win[bb], win[QX + bb]));
+#pragma unroll
+                    for (int tp = 1; tp < TX; ++tp)
+                        v2 = ffma2_rn(GX::w(jx, tp), make_float2(win[bb + tp], win[QX + bb + tp]), v2);
+                    h[jx] = v2.x;
+                    h[PX + jx] = v2.y;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+#pragma unroll
+                for (int jx = 0; jx < PX; ++jx) {
+                    float v;
+                    if (GX::frac0(jx)) {
+                        v = win[k * QX + GX::base(jx) - LOX];
+                    } else {
+                        const int bb = k * QX + GX::base(jx);
+                        v = __fmul_rn(GX::w(jx, 0), win[bb]);
+#pragma unroll
+                        for (int tp = 1; tp < TX; ++tp) v = __fmaf_rn(GX::w(jx, tp), win[bb + tp], v);
+                    }
+                    h[k * PX + jx] = v;
+                }
+            }
+        }
+    };
+    // replicate / reflect margins of this warp's band rows in buffer pl (§3 Padding)
+    auto pad_band = [&](T *pl) {
+        for (int br = br0 + lane; br < br1; br += 32) {
+            const int v = br + a.row_lo;
+            if (v < 0 || v >= a.H) continue;
+            T *row = pl + br * a.BW + A;
+            for (int c = -a.lpad; c < 0; ++c) row[c] = row[pad_src32(c, a.W, a.pad)];
+            for (int c = a.W; c < a.W + a.rpad; ++c) row[c] = row[pad_src32(c, a.W, a.pad)];
+        }
+        const int n16 = a.BW * ESZ / 16;
+        auto pad_row = [&](int br) {
+            const int v = br + a.row_lo;
+            T *row = pl + br * a.BW + A;
+            const T *src = pl + (pad_src32(v, a.H, a.pad) - a.row_lo) * a.BW + A;
+            for (int c16 = lane; c16 < n16; c16 += 32)
+                reinterpret_cast<uint4 *>(row - A)[c16] = reinterpret_cast<const uint4 *>(src - A)[c16];
+            __syncwarp();
+            if (lane < a.lpad) row[lane - a.lpad] = src[pad_src32(lane - a.lpad, a.W, a.pad)];
+            else if (lane < a.lpad + a.rpad) row[a.W + lane - a.lpad] = src[pad_src32(a.W + lane - a.lpad, a.W, a.pad)];
+        };
+        for (int br = max(br0, -a.tpad - a.row_lo); br < min(br1, -a.row_lo); ++br) pad_row(br);
+        for (int br = max(br0, a.H - a.row_lo); br < min(br1, a.H + a.bpad - a.row_lo); ++br) pad_row(br);
+        __syncwarp();
+    };
+
+    uint32_t seq0 = 0;  // sequence element of the current task's first slice
+    uint32_t acq = 0;   // next sequence element this warp has not yet waited for
+    uint32_t rel = 0;   // next sequence element this warp has not yet released
+    for (int t = (int)blockIdx.x; t < a.ntasks; t += (int)gridDim.x) {
+        int vol, m0, m1, zf, ns;
+        task_span(t, vol, m0, m1, zf, ns);
+        for (int mz = m0; mz < m1; ++mz) {
+            const uint32_t s0 = seq0 + (uint32_t)(zfirst(mz) - zf);
+            // the slices of this output slice: landed (and, first time, this band padded)
+            for (; acq < s0 + TZ; ++acq) {
+                const int b = (int)(acq % (uint32_t)S);
+                mbar_wait(&full[b], (acq / (uint32_t)S) & 1u);
+                if (a.pad != FCFS_PAD_ZERO && iy0 < iy1) pad_band(reinterpret_cast<T *>(pbuf + b * a.plane_bytes));
+            }
+            const T *sl[TZ];
+#pragma unroll
+            for (int i = 0; i < TZ; ++i) sl[i] = reinterpret_cast<const T *>(pbuf + ((s0 + i) % (uint32_t)S) * a.plane_bytes);
+            float wz[TZ];
+            const int jz = mz % a.pz;
+#pragma unroll
+            for (int i = 0; i < TZ; ++i) wz[i] = a.zw[jz][i];
+            const bool zcopy = jz == 0;
+            unsigned char *const out_plane = reinterpret_cast<unsigned char *>(a.out) +
+                                             ((int64_t)vol * a.out_plane_stride + (int64_t)mz * a.out_slice_stride) * ESZ;
+
+            auto period = [&](auto m_c, const int iy, unsigned char *const gp) {
+                constexpr int M = decltype(m_c)::value;
+                const int mr0 = iy * PY, mr1 = min(mr0 + PY, a.Ho);
+                const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(gp) & 15);
+                unsigned char *const sp = slots + (fk & 1) * a.slot_bytes;
+                if (lane == 0) bulk_wait_read1();
+                __syncwarp();
+                auto emit = [&](const int jy) {
+                    float o[KP];
+                    if (GY::frac0(jy)) {
+#pragma unroll
+                        for (int c = 0; c < KP; ++c) o[c] = hr[(M * QY + GY::base(jy) - GY::LO) % R][c];
+                    } else {
+                        const int bb = GY::base(jy);
+                        constexpr int H2 = KP / 2;
+#pragma unroll
+                        for (int c = 0; c < H2; ++c) {
+                            float2 v2 = fmul2_rn(GY::w(jy, 0), make_float2(hr[(M * QY + bb) % R][c], hr[(M * QY + bb) % R][c + H2]));
+#pragma unroll
+                            for (int tp = 1; tp < TY; ++tp)
+                                v2 = ffma2_rn(GY::w(jy, tp),
+                                              make_float2(hr[(M * QY + bb + tp) % R][c], hr[(M * QY + bb + tp) % R][c + H2]), v2);
+                            o[c] = v2.x;
+                            o[c + H2] = v2.y;
+                        }
+                        if constexpr (KP % 2 == 1) {
+                            float v1 = __fmul_rn(GY::w(jy, 0), hr[(M * QY + bb) % R][KP - 1]);
+#pragma unroll
+                            for (int tp = 1; tp < TY; ++tp) v1 = __fmaf_rn(GY::w(jy, tp), hr[(M * QY + bb + tp) % R][KP - 1], v1);
+                            o[KP - 1] = v1;
+                        }
+                    }
+                    store_row<T, KP>(reinterpret_cast<T *>(sp + mis + jy * rowb + col_b), o, KP);
+                    __syncwarp();
+                };
+#pragma unroll
+                for (int jy = 0; jy < PY; ++jy)
+                    if (GY::last_row(jy) < C) emit(jy);
+#pragma unroll
+                for (int r = C; r < L; ++r) {
+                    row_h(hr[(M * QY + r) % R], sl, iy * QY + r, wz, zcopy);
+#pragma unroll
+                    for (int jy = 0; jy < PY; ++jy)
+                        if (GY::last_row(jy) == r) emit(jy);
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                const int bytes = (mr1 - mr0) * rowb;
+                const int head = min(bytes, (int)((16 - mis) & 15));
+                const int body = (bytes - head) & ~15;
+                const int tail = bytes - head - body;
+                if (lane == 0) {
+                    if (body > 0) bulk_s2g(gp + head, sp + mis + head, (uint32_t)body);
+                    bulk_commit();
+                }
+                {
+                    const int e = lane & 7;
+                    const int off = (lane < 8 ? 0 : head + body) + e * ESZ;
+                    if (lane < 16 && e * ESZ < (lane < 8 ? head : tail))
+                        *reinterpret_cast<T *>(gp + off) = *reinterpret_cast<const T *>(sp + mis + off);
+                }
+                ++fk;
+            };
+            auto warm = [&](auto m_c) {
+                constexpr int M = decltype(m_c)::value;
+#pragma unroll
+                for (int r = 0; r < C; ++r) row_h(hr[(M * QY + r) % R], sl, iy0 * QY + r, wz, zcopy);
+            };
+            if (iy0 < iy1) {
+                const int mm0 = iy0 % U;
+                if (mm0 == 0) warm(std::integral_constant<int, 0>{});
+                if constexpr (U > 1) if (mm0 == 1) warm(std::integral_constant<int, (U > 1 ? 1 : 0)>{});
+                if constexpr (U > 2) if (mm0 == 2) warm(std::integral_constant<int, (U > 2 ? 2 : 0)>{});
+                if constexpr (U > 3) if (mm0 == 3) warm(std::integral_constant<int, (U > 3 ? 3 : 0)>{});
+                for (int iy = iy0; iy < iy1; ++iy) {
+                    const int m = iy % U;
+                    unsigned char *const gp = out_plane + (int64_t)(iy * PY) * rowb;
+                    auto go = [&](auto m_c) { period(m_c, iy, gp); };
+                    if (m == 0) go(std::integral_constant<int, 0>{});
+                    if constexpr (U > 1) if (m == 1) go(std::integral_constant<int, (U > 1 ? 1 : 0)>{});
+                    if constexpr (U > 2) if (m == 2) go(std::integral_constant<int, (U > 2 ? 2 : 0)>{});
+                    if constexpr (U > 3) if (m == 3) go(std::integral_constant<int, (U > 3 ? 3 : 0)>{});
+                }
+            }
+            // release the elements no later output slice of this task reads (all of
+            // them after the task's last output slice); the last warp reloads
+            const uint32_t keep = mz + 1 < m1 ? seq0 + (uint32_t)(zfirst(mz + 1) - zf) : seq0 + (uint32_t)ns;
+            if (rel < keep) {
+                fence_proxy_async_smem();  // this warp's reads and margin writes precede the reload
+                __syncwarp();
+                if (lane == 0) {
+                    for (; rel < keep; ++rel) {
+                        const int b = (int)(rel % (uint32_t)S);
+                        __threadfence_block();
+                        const int old = atomicAdd(&done[b], 1);
+                        if (old % kPlaneConsumerWarps == kPlaneConsumerWarps - 1) {
+                            __threadfence_block();
+                            issue(rel + (uint32_t)S);
+                        }
+                    }
+                }
+                rel = keep;
+            }
+        }
+        seq0 += (uint32_t)ns;
+    }
+    if (lane == 0) bulk_wait0();
+}
+
 }  // namespace fcfs
