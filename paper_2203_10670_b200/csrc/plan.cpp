@@ -551,7 +551,9 @@ bool plan_plane3(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     a.rpad = pl->pad == FCFS_PAD_ZERO ? 0 : (int32_t)std::max<int64_t>(0, reach_x - g.W);
     a.tpad = pl->pad == FCFS_PAD_ZERO ? 0 : -LOY;
     a.bpad = pl->pad == FCFS_PAD_ZERO ? 0 : (int32_t)std::max<int64_t>(0, reach_y - g.H);
-    if (a.lpad > A || g.W + a.rpad > a.BW - A || g.H + a.bpad - a.row_lo > a.BH) return false;
+    // (rows past BH are never read: BH covers every period's window rows, and the
+    // margin / padding-row writes stop at each band's last window row)
+    if (a.lpad > A || g.W + a.rpad > a.BW - A) return false;
     // runs of output slices: enough tasks for every SM, each run >= 4 output slices
     // (a run re-reads the taps - 1 slices its first output slice shares with the previous run)
     const int64_t sms = pl->sm_count > 0 ? pl->sm_count : 148;
