@@ -117,7 +117,7 @@ int launch_plane3(const FusedVariant *v, const Plane3Args &a, int grid, int smem
     }
     Plane3Args local = a;
     void *args[] = {&local};
-    return launch_pdl(v->fn, grid, kPlaneThreads, args, smem, stream);
+    return launch_pdl(v->fn, grid, 32 * kPlane3Warps, args, smem, stream);
 }
 
 int launch_pdl(const void *fn, int grid, int block, void **args, int smem, void *stream) {

@@ -539,7 +539,7 @@ bool plan_plane3(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     a.plane_bytes = (a.BW * a.BH * ESZ + 127) / 128 * 128;
     const int64_t rowb = g.Wo * ESZ;
     a.slot_bytes = (int32_t)((16 + PY * rowb + KP * ESZ + 15) / 16 * 16);
-    const int64_t fixed = 256 + 2 * kPlaneConsumerWarps * a.slot_bytes;
+    const int64_t fixed = 256 + kPlane3Slots * kPlane3Warps * a.slot_bytes;
     const int64_t budget = 227 * 1024;
     a.S = (int32_t)std::min<int64_t>(kPlane3MaxS, (budget - fixed) / a.plane_bytes);
     if (const char *e = std::getenv("FCFS_DEBUG_PLANE3_S")) a.S = std::min(a.S, std::atoi(e));
@@ -597,7 +597,7 @@ bool plan_plane3(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
                   "\"S\": %d, \"slot_bytes\": %d, \"chunks\": %d, \"ntasks\": %d, \"grid\": %d, \"block\": %d, "
                   "\"smem\": %d, \"busy_lanes\": %d, \"pads\": [%d, %d, %d, %d]}",
                   PY, QY, PX, QX, TX, K, a.nch, a.nper, a.BW, a.BH, a.plane_bytes, a.S, a.slot_bytes, a.chunks,
-                  a.ntasks, L.grid, kPlaneThreads, L.smem, a.nch, a.tpad, a.bpad, a.lpad, a.rpad);
+                  a.ntasks, L.grid, 32 * kPlane3Warps, L.smem, a.nch, a.tpad, a.bpad, a.lpad, a.rpad);
     if (std::getenv("FCFS_DEBUG_PRINT")) std::fprintf(stderr, "%s\n", L.desc);
     return true;
 }

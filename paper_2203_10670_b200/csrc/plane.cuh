@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kPlaneThreads, 2) fcfs_plane_kernel(const __gr
 // ---------------------------------------------------------------------------
 
 template <typename T, int PY0, int QY0, int PX0, int QX0, int T0, int LO0, int K>
-__global__ void __launch_bounds__(kPlaneThreads, 1) fcfs_plane3_kernel(const __grid_constant__ Plane3Args a) {
+__global__ void __launch_bounds__(32 * kPlane3Warps, 1) fcfs_plane3_kernel(const __grid_constant__ Plane3Args a) {
     using GY = GeoSel<PY0, QY0, T0, LO0, false>;
     using GX = GeoSel<PX0, QX0, T0, LO0, false>;
     constexpr int PY = GY::P, QY = GY::Q, PX = GX::P, QX = GX::Q;
@@ -394,11 +394,11 @@ __global__ void __launch_bounds__(kPlaneThreads, 1) fcfs_plane3_kernel(const __g
     const int e0 = A + chunk * K * QX + LOX;
     const int rowb = a.Wo * ESZ;
     const int col_b = chunk * KP * ESZ;
-    unsigned char *const slots = obuf + warp * 2 * a.slot_bytes;
+    unsigned char *const slots = obuf + warp * kPlane3Slots * a.slot_bytes;
     float hr[R][KP];
     uint32_t fk = 0;
     // this warp's fixed band of y-periods and the buffer rows it reads
-    const int iy0 = warp * a.nper / kPlaneConsumerWarps, iy1 = (warp + 1) * a.nper / kPlaneConsumerWarps;
+    const int iy0 = warp * a.nper / kPlane3Warps, iy1 = (warp + 1) * a.nper / kPlane3Warps;
     const int br0 = iy0 * QY, br1 = min(a.BH, (iy1 - 1) * QY + L);
 
     // horizontal taps of one window row combined over the TZ slices of sl[]
@@ -410,11 +410,19 @@ __global__ void __launch_bounds__(kPlaneThreads, 1) fcfs_plane3_kernel(const __g
             for (int t = 0; t < TZ; ++t) {
                 float sub[WIN];
                 load_win<T, WIN, PAR>(sl[t] + br * a.BW, e0, sub);
+                // packed pairs (FMUL2 / FFMA2: each lane an RN op, the scalar chain's bits)
 #pragma unroll
-                for (int i = 0; i < WIN; ++i) {
-                    acc[i] = t == 0 ? __fmul_rn(wz[0], sub[i]) : __fmaf_rn(wz[t], sub[i], acc[i]);
-                    if (t == -LOZ) cp[i] = sub[i];
+                for (int i = 0; i + 1 < WIN; i += 2) {
+                    float2 v2 = t == 0 ? fmul2_rn(wz[0], make_float2(sub[i], sub[i + 1]))
+                                       : ffma2_rn(wz[t], make_float2(sub[i], sub[i + 1]), make_float2(acc[i], acc[i + 1]));
+                    acc[i] = v2.x;
+                    acc[i + 1] = v2.y;
                 }
+                if constexpr (WIN % 2 == 1)
+                    acc[WIN - 1] = t == 0 ? __fmul_rn(wz[0], sub[WIN - 1]) : __fmaf_rn(wz[t], sub[WIN - 1], acc[WIN - 1]);
+#pragma unroll
+                for (int i = 0; i < WIN; ++i)
+                    if (t == -LOZ) cp[i] = sub[i];
             }
 #pragma unroll
             for (int i = 0; i < WIN; ++i) win[i] = zcopy ? cp[i] : acc[i];
@@ -508,8 +516,12 @@ __global__ void __launch_bounds__(kPlaneThreads, 1) fcfs_plane3_kernel(const __g
                 constexpr int M = decltype(m_c)::value;
                 const int mr0 = iy * PY, mr1 = min(mr0 + PY, a.Ho);
                 const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(gp) & 15);
-                unsigned char *const sp = slots + (fk & 1) * a.slot_bytes;
-                if (lane == 0) bulk_wait_read1();
+                unsigned char *const sp = slots + (fk % kPlane3Slots) * a.slot_bytes;
+                // the slot's previous bulk store has read it
+                if (lane == 0) {
+                    if constexpr (kPlane3Slots == 1) bulk_wait_read0();
+                    else bulk_wait_read1();
+                }
                 __syncwarp();
                 auto emit = [&](const int jy) {
                     float o[KP];
@@ -599,7 +611,7 @@ __global__ void __launch_bounds__(kPlaneThreads, 1) fcfs_plane3_kernel(const __g
                         const int b = (int)(rel % (uint32_t)S);
                         __threadfence_block();
                         const int old = atomicAdd(&done[b], 1);
-                        if (old % kPlaneConsumerWarps == kPlaneConsumerWarps - 1) {
+                        if (old % kPlane3Warps == kPlane3Warps - 1) {
                             __threadfence_block();
                             issue(rel + (uint32_t)S);
                         }
