@@ -264,7 +264,7 @@ int launch_plane(const FusedVariant *v, const PlaneArgs &a, int grid, int smem, 
 // Volumes of small slices (plane.cuh fcfs_plane3_kernel): a ring of S whole
 // padded input slices, a task = a run of output slices of one volume.
 constexpr int kPlane3MaxS = 8;
-constexpr int kPlane3Warps = 12;  // one band of y-periods each (one CTA per SM)
+constexpr int kPlane3Warps = 16;  // one band of y-periods each (one CTA per SM)
 constexpr int kPlane3Slots = 1;   // output staging slots per warp
 struct Plane3Args {
     // 4D tiled TMA descriptor of the input (columns, rows, slices, volumes), box (BW, BH, 1, 1);
