@@ -238,7 +238,13 @@ constexpr int kFusedThreads = 32 * (2 + kFusedConsumerWarps);  // issuer warp, p
 // Plane-resident fused kernel (plane.cuh): batches of small 2D planes, a whole
 // padded input plane per TMA box, one warp per band of y-periods across the
 // full output width (at most 32 column chunks).
-constexpr int kPlaneConsumerWarps = 8;  // 16 warps per SM at two CTAs (<= 128 registers per thread)
+#ifndef FCFS_PLANE_WARPS
+#define FCFS_PLANE_WARPS 8
+#define FCFS_PLANE_SLOTS 2
+#endif
+constexpr int kPlaneConsumerWarps = FCFS_PLANE_WARPS;  // 16 warps per SM at two CTAs (<= 128 registers per thread)
+constexpr int kPlaneSlots = FCFS_PLANE_SLOTS;          // output staging slots per warp
+constexpr int kPlaneCtasPerSm = 2;
 constexpr int kPlaneThreads = 32 * kPlaneConsumerWarps;   // every warp computes; no producer warp
 struct PlaneArgs {
     // 3D tiled TMA descriptor of the input (columns, rows, planes), box (BW, BH, 1);

@@ -440,7 +440,7 @@ bool plan_plane(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     a.plane_bytes = (a.BW * a.BH * ESZ + 127) / 128 * 128;
     const int64_t rowb = g.Wo * ESZ;
     a.slot_bytes = (int32_t)((16 + PY * rowb + KP * ESZ + 15) / 16 * 16);
-    L.smem = 256 + 2 * a.plane_bytes + 2 * kPlaneConsumerWarps * a.slot_bytes;
+    L.smem = 256 + 2 * a.plane_bytes + kPlaneSlots * kPlaneConsumerWarps * a.slot_bytes;
     if (L.smem > 112 * 1024) return false;  // two CTAs per SM
     // margins the kept outputs read (written by the producer for replicate / reflect)
     const int64_t reach_x = ((g.Wo - 1) / PX) * QX + LOX + geo[24 + (int)((g.Wo - 1) % PX)] + TX;

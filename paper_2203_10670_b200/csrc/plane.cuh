@@ -54,7 +54,7 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 
 template <typename T, int PY0, int QY0, int PX0, int QX0, int T0, int LO0, int K>
-__global__ void __launch_bounds__(kPlaneThreads, 2) fcfs_plane_kernel(const __grid_constant__ PlaneArgs a) {
+__global__ void __launch_bounds__(kPlaneThreads, kPlaneCtasPerSm) fcfs_plane_kernel(const __grid_constant__ PlaneArgs a) {
     using GY = GeoSel<PY0, QY0, T0, LO0, false>;
     using GX = GeoSel<PX0, QX0, T0, LO0, false>;
     constexpr int PY = GY::P, QY = GY::Q, PX = GX::P, QX = GX::Q;
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kPlaneThreads, 2) fcfs_plane_kernel(const __gr
     const int e0 = A + chunk * K * QX + LOX;  // window start (element) in a plane-buffer row
     const int rowb = a.Wo * ESZ;
     const int col_b = chunk * KP * ESZ;       // this lane's byte offset inside a staging row
-    unsigned char *const slots = obuf + warp * 2 * a.slot_bytes;
+    unsigned char *const slots = obuf + warp * kPlaneSlots * a.slot_bytes;
     float hr[R][KP];  // ring of horizontally filtered window rows
     uint32_t fk = 0;  // periods flushed by this warp (staging slot = fk & 1)
 
@@ -194,10 +194,13 @@ __global__ void __launch_bounds__(kPlaneThreads, 2) fcfs_plane_kernel(const __gr
             constexpr int M = decltype(m_c)::value;
             const int m0 = iy * PY, m1 = min(m0 + PY, a.Ho);
             const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(gp) & 15);
-            unsigned char *const sp = slots + (fk & 1) * a.slot_bytes;  // span start co-aligned at sp + mis
+            unsigned char *const sp = slots + (fk % kPlaneSlots) * a.slot_bytes;  // span start co-aligned at sp + mis
             const T *const prow = pl + iy * QY * a.BW;  // window row 0 of this period
             // the slot's previous bulk store (two periods ago) has read it
-            if (lane == 0) bulk_wait_read1();
+            if (lane == 0) {
+                if constexpr (kPlaneSlots == 1) bulk_wait_read0();
+                else bulk_wait_read1();
+            }
             __syncwarp();
             auto emit = [&](const int jy) {
                 float o[KP];
