@@ -227,7 +227,6 @@ struct FusedVariant {
     // geometry the kernel runs (GeoSel): [0..3] rows P, Q, TAPS, LO; [4..7] columns;
     // [8..23] rows' per-phase base offsets; [24..39] columns'
     const int *geo;
-    const void *fn_bm = nullptr;   // plane variants: the band-major lane map (fcfs_plane_bm_kernel)
 };
 const FusedVariant *fused_lookup(int dtype, int py, int qy, int px, int qx, int ntaps, bool slices);
 const FusedVariant *fused_lookup_adjoint(int dtype, int py, int qy, int px, int qx, int ntaps);
@@ -263,10 +262,6 @@ struct PlaneArgs {
     int32_t slot_bytes;        // one staging slot (a y-period's rows + spill, 16-B multiple)
     int32_t lpad, rpad;        // margin columns the kept outputs read (left of 0 / from W on)
     int32_t tpad, bpad;        // margin rows the kept outputs read (above 0 / from H on)
-    // band-major lane map (fcfs_plane_bm_kernel): the CTA's 256 lanes are bm_bands
-    // bands x nch chunks, a band = bm_L0 y-periods (a multiple of the ring phases);
-    // bm_rowp: staging bytes per output row of a warp (its <= 3 band segments)
-    int32_t bm_bands, bm_L0, bm_rowp;
 };
 // The plane-resident variant of the 2D layer (py/qy, px/qx) with ntaps taps, or nullptr.
 const FusedVariant *plane_lookup(int dtype, int py, int qy, int px, int qx, int ntaps);

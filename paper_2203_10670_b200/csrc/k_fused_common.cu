@@ -87,20 +87,19 @@ int launch_fused(const FusedVariant *v, const FusedArgs &a, int grid, int block,
 int launch_plane(const FusedVariant *v, const PlaneArgs &a, int grid, int smem, void *stream) {
     static std::mutex mu;
     static std::set<std::pair<const void *, int>> configured;  // (fn, device)
-    const void *fn = a.bm_bands > 0 ? v->fn_bm : v->fn;
     int dev = 0;
     cudaGetDevice(&dev);
     {
         std::lock_guard<std::mutex> lk(mu);
-        if (!configured.count({fn, dev})) {
-            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        if (!configured.count({v->fn, dev})) {
+            cudaError_t e = cudaFuncSetAttribute(v->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
             if (e != cudaSuccess) return (int)e;
-            configured.insert({fn, dev});
+            configured.insert({v->fn, dev});
         }
     }
     PlaneArgs local = a;
     void *args[] = {&local};
-    return launch_pdl(fn, grid, kPlaneThreads, args, smem, stream);
+    return launch_pdl(v->fn, grid, kPlaneThreads, args, smem, stream);
 }
 
 int launch_plane3(const FusedVariant *v, const Plane3Args &a, int grid, int smem, void *stream) {

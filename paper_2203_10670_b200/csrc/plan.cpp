@@ -442,22 +442,6 @@ bool plan_plane(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     a.slot_bytes = (int32_t)((16 + PY * rowb + KP * ESZ + 15) / 16 * 16);
     L.smem = 256 + 2 * a.plane_bytes + kPlaneSlots * kPlaneConsumerWarps * a.slot_bytes;
     if (L.smem > 112 * 1024) return false;  // two CTAs per SM
-    // band-major lane map (fcfs_plane_bm_kernel) when a row leaves lanes idle:
-    // 16 <= chunks < 32 (a warp holds <= 3 band segments, 3 x PY copy-out spans <= 32)
-    a.bm_bands = 0;
-    if (v->fn_bm && a.nch >= 16 && a.nch < 32 && 3 * PY <= 32 && std::getenv("FCFS_PLANE_BM")) {
-        const int nb = 32 * kPlaneConsumerWarps / a.nch;
-        const int per = (a.nper + nb - 1) / nb;
-        const int L0 = (per + U - 1) / U * U;
-        const int rowp = (32 * KP * ESZ + 3 * 48 + 15) / 16 * 16;  // 3 segments: 16-B rounding + 32 slack each
-        const int smem_bm = 256 + 2 * a.plane_bytes + kPlaneConsumerWarps * PY * rowp;
-        if (smem_bm <= 112 * 1024) {
-            a.bm_bands = nb;
-            a.bm_L0 = L0;
-            a.bm_rowp = rowp;
-            L.smem = smem_bm;
-        }
-    }
     // margins the kept outputs read (written by the producer for replicate / reflect)
     const int64_t reach_x = ((g.Wo - 1) / PX) * QX + LOX + geo[24 + (int)((g.Wo - 1) % PX)] + TX;
     const int64_t reach_y = ((g.Ho - 1) / PY) * QY + LOY + geo[8 + (int)((g.Ho - 1) % PY)] + TY;
@@ -497,13 +481,9 @@ bool plan_plane(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
                   "{\"kernel\": \"fused_plane\", \"PY\": %d, \"QY\": %d, \"PX\": %d, \"QX\": %d, \"taps\": %d, "
                   "\"K\": %d, \"nch\": %d, \"periods\": %d, \"ring_phases\": %d, \"BW\": %d, \"BH\": %d, "
                   "\"plane_bytes\": %d, \"slot_bytes\": %d, \"bands\": %d, \"grid\": %d, \"block\": %d, "
-                  "\"smem\": %d, \"busy_lanes\": %d, \"lane_map\": \"%s\", \"band_periods\": %d, "
-                  "\"pads\": [%d, %d, %d, %d]}",
+                  "\"smem\": %d, \"busy_lanes\": %d, \"pads\": [%d, %d, %d, %d]}",
                   PY, QY, PX, QX, TX, K, a.nch, a.nper, U, a.BW, a.BH, a.plane_bytes, a.slot_bytes,
-                  a.bm_bands ? a.bm_bands : kPlaneConsumerWarps, L.grid, kPlaneThreads, L.smem,
-                  a.bm_bands ? a.bm_bands * a.nch : kPlaneConsumerWarps * a.nch, a.bm_bands ? "band_major" : "row",
-                  a.bm_bands ? a.bm_L0 : (a.nper + kPlaneConsumerWarps - 1) / kPlaneConsumerWarps,
-                  a.tpad, a.bpad, a.lpad, a.rpad);
+                  kPlaneConsumerWarps, L.grid, kPlaneThreads, L.smem, a.nch, a.tpad, a.bpad, a.lpad, a.rpad);
     if (std::getenv("FCFS_DEBUG_PRINT")) std::fprintf(stderr, "%s\n", L.desc);
     return true;
 }
@@ -896,7 +876,7 @@ fcfs_status launch(const Prepared &pr, void *stream) {
     int rc = 0;
     if (pr.kernel == 1) rc = launch_nearest(pr.pl->dtype, pr.na, stream);
     else if (pr.kernel == 2) rc = launch_fused(pr.pl->fused, pr.L.a, pr.L.grid, kFusedThreads, pr.L.smem, stream);
-    else if (pr.kernel == 4) rc = launch_plane(pr.pl->plane, pr.L.pa, pr.L.grid, pr.L.smem, stream);  // (band-major when pa.bm_bands)
+    else if (pr.kernel == 4) rc = launch_plane(pr.pl->plane, pr.L.pa, pr.L.grid, pr.L.smem, stream);
     else if (pr.kernel == 5) rc = launch_plane3(pr.pl->plane3, pr.L.p3, pr.L.grid, pr.L.smem, stream);
     else if (pr.kernel == 3) rc = launch_tile(pr.pl->dtype, pr.ta, pr.tgrid, pr.tsmem, stream);
     else if (pr.kernel == 0) rc = launch_reference(pr.pl->dtype, pr.ra, stream);

@@ -301,283 +301,6 @@ __global__ void __launch_bounds__(kPlaneThreads, kPlaneCtasPerSm) fcfs_plane_ker
 }
 
 // ---------------------------------------------------------------------------
-// Band-major lane map for planes whose output row has fewer than 32 chunks
-// (C3: 213 columns = 22 chunks of 10, so the row-per-warp map above leaves 10
-// of 32 lanes idle).  The CTA's 256 lanes form bm_bands = 256 / nch bands of
-// nch consecutive lanes (C3: 11 bands, 242 busy lanes); band b owns y-periods
-// [b L0, (b + 1) L0) of the plane, L0 a multiple of the ring phases U so that
-// every lane of a warp sits at the same ring phase (period t of every band at
-// once).  A warp holds up to three band segments (a band may straddle two
-// warps).  Each warp flushes its own segments: the lanes write their chunks
-// into a per-warp staging row (each segment co-aligned mod 16 with its global
-// row span), then groups of lanes copy each (segment, row) span with 16-B
-// shared loads and global stores (partial rows are not contiguous in global
-// memory, so no bulk copy) and the ragged head / tail elements.  No barrier
-// between warps; one staging slot (the copies are synchronous).  Same
-// arithmetic per output as the kernels above (bitwise equal).
-template <typename T, int PY0, int QY0, int PX0, int QX0, int T0, int LO0, int K>
-__global__ void __launch_bounds__(kPlaneThreads, kPlaneCtasPerSm) fcfs_plane_bm_kernel(const __grid_constant__ PlaneArgs a) {
-    using GY = GeoSel<PY0, QY0, T0, LO0, false>;
-    using GX = GeoSel<PX0, QX0, T0, LO0, false>;
-    constexpr int PY = GY::P, QY = GY::Q, PX = GX::P, QX = GX::Q;
-    constexpr int TY = GY::TAPS, TX = GX::TAPS, LOX = GX::LO;
-    constexpr int L = GY::L, C = GY::C;
-    constexpr int KP = K * PX;
-    constexpr int WIN = (K - 1) * QX + GX::L;
-    constexpr int ESZ = sizeof(T);
-    constexpr int A = 16 / ESZ;
-    constexpr int PAR = (ESZ == 2 && (K * QX) % 2 == 0) ? ((LOX % 2 + 2) % 2) : -1;
-    constexpr int R = QY * ((L + QY - 1) / QY);
-    constexpr int U = R / QY;
-    constexpr int SEGMAX = 3;
-    static_assert(PX <= 16 && PY <= 16, "plane variants have p <= 16");
-
-    extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem);
-    int *done = reinterpret_cast<int *>(smem + 64);
-    unsigned char *pbuf = smem + 256;
-    unsigned char *obuf = pbuf + 2 * a.plane_bytes;  // per warp: PY staging rows of bm_rowp bytes
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nmine = a.planes > (int)blockIdx.x ? (a.planes - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-    const uint32_t box_bytes = (uint32_t)(a.BW * a.BH * ESZ);
-    auto issue = [&](int n) {
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&full[n & 1], box_bytes);
-        tma_load_3d(pbuf + (n & 1) * a.plane_bytes, &a.tmap, -A, a.row_lo, (int)blockIdx.x + n * (int)gridDim.x,
-                    &full[n & 1], policy_evict_first());
-    };
-    if (threadIdx.x == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-        done[0] = done[1] = 0;
-        mbar_fence_init();
-    }
-    __syncthreads();
-    pdl_wait();
-    pdl_launch_dependents();
-    if (threadIdx.x == 0) {
-        if (nmine > 0) issue(0);
-        if (nmine > 1) issue(1);
-    }
-
-    // lane map: virtual lane vl -> (band, chunk); lanes past the last band repeat the
-    // CTA's last real lane (same values to the same staging addresses, in warp 7)
-    const int nch = a.nch, nb = a.bm_bands, L0 = a.bm_L0;
-    const int vlast = nb * nch - 1;
-    const int vl = min(warp * 32 + lane, vlast);
-    const int band = vl / nch, chunk = vl - band * nch;
-    // this warp's band segments (warp-uniform): s = band - b_first
-    const int vw0 = min(warp * 32, vlast), vw1 = min(warp * 32 + 31, vlast);
-    const int b_first = vw0 / nch, nseg = vw1 / nch - b_first + 1;
-    const int seg = band - b_first;
-    // first chunk (in band coordinates) and first lane of each segment, its chunk count
-    int sch0[SEGMAX], slane0[SEGMAX], snch[SEGMAX];
-#pragma unroll
-    for (int s = 0; s < SEGMAX; ++s) {
-        const int b = b_first + s;
-        const int v0 = max(vw0, b * nch), v1 = min(vw1, b * nch + nch - 1);
-        sch0[s] = v0 - b * nch;
-        slane0[s] = v0 - vw0;
-        snch[s] = s < nseg ? v1 - v0 + 1 : 0;
-    }
-    const int e0 = A + chunk * K * QX + LOX;
-    const int rowb = a.Wo * ESZ;
-    // segment s of staging row jy: obuf_w + jy * rowp + segbase(slane0[s], s) + (global span start & 15)
-    unsigned char *const stw = obuf + warp * PY * a.bm_rowp;
-    int my_slane0 = 0, my_sch0 = 0;
-#pragma unroll
-    for (int s = 0; s < SEGMAX; ++s)
-        if (s == seg) my_slane0 = slane0[s], my_sch0 = sch0[s];
-    // a segment's staging starts 16-B aligned (its copy-out uses 16-B shared loads)
-    auto segbase = [&](int l0, int s) { return ((l0 * KP * ESZ + 15) & ~15) + 32 * s; };
-    const int my_off = segbase(my_slane0, seg) + (lane - my_slane0) * KP * ESZ;
-    float hr[R][KP];
-
-    auto row_h = [&](float(&h)[KP], const T *srow) {
-        float win[WIN];
-        load_win<T, WIN, PAR>(srow, e0, win);
-        if constexpr (K == 2) {
-#pragma unroll
-            for (int jx = 0; jx < PX; ++jx) {
-                if (GX::frac0(jx)) {
-                    h[jx] = win[GX::base(jx) - LOX];
-                    h[PX + jx] = win[QX + GX::base(jx) - LOX];
-                } else {
-                    const int bb = GX::base(jx);
-                    float2 v2 = fmul2_rn(GX::w(jx, 0), make_float2(win[bb], win[QX + bb]));
-#pragma unroll
-                    for (int tp = 1; tp < TX; ++tp)
-                        v2 = ffma2_rn(GX::w(jx, tp), make_float2(win[bb + tp], win[QX + bb + tp]), v2);
-                    h[jx] = v2.x;
-                    h[PX + jx] = v2.y;
-                }
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-#pragma unroll
-                for (int jx = 0; jx < PX; ++jx) {
-                    float v;
-                    if (GX::frac0(jx)) {
-                        v = win[k * QX + GX::base(jx) - LOX];
-                    } else {
-                        const int bb = k * QX + GX::base(jx);
-                        v = __fmul_rn(GX::w(jx, 0), win[bb]);
-#pragma unroll
-                        for (int tp = 1; tp < TX; ++tp) v = __fmaf_rn(GX::w(jx, tp), win[bb + tp], v);
-                    }
-                    h[k * PX + jx] = v;
-                }
-            }
-        }
-    };
-
-    // periods of band b: [b L0, min((b + 1) L0, nper)); the warp runs its longest segment's
-    int steps = 0;
-#pragma unroll
-    for (int s = 0; s < SEGMAX; ++s)
-        if (s < nseg) steps = max(steps, min(L0, a.nper - (b_first + s) * L0));
-    const int iy0 = band * L0;  // this lane's band start (a multiple of U: ring phase 0)
-
-    for (int n = 0; n < nmine; ++n) {
-        const int plane = (int)blockIdx.x + n * (int)gridDim.x;
-        T *const pl = reinterpret_cast<T *>(pbuf + (n & 1) * a.plane_bytes);
-        mbar_wait(&full[n & 1], (n >> 1) & 1);
-        if (a.pad != FCFS_PAD_ZERO) {
-            // margins of the rows each of this warp's bands reads (§3 Padding); neighbouring
-            // bands and warps write the same values into rows they share
-            const int n16 = a.BW * ESZ / 16;
-            for (int s = 0; s < nseg; ++s) {
-                const int b0 = (b_first + s) * L0, b1 = min(b0 + L0, a.nper);
-                if (b0 >= b1) continue;
-                const int br0 = b0 * QY, br1 = min(a.BH, (b1 - 1) * QY + L);
-                for (int br = br0 + lane; br < br1; br += 32) {
-                    const int v = br + a.row_lo;
-                    if (v < 0 || v >= a.H) continue;
-                    T *row = pl + br * a.BW + A;
-                    for (int c = -a.lpad; c < 0; ++c) row[c] = row[pad_src32(c, a.W, a.pad)];
-                    for (int c = a.W; c < a.W + a.rpad; ++c) row[c] = row[pad_src32(c, a.W, a.pad)];
-                }
-                auto pad_row = [&](int br) {
-                    const int v = br + a.row_lo;
-                    T *row = pl + br * a.BW + A;
-                    const T *src = pl + (pad_src32(v, a.H, a.pad) - a.row_lo) * a.BW + A;
-                    for (int c16 = lane; c16 < n16; c16 += 32)
-                        reinterpret_cast<uint4 *>(row - A)[c16] = reinterpret_cast<const uint4 *>(src - A)[c16];
-                    __syncwarp();
-                    if (lane < a.lpad) row[lane - a.lpad] = src[pad_src32(lane - a.lpad, a.W, a.pad)];
-                    else if (lane < a.lpad + a.rpad) row[a.W + lane - a.lpad] = src[pad_src32(a.W + lane - a.lpad, a.W, a.pad)];
-                };
-                for (int br = max(br0, -a.tpad - a.row_lo); br < min(br1, -a.row_lo); ++br) pad_row(br);
-                for (int br = max(br0, a.H - a.row_lo); br < min(br1, a.H + a.bpad - a.row_lo); ++br) pad_row(br);
-            }
-            __syncwarp();
-        }
-        unsigned char *const out_plane =
-            reinterpret_cast<unsigned char *>(a.out) + ((int64_t)plane * a.out_plane_stride) * ESZ;
-
-        auto period = [&](auto m_c, const int t) {
-            constexpr int M = decltype(m_c)::value;
-            const int iy = min(iy0 + t, a.nper - 1);  // past the band's end: any valid rows (not flushed)
-            const T *const prow = pl + iy * QY * a.BW;
-            auto emit = [&](const int jy) {
-                float o[KP];
-                if (GY::frac0(jy)) {
-#pragma unroll
-                    for (int c = 0; c < KP; ++c) o[c] = hr[(M * QY + GY::base(jy) - GY::LO) % R][c];
-                } else {
-                    const int bb = GY::base(jy);
-                    constexpr int H2 = KP / 2;
-#pragma unroll
-                    for (int c = 0; c < H2; ++c) {
-                        float2 v2 = fmul2_rn(GY::w(jy, 0), make_float2(hr[(M * QY + bb) % R][c], hr[(M * QY + bb) % R][c + H2]));
-#pragma unroll
-                        for (int tp = 1; tp < TY; ++tp)
-                            v2 = ffma2_rn(GY::w(jy, tp),
-                                          make_float2(hr[(M * QY + bb + tp) % R][c], hr[(M * QY + bb + tp) % R][c + H2]), v2);
-                        o[c] = v2.x;
-                        o[c + H2] = v2.y;
-                    }
-                    if constexpr (KP % 2 == 1) {
-                        float v1 = __fmul_rn(GY::w(jy, 0), hr[(M * QY + bb) % R][KP - 1]);
-#pragma unroll
-                        for (int tp = 1; tp < TY; ++tp) v1 = __fmaf_rn(GY::w(jy, tp), hr[(M * QY + bb + tp) % R][KP - 1], v1);
-                        o[KP - 1] = v1;
-                    }
-                }
-                // the lane's segment span of row jy starts at global g (mod 16 = mis)
-                const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(out_plane) +
-                                                (uint32_t)((iy * PY + jy) * rowb + my_sch0 * KP * ESZ)) & 15u;
-                store_row<T, KP>(reinterpret_cast<T *>(stw + jy * a.bm_rowp + my_off + mis), o, KP);
-            };
-#pragma unroll
-            for (int jy = 0; jy < PY; ++jy)
-                if (GY::last_row(jy) < C) emit(jy);
-#pragma unroll
-            for (int r = C; r < L; ++r) {
-                row_h(hr[(M * QY + r) % R], prow + r * a.BW);
-#pragma unroll
-                for (int jy = 0; jy < PY; ++jy)
-                    if (GY::last_row(jy) == r) emit(jy);
-            }
-            __syncwarp();
-            // copy-out: (segment, row) spans, G lanes each (16-B vectors, then head / tail)
-            const int nspan = nseg * PY, G = 32 / nspan;
-            const int sp = lane / G, k = lane - sp * G;
-            if (sp < nspan) {
-                const int s = sp / PY, jy = sp - s * PY;
-                int s_ch0 = 0, s_l0 = 0, s_n = 0;
-#pragma unroll
-                for (int q = 0; q < SEGMAX; ++q)
-                    if (q == s) s_ch0 = sch0[q], s_l0 = slane0[q], s_n = snch[q];
-                const int ib = (b_first + s) * L0 + t;  // the segment's period
-                const int m = ib * PY + jy;             // output row
-                if (ib < min((b_first + s + 1) * L0, a.nper) && m < a.Ho) {
-                    unsigned char *g = out_plane + (int64_t)m * rowb + s_ch0 * KP * ESZ;
-                    const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(g) & 15u);
-                    const unsigned char *src = stw + jy * a.bm_rowp + segbase(s_l0, s) + mis;
-                    const int len = (min(a.Wo, (s_ch0 + s_n) * KP) - s_ch0 * KP) * ESZ;
-                    const int head = min(len, (int)((16u - mis) & 15u));
-                    const int body = (len - head) & ~15;
-                    for (int v = k; v < body / 16; v += G)
-                        *reinterpret_cast<uint4 *>(g + head + 16 * v) = *reinterpret_cast<const uint4 *>(src + head + 16 * v);
-                    if (k == 0)
-                        for (int e = 0; e < head; e += ESZ) *reinterpret_cast<T *>(g + e) = *reinterpret_cast<const T *>(src + e);
-                    if (k == G - 1)
-                        for (int e = head + body; e < len; e += ESZ) *reinterpret_cast<T *>(g + e) = *reinterpret_cast<const T *>(src + e);
-                }
-            }
-            __syncwarp();  // the staging rows are free for the next period
-        };
-        // warm-up: window rows 0..C-1 of the band's first period (ring phase 0)
-        {
-            const int iyw = min(iy0, a.nper - 1);
-#pragma unroll
-            for (int r = 0; r < C; ++r) row_h(hr[r % R], pl + (iyw * QY + r) * a.BW);
-        }
-        static_assert(U <= 4, "ring phases");
-        for (int t = 0; t < steps; ++t) {
-            const int m = t % U;
-            if (m == 0) period(std::integral_constant<int, 0>{}, t);
-            if constexpr (U > 1) if (m == 1) period(std::integral_constant<int, (U > 1 ? 1 : 0)>{}, t);
-            if constexpr (U > 2) if (m == 2) period(std::integral_constant<int, (U > 2 ? 2 : 0)>{}, t);
-            if constexpr (U > 3) if (m == 3) period(std::integral_constant<int, (U > 3 ? 3 : 0)>{}, t);
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-            __threadfence_block();
-            const int old = atomicAdd(&done[n & 1], 1);
-            if (old % kPlaneConsumerWarps == kPlaneConsumerWarps - 1 && n + 2 < nmine) {
-                __threadfence_block();
-                issue(n + 2);
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
 // Volumes of small slices (3D layers, §4.2 per-dimension factors with a slice
 // factor pz/qz): the same plane-resident scheme over a RING of S input slices.
 // A task is a run of output slices [mz0, mz1) of one volume; output slice mz

@@ -7,8 +7,7 @@
 #define FCFS_PLANE_VARIANT(T, PY, QY, PX, QX, TAPS, LO)                                                               \
     {reinterpret_cast<const void *>(&fcfs::fcfs_plane_kernel<T, PY, QY, PX, QX, TAPS, LO, fcfs::fused_k<T, PX, QX>()>), \
      PY, QY, PX, QX, TAPS, LO, fcfs::fused_k<T, PX, QX>(), 1, fcfs::PhaseW<PY, QY, TAPS>::tab.v,                         \
-     fcfs::PhaseW<PX, QX, TAPS>::tab.v, 0, 1, VariantGeo<PY, QY, PX, QX, TAPS, LO, false>::tab.v,                      \
-     reinterpret_cast<const void *>(&fcfs::fcfs_plane_bm_kernel<T, PY, QY, PX, QX, TAPS, LO, fcfs::fused_k<T, PX, QX>()>)},
+     fcfs::PhaseW<PX, QX, TAPS>::tab.v, 0, 1, VariantGeo<PY, QY, PX, QX, TAPS, LO, false>::tab.v},
 #define FCFS_PLANE_BOTH_MODES(T, PY, QY, PX, QX) \
     FCFS_PLANE_VARIANT(T, PY, QY, PX, QX, 2, 0) FCFS_PLANE_VARIANT(T, PY, QY, PX, QX, 4, -1)
 
