@@ -118,7 +118,10 @@ def test_height_only_variants(pad):
 
 
 @pytest.mark.parametrize("pad", PADS)
-def test_volume_variants(pad):
+def test_volume_variants(pad, monkeypatch):
+    # the row-pipelined 3D variants (the slice-ring plane kernel, which takes most
+    # of these volumes by default, has its own table test: test_gpu_plane3.py)
+    monkeypatch.setenv("FCFS_NO_PLANE3", "1")
     for i, P, Q, mode, dtype in _cases(ZPAIRS):
         pz, qz = SLICE_FACTORS[i % len(SLICE_FACTORS)]
         ext = ["floor", "paper"][i % 2]
