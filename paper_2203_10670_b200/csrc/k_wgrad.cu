@@ -380,6 +380,16 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
             : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
+// two 16-bit shared loads at byte offsets O0 and O1 from addr, packed (O0 in the low half)
+template <int O0, int O1>
+__device__ __forceinline__ uint32_t lds_pair(uint32_t addr) {
+    unsigned short lo, hi;
+    asm volatile("ld.shared.u16 %0, [%2+%3];\n\tld.shared.u16 %1, [%2+%4];"
+                 : "=h"(lo), "=h"(hi)
+                 : "r"(addr), "n"(O0), "n"(O1));
+    return __byte_perm((uint32_t)lo, (uint32_t)hi, 0x5410);
+}
+
 template <typename T, int PY, int QY, int PX, int QX, int NT>
 __global__ void __launch_bounds__(256) fcfs_wgrad_mma_kernel(const __grid_constant__ WgradArgs a) {
     constexpr int LO = NT == 4 ? -1 : 0;
@@ -525,17 +535,30 @@ __global__ void __launch_bounds__(256) fcfs_wgrad_mma_kernel(const __grid_consta
         // this warp's contiguous share of the blocks, walked row by row (no division per block)
         const int b0 = warp * nblk / 8, b1 = (warp + 1) * nblk / 8;
         int iy = b0 / nxb, xb = b0 - iy * nxb;
+        // 32-bit shared byte addresses of every fragment element's base, fixed for the
+        // task (kept in registers, not re-derived per block), plus the block's offset
+        uint32_t aad[2 * MT], bad[NTL];
+#pragma unroll
+        for (int i = 0; i < 2 * MT; ++i) {
+            aad[i] = smem_u32(gs) + 2u * (uint32_t)(bd.gsh + abase[i]);
+            asm volatile("" : "+r"(aad[i]));
+        }
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) {
+            bad[j] = smem_u32(xs) + 2u * (uint32_t)bbase[j];
+            asm volatile("" : "+r"(bad[j]));
+        }
+        uint32_t offa = 2u * (uint32_t)(iy * PY * a.Wo + xb * 16 * PX), offb = 2u * (uint32_t)(iy * QY * XP + xb * 16 * QX);
+        const uint32_t rowa = 2u * (uint32_t)(PY * a.Wo), rowb = 2u * (uint32_t)(QY * XP);
         for (int blk = b0; blk < b1; ++blk) {
-            const uint16_t *ga = gs + bd.gsh + iy * PY * a.Wo + xb * 16 * PX;
-            const uint16_t *xb_ = xs + iy * QY * XP + xb * 16 * QX;
             uint32_t af[MT][4];
 #pragma unroll
             for (int i = 0; i < MT; ++i) {
-                const uint16_t *p0 = ga + abase[2 * i], *p1 = ga + abase[2 * i + 1];
-                af[i][0] = __byte_perm(p0[0], p0[PX], 0x5410);
-                af[i][1] = __byte_perm(p1[0], p1[PX], 0x5410);
-                af[i][2] = __byte_perm(p0[8 * PX], p0[9 * PX], 0x5410);
-                af[i][3] = __byte_perm(p1[8 * PX], p1[9 * PX], 0x5410);
+                const uint32_t p0 = aad[2 * i] + offa, p1 = aad[2 * i + 1] + offa;
+                af[i][0] = lds_pair<0, 2 * PX>(p0);
+                af[i][1] = lds_pair<0, 2 * PX>(p1);
+                af[i][2] = lds_pair<16 * PX, 18 * PX>(p0);
+                af[i][3] = lds_pair<16 * PX, 18 * PX>(p1);
             }
             if (xb == nxb - 1) {  // a row's last block: columns past Wo are zero
 #pragma unroll
@@ -543,14 +566,24 @@ __global__ void __launch_bounds__(256) fcfs_wgrad_mma_kernel(const __grid_consta
 #pragma unroll
                     for (int r = 0; r < 4; ++r) af[i][r] &= amask[i][r];
             }
-            if (++xb == nxb) xb = 0, ++iy;
 #pragma unroll
             for (int j = 0; j < NTL; ++j) {
-                const uint16_t *q = xb_ + bbase[j];
-                const uint32_t bf[2] = {__byte_perm(q[0], q[QX], 0x5410), __byte_perm(q[8 * QX], q[9 * QX], 0x5410)};
+                const uint32_t q = bad[j] + offb;
+                const uint32_t bf[2] = {lds_pair<0, 2 * QX>(q), lds_pair<16 * QX, 18 * QX>(q)};
 #pragma unroll
                 for (int i = 0; i < MT; ++i) mma16816<T>(d[i][j], af[i], bf);
             }
+            if (++xb == nxb) {
+                xb = 0;
+                ++iy;
+                offa = 2u * (uint32_t)(iy * PY * a.Wo);
+                offb = 2u * (uint32_t)(iy * QY * XP);
+            } else {
+                offa += 32u * PX;
+                offb += 32u * QX;
+            }
+            (void)rowa;
+            (void)rowb;
         }
         // (no barrier here: the next task's barrier also orders this task's reads
         // before the copies that reuse this buffer, issued after it)
