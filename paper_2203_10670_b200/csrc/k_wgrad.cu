@@ -507,7 +507,10 @@ __global__ void __launch_bounds__(256) fcfs_wgrad_mma_kernel(const __grid_consta
             const uint16_t *xg = reinterpret_cast<const uint16_t *>(static_cast<const T *>(a.x) + bd.plane * (int64_t)a.H * a.W);
             auto pad_row = [&](int rr) {
                 uint16_t *row = xs + rr * XP + XO;
-                const uint16_t *src = xg + (int64_t)pad_src32(bd.vr0 + rr, a.H, a.pad) * a.W;
+                const int vs = pad_src32(bd.vr0 + rr, a.H, a.pad), ts = vs - bd.vr0;
+                // the source row from the tile when the band holds it (its interior has
+                // landed and only margins are being written), else from global memory
+                const uint16_t *src = (ts >= 0 && ts < XR) ? xs + ts * XP + XO : xg + (int64_t)vs * a.W;
                 for (int c = lane - a.lpad; c < a.W + a.rpad; c += 32) row[c] = src[pad_src32(c, a.W, a.pad)];
             };
             // tile rows of virtual rows [-tpad, 0) and [H, H + bpad)
