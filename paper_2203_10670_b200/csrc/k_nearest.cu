@@ -497,10 +497,11 @@ static int launch_nearest_rows(const NearestBatch &nb, cudaStream_t s) {
     }
     a.tab_bytes = (tab + 127) / 128 * 128;
     const int sms0 = nb.job[0].sm_count > 0 ? nb.job[0].sm_count : 148;
-    {   // the async row kernel (default): NB row buffers per warp, as many CTAs per SM (<= 4)
-        // as the tables and buffers allow
-        int nb_ = 2, cs = 1;  // streaming stores measured 2% faster on C2
-        if (const char *e = std::getenv("FCFS_DEBUG_NEAREST_NBUF")) nb_ = std::max(2, std::min(4, std::atoi(e)));
+    {   // the async row kernel (default): as many CTAs per SM (<= 4) as the tables and
+        // buffers allow; two row buffers per warp (three or four, with fewer CTAs per SM, measured
+        // 20.4 / 24.9 us on C2 against 19.9); streaming stores (+2%)
+        constexpr int nb_ = 2;
+        int cs = 1;
         if (const char *e = std::getenv("FCFS_DEBUG_NEAREST_CS")) cs = std::atoi(e) != 0;
         a.list_bytes = (int32_t)((2 * g0.H + 127) / 128 * 128);
         const int smem = a.tab_bytes + a.list_bytes + nb_ * kRowsAsyncWarps * a.slot_pitch + 16;
@@ -511,12 +512,8 @@ static int launch_nearest_rows(const NearestBatch &nb, cudaStream_t s) {
                                               (int64_t)sms0 * per_sm);
             if (const char *e = std::getenv("FCFS_DEBUG_NEAREST_GRID")) grid = std::max(1, std::min(grid, std::atoi(e)));
             if (grid <= 0) return 0;
-            const void *fn = nb_ == 2 ? (cs ? reinterpret_cast<const void *>(&fcfs_nearest_rows_async_kernel<T, 2, true>)
-                                            : reinterpret_cast<const void *>(&fcfs_nearest_rows_async_kernel<T, 2, false>))
-                           : nb_ == 3 ? (cs ? reinterpret_cast<const void *>(&fcfs_nearest_rows_async_kernel<T, 3, true>)
-                                            : reinterpret_cast<const void *>(&fcfs_nearest_rows_async_kernel<T, 3, false>))
-                                      : (cs ? reinterpret_cast<const void *>(&fcfs_nearest_rows_async_kernel<T, 4, true>)
-                                            : reinterpret_cast<const void *>(&fcfs_nearest_rows_async_kernel<T, 4, false>));
+            const void *fn = cs ? reinterpret_cast<const void *>(&fcfs_nearest_rows_async_kernel<T, nb_, true>)
+                                : reinterpret_cast<const void *>(&fcfs_nearest_rows_async_kernel<T, nb_, false>);
             cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 108 * 1024);
             if (e != cudaSuccess) return (int)e;
             void *args[] = {&a};
