@@ -57,6 +57,16 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f) {
     uint32_t t = __umulhi(n, f.m);
     return (t + n) >> f.s;
 }
+// the same divisor built on the device (make_fastdiv; d >= 1, numerators < 2^31)
+__device__ __forceinline__ FastDiv make_fastdiv_dev(uint32_t d) {
+    FastDiv f;
+    f.d = d;
+    uint32_t s = 0;
+    while (s < 32 && (1ull << s) < (uint64_t)d) ++s;
+    f.s = s;
+    f.m = (uint32_t)(((1ull << 32) * ((1ull << s) - (uint64_t)d)) / (uint64_t)d + 1);
+    return f;
+}
 
 // Packed fp32x2 arithmetic (sm_100a FFMA2 / FMUL2, scalar operand broadcast):
 // each lane is an independent round-to-nearest-even fp32 operation, so the

@@ -169,6 +169,14 @@ __global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_con
     __syncthreads();
     const int mx_lo = ext[0], my_lo = ext[2];
     const int NCg = ext[1] - mx_lo + 1, NRg = ext[3] - my_lo + 1;
+    // multiply-shift divisors of the flattened (plane, row, column) loops (shared:
+    // built once per CTA, read where a loop needs them)
+    __shared__ FastDiv dv_s[5];  // NCg, NRg * NCg, NH * NCg, NW, NH * NW
+    if (threadIdx.x < 5) {
+        const int d[5] = {NCg, NRg * NCg, NH * NCg, NW, NH * NW};
+        dv_s[threadIdx.x] = make_fastdiv_dev((uint32_t)max(1, d[threadIdx.x]));
+    }
+    __syncthreads();
     float *hy = hx;  // [PB][TH][NCcap]: the row pass over the window columns
     const int PB = max(1, R.PB), gstride = R.gw_cap, hstride = TH * nc_cap;
     // CTA planes: groups of PB consecutive planes, group bid / ngeom, + pstep, ...
@@ -188,7 +196,8 @@ __global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_con
             const int per = NRg * NCg, tot = nP * per;
 #pragma unroll 8
             for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-                const int pp = idx / per, rc = idx - pp * per, r = rc / NCg, c = rc - r * NCg;
+                const int pp = (int)fdiv((uint32_t)idx, dv_s[1]), rc = idx - pp * per, r = (int)fdiv((uint32_t)rc, dv_s[0]),
+                          c = rc - r * NCg;
                 gw[pp * gstride + r * nc_cap + c] =
                     DT<T>::to_f(g0[(int64_t)pp * Ho * Wo + (int64_t)(my_lo + r) * Wo + mx_lo + c]);
             }
@@ -221,7 +230,8 @@ __global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_con
         } else {
             const int per = NH * NCg;
             for (int idx = threadIdx.x; idx < nP * per; idx += blockDim.x) {
-                const int pp = idx / per, rc = idx - pp * per, rr = rc / NCg, c = rc - rr * NCg;
+                const int pp = (int)fdiv((uint32_t)idx, dv_s[2]), rc = idx - pp * per, rr = (int)fdiv((uint32_t)rc, dv_s[0]),
+                          c = rc - rr * NCg;
                 const int n = rn[rr];
                 const float *gp = gw + pp * gstride;
                 float acc = 0.0f;
@@ -236,7 +246,8 @@ __global__ void __launch_bounds__(256) fcfs_adjoint_tile_kernel(const __grid_con
         if (NW < 32) {  // narrow tile (border bands): one thread per (plane, row, column), lists from shared memory
             const int per = NH * NW;
             for (int idx = threadIdx.x; idx < nP * per; idx += blockDim.x) {
-                const int pp = idx / per, rc = idx - pp * per, rr = rc / NW, kk = rc - rr * NW;
+                const int pp = (int)fdiv((uint32_t)idx, dv_s[4]), rc = idx - pp * per, rr = (int)fdiv((uint32_t)rc, dv_s[3]),
+                          kk = rc - rr * NW;
                 const float *hr = hy + pp * hstride + rr * nc_cap - mx_lo;
                 const int n = cn[kk];
                 float acc = 0.0f;
