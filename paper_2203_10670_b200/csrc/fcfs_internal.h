@@ -290,6 +290,27 @@ struct Plane3Args {
     int32_t zbase[kZMax];
 };
 const FusedVariant *plane3_lookup(int dtype, int py, int qy, int px, int qx, int ntaps);
+
+// Height-only layers (k_vpass.cu): a thread per (plane, band of y-periods, 16-B
+// column vector), window rows in a register ring.
+struct VpassArgs {
+    const void *in;
+    void *out;
+    int64_t planes;
+    int32_t H, W, Ho, pad;
+    int32_t nvec;    // 16-B column vectors per row (W * esize / 16)
+    int32_t nper;    // y-periods per plane
+    int32_t PB;      // y-periods per band
+    int32_t nbands;  // bands per plane
+    FastDiv div_nvec, div_nbands;
+};
+struct VpassVariant {
+    const void *fn;
+    int PY, QY, TAPS;
+    const float *wtab_y;  // the compile-time phase weights, [4*j + t]
+};
+const VpassVariant *vpass_lookup(int dtype, int py, int qy, int ntaps);
+int launch_vpass(const VpassVariant *v, const VpassArgs &a, int grid, void *stream);
 int launch_plane3(const FusedVariant *v, const Plane3Args &a, int grid, int smem, void *stream);
 
 }  // namespace fcfs

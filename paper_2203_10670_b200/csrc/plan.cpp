@@ -38,6 +38,7 @@ struct fcfs_plan_s {
     const FusedVariant *fused;
     const FusedVariant *plane;  // plane-resident variant of `fused` (2D planes), or nullptr
     const FusedVariant *plane3; // slice-ring plane variant of `fused` (3D volumes with a slice factor), or nullptr
+    const VpassVariant *vpass;  // height-only variant (2D, columns 1/1), or nullptr
     int device;
     int64_t rows_ref;
     int sm_count;
@@ -168,6 +169,7 @@ struct FusedLaunch {
     FusedArgs a;
     PlaneArgs pa;  // the plane-resident kernel (select_kernel returns 4)
     Plane3Args p3; // the slice-ring plane kernel (select_kernel returns 5)
+    VpassArgs va;  // the height-only row kernel (select_kernel returns 6)
     int grid, smem;
     char desc[768];
 };
@@ -602,6 +604,49 @@ bool plan_plane3(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     return true;
 }
 
+// Height-only geometry (k_vpass.cu): whole 2D planes with 16-B aligned rows;
+// bands of y-periods sized for about four waves of threads.  False: the
+// row-pipelined kernel's identity-column variant runs.
+bool plan_vpass(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
+    const VpassVariant *v = pl->vpass;
+    if (!v || std::getenv("FCFS_NO_VPASS") || g.D != 1 || g.Do != 1) return false;
+    if (g.in_row0 != 0 || g.in_nrows != g.H || g.out_row0 != 0 || g.out_nrows != g.Ho || g.Wo != g.W) return false;
+    if (g.in_plane_stride != g.H * g.W || g.out_plane_stride != g.Ho * g.W) return false;
+    const int ESZ = esize(pl->dtype);
+    if ((g.W * ESZ) % 16 != 0 || (reinterpret_cast<uintptr_t>(g.in) & 15) || (reinterpret_cast<uintptr_t>(g.out) & 15))
+        return false;
+    if (g.H >= INT32_MAX / 64 || g.Ho >= INT32_MAX / 2 || g.W >= INT32_MAX) return false;
+    VpassArgs &a = L.va;
+    std::memset(&a, 0, sizeof(a));
+    a.in = g.in;
+    a.out = g.out;
+    a.planes = g.planes;
+    a.H = (int32_t)g.H;
+    a.W = (int32_t)g.W;
+    a.Ho = (int32_t)g.Ho;
+    a.pad = pl->pad;
+    a.nvec = (int32_t)(g.W * ESZ / 16);
+    a.nper = (int32_t)((g.Ho + v->PY - 1) / v->PY);
+    const int64_t sms = pl->sm_count > 0 ? pl->sm_count : 148;
+    const int64_t per_plane = (int64_t)a.nvec * g.planes;
+    int64_t nb = std::max<int64_t>(1, (4 * sms * 768 + per_plane - 1) / per_plane);
+    nb = std::min<int64_t>(nb, a.nper);
+    a.PB = (int32_t)((a.nper + nb - 1) / nb);
+    a.nbands = (int32_t)((a.nper + a.PB - 1) / a.PB);
+    const int64_t threads = per_plane * a.nbands;
+    if (threads >= (1LL << 31)) return false;
+    a.div_nvec = make_fastdiv((uint32_t)a.nvec);
+    a.div_nbands = make_fastdiv((uint32_t)a.nbands);
+    L.grid = (int)((threads + 255) / 256);
+    L.smem = 0;
+    std::snprintf(L.desc, sizeof(L.desc),
+                  "{\"kernel\": \"fused_vpass\", \"PY\": %d, \"QY\": %d, \"taps\": %d, \"nvec\": %d, "
+                  "\"periods\": %d, \"band_periods\": %d, \"bands\": %d, \"grid\": %d, \"block\": 256}",
+                  v->PY, v->QY, v->TAPS, a.nvec, a.nper, a.PB, a.nbands, L.grid);
+    if (std::getenv("FCFS_DEBUG_PRINT")) std::fprintf(stderr, "%s\n", L.desc);
+    return true;
+}
+
 // 1D plans: every row of every plane is an independent signal, so a whole-row
 // run is one plane of planes * H rows (long columns of rows keep the kernels'
 // row bands full however small H is).
@@ -644,6 +689,7 @@ int select_kernel(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
             g2.in_plane_stride = g.in_nrows * pl->W;
             g2.out_plane_stride = g.out_nrows * pl->Wo;
         }
+        if (pl->fused->TZ == 1 && plan_vpass(pl, g, L)) return 6;
         if (pl->fused->TZ == 1 && plan_plane(pl, g2, L)) return 4;
         if (pl->fused->TZ > 1 && plan_plane3(pl, g, L)) return 5;
         if ((reinterpret_cast<uintptr_t>(g.in) % esize(pl->dtype)) ||
@@ -878,6 +924,7 @@ fcfs_status launch(const Prepared &pr, void *stream) {
     else if (pr.kernel == 2) rc = launch_fused(pr.pl->fused, pr.L.a, pr.L.grid, kFusedThreads, pr.L.smem, stream);
     else if (pr.kernel == 4) rc = launch_plane(pr.pl->plane, pr.L.pa, pr.L.grid, pr.L.smem, stream);
     else if (pr.kernel == 5) rc = launch_plane3(pr.pl->plane3, pr.L.p3, pr.L.grid, pr.L.smem, stream);
+    else if (pr.kernel == 6) rc = launch_vpass(pr.pl->vpass, pr.L.va, pr.L.grid, stream);
     else if (pr.kernel == 3) rc = launch_tile(pr.pl->dtype, pr.ta, pr.tgrid, pr.tsmem, stream);
     else if (pr.kernel == 0) rc = launch_reference(pr.pl->dtype, pr.ra, stream);
     return rc == 0 ? FCFS_OK : FCFS_E_CUDA;
@@ -969,6 +1016,7 @@ fcfs_status make_plan(int rank, const int *pd, const int *qd, int mode, int pad,
     pl->fused = nullptr;
     pl->plane = nullptr;
     pl->plane3 = nullptr;
+    pl->vpass = nullptr;
     if (!(flags & FCFS_FLAG_FORCE_REFERENCE)) {
         if (mode == FCFS_NEAREST) {
             pl->kernel = 1;
@@ -989,6 +1037,15 @@ fcfs_status make_plan(int rank, const int *pd, const int *qd, int mode, int pad,
                         pl->fused = nullptr;
             if (pl->fused) pl->kernel = 2;
             // batches of small planes: the plane-resident form of the same layer
+            // height-only 2D layers (columns 1/1): the column-vector row kernel
+            if (pl->fused && !slices && !pl->is1d && pl->D == 1 && pl->p == 1 && pl->q == 1 &&
+                !(pl->py == 1 && pl->qy == 1)) {
+                pl->vpass = vpass_lookup(dtype, pl->py, pl->qy, pl->taby.ntaps);
+                for (int j = 0; pl->vpass && j < pl->py; ++j)
+                    for (int t = 0; t < pl->taby.ntaps; ++t)
+                        if (std::memcmp(&pl->vpass->wtab_y[4 * j + t], &pl->taby.w[j][t], sizeof(float)) != 0)
+                            pl->vpass = nullptr;
+            }
             // volumes of small slices: the slice-ring form
             if (pl->fused && slices && !pl->is1d) {
                 pl->plane3 = plane3_lookup(dtype, pl->py, pl->qy, pl->p, pl->q, pl->tab.ntaps);
