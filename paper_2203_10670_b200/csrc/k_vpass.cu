@@ -36,15 +36,14 @@ __global__ void __launch_bounds__(256) fcfs_vpass_kernel(const __grid_constant__
     const T *in_p = static_cast<const T *>(a.in) + (int64_t)plane * a.H * a.W + (int64_t)cv * V;
     T *out_p = static_cast<T *>(a.out) + (int64_t)plane * a.Ho * a.W + (int64_t)cv * V;
     float hr[R][V];
-    // window row r of period iy into a ring slot (virtual row iy QY + LO + r, padded)
-    auto load = [&](float(&h)[V], int iy, int r) {
+    // raw 16-B vector of window row r of period iy (virtual row iy QY + LO + r, padded;
+    // a zero-padding row reads nothing)
+    auto fetch = [&](int iy, int r) {
         const int src = pad_src32(iy * QY + GY::LO + r, a.H, a.pad);
-        if (src < 0) {
-#pragma unroll
-            for (int v = 0; v < V; ++v) h[v] = 0.0f;
-            return;
-        }
-        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(in_p + (int64_t)src * a.W));
+        if (src < 0) return make_uint4(0u, 0u, 0u, 0u);
+        return __ldg(reinterpret_cast<const uint4 *>(in_p + (int64_t)src * a.W));
+    };
+    auto unpack = [&](float(&h)[V], const uint4 q) {
         const uint32_t w[4] = {q.x, q.y, q.z, q.w};
         if constexpr (ESZ == 4) {
 #pragma unroll
@@ -54,8 +53,18 @@ __global__ void __launch_bounds__(256) fcfs_vpass_kernel(const __grid_constant__
             for (int v = 0; v < V; ++v) h[v] = HalfBits<T>::f((v & 1) ? (w[v >> 1] >> 16) : (w[v >> 1] & 0xffffu));
         }
     };
+    constexpr int F = L - C;  // fresh window rows per period
+    uint4 nxt[F];             // the next period's fresh rows, in flight while this period is emitted
     auto period = [&](auto m_c, const int iy) {
         constexpr int M = decltype(m_c)::value;
+        // this period's fresh rows (fetched one period ahead) into their ring slots,
+        // then the next period's fetches
+#pragma unroll
+        for (int r = C; r < L; ++r) unpack(hr[(M * QY + r) % R], nxt[r - C]);
+        if (iy + 1 < iy1) {
+#pragma unroll
+            for (int r = C; r < L; ++r) nxt[r - C] = fetch(iy + 1, r);
+        }
         auto emit = [&](const int jy) {
             const int m = iy * PY + jy;
             if (m >= a.Ho) return;
@@ -91,7 +100,6 @@ __global__ void __launch_bounds__(256) fcfs_vpass_kernel(const __grid_constant__
             if (GY::last_row(jy) < C) emit(jy);
 #pragma unroll
         for (int r = C; r < L; ++r) {
-            load(hr[(M * QY + r) % R], iy, r);
 #pragma unroll
             for (int jy = 0; jy < PY; ++jy)
                 if (GY::last_row(jy) == r) emit(jy);
@@ -100,9 +108,11 @@ __global__ void __launch_bounds__(256) fcfs_vpass_kernel(const __grid_constant__
     auto warm = [&](auto m_c) {
         constexpr int M = decltype(m_c)::value;
 #pragma unroll
-        for (int r = 0; r < C; ++r) load(hr[(M * QY + r) % R], iy0, r);
+        for (int r = 0; r < C; ++r) unpack(hr[(M * QY + r) % R], fetch(iy0, r));
     };
     if (iy0 >= iy1) return;
+#pragma unroll
+    for (int r = C; r < L; ++r) nxt[r - C] = fetch(iy0, r);
     const int m0 = iy0 % U;
     if (m0 == 0) warm(std::integral_constant<int, 0>{});
     if constexpr (U > 1) if (m0 == 1) warm(std::integral_constant<int, (U > 1 ? 1 : 0)>{});
