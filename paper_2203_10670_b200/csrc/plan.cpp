@@ -629,7 +629,9 @@ bool plan_vpass(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     a.nper = (int32_t)((g.Ho + v->PY - 1) / v->PY);
     const int64_t sms = pl->sm_count > 0 ? pl->sm_count : 148;
     const int64_t per_plane = (int64_t)a.nvec * g.planes;
-    int64_t nb = std::max<int64_t>(1, (4 * sms * 768 + per_plane - 1) / per_plane);
+    int64_t waves = 8;  // measured on A2: 2 / 4 / 8 / 16 waves 217.6 / 207.6 / 198.6 / 202.7 us
+    if (const char *e = std::getenv("FCFS_DEBUG_VPASS_WAVES")) waves = std::max(1, std::atoi(e));
+    int64_t nb = std::max<int64_t>(1, (waves * sms * 768 + per_plane - 1) / per_plane);
     nb = std::min<int64_t>(nb, a.nper);
     a.PB = (int32_t)((a.nper + nb - 1) / nb);
     a.nbands = (int32_t)((a.nper + a.PB - 1) / a.PB);
