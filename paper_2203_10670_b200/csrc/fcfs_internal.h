@@ -310,24 +310,6 @@ struct VpassVariant {
     const float *wtab_y;  // the compile-time phase weights, [4*j + t]
 };
 const VpassVariant *vpass_lookup(int dtype, int py, int qy, int ntaps);
-
-// Width-only layers and rank-1 plans (k_hpass.cu): a thread per (row, chunk of K
-// x-periods whose input and output columns are whole 16-B vectors).
-struct HpassArgs {
-    const void *in;
-    void *out;
-    int64_t rows;   // planes x H (every row independent)
-    int32_t W, Wo, pad;
-    int32_t nch;    // chunks per output row
-    FastDiv div_nch;
-};
-struct HpassVariant {
-    const void *fn;
-    int PX, QX, TAPS, K;
-    const float *wtab_x;  // the compile-time phase weights, [4*j + t]
-};
-const HpassVariant *hpass_lookup(int dtype, int px, int qx, int ntaps);
-int launch_hpass(const HpassVariant *v, const HpassArgs &a, int grid, void *stream);
 int launch_vpass(const VpassVariant *v, const VpassArgs &a, int grid, void *stream);
 int launch_plane3(const FusedVariant *v, const Plane3Args &a, int grid, int smem, void *stream);
 

@@ -30,8 +30,3 @@
 // pairs of 3D volumes with small slices (any slice factor, run-time slice weights)
 #define FCFS_PLANE3_PAIRS(Y) \
     Y(2, 1) Y(3, 2) Y(4, 3) Y(5, 3) Y(5, 4) Y(1, 2) Y(2, 3) Y(3, 4) Y(3, 5) Y(4, 5)
-// width-only row kernel (k_hpass.cu): column pairs whose 16-B-vector chunk keeps
-// the window in registers (the strong down-scales 1/4 and 2/11 stay on the fused kernel)
-#define FCFS_HPASS_PAIRS(Y) \
-    Y(2, 1) Y(3, 1) Y(4, 1) Y(1, 2) Y(1, 3) Y(3, 2) Y(2, 3) Y(4, 3) Y(3, 4) Y(5, 3) Y(3, 5) Y(5, 4) Y(4, 5) \
-    Y(7, 5) Y(5, 7) Y(4, 7) Y(7, 4) Y(5, 2) Y(2, 5)

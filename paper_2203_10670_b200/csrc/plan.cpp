@@ -39,7 +39,6 @@ struct fcfs_plan_s {
     const FusedVariant *plane;  // plane-resident variant of `fused` (2D planes), or nullptr
     const FusedVariant *plane3; // slice-ring plane variant of `fused` (3D volumes with a slice factor), or nullptr
     const VpassVariant *vpass;  // height-only variant (2D, columns 1/1), or nullptr
-    const HpassVariant *hpass;  // width-only variant (2D rows 1/1, or rank-1 plans), or nullptr
     int device;
     int64_t rows_ref;
     int sm_count;
@@ -171,7 +170,6 @@ struct FusedLaunch {
     PlaneArgs pa;  // the plane-resident kernel (select_kernel returns 4)
     Plane3Args p3; // the slice-ring plane kernel (select_kernel returns 5)
     VpassArgs va;  // the height-only row kernel (select_kernel returns 6)
-    HpassArgs ha;  // the width-only row kernel (select_kernel returns 7)
     int grid, smem;
     char desc[768];
 };
@@ -651,42 +649,6 @@ bool plan_vpass(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
     return true;
 }
 
-// Width-only geometry (k_hpass.cu): every row of every plane independent (2D rows
-// 1/1, or rank-1 plans), 16-B aligned input and output rows.  False: the
-// row-pipelined kernel's identity-row variant runs.
-bool plan_hpass(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
-    const HpassVariant *v = pl->hpass;
-    if (!v || std::getenv("FCFS_NO_HPASS") || g.D != 1 || g.Do != 1) return false;
-    if (g.in_row0 != 0 || g.in_nrows != g.H || g.out_row0 != 0 || g.out_nrows != g.Ho || g.Ho != g.H) return false;
-    if (g.in_plane_stride != g.H * g.W || g.out_plane_stride != g.Ho * g.Wo) return false;
-    const int ESZ = esize(pl->dtype);
-    if ((g.W * ESZ) % 16 != 0 || (g.Wo * ESZ) % 16 != 0 || (reinterpret_cast<uintptr_t>(g.in) & 15) ||
-        (reinterpret_cast<uintptr_t>(g.out) & 15))
-        return false;
-    if (g.W >= INT32_MAX / 2 || g.Wo >= INT32_MAX / 2) return false;
-    HpassArgs &a = L.ha;
-    std::memset(&a, 0, sizeof(a));
-    a.in = g.in;
-    a.out = g.out;
-    a.rows = g.planes * g.H;
-    a.W = (int32_t)g.W;
-    a.Wo = (int32_t)g.Wo;
-    a.pad = pl->pad;
-    const int KO = v->K * v->PX;
-    a.nch = (int32_t)((g.Wo + KO - 1) / KO);
-    const int64_t threads = a.rows * a.nch;
-    if (threads >= (1LL << 31)) return false;
-    a.div_nch = make_fastdiv((uint32_t)a.nch);
-    L.grid = (int)((threads + 255) / 256);
-    L.smem = 0;
-    std::snprintf(L.desc, sizeof(L.desc),
-                  "{\"kernel\": \"fused_hpass\", \"PX\": %d, \"QX\": %d, \"taps\": %d, \"K\": %d, "
-                  "\"chunks\": %d, \"rows\": %lld, \"grid\": %d, \"block\": 256}",
-                  v->PX, v->QX, v->TAPS, v->K, a.nch, (long long)a.rows, L.grid);
-    if (std::getenv("FCFS_DEBUG_PRINT")) std::fprintf(stderr, "%s\n", L.desc);
-    return true;
-}
-
 // 1D plans: every row of every plane is an independent signal, so a whole-row
 // run is one plane of planes * H rows (long columns of rows keep the kernels'
 // row bands full however small H is).
@@ -730,7 +692,6 @@ int select_kernel(const fcfs_plan_s *pl, const RunGeom &g, FusedLaunch &L) {
             g2.out_plane_stride = g.out_nrows * pl->Wo;
         }
         if (pl->fused->TZ == 1 && plan_vpass(pl, g, L)) return 6;
-        if (pl->fused->TZ == 1 && plan_hpass(pl, g, L)) return 7;
         if (pl->fused->TZ == 1 && plan_plane(pl, g2, L)) return 4;
         if (pl->fused->TZ > 1 && plan_plane3(pl, g, L)) return 5;
         if ((reinterpret_cast<uintptr_t>(g.in) % esize(pl->dtype)) ||
@@ -966,7 +927,6 @@ fcfs_status launch(const Prepared &pr, void *stream) {
     else if (pr.kernel == 4) rc = launch_plane(pr.pl->plane, pr.L.pa, pr.L.grid, pr.L.smem, stream);
     else if (pr.kernel == 5) rc = launch_plane3(pr.pl->plane3, pr.L.p3, pr.L.grid, pr.L.smem, stream);
     else if (pr.kernel == 6) rc = launch_vpass(pr.pl->vpass, pr.L.va, pr.L.grid, stream);
-    else if (pr.kernel == 7) rc = launch_hpass(pr.pl->hpass, pr.L.ha, pr.L.grid, stream);
     else if (pr.kernel == 3) rc = launch_tile(pr.pl->dtype, pr.ta, pr.tgrid, pr.tsmem, stream);
     else if (pr.kernel == 0) rc = launch_reference(pr.pl->dtype, pr.ra, stream);
     return rc == 0 ? FCFS_OK : FCFS_E_CUDA;
@@ -1059,7 +1019,6 @@ fcfs_status make_plan(int rank, const int *pd, const int *qd, int mode, int pad,
     pl->plane = nullptr;
     pl->plane3 = nullptr;
     pl->vpass = nullptr;
-    pl->hpass = nullptr;
     if (!(flags & FCFS_FLAG_FORCE_REFERENCE)) {
         if (mode == FCFS_NEAREST) {
             pl->kernel = 1;
@@ -1088,15 +1047,6 @@ fcfs_status make_plan(int rank, const int *pd, const int *qd, int mode, int pad,
                     for (int t = 0; t < pl->taby.ntaps; ++t)
                         if (std::memcmp(&pl->vpass->wtab_y[4 * j + t], &pl->taby.w[j][t], sizeof(float)) != 0)
                             pl->vpass = nullptr;
-            }
-            // width-only 2D layers (rows 1/1) and rank-1 plans: the row-chunk kernel
-            if (pl->fused && !slices && pl->D == 1 && (pl->is1d || (pl->py == 1 && pl->qy == 1)) &&
-                !(pl->p == 1 && pl->q == 1)) {
-                pl->hpass = hpass_lookup(dtype, pl->p, pl->q, pl->tab.ntaps);
-                for (int j = 0; pl->hpass && j < pl->p; ++j)
-                    for (int t = 0; t < pl->tab.ntaps; ++t)
-                        if (std::memcmp(&pl->hpass->wtab_x[4 * j + t], &pl->tab.w[j][t], sizeof(float)) != 0)
-                            pl->hpass = nullptr;
             }
             // volumes of small slices: the slice-ring form
             if (pl->fused && slices && !pl->is1d) {

@@ -97,10 +97,7 @@ def test_isotropic_variants(pad):
 
 
 @pytest.mark.parametrize("pad", PADS)
-def test_width_only_variants(pad, monkeypatch):
-    # the row-pipelined kernel's identity-row variants (the width-only row kernel,
-    # which takes aligned shapes by default, has its own table test: test_gpu_hpass.py)
-    monkeypatch.setenv("FCFS_NO_HPASS", "1")
+def test_width_only_variants(pad):
     for i, P, Q, mode, dtype in _cases(NONUNIT):
         H, W = SHAPES[(i + 1) % len(SHAPES)]
         ext = ["paper", "floor"][i % 2]
