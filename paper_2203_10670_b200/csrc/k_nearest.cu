@@ -505,7 +505,9 @@ static int launch_nearest_rows(const NearestBatch &nb, cudaStream_t s) {
         if (const char *e = std::getenv("FCFS_DEBUG_NEAREST_CS")) cs = std::atoi(e) != 0;
         a.list_bytes = (int32_t)((2 * g0.H + 127) / 128 * 128);
         const int smem = a.tab_bytes + a.list_bytes + nb_ * kRowsAsyncWarps * a.slot_pitch + 16;
-        if (!std::getenv("FCFS_NEAREST_STAGED") && g0.H <= 8192 && smem <= 108 * 1024) {
+        // (item indices stay below 2^31 with a grid's stride added)
+        if (!std::getenv("FCFS_NEAREST_STAGED") && g0.H <= 8192 && smem <= 108 * 1024 &&
+            a.nitems < INT32_MAX - (1 << 22)) {
             int per_sm = std::min(4, 216 * 1024 / smem);
             if (const char *e = std::getenv("FCFS_DEBUG_NEAREST_CTAS")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
             int grid = (int)std::min<int64_t>(((int64_t)a.nitems + kRowsAsyncWarps - 1) / kRowsAsyncWarps,
