@@ -278,8 +278,10 @@ fcfs_status fcfs_plan_info(fcfs_plan_t plan, fcfs_plan_info_t *info);
 /* fcfs_launch_info -- host-only description (a JSON object written to buf,
  * NUL-terminated, truncated to buflen) of the kernel and launch geometry a run
  * of N images over output rows [out_row0, out_row0 + out_nrows) would use,
- * assuming 16-B-aligned buffers: kernel name, grid, block, dynamic shared
- * memory and, for the fused kernel, the task decomposition.  Errors:
+ * assuming 16-B-aligned buffers: kernel name ("fused_separable" -- the
+ * row-pipelined kernel --, "fused_plane", "fused_plane3", "fused_vpass",
+ * "tiled", "nearest_gather" with its "variant", "reference"), grid, block,
+ * dynamic shared memory and the kernel's task decomposition.  Errors:
  * FCFS_E_ARG. */
 fcfs_status fcfs_launch_info(fcfs_plan_t plan, int64_t N, int64_t out_row0, int64_t out_nrows, char *buf,
                              int64_t buflen);
