@@ -265,3 +265,34 @@ def test_compulsory_bytes(fc):
     assert pl.compulsory_bytes(8) == 1178468352
     pl = fc.Plan(4, 7, "bilinear", "replicate", 3, 2160, 3840, "float16", "floor")
     assert pl.compulsory_bytes(8) == 527901888
+
+
+def test_round2_kernel_geometry(fc):
+    """Host logic of the round-2 kernels (no GPU): which kernel a run takes and
+    the geometry invariants each relies on."""
+    # nearest C2: the async row kernel, four CTAs per SM at most, 8 warps each
+    pl = fc.Plan(2, 3, "nearest", "zero", 3, 512, 512, "float32", "floor")
+    info = pl.launch_info(16)
+    assert info["kernel"] == "nearest_gather" and info["variant"] == "rows_async", info
+    assert info["block"] == 256 and info["grid"] <= 4 * 148
+    # V2: the slice-ring plane kernel; taps + 1 slice buffers; runs of output slices
+    # per volume sized for one wave; the ring and staging fit one SM
+    pl = fc.Plan.nd((5, 5, 5), (3, 3, 3), "bicubic", "reflect", 8, (64, 128, 128), "bfloat16", "floor")
+    info = pl.launch_info(2)
+    assert info["kernel"] == "fused_plane3", info
+    assert info["S"] >= info["taps"] + 1 and info["smem"] <= 227 * 1024
+    assert info["ntasks"] == 2 * 8 * info["chunks"] and info["grid"] == min(info["ntasks"], 148)
+    assert info["BH"] >= (info["periods"] - 1) * info["QY"] + 1 and info["BW"] <= 256
+    # f32 bicubic 128^2 slices: taps + 1 buffers do not fit -> the row-pipelined 3D kernel
+    pl = fc.Plan.nd((5, 5, 5), (3, 3, 3), "bicubic", "reflect", 2, (16, 128, 128), "float32", "floor")
+    assert pl.launch_info(1)["kernel"] == "fused_separable"
+    # A2: height-only rows -> the column-vector kernel; every (plane, band, vector) a thread
+    pl = fc.Plan.nd((5, 1), (3, 1), "bicubic", "reflect", 3, (2160, 3840), "float16", "floor")
+    info = pl.launch_info(8)
+    assert info["kernel"] == "fused_vpass", info
+    assert info["nvec"] == 3840 * 2 // 16 and info["periods"] == -(-pl.odims[0] // 5)
+    assert info["band_periods"] * info["bands"] >= info["periods"]
+    assert info["grid"] * 256 >= 8 * 3 * info["nvec"] * info["bands"]
+    # unaligned rows (W * esize not a 16-B multiple) keep the fused kernel
+    pl = fc.Plan.nd((5, 1), (3, 1), "bicubic", "reflect", 3, (64, 101), "float32", "floor")
+    assert pl.launch_info(2)["kernel"] == "fused_separable"
