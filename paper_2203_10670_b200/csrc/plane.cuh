@@ -312,11 +312,13 @@ __global__ void __launch_bounds__(kPlaneThreads, kPlaneCtasPerSm) fcfs_plane_ker
 // kernel, so all three agree bit for bit.  The CTA's slices form one sequence
 // (task by task, each task's slices z0(mz0) .. z0(mz1 - 1) + TZ - 1 in order);
 // sequence element s lands in buffer s mod S (one 3D box per slice), and the
-// last of the 8 warps to finish with element s loads element s + S into it.
-// Warp w keeps band w of every output slice (a fixed band: it writes the
-// replicate / reflect margins of its band's rows once per slice, after the
-// slice lands, and no other warp reads them first).  One CTA per SM (S = 5
-// whole padded slices of 128^2 bf16 fill the shared memory).
+// last of the 16 warps to finish with element s loads element s + S into it.
+// Warp w takes band (w + mz) mod 16 of the y-periods of output slice mz
+// (uneven bands rotate); a slice's replicate / reflect margins are written by
+// the warps for their bands' rows when the slice first enters their window,
+// and a second mbarrier per buffer (every warp arrives) orders those writes
+// before any read.  One CTA per SM (S = 5 whole padded slices of 128^2 bf16
+// fill the shared memory).
 // ---------------------------------------------------------------------------
 
 template <typename T, int PY0, int QY0, int PX0, int QX0, int T0, int LO0, int K>
@@ -339,6 +341,7 @@ __global__ void __launch_bounds__(32 * kPlane3Warps, 1) fcfs_plane3_kernel(const
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);  // [kPlane3MaxS] slice landed
     int *done = reinterpret_cast<int *>(smem + 8 * kPlane3MaxS);  // [kPlane3MaxS] warps done with the element
+    uint64_t *ready = reinterpret_cast<uint64_t *>(smem + 128);       // [kPlane3MaxS] every warp's margins written
     unsigned char *pbuf = smem + 256;
     unsigned char *obuf = pbuf + a.S * a.plane_bytes;
 
@@ -383,6 +386,7 @@ __global__ void __launch_bounds__(32 * kPlane3Warps, 1) fcfs_plane3_kernel(const
     if (threadIdx.x == 0) {
         for (int b = 0; b < S; ++b) {
             mbar_init(&full[b], 1);
+            mbar_init(&ready[b], kPlane3Warps);
             done[b] = 0;
         }
         mbar_fence_init();
@@ -401,8 +405,16 @@ __global__ void __launch_bounds__(32 * kPlane3Warps, 1) fcfs_plane3_kernel(const
     float hr[R][KP];
     uint32_t fk = 0;
     // this warp's fixed band of y-periods and the buffer rows it reads
-    const int iy0 = warp * a.nper / kPlane3Warps, iy1 = (warp + 1) * a.nper / kPlane3Warps;
-    const int br0 = iy0 * QY, br1 = min(a.BH, (iy1 - 1) * QY + L);
+    // this warp's band of y-periods (and the buffer rows it reads) for the current
+    // output slice: band (warp + mz) mod warps, so that uneven bands rotate
+    int iy0 = 0, iy1 = 0, br0 = 0, br1 = 0;
+    auto set_band = [&](int mz) {
+        const int band = (warp + mz) % kPlane3Warps;
+        iy0 = band * a.nper / kPlane3Warps;
+        iy1 = (band + 1) * a.nper / kPlane3Warps;
+        br0 = iy0 * QY;
+        br1 = min(a.BH, (iy1 - 1) * QY + L);
+    };
 
     // horizontal taps of one window row combined over the TZ slices of sl[]
     auto row_h = [&](float(&h)[KP], const T *const (&sl)[TZ], int br, const float (&wz)[TZ], bool zcopy) {
@@ -498,11 +510,22 @@ __global__ void __launch_bounds__(32 * kPlane3Warps, 1) fcfs_plane3_kernel(const
         task_span(t, vol, m0, m1, zf, ns);
         for (int mz = m0; mz < m1; ++mz) {
             const uint32_t s0 = seq0 + (uint32_t)(zfirst(mz) - zf);
-            // the slices of this output slice: landed (and, first time, this band padded)
+            set_band(mz);
+            // the slices of this output slice: landed; a slice new to this warp gets the
+            // margins of this warp's band rows (the bands of one output slice cover every
+            // row), and then every warp's margins are awaited (ready: all warps arrived)
             for (; acq < s0 + TZ; ++acq) {
                 const int b = (int)(acq % (uint32_t)S);
                 mbar_wait(&full[b], (acq / (uint32_t)S) & 1u);
-                if (a.pad != FCFS_PAD_ZERO && iy0 < iy1) pad_band(reinterpret_cast<T *>(pbuf + b * a.plane_bytes));
+                if (a.pad != FCFS_PAD_ZERO) {
+                    if (iy0 < iy1) pad_band(reinterpret_cast<T *>(pbuf + b * a.plane_bytes));
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&ready[b]);
+                }
+            }
+            if (a.pad != FCFS_PAD_ZERO) {
+#pragma unroll
+                for (int i = 0; i < TZ; ++i) mbar_wait(&ready[(s0 + i) % (uint32_t)S], ((s0 + i) / (uint32_t)S) & 1u);
             }
             const T *sl[TZ];
 #pragma unroll
